@@ -1,0 +1,329 @@
+#!/usr/bin/env python
+"""Benchmark: simulated lane-cycles/s of the B200 RTeAAL Sim hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+
+One step = one rs_step_cycles launch over the config's full cycle count for
+this rank's lanes (inject -> every level's gather/op/write -> hash -> commit,
+all cycles), hashes on.  N > 1 runs under torchrun, one process per GPU;
+each rank simulates its own `lanes` global lanes (weak scaling: lanes are
+independent units, no data-path collective).  Timing: CUDA events on the
+launching stream around each step, barrier + synchronize on both sides of
+the timed region, max over ranks; L2 flushed (256 MB write) before every
+timed step.  `--impl reference` times the CPU oracle (test infrastructure,
+oracle/) on the host cores over a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "simulated lane-cycles/s and op-evals/s at 1/2/4/8 B200; % of BW roofline"
+UNIT = "lane-cycles/s"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def workload(cfg_name, lanes, cycles, n_ops, n_levels, n_gpus):
+    return (f"{cfg_name}: {n_ops} ops / {n_levels} levels, {lanes} lanes per GPU x {cycles} cycles "
+            f"per step, {n_gpus} GPU(s), synthetic seeded circuit + stimulus")
+
+
+def oracle_rate(circ, seed, n_lanes, n_cycles, lane0=0, threads=1):
+    import oracle
+    t = time.perf_counter()
+    oracle.simulate(circ, n_cycles, seed=seed, lane0=lane0, n_lanes=n_lanes, threads=threads)
+    dt = time.perf_counter() - t
+    return n_lanes * n_cycles / dt, dt
+
+
+def cpu_sample_plan(circ, target_s, cores):
+    """Lanes x cycles of oracle work taking about target_s on `cores` threads
+    (calibrated with a short run)."""
+    import oracle
+    lanes = max(1, cores)
+    t = time.perf_counter()
+    oracle.simulate(circ, 2, seed=1, n_lanes=lanes, threads=cores)
+    per_cycle = max((time.perf_counter() - t) / 2, 1e-6)
+    cycles = int(max(2, min(100000, target_s / per_cycle)))
+    return lanes, cycles
+
+
+def run_reference(args, cfg, circ):
+    """--impl reference: the oracle (as it stands) on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    lanes, cycles = cpu_sample_plan(circ, args.ref_step_s, cores)
+    for w in range(args.warmup):
+        oracle_rate(circ, cfg.stim_seed, lanes, max(2, cycles // 10), threads=cores)
+    tot = 0.0
+    for k in range(args.steps):
+        _, dt = oracle_rate(circ, cfg.stim_seed, lanes, cycles, lane0=k * lanes, threads=cores)
+        tot += dt
+    value = lanes * cycles * args.steps / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic",
+        "config": {"workload": workload(cfg.name, cfg.lanes, cfg.cycles, circ.n_ops, cfg.n_levels, args.gpus)},
+        "op_evals_per_s": value * circ.n_ops,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"{lanes} lanes x {cycles} cycles per step (one lane per thread)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--cycles", type=int, default=0, help="cycles per step (default: the config's)")
+    ap.add_argument("--lanes", type=int, default=0, help="lanes per GPU (default: the config's)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-hash", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--lane-tile", type=int, default=0)
+    ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--ref-step-s", type=float, default=4.0)
+    args = ap.parse_args()
+
+    from synth import CONFIGS, config_circuit
+    cfg = CONFIGS[args.config]
+    circ = config_circuit(args.config)
+    if args.impl == "reference":
+        return run_reference(args, cfg, circ)
+
+    import torch
+    from paper_2601_18140_b200 import rtlsim as rs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"warning: WORLD_SIZE={world} but --gpus={args.gpus}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    single = args.config in ("C1", "C5")
+    lanes = args.lanes or cfg.lanes
+    if single:
+        lanes = 1
+    cycles = args.cycles or cfg.cycles
+    stream = torch.cuda.Stream()
+    g = rs.Graph(circ, device=local, mode="single" if single else "lanes")
+    info = g.info()
+    L = rs.Lanes(g, lanes, lane0=rank * lanes, lane_tile=args.lane_tile, threads=args.threads, stream=stream)
+    L.set_seed(cfg.stim_seed)
+    hashes = None if args.no_hash else torch.empty(cycles * lanes, dtype=torch.int64, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            L.step(cycles, hashes=hashes)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        launches0 = L.launches
+        evs = []
+        with ClockSampler(local) as clk:
+            for _ in range(args.steps):
+                flush.fill_(1)                          # L2 flush between timed steps
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                L.step(cycles, hashes=hashes)
+                e1.record(stream)
+                evs.append((e0, e1))
+            torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        launches = L.launches - launches0
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = float(sum(step_ms))
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    lane_cycles = lanes * world * cycles * args.steps
+    value = lane_cycles / (total_ms / 1e3)
+
+    # roofline of the dominant (only) kernel: algorithmic bytes per launch / launch duration
+    bytes_per_cycle = lanes * info["alg_bytes_per_lane_cycle"] + info["graph_alg_bytes"]
+    alg_bytes = bytes_per_cycle * cycles
+    kern_s = (total_ms / args.steps) / 1e3
+    peak, peak_src = load_peaks()
+    achieved = alg_bytes / kern_s / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tp):
+        tj = json.load(open(tp))
+        traffic = tj.get("dram_bytes_per_lane_cycle", 0) * lanes * cycles or None
+
+    # end to end through the public API with host buffers: staged inputs H2D
+    # from pinned memory, hashes D2H, every chunk.
+    e2e = None
+    if not args.no_e2e and rank == 0 or (not args.no_e2e and world > 1):
+        chunk = min(cycles, max(1, (256 << 20) // max(1, 8 * circ.n_inputs * lanes)))
+        Ls = rs.Lanes(g, lanes, lane0=rank * lanes, lane_tile=args.lane_tile, threads=args.threads,
+                      stage_cycles=chunk, stream=stream)
+        rng = np.random.default_rng(rank)
+        host_in = torch.from_numpy(rng.integers(0, 2**63, size=(chunk, circ.n_inputs, lanes),
+                                                dtype=np.int64)).pin_memory()
+        host_h = torch.empty((chunk, lanes), dtype=torch.int64).pin_memory()
+        in_np = host_in.numpy().view(np.uint64)
+        h_np = host_h.numpy().view(np.uint64)
+
+        def e2e_step():
+            done = 0
+            while done < cycles:
+                n = min(chunk, cycles - done)
+                Ls.set_inputs(Ls.cycle, in_np[:n])
+                Ls.step(n, hashes=h_np[:n] if n == chunk else np.ascontiguousarray(h_np[:n]))
+                done += n
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        e2e_steps = max(1, min(args.steps, 2))
+        for _ in range(e2e_steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        te = torch.tensor([el], dtype=torch.float64, device="cuda")
+        if dist is not None:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        el = float(te.item())
+        e2e = {"value": lanes * world * cycles * e2e_steps / el, "unit": UNIT,
+               "h2d_bytes_per_step": int(cycles * circ.n_inputs * lanes * 8),
+               "d2h_bytes_per_step": int(cycles * lanes * 8), "steps": e2e_steps,
+               "path": "rs_set_inputs(host pinned) + rs_step_cycles(hashes=HOST) per chunk of "
+                       f"{chunk} cycles"}
+        Ls.close()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores = os.cpu_count() or 1
+        nl, nc = cpu_sample_plan(circ, 10.0, cores)
+        rate, dt = oracle_rate(circ, cfg.stim_seed, nl, nc, threads=cores)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{nl} lanes x {nc} cycles of {args.config} ({dt:.1f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": workload(args.config, lanes, cycles, circ.n_ops, info["n_levels"], world),
+                       "lanes_per_gpu": lanes, "cycles_per_step": cycles, "hash": not args.no_hash,
+                       "l2": "flushed (256 MB write) before every timed step",
+                       "mode": "single" if single else "lanes", "launch": L.shape(),
+                       "state_bytes_per_gpu": info["state_bytes_per_lane"] * lanes},
+            "op_evals_per_s": value * circ.n_ops,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "alg_bytes_per_launch": alg_bytes,
+                         "alg_bytes_per_lane_cycle": info["alg_bytes_per_lane_cycle"],
+                         "kernel": "k_lanes" if not single else "k_single"},
+            "clocks": clk.summary(),
+            "gpu_launches": launches,
+            "step_ms": step_ms,
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,206 @@
+/*
+ * rtlsim.h -- C ABI of the B200-native RTeAAL Sim hot path.
+ *
+ * The library evaluates a synchronous circuit cycle by cycle, batched over
+ * many independent stimulus lanes, as the cascade of extended Einsums of
+ * PAPER.md Cascade 1 (box:einsum):
+ *
+ *   per cycle c:
+ *     1. input injection   LI[in_k]  = stimulus & M(w)      (§2.1; §6.2)
+ *     2. for each level i (iterative rank I, stop condition "i == I"):
+ *          a. gather  OI_{i,n,o,r,s} = LI_{i,r} . OIM_{i,n,o,r,s}  :: AND <-(->)   (eq:split_einsum1 P:809-812)
+ *          b. op      LO = OI :: AND op_u[n](<-) OR op_r[n](->),   LO_sel :: populate op_s[n]
+ *                     (eq:step4c P:826-830, eq:step5b P:839-843, alg:opn P:753-775, App. A)
+ *          c. write   LI_{i+1,s} = LO | LO_sel  :: OR ANY(->)    (Cascade 1 P:956-966; alg:RU P:1012)
+ *          d. level barrier
+ *     3. per-cycle signal hash (reading R12), fused
+ *     4. register commit (Fig. 1 caption P:187), simultaneous
+ *
+ * Op semantics are FIRRTL unsigned semantics masked to the op's declared
+ * width <= 64 (readings R1-R5).  All arithmetic is exact integer.
+ *
+ * Process model: one process per GPU.  A graph is loaded onto ONE device;
+ * multi-GPU lane sharding uses one rs_lanes per process with a global lane
+ * offset (rs_lane_opts.lane0), so results never depend on the GPU count.
+ *
+ * Conventions (all functions):
+ *   - Never abort or throw across the ABI.  On a non-RS_OK status outputs are
+ *     unspecified and rs_last_error() (thread-local) explains.
+ *   - The caller owns every input array; the library copies what it keeps.
+ *   - Handles are not thread-safe; free lanes before their graph.
+ *   - rs_step_cycles is asynchronous on the lanes' stream unless it writes a
+ *     HOST hash buffer; rs_read_signals / rs_write_registers synchronise.
+ */
+#ifndef RTLSIM_H
+#define RTLSIM_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RS_OK = 0,
+  RS_E_INVALID_ARG = -1,  /* NULL pointer, zero/oversized count, bad option value */
+  RS_E_GRAPH = -2,        /* comb. loop, bad arity/width/id/param, multiple or missing driver, bad level */
+  RS_E_CAPACITY = -3,     /* > 2^30 rows in a width class, arity > 63, lane count overflow */
+  RS_E_OOM = -4,          /* device or host allocation failed */
+  RS_E_CUDA = -5,         /* CUDA runtime error (message has the CUDA error string) */
+  RS_E_STATE = -6,        /* call order: e.g. staged mode with cycles not staged */
+  RS_E_RANGE = -7,        /* lane / signal / cycle index out of range */
+  RS_E_UNSUPPORTED = -8   /* valid request this build does not implement */
+} rs_status;
+
+/* Opcodes: the interchange format's numbering (same values in synth/circuit.py). */
+enum {
+  RS_OP_AND = 0, RS_OP_OR = 1, RS_OP_XOR = 2, RS_OP_NOT = 3, RS_OP_ADD = 4, RS_OP_SUB = 5,
+  RS_OP_MUL = 6, RS_OP_EQ = 7, RS_OP_LT = 8, RS_OP_SHL = 9, RS_OP_SHR = 10, RS_OP_BITS = 11,
+  RS_OP_CAT = 12, RS_OP_MUX = 13, RS_NUM_OPS = 14
+};
+
+/* Execution modes for rs_load_graph. */
+enum {
+  RS_MODE_LANES = 0,   /* many lanes: a CTA owns a lane tile; CTA barrier between levels */
+  RS_MODE_SINGLE = 1   /* one lane: ops of a level spread over the grid; grid barrier between levels */
+};
+
+/* Where a pointer lives. */
+enum { RS_MEM_NONE = 0, RS_MEM_HOST = 1, RS_MEM_DEVICE = 2 };
+
+/*
+ * Circuit in canonical-id form; signal id = index into width[].
+ * Every signal has exactly one driver: an input, a register, a constant or
+ * one op.  All arrays are host-side and caller-owned; rs_load_graph copies.
+ *   width[n_signals]          1..64 (reading R2)
+ *   input_id[n_inputs]        input k = position k (the stimulus index)
+ *   reg_id/reg_next_id[n_regs]; reg_init[n_regs] or NULL (-> 0); init is masked
+ *   const_id/const_val[n_consts]; values are masked to the width
+ *   opcode/out_id[n_ops]; operands of op j are arg_id[arg_off[j] .. arg_off[j+1])
+ *     in O-rank order (PAPER.md eq:custom_reduce P:778-796).  Arity: and/or/xor/
+ *     add/sub/mul 2..63 (left fold), eq/lt/cat 2, not/shl/shr/bits 1, mux 3
+ *     (selector, then O=1 value chosen when selector != 0, then O=2 value).
+ *   param[n_ops][2]           shl/shr: [0] = n (n >= 64 gives 0); bits: [0] = hi,
+ *                             [1] = lo (lo <= hi <= 63); other ops: ignored.
+ *                             cat's w_b is the declared width of operand 1.
+ *   level[n_ops] or NULL      optional level per op; must satisfy level(op) >
+ *                             level(producer of each operand).  NULL -> ASAP
+ *                             levels (§6.1).  Results do not
+ *                             depend on levels (§4.2).
+ */
+typedef struct {
+  uint32_t n_signals;  const uint8_t* width;
+  uint32_t n_inputs;   const uint32_t* input_id;
+  uint32_t n_regs;     const uint32_t* reg_id;   const uint32_t* reg_next_id; const uint64_t* reg_init;
+  uint32_t n_consts;   const uint32_t* const_id; const uint64_t* const_val;
+  uint32_t n_ops;      const uint8_t* opcode;    const uint32_t* out_id;
+                       const uint32_t* arg_off;  const uint32_t* arg_id;
+                       const uint32_t* param;    const uint32_t* level;
+} rs_graph_desc;
+
+/* Compiled-graph statistics (filled by rs_graph_info). */
+typedef struct {
+  uint32_t mode;
+  uint32_t n_levels;
+  uint32_t n_ops;                 /* canonical ops */
+  uint32_t n_copy_ops;            /* identity ops the compiler inserted (register -> source next edges) */
+  uint32_t n_runs;                /* (level, opcode, arity, out class) runs */
+  uint32_t n_coords;
+  uint32_t rows[4];               /* rows per width class (1, 2, 4, 8-byte containers) */
+  uint64_t state_bytes_per_lane;  /* sum_c rows[c] * 2^c */
+  uint64_t graph_device_bytes;    /* bytes of the device graph format */
+  uint64_t graph_alg_bytes;       /* G: int32 operand coords + one u32 param word per op */
+  uint64_t alg_bytes_per_lane_cycle;  /* SURVEY §8(d) B_alg per lane per cycle, excluding G */
+  uint64_t identity_ops_naive;    /* copies a naive §4.2 construction would need */
+} rs_graph_info;
+
+/* Options for rs_alloc_lanes (NULL -> all defaults). */
+typedef struct {
+  uint64_t lane0;          /* global index of this allocation's first lane (stimulus, hashes) */
+  uint32_t lane_tile;      /* RS_MODE_LANES: lanes per CTA tile, 0 = auto, else 8, 16 or 32 */
+  uint32_t threads;        /* threads per CTA, 0 = auto (multiple of 32, <= 1024) */
+  uint32_t stage_cycles;   /* capacity (cycles) of the staged-input ring, 0 = none */
+  uint32_t unroll_hint;    /* reserved, 0 */
+  void* stream;            /* cudaStream_t to run on; NULL = a stream the library creates */
+} rs_lane_opts;
+
+typedef struct rs_graph rs_graph;
+typedef struct rs_lanes rs_lanes;
+
+const char* rs_version(void);
+/* Thread-local message for the last non-RS_OK status (never NULL). */
+const char* rs_last_error(void);
+
+/* device value for rs_load_graph: compile and validate only (no device
+ * memory; the handle supports rs_graph_info_get / rs_graph_export and
+ * rs_free_graph only -- rs_alloc_lanes returns RS_E_STATE). */
+#define RS_DEVICE_NONE (-1)
+
+/* Validate + compile the circuit into the GPU graph format (levelize, insert
+ * identity copies for register->source next edges, group each level by
+ * (opcode, arity, width class) as in PAPER.md Format c P:1123-1129, renumber
+ * signals so op outputs are implicit, pack operand coords as int32) and copy
+ * it to `device`.  mode: RS_MODE_LANES or RS_MODE_SINGLE. */
+rs_status rs_load_graph(const rs_graph_desc* desc, int device, uint32_t mode, rs_graph** out);
+rs_status rs_graph_info_get(const rs_graph* g, rs_graph_info* out);
+
+/* Copy one array of the compiled graph format to host memory `out` (or,
+ * with out == NULL, only report its element count in *count).  Element
+ * types: RUNS = 5 x u32 per run {op_begin, count, coord_begin, out_row0,
+ * meta = opcode | arity<<8 | out_class<<16}; OPK = u64; all others u32.
+ * For inspection and tests of the format; never needed to simulate. */
+enum {
+  RS_EXPORT_RUNS = 0, RS_EXPORT_LEVEL_RUN_BEGIN = 1, RS_EXPORT_LEVEL_OP_BEGIN = 2, RS_EXPORT_OPW = 3,
+  RS_EXPORT_OPK = 4, RS_EXPORT_COORD_OFF = 5, RS_EXPORT_COORD = 6, RS_EXPORT_SIG_COORD = 7,
+  RS_EXPORT_REG_COORD = 8, RS_EXPORT_REG_NEXT_COORD = 9, RS_EXPORT_IN_COORD = 10
+};
+rs_status rs_graph_export(const rs_graph* g, uint32_t what, void* out, uint64_t* count);
+void rs_free_graph(rs_graph* g);
+
+/* Allocate the signal state for n_lanes lanes (RS_MODE_SINGLE: n_lanes must
+ * be 1), initialised to: registers = init & M(w), constants = value, all
+ * other signals 0; the absolute cycle counter = 0; input source = seed 0. */
+rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts, rs_lanes** out);
+void rs_free_lanes(rs_lanes* s);
+/* Device bytes held by this allocation. */
+uint64_t rs_lanes_bytes(const rs_lanes* s);
+
+/* Input source = counter-based stimulus of (seed, input k, absolute cycle,
+ * global lane) (reading R13). */
+rs_status rs_set_input_seed(rs_lanes* s, uint64_t seed);
+/* Input source = staged values for absolute cycles [first_cycle,
+ * first_cycle + n_cycles): values[n_cycles][n_inputs][n_lanes] (u64, masked to
+ * each input's width when injected), host (on_device = 0) or device memory
+ * of the lanes' device (on_device = 1).  n_cycles <= stage_cycles.  The
+ * ring keeps the last stage_cycles staged cycles. Async on the stream. */
+rs_status rs_set_inputs(rs_lanes* s, uint64_t first_cycle, uint32_t n_cycles,
+                        const uint64_t* values, int on_device);
+
+/* Advance n_cycles cycles.  hashes: RS_MEM_NONE (no hash computed, pointer
+ * ignored), RS_MEM_DEVICE ([n_cycles][n_lanes] u64 on the lanes' device) or
+ * RS_MEM_HOST ([n_cycles][n_lanes] u64 host; the call synchronises).
+ * H[c][l] = sum over all canonical signals of value * K_s mod 2^64, taken
+ * after the combinational evaluation of cycle c and before the commit. */
+rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int hashes_mem);
+
+/* Read canonical signals ids[n_ids] for lanes [lane_begin, lane_begin+n_lanes)
+ * (allocation-relative) into out[n_ids][n_lanes] (host).  Registers hold the
+ * committed values; other signals hold the values of the last cycle. Syncs. */
+rs_status rs_read_signals(rs_lanes* s, const uint32_t* ids, uint32_t n_ids,
+                          uint32_t lane_begin, uint32_t n_lanes, uint64_t* out);
+/* Checkpoint restore: overwrite registers reg_ids[n] (canonical ids of
+ * registers) for lanes [lane_begin, lane_begin+n_lanes) from values[n][n_lanes]
+ * (host, masked).  RS_E_RANGE if an id is not a register. Syncs. */
+rs_status rs_write_registers(rs_lanes* s, const uint32_t* reg_ids, uint32_t n,
+                             uint32_t lane_begin, uint32_t n_lanes, const uint64_t* values);
+rs_status rs_get_cycle(const rs_lanes* s, uint64_t* cycle);
+rs_status rs_set_cycle(rs_lanes* s, uint64_t cycle);
+/* Kernel launches issued by this allocation so far (evidence counter). */
+uint64_t rs_launch_count(const rs_lanes* s);
+/* Chosen launch shape: lane tile, threads per CTA, CTAs. */
+rs_status rs_launch_shape(const rs_lanes* s, uint32_t* lane_tile, uint32_t* threads, uint32_t* ctas);
+rs_status rs_sync(rs_lanes* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,335 @@
+// compiler.cpp -- see compiler.hpp.
+#include "compiler.hpp"
+
+#include <algorithm>
+#include <cstdio>
+#include <numeric>
+#include <unordered_map>
+
+namespace rtlsim {
+
+uint64_t CompiledGraph::device_bytes() const {
+  return opw.size() * 4ull + opk.size() * 8ull + coord_off.size() * 4ull + coord.size() * 4ull +
+         runs.size() * sizeof(DevRun) + (level_run_begin.size() + level_op_begin.size()) * 4ull +
+         in_coord.size() * 16ull + reg_coord.size() * 28ull;
+}
+
+namespace {
+
+bool fixed_arity_ok(uint32_t op, uint32_t n) {
+  switch (op) {
+    case RS_OP_AND: case RS_OP_OR: case RS_OP_XOR: case RS_OP_ADD: case RS_OP_SUB: case RS_OP_MUL:
+      return n >= 2 && n <= MAX_ARITY;
+    case RS_OP_EQ: case RS_OP_LT: case RS_OP_CAT: return n == 2;
+    case RS_OP_NOT: case RS_OP_SHL: case RS_OP_SHR: case RS_OP_BITS: return n == 1;
+    case RS_OP_MUX: return n == 3;
+    default: return false;
+  }
+}
+
+rs_status fail(std::string* err, rs_status st, const char* fmt, unsigned long long a = 0,
+               unsigned long long b = 0) {
+  char buf[256];
+  snprintf(buf, sizeof buf, fmt, a, b);
+  *err = buf;
+  return st;
+}
+
+}  // namespace
+
+rs_status compile_graph(const rs_graph_desc* d, uint32_t mode, CompiledGraph* out, std::string* err) {
+  if (!d || !out) return fail(err, RS_E_INVALID_ARG, "NULL desc or out");
+  if (mode != RS_MODE_LANES && mode != RS_MODE_SINGLE)
+    return fail(err, RS_E_INVALID_ARG, "unknown mode %llu", mode);
+  const uint32_t NS = d->n_signals, NO = d->n_ops;
+  if (NS > 0 && !d->width) return fail(err, RS_E_INVALID_ARG, "width is NULL");
+  if ((d->n_inputs && !d->input_id) || (d->n_regs && (!d->reg_id || !d->reg_next_id)) ||
+      (d->n_consts && (!d->const_id || !d->const_val)) ||
+      (NO && (!d->opcode || !d->out_id || !d->arg_off || !d->arg_id)))
+    return fail(err, RS_E_INVALID_ARG, "NULL array with nonzero count");
+  if (NO && d->arg_off[0] != 0) return fail(err, RS_E_GRAPH, "arg_off[0] must be 0");
+
+  CompiledGraph& g = *out;
+  g = CompiledGraph();
+  g.mode = mode;
+  g.n_signals = NS;
+  g.n_inputs = d->n_inputs;
+  g.n_regs = d->n_regs;
+  g.n_consts = d->n_consts;
+  g.n_ops = NO;
+
+  for (uint32_t s = 0; s < NS; ++s)
+    if (d->width[s] < 1 || d->width[s] > 64)
+      return fail(err, RS_E_GRAPH, "signal %llu has width %llu (must be 1..64)", s, d->width[s]);
+
+  // ---- drivers: exactly one per signal
+  // driver: -1 none, -2 input, -3 reg, -4 const, >=0 op index
+  std::vector<int64_t> drv(NS, -1);
+  auto claim = [&](uint32_t s, int64_t v) -> bool {
+    if (s >= NS || drv[s] != -1) return false;
+    drv[s] = v;
+    return true;
+  };
+  for (uint32_t i = 0; i < d->n_inputs; ++i)
+    if (!claim(d->input_id[i], -2)) return fail(err, RS_E_GRAPH, "input %llu: bad id or multiple drivers", i);
+  for (uint32_t i = 0; i < d->n_regs; ++i)
+    if (!claim(d->reg_id[i], -3)) return fail(err, RS_E_GRAPH, "register %llu: bad id or multiple drivers", i);
+  for (uint32_t i = 0; i < d->n_consts; ++i)
+    if (!claim(d->const_id[i], -4)) return fail(err, RS_E_GRAPH, "const %llu: bad id or multiple drivers", i);
+  for (uint32_t j = 0; j < NO; ++j)
+    if (!claim(d->out_id[j], j)) return fail(err, RS_E_GRAPH, "op %llu: bad out id or multiple drivers", j);
+  for (uint32_t s = 0; s < NS; ++s)
+    if (drv[s] == -1) return fail(err, RS_E_GRAPH, "signal %llu has no driver", s);
+  for (uint32_t i = 0; i < d->n_regs; ++i)
+    if (d->reg_next_id[i] >= NS) return fail(err, RS_E_GRAPH, "register %llu: next id out of range", i);
+
+  // ---- ops: opcode, arity, params, operand ids
+  for (uint32_t j = 0; j < NO; ++j) {
+    const uint32_t op = d->opcode[j];
+    if (d->arg_off[j + 1] < d->arg_off[j]) return fail(err, RS_E_GRAPH, "op %llu: arg_off decreasing", j);
+    const uint32_t n = d->arg_off[j + 1] - d->arg_off[j];
+    if (op >= RS_NUM_OPS) return fail(err, RS_E_GRAPH, "op %llu: unknown opcode %llu", j, op);
+    if (n > MAX_ARITY && (op == RS_OP_AND || op == RS_OP_OR || op == RS_OP_XOR || op == RS_OP_ADD ||
+                          op == RS_OP_SUB || op == RS_OP_MUL))
+      return fail(err, RS_E_CAPACITY, "op %llu: arity %llu > 63", j, n);
+    if (!fixed_arity_ok(op, n)) return fail(err, RS_E_GRAPH, "op %llu: bad arity %llu", j, n);
+    for (uint32_t a = d->arg_off[j]; a < d->arg_off[j + 1]; ++a)
+      if (d->arg_id[a] >= NS) return fail(err, RS_E_GRAPH, "op %llu: operand id out of range", j);
+    if (op == RS_OP_BITS) {
+      if (!d->param) return fail(err, RS_E_GRAPH, "op %llu: bits needs param", j);
+      const uint32_t hi = d->param[2 * j], lo = d->param[2 * j + 1];
+      if (lo > hi || hi > 63) return fail(err, RS_E_GRAPH, "op %llu: bits hi=%llu lo out of range", j, hi);
+    }
+    if ((op == RS_OP_SHL || op == RS_OP_SHR) && !d->param)
+      return fail(err, RS_E_GRAPH, "op %llu: shift needs param", j);
+  }
+
+  // ---- levels (ASAP via Kahn, or validated given levels)
+  std::vector<uint32_t> lev(NO, 0);
+  {
+    std::vector<uint32_t> indeg(NO, 0), cnt(NS + 1, 0);
+    for (uint32_t j = 0; j < NO; ++j)
+      for (uint32_t a = d->arg_off[j]; a < d->arg_off[j + 1]; ++a)
+        if (drv[d->arg_id[a]] >= 0) { indeg[j]++; cnt[d->arg_id[a]]++; }
+    std::vector<uint32_t> off(NS + 1, 0);
+    for (uint32_t s = 0; s < NS; ++s) off[s + 1] = off[s] + cnt[s];
+    std::vector<uint32_t> users(off[NS]), fill(NS, 0);
+    for (uint32_t j = 0; j < NO; ++j)
+      for (uint32_t a = d->arg_off[j]; a < d->arg_off[j + 1]; ++a) {
+        uint32_t s = d->arg_id[a];
+        if (drv[s] >= 0) users[off[s] + fill[s]++] = j;
+      }
+    std::vector<uint32_t> q;
+    q.reserve(NO);
+    for (uint32_t j = 0; j < NO; ++j) if (indeg[j] == 0) q.push_back(j);
+    for (size_t h = 0; h < q.size(); ++h) {
+      const uint32_t j = q[h], s = d->out_id[j];
+      for (uint32_t u = off[s]; u < off[s + 1]; ++u) {
+        const uint32_t k = users[u];
+        lev[k] = std::max(lev[k], lev[j] + 1);
+        if (--indeg[k] == 0) q.push_back(k);
+      }
+    }
+    if (q.size() != NO) return fail(err, RS_E_GRAPH, "combinational loop (%llu ops unreachable)", NO - q.size());
+  }
+  if (d->level) {
+    for (uint32_t j = 0; j < NO; ++j) {
+      for (uint32_t a = d->arg_off[j]; a < d->arg_off[j + 1]; ++a) {
+        const int64_t p = drv[d->arg_id[a]];
+        if (p >= 0 && d->level[p] >= d->level[j])
+          return fail(err, RS_E_GRAPH, "op %llu: level not above operand producer op %llu", j, p);
+      }
+      if (d->level[j] > (1u << 24)) return fail(err, RS_E_CAPACITY, "op %llu: level too large", j);
+    }
+    for (uint32_t j = 0; j < NO; ++j) lev[j] = d->level[j];
+  }
+  uint32_t n_levels = 0;
+  for (uint32_t j = 0; j < NO; ++j) n_levels = std::max(n_levels, lev[j] + 1);
+
+  // ---- identity copies for register next edges that point at an input or a
+  // register: the kernel commits registers in one pass and injects the next
+  // cycle's inputs in the same phase, so the latch must only read op rows.
+  struct Copy { uint32_t src; };
+  std::vector<Copy> copies;
+  std::unordered_map<uint32_t, uint32_t> copy_of;  // source signal -> copy index
+  std::vector<uint32_t> reg_src(d->n_regs);          // effective next: signal id or NS + copy index
+  for (uint32_t i = 0; i < d->n_regs; ++i) {
+    const uint32_t nx = d->reg_next_id[i];
+    if (drv[nx] == -2 || drv[nx] == -3) {
+      auto it = copy_of.find(nx);
+      uint32_t ci;
+      if (it == copy_of.end()) {
+        ci = (uint32_t)copies.size();
+        copies.push_back({nx});
+        copy_of[nx] = ci;
+      } else {
+        ci = it->second;
+      }
+      reg_src[i] = NS + ci;
+    } else {
+      reg_src[i] = nx;
+    }
+  }
+  if (!copies.empty() && n_levels == 0) n_levels = 1;
+  g.n_copy = (uint32_t)copies.size();
+  g.n_levels = n_levels;
+  const uint32_t NT = NO + g.n_copy;  // total ops (canonical + copies); copies are op NO + ci
+
+  auto op_code = [&](uint32_t t) -> uint32_t { return t < NO ? d->opcode[t] : OP_COPY; };
+  auto op_arity = [&](uint32_t t) -> uint32_t { return t < NO ? d->arg_off[t + 1] - d->arg_off[t] : 1; };
+  auto op_width = [&](uint32_t t) -> uint32_t {
+    return t < NO ? d->width[d->out_id[t]] : d->width[copies[t - NO].src];
+  };
+  auto op_level = [&](uint32_t t) -> uint32_t { return t < NO ? lev[t] : 0; };
+
+  // ---- group each level by (opcode, arity, out class): Format-c swizzle
+  std::vector<uint32_t> order(NT);
+  std::iota(order.begin(), order.end(), 0u);
+  auto key = [&](uint32_t t) -> uint64_t {
+    return ((uint64_t)op_level(t) << 32) | ((uint64_t)op_code(t) << 16) | ((uint64_t)op_arity(t) << 8) |
+           width_class(op_width(t));
+  };
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return key(a) < key(b); });
+
+  // ---- rows: per class, [consts][inputs][registers][ops in device order]
+  std::vector<uint32_t> sig_coord(NS + g.n_copy, 0);
+  uint32_t rows[4] = {0, 0, 0, 0};
+  auto assign = [&](uint32_t sig, uint32_t w) -> bool {
+    const uint32_t c = width_class(w);
+    if (rows[c] >= MAX_ROWS) return false;
+    sig_coord[sig] = make_coord(c, rows[c]++);
+    return true;
+  };
+  for (uint32_t i = 0; i < d->n_consts; ++i)
+    if (!assign(d->const_id[i], d->width[d->const_id[i]])) return fail(err, RS_E_CAPACITY, "> 2^30 rows in a class");
+  for (uint32_t i = 0; i < d->n_inputs; ++i)
+    if (!assign(d->input_id[i], d->width[d->input_id[i]])) return fail(err, RS_E_CAPACITY, "> 2^30 rows in a class");
+  for (uint32_t i = 0; i < d->n_regs; ++i)
+    if (!assign(d->reg_id[i], d->width[d->reg_id[i]])) return fail(err, RS_E_CAPACITY, "> 2^30 rows in a class");
+
+  g.level_run_begin.assign(n_levels + 1, 0);
+  g.level_op_begin.assign(n_levels + 1, 0);
+  g.opw.reserve(NT);
+  g.opk.reserve(NT);
+  g.coord_off.reserve(NT + 1);
+  g.coord_off.push_back(0);
+  {
+    // out rows first (implicit S coordinates), run by run
+    size_t i = 0;
+    uint32_t cur_level = 0;
+    while (i < NT) {
+      const uint32_t t0 = order[i];
+      const uint64_t k0 = key(t0);
+      size_t e = i;
+      while (e < NT && key(order[e]) == k0) ++e;
+      const uint32_t L = op_level(t0);
+      while (cur_level < L) { ++cur_level; g.level_run_begin[cur_level] = (uint32_t)g.runs.size(); g.level_op_begin[cur_level] = (uint32_t)i; }
+      DevRun r;
+      r.op_begin = (uint32_t)i;
+      r.count = (uint32_t)(e - i);
+      r.coord_begin = 0;  // filled below
+      const uint32_t cls = width_class(op_width(t0));
+      r.out_row0 = rows[cls];
+      r.meta = op_code(t0) | (op_arity(t0) << 8) | (cls << 16);
+      for (size_t k = i; k < e; ++k) {
+        const uint32_t t = order[k];
+        const uint32_t sig = t < NO ? d->out_id[t] : NS + (t - NO);
+        if (!assign(sig, op_width(t))) return fail(err, RS_E_CAPACITY, "> 2^30 rows in a class");
+      }
+      g.runs.push_back(r);
+      i = e;
+    }
+    while (cur_level < n_levels) { ++cur_level; g.level_run_begin[cur_level] = (uint32_t)g.runs.size(); g.level_op_begin[cur_level] = (uint32_t)NT; }
+    g.level_run_begin[n_levels] = (uint32_t)g.runs.size();
+    g.level_op_begin[n_levels] = NT;
+  }
+  for (int c = 0; c < 4; ++c) g.rows[c] = rows[c];
+
+  // ---- per-op arrays in device order
+  size_t run_i = 0;
+  for (uint32_t k = 0; k < NT; ++k) {
+    while (run_i + 1 < g.runs.size() && g.runs[run_i + 1].op_begin <= k) ++run_i;
+    if (!g.runs.empty() && g.runs[run_i].op_begin == k) g.runs[run_i].coord_begin = (uint32_t)g.coord.size();
+    const uint32_t t = order[k];
+    const uint32_t op = op_code(t), n = op_arity(t), w = op_width(t);
+    uint32_t p0 = 0, p1 = 0;
+    if (t < NO) {
+      const uint32_t a0 = d->arg_off[t];
+      if (op == RS_OP_SHL || op == RS_OP_SHR) p0 = std::min<uint32_t>(d->param[2 * t], 64u);
+      if (op == RS_OP_BITS) { p0 = d->param[2 * t]; p1 = d->param[2 * t + 1]; }
+      if (op == RS_OP_CAT) p0 = d->width[d->arg_id[a0 + 1]];
+      for (uint32_t a = a0; a < a0 + n; ++a) g.coord.push_back(sig_coord[d->arg_id[a]]);
+      g.opk.push_back(hash_weight(d->out_id[t]));
+    } else {
+      g.coord.push_back(sig_coord[copies[t - NO].src]);
+      g.opk.push_back(0);
+    }
+    g.opw.push_back(pack_pw(w, p0, p1, width_class(w), op, n));
+    g.coord_off.push_back((uint32_t)g.coord.size());
+  }
+
+  // ---- inputs, registers, constants
+  uint64_t B = 0;
+  for (uint32_t i = 0; i < d->n_inputs; ++i) {
+    const uint32_t s = d->input_id[i];
+    g.in_coord.push_back(sig_coord[s]);
+    g.in_w.push_back(d->width[s]);
+    g.in_k.push_back(hash_weight(s));
+    B += 1ull << width_class(d->width[s]);
+  }
+  for (uint32_t i = 0; i < d->n_regs; ++i) {
+    const uint32_t s = d->reg_id[i];
+    const uint32_t w = d->width[s];
+    g.reg_coord.push_back(sig_coord[s]);
+    g.reg_next_coord.push_back(sig_coord[reg_src[i]]);
+    g.reg_w.push_back(w);
+    g.reg_k.push_back(hash_weight(s));
+    const uint64_t init = (d->reg_init ? d->reg_init[i] : 0) & width_mask(w);
+    g.reg_init.push_back(init);
+    g.init_reg_hash += init * hash_weight(s);
+    B += (1ull << width_class(w)) + (1ull << width_class(d->width[d->reg_next_id[i]]));
+  }
+  for (uint32_t i = 0; i < d->n_consts; ++i) {
+    const uint32_t s = d->const_id[i];
+    const uint64_t v = d->const_val[i] & width_mask(d->width[s]);
+    g.const_coord.push_back(sig_coord[s]);
+    g.const_val.push_back(v);
+    g.const_hash += v * hash_weight(s);
+  }
+  // canonical maps
+  g.sig_coord.assign(sig_coord.begin(), sig_coord.begin() + NS);
+  g.sig_kind.assign(NS, 3);
+  g.sig_reg_index.assign(NS, -1);
+  for (uint32_t i = 0; i < d->n_inputs; ++i) g.sig_kind[d->input_id[i]] = 0;
+  for (uint32_t i = 0; i < d->n_regs; ++i) { g.sig_kind[d->reg_id[i]] = 1; g.sig_reg_index[d->reg_id[i]] = (int32_t)i; }
+  for (uint32_t i = 0; i < d->n_consts; ++i) g.sig_kind[d->const_id[i]] = 2;
+
+  // ---- statistics: B_alg per lane-cycle, G, naive identity count
+  uint64_t G = 0;
+  for (uint32_t j = 0; j < NO; ++j) {
+    const uint32_t a0 = d->arg_off[j], a1 = d->arg_off[j + 1];
+    for (uint32_t a = a0; a < a1; ++a) B += 1ull << width_class(d->width[d->arg_id[a]]);
+    B += 1ull << width_class(d->width[d->out_id[j]]);
+    G += 4ull * (a1 - a0) + 4ull;
+  }
+  g.alg_bytes_per_lane_cycle = B;
+  g.graph_alg_bytes = G;
+  {
+    // naive §4.2 construction: a value produced at level l (sources: -1) and
+    // last needed at level u needs u - l - 1 identity copies; register next
+    // values are needed after the last level (level n_levels).
+    std::vector<int64_t> plev(NS, -1), last(NS, -1);
+    for (uint32_t j = 0; j < NO; ++j) plev[d->out_id[j]] = lev[j];
+    for (uint32_t j = 0; j < NO; ++j)
+      for (uint32_t a = d->arg_off[j]; a < d->arg_off[j + 1]; ++a)
+        last[d->arg_id[a]] = std::max<int64_t>(last[d->arg_id[a]], lev[j]);
+    for (uint32_t i = 0; i < d->n_regs; ++i) last[d->reg_next_id[i]] = std::max<int64_t>(last[d->reg_next_id[i]], n_levels);
+    uint64_t ids = 0;
+    for (uint32_t s = 0; s < NS; ++s)
+      if (last[s] - plev[s] - 1 > 0) ids += (uint64_t)(last[s] - plev[s] - 1);
+    g.identity_ops_naive = ids;
+  }
+  return RS_OK;
+}
+
+}  // namespace rtlsim

@@ -1,0 +1,105 @@
+// compiler.hpp -- host graph-tensor compiler.
+//
+// Turns an rs_graph_desc (canonical ids) into the GPU graph format:
+//   * levelization (§4.2; §6.1 P:1266 "slicing the graph
+//     into layers via topological sort");
+//   * identity elision by coordinate assignment (§4.3 P:1030-1039,
+//     P:1272-1273): every signal keeps ONE row for the whole cycle, so no
+//     identity copies are stored; the only copies inserted are for register
+//     next edges that point at a source (an input or a register), which the
+//     single-pass commit of the kernel needs (DESIGN.md §"Register commit");
+//   * Format-c swizzle (§5.1, alg:NU P:1171-1174): each level's
+//     ops grouped into runs by (opcode, arity, width class) so a warp never
+//     diverges on the op, and each run writes consecutive rows of its class
+//     (the S coordinate array vanishes: out rows are implicit);
+//   * operand coordinates (the R coordinates of OIM) packed as int32:
+//     bits 31..30 = width class, bits 29..0 = row in that class array.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/rtlsim.h"
+
+namespace rtlsim {
+
+constexpr uint32_t OP_COPY = 14;         // internal identity op (never in a desc)
+constexpr uint32_t ROW_MASK = 0x3FFFFFFFu;
+constexpr uint32_t MAX_ROWS = 1u << 30;
+constexpr uint32_t MAX_ARITY = 63;
+
+inline uint32_t width_class(uint32_t w) { return w <= 8 ? 0 : w <= 16 ? 1 : w <= 32 ? 2 : 3; }
+inline uint32_t make_coord(uint32_t cls, uint32_t row) { return (cls << 30) | row; }
+
+// Param word of one op (u32):
+//   [6:0] w_out  [13:7] p0  [19:14] p1  [21:20] out class  [25:22] opcode  [31:26] arity
+//   p0 = shl/shr amount clamped to 64 | bits hi | cat w_b;  p1 = bits lo.
+inline uint32_t pack_pw(uint32_t w_out, uint32_t p0, uint32_t p1, uint32_t cls, uint32_t op,
+                        uint32_t arity) {
+  return (w_out & 127u) | ((p0 & 127u) << 7) | ((p1 & 63u) << 14) | ((cls & 3u) << 20) |
+         ((op & 15u) << 22) | ((arity & 63u) << 26);
+}
+
+struct DevRun {            // one (level, opcode, arity, out class) run
+  uint32_t op_begin;       // index of the run's first op in the per-op arrays
+  uint32_t count;
+  uint32_t coord_begin;    // index of the first operand coord
+  uint32_t out_row0;       // first output row in the out class array
+  uint32_t meta;           // opcode | arity << 8 | out_cls << 16
+};
+
+struct CompiledGraph {
+  uint32_t mode = 0;
+  uint32_t n_signals = 0, n_inputs = 0, n_regs = 0, n_consts = 0;
+  uint32_t n_ops = 0, n_copy = 0, n_levels = 0;
+  uint32_t rows[4] = {0, 0, 0, 0};
+  // per-op arrays in device order (level-major, run-major)
+  std::vector<uint32_t> opw;        // param word
+  std::vector<uint64_t> opk;        // hash weight of the op's output (0 for copies)
+  std::vector<uint32_t> coord_off;  // [n_ops_total + 1]
+  std::vector<uint32_t> coord;      // packed operand coords
+  std::vector<DevRun> runs;
+  std::vector<uint32_t> level_run_begin;  // [n_levels + 1]
+  std::vector<uint32_t> level_op_begin;   // [n_levels + 1]
+  // inputs (stimulus index k = position)
+  std::vector<uint32_t> in_coord;
+  std::vector<uint32_t> in_w;
+  std::vector<uint64_t> in_k;
+  // registers (latch)
+  std::vector<uint32_t> reg_coord, reg_next_coord, reg_w;
+  std::vector<uint64_t> reg_k, reg_init;
+  // constants
+  std::vector<uint32_t> const_coord;
+  std::vector<uint64_t> const_val;
+  // canonical id -> coord; kind 0 input 1 reg 2 const 3 op
+  std::vector<uint32_t> sig_coord;
+  std::vector<uint8_t> sig_kind;
+  std::vector<int32_t> sig_reg_index;
+  uint64_t const_hash = 0;
+  uint64_t init_reg_hash = 0;
+  // statistics
+  uint64_t alg_bytes_per_lane_cycle = 0;
+  uint64_t graph_alg_bytes = 0;
+  uint64_t identity_ops_naive = 0;
+
+  uint32_t n_ops_total() const { return (uint32_t)opw.size(); }
+  uint64_t state_bytes_per_lane() const {
+    return (uint64_t)rows[0] + 2ull * rows[1] + 4ull * rows[2] + 8ull * rows[3];
+  }
+  uint64_t device_bytes() const;
+};
+
+// splitmix64 (public algorithm; independent implementation of DESIGN.md R12/R13)
+inline uint64_t splitmix_next(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+inline uint64_t hash_weight(uint64_t s) { return splitmix_next(0x5EED000000000000ull + s) | 1ull; }
+inline uint64_t width_mask(uint32_t w) { return w >= 64 ? ~0ull : ((1ull << w) - 1ull); }
+
+// Returns RS_OK or an error status with *err set.
+rs_status compile_graph(const rs_graph_desc* d, uint32_t mode, CompiledGraph* out, std::string* err);
+
+}  // namespace rtlsim

@@ -1,0 +1,599 @@
+// kernels.cuh -- sm_100a step kernels for the RTeAAL Sim cascade.
+//
+// State layout (SURVEY.md §8(a) "signal-major x lane-minor"): one array per
+// width class c (containers of 2^c bytes), laid out [tile][row][LT]: a
+// lane tile's rows are contiguous and, inside a row, the LT lanes are
+// contiguous, so the gather of one operand for the tile's lanes is one
+// coalesced LT * 2^c byte access (PAPER.md P:1441-1443 names this gather as
+// the CPU kernels' main D-cache-miss source).
+//
+// Lane mode (k_lanes): CTA = one lane tile; the CTA's sub-warps (LT threads
+// each) split every level's ops into contiguous chunks; a sub-warp walks its
+// chunk run by run -- one (opcode, arity) specialisation per run, the NU
+// "switch hoisted out of the op loop" (alg:NU P:1175-1202) -- gathering U
+// ops' operands before computing any (the PSU partial S unrolling,
+// P:1204-1209, used here for memory-level parallelism).  __syncthreads is the
+// level barrier (iterative rank I).
+//
+// Single-lane mode (k_single): one op per thread, all CTAs of a cooperative
+// grid; a grid barrier separates levels.
+#pragma once
+#include <cstdint>
+
+#include "compiler.hpp"
+
+namespace rtlsim {
+
+struct GraphDev {
+  const DevRun* runs;
+  const uint32_t* level_run_begin;
+  const uint32_t* level_op_begin;
+  const uint32_t* opw;
+  const uint64_t* opk;
+  const uint32_t* coord_off;
+  const uint32_t* coord;
+  const uint32_t* out_coord;
+  const uint32_t* in_coord;
+  const uint32_t* in_w;
+  const uint64_t* in_k;
+  const uint32_t* reg_coord;
+  const uint32_t* reg_next_coord;
+  const uint32_t* reg_w;
+  const uint64_t* reg_k;
+  uint32_t n_levels, n_inputs, n_regs, n_ops_total;
+  uint64_t const_hash;
+};
+
+struct StepArgs {
+  GraphDev g;
+  uint8_t* st[4];          // class base pointers
+  uint32_t rows[4];
+  uint32_t n_lanes;        // lanes in this allocation
+  uint64_t lane0;          // global id of lane 0
+  uint64_t cycle0;         // absolute cycle of the first stepped cycle
+  uint32_t n_cycles;
+  int staged;              // 0: stimulus from seed; 1: staged ring
+  uint64_t seed;
+  const uint64_t* stage;   // [stage_cap][n_inputs][n_lanes]
+  uint32_t stage_cap;
+  uint64_t* hashes;        // [n_cycles][n_lanes] or nullptr
+  uint64_t* hcarry_in;     // per-lane register-term of the hash for cycle0
+  uint64_t* hcarry_out;    // same for cycle0 + n_cycles (may alias hcarry_in in lane mode)
+  unsigned long long* bar; // grid barrier counter (single mode)
+};
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ uint64_t wmask(uint32_t w) { return ~0ull >> (64u - w); }  // w in 1..64
+
+__device__ __forceinline__ uint64_t d_splitmix_next(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+// DESIGN.md reading R13 (independent of oracle/; same public algorithm).
+__device__ __forceinline__ uint64_t d_stimulus(uint64_t seed, uint64_t k, uint64_t c, uint64_t lane) {
+  uint64_t x = d_splitmix_next(seed);
+  x = d_splitmix_next(x + k);
+  x = d_splitmix_next(x + c);
+  return d_splitmix_next(x + lane);
+}
+
+template <int LT>
+struct TileP {
+  uint8_t* p0;
+  uint16_t* p1;
+  uint32_t* p2;
+  uint64_t* p3;
+  __device__ __forceinline__ uint64_t ld(uint32_t c) const {
+    const size_t r = (size_t)(c & ROW_MASK) * LT;
+    switch (c >> 30) {
+      case 0: return p0[r];
+      case 1: return p1[r];
+      case 2: return p2[r];
+      default: return p3[r];
+    }
+  }
+  // L2-coherent load (single-lane mode: other SMs write the state)
+  __device__ __forceinline__ uint64_t ld_cg(uint32_t c) const {
+    const size_t r = (size_t)(c & ROW_MASK) * LT;
+    switch (c >> 30) {
+      case 0: return __ldcg(p0 + r);
+      case 1: return __ldcg(p1 + r);
+      case 2: return __ldcg(p2 + r);
+      default: return __ldcg(p3 + r);
+    }
+  }
+  __device__ __forceinline__ void st(uint32_t cls, uint32_t row, uint64_t v) const {
+    const size_t r = (size_t)row * LT;
+    switch (cls) {
+      case 0: p0[r] = (uint8_t)v; break;
+      case 1: p1[r] = (uint16_t)v; break;
+      case 2: p2[r] = (uint32_t)v; break;
+      default: p3[r] = v; break;
+    }
+  }
+  __device__ __forceinline__ void stc(uint32_t c, uint64_t v) const { st(c >> 30, c & ROW_MASK, v); }
+};
+
+template <int LT>
+__device__ __forceinline__ TileP<LT> tile_ptrs(const StepArgs& a, uint32_t tile, uint32_t lin) {
+  TileP<LT> t;
+  t.p0 = a.st[0] + ((size_t)tile * a.rows[0] * LT + lin);
+  t.p1 = reinterpret_cast<uint16_t*>(a.st[1]) + ((size_t)tile * a.rows[1] * LT + lin);
+  t.p2 = reinterpret_cast<uint32_t*>(a.st[2]) + ((size_t)tile * a.rows[2] * LT + lin);
+  t.p3 = reinterpret_cast<uint64_t*>(a.st[3]) + ((size_t)tile * a.rows[3] * LT + lin);
+  return t;
+}
+
+// op_u / op_r / op_s of Cascade 1 for one op with A operands (A = 0: runtime n).
+// pw: [6:0] w_out [13:7] p0 [19:14] p1 (compiler.hpp pack_pw).
+template <int OP, int A>
+__device__ __forceinline__ uint64_t apply_op(const uint64_t* x, uint32_t pw) {
+  uint64_t r;
+  const uint32_t p0 = (pw >> 7) & 127u;
+  if constexpr (OP == RS_OP_AND) { r = x[0]; _Pragma("unroll") for (int o = 1; o < A; ++o) r &= x[o]; }
+  else if constexpr (OP == RS_OP_OR) { r = x[0]; _Pragma("unroll") for (int o = 1; o < A; ++o) r |= x[o]; }
+  else if constexpr (OP == RS_OP_XOR) { r = x[0]; _Pragma("unroll") for (int o = 1; o < A; ++o) r ^= x[o]; }
+  else if constexpr (OP == RS_OP_ADD) { r = x[0]; _Pragma("unroll") for (int o = 1; o < A; ++o) r += x[o]; }
+  else if constexpr (OP == RS_OP_SUB) { r = x[0]; _Pragma("unroll") for (int o = 1; o < A; ++o) r -= x[o]; }
+  else if constexpr (OP == RS_OP_MUL) { r = x[0]; _Pragma("unroll") for (int o = 1; o < A; ++o) r *= x[o]; }
+  else if constexpr (OP == RS_OP_EQ) { r = (x[0] == x[1]) ? 1ull : 0ull; }
+  else if constexpr (OP == RS_OP_LT) { r = (x[0] < x[1]) ? 1ull : 0ull; }
+  else if constexpr (OP == RS_OP_NOT) { r = ~x[0]; }
+  else if constexpr (OP == RS_OP_SHL) { r = p0 >= 64 ? 0ull : (x[0] << p0); }
+  else if constexpr (OP == RS_OP_SHR) { r = p0 >= 64 ? 0ull : (x[0] >> p0); }
+  else if constexpr (OP == RS_OP_BITS) {
+    const uint32_t lo = (pw >> 14) & 63u;
+    r = (x[0] >> lo) & wmask(p0 - lo + 1u);
+  }
+  else if constexpr (OP == RS_OP_CAT) { r = p0 >= 64 ? x[1] : ((x[0] << p0) | x[1]); }
+  else if constexpr (OP == RS_OP_MUX) { r = x[0] != 0 ? x[1] : x[2]; }
+  else { r = x[0]; }  // OP_COPY
+  return r & wmask(pw & 127u);
+}
+
+// Runtime-arity fold (arity > 3; rare).
+__device__ __forceinline__ uint64_t fold_step(uint32_t op, uint64_t r, uint64_t x) {
+  switch (op) {
+    case RS_OP_AND: return r & x;
+    case RS_OP_OR: return r | x;
+    case RS_OP_XOR: return r ^ x;
+    case RS_OP_ADD: return r + x;
+    case RS_OP_SUB: return r - x;
+    default: return r * x;
+  }
+}
+
+// ------------------------------------------------------------------ lane mode
+// Everything a run segment needs, passed by value (registers) to a
+// non-inlined specialisation: keeps each (opcode, arity) body's register
+// allocation independent of the kernel's outer loops.
+template <int LT>
+struct SegCtx {
+  TileP<LT> t;
+  const uint32_t* __restrict__ coord;
+  const uint32_t* __restrict__ opw;
+  const uint64_t* __restrict__ opk;
+};
+
+template <int LT, bool HASH, int OP, int A>
+__device__ __noinline__ uint64_t run_segment(uint8_t* p0, uint16_t* p1, uint32_t* p2, uint64_t* p3,
+                                             const uint32_t* __restrict__ coord, const uint32_t* __restrict__ opw,
+                                             const uint64_t* __restrict__ opk, uint32_t op_begin,
+                                             uint32_t coord_begin, uint32_t out_row0, uint32_t out_cls,
+                                             uint32_t b, uint32_t e) {
+  constexpr int U = (A <= 2) ? 8 : 4;
+  const SegCtx<LT> c{{p0, p1, p2, p3}, coord, opw, opk};
+  uint64_t hacc = 0;
+  const uint32_t* __restrict__ cp = c.coord + coord_begin + (b - op_begin) * A;
+  uint32_t row = out_row0 + (b - op_begin);
+  for (uint32_t j = b; j < e; j += U, cp += U * A, row += U) {
+    uint64_t x[U][A];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (j + u < e) {
+#pragma unroll
+        for (int o = 0; o < A; ++o) x[u][o] = c.t.ld(__ldg(cp + u * A + o));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (j + u < e) {
+        const uint64_t y = apply_op<OP, A>(x[u], __ldg(c.opw + j + u));
+        c.t.st(out_cls, row + u, y);
+        if constexpr (HASH) hacc += y * __ldg(c.opk + j + u);
+      }
+    }
+  }
+  return hacc;
+}
+
+template <int LT, bool HASH>
+__device__ __noinline__ uint64_t run_generic(const SegCtx<LT> c, const DevRun run, uint32_t b, uint32_t e) {
+  const uint32_t op = run.meta & 0xffu, n = (run.meta >> 8) & 0xffu, out_cls = (run.meta >> 16) & 3u;
+  uint64_t hacc = 0;
+  for (uint32_t j = b; j < e; ++j) {
+    const uint32_t* cp = c.coord + run.coord_begin + (j - run.op_begin) * n;
+    uint64_t r = c.t.ld(__ldg(cp));
+    for (uint32_t o = 1; o < n; ++o) r = fold_step(op, r, c.t.ld(__ldg(cp + o)));
+    const uint64_t y = r & wmask(__ldg(c.opw + j) & 127u);
+    c.t.st(out_cls, run.out_row0 + (j - run.op_begin), y);
+    if constexpr (HASH) hacc += y * __ldg(c.opk + j);
+  }
+  return hacc;
+}
+
+template <int LT, bool HASH>
+__device__ __forceinline__ uint64_t dispatch_run(const SegCtx<LT>& c, const DevRun& run, uint32_t b, uint32_t e) {
+  const uint32_t op = run.meta & 0xffu, n = (run.meta >> 8) & 0xffu;
+#define RS_SEG(OPC, N) \
+  run_segment<LT, HASH, OPC, N>(c.t.p0, c.t.p1, c.t.p2, c.t.p3, c.coord, c.opw, c.opk, run.op_begin, \
+                                run.coord_begin, run.out_row0, (run.meta >> 16) & 3u, b, e)
+#define RS_FOLD(OPC)                                                    \
+  case OPC:                                                             \
+    if (n == 2) return RS_SEG(OPC, 2);                                  \
+    if (n == 3) return RS_SEG(OPC, 3);                                  \
+    return run_generic<LT, HASH>(c, run, b, e);
+  switch (op) {
+    RS_FOLD(RS_OP_AND)
+    RS_FOLD(RS_OP_OR)
+    RS_FOLD(RS_OP_XOR)
+    RS_FOLD(RS_OP_ADD)
+    RS_FOLD(RS_OP_SUB)
+    RS_FOLD(RS_OP_MUL)
+    case RS_OP_EQ: return RS_SEG(RS_OP_EQ, 2);
+    case RS_OP_LT: return RS_SEG(RS_OP_LT, 2);
+    case RS_OP_CAT: return RS_SEG(RS_OP_CAT, 2);
+    case RS_OP_NOT: return RS_SEG(RS_OP_NOT, 1);
+    case RS_OP_SHL: return RS_SEG(RS_OP_SHL, 1);
+    case RS_OP_SHR: return RS_SEG(RS_OP_SHR, 1);
+    case RS_OP_BITS: return RS_SEG(RS_OP_BITS, 1);
+    case RS_OP_MUX: return RS_SEG(RS_OP_MUX, 3);
+    default: return RS_SEG(OP_COPY, 1);
+  }
+#undef RS_FOLD
+#undef RS_SEG
+}
+
+// Registers: tmp = LI[next] & M(w_r); LI[r] = tmp.  Hazard-free in one pass
+// because the compiler made every next row an op row (reading R8).
+template <int LT, bool HASH>
+__device__ __noinline__ uint64_t latch_range(uint8_t* p0, uint16_t* p1, uint32_t* p2, uint64_t* p3,
+                                             const uint32_t* __restrict__ next_coord,
+                                             const uint32_t* __restrict__ reg_coord,
+                                             const uint32_t* __restrict__ reg_w, const uint64_t* __restrict__ reg_k,
+                                             uint32_t b, uint32_t e) {
+  constexpr int U = 8;
+  const TileP<LT> t{p0, p1, p2, p3};
+  uint64_t h = 0;
+  for (uint32_t j = b; j < e; j += U) {
+    uint64_t v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (j + u < e) v[u] = t.ld(__ldg(next_coord + j + u));
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (j + u < e) {
+        const uint64_t x = v[u] & wmask(__ldg(reg_w + j + u));
+        t.stc(__ldg(reg_coord + j + u), x);
+        if constexpr (HASH) h += x * __ldg(reg_k + j + u);
+      }
+  }
+  return h;
+}
+
+template <int LT, bool HASH>
+__device__ __noinline__ uint64_t inject_range(uint8_t* p0, uint16_t* p1, uint32_t* p2, uint64_t* p3,
+                                              const uint32_t* __restrict__ in_coord,
+                                              const uint32_t* __restrict__ in_w, const uint64_t* __restrict__ in_k,
+                                              const uint64_t* __restrict__ stage, uint32_t n_inputs, uint32_t n_lanes,
+                                              uint64_t seed, uint64_t glane, uint64_t slot_or_cycle, int staged,
+                                              uint32_t lane, bool valid, uint32_t b, uint32_t e) {
+  const TileP<LT> t{p0, p1, p2, p3};
+  uint64_t h = 0;
+  for (uint32_t k = b; k < e; ++k) {
+    uint64_t v;
+    if (staged)
+      v = valid ? __ldg(stage + (slot_or_cycle * n_inputs + k) * n_lanes + lane) : 0ull;
+    else
+      v = d_stimulus(seed, k, slot_or_cycle, glane);
+    v &= wmask(__ldg(in_w + k));
+    t.stc(__ldg(in_coord + k), v);
+    if constexpr (HASH) h += v * __ldg(in_k + k);
+  }
+  return h;
+}
+
+__device__ __forceinline__ void chunk_of(uint32_t n, uint32_t part, uint32_t nparts, uint32_t& b, uint32_t& e) {
+  const uint32_t c = (n + nparts - 1) / nparts;
+  b = min(n, part * c);
+  e = min(n, b + c);
+}
+
+template <int LT, bool HASH>
+__device__ __forceinline__ void do_level_lanes(const StepArgs& a, const TileP<LT>& t, uint32_t lev,
+                                               uint32_t sub, uint32_t nsub, uint64_t& hacc) {
+  const uint32_t ob = __ldg(a.g.level_op_begin + lev), oe = __ldg(a.g.level_op_begin + lev + 1);
+  uint32_t b, e;
+  chunk_of(oe - ob, sub, nsub, b, e);
+  if (b >= e) return;
+  b += ob;
+  e += ob;
+  uint32_t lo = __ldg(a.g.level_run_begin + lev), hi = __ldg(a.g.level_run_begin + lev + 1) - 1;
+  while (lo < hi) {  // last run with op_begin <= b
+    const uint32_t mid = (lo + hi + 1) >> 1;
+    if (__ldg(&a.g.runs[mid].op_begin) <= b) lo = mid; else hi = mid - 1;
+  }
+  for (uint32_t r = lo; b < e; ++r) {
+    DevRun run;
+    run.op_begin = __ldg(&a.g.runs[r].op_begin);
+    run.count = __ldg(&a.g.runs[r].count);
+    run.coord_begin = __ldg(&a.g.runs[r].coord_begin);
+    run.out_row0 = __ldg(&a.g.runs[r].out_row0);
+    run.meta = __ldg(&a.g.runs[r].meta);
+    const uint32_t se = min(e, run.op_begin + run.count);
+    const SegCtx<LT> c{t, a.g.coord, a.g.opw, a.g.opk};
+    const uint64_t h = dispatch_run<LT, HASH>(c, run, b, se);
+    if constexpr (HASH) hacc += h;
+    b = se;
+  }
+}
+
+template <int LT, bool HASH>
+__global__ void __launch_bounds__(1024, 1) k_lanes(const StepArgs a) {
+  constexpr int LTL = (LT == 32) ? 5 : (LT == 16) ? 4 : (LT == 8) ? 3 : (LT == 4) ? 2 : (LT == 2) ? 1 : 0;
+  extern __shared__ uint64_t red[];  // [2][nsub][LT]
+  const uint32_t tile = blockIdx.x;
+  const uint32_t lin = threadIdx.x & (LT - 1);
+  const uint32_t sub = threadIdx.x >> LTL;
+  const uint32_t nsub = blockDim.x >> LTL;
+  const uint32_t lane = tile * LT + lin;
+  const bool valid = lane < a.n_lanes;
+  const TileP<LT> t = tile_ptrs<LT>(a, tile, lin);
+
+  uint32_t ib, ie, rb, re;
+  chunk_of(a.g.n_inputs, sub, nsub, ib, ie);
+  chunk_of(a.g.n_regs, sub, nsub, rb, re);
+
+  uint64_t hacc = 0;
+  if (HASH && sub == 0 && valid) hacc = a.hcarry_in[lane];
+  if (a.n_cycles == 0) return;
+  auto inject = [&](uint64_t cycle) -> uint64_t {
+    const uint64_t sc = a.staged ? cycle % a.stage_cap : cycle;
+    return inject_range<LT, HASH>(t.p0, t.p1, t.p2, t.p3, a.g.in_coord, a.g.in_w, a.g.in_k, a.stage,
+                                  a.g.n_inputs, a.n_lanes, a.seed, a.lane0 + lane, sc, a.staged, lane, valid, ib, ie);
+  };
+  hacc += inject(a.cycle0);
+  __syncthreads();
+  uint64_t hr = 0;
+  for (uint32_t cyc = 0; cyc < a.n_cycles; ++cyc) {
+    for (uint32_t lev = 0; lev < a.g.n_levels; ++lev) {
+      do_level_lanes<LT, HASH>(a, t, lev, sub, nsub, hacc);
+      __syncthreads();
+    }
+    hr = latch_range<LT, HASH>(t.p0, t.p1, t.p2, t.p3, a.g.reg_next_coord, a.g.reg_coord, a.g.reg_w, a.g.reg_k, rb, re);
+    uint64_t hin = 0;
+    if (cyc + 1 < a.n_cycles) hin = inject(a.cycle0 + cyc + 1);
+    if constexpr (HASH) red[((cyc & 1) * nsub + sub) * LT + lin] = hacc;
+    __syncthreads();
+    if constexpr (HASH) {
+      if (sub == 0 && a.hashes != nullptr) {
+        const uint64_t* rr = red + (cyc & 1) * nsub * LT + lin;
+        uint64_t s = a.g.const_hash;
+        for (uint32_t i = 0; i < nsub; ++i) s += rr[i * LT];
+        if (valid) a.hashes[(size_t)cyc * a.n_lanes + lane] = s;
+      }
+      hacc = hr + hin;
+    }
+  }
+  if constexpr (HASH) {
+    // register term of the hash for the next cycle
+    const uint32_t buf = a.n_cycles & 1u;
+    red[(buf * nsub + sub) * LT + lin] = hr;
+    __syncthreads();
+    if (sub == 0) {
+      const uint64_t* rr = red + buf * nsub * LT + lin;
+      uint64_t s = 0;
+      for (uint32_t i = 0; i < nsub; ++i) s += rr[i * LT];
+      if (valid) a.hcarry_out[lane] = s;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ single-lane mode
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned long long& target) {
+  __syncthreads();
+  if (gridDim.x == 1) return;
+  target += gridDim.x;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1ull);
+    while (ld_acquire(bar) < target) {
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ uint64_t block_sum(uint64_t v, uint64_t* sm) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const uint32_t w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0) sm[w] = v;
+  __syncthreads();
+  uint64_t s = 0;
+  if (threadIdx.x == 0)
+    for (uint32_t i = 0; i < nw; ++i) s += sm[i];
+  __syncthreads();
+  return s;
+}
+
+__device__ __forceinline__ uint64_t single_op(const StepArgs& a, const TileP<1>& t, uint32_t j) {
+  const uint32_t pw = __ldg(a.g.opw + j);
+  const uint32_t op = (pw >> 22) & 15u, n = pw >> 26;
+  const uint32_t* cp = a.g.coord + __ldg(a.g.coord_off + j);
+  uint64_t x[3];
+  switch (op) {
+    case RS_OP_AND: case RS_OP_OR: case RS_OP_XOR: case RS_OP_ADD: case RS_OP_SUB: case RS_OP_MUL: {
+      uint64_t r = t.ld_cg(__ldg(cp));
+      for (uint32_t o = 1; o < n; ++o) r = fold_step(op, r, t.ld_cg(__ldg(cp + o)));
+      return r & wmask(pw & 127u);
+    }
+    case RS_OP_EQ: x[0] = t.ld_cg(__ldg(cp)); x[1] = t.ld_cg(__ldg(cp + 1)); return apply_op<RS_OP_EQ, 2>(x, pw);
+    case RS_OP_LT: x[0] = t.ld_cg(__ldg(cp)); x[1] = t.ld_cg(__ldg(cp + 1)); return apply_op<RS_OP_LT, 2>(x, pw);
+    case RS_OP_CAT: x[0] = t.ld_cg(__ldg(cp)); x[1] = t.ld_cg(__ldg(cp + 1)); return apply_op<RS_OP_CAT, 2>(x, pw);
+    case RS_OP_NOT: x[0] = t.ld_cg(__ldg(cp)); return apply_op<RS_OP_NOT, 1>(x, pw);
+    case RS_OP_SHL: x[0] = t.ld_cg(__ldg(cp)); return apply_op<RS_OP_SHL, 1>(x, pw);
+    case RS_OP_SHR: x[0] = t.ld_cg(__ldg(cp)); return apply_op<RS_OP_SHR, 1>(x, pw);
+    case RS_OP_BITS: x[0] = t.ld_cg(__ldg(cp)); return apply_op<RS_OP_BITS, 1>(x, pw);
+    case RS_OP_MUX:
+      x[0] = t.ld_cg(__ldg(cp)); x[1] = t.ld_cg(__ldg(cp + 1)); x[2] = t.ld_cg(__ldg(cp + 2));
+      return apply_op<RS_OP_MUX, 3>(x, pw);
+    default: x[0] = t.ld_cg(__ldg(cp)); return apply_op<OP_COPY, 1>(x, pw);
+  }
+}
+
+template <bool HASH>
+__global__ void __launch_bounds__(1024, 1) k_single(const StepArgs a) {
+  __shared__ uint64_t sm[32];
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, T = gridDim.x * blockDim.x;
+  const TileP<1> t = tile_ptrs<1>(a, 0, 0);
+  unsigned long long target = 0;
+  uint64_t hacc = 0;
+  if (HASH && tid == 0) hacc = a.hcarry_in[0];
+  if (a.n_cycles == 0) return;
+  for (uint32_t k = tid; k < a.g.n_inputs; k += T) {
+    uint64_t v = a.staged ? __ldg(a.stage + (size_t)(a.cycle0 % a.stage_cap) * a.g.n_inputs + k)
+                          : d_stimulus(a.seed, k, a.cycle0, a.lane0);
+    v &= wmask(__ldg(a.g.in_w + k));
+    t.stc(__ldg(a.g.in_coord + k), v);
+    if (HASH) hacc += v * __ldg(a.g.in_k + k);
+  }
+  grid_barrier(a.bar, target);
+  uint64_t hr = 0;
+  for (uint32_t cyc = 0; cyc < a.n_cycles; ++cyc) {
+    for (uint32_t lev = 0; lev < a.g.n_levels; ++lev) {
+      const uint32_t ob = __ldg(a.g.level_op_begin + lev), oe = __ldg(a.g.level_op_begin + lev + 1);
+      for (uint32_t j = ob + tid; j < oe; j += T) {
+        const uint64_t y = single_op(a, t, j);
+        t.stc(__ldg(a.g.out_coord + j), y);
+        if (HASH) hacc += y * __ldg(a.g.opk + j);
+      }
+      grid_barrier(a.bar, target);
+    }
+    hr = 0;
+    for (uint32_t j = tid; j < a.g.n_regs; j += T) {
+      const uint64_t x = t.ld_cg(__ldg(a.g.reg_next_coord + j)) & wmask(__ldg(a.g.reg_w + j));
+      t.stc(__ldg(a.g.reg_coord + j), x);
+      if (HASH) hr += x * __ldg(a.g.reg_k + j);
+    }
+    uint64_t hin = 0;
+    if (cyc + 1 < a.n_cycles) {
+      const uint64_t c = a.cycle0 + cyc + 1;
+      for (uint32_t k = tid; k < a.g.n_inputs; k += T) {
+        uint64_t v = a.staged ? __ldg(a.stage + (size_t)(c % a.stage_cap) * a.g.n_inputs + k)
+                              : d_stimulus(a.seed, k, c, a.lane0);
+        v &= wmask(__ldg(a.g.in_w + k));
+        t.stc(__ldg(a.g.in_coord + k), v);
+        if (HASH) hin += v * __ldg(a.g.in_k + k);
+      }
+    }
+    if (HASH) {
+      const uint64_t s = block_sum(hacc, sm) + (blockIdx.x == 0 ? a.g.const_hash : 0ull);
+      if (threadIdx.x == 0 && a.hashes) atomicAdd((unsigned long long*)(a.hashes + cyc), (unsigned long long)s);
+      hacc = hr + hin;
+    }
+    grid_barrier(a.bar, target);
+  }
+  if (HASH) {
+    const uint64_t s = block_sum(hr, sm);
+    if (threadIdx.x == 0) atomicAdd((unsigned long long*)a.hcarry_out, (unsigned long long)s);
+  }
+}
+
+// ------------------------------------------------------------------ aux kernels
+// Fill every lane of the given rows with a value (constants, register init).
+__global__ void k_broadcast(StepArgs a, uint32_t LT, uint32_t n_tiles, const uint32_t* coords,
+                            const uint64_t* vals, uint32_t n) {
+  const uint64_t per = (uint64_t)n_tiles * LT;
+  for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < (uint64_t)n * per;
+       idx += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = (uint32_t)(idx / per);
+    const uint64_t rem = idx % per;
+    const uint32_t tile = (uint32_t)(rem / LT), lin = (uint32_t)(rem % LT);
+    const uint32_t c = coords[i], cls = c >> 30, row = c & ROW_MASK;
+    const size_t off = ((size_t)tile * a.rows[cls] + row) * LT + lin;
+    const uint64_t v = vals[i];
+    switch (cls) {
+      case 0: a.st[0][off] = (uint8_t)v; break;
+      case 1: reinterpret_cast<uint16_t*>(a.st[1])[off] = (uint16_t)v; break;
+      case 2: reinterpret_cast<uint32_t*>(a.st[2])[off] = (uint32_t)v; break;
+      default: reinterpret_cast<uint64_t*>(a.st[3])[off] = v; break;
+    }
+  }
+}
+
+__device__ __forceinline__ size_t state_off(const StepArgs& a, uint32_t LT, uint32_t c, uint32_t lane) {
+  const uint32_t cls = c >> 30, row = c & ROW_MASK;
+  return ((size_t)(lane / LT) * a.rows[cls] + row) * LT + (lane % LT);
+}
+
+__device__ __forceinline__ uint64_t state_ld(const StepArgs& a, uint32_t c, size_t off) {
+  switch (c >> 30) {
+    case 0: return a.st[0][off];
+    case 1: return reinterpret_cast<const uint16_t*>(a.st[1])[off];
+    case 2: return reinterpret_cast<const uint32_t*>(a.st[2])[off];
+    default: return reinterpret_cast<const uint64_t*>(a.st[3])[off];
+  }
+}
+
+__device__ __forceinline__ void state_st(const StepArgs& a, uint32_t c, size_t off, uint64_t v) {
+  switch (c >> 30) {
+    case 0: a.st[0][off] = (uint8_t)v; break;
+    case 1: reinterpret_cast<uint16_t*>(a.st[1])[off] = (uint16_t)v; break;
+    case 2: reinterpret_cast<uint32_t*>(a.st[2])[off] = (uint32_t)v; break;
+    default: reinterpret_cast<uint64_t*>(a.st[3])[off] = v; break;
+  }
+}
+
+// out[i][l] = value of coords[i] at lane lane_begin + l (rs_read_signals, step 5)
+__global__ void k_read(StepArgs a, uint32_t LT, const uint32_t* coords, uint32_t n_ids, uint32_t lane_begin,
+                       uint32_t n, uint64_t* out) {
+  for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < (uint64_t)n_ids * n;
+       idx += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = (uint32_t)(idx / n), l = (uint32_t)(idx % n);
+    const uint32_t c = coords[i];
+    out[idx] = state_ld(a, c, state_off(a, LT, c, lane_begin + l));
+  }
+}
+
+__global__ void k_write(StepArgs a, uint32_t LT, const uint32_t* coords, const uint32_t* widths, uint32_t n_ids,
+                        uint32_t lane_begin, uint32_t n, const uint64_t* vals) {
+  for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < (uint64_t)n_ids * n;
+       idx += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = (uint32_t)(idx / n), l = (uint32_t)(idx % n);
+    const uint32_t c = coords[i];
+    state_st(a, c, state_off(a, LT, c, lane_begin + l), vals[idx] & wmask(widths[i]));
+  }
+}
+
+// hcarry[l] = sum_r v_r * K_r (register term of the next cycle's hash)
+__global__ void k_reg_hash(StepArgs a, uint32_t LT, uint32_t n_lanes, uint64_t* hcarry) {
+  for (uint32_t l = blockIdx.x * blockDim.x + threadIdx.x; l < n_lanes; l += gridDim.x * blockDim.x) {
+    uint64_t h = 0;
+    for (uint32_t j = 0; j < a.g.n_regs; ++j) {
+      const uint32_t c = a.g.reg_coord[j];
+      h += state_ld(a, c, state_off(a, LT, c, l)) * a.g.reg_k[j];
+    }
+    hcarry[l] = h;
+  }
+}
+
+}  // namespace rtlsim

@@ -1,0 +1,636 @@
+// runtime.cu -- C ABI (include/rtlsim.h): device graph replicas, lane state,
+// staged-input ring, launches.  No host fallback: every simulated cycle runs
+// in the kernels of kernels.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/rtlsim.h"
+#include "compiler.hpp"
+#include "kernels.cuh"
+
+using namespace rtlsim;
+
+namespace {
+thread_local std::string g_err = "no error";
+
+rs_status set_err(rs_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define CU(call)                                                                                   \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess) {                                                                       \
+      return set_err(e_ == cudaErrorMemoryAllocation ? RS_E_OOM : RS_E_CUDA, "%s: %s (%s:%d)", #call, \
+                     cudaGetErrorString(e_), __FILE__, __LINE__);                                  \
+    }                                                                                              \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+};
+
+template <class T>
+size_t bytes_of(const std::vector<T>& v) { return v.size() * sizeof(T); }
+
+}  // namespace
+
+struct rs_graph {
+  int device = 0;
+  CompiledGraph cg;
+  void* dmem = nullptr;   // one allocation holding every device array
+  size_t dbytes = 0;
+  GraphDev gd{};
+  // device copies for read/write kernels
+  uint32_t* d_sig_coord = nullptr;
+  int sm_count = 148;
+  int live_lanes = 0;
+};
+
+struct rs_lanes {
+  rs_graph* g = nullptr;
+  uint32_t n_lanes = 0, LT = 1, n_tiles = 1, threads = 1024, ctas = 1;
+  uint64_t lane0 = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  uint8_t* st[4] = {nullptr, nullptr, nullptr, nullptr};
+  void* state_mem = nullptr;
+  size_t state_bytes = 0;
+  uint64_t* hcarry = nullptr;       // [2][n_lanes_pad]
+  int hc_cur = 0;
+  bool hc_valid = true;
+  uint64_t cycle = 0;
+  int staged = 0;
+  uint64_t seed = 0;
+  uint64_t* stage = nullptr;
+  uint32_t stage_cap = 0;
+  uint64_t st_lo = 0, st_hi = 0;    // staged window [st_lo, st_hi)
+  uint64_t* hbuf = nullptr;         // device hash temp for host outputs
+  size_t hbuf_cap = 0;
+  unsigned long long* bar = nullptr;
+  uint64_t launches = 0;
+  size_t total_bytes = 0;
+};
+
+namespace {
+
+StepArgs base_args(const rs_lanes* s) {
+  StepArgs a{};
+  a.g = s->g->gd;
+  for (int c = 0; c < 4; ++c) {
+    a.st[c] = s->st[c];
+    a.rows[c] = s->g->cg.rows[c];
+  }
+  a.n_lanes = s->n_lanes;
+  a.lane0 = s->lane0;
+  a.seed = s->seed;
+  a.staged = s->staged;
+  a.stage = s->stage;
+  a.stage_cap = s->stage_cap;
+  a.bar = s->bar;
+  return a;
+}
+
+rs_status set_device(const rs_graph* g) {
+  CU(cudaSetDevice(g->device));
+  return RS_OK;
+}
+
+template <class T>
+void put(std::vector<uint8_t>& blob, size_t& off, const std::vector<T>& v, size_t* where) {
+  off = (off + 255) & ~(size_t)255;
+  *where = off;
+  if (!v.empty()) {
+    if (blob.size() < off + bytes_of(v)) blob.resize(off + bytes_of(v));
+    std::memcpy(blob.data() + off, v.data(), bytes_of(v));
+  }
+  off += bytes_of(v);
+}
+
+int choose_lt(uint32_t n_lanes, int sms) {
+  for (int lt : {32, 16, 8}) {
+    const uint64_t tiles = (n_lanes + lt - 1) / lt;
+    if (tiles * 10 >= (uint64_t)sms * 8) return lt;   // >= 80% of the SMs busy
+  }
+  return 8;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rs_version(void) { return "rtlsim-b200 0.1 (sm_100a)"; }
+const char* rs_last_error(void) { return g_err.c_str(); }
+
+rs_status rs_load_graph(const rs_graph_desc* desc, int device, uint32_t mode, rs_graph** out) {
+  if (!desc || !out) return set_err(RS_E_INVALID_ARG, "NULL desc/out");
+  *out = nullptr;
+  if (device != RS_DEVICE_NONE) {
+    int ndev = 0;
+    CU(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return set_err(RS_E_INVALID_ARG, "device %d out of range (%d devices)", device, ndev);
+  }
+  rs_graph* g = new (std::nothrow) rs_graph();
+  if (!g) return set_err(RS_E_OOM, "host allocation failed");
+  g->device = device;
+  std::string err;
+  rs_status st = compile_graph(desc, mode, &g->cg, &err);
+  if (st != RS_OK) {
+    delete g;
+    return set_err(st, "%s", err.c_str());
+  }
+  CompiledGraph& cg = g->cg;
+  // out coords per op (single-lane mode and diagnostics)
+  std::vector<uint32_t> out_coord(cg.n_ops_total());
+  for (const DevRun& r : cg.runs)
+    for (uint32_t k = 0; k < r.count; ++k) out_coord[r.op_begin + k] = make_coord((r.meta >> 16) & 3u, r.out_row0 + k);
+  std::vector<uint8_t> blob;
+  size_t off = 0, o_runs, o_lrb, o_lob, o_opw, o_opk, o_coff, o_coord, o_outc, o_inc, o_inw, o_ink, o_rc, o_rn, o_rw,
+         o_rk, o_sig;
+  put(blob, off, cg.runs, &o_runs);
+  put(blob, off, cg.level_run_begin, &o_lrb);
+  put(blob, off, cg.level_op_begin, &o_lob);
+  put(blob, off, cg.opw, &o_opw);
+  put(blob, off, cg.opk, &o_opk);
+  put(blob, off, cg.coord_off, &o_coff);
+  put(blob, off, cg.coord, &o_coord);
+  put(blob, off, out_coord, &o_outc);
+  put(blob, off, cg.in_coord, &o_inc);
+  put(blob, off, cg.in_w, &o_inw);
+  put(blob, off, cg.in_k, &o_ink);
+  put(blob, off, cg.reg_coord, &o_rc);
+  put(blob, off, cg.reg_next_coord, &o_rn);
+  put(blob, off, cg.reg_w, &o_rw);
+  put(blob, off, cg.reg_k, &o_rk);
+  put(blob, off, cg.sig_coord, &o_sig);
+  blob.resize(std::max<size_t>(off, 256));
+  if (device == RS_DEVICE_NONE) {  // compile-only handle
+    g->dbytes = blob.size();
+    *out = g;
+    return RS_OK;
+  }
+  if ((st = set_device(g)) != RS_OK) { delete g; return st; }
+  cudaError_t e = cudaMalloc(&g->dmem, blob.size());
+  if (e != cudaSuccess) { delete g; return set_err(RS_E_OOM, "cudaMalloc graph (%zu B): %s", blob.size(), cudaGetErrorString(e)); }
+  g->dbytes = blob.size();
+  e = cudaMemcpy(g->dmem, blob.data(), blob.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) { cudaFree(g->dmem); delete g; return set_err(RS_E_CUDA, "graph H2D: %s", cudaGetErrorString(e)); }
+  auto P = [&](size_t o) { return (const void*)((const uint8_t*)g->dmem + o); };
+  GraphDev& d = g->gd;
+  d.runs = (const DevRun*)P(o_runs);
+  d.level_run_begin = (const uint32_t*)P(o_lrb);
+  d.level_op_begin = (const uint32_t*)P(o_lob);
+  d.opw = (const uint32_t*)P(o_opw);
+  d.opk = (const uint64_t*)P(o_opk);
+  d.coord_off = (const uint32_t*)P(o_coff);
+  d.coord = (const uint32_t*)P(o_coord);
+  d.out_coord = (const uint32_t*)P(o_outc);
+  d.in_coord = (const uint32_t*)P(o_inc);
+  d.in_w = (const uint32_t*)P(o_inw);
+  d.in_k = (const uint64_t*)P(o_ink);
+  d.reg_coord = (const uint32_t*)P(o_rc);
+  d.reg_next_coord = (const uint32_t*)P(o_rn);
+  d.reg_w = (const uint32_t*)P(o_rw);
+  d.reg_k = (const uint64_t*)P(o_rk);
+  d.n_levels = cg.n_levels;
+  d.n_inputs = cg.n_inputs;
+  d.n_regs = cg.n_regs;
+  d.n_ops_total = cg.n_ops_total();
+  d.const_hash = cg.const_hash;
+  g->d_sig_coord = (uint32_t*)P(o_sig);
+  cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, device);
+  *out = g;
+  return RS_OK;
+}
+
+rs_status rs_graph_info_get(const rs_graph* g, rs_graph_info* o) {
+  if (!g || !o) return set_err(RS_E_INVALID_ARG, "NULL graph/out");
+  const CompiledGraph& cg = g->cg;
+  std::memset(o, 0, sizeof *o);
+  o->mode = cg.mode;
+  o->n_levels = cg.n_levels;
+  o->n_ops = cg.n_ops;
+  o->n_copy_ops = cg.n_copy;
+  o->n_runs = (uint32_t)cg.runs.size();
+  o->n_coords = (uint32_t)cg.coord.size();
+  for (int c = 0; c < 4; ++c) o->rows[c] = cg.rows[c];
+  o->state_bytes_per_lane = cg.state_bytes_per_lane();
+  o->graph_device_bytes = g->dbytes;
+  o->graph_alg_bytes = cg.graph_alg_bytes;
+  o->alg_bytes_per_lane_cycle = cg.alg_bytes_per_lane_cycle;
+  o->identity_ops_naive = cg.identity_ops_naive;
+  return RS_OK;
+}
+
+rs_status rs_graph_export(const rs_graph* g, uint32_t what, void* out, uint64_t* count) {
+  if (!g || !count) return set_err(RS_E_INVALID_ARG, "NULL graph/count");
+  const CompiledGraph& cg = g->cg;
+  const void* src = nullptr;
+  size_t n = 0, esz = 4;
+  switch (what) {
+    case RS_EXPORT_RUNS: src = cg.runs.data(); n = cg.runs.size() * 5; break;
+    case RS_EXPORT_LEVEL_RUN_BEGIN: src = cg.level_run_begin.data(); n = cg.level_run_begin.size(); break;
+    case RS_EXPORT_LEVEL_OP_BEGIN: src = cg.level_op_begin.data(); n = cg.level_op_begin.size(); break;
+    case RS_EXPORT_OPW: src = cg.opw.data(); n = cg.opw.size(); break;
+    case RS_EXPORT_OPK: src = cg.opk.data(); n = cg.opk.size(); esz = 8; break;
+    case RS_EXPORT_COORD_OFF: src = cg.coord_off.data(); n = cg.coord_off.size(); break;
+    case RS_EXPORT_COORD: src = cg.coord.data(); n = cg.coord.size(); break;
+    case RS_EXPORT_SIG_COORD: src = cg.sig_coord.data(); n = cg.sig_coord.size(); break;
+    case RS_EXPORT_REG_COORD: src = cg.reg_coord.data(); n = cg.reg_coord.size(); break;
+    case RS_EXPORT_REG_NEXT_COORD: src = cg.reg_next_coord.data(); n = cg.reg_next_coord.size(); break;
+    case RS_EXPORT_IN_COORD: src = cg.in_coord.data(); n = cg.in_coord.size(); break;
+    default: return set_err(RS_E_INVALID_ARG, "unknown export %u", what);
+  }
+  *count = n;
+  if (out && n) std::memcpy(out, src, n * esz);
+  return RS_OK;
+}
+
+void rs_free_graph(rs_graph* g) {
+  if (!g) return;
+  if (g->dmem) {
+    cudaSetDevice(g->device);
+    cudaFree(g->dmem);
+  }
+  delete g;
+}
+
+rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts, rs_lanes** out) {
+  if (!g || !out) return set_err(RS_E_INVALID_ARG, "NULL graph/out");
+  *out = nullptr;
+  if (n_lanes == 0) return set_err(RS_E_INVALID_ARG, "n_lanes must be >= 1");
+  if (!g->dmem) return set_err(RS_E_STATE, "graph was loaded with RS_DEVICE_NONE (compile only)");
+  if (g->cg.mode == RS_MODE_SINGLE && n_lanes != 1)
+    return set_err(RS_E_INVALID_ARG, "RS_MODE_SINGLE simulates exactly one lane (got %u)", n_lanes);
+  rs_lane_opts o{};
+  if (opts) o = *opts;
+  rs_status st = set_device(g);
+  if (st != RS_OK) return st;
+  rs_lanes* s = new (std::nothrow) rs_lanes();
+  if (!s) return set_err(RS_E_OOM, "host allocation failed");
+  s->g = g;
+  s->n_lanes = n_lanes;
+  s->lane0 = o.lane0;
+  if (g->cg.mode == RS_MODE_SINGLE) {
+    s->LT = 1;
+    s->n_tiles = 1;
+  } else {
+    uint32_t lt = o.lane_tile ? o.lane_tile : (uint32_t)choose_lt(n_lanes, g->sm_count);
+    if (lt != 8 && lt != 16 && lt != 32) { delete s; return set_err(RS_E_INVALID_ARG, "lane_tile must be 8, 16 or 32"); }
+    s->LT = lt;
+    s->n_tiles = (n_lanes + lt - 1) / lt;
+  }
+  // launch shape
+  if (o.threads) {
+    if (o.threads % 32 || o.threads > 1024 || o.threads < s->LT) { delete s; return set_err(RS_E_INVALID_ARG, "threads must be a multiple of 32 in [32, 1024]"); }
+    s->threads = o.threads;
+  } else if (g->cg.mode == RS_MODE_SINGLE) {
+    s->threads = 1024;
+  } else {
+    const uint32_t per_sm = (s->n_tiles + g->sm_count - 1) / g->sm_count;
+    uint32_t th = 1024 / std::max<uint32_t>(1, per_sm);
+    th = std::max<uint32_t>(64, th & ~31u);
+    s->threads = th;
+  }
+  if (g->cg.mode == RS_MODE_SINGLE) {
+    const uint32_t work = std::max<uint32_t>(1, std::max(g->cg.n_inputs, g->cg.n_regs));
+    uint32_t maxops = 0;
+    for (uint32_t l = 0; l < g->cg.n_levels; ++l)
+      maxops = std::max(maxops, g->cg.level_op_begin[l + 1] - g->cg.level_op_begin[l]);
+    const uint32_t need = std::max(work, maxops);
+    uint32_t ctas = (need + s->threads - 1) / s->threads;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_single<true>, s->threads, 0);
+    const uint32_t maxc = (uint32_t)std::max(1, occ) * g->sm_count;
+    s->ctas = std::max<uint32_t>(1, std::min(ctas, maxc));
+  } else {
+    s->ctas = s->n_tiles;
+  }
+  // state: per class [n_tiles][rows][LT]
+  size_t off = 0, offs[4];
+  for (int c = 0; c < 4; ++c) {
+    off = (off + 255) & ~(size_t)255;
+    offs[c] = off;
+    off += (size_t)s->n_tiles * g->cg.rows[c] * s->LT * (1u << c);
+  }
+  s->state_bytes = std::max<size_t>(off, 256);
+  cudaError_t e;
+  if ((e = cudaMalloc(&s->state_mem, s->state_bytes)) != cudaSuccess) {
+    delete s;
+    return set_err(RS_E_OOM, "cudaMalloc state (%zu B): %s", (size_t)off, cudaGetErrorString(e));
+  }
+  for (int c = 0; c < 4; ++c) s->st[c] = (uint8_t*)s->state_mem + offs[c];
+  const size_t lanes_pad = (size_t)s->n_tiles * s->LT;
+  if ((e = cudaMalloc(&s->hcarry, 2 * lanes_pad * sizeof(uint64_t))) != cudaSuccess ||
+      (e = cudaMalloc(&s->bar, 256)) != cudaSuccess) {
+    rs_free_lanes(s);
+    return set_err(RS_E_OOM, "cudaMalloc: %s", cudaGetErrorString(e));
+  }
+  if (o.stage_cycles) {
+    const size_t sb = (size_t)o.stage_cycles * std::max<uint32_t>(1, g->cg.n_inputs) * n_lanes * sizeof(uint64_t);
+    if ((e = cudaMalloc(&s->stage, sb)) != cudaSuccess) {
+      rs_free_lanes(s);
+      return set_err(RS_E_OOM, "cudaMalloc stage ring (%zu B): %s", sb, cudaGetErrorString(e));
+    }
+    s->stage_cap = o.stage_cycles;
+  }
+  s->total_bytes = s->state_bytes + 2 * lanes_pad * 8 + 256 +
+                   (size_t)s->stage_cap * std::max<uint32_t>(1, g->cg.n_inputs) * n_lanes * 8;
+  if (o.stream) {
+    s->stream = (cudaStream_t)o.stream;
+  } else {
+    if ((e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking)) != cudaSuccess) {
+      rs_free_lanes(s);
+      return set_err(RS_E_CUDA, "stream: %s", cudaGetErrorString(e));
+    }
+    s->own_stream = true;
+  }
+  // init: zero, constants, register init, hash carry
+  StepArgs a = base_args(s);
+  e = cudaMemsetAsync(s->state_mem, 0, s->state_bytes, s->stream);
+  std::vector<uint32_t> coords;
+  std::vector<uint64_t> vals;
+  coords.insert(coords.end(), g->cg.const_coord.begin(), g->cg.const_coord.end());
+  vals.insert(vals.end(), g->cg.const_val.begin(), g->cg.const_val.end());
+  coords.insert(coords.end(), g->cg.reg_coord.begin(), g->cg.reg_coord.end());
+  vals.insert(vals.end(), g->cg.reg_init.begin(), g->cg.reg_init.end());
+  if (e == cudaSuccess && !coords.empty()) {
+    void* tmp = nullptr;
+    const size_t nb = coords.size() * 4, vb = vals.size() * 8;
+    e = cudaMalloc(&tmp, nb + vb + 8);
+    if (e == cudaSuccess) {
+      cudaMemcpyAsync(tmp, coords.data(), nb, cudaMemcpyHostToDevice, s->stream);
+      uint64_t* dv = (uint64_t*)((uint8_t*)tmp + ((nb + 7) & ~(size_t)7));
+      cudaMemcpyAsync(dv, vals.data(), vb, cudaMemcpyHostToDevice, s->stream);
+      k_broadcast<<<std::min<uint64_t>(4096, (coords.size() * lanes_pad + 255) / 256), 256, 0, s->stream>>>(
+          a, s->LT, s->n_tiles, (const uint32_t*)tmp, dv, (uint32_t)coords.size());
+      e = cudaStreamSynchronize(s->stream);
+      cudaFree(tmp);
+      s->launches++;
+    }
+  }
+  if (e == cudaSuccess) {
+    std::vector<uint64_t> hc(lanes_pad, g->cg.init_reg_hash);
+    e = cudaMemcpy(s->hcarry, hc.data(), lanes_pad * 8, cudaMemcpyHostToDevice);
+  }
+  if (e != cudaSuccess) {
+    rs_free_lanes(s);
+    return set_err(RS_E_CUDA, "state init: %s", cudaGetErrorString(e));
+  }
+  g->live_lanes++;
+  *out = s;
+  return RS_OK;
+}
+
+void rs_free_lanes(rs_lanes* s) {
+  if (!s) return;
+  cudaSetDevice(s->g->device);
+  if (s->stream) cudaStreamSynchronize(s->stream);
+  if (s->state_mem) cudaFree(s->state_mem);
+  if (s->hcarry) cudaFree(s->hcarry);
+  if (s->bar) cudaFree(s->bar);
+  if (s->stage) cudaFree(s->stage);
+  if (s->hbuf) cudaFree(s->hbuf);
+  if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
+  if (s->g) s->g->live_lanes--;
+  delete s;
+}
+
+uint64_t rs_lanes_bytes(const rs_lanes* s) { return s ? s->total_bytes : 0; }
+
+rs_status rs_set_input_seed(rs_lanes* s, uint64_t seed) {
+  if (!s) return set_err(RS_E_INVALID_ARG, "NULL lanes");
+  s->seed = seed;
+  s->staged = 0;
+  return RS_OK;
+}
+
+rs_status rs_set_inputs(rs_lanes* s, uint64_t first_cycle, uint32_t n_cycles, const uint64_t* values, int on_device) {
+  if (!s) return set_err(RS_E_INVALID_ARG, "NULL lanes");
+  if (!s->stage_cap) return set_err(RS_E_STATE, "no staged-input ring (rs_lane_opts.stage_cycles = 0)");
+  if (n_cycles > s->stage_cap) return set_err(RS_E_RANGE, "n_cycles %u > stage_cycles %u", n_cycles, s->stage_cap);
+  if (n_cycles && !values) return set_err(RS_E_INVALID_ARG, "NULL values");
+  rs_status st = set_device(s->g);
+  if (st != RS_OK) return st;
+  const uint32_t NI = s->g->cg.n_inputs;
+  const size_t per = (size_t)NI * s->n_lanes;
+  const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  uint32_t done = 0;
+  while (done < n_cycles && per) {
+    const uint64_t c = first_cycle + done;
+    const uint32_t slot = (uint32_t)(c % s->stage_cap);
+    const uint32_t n = std::min<uint32_t>(n_cycles - done, s->stage_cap - slot);
+    CU(cudaMemcpyAsync(s->stage + (size_t)slot * per, values + (size_t)done * per, (size_t)n * per * 8, kind, s->stream));
+    done += n;
+  }
+  // staged window
+  if (s->staged && first_cycle <= s->st_hi && first_cycle >= s->st_lo) {
+    s->st_hi = std::max<uint64_t>(s->st_hi, first_cycle + n_cycles);
+  } else {
+    s->st_lo = first_cycle;
+    s->st_hi = first_cycle + n_cycles;
+  }
+  if (s->st_hi - s->st_lo > s->stage_cap) s->st_lo = s->st_hi - s->stage_cap;
+  s->staged = 1;
+  return RS_OK;
+}
+
+static rs_status refresh_hcarry(rs_lanes* s) {
+  if (s->hc_valid) return RS_OK;
+  StepArgs a = base_args(s);
+  k_reg_hash<<<std::max<uint32_t>(1, (s->n_lanes + 127) / 128), 128, 0, s->stream>>>(a, s->LT, s->n_lanes,
+                                                                                     s->hcarry + s->hc_cur * (size_t)s->n_tiles * s->LT);
+  s->launches++;
+  CU(cudaGetLastError());
+  s->hc_valid = true;
+  return RS_OK;
+}
+
+rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int hashes_mem) {
+  if (!s) return set_err(RS_E_INVALID_ARG, "NULL lanes");
+  if (hashes_mem != RS_MEM_NONE && hashes_mem != RS_MEM_HOST && hashes_mem != RS_MEM_DEVICE)
+    return set_err(RS_E_INVALID_ARG, "bad hashes_mem %d", hashes_mem);
+  if (hashes_mem != RS_MEM_NONE && !hashes && n_cycles) return set_err(RS_E_INVALID_ARG, "NULL hashes");
+  if (n_cycles == 0) return RS_OK;
+  if (s->staged && (s->cycle < s->st_lo || s->cycle + n_cycles > s->st_hi))
+    return set_err(RS_E_STATE, "cycles [%llu, %llu) are not staged (window [%llu, %llu))",
+                   (unsigned long long)s->cycle, (unsigned long long)(s->cycle + n_cycles),
+                   (unsigned long long)s->st_lo, (unsigned long long)s->st_hi);
+  rs_status st = set_device(s->g);
+  if (st != RS_OK) return st;
+  const bool hash = hashes_mem != RS_MEM_NONE;
+  if (hash && (st = refresh_hcarry(s)) != RS_OK) return st;
+  uint64_t* hout = nullptr;
+  const size_t hn = (size_t)n_cycles * s->n_lanes;
+  if (hashes_mem == RS_MEM_DEVICE) {
+    hout = hashes;
+  } else if (hashes_mem == RS_MEM_HOST) {
+    if (s->hbuf_cap < hn) {
+      if (s->hbuf) cudaFree(s->hbuf);
+      s->hbuf = nullptr;
+      s->hbuf_cap = 0;
+      CU(cudaMalloc(&s->hbuf, hn * 8));
+      s->hbuf_cap = hn;
+    }
+    hout = s->hbuf;
+  }
+  StepArgs a = base_args(s);
+  a.cycle0 = s->cycle;
+  a.n_cycles = n_cycles;
+  a.hashes = hout;
+  const size_t lanes_pad = (size_t)s->n_tiles * s->LT;
+  a.hcarry_in = s->hcarry + s->hc_cur * lanes_pad;
+  if (s->g->cg.mode == RS_MODE_SINGLE) {
+    a.hcarry_out = s->hcarry + (1 - s->hc_cur) * lanes_pad;
+    if (hash) {
+      CU(cudaMemsetAsync(a.hcarry_out, 0, 8, s->stream));
+      if (hout) CU(cudaMemsetAsync(hout, 0, hn * 8, s->stream));
+    }
+    CU(cudaMemsetAsync(s->bar, 0, 8, s->stream));
+    void* args[] = {&a};
+    cudaError_t e = hash ? cudaLaunchCooperativeKernel((const void*)k_single<true>, s->ctas, s->threads, args, 0, s->stream)
+                         : cudaLaunchCooperativeKernel((const void*)k_single<false>, s->ctas, s->threads, args, 0, s->stream);
+    if (e != cudaSuccess) return set_err(RS_E_CUDA, "k_single launch: %s", cudaGetErrorString(e));
+    if (hash) s->hc_cur = 1 - s->hc_cur;
+  } else {
+    a.hcarry_out = a.hcarry_in;
+    const uint32_t nsub = s->threads / s->LT;
+    const size_t smem = hash ? 2ull * nsub * s->LT * 8 : 0;
+    const dim3 grid(s->n_tiles), block(s->threads);
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(k_lanes<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      cudaFuncSetAttribute(k_lanes<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      cudaFuncSetAttribute(k_lanes<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      attr_set = true;
+    }
+    switch (s->LT * 2 + (hash ? 1 : 0)) {
+      case 65: k_lanes<32, true><<<grid, block, smem, s->stream>>>(a); break;
+      case 64: k_lanes<32, false><<<grid, block, smem, s->stream>>>(a); break;
+      case 33: k_lanes<16, true><<<grid, block, smem, s->stream>>>(a); break;
+      case 32: k_lanes<16, false><<<grid, block, smem, s->stream>>>(a); break;
+      case 17: k_lanes<8, true><<<grid, block, smem, s->stream>>>(a); break;
+      default: k_lanes<8, false><<<grid, block, smem, s->stream>>>(a); break;
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_err(RS_E_CUDA, "k_lanes launch: %s", cudaGetErrorString(e));
+  }
+  s->launches++;
+  if (!hash) s->hc_valid = false;
+  s->cycle += n_cycles;
+  if (hashes_mem == RS_MEM_HOST) {
+    CU(cudaMemcpyAsync(hashes, hout, hn * 8, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaStreamSynchronize(s->stream));
+  }
+  return RS_OK;
+}
+
+rs_status rs_read_signals(rs_lanes* s, const uint32_t* ids, uint32_t n_ids, uint32_t lane_begin, uint32_t n_lanes,
+                          uint64_t* out) {
+  if (!s || (n_ids && (!ids || !out))) return set_err(RS_E_INVALID_ARG, "NULL argument");
+  if ((uint64_t)lane_begin + n_lanes > s->n_lanes) return set_err(RS_E_RANGE, "lanes [%u, %u) out of range (%u lanes)", lane_begin, lane_begin + n_lanes, s->n_lanes);
+  if (n_ids == 0 || n_lanes == 0) return RS_OK;
+  std::vector<uint32_t> coords(n_ids);
+  for (uint32_t i = 0; i < n_ids; ++i) {
+    if (ids[i] >= s->g->cg.n_signals) return set_err(RS_E_RANGE, "signal id %u out of range", ids[i]);
+    coords[i] = s->g->cg.sig_coord[ids[i]];
+  }
+  rs_status st = set_device(s->g);
+  if (st != RS_OK) return st;
+  const size_t n = (size_t)n_ids * n_lanes;
+  void* tmp = nullptr;
+  CU(cudaMalloc(&tmp, n * 8 + n_ids * 4 + 8));
+  uint64_t* dout = (uint64_t*)tmp;
+  uint32_t* dco = (uint32_t*)(dout + n);
+  cudaError_t e = cudaMemcpyAsync(dco, coords.data(), n_ids * 4, cudaMemcpyHostToDevice, s->stream);
+  if (e == cudaSuccess) {
+    StepArgs a = base_args(s);
+    k_read<<<(unsigned)std::min<size_t>(8192, (n + 255) / 256), 256, 0, s->stream>>>(a, s->LT, dco, n_ids, lane_begin, n_lanes, dout);
+    s->launches++;
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, dout, n * 8, cudaMemcpyDeviceToHost, s->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+  cudaFree(tmp);
+  if (e != cudaSuccess) return set_err(RS_E_CUDA, "read_signals: %s", cudaGetErrorString(e));
+  return RS_OK;
+}
+
+rs_status rs_write_registers(rs_lanes* s, const uint32_t* reg_ids, uint32_t n, uint32_t lane_begin, uint32_t n_lanes,
+                             const uint64_t* values) {
+  if (!s || (n && (!reg_ids || !values))) return set_err(RS_E_INVALID_ARG, "NULL argument");
+  if ((uint64_t)lane_begin + n_lanes > s->n_lanes) return set_err(RS_E_RANGE, "lanes out of range");
+  if (n == 0 || n_lanes == 0) return RS_OK;
+  std::vector<uint32_t> cw(2 * (size_t)n);
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t id = reg_ids[i];
+    if (id >= s->g->cg.n_signals || s->g->cg.sig_kind[id] != 1) return set_err(RS_E_RANGE, "signal %u is not a register", id);
+    cw[i] = s->g->cg.sig_coord[id];
+    cw[n + i] = s->g->cg.reg_w[s->g->cg.sig_reg_index[id]];
+  }
+  rs_status st = set_device(s->g);
+  if (st != RS_OK) return st;
+  const size_t nv = (size_t)n * n_lanes;
+  void* tmp = nullptr;
+  CU(cudaMalloc(&tmp, nv * 8 + cw.size() * 4 + 8));
+  uint64_t* dv = (uint64_t*)tmp;
+  uint32_t* dc = (uint32_t*)(dv + nv);
+  cudaError_t e = cudaMemcpyAsync(dv, values, nv * 8, cudaMemcpyHostToDevice, s->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dc, cw.data(), cw.size() * 4, cudaMemcpyHostToDevice, s->stream);
+  if (e == cudaSuccess) {
+    StepArgs a = base_args(s);
+    k_write<<<(unsigned)std::min<size_t>(8192, (nv + 255) / 256), 256, 0, s->stream>>>(a, s->LT, dc, dc + n, n, lane_begin, n_lanes, dv);
+    s->launches++;
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+  cudaFree(tmp);
+  if (e != cudaSuccess) return set_err(RS_E_CUDA, "write_registers: %s", cudaGetErrorString(e));
+  s->hc_valid = false;
+  return refresh_hcarry(s);
+}
+
+rs_status rs_get_cycle(const rs_lanes* s, uint64_t* cycle) {
+  if (!s || !cycle) return set_err(RS_E_INVALID_ARG, "NULL argument");
+  *cycle = s->cycle;
+  return RS_OK;
+}
+
+rs_status rs_set_cycle(rs_lanes* s, uint64_t cycle) {
+  if (!s) return set_err(RS_E_INVALID_ARG, "NULL lanes");
+  s->cycle = cycle;
+  return RS_OK;
+}
+
+uint64_t rs_launch_count(const rs_lanes* s) { return s ? s->launches : 0; }
+
+rs_status rs_launch_shape(const rs_lanes* s, uint32_t* lt, uint32_t* threads, uint32_t* ctas) {
+  if (!s) return set_err(RS_E_INVALID_ARG, "NULL lanes");
+  if (lt) *lt = s->LT;
+  if (threads) *threads = s->threads;
+  if (ctas) *ctas = s->ctas;
+  return RS_OK;
+}
+
+rs_status rs_sync(rs_lanes* s) {
+  if (!s) return set_err(RS_E_INVALID_ARG, "NULL lanes");
+  rs_status st = set_device(s->g);
+  if (st != RS_OK) return st;
+  CU(cudaStreamSynchronize(s->stream));
+  return RS_OK;
+}
+
+}  // extern "C"

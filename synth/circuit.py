@@ -85,7 +85,7 @@ class Circuit:
     def normalized(self) -> "Circuit":
         """Return a copy with contiguous arrays of the interchange dtypes."""
         def a(x, dt):
-            return np.ascontiguousarray(np.asarray(x, dtype=dt))
+            return np.array(x, dtype=dt, copy=True, order="C")
         return Circuit(
             width=a(self.width, np.uint8), input_id=a(self.input_id, np.uint32),
             reg_id=a(self.reg_id, np.uint32), reg_next_id=a(self.reg_next_id, np.uint32),

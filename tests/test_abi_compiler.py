@@ -1,0 +1,220 @@
+"""CPU tests of the product library: every symbol include/rtlsim.h declares is
+exported; graph validation statuses; the compiled format (RS_DEVICE_NONE,
+compile only -- nothing is simulated here) decodes back to the input circuit.
+"""
+import os
+import re
+from collections import Counter
+
+import numpy as np
+import pytest
+
+from synth import Builder, config_circuit, fuzz_circuit
+from synth.circuit import MUX
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "rtlsim.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(rs_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol(rs):
+    L = rs.lib()
+    syms = header_symbols()
+    assert len(syms) >= 18
+    for s in syms:
+        assert hasattr(L, s), s
+    assert set(syms) == set(rs.EXPORTS)
+    assert b"sm_100a" in L.rs_version()
+
+
+def test_no_cuda_is_an_error_not_a_fallback(rs):
+    """Without a GPU, loading onto a device fails with a status (no host path)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    c, _ = __import__("synth.closed_form", fromlist=["x"]).counter(8)
+    with pytest.raises(rs.RtlSimError) as e:
+        rs.Graph(c, device=0)
+    assert e.value.name in ("RS_E_CUDA", "RS_E_INVALID_ARG")
+
+
+def _graph(rs, c, mode="lanes"):
+    return rs.Graph(c, device=rs.RS_DEVICE_NONE, mode=mode)
+
+
+def test_compile_only_cannot_allocate(rs):
+    c, _ = __import__("synth.closed_form", fromlist=["x"]).counter(8)
+    g = _graph(rs, c)
+    with pytest.raises(rs.RtlSimError) as e:
+        rs.Lanes(g, 4)
+    assert e.value.name == "RS_E_STATE"
+
+
+def test_validation_statuses(rs):
+    b = Builder()
+    x = b.input(8)
+    y = b.op("add", [x, x], 8)
+    good = b.build()
+    _graph(rs, good)
+
+    def bad(mut, status):
+        c = good.normalized()
+        mut(c)
+        with pytest.raises(rs.RtlSimError) as e:
+            _graph(rs, c)
+        assert e.value.name == status, (e.value, status)
+
+    bad(lambda c: c.arg_id.__setitem__(0, y), "RS_E_GRAPH")                 # comb. loop
+    bad(lambda c: c.out_id.__setitem__(0, x), "RS_E_GRAPH")                 # two drivers
+    bad(lambda c: c.width.__setitem__(1, 0), "RS_E_GRAPH")                  # width 0
+    bad(lambda c: c.width.__setitem__(1, 65), "RS_E_GRAPH")                 # width 65
+    bad(lambda c: c.opcode.__setitem__(0, 3), "RS_E_GRAPH")                 # not with 2 args
+    bad(lambda c: c.opcode.__setitem__(0, 99), "RS_E_GRAPH")                # unknown opcode
+    bad(lambda c: c.arg_id.__setitem__(1, 77), "RS_E_GRAPH")                # id out of range
+    b2 = Builder()
+    z = b2.input(8)
+    b2.op("bits", [z], 4, 70, 0)
+    with pytest.raises(rs.RtlSimError):
+        _graph(rs, b2.build())                                              # bits hi > 63
+    b3 = Builder()
+    z = b3.input(8)
+    b3.width.append(8)                                                      # undriven signal
+    b3.op("add", [z, z], 8)
+    with pytest.raises(rs.RtlSimError) as e:
+        _graph(rs, b3.build())
+    assert e.value.name == "RS_E_GRAPH"
+    c = good.normalized()                                                   # bad explicit level
+    c.level = np.array([0], dtype=np.uint32)
+    _graph(rs, c)
+    b4 = Builder()
+    z = b4.input(8)
+    a = b4.op("not", [z], 8)
+    b4.op("not", [a], 8)
+    c4 = b4.build()
+    c4.level = np.array([1, 1], dtype=np.uint32)
+    with pytest.raises(rs.RtlSimError) as e:
+        _graph(rs, c4)
+    assert e.value.name == "RS_E_GRAPH"
+
+
+def decode(rs, c, g):
+    """Decode the compiled format back to (level, opcode, out id, operand ids, params)."""
+    runs = g.export("runs")
+    lrb = g.export("level_run_begin")
+    lob = g.export("level_op_begin")
+    opw = g.export("opw")
+    coff = g.export("coord_off")
+    coord = g.export("coord")
+    sigc = g.export("sig_coord")
+    n_sig = c.n_signals
+    by_coord = {int(v): s for s, v in enumerate(sigc)}
+    assert len(by_coord) == n_sig, "coords must be unique per signal"
+    ops = []
+    levels_of = {}
+    for lev in range(len(lrb) - 1):
+        assert lob[lev] <= lob[lev + 1]
+        for r in range(lrb[lev], lrb[lev + 1]):
+            ob, cnt, cb, row0, meta = (int(v) for v in runs[r])
+            opc, ar, cls = meta & 0xFF, (meta >> 8) & 0xFF, (meta >> 16) & 3
+            assert lob[lev] <= ob and ob + cnt <= lob[lev + 1]
+            assert cb == coff[ob]
+            for k in range(cnt):
+                j = ob + k
+                pw = int(opw[j])
+                assert pw & 127 >= 1 and (pw >> 20) & 3 == cls and (pw >> 22) & 15 == opc and pw >> 26 == ar
+                out_c = (cls << 30) | (row0 + k)                       # implicit S coordinate
+                args_c = [int(x) for x in coord[coff[j]:coff[j + 1]]]
+                assert len(args_c) == ar
+                out = by_coord.get(out_c, ("copy", out_c))
+                args = [by_coord.get(a, ("copy", a)) for a in args_c]
+                ops.append((lev, opc, out, tuple(args), pw))
+                levels_of[out_c] = lev
+    return ops, levels_of, by_coord
+
+
+@pytest.mark.parametrize("which", ["C1", "C2", "fuzz3", "fuzz8", "fuzz11", "paper"])
+def test_format_decodes_to_input_graph(rs, which):
+    """SURVEY §4.3 layer 4: the decoded graph tensor equals the input graph as a
+    multiset of (opcode, out, operands in O order, params); every op reads only
+    signals produced at a lower level; runs are grouped by (opcode, arity,
+    width class); zero identity entries except register->source copies."""
+    from synth import closed_form as cf
+    if which == "paper":
+        c, _ = cf.paper_example()
+    elif which.startswith("fuzz"):
+        c = fuzz_circuit(int(which[4:]))
+    else:
+        c = config_circuit(which)
+    g = _graph(rs, c)
+    info = g.info()
+    ops, levels_of, by_coord = decode(rs, c, g)
+    canon = [o for o in ops if not isinstance(o[2], tuple)]
+    copies = [o for o in ops if isinstance(o[2], tuple)]
+    assert len(canon) == c.n_ops and len(copies) == info["n_copy_ops"]
+    want = Counter()
+    for j in range(c.n_ops):
+        opc = int(c.opcode[j])
+        want[(opc, int(c.out_id[j]), tuple(c.op_args(j)))] += 1
+    got = Counter((o[1], o[2], o[3]) for o in canon)
+    assert got == want
+    # params survive: w_out and shift / bits / cat parameters
+    pmap = {o[2]: o[4] for o in canon}
+    for j in range(c.n_ops):
+        pw = pmap[int(c.out_id[j])]
+        assert pw & 127 == int(c.width[c.out_id[j]])
+        opc = int(c.opcode[j])
+        if opc in (9, 10):
+            assert (pw >> 7) & 127 == min(int(c.param[j, 0]), 64)
+        if opc == 11:
+            assert ((pw >> 7) & 127, (pw >> 14) & 63) == (int(c.param[j, 0]), int(c.param[j, 1]))
+        if opc == 12:
+            assert (pw >> 7) & 127 == int(c.width[c.op_args(j)[1]])
+    # levels: operands come from strictly lower levels (or sources)
+    sig_coord = g.export("sig_coord")
+    for (lev, _, out, args, _) in ops:
+        for a in args:
+            if isinstance(a, tuple):
+                continue
+            ac = int(sig_coord[a])
+            if ac in levels_of:
+                assert levels_of[ac] < lev
+    # copies only for register next edges that point at inputs / registers
+    srcs = set(int(x) for x in c.input_id) | set(int(x) for x in c.reg_id)
+    need = set(int(n) for n in c.reg_next_id if int(n) in srcs)
+    assert len(copies) == len(need)
+    rnc = g.export("reg_next_coord")
+    assert all(int(x) in levels_of for x in rnc) or c.n_consts > 0
+
+
+def test_format_runs_sorted_and_stats(rs):
+    c = config_circuit("C3", n_ops=30000, n_levels=20, n_regs=3000)
+    g = _graph(rs, c)
+    info = g.info()
+    runs = g.export("runs")
+    lrb = g.export("level_run_begin")
+    assert info["n_levels"] == 20 and info["n_runs"] == runs.shape[0]
+    for lev in range(20):
+        keys = [(int(m) & 0xFF, (int(m) >> 8) & 0xFF, (int(m) >> 16) & 3) for m in runs[lrb[lev]:lrb[lev + 1], 4]]
+        assert keys == sorted(keys) and len(set(keys)) == len(keys)
+    # B_alg per lane-cycle equals the SURVEY §8(d) formula recomputed here
+    cls_b = lambda w: 1 if w <= 8 else 2 if w <= 16 else 4 if w <= 32 else 8
+    W = [cls_b(int(w)) for w in c.width]
+    B = sum(W[a] for a in c.arg_id) + sum(W[o] for o in c.out_id)
+    B += sum(W[r] + W[n] for r, n in zip(c.reg_id, c.reg_next_id)) + sum(W[i] for i in c.input_id)
+    assert info["alg_bytes_per_lane_cycle"] == B
+    assert info["graph_alg_bytes"] == 4 * len(c.arg_id) + 4 * c.n_ops
+    assert info["state_bytes_per_lane"] == sum(W)
+    assert info["identity_ops_naive"] > 0
+
+
+def test_identity_copy_for_register_chains(rs):
+    from synth import closed_form as cf
+    c, x, rs_ = cf.shift_register(5, 8)
+    g = _graph(rs, c)
+    assert g.info()["n_copy_ops"] == 5            # next(r0) = input, next(r_k) = register
+    c2, _, _ = cf.swap(8, 1, 2)
+    assert _graph(rs, c2).info()["n_copy_ops"] == 2

@@ -1,0 +1,273 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, bit-exact.
+
+Per-cycle, per-lane signal hashes (reading R12) plus full signal state via
+rs_read_signals.  Integer work: the bar is bit equality everywhere.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from synth import CONFIGS, closed_form as cf, config_circuit, fuzz_circuit
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def run_gpu(rs, c, n_cycles, n_lanes=1, seed=0, mode="lanes", lane0=0, lane_tile=0, threads=0,
+            staged=None, chunks=None, final=True):
+    g = rs.Graph(c, device=0, mode=mode)
+    L = rs.Lanes(g, n_lanes, lane0=lane0, lane_tile=lane_tile, threads=threads,
+                 stage_cycles=(n_cycles if staged is not None else 0))
+    if staged is not None:
+        L.set_inputs(0, staged)
+    else:
+        L.set_seed(seed)
+    hs = []
+    for n in (chunks or [n_cycles]):
+        hs.append(L.step(n, hashes="host"))
+    H = np.concatenate(hs) if hs else np.zeros((0, n_lanes), np.uint64)
+    F = L.read(list(range(c.n_signals))) if final else None
+    return H, F, L
+
+
+def check(rs, c, n_cycles, n_lanes=1, seed=0, mode="lanes", **kw):
+    H, F, L = run_gpu(rs, c, n_cycles, n_lanes, seed, mode, **kw)
+    lane0 = kw.get("lane0", 0)
+    staged = kw.get("staged")
+    r = oracle.simulate(c, n_cycles, seed=seed, lane0=lane0, n_lanes=n_lanes, staged=staged,
+                        final=True, threads=8)
+    if not np.array_equal(H, r.hashes):
+        bad = np.argwhere(H != r.hashes)
+        pytest.fail(f"hash mismatch at (cycle, lane) {bad[:5].tolist()} of {bad.shape[0]}")
+    assert np.array_equal(F, r.final_state), np.argwhere(F != r.final_state)[:5]
+    return L
+
+
+def test_paper_example_both_modes(rs):
+    c, outs = cf.paper_example(two_muls=True)
+    for mode in ("lanes", "single"):
+        H, F, _ = run_gpu(rs, c, 2, mode=mode)
+        assert [int(F[o, 0]) for o in outs] == [4, 8]
+        check(rs, c, 2, mode=mode)
+
+
+def test_stimulus_matches_golden(rs):
+    """The kernel's independent stimulus generator reproduces the golden values
+    written by tests/golden/make_golden.py (oracle only)."""
+    from synth import Builder
+    b = Builder()
+    ins = [b.input(64) for _ in range(4)]
+    c = b.build()
+    g = rs.Graph(c)
+    L = rs.Lanes(g, 1024)
+    L.set_seed(1)
+    gold = json.load(open(os.path.join(HERE, "golden", "stimulus_seed1.json")))
+    for cyc in range(3):
+        L.step(1)
+        vals = L.read(ins)
+        for row in gold["values"]:
+            if row["c"] == cyc:
+                assert int(vals[row["k"], row["lane"]]) == int(row["value"]), row
+
+
+@pytest.mark.parametrize("mode", ["lanes", "single"])
+def test_c1_full(rs, mode):
+    cfg = CONFIGS["C1"]
+    check(rs, config_circuit("C1"), cfg.cycles, 1, seed=cfg.stim_seed, mode=mode)
+
+
+@pytest.mark.parametrize("lt", [8, 16, 32])
+def test_c2_structure_ragged_lanes(rs, lt):
+    """Full C2 circuit, 37 lanes (ragged last tile), 25 cycles, each lane tile."""
+    check(rs, config_circuit("C2"), 25, 37, seed=CONFIGS["C2"].stim_seed, lane_tile=lt)
+
+
+def test_c2_threads_variants(rs):
+    c = config_circuit("C2", n_ops=5000, n_levels=40, n_regs=500)
+    for th in (64, 256, 1024):
+        check(rs, c, 12, 40, seed=7, threads=th, lane_tile=8)
+
+
+def test_c3_structure(rs):
+    check(rs, config_circuit("C3"), 6, 40, seed=CONFIGS["C3"].stim_seed)
+
+
+def test_c5_structure_single_lane(rs):
+    """C5 generator, scaled to 200k ops / 150 levels, single-lane grid mode."""
+    c = config_circuit("C5", n_ops=200_000, n_regs=25_000, n_inputs=512)
+    check(rs, c, 12, 1, seed=CONFIGS["C5"].stim_seed, mode="single")
+
+
+def test_fuzz_corpus(rs):
+    """Fuzz corpus (SPEC.md S:405 shape): constants, register->source edges,
+    wide folds, permuted ids; 60 cycles, both modes."""
+    for seed in range(200):
+        c = fuzz_circuit(seed)
+        check(rs, c, 60, 3, seed=seed)
+        if seed % 4 == 0:
+            check(rs, c, 60, 1, seed=seed, mode="single")
+
+
+def test_closed_forms_on_gpu(rs):
+    c, r = cf.counter(13)
+    H, F, _ = run_gpu(rs, c, 300, 4)
+    assert (F[r] == 300 % 2 ** 13).all()
+    c, s = cf.lfsr(16, (16, 14, 13, 11), seed=1)
+    H, F, L = run_gpu(rs, c, 65535, 2)
+    assert (F[s] == 1).all()                             # period 2^16 - 1
+    H1, F1, _ = run_gpu(rs, c, 65535, 1, mode="single", final=True)
+    assert int(F1[s, 0]) == 1
+    r0 = oracle.simulate(c, 65535, n_lanes=1)
+    assert np.array_equal(H1, r0.hashes) and np.array_equal(H[:, :1], r0.hashes)
+    c, a, b, out = cf.ripple_adder(8)
+    A = np.repeat(np.arange(256, dtype=np.uint64), 256)
+    B = np.tile(np.arange(256, dtype=np.uint64), 256)
+    H, F, _ = run_gpu(rs, c, 1, 65536, staged=np.stack([A, B])[None])
+    assert np.array_equal(F[out], A + B)
+    c, x, regs = cf.shift_register(6, 16)
+    vals = (np.arange(40, dtype=np.uint64) * np.uint64(977) + np.uint64(5))[:, None, None]
+    check(rs, c, 40, 1, staged=vals)
+
+
+def test_chunking_and_hash_toggle(rs):
+    c = config_circuit("C2", n_ops=4000, n_levels=20, n_regs=400)
+    g = rs.Graph(c)
+    L = rs.Lanes(g, 50)
+    L.set_seed(11)
+    h1 = L.step(7, hashes="host")
+    L.step(5)                                             # hash off: carry must be refreshed
+    h3 = L.step(8, hashes="host")
+    h4 = L.step(1, hashes="host")
+    r = oracle.simulate(c, 21, seed=11, n_lanes=50)
+    assert np.array_equal(h1, r.hashes[:7])
+    assert np.array_equal(h3, r.hashes[12:20]) and np.array_equal(h4, r.hashes[20:21])
+    assert L.cycle == 21
+    L.step(0)
+    assert L.cycle == 21
+
+
+def test_staged_inputs_chunks(rs):
+    c = config_circuit("C2", n_ops=3000, n_levels=15, n_regs=300)
+    rng = np.random.default_rng(3)
+    n, nl = 30, 33
+    vals = rng.integers(0, 2**63, size=(n, c.n_inputs, nl), dtype=np.int64).astype(np.uint64) * np.uint64(3)
+    g = rs.Graph(c)
+    L = rs.Lanes(g, nl, stage_cycles=8)
+    hs = []
+    for c0 in range(0, n, 6):
+        L.set_inputs(c0, vals[c0:c0 + 6])
+        hs.append(L.step(6, hashes="host"))
+    r = oracle.simulate(c, n, n_lanes=nl, staged=vals)
+    assert np.array_equal(np.concatenate(hs), r.hashes)
+    with pytest.raises(rs.RtlSimError) as e:
+        L.step(3)                                         # cycles 30..32 not staged
+    assert e.value.name == "RS_E_STATE"
+
+
+def test_checkpoint_restore(rs):
+    c = config_circuit("C2", n_ops=3000, n_levels=15, n_regs=300)
+    full = oracle.simulate(c, 20, seed=5, n_lanes=24)
+    g = rs.Graph(c)
+    a = rs.Lanes(g, 24)
+    a.set_seed(5)
+    h0 = a.step(10, hashes="host")
+    regs = a.read(c.reg_id)
+    b = rs.Lanes(g, 24)
+    b.set_seed(5)
+    b.write_registers(c.reg_id, regs)
+    b.cycle = 10
+    h1 = b.step(10, hashes="host")
+    assert np.array_equal(np.concatenate([h0, h1]), full.hashes)
+    with pytest.raises(rs.RtlSimError) as e:
+        b.write_registers([int(c.input_id[0])], np.zeros((1, 24), np.uint64))
+    assert e.value.name == "RS_E_RANGE"
+
+
+def test_lane_sharding_invariance(rs):
+    """Global lane ids: two shards (lane0 = 0, 37) reproduce one 74-lane run
+    (the multi-GPU partition of SURVEY §8(e))."""
+    c = config_circuit("C2", n_ops=3000, n_levels=15, n_regs=300)
+    Hf, Ff, _ = run_gpu(rs, c, 15, 74, seed=9)
+    Ha, Fa, _ = run_gpu(rs, c, 15, 37, seed=9, lane0=0)
+    Hb, Fb, _ = run_gpu(rs, c, 15, 37, seed=9, lane0=37)
+    assert np.array_equal(Hf, np.concatenate([Ha, Hb], axis=1))
+    assert np.array_equal(Ff, np.concatenate([Fa, Fb], axis=1))
+
+
+def test_error_statuses(rs):
+    c = config_circuit("C1")
+    g = rs.Graph(c)
+    L = rs.Lanes(g, 4)
+    with pytest.raises(rs.RtlSimError) as e:
+        L.read([0], lane_begin=3, n_lanes=2)
+    assert e.value.name == "RS_E_RANGE"
+    with pytest.raises(rs.RtlSimError) as e:
+        L.read([c.n_signals])
+    assert e.value.name == "RS_E_RANGE"
+    with pytest.raises(rs.RtlSimError) as e:
+        L.set_inputs(0, np.zeros((1, c.n_inputs, 4), np.uint64))
+    assert e.value.name == "RS_E_STATE"
+    gs = rs.Graph(c, mode="single")
+    with pytest.raises(rs.RtlSimError) as e:
+        rs.Lanes(gs, 2)
+    assert e.value.name == "RS_E_INVALID_ARG"
+    with pytest.raises(rs.RtlSimError) as e:
+        rs.Lanes(g, 0)
+    assert e.value.name == "RS_E_INVALID_ARG"
+
+
+def test_degenerate_graphs(rs):
+    from synth import Builder
+    b = Builder()                                   # registers only, no ops
+    r = b.reg(8, 3)
+    b.set_next(r, r)
+    check(rs, b.build(), 5, 3)
+    b = Builder()                                   # inputs only
+    b.input(12)
+    b.input(64)
+    check(rs, b.build(), 5, 70, seed=4)
+    b = Builder()                                   # constants feeding ops, no inputs
+    k = b.const(64, 2**64 - 1)
+    k2 = b.const(7, 5)
+    b.op("add", [k, k2], 64)
+    b.op("cat", [k2, k], 64)
+    c = b.build()
+    for mode in ("lanes", "single"):
+        check(rs, c, 3, 1, mode=mode)
+
+
+@pytest.mark.slow
+def test_full_size_sampled(rs):
+    """BASELINE.json full sizes in the bench's launch configuration (auto
+    lane tile / threads): GPU runs all lanes; the oracle checks sampled
+    lanes (first/last of tiles, spread) cycle by cycle."""
+    for name, cycles, sample in (("C2", 60, 12), ("C3", 6, 6)):
+        cfg = CONFIGS[name]
+        c = config_circuit(name)
+        H, _, L = run_gpu(rs, c, cycles, cfg.lanes, seed=cfg.stim_seed, final=False)
+        lt = L.shape()["lane_tile"]
+        lanes = sorted(set([0, lt - 1, lt, cfg.lanes - 1] +
+                           list(np.linspace(0, cfg.lanes - 1, sample).astype(int))))
+        r = oracle.simulate(c, cycles, seed=cfg.stim_seed, lanes=lanes, threads=8)
+        assert np.array_equal(H[:, lanes], r.hashes), name
+        F = L.read(list(range(0, c.n_signals, 7)))
+        rf = oracle.simulate(c, cycles, seed=cfg.stim_seed, lanes=lanes[:3], final=True, hashes=False)
+        assert np.array_equal(F[:, lanes[:3]], rf.final_state[::7])
+
+
+@pytest.mark.slow
+def test_c4_c5_full_size_sampled(rs):
+    c = config_circuit("C4")
+    cfg = CONFIGS["C4"]
+    H, _, L = run_gpu(rs, c, 2, cfg.lanes, seed=cfg.stim_seed, final=False)
+    lanes = [0, 31, 4096, cfg.lanes - 1]
+    r = oracle.simulate(c, 2, seed=cfg.stim_seed, lanes=lanes, threads=4)
+    assert np.array_equal(H[:, lanes], r.hashes)
+    del L
+    c = config_circuit("C5")
+    H, F, _ = run_gpu(rs, c, 10, 1, seed=CONFIGS["C5"].stim_seed, mode="single", final=True)
+    r = oracle.simulate(c, 10, seed=CONFIGS["C5"].stim_seed, final=True)
+    assert np.array_equal(H, r.hashes) and np.array_equal(F, r.final_state)
