@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstring>
 #include <numeric>
 #include <unordered_map>
 
@@ -330,6 +331,131 @@ rs_status compile_graph(const rs_graph_desc* d, uint32_t mode, CompiledGraph* ou
     g.identity_ops_naive = ids;
   }
   return RS_OK;
+}
+
+namespace {
+inline uint32_t al16(uint32_t x) { return (x + 15u) & ~15u; }
+
+struct StageWriter {
+  std::vector<uint8_t>* blob;
+  std::vector<StageRef>* table;
+  void emit(StageHdr h, const uint32_t* w, const uint64_t* k, const uint32_t* c, const StageRun* runs) {
+    h.off_w = al16((uint32_t)sizeof(StageHdr));
+    h.off_k = al16(h.off_w + 4 * h.n);
+    h.off_c = al16(h.off_k + 8 * h.n);
+    h.off_runs = al16(h.off_c + 4 * h.n_coords);
+    h.bytes = al16(h.off_runs + (uint32_t)sizeof(StageRun) * h.n_runs);
+    const size_t base = (blob->size() + 15) & ~(size_t)15;
+    blob->resize(base + h.bytes, 0);
+    uint8_t* p = blob->data() + base;
+    std::memcpy(p, &h, sizeof h);
+    if (h.n) {
+      std::memcpy(p + h.off_w, w, 4ull * h.n);
+      std::memcpy(p + h.off_k, k, 8ull * h.n);
+    }
+    if (h.n_coords) std::memcpy(p + h.off_c, c, 4ull * h.n_coords);
+    if (h.n_runs) std::memcpy(p + h.off_runs, runs, sizeof(StageRun) * h.n_runs);
+    table->push_back({base, h.bytes, h.type});
+  }
+};
+
+uint32_t stage_size(uint32_t n, uint32_t n_coords, uint32_t n_runs) {
+  uint32_t off_w = al16((uint32_t)sizeof(StageHdr));
+  uint32_t off_k = al16(off_w + 4 * n);
+  uint32_t off_c = al16(off_k + 8 * n);
+  uint32_t off_r = al16(off_c + 4 * n_coords);
+  return al16(off_r + (uint32_t)sizeof(StageRun) * n_runs);
+}
+}  // namespace
+
+void build_stages(const CompiledGraph& g, uint32_t stage_bytes, std::vector<uint8_t>* blob,
+                  std::vector<StageRef>* table) {
+  blob->clear();
+  table->clear();
+  StageWriter W{blob, table};
+  // inputs: w, K, coord
+  {
+    uint32_t i = 0;
+    while (i < g.n_inputs) {
+      uint32_t n = 0;
+      while (i + n < g.n_inputs && stage_size(n + 1, n + 1, 0) <= stage_bytes) ++n;
+      StageHdr h{};
+      h.type = ST_INJECT;
+      h.n = n;
+      h.n_coords = n;
+      h.first = i;
+      W.emit(h, &g.in_w[i], &g.in_k[i], &g.in_coord[i], nullptr);
+      i += n;
+    }
+  }
+  // ops, level by level
+  for (uint32_t l = 0; l < g.n_levels; ++l) {
+    const uint32_t ob = g.level_op_begin[l], oe = g.level_op_begin[l + 1];
+    uint32_t r = g.level_run_begin[l];
+    uint32_t j = ob;
+    while (j < oe) {
+      // grow the stage op by op
+      uint32_t e = j, nruns = 0, ncoords = 0, rr = r;
+      while (e < oe) {
+        while (rr + 1 < g.level_run_begin[l + 1] && g.runs[rr + 1].op_begin <= e) ++rr;
+        const bool new_run = (e == j) || (g.runs[rr].op_begin == e);
+        const uint32_t ar = g.coord_off[e + 1] - g.coord_off[e];
+        if (stage_size(e - j + 1, ncoords + ar, nruns + (new_run ? 1 : 0)) > stage_bytes && e > j) break;
+        nruns += new_run ? 1 : 0;
+        ncoords += ar;
+        ++e;
+      }
+      std::vector<StageRun> runs;
+      uint32_t k = j;
+      while (k < e) {
+        while (r + 1 < g.level_run_begin[l + 1] && g.runs[r + 1].op_begin <= k) ++r;
+        const DevRun& R = g.runs[r];
+        const uint32_t se = std::min(e, R.op_begin + R.count);
+        StageRun sr{};
+        sr.op_begin = k - j;
+        sr.count = se - k;
+        sr.coord_begin = g.coord_off[k] - g.coord_off[j];
+        sr.out_row0 = R.out_row0 + (k - R.op_begin);
+        sr.meta = R.meta;
+        runs.push_back(sr);
+        k = se;
+      }
+      StageHdr h{};
+      h.type = ST_OPS;
+      h.n = e - j;
+      h.n_runs = (uint32_t)runs.size();
+      h.n_coords = g.coord_off[e] - g.coord_off[j];
+      h.first = j;
+      h.level = l;
+      W.emit(h, &g.opw[j], &g.opk[j], &g.coord[g.coord_off[j]], runs.data());
+      j = e;
+    }
+  }
+  // registers: w, K, (next, reg) coord pairs
+  {
+    uint32_t i = 0;
+    while (i < g.n_regs) {
+      uint32_t n = 0;
+      while (i + n < g.n_regs && stage_size(n + 1, 2 * (n + 1), 0) <= stage_bytes) ++n;
+      std::vector<uint32_t> pairs(2 * n);
+      for (uint32_t q = 0; q < n; ++q) {
+        pairs[2 * q] = g.reg_next_coord[i + q];
+        pairs[2 * q + 1] = g.reg_coord[i + q];
+      }
+      StageHdr h{};
+      h.type = ST_LATCH;
+      h.n = n;
+      h.n_coords = 2 * n;
+      h.first = i;
+      W.emit(h, &g.reg_w[i], &g.reg_k[i], pairs.data(), nullptr);
+      i += n;
+    }
+  }
+  if (table->empty()) {
+    StageHdr h{};
+    h.type = ST_NOP;
+    W.emit(h, nullptr, nullptr, nullptr, nullptr);
+  }
 }
 
 }  // namespace rtlsim

@@ -102,4 +102,49 @@ inline uint64_t width_mask(uint32_t w) { return w >= 64 ? ~0ull : ((1ull << w) -
 // Returns RS_OK or an error status with *err set.
 rs_status compile_graph(const rs_graph_desc* d, uint32_t mode, CompiledGraph* out, std::string* err);
 
+// ---------------------------------------------------------------- stages
+// The lane kernel walks a fixed per-cycle schedule of *stages*; each stage's
+// descriptors live in one contiguous, 16-byte aligned block of the stage blob
+// so a single TMA bulk copy (cp.async.bulk) brings it into shared memory,
+// prefetched one stage ahead.  Schedule per cycle:
+//   INJECT chunks (inputs) | OPS chunks, level by level | LATCH chunks (registers)
+// with a CTA barrier after every stage.  A level larger than one stage is
+// split into several OPS stages (barrier after each; only the last one ends
+// the level, but an extra barrier is harmless).
+enum StageType : uint32_t { ST_INJECT = 1, ST_OPS = 2, ST_LATCH = 3, ST_NOP = 4 };
+
+struct StageHdr {          // first 64 bytes of a stage block
+  uint32_t type;
+  uint32_t n;              // ops / inputs / registers in the stage
+  uint32_t n_runs;
+  uint32_t n_coords;
+  uint32_t first;          // index of the first input / register / op (global numbering)
+  uint32_t level;
+  uint32_t off_w;          // u32[n]: op param words / input widths / register widths
+  uint32_t off_k;          // u64[n]: hash weights
+  uint32_t off_c;          // u32[..]: op operand coords | input coords | (next, reg) coord pairs
+  uint32_t off_runs;       // StageRun[n_runs]
+  uint32_t bytes;
+  uint32_t pad[5];
+};
+
+struct StageRun {          // a run clipped to the stage; indices relative to the stage
+  uint32_t op_begin;
+  uint32_t count;
+  uint32_t coord_begin;
+  uint32_t out_row0;
+  uint32_t meta;           // opcode | arity << 8 | out_cls << 16
+  uint32_t pad[3];
+};
+
+struct StageRef {
+  uint64_t off;            // byte offset of the block in the blob
+  uint32_t bytes;
+  uint32_t type;
+};
+
+// Build the per-cycle stage schedule with blocks of at most stage_bytes.
+void build_stages(const CompiledGraph& g, uint32_t stage_bytes, std::vector<uint8_t>* blob,
+                  std::vector<StageRef>* table);
+
 }  // namespace rtlsim

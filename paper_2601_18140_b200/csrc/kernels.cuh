@@ -60,6 +60,10 @@ struct StepArgs {
   uint64_t* hcarry_in;     // per-lane register-term of the hash for cycle0
   uint64_t* hcarry_out;    // same for cycle0 + n_cycles (may alias hcarry_in in lane mode)
   unsigned long long* bar; // grid barrier counter (single mode)
+  const uint8_t* stage_blob;   // lane mode: per-cycle stage schedule (compiler.hpp)
+  const StageRef* stage_tab;
+  uint32_t n_stages;
+  uint32_t stage_bytes;        // shared-memory bytes per stage buffer
 };
 
 // ------------------------------------------------------------------ helpers
@@ -166,43 +170,71 @@ __device__ __forceinline__ uint64_t fold_step(uint32_t op, uint64_t r, uint64_t 
 }
 
 // ------------------------------------------------------------------ lane mode
-// Everything a run segment needs, passed by value (registers) to a
-// non-inlined specialisation: keeps each (opcode, arity) body's register
-// allocation independent of the kernel's outer loops.
-template <int LT>
-struct SegCtx {
-  TileP<LT> t;
-  const uint32_t* __restrict__ coord;
-  const uint32_t* __restrict__ opw;
-  const uint64_t* __restrict__ opk;
-};
+// Shared-memory helpers (explicit .shared accesses from non-inlined code).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint64_t lds64(uint32_t a) {
+  uint64_t v;
+  asm("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
 
+// mbarrier + TMA 1-D bulk copy (cp.async.bulk) -- the stage prefetch.
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+
+// One run segment of a stage: n ops of opcode OP, arity A, out class out_cls,
+// descriptors in shared memory (s_c: first coord, s_w: first param word,
+// s_k: first hash weight), outputs in consecutive rows from row0.  U ops'
+// operands are gathered before any is computed (memory-level parallelism).
 template <int LT, bool HASH, int OP, int A>
-__device__ __noinline__ uint64_t run_segment(uint8_t* p0, uint16_t* p1, uint32_t* p2, uint64_t* p3,
-                                             const uint32_t* __restrict__ coord, const uint32_t* __restrict__ opw,
-                                             const uint64_t* __restrict__ opk, uint32_t op_begin,
-                                             uint32_t coord_begin, uint32_t out_row0, uint32_t out_cls,
-                                             uint32_t b, uint32_t e) {
+__device__ __noinline__ uint64_t run_segment(uint8_t* p0, uint16_t* p1, uint32_t* p2, uint64_t* p3, uint32_t s_c,
+                                             uint32_t s_w, uint32_t s_k, uint32_t out_cls, uint32_t row0,
+                                             uint32_t n) {
   constexpr int U = (A <= 2) ? 8 : 4;
-  const SegCtx<LT> c{{p0, p1, p2, p3}, coord, opw, opk};
+  const TileP<LT> t{p0, p1, p2, p3};
   uint64_t hacc = 0;
-  const uint32_t* __restrict__ cp = c.coord + coord_begin + (b - op_begin) * A;
-  uint32_t row = out_row0 + (b - op_begin);
-  for (uint32_t j = b; j < e; j += U, cp += U * A, row += U) {
+  for (uint32_t j = 0; j < n; j += U, s_c += 4 * U * A) {
     uint64_t x[U][A];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      if (j + u < e) {
+      if (j + u < n) {
 #pragma unroll
-        for (int o = 0; o < A; ++o) x[u][o] = c.t.ld(__ldg(cp + u * A + o));
+        for (int o = 0; o < A; ++o) x[u][o] = t.ld(lds32(s_c + 4 * (u * A + o)));
       }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      if (j + u < e) {
-        const uint64_t y = apply_op<OP, A>(x[u], __ldg(c.opw + j + u));
-        c.t.st(out_cls, row + u, y);
-        if constexpr (HASH) hacc += y * __ldg(c.opk + j + u);
+      if (j + u < n) {
+        const uint64_t y = apply_op<OP, A>(x[u], lds32(s_w + 4 * (j + u)));
+        t.st(out_cls, row0 + j + u, y);
+        if constexpr (HASH) hacc += y * lds64(s_k + 8 * (j + u));
       }
     }
   }
@@ -210,31 +242,32 @@ __device__ __noinline__ uint64_t run_segment(uint8_t* p0, uint16_t* p1, uint32_t
 }
 
 template <int LT, bool HASH>
-__device__ __noinline__ uint64_t run_generic(const SegCtx<LT> c, const DevRun run, uint32_t b, uint32_t e) {
-  const uint32_t op = run.meta & 0xffu, n = (run.meta >> 8) & 0xffu, out_cls = (run.meta >> 16) & 3u;
+__device__ __noinline__ uint64_t run_generic(uint8_t* p0, uint16_t* p1, uint32_t* p2, uint64_t* p3, uint32_t s_c,
+                                             uint32_t s_w, uint32_t s_k, uint32_t meta, uint32_t row0, uint32_t n) {
+  const TileP<LT> t{p0, p1, p2, p3};
+  const uint32_t op = meta & 0xffu, ar = (meta >> 8) & 0xffu, out_cls = (meta >> 16) & 3u;
   uint64_t hacc = 0;
-  for (uint32_t j = b; j < e; ++j) {
-    const uint32_t* cp = c.coord + run.coord_begin + (j - run.op_begin) * n;
-    uint64_t r = c.t.ld(__ldg(cp));
-    for (uint32_t o = 1; o < n; ++o) r = fold_step(op, r, c.t.ld(__ldg(cp + o)));
-    const uint64_t y = r & wmask(__ldg(c.opw + j) & 127u);
-    c.t.st(out_cls, run.out_row0 + (j - run.op_begin), y);
-    if constexpr (HASH) hacc += y * __ldg(c.opk + j);
+  for (uint32_t j = 0; j < n; ++j) {
+    const uint32_t c = s_c + 4 * j * ar;
+    uint64_t r = t.ld(lds32(c));
+    for (uint32_t o = 1; o < ar; ++o) r = fold_step(op, r, t.ld(lds32(c + 4 * o)));
+    const uint64_t y = r & wmask(lds32(s_w + 4 * j) & 127u);
+    t.st(out_cls, row0 + j, y);
+    if constexpr (HASH) hacc += y * lds64(s_k + 8 * j);
   }
   return hacc;
 }
 
 template <int LT, bool HASH>
-__device__ __forceinline__ uint64_t dispatch_run(const SegCtx<LT>& c, const DevRun& run, uint32_t b, uint32_t e) {
-  const uint32_t op = run.meta & 0xffu, n = (run.meta >> 8) & 0xffu;
-#define RS_SEG(OPC, N) \
-  run_segment<LT, HASH, OPC, N>(c.t.p0, c.t.p1, c.t.p2, c.t.p3, c.coord, c.opw, c.opk, run.op_begin, \
-                                run.coord_begin, run.out_row0, (run.meta >> 16) & 3u, b, e)
-#define RS_FOLD(OPC)                                                    \
-  case OPC:                                                             \
-    if (n == 2) return RS_SEG(OPC, 2);                                  \
-    if (n == 3) return RS_SEG(OPC, 3);                                  \
-    return run_generic<LT, HASH>(c, run, b, e);
+__device__ __forceinline__ uint64_t dispatch_run(const TileP<LT>& t, uint32_t meta, uint32_t s_c, uint32_t s_w,
+                                                 uint32_t s_k, uint32_t row0, uint32_t n) {
+  const uint32_t op = meta & 0xffu, ar = (meta >> 8) & 0xffu, cls = (meta >> 16) & 3u;
+#define RS_SEG(OPC, N) run_segment<LT, HASH, OPC, N>(t.p0, t.p1, t.p2, t.p3, s_c, s_w, s_k, cls, row0, n)
+#define RS_FOLD(OPC)                                                                  \
+  case OPC:                                                                           \
+    if (ar == 2) return RS_SEG(OPC, 2);                                               \
+    if (ar == 3) return RS_SEG(OPC, 3);                                               \
+    return run_generic<LT, HASH>(t.p0, t.p1, t.p2, t.p3, s_c, s_w, s_k, meta, row0, n);
   switch (op) {
     RS_FOLD(RS_OP_AND)
     RS_FOLD(RS_OP_OR)
@@ -256,14 +289,45 @@ __device__ __forceinline__ uint64_t dispatch_run(const SegCtx<LT>& c, const DevR
 #undef RS_SEG
 }
 
-// Registers: tmp = LI[next] & M(w_r); LI[r] = tmp.  Hazard-free in one pass
-// because the compiler made every next row an op row (reading R8).
+__device__ __forceinline__ void chunk_of(uint32_t n, uint32_t part, uint32_t nparts, uint32_t& b, uint32_t& e) {
+  const uint32_t c = (n + nparts - 1) / nparts;
+  b = min(n, part * c);
+  e = min(n, b + c);
+}
+
+// OPS stage: the sub-warp's contiguous chunk of the stage's ops, run by run.
 template <int LT, bool HASH>
-__device__ __noinline__ uint64_t latch_range(uint8_t* p0, uint16_t* p1, uint32_t* p2, uint64_t* p3,
-                                             const uint32_t* __restrict__ next_coord,
-                                             const uint32_t* __restrict__ reg_coord,
-                                             const uint32_t* __restrict__ reg_w, const uint64_t* __restrict__ reg_k,
-                                             uint32_t b, uint32_t e) {
+__device__ __forceinline__ uint64_t stage_ops(const TileP<LT>& t, const uint8_t* buf, uint32_t sub, uint32_t nsub) {
+  const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
+  uint32_t b, e;
+  chunk_of(h->n, sub, nsub, b, e);
+  uint64_t hacc = 0;
+  if (b >= e) return 0;
+  const StageRun* runs = reinterpret_cast<const StageRun*>(buf + h->off_runs);
+  uint32_t lo = 0, hi = h->n_runs - 1;
+  while (lo < hi) {  // last run with op_begin <= b
+    const uint32_t mid = (lo + hi + 1) >> 1;
+    if (runs[mid].op_begin <= b) lo = mid; else hi = mid - 1;
+  }
+  const uint32_t base = smem_addr(buf);
+  for (uint32_t r = lo; b < e; ++r) {
+    const StageRun R = runs[r];
+    const uint32_t se = min(e, R.op_begin + R.count);
+    const uint32_t ar = (R.meta >> 8) & 0xffu, k = b - R.op_begin;
+    const uint64_t hh = dispatch_run<LT, HASH>(t, R.meta, base + h->off_c + 4 * (R.coord_begin + k * ar),
+                                               base + h->off_w + 4 * b, base + h->off_k + 8 * b, R.out_row0 + k,
+                                               se - b);
+    if constexpr (HASH) hacc += hh;
+    b = se;
+  }
+  return hacc;
+}
+
+// LATCH stage: tmp = LI[next] & M(w_r); LI[r] = tmp.  One pass is hazard-free
+// because every next row is an op row (compiler identity copies; reading R8).
+template <int LT, bool HASH>
+__device__ __noinline__ uint64_t stage_latch(uint8_t* p0, uint16_t* p1, uint32_t* p2, uint64_t* p3, uint32_t s_c,
+                                             uint32_t s_w, uint32_t s_k, uint32_t b, uint32_t e) {
   constexpr int U = 8;
   const TileP<LT> t{p0, p1, p2, p3};
   uint64_t h = 0;
@@ -271,79 +335,49 @@ __device__ __noinline__ uint64_t latch_range(uint8_t* p0, uint16_t* p1, uint32_t
     uint64_t v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (j + u < e) v[u] = t.ld(__ldg(next_coord + j + u));
+      if (j + u < e) v[u] = t.ld(lds32(s_c + 8 * (j + u)));
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (j + u < e) {
-        const uint64_t x = v[u] & wmask(__ldg(reg_w + j + u));
-        t.stc(__ldg(reg_coord + j + u), x);
-        if constexpr (HASH) h += x * __ldg(reg_k + j + u);
+        const uint64_t x = v[u] & wmask(lds32(s_w + 4 * (j + u)));
+        t.stc(lds32(s_c + 8 * (j + u) + 4), x);
+        if constexpr (HASH) h += x * lds64(s_k + 8 * (j + u));
       }
   }
   return h;
 }
 
+// INJECT stage: LI[in_k] = stimulus & M(w_k) (or the staged value).
 template <int LT, bool HASH>
-__device__ __noinline__ uint64_t inject_range(uint8_t* p0, uint16_t* p1, uint32_t* p2, uint64_t* p3,
-                                              const uint32_t* __restrict__ in_coord,
-                                              const uint32_t* __restrict__ in_w, const uint64_t* __restrict__ in_k,
-                                              const uint64_t* __restrict__ stage, uint32_t n_inputs, uint32_t n_lanes,
-                                              uint64_t seed, uint64_t glane, uint64_t slot_or_cycle, int staged,
-                                              uint32_t lane, bool valid, uint32_t b, uint32_t e) {
+__device__ __noinline__ uint64_t stage_inject(uint8_t* p0, uint16_t* p1, uint32_t* p2, uint64_t* p3, uint32_t s_c,
+                                              uint32_t s_w, uint32_t s_k, uint32_t first, uint32_t b, uint32_t e,
+                                              const uint64_t* __restrict__ stage, uint32_t n_inputs,
+                                              uint32_t n_lanes, uint64_t seed, uint64_t glane, uint64_t cycle_or_slot,
+                                              int staged, uint32_t lane, bool valid) {
   const TileP<LT> t{p0, p1, p2, p3};
   uint64_t h = 0;
-  for (uint32_t k = b; k < e; ++k) {
+  for (uint32_t j = b; j < e; ++j) {
+    const uint32_t k = first + j;
     uint64_t v;
     if (staged)
-      v = valid ? __ldg(stage + (slot_or_cycle * n_inputs + k) * n_lanes + lane) : 0ull;
+      v = valid ? __ldg(stage + (cycle_or_slot * n_inputs + k) * n_lanes + lane) : 0ull;
     else
-      v = d_stimulus(seed, k, slot_or_cycle, glane);
-    v &= wmask(__ldg(in_w + k));
-    t.stc(__ldg(in_coord + k), v);
-    if constexpr (HASH) h += v * __ldg(in_k + k);
+      v = d_stimulus(seed, k, cycle_or_slot, glane);
+    v &= wmask(lds32(s_w + 4 * j));
+    t.stc(lds32(s_c + 4 * j), v);
+    if constexpr (HASH) h += v * lds64(s_k + 8 * j);
   }
   return h;
-}
-
-__device__ __forceinline__ void chunk_of(uint32_t n, uint32_t part, uint32_t nparts, uint32_t& b, uint32_t& e) {
-  const uint32_t c = (n + nparts - 1) / nparts;
-  b = min(n, part * c);
-  e = min(n, b + c);
-}
-
-template <int LT, bool HASH>
-__device__ __forceinline__ void do_level_lanes(const StepArgs& a, const TileP<LT>& t, uint32_t lev,
-                                               uint32_t sub, uint32_t nsub, uint64_t& hacc) {
-  const uint32_t ob = __ldg(a.g.level_op_begin + lev), oe = __ldg(a.g.level_op_begin + lev + 1);
-  uint32_t b, e;
-  chunk_of(oe - ob, sub, nsub, b, e);
-  if (b >= e) return;
-  b += ob;
-  e += ob;
-  uint32_t lo = __ldg(a.g.level_run_begin + lev), hi = __ldg(a.g.level_run_begin + lev + 1) - 1;
-  while (lo < hi) {  // last run with op_begin <= b
-    const uint32_t mid = (lo + hi + 1) >> 1;
-    if (__ldg(&a.g.runs[mid].op_begin) <= b) lo = mid; else hi = mid - 1;
-  }
-  for (uint32_t r = lo; b < e; ++r) {
-    DevRun run;
-    run.op_begin = __ldg(&a.g.runs[r].op_begin);
-    run.count = __ldg(&a.g.runs[r].count);
-    run.coord_begin = __ldg(&a.g.runs[r].coord_begin);
-    run.out_row0 = __ldg(&a.g.runs[r].out_row0);
-    run.meta = __ldg(&a.g.runs[r].meta);
-    const uint32_t se = min(e, run.op_begin + run.count);
-    const SegCtx<LT> c{t, a.g.coord, a.g.opw, a.g.opk};
-    const uint64_t h = dispatch_run<LT, HASH>(c, run, b, se);
-    if constexpr (HASH) hacc += h;
-    b = se;
-  }
 }
 
 template <int LT, bool HASH>
 __global__ void __launch_bounds__(1024, 1) k_lanes(const StepArgs a) {
   constexpr int LTL = (LT == 32) ? 5 : (LT == 16) ? 4 : (LT == 8) ? 3 : (LT == 4) ? 2 : (LT == 2) ? 1 : 0;
-  extern __shared__ uint64_t red[];  // [2][nsub][LT]
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
+  uint8_t* bufs[2] = {smem + 128, smem + 128 + a.stage_bytes};
+  uint64_t* red = reinterpret_cast<uint64_t*>(smem + 128 + 2 * (size_t)a.stage_bytes);  // [2][nsub][LT]
+
   const uint32_t tile = blockIdx.x;
   const uint32_t lin = threadIdx.x & (LT - 1);
   const uint32_t sub = threadIdx.x >> LTL;
@@ -352,51 +386,89 @@ __global__ void __launch_bounds__(1024, 1) k_lanes(const StepArgs a) {
   const bool valid = lane < a.n_lanes;
   const TileP<LT> t = tile_ptrs<LT>(a, tile, lin);
 
-  uint32_t ib, ie, rb, re;
-  chunk_of(a.g.n_inputs, sub, nsub, ib, ie);
-  chunk_of(a.g.n_regs, sub, nsub, rb, re);
-
-  uint64_t hacc = 0;
-  if (HASH && sub == 0 && valid) hacc = a.hcarry_in[lane];
-  if (a.n_cycles == 0) return;
-  auto inject = [&](uint64_t cycle) -> uint64_t {
-    const uint64_t sc = a.staged ? cycle % a.stage_cap : cycle;
-    return inject_range<LT, HASH>(t.p0, t.p1, t.p2, t.p3, a.g.in_coord, a.g.in_w, a.g.in_k, a.stage,
-                                  a.g.n_inputs, a.n_lanes, a.seed, a.lane0 + lane, sc, a.staged, lane, valid, ib, ie);
-  };
-  hacc += inject(a.cycle0);
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    mbar_fence_init();
+  }
   __syncthreads();
-  uint64_t hr = 0;
-  for (uint32_t cyc = 0; cyc < a.n_cycles; ++cyc) {
-    for (uint32_t lev = 0; lev < a.g.n_levels; ++lev) {
-      do_level_lanes<LT, HASH>(a, t, lev, sub, nsub, hacc);
-      __syncthreads();
+  const uint32_t S = a.n_stages;
+  const uint64_t total = (uint64_t)a.n_cycles * S;
+  auto issue = [&](uint32_t idx, int b) {
+    const StageRef r = a.stage_tab[idx];
+    tma_load_1d(bufs[b], a.stage_blob + r.off, r.bytes, &mbar[b]);
+  };
+  if (threadIdx.x == 0 && total) issue(0, 0);
+
+  uint64_t hacc = 0, hr = 0;
+  uint64_t hr_prev = (HASH && sub == 0 && valid) ? a.hcarry_in[lane] : 0ull;
+  uint32_t s = 0, cyc = 0;
+  for (uint64_t gi = 0; gi < total; ++gi) {
+    const int bsel = (int)(gi & 1);
+    if (threadIdx.x == 0 && gi + 1 < total) issue(s + 1 == S ? 0 : s + 1, bsel ^ 1);
+    mbar_wait(&mbar[bsel], (uint32_t)((gi >> 1) & 1));
+    const uint8_t* buf = bufs[bsel];
+    const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
+    const uint32_t base = smem_addr(buf);
+    const uint32_t type = h->type;
+    if (type == ST_OPS) {
+      const uint64_t hh = stage_ops<LT, HASH>(t, buf, sub, nsub);
+      if constexpr (HASH) hacc += hh;
+    } else if (type == ST_LATCH) {
+      uint32_t b, e;
+      chunk_of(h->n, sub, nsub, b, e);
+      if (b < e) {
+        const uint64_t hh = stage_latch<LT, HASH>(t.p0, t.p1, t.p2, t.p3, base + h->off_c, base + h->off_w,
+                                                  base + h->off_k, b, e);
+        if constexpr (HASH) hr += hh;
+      }
+    } else if (type == ST_INJECT) {
+      uint32_t b, e;
+      chunk_of(h->n, sub, nsub, b, e);
+      if (b < e) {
+        const uint64_t c = a.cycle0 + cyc;
+        const uint64_t hh = stage_inject<LT, HASH>(t.p0, t.p1, t.p2, t.p3, base + h->off_c, base + h->off_w,
+                                                   base + h->off_k, h->first, b, e, a.stage, a.g.n_inputs, a.n_lanes,
+                                                   a.seed, a.lane0 + lane, a.staged ? c % a.stage_cap : c, a.staged,
+                                                   lane, valid);
+        if constexpr (HASH) hacc += hh;
+      }
     }
-    hr = latch_range<LT, HASH>(t.p0, t.p1, t.p2, t.p3, a.g.reg_next_coord, a.g.reg_coord, a.g.reg_w, a.g.reg_k, rb, re);
-    uint64_t hin = 0;
-    if (cyc + 1 < a.n_cycles) hin = inject(a.cycle0 + cyc + 1);
-    if constexpr (HASH) red[((cyc & 1) * nsub + sub) * LT + lin] = hacc;
+    const bool eoc = (s + 1 == S);
+    if constexpr (HASH) {
+      if (eoc) {
+        red[((cyc & 1) * nsub + sub) * LT + lin] = hacc + hr_prev;
+        hr_prev = hr;
+        hr = 0;
+        hacc = 0;
+      }
+    }
     __syncthreads();
     if constexpr (HASH) {
-      if (sub == 0 && a.hashes != nullptr) {
+      if (eoc && sub == 0 && a.hashes != nullptr) {
         const uint64_t* rr = red + (cyc & 1) * nsub * LT + lin;
-        uint64_t s = a.g.const_hash;
-        for (uint32_t i = 0; i < nsub; ++i) s += rr[i * LT];
-        if (valid) a.hashes[(size_t)cyc * a.n_lanes + lane] = s;
+        uint64_t sum = a.g.const_hash;
+        for (uint32_t i = 0; i < nsub; ++i) sum += rr[i * LT];
+        if (valid) a.hashes[(size_t)cyc * a.n_lanes + lane] = sum;
       }
-      hacc = hr + hin;
+    }
+    if (eoc) {
+      s = 0;
+      ++cyc;
+    } else {
+      ++s;
     }
   }
   if constexpr (HASH) {
-    // register term of the hash for the next cycle
-    const uint32_t buf = a.n_cycles & 1u;
-    red[(buf * nsub + sub) * LT + lin] = hr;
+    // register term of the hash of the next cycle
+    const uint32_t bb = a.n_cycles & 1u;
+    red[(bb * nsub + sub) * LT + lin] = hr_prev;
     __syncthreads();
-    if (sub == 0) {
-      const uint64_t* rr = red + buf * nsub * LT + lin;
-      uint64_t s = 0;
-      for (uint32_t i = 0; i < nsub; ++i) s += rr[i * LT];
-      if (valid) a.hcarry_out[lane] = s;
+    if (sub == 0 && valid) {
+      const uint64_t* rr = red + bb * nsub * LT + lin;
+      uint64_t sum = 0;
+      for (uint32_t i = 0; i < nsub; ++i) sum += rr[i * LT];
+      a.hcarry_out[lane] = sum;
     }
   }
 }

@@ -58,6 +58,12 @@ struct rs_graph {
   uint32_t* d_sig_coord = nullptr;
   int sm_count = 148;
   int live_lanes = 0;
+  // lane mode stage schedule (compiler.hpp build_stages)
+  void* dstages = nullptr;
+  const uint8_t* stage_blob = nullptr;
+  const StageRef* stage_tab = nullptr;
+  uint32_t n_stages = 0;
+  uint32_t stage_bytes = 0;
 };
 
 struct rs_lanes {
@@ -101,6 +107,10 @@ StepArgs base_args(const rs_lanes* s) {
   a.stage = s->stage;
   a.stage_cap = s->stage_cap;
   a.bar = s->bar;
+  a.stage_blob = s->g->stage_blob;
+  a.stage_tab = s->g->stage_tab;
+  a.n_stages = s->g->n_stages;
+  a.stage_bytes = s->g->stage_bytes;
   return a;
 }
 
@@ -118,6 +128,14 @@ void put(std::vector<uint8_t>& blob, size_t& off, const std::vector<T>& v, size_
     std::memcpy(blob.data() + off, v.data(), bytes_of(v));
   }
   off += bytes_of(v);
+}
+
+// Shared-memory bytes of one stage buffer (two buffers per CTA: the stage in
+// use and the one being prefetched by TMA).
+constexpr uint32_t kStageBytes = 48 * 1024;
+
+size_t lanes_smem(uint32_t stage_bytes, uint32_t threads) {
+  return 128 + 2ull * stage_bytes + 2ull * threads * sizeof(uint64_t);
 }
 
 int choose_lt(uint32_t n_lanes, int sms) {
@@ -212,6 +230,25 @@ rs_status rs_load_graph(const rs_graph_desc* desc, int device, uint32_t mode, rs
   d.const_hash = cg.const_hash;
   g->d_sig_coord = (uint32_t*)P(o_sig);
   cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, device);
+  if (mode == RS_MODE_LANES) {
+    std::vector<uint8_t> sblob;
+    std::vector<StageRef> stab;
+    g->stage_bytes = kStageBytes;
+    build_stages(cg, g->stage_bytes, &sblob, &stab);
+    const size_t tab_off = (sblob.size() + 255) & ~(size_t)255;
+    const size_t nbytes = tab_off + stab.size() * sizeof(StageRef);
+    e = cudaMalloc(&g->dstages, nbytes);
+    if (e == cudaSuccess) e = cudaMemcpy(g->dstages, sblob.data(), sblob.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+      e = cudaMemcpy((uint8_t*)g->dstages + tab_off, stab.data(), stab.size() * sizeof(StageRef), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      rs_free_graph(g);
+      return set_err(RS_E_OOM, "stage schedule (%zu B): %s", nbytes, cudaGetErrorString(e));
+    }
+    g->stage_blob = (const uint8_t*)g->dstages;
+    g->stage_tab = (const StageRef*)((const uint8_t*)g->dstages + tab_off);
+    g->n_stages = (uint32_t)stab.size();
+  }
   *out = g;
   return RS_OK;
 }
@@ -261,9 +298,10 @@ rs_status rs_graph_export(const rs_graph* g, uint32_t what, void* out, uint64_t*
 
 void rs_free_graph(rs_graph* g) {
   if (!g) return;
-  if (g->dmem) {
+  if (g->dmem || g->dstages) {
     cudaSetDevice(g->device);
-    cudaFree(g->dmem);
+    if (g->dmem) cudaFree(g->dmem);
+    if (g->dstages) cudaFree(g->dstages);
   }
   delete g;
 }
@@ -507,15 +545,15 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
     if (hash) s->hc_cur = 1 - s->hc_cur;
   } else {
     a.hcarry_out = a.hcarry_in;
-    const uint32_t nsub = s->threads / s->LT;
-    const size_t smem = hash ? 2ull * nsub * s->LT * 8 : 0;
+    const size_t smem = lanes_smem(s->g->stage_bytes, s->threads);
     const dim3 grid(s->n_tiles), block(s->threads);
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaFuncSetAttribute(k_lanes<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-      cudaFuncSetAttribute(k_lanes<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-      cudaFuncSetAttribute(k_lanes<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-      attr_set = true;
+    static size_t attr_set = 0;
+    if (attr_set < smem) {
+      const void* fns[] = {(const void*)k_lanes<32, true>, (const void*)k_lanes<32, false>,
+                           (const void*)k_lanes<16, true>, (const void*)k_lanes<16, false>,
+                           (const void*)k_lanes<8, true>,  (const void*)k_lanes<8, false>};
+      for (const void* f : fns) CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr_set = smem;
     }
     switch (s->LT * 2 + (hash ? 1 : 0)) {
       case 65: k_lanes<32, true><<<grid, block, smem, s->stream>>>(a); break;
