@@ -1,22 +1,24 @@
 // kernels.cuh -- sm_100a step kernels for the RTeAAL Sim cascade.
 //
-// State layout (SURVEY.md §8(a) "signal-major x lane-minor"): one array per
-// width class c (containers of 2^c bytes), laid out [tile][row][LT]: a
-// lane tile's rows are contiguous and, inside a row, the LT lanes are
-// contiguous, so the gather of one operand for the tile's lanes is one
-// coalesced LT * 2^c byte access (PAPER.md P:1441-1443 names this gather as
-// the CPU kernels' main D-cache-miss source).
+// State layout (SURVEY.md §8(a) "signal-major x lane-minor"): the lanes of an
+// allocation are cut into tiles of LT lanes; a tile owns one contiguous block
+// [class 0 region | class 1 | class 2 | class 3] where class c holds rows of
+// LT containers of 2^c bytes (lane-minor).  The gather of one operand for the
+// tile's lanes is one coalesced LT * 2^c byte access (PAPER.md P:1441-1443
+// names this gather as the CPU kernels' main D-cache-miss source).
 //
-// Lane mode (k_lanes): CTA = one lane tile; the CTA's sub-warps (LT threads
-// each) split every level's ops into contiguous chunks; a sub-warp walks its
-// chunk run by run -- one (opcode, arity) specialisation per run, the NU
-// "switch hoisted out of the op loop" (alg:NU P:1175-1202) -- gathering U
-// ops' operands before computing any (the PSU partial S unrolling,
-// P:1204-1209, used here for memory-level parallelism).  __syncthreads is the
-// level barrier (iterative rank I).
+// Lane mode (k_lanes): CTA = one lane tile.  Every cycle walks a fixed stage
+// schedule (compiler.hpp build_stages); each stage's descriptors are brought
+// into shared memory by a TMA bulk copy issued one stage ahead.  Sub-warps
+// (LT threads) split a stage's ops into contiguous chunks and walk them run by
+// run -- one (opcode, arity) specialisation per run, the NU "switch hoisted out
+// of the op loop" (alg:NU P:1175-1202) -- gathering U ops' operands with
+// branch-free loads before computing any (the PSU partial S unrolling,
+// P:1204-1209, used for memory-level parallelism).  __syncthreads is the level
+// barrier (iterative rank I).
 //
-// Single-lane mode (k_single): one op per thread, all CTAs of a cooperative
-// grid; a grid barrier separates levels.
+// Single-lane mode (k_single): one op per thread over a cooperative grid; a
+// grid barrier separates levels.
 #pragma once
 #include <cstdint>
 
@@ -46,8 +48,11 @@ struct GraphDev {
 
 struct StepArgs {
   GraphDev g;
-  uint8_t* st[4];          // class base pointers
+  uint8_t* state;          // [n_tiles][tile_bytes]
+  uint64_t tile_bytes;
+  uint64_t region[4];      // byte offset of class c's region inside a tile
   uint32_t rows[4];
+  uint32_t LT;
   uint32_t n_lanes;        // lanes in this allocation
   uint64_t lane0;          // global id of lane 0
   uint64_t cycle0;         // absolute cycle of the first stepped cycle
@@ -57,10 +62,10 @@ struct StepArgs {
   const uint64_t* stage;   // [stage_cap][n_inputs][n_lanes]
   uint32_t stage_cap;
   uint64_t* hashes;        // [n_cycles][n_lanes] or nullptr
-  uint64_t* hcarry_in;     // per-lane register-term of the hash for cycle0
+  uint64_t* hcarry_in;     // per-lane register term of the hash for cycle0
   uint64_t* hcarry_out;    // same for cycle0 + n_cycles (may alias hcarry_in in lane mode)
   unsigned long long* bar; // grid barrier counter (single mode)
-  const uint8_t* stage_blob;   // lane mode: per-cycle stage schedule (compiler.hpp)
+  const uint8_t* stage_blob;   // lane mode: this allocation's bound stage schedule
   const StageRef* stage_tab;
   uint32_t n_stages;
   uint32_t stage_bytes;        // shared-memory bytes per stage buffer
@@ -83,21 +88,13 @@ __device__ __forceinline__ uint64_t d_stimulus(uint64_t seed, uint64_t k, uint64
   return d_splitmix_next(x + lane);
 }
 
+// Row-coordinate access ((class << 30) | row): single-lane and aux kernels.
 template <int LT>
 struct TileP {
   uint8_t* p0;
   uint16_t* p1;
   uint32_t* p2;
   uint64_t* p3;
-  __device__ __forceinline__ uint64_t ld(uint32_t c) const {
-    const size_t r = (size_t)(c & ROW_MASK) * LT;
-    switch (c >> 30) {
-      case 0: return p0[r];
-      case 1: return p1[r];
-      case 2: return p2[r];
-      default: return p3[r];
-    }
-  }
   // L2-coherent load (single-lane mode: other SMs write the state)
   __device__ __forceinline__ uint64_t ld_cg(uint32_t c) const {
     const size_t r = (size_t)(c & ROW_MASK) * LT;
@@ -122,15 +119,16 @@ struct TileP {
 
 template <int LT>
 __device__ __forceinline__ TileP<LT> tile_ptrs(const StepArgs& a, uint32_t tile, uint32_t lin) {
+  uint8_t* tb = a.state + (size_t)tile * a.tile_bytes;
   TileP<LT> t;
-  t.p0 = a.st[0] + ((size_t)tile * a.rows[0] * LT + lin);
-  t.p1 = reinterpret_cast<uint16_t*>(a.st[1]) + ((size_t)tile * a.rows[1] * LT + lin);
-  t.p2 = reinterpret_cast<uint32_t*>(a.st[2]) + ((size_t)tile * a.rows[2] * LT + lin);
-  t.p3 = reinterpret_cast<uint64_t*>(a.st[3]) + ((size_t)tile * a.rows[3] * LT + lin);
+  t.p0 = tb + a.region[0] + lin;
+  t.p1 = reinterpret_cast<uint16_t*>(tb + a.region[1]) + lin;
+  t.p2 = reinterpret_cast<uint32_t*>(tb + a.region[2]) + lin;
+  t.p3 = reinterpret_cast<uint64_t*>(tb + a.region[3]) + lin;
   return t;
 }
 
-// op_u / op_r / op_s of Cascade 1 for one op with A operands (A = 0: runtime n).
+// op_u / op_r / op_s of Cascade 1 for one op with A operands.
 // pw: [6:0] w_out [13:7] p0 [19:14] p1 (compiler.hpp pack_pw).
 template <int OP, int A>
 __device__ __forceinline__ uint64_t apply_op(const uint64_t* x, uint32_t pw) {
@@ -187,9 +185,7 @@ __device__ __forceinline__ uint64_t lds64(uint32_t a) {
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
 }
-__device__ __forceinline__ void mbar_fence_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n .reg .pred p;\n"
@@ -203,71 +199,143 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_addr(dst)),
-               "l"(src), "r"(bytes), "r"(smem_addr(bar))
-               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+// Per-thread lane constants for bound coordinates ((class << 30) | byte offset
+// of the row's lane 0 inside the tile; rows are 8-byte aligned).
+struct Lane {
+  uint8_t* tb;     // tile base
+  uint32_t loff;   // byte c = (lin << c) & ~3  (lane byte offset rounded to the 32-bit word)
+  uint32_t sel0;   // PRMT selector extracting this lane's u8 from its word
+  uint32_t sel1;   // ... its u16
+  uint32_t lin;
+};
+
+__device__ __forceinline__ Lane make_lane(uint8_t* tb, uint32_t lin) {
+  Lane L;
+  L.tb = tb;
+  L.lin = lin;
+  L.loff = ((lin & ~3u)) | (((lin << 1) & ~3u) << 8) | ((lin << 2) << 16) | ((lin << 3) << 24);
+  L.sel0 = 0x4440u | (lin & 3u);
+  const uint32_t b = (lin << 1) & 3u;
+  L.sel1 = 0x4400u | ((b + 1u) << 4) | b;
+  return L;
+}
+
+// Branch-free gather of one operand: one 32-bit word (classes 0-2, the lane's
+// bytes picked by PRMT afterwards) or one 64-bit word (class 3), selected by a
+// predicate -- no control flow, so a batch's loads are all in flight together.
+__device__ __forceinline__ uint64_t gather(const Lane& L, uint32_t c) {
+  const uint32_t cls = c >> 30;
+  const uint32_t byte = (c & ROW_MASK) + __byte_perm(L.loff, 0u, cls | 0x4440u);
+  const uint8_t* p = L.tb + byte;
+  uint32_t lo, hi = 0;
+  asm("{\n .reg .pred p3;\n setp.eq.u32 p3, %2, 3;\n"
+      " @p3 ld.global.v2.u32 {%0, %1}, [%3];\n"
+      " @!p3 ld.global.u32 %0, [%3];\n}"
+      : "=r"(lo), "+r"(hi)
+      : "r"(cls), "l"(p));
+  const uint32_t s = (cls >= 2u) ? 0x3210u : (cls ? L.sel1 : L.sel0);
+  return ((uint64_t)hi << 32) | __byte_perm(lo, 0u, s);
+}
+
+// Store to a bound coordinate (class varies per value: latch / inject).
+__device__ __forceinline__ void scatter(const Lane& L, uint32_t c, uint64_t v) {
+  const uint32_t cls = c >> 30;
+  uint8_t* p = L.tb + (c & ROW_MASK) + (L.lin << cls);
+  switch (cls) {
+    case 0: *p = (uint8_t)v; break;
+    case 1: *reinterpret_cast<uint16_t*>(p) = (uint16_t)v; break;
+    case 2: *reinterpret_cast<uint32_t*>(p) = (uint32_t)v; break;
+    default: *reinterpret_cast<uint64_t*>(p) = v; break;
+  }
 }
 
 // One run segment of a stage: n ops of opcode OP, arity A, out class out_cls,
 // descriptors in shared memory (s_c: first coord, s_w: first param word,
-// s_k: first hash weight), outputs in consecutive rows from row0.  U ops'
-// operands are gathered before any is computed (memory-level parallelism).
+// s_k: first hash weight), outputs at consecutive rows from out_byte0.
 template <int LT, bool HASH, int OP, int A>
-__device__ __noinline__ uint64_t run_segment(uint8_t* p0, uint16_t* p1, uint32_t* p2, uint64_t* p3, uint32_t s_c,
-                                             uint32_t s_w, uint32_t s_k, uint32_t out_cls, uint32_t row0,
-                                             uint32_t n) {
+__device__ __noinline__ uint64_t run_segment(uint8_t* tb, uint32_t lin, uint32_t s_c, uint32_t s_w, uint32_t s_k,
+                                             uint32_t out_cls, uint32_t out_byte0, uint32_t n) {
   constexpr int U = (A <= 2) ? 8 : 4;
-  const TileP<LT> t{p0, p1, p2, p3};
+  const Lane L = make_lane(tb, lin);
   uint64_t hacc = 0;
-  for (uint32_t j = 0; j < n; j += U, s_c += 4 * U * A) {
+  uint8_t* ob = tb + out_byte0 + (lin << out_cls);
+  const uint32_t ostride = (uint32_t)LT << out_cls;
+  for (uint32_t j = 0; j < n; j += U, s_c += 4 * U * A, ob += U * ostride) {
     uint64_t x[U][A];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (j + u < n) {
 #pragma unroll
-        for (int o = 0; o < A; ++o) x[u][o] = t.ld(lds32(s_c + 4 * (u * A + o)));
+        for (int o = 0; o < A; ++o) x[u][o] = gather(L, lds32(s_c + 4 * (u * A + o)));
       }
     }
+    uint64_t y[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (j + u < n) {
-        const uint64_t y = apply_op<OP, A>(x[u], lds32(s_w + 4 * (j + u)));
-        t.st(out_cls, row0 + j + u, y);
-        if constexpr (HASH) hacc += y * lds64(s_k + 8 * (j + u));
+        y[u] = apply_op<OP, A>(x[u], lds32(s_w + 4 * (j + u)));
+        if constexpr (HASH) hacc += y[u] * lds64(s_k + 8 * (j + u));
       }
+    }
+    switch (out_cls) {
+      case 0:
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (j + u < n) ob[u * ostride] = (uint8_t)y[u];
+        break;
+      case 1:
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (j + u < n) *reinterpret_cast<uint16_t*>(ob + u * ostride) = (uint16_t)y[u];
+        break;
+      case 2:
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (j + u < n) *reinterpret_cast<uint32_t*>(ob + u * ostride) = (uint32_t)y[u];
+        break;
+      default:
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (j + u < n) *reinterpret_cast<uint64_t*>(ob + u * ostride) = y[u];
+        break;
     }
   }
   return hacc;
 }
 
 template <int LT, bool HASH>
-__device__ __noinline__ uint64_t run_generic(uint8_t* p0, uint16_t* p1, uint32_t* p2, uint64_t* p3, uint32_t s_c,
-                                             uint32_t s_w, uint32_t s_k, uint32_t meta, uint32_t row0, uint32_t n) {
-  const TileP<LT> t{p0, p1, p2, p3};
+__device__ __noinline__ uint64_t run_generic(uint8_t* tb, uint32_t lin, uint32_t s_c, uint32_t s_w, uint32_t s_k,
+                                             uint32_t meta, uint32_t out_byte0, uint32_t n) {
+  const Lane L = make_lane(tb, lin);
   const uint32_t op = meta & 0xffu, ar = (meta >> 8) & 0xffu, out_cls = (meta >> 16) & 3u;
   uint64_t hacc = 0;
   for (uint32_t j = 0; j < n; ++j) {
     const uint32_t c = s_c + 4 * j * ar;
-    uint64_t r = t.ld(lds32(c));
-    for (uint32_t o = 1; o < ar; ++o) r = fold_step(op, r, t.ld(lds32(c + 4 * o)));
+    uint64_t r = gather(L, lds32(c));
+    for (uint32_t o = 1; o < ar; ++o) r = fold_step(op, r, gather(L, lds32(c + 4 * o)));
     const uint64_t y = r & wmask(lds32(s_w + 4 * j) & 127u);
-    t.st(out_cls, row0 + j, y);
+    scatter(L, (out_cls << 30) | (out_byte0 + j * ((uint32_t)LT << out_cls)), y);
     if constexpr (HASH) hacc += y * lds64(s_k + 8 * j);
   }
   return hacc;
 }
 
 template <int LT, bool HASH>
-__device__ __forceinline__ uint64_t dispatch_run(const TileP<LT>& t, uint32_t meta, uint32_t s_c, uint32_t s_w,
-                                                 uint32_t s_k, uint32_t row0, uint32_t n) {
+__device__ __forceinline__ uint64_t dispatch_run(uint8_t* tb, uint32_t lin, uint32_t meta, uint32_t s_c, uint32_t s_w,
+                                                 uint32_t s_k, uint32_t out_byte0, uint32_t n) {
   const uint32_t op = meta & 0xffu, ar = (meta >> 8) & 0xffu, cls = (meta >> 16) & 3u;
-#define RS_SEG(OPC, N) run_segment<LT, HASH, OPC, N>(t.p0, t.p1, t.p2, t.p3, s_c, s_w, s_k, cls, row0, n)
-#define RS_FOLD(OPC)                                                                  \
-  case OPC:                                                                           \
-    if (ar == 2) return RS_SEG(OPC, 2);                                               \
-    if (ar == 3) return RS_SEG(OPC, 3);                                               \
-    return run_generic<LT, HASH>(t.p0, t.p1, t.p2, t.p3, s_c, s_w, s_k, meta, row0, n);
+#define RS_SEG(OPC, N) run_segment<LT, HASH, OPC, N>(tb, lin, s_c, s_w, s_k, cls, out_byte0, n)
+#define RS_FOLD(OPC)                                    \
+  case OPC:                                             \
+    if (ar == 2) return RS_SEG(OPC, 2);                 \
+    if (ar == 3) return RS_SEG(OPC, 3);                 \
+    return run_generic<LT, HASH>(tb, lin, s_c, s_w, s_k, meta, out_byte0, n);
   switch (op) {
     RS_FOLD(RS_OP_AND)
     RS_FOLD(RS_OP_OR)
@@ -297,7 +365,8 @@ __device__ __forceinline__ void chunk_of(uint32_t n, uint32_t part, uint32_t npa
 
 // OPS stage: the sub-warp's contiguous chunk of the stage's ops, run by run.
 template <int LT, bool HASH>
-__device__ __forceinline__ uint64_t stage_ops(const TileP<LT>& t, const uint8_t* buf, uint32_t sub, uint32_t nsub) {
+__device__ __forceinline__ uint64_t stage_ops(uint8_t* tb, uint32_t lin, const uint8_t* buf, uint32_t sub,
+                                              uint32_t nsub) {
   const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
   uint32_t b, e;
   chunk_of(h->n, sub, nsub, b, e);
@@ -313,10 +382,10 @@ __device__ __forceinline__ uint64_t stage_ops(const TileP<LT>& t, const uint8_t*
   for (uint32_t r = lo; b < e; ++r) {
     const StageRun R = runs[r];
     const uint32_t se = min(e, R.op_begin + R.count);
-    const uint32_t ar = (R.meta >> 8) & 0xffu, k = b - R.op_begin;
-    const uint64_t hh = dispatch_run<LT, HASH>(t, R.meta, base + h->off_c + 4 * (R.coord_begin + k * ar),
-                                               base + h->off_w + 4 * b, base + h->off_k + 8 * b, R.out_row0 + k,
-                                               se - b);
+    const uint32_t ar = (R.meta >> 8) & 0xffu, k = b - R.op_begin, cls = (R.meta >> 16) & 3u;
+    const uint64_t hh = dispatch_run<LT, HASH>(tb, lin, R.meta, base + h->off_c + 4 * (R.coord_begin + k * ar),
+                                               base + h->off_w + 4 * b, base + h->off_k + 8 * b,
+                                               R.out_row0 + k * ((uint32_t)LT << cls), se - b);
     if constexpr (HASH) hacc += hh;
     b = se;
   }
@@ -326,21 +395,21 @@ __device__ __forceinline__ uint64_t stage_ops(const TileP<LT>& t, const uint8_t*
 // LATCH stage: tmp = LI[next] & M(w_r); LI[r] = tmp.  One pass is hazard-free
 // because every next row is an op row (compiler identity copies; reading R8).
 template <int LT, bool HASH>
-__device__ __noinline__ uint64_t stage_latch(uint8_t* p0, uint16_t* p1, uint32_t* p2, uint64_t* p3, uint32_t s_c,
-                                             uint32_t s_w, uint32_t s_k, uint32_t b, uint32_t e) {
+__device__ __noinline__ uint64_t stage_latch(uint8_t* tb, uint32_t lin, uint32_t s_c, uint32_t s_w, uint32_t s_k,
+                                             uint32_t b, uint32_t e) {
   constexpr int U = 8;
-  const TileP<LT> t{p0, p1, p2, p3};
+  const Lane L = make_lane(tb, lin);
   uint64_t h = 0;
   for (uint32_t j = b; j < e; j += U) {
     uint64_t v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (j + u < e) v[u] = t.ld(lds32(s_c + 8 * (j + u)));
+      if (j + u < e) v[u] = gather(L, lds32(s_c + 8 * (j + u)));
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (j + u < e) {
         const uint64_t x = v[u] & wmask(lds32(s_w + 4 * (j + u)));
-        t.stc(lds32(s_c + 8 * (j + u) + 4), x);
+        scatter(L, lds32(s_c + 8 * (j + u) + 4), x);
         if constexpr (HASH) h += x * lds64(s_k + 8 * (j + u));
       }
   }
@@ -349,12 +418,12 @@ __device__ __noinline__ uint64_t stage_latch(uint8_t* p0, uint16_t* p1, uint32_t
 
 // INJECT stage: LI[in_k] = stimulus & M(w_k) (or the staged value).
 template <int LT, bool HASH>
-__device__ __noinline__ uint64_t stage_inject(uint8_t* p0, uint16_t* p1, uint32_t* p2, uint64_t* p3, uint32_t s_c,
-                                              uint32_t s_w, uint32_t s_k, uint32_t first, uint32_t b, uint32_t e,
+__device__ __noinline__ uint64_t stage_inject(uint8_t* tb, uint32_t lin, uint32_t s_c, uint32_t s_w, uint32_t s_k,
+                                              uint32_t first, uint32_t b, uint32_t e,
                                               const uint64_t* __restrict__ stage, uint32_t n_inputs,
                                               uint32_t n_lanes, uint64_t seed, uint64_t glane, uint64_t cycle_or_slot,
                                               int staged, uint32_t lane, bool valid) {
-  const TileP<LT> t{p0, p1, p2, p3};
+  const Lane L = make_lane(tb, lin);
   uint64_t h = 0;
   for (uint32_t j = b; j < e; ++j) {
     const uint32_t k = first + j;
@@ -364,7 +433,7 @@ __device__ __noinline__ uint64_t stage_inject(uint8_t* p0, uint16_t* p1, uint32_
     else
       v = d_stimulus(seed, k, cycle_or_slot, glane);
     v &= wmask(lds32(s_w + 4 * j));
-    t.stc(lds32(s_c + 4 * j), v);
+    scatter(L, lds32(s_c + 4 * j), v);
     if constexpr (HASH) h += v * lds64(s_k + 8 * j);
   }
   return h;
@@ -384,7 +453,7 @@ __global__ void __launch_bounds__(1024, 1) k_lanes(const StepArgs a) {
   const uint32_t nsub = blockDim.x >> LTL;
   const uint32_t lane = tile * LT + lin;
   const bool valid = lane < a.n_lanes;
-  const TileP<LT> t = tile_ptrs<LT>(a, tile, lin);
+  uint8_t* tb = a.state + (size_t)tile * a.tile_bytes;
 
   if (threadIdx.x == 0) {
     mbar_init(&mbar[0], 1);
@@ -412,14 +481,13 @@ __global__ void __launch_bounds__(1024, 1) k_lanes(const StepArgs a) {
     const uint32_t base = smem_addr(buf);
     const uint32_t type = h->type;
     if (type == ST_OPS) {
-      const uint64_t hh = stage_ops<LT, HASH>(t, buf, sub, nsub);
+      const uint64_t hh = stage_ops<LT, HASH>(tb, lin, buf, sub, nsub);
       if constexpr (HASH) hacc += hh;
     } else if (type == ST_LATCH) {
       uint32_t b, e;
       chunk_of(h->n, sub, nsub, b, e);
       if (b < e) {
-        const uint64_t hh = stage_latch<LT, HASH>(t.p0, t.p1, t.p2, t.p3, base + h->off_c, base + h->off_w,
-                                                  base + h->off_k, b, e);
+        const uint64_t hh = stage_latch<LT, HASH>(tb, lin, base + h->off_c, base + h->off_w, base + h->off_k, b, e);
         if constexpr (HASH) hr += hh;
       }
     } else if (type == ST_INJECT) {
@@ -427,10 +495,9 @@ __global__ void __launch_bounds__(1024, 1) k_lanes(const StepArgs a) {
       chunk_of(h->n, sub, nsub, b, e);
       if (b < e) {
         const uint64_t c = a.cycle0 + cyc;
-        const uint64_t hh = stage_inject<LT, HASH>(t.p0, t.p1, t.p2, t.p3, base + h->off_c, base + h->off_w,
-                                                   base + h->off_k, h->first, b, e, a.stage, a.g.n_inputs, a.n_lanes,
-                                                   a.seed, a.lane0 + lane, a.staged ? c % a.stage_cap : c, a.staged,
-                                                   lane, valid);
+        const uint64_t hh = stage_inject<LT, HASH>(tb, lin, base + h->off_c, base + h->off_w, base + h->off_k, h->first,
+                                                   b, e, a.stage, a.g.n_inputs, a.n_lanes, a.seed, a.lane0 + lane,
+                                                   a.staged ? c % a.stage_cap : c, a.staged, lane, valid);
         if constexpr (HASH) hacc += hh;
       }
     }
@@ -591,78 +658,70 @@ __global__ void __launch_bounds__(1024, 1) k_single(const StepArgs a) {
 }
 
 // ------------------------------------------------------------------ aux kernels
-// Fill every lane of the given rows with a value (constants, register init).
-__global__ void k_broadcast(StepArgs a, uint32_t LT, uint32_t n_tiles, const uint32_t* coords,
-                            const uint64_t* vals, uint32_t n) {
-  const uint64_t per = (uint64_t)n_tiles * LT;
-  for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < (uint64_t)n * per;
-       idx += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t i = (uint32_t)(idx / per);
-    const uint64_t rem = idx % per;
-    const uint32_t tile = (uint32_t)(rem / LT), lin = (uint32_t)(rem % LT);
-    const uint32_t c = coords[i], cls = c >> 30, row = c & ROW_MASK;
-    const size_t off = ((size_t)tile * a.rows[cls] + row) * LT + lin;
-    const uint64_t v = vals[i];
-    switch (cls) {
-      case 0: a.st[0][off] = (uint8_t)v; break;
-      case 1: reinterpret_cast<uint16_t*>(a.st[1])[off] = (uint16_t)v; break;
-      case 2: reinterpret_cast<uint32_t*>(a.st[2])[off] = (uint32_t)v; break;
-      default: reinterpret_cast<uint64_t*>(a.st[3])[off] = v; break;
-    }
-  }
-}
-
-__device__ __forceinline__ size_t state_off(const StepArgs& a, uint32_t LT, uint32_t c, uint32_t lane) {
+// Row-coordinate addressing for a given lane of the allocation.
+__device__ __forceinline__ uint8_t* row_addr(const StepArgs& a, uint32_t c, uint32_t lane) {
   const uint32_t cls = c >> 30, row = c & ROW_MASK;
-  return ((size_t)(lane / LT) * a.rows[cls] + row) * LT + (lane % LT);
+  const uint32_t tile = lane / a.LT, lin = lane % a.LT;
+  return a.state + (size_t)tile * a.tile_bytes + a.region[cls] + (((size_t)row * a.LT + lin) << cls);
 }
 
-__device__ __forceinline__ uint64_t state_ld(const StepArgs& a, uint32_t c, size_t off) {
-  switch (c >> 30) {
-    case 0: return a.st[0][off];
-    case 1: return reinterpret_cast<const uint16_t*>(a.st[1])[off];
-    case 2: return reinterpret_cast<const uint32_t*>(a.st[2])[off];
-    default: return reinterpret_cast<const uint64_t*>(a.st[3])[off];
+__device__ __forceinline__ uint64_t ld_any(const uint8_t* p, uint32_t cls) {
+  switch (cls) {
+    case 0: return *p;
+    case 1: return *reinterpret_cast<const uint16_t*>(p);
+    case 2: return *reinterpret_cast<const uint32_t*>(p);
+    default: return *reinterpret_cast<const uint64_t*>(p);
   }
 }
 
-__device__ __forceinline__ void state_st(const StepArgs& a, uint32_t c, size_t off, uint64_t v) {
-  switch (c >> 30) {
-    case 0: a.st[0][off] = (uint8_t)v; break;
-    case 1: reinterpret_cast<uint16_t*>(a.st[1])[off] = (uint16_t)v; break;
-    case 2: reinterpret_cast<uint32_t*>(a.st[2])[off] = (uint32_t)v; break;
-    default: reinterpret_cast<uint64_t*>(a.st[3])[off] = v; break;
+__device__ __forceinline__ void st_any(uint8_t* p, uint32_t cls, uint64_t v) {
+  switch (cls) {
+    case 0: *p = (uint8_t)v; break;
+    case 1: *reinterpret_cast<uint16_t*>(p) = (uint16_t)v; break;
+    case 2: *reinterpret_cast<uint32_t*>(p) = (uint32_t)v; break;
+    default: *reinterpret_cast<uint64_t*>(p) = v; break;
+  }
+}
+
+// Fill every lane (padded lanes included) of the given rows with a value
+// (constants, register init).
+__global__ void k_broadcast(StepArgs a, uint32_t n_lanes_pad, const uint32_t* coords, const uint64_t* vals, uint32_t n) {
+  for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < (uint64_t)n * n_lanes_pad;
+       idx += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = (uint32_t)(idx / n_lanes_pad), l = (uint32_t)(idx % n_lanes_pad);
+    const uint32_t c = coords[i];
+    st_any(row_addr(a, c, l), c >> 30, vals[i]);
   }
 }
 
 // out[i][l] = value of coords[i] at lane lane_begin + l (rs_read_signals, step 5)
-__global__ void k_read(StepArgs a, uint32_t LT, const uint32_t* coords, uint32_t n_ids, uint32_t lane_begin,
-                       uint32_t n, uint64_t* out) {
+__global__ void k_read(StepArgs a, const uint32_t* coords, uint32_t n_ids, uint32_t lane_begin, uint32_t n,
+                       uint64_t* out) {
   for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < (uint64_t)n_ids * n;
        idx += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t i = (uint32_t)(idx / n), l = (uint32_t)(idx % n);
     const uint32_t c = coords[i];
-    out[idx] = state_ld(a, c, state_off(a, LT, c, lane_begin + l));
+    out[idx] = ld_any(row_addr(a, c, lane_begin + l), c >> 30);
   }
 }
 
-__global__ void k_write(StepArgs a, uint32_t LT, const uint32_t* coords, const uint32_t* widths, uint32_t n_ids,
-                        uint32_t lane_begin, uint32_t n, const uint64_t* vals) {
+__global__ void k_write(StepArgs a, const uint32_t* coords, const uint32_t* widths, uint32_t n_ids, uint32_t lane_begin,
+                        uint32_t n, const uint64_t* vals) {
   for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < (uint64_t)n_ids * n;
        idx += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t i = (uint32_t)(idx / n), l = (uint32_t)(idx % n);
     const uint32_t c = coords[i];
-    state_st(a, c, state_off(a, LT, c, lane_begin + l), vals[idx] & wmask(widths[i]));
+    st_any(row_addr(a, c, lane_begin + l), c >> 30, vals[idx] & wmask(widths[i]));
   }
 }
 
 // hcarry[l] = sum_r v_r * K_r (register term of the next cycle's hash)
-__global__ void k_reg_hash(StepArgs a, uint32_t LT, uint32_t n_lanes, uint64_t* hcarry) {
+__global__ void k_reg_hash(StepArgs a, uint32_t n_lanes, uint64_t* hcarry) {
   for (uint32_t l = blockIdx.x * blockDim.x + threadIdx.x; l < n_lanes; l += gridDim.x * blockDim.x) {
     uint64_t h = 0;
     for (uint32_t j = 0; j < a.g.n_regs; ++j) {
       const uint32_t c = a.g.reg_coord[j];
-      h += state_ld(a, c, state_off(a, LT, c, l)) * a.g.reg_k[j];
+      h += ld_any(row_addr(a, c, l), c >> 30) * a.g.reg_k[j];
     }
     hcarry[l] = h;
   }

@@ -59,10 +59,9 @@ struct rs_graph {
   int sm_count = 148;
   int live_lanes = 0;
   // lane mode stage schedule (compiler.hpp build_stages)
-  void* dstages = nullptr;
-  const uint8_t* stage_blob = nullptr;
-  const StageRef* stage_tab = nullptr;
-  uint32_t n_stages = 0;
+  // (host copy; every allocation binds it to its own layout, see bind_stages)
+  std::vector<uint8_t> stage_blob;
+  std::vector<StageRef> stage_tab;
   uint32_t stage_bytes = 0;
 };
 
@@ -72,9 +71,14 @@ struct rs_lanes {
   uint64_t lane0 = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  uint8_t* st[4] = {nullptr, nullptr, nullptr, nullptr};
-  void* state_mem = nullptr;
+  void* state_mem = nullptr;       // [n_tiles][tile_bytes]
   size_t state_bytes = 0;
+  uint64_t tile_bytes = 0;
+  uint64_t region[4] = {0, 0, 0, 0};
+  void* dstages = nullptr;         // bound stage schedule: blob, then table
+  const uint8_t* stage_blob = nullptr;
+  const StageRef* stage_tab = nullptr;
+  uint32_t n_stages = 0;
   uint64_t* hcarry = nullptr;       // [2][n_lanes_pad]
   int hc_cur = 0;
   bool hc_valid = true;
@@ -96,10 +100,13 @@ namespace {
 StepArgs base_args(const rs_lanes* s) {
   StepArgs a{};
   a.g = s->g->gd;
+  a.state = (uint8_t*)s->state_mem;
+  a.tile_bytes = s->tile_bytes;
   for (int c = 0; c < 4; ++c) {
-    a.st[c] = s->st[c];
+    a.region[c] = s->region[c];
     a.rows[c] = s->g->cg.rows[c];
   }
+  a.LT = s->LT;
   a.n_lanes = s->n_lanes;
   a.lane0 = s->lane0;
   a.seed = s->seed;
@@ -107,11 +114,35 @@ StepArgs base_args(const rs_lanes* s) {
   a.stage = s->stage;
   a.stage_cap = s->stage_cap;
   a.bar = s->bar;
-  a.stage_blob = s->g->stage_blob;
-  a.stage_tab = s->g->stage_tab;
-  a.n_stages = s->g->n_stages;
+  a.stage_blob = s->stage_blob;
+  a.stage_tab = s->stage_tab;
+  a.n_stages = s->n_stages;
   a.stage_bytes = s->g->stage_bytes;
   return a;
+}
+
+// Bind the graph's stage schedule to one allocation's layout: every state
+// coordinate (class << 30 | row) becomes (class << 30 | byte offset of the
+// row's lane 0 inside a tile); run out rows become byte offsets.  Requires
+// tile_bytes < 2^30.
+void bind_stages(const rs_graph* g, uint32_t LT, const uint64_t* region, std::vector<uint8_t>* out) {
+  *out = g->stage_blob;
+  auto bind = [&](uint32_t c) -> uint32_t {
+    const uint32_t cls = c >> 30, row = c & ROW_MASK;
+    return (cls << 30) | (uint32_t)(region[cls] + ((uint64_t)row * LT << cls));
+  };
+  for (const StageRef& r : g->stage_tab) {
+    uint8_t* p = out->data() + r.off;
+    StageHdr h;
+    std::memcpy(&h, p, sizeof h);
+    uint32_t* c = reinterpret_cast<uint32_t*>(p + h.off_c);
+    for (uint32_t i = 0; i < h.n_coords; ++i) c[i] = bind(c[i]);
+    StageRun* runs = reinterpret_cast<StageRun*>(p + h.off_runs);
+    for (uint32_t i = 0; i < h.n_runs; ++i) {
+      const uint32_t cls = (runs[i].meta >> 16) & 3u;
+      runs[i].out_row0 = bind((cls << 30) | runs[i].out_row0) & ROW_MASK;
+    }
+  }
 }
 
 rs_status set_device(const rs_graph* g) {
@@ -231,23 +262,8 @@ rs_status rs_load_graph(const rs_graph_desc* desc, int device, uint32_t mode, rs
   g->d_sig_coord = (uint32_t*)P(o_sig);
   cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, device);
   if (mode == RS_MODE_LANES) {
-    std::vector<uint8_t> sblob;
-    std::vector<StageRef> stab;
     g->stage_bytes = kStageBytes;
-    build_stages(cg, g->stage_bytes, &sblob, &stab);
-    const size_t tab_off = (sblob.size() + 255) & ~(size_t)255;
-    const size_t nbytes = tab_off + stab.size() * sizeof(StageRef);
-    e = cudaMalloc(&g->dstages, nbytes);
-    if (e == cudaSuccess) e = cudaMemcpy(g->dstages, sblob.data(), sblob.size(), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess)
-      e = cudaMemcpy((uint8_t*)g->dstages + tab_off, stab.data(), stab.size() * sizeof(StageRef), cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) {
-      rs_free_graph(g);
-      return set_err(RS_E_OOM, "stage schedule (%zu B): %s", nbytes, cudaGetErrorString(e));
-    }
-    g->stage_blob = (const uint8_t*)g->dstages;
-    g->stage_tab = (const StageRef*)((const uint8_t*)g->dstages + tab_off);
-    g->n_stages = (uint32_t)stab.size();
+    build_stages(cg, g->stage_bytes, &g->stage_blob, &g->stage_tab);
   }
   *out = g;
   return RS_OK;
@@ -298,10 +314,9 @@ rs_status rs_graph_export(const rs_graph* g, uint32_t what, void* out, uint64_t*
 
 void rs_free_graph(rs_graph* g) {
   if (!g) return;
-  if (g->dmem || g->dstages) {
+  if (g->dmem) {
     cudaSetDevice(g->device);
-    if (g->dmem) cudaFree(g->dmem);
-    if (g->dstages) cudaFree(g->dstages);
+    cudaFree(g->dmem);
   }
   delete g;
 }
@@ -357,20 +372,44 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
   } else {
     s->ctas = s->n_tiles;
   }
-  // state: per class [n_tiles][rows][LT]
-  size_t off = 0, offs[4];
+  // state: [n_tiles][class 0 rows x LT | class 1 | class 2 | class 3], regions 128-B aligned
+  uint64_t off = 0;
   for (int c = 0; c < 4; ++c) {
-    off = (off + 255) & ~(size_t)255;
-    offs[c] = off;
-    off += (size_t)s->n_tiles * g->cg.rows[c] * s->LT * (1u << c);
+    off = (off + 127) & ~(uint64_t)127;
+    s->region[c] = off;
+    off += (uint64_t)g->cg.rows[c] * s->LT * (1u << c);
   }
-  s->state_bytes = std::max<size_t>(off, 256);
+  s->tile_bytes = std::max<uint64_t>((off + 127) & ~(uint64_t)127, 128);
+  if (g->cg.mode == RS_MODE_LANES && s->tile_bytes >= (1ull << 30)) {
+    delete s;
+    return set_err(RS_E_CAPACITY, "a lane tile needs %llu B of state (limit 2^30); use a smaller lane_tile",
+                   (unsigned long long)s->tile_bytes);
+  }
+  s->state_bytes = (size_t)s->tile_bytes * s->n_tiles;
   cudaError_t e;
   if ((e = cudaMalloc(&s->state_mem, s->state_bytes)) != cudaSuccess) {
     delete s;
-    return set_err(RS_E_OOM, "cudaMalloc state (%zu B): %s", (size_t)off, cudaGetErrorString(e));
+    return set_err(RS_E_OOM, "cudaMalloc state (%zu B): %s", s->state_bytes, cudaGetErrorString(e));
   }
-  for (int c = 0; c < 4; ++c) s->st[c] = (uint8_t*)s->state_mem + offs[c];
+  if (g->cg.mode == RS_MODE_LANES) {
+    std::vector<uint8_t> bound;
+    bind_stages(g, s->LT, s->region, &bound);
+    const size_t tab_off = (bound.size() + 255) & ~(size_t)255;
+    const size_t nbytes = tab_off + g->stage_tab.size() * sizeof(StageRef);
+    e = cudaMalloc(&s->dstages, nbytes);
+    if (e == cudaSuccess) e = cudaMemcpy(s->dstages, bound.data(), bound.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+      e = cudaMemcpy((uint8_t*)s->dstages + tab_off, g->stage_tab.data(), g->stage_tab.size() * sizeof(StageRef),
+                     cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      rs_free_lanes(s);
+      return set_err(RS_E_OOM, "stage schedule (%zu B): %s", nbytes, cudaGetErrorString(e));
+    }
+    s->stage_blob = (const uint8_t*)s->dstages;
+    s->stage_tab = (const StageRef*)((const uint8_t*)s->dstages + tab_off);
+    s->n_stages = (uint32_t)g->stage_tab.size();
+    s->total_bytes += nbytes;
+  }
   const size_t lanes_pad = (size_t)s->n_tiles * s->LT;
   if ((e = cudaMalloc(&s->hcarry, 2 * lanes_pad * sizeof(uint64_t))) != cudaSuccess ||
       (e = cudaMalloc(&s->bar, 256)) != cudaSuccess) {
@@ -385,7 +424,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     }
     s->stage_cap = o.stage_cycles;
   }
-  s->total_bytes = s->state_bytes + 2 * lanes_pad * 8 + 256 +
+  s->total_bytes += s->state_bytes + 2 * lanes_pad * 8 + 256 +
                    (size_t)s->stage_cap * std::max<uint32_t>(1, g->cg.n_inputs) * n_lanes * 8;
   if (o.stream) {
     s->stream = (cudaStream_t)o.stream;
@@ -414,7 +453,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
       uint64_t* dv = (uint64_t*)((uint8_t*)tmp + ((nb + 7) & ~(size_t)7));
       cudaMemcpyAsync(dv, vals.data(), vb, cudaMemcpyHostToDevice, s->stream);
       k_broadcast<<<std::min<uint64_t>(4096, (coords.size() * lanes_pad + 255) / 256), 256, 0, s->stream>>>(
-          a, s->LT, s->n_tiles, (const uint32_t*)tmp, dv, (uint32_t)coords.size());
+          a, (uint32_t)lanes_pad, (const uint32_t*)tmp, dv, (uint32_t)coords.size());
       e = cudaStreamSynchronize(s->stream);
       cudaFree(tmp);
       s->launches++;
@@ -438,6 +477,7 @@ void rs_free_lanes(rs_lanes* s) {
   cudaSetDevice(s->g->device);
   if (s->stream) cudaStreamSynchronize(s->stream);
   if (s->state_mem) cudaFree(s->state_mem);
+  if (s->dstages) cudaFree(s->dstages);
   if (s->hcarry) cudaFree(s->hcarry);
   if (s->bar) cudaFree(s->bar);
   if (s->stage) cudaFree(s->stage);
@@ -489,8 +529,8 @@ rs_status rs_set_inputs(rs_lanes* s, uint64_t first_cycle, uint32_t n_cycles, co
 static rs_status refresh_hcarry(rs_lanes* s) {
   if (s->hc_valid) return RS_OK;
   StepArgs a = base_args(s);
-  k_reg_hash<<<std::max<uint32_t>(1, (s->n_lanes + 127) / 128), 128, 0, s->stream>>>(a, s->LT, s->n_lanes,
-                                                                                     s->hcarry + s->hc_cur * (size_t)s->n_tiles * s->LT);
+  k_reg_hash<<<std::max<uint32_t>(1, (s->n_lanes + 127) / 128), 128, 0, s->stream>>>(
+      a, s->n_lanes, s->hcarry + s->hc_cur * (size_t)s->n_tiles * s->LT);
   s->launches++;
   CU(cudaGetLastError());
   s->hc_valid = true;
@@ -596,7 +636,7 @@ rs_status rs_read_signals(rs_lanes* s, const uint32_t* ids, uint32_t n_ids, uint
   cudaError_t e = cudaMemcpyAsync(dco, coords.data(), n_ids * 4, cudaMemcpyHostToDevice, s->stream);
   if (e == cudaSuccess) {
     StepArgs a = base_args(s);
-    k_read<<<(unsigned)std::min<size_t>(8192, (n + 255) / 256), 256, 0, s->stream>>>(a, s->LT, dco, n_ids, lane_begin, n_lanes, dout);
+    k_read<<<(unsigned)std::min<size_t>(8192, (n + 255) / 256), 256, 0, s->stream>>>(a, dco, n_ids, lane_begin, n_lanes, dout);
     s->launches++;
     e = cudaGetLastError();
   }
@@ -630,7 +670,7 @@ rs_status rs_write_registers(rs_lanes* s, const uint32_t* reg_ids, uint32_t n, u
   if (e == cudaSuccess) e = cudaMemcpyAsync(dc, cw.data(), cw.size() * 4, cudaMemcpyHostToDevice, s->stream);
   if (e == cudaSuccess) {
     StepArgs a = base_args(s);
-    k_write<<<(unsigned)std::min<size_t>(8192, (nv + 255) / 256), 256, 0, s->stream>>>(a, s->LT, dc, dc + n, n, lane_begin, n_lanes, dv);
+    k_write<<<(unsigned)std::min<size_t>(8192, (nv + 255) / 256), 256, 0, s->stream>>>(a, dc, dc + n, n, lane_begin, n_lanes, dv);
     s->launches++;
     e = cudaGetLastError();
   }
