@@ -24,6 +24,18 @@
 
 #include "compiler.hpp"
 
+// Build-time tuning knobs (ops gathered per batch for arity <= 2 / 3, and the
+// CTA size the lane kernel's register budget is compiled for).
+#ifndef RS_U2
+#define RS_U2 4
+#endif
+#ifndef RS_U3
+#define RS_U3 2
+#endif
+#ifndef RS_LANES_MAX_THREADS
+#define RS_LANES_MAX_THREADS 1024
+#endif
+
 namespace rtlsim {
 
 struct GraphDev {
@@ -255,33 +267,80 @@ __device__ __forceinline__ void scatter(const Lane& L, uint32_t c, uint64_t v) {
   }
 }
 
-// One run segment of a stage: n ops of opcode OP, arity A, out class out_cls,
+// op_u / op_r / op_s of Cascade 1 for a batch of U ops of one run (same
+// opcode and arity): one uniform switch per batch, the batch's U ops
+// unrolled inside each case; only the opcodes of arity A are instantiated.
+// Per-op parameters come from the param words (compiler.hpp pack_pw).
+template <int U, int A>
+__device__ __forceinline__ void batch_compute(uint32_t op, const uint64_t (&x)[U][A], const uint32_t (&pw)[U],
+                                              uint64_t (&y)[U]) {
+#define RS_EACH(EXPR) _Pragma("unroll") for (int u = 0; u < U; ++u) { y[u] = (EXPR); } break;
+  if constexpr (A == 1) {
+    switch (op) {
+      case RS_OP_NOT: RS_EACH(~x[u][0])
+      case RS_OP_SHL: RS_EACH(((pw[u] >> 7) & 127u) >= 64 ? 0ull : (x[u][0] << ((pw[u] >> 7) & 127u)))
+      case RS_OP_SHR: RS_EACH(((pw[u] >> 7) & 127u) >= 64 ? 0ull : (x[u][0] >> ((pw[u] >> 7) & 127u)))
+      case RS_OP_BITS: RS_EACH((x[u][0] >> ((pw[u] >> 14) & 63u)) &
+                               wmask(((pw[u] >> 7) & 127u) - ((pw[u] >> 14) & 63u) + 1u))
+      default: RS_EACH(x[u][0])  // OP_COPY
+    }
+  } else if constexpr (A == 2) {
+    switch (op) {
+      case RS_OP_AND: RS_EACH(x[u][0] & x[u][1])
+      case RS_OP_OR: RS_EACH(x[u][0] | x[u][1])
+      case RS_OP_XOR: RS_EACH(x[u][0] ^ x[u][1])
+      case RS_OP_ADD: RS_EACH(x[u][0] + x[u][1])
+      case RS_OP_SUB: RS_EACH(x[u][0] - x[u][1])
+      case RS_OP_MUL: RS_EACH(x[u][0] * x[u][1])
+      case RS_OP_EQ: RS_EACH(x[u][0] == x[u][1] ? 1ull : 0ull)
+      case RS_OP_LT: RS_EACH(x[u][0] < x[u][1] ? 1ull : 0ull)
+      default: RS_EACH(((pw[u] >> 7) & 127u) >= 64 ? x[u][1] : ((x[u][0] << ((pw[u] >> 7) & 127u)) | x[u][1]))  // CAT
+    }
+  } else {
+    switch (op) {
+      case RS_OP_AND: RS_EACH(x[u][0] & x[u][1] & x[u][2])
+      case RS_OP_OR: RS_EACH(x[u][0] | x[u][1] | x[u][2])
+      case RS_OP_XOR: RS_EACH(x[u][0] ^ x[u][1] ^ x[u][2])
+      case RS_OP_ADD: RS_EACH(x[u][0] + x[u][1] + x[u][2])
+      case RS_OP_SUB: RS_EACH(x[u][0] - x[u][1] - x[u][2])
+      case RS_OP_MUL: RS_EACH(x[u][0] * x[u][1] * x[u][2])
+      default: RS_EACH(x[u][0] != 0 ? x[u][1] : x[u][2])  // MUX
+    }
+  }
+#undef RS_EACH
+#pragma unroll
+  for (int u = 0; u < U; ++u) y[u] &= wmask(pw[u] & 127u);
+}
+
+// n ops of one run (opcode op, arity A in 1..3, out class out_cls),
 // descriptors in shared memory (s_c: first coord, s_w: first param word,
-// s_k: first hash weight), outputs at consecutive rows from out_byte0.
-template <int LT, bool HASH, int OP, int A>
-__device__ __noinline__ uint64_t run_segment(uint8_t* tb, uint32_t lin, uint32_t s_c, uint32_t s_w, uint32_t s_k,
+// s_k: first hash weight), outputs at consecutive rows from out_byte0.  U
+// ops' operands are gathered with branch-free loads before any is computed
+// (memory-level parallelism).
+template <int LT, bool HASH, int A>
+__device__ __forceinline__ uint64_t seg_loop(const Lane& L, uint32_t op, uint32_t s_c, uint32_t s_w, uint32_t s_k,
                                              uint32_t out_cls, uint32_t out_byte0, uint32_t n) {
-  constexpr int U = (A <= 2) ? 8 : 4;
-  const Lane L = make_lane(tb, lin);
+  constexpr int U = (A <= 2) ? RS_U2 : RS_U3;
   uint64_t hacc = 0;
-  uint8_t* ob = tb + out_byte0 + (lin << out_cls);
+  uint8_t* ob = L.tb + out_byte0 + (L.lin << out_cls);
   const uint32_t ostride = (uint32_t)LT << out_cls;
-  for (uint32_t j = 0; j < n; j += U, s_c += 4 * U * A, ob += U * ostride) {
+#pragma unroll 1
+  for (uint32_t j = 0; j < n; j += U, s_c += 4 * U * A, s_w += 4 * U, s_k += 8 * U, ob += U * ostride) {
     uint64_t x[U][A];
+    uint32_t pw[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      if (j + u < n) {
+      const bool v = j + u < n;
 #pragma unroll
-        for (int o = 0; o < A; ++o) x[u][o] = gather(L, lds32(s_c + 4 * (u * A + o)));
-      }
+      for (int o = 0; o < A; ++o) x[u][o] = v ? gather(L, lds32(s_c + 4 * (u * A + o))) : 0ull;
+      pw[u] = v ? lds32(s_w + 4 * u) : 1u;
     }
     uint64_t y[U];
+    batch_compute<U, A>(op, x, pw, y);
+    if constexpr (HASH) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (j + u < n) {
-        y[u] = apply_op<OP, A>(x[u], lds32(s_w + 4 * (j + u)));
-        if constexpr (HASH) hacc += y[u] * lds64(s_k + 8 * (j + u));
-      }
+      for (int u = 0; u < U; ++u)
+        if (j + u < n) hacc += y[u] * lds64(s_k + 8 * u);
     }
     switch (out_cls) {
       case 0:
@@ -309,15 +368,17 @@ __device__ __noinline__ uint64_t run_segment(uint8_t* tb, uint32_t lin, uint32_t
   return hacc;
 }
 
+// Folds with more than 3 operands (left fold over the O rank; rare).
 template <int LT, bool HASH>
-__device__ __noinline__ uint64_t run_generic(uint8_t* tb, uint32_t lin, uint32_t s_c, uint32_t s_w, uint32_t s_k,
-                                             uint32_t meta, uint32_t out_byte0, uint32_t n) {
-  const Lane L = make_lane(tb, lin);
+__device__ __forceinline__ uint64_t seg_generic(const Lane& L, uint32_t s_c, uint32_t s_w, uint32_t s_k, uint32_t meta,
+                                                uint32_t out_byte0, uint32_t n) {
   const uint32_t op = meta & 0xffu, ar = (meta >> 8) & 0xffu, out_cls = (meta >> 16) & 3u;
   uint64_t hacc = 0;
+#pragma unroll 1
   for (uint32_t j = 0; j < n; ++j) {
     const uint32_t c = s_c + 4 * j * ar;
     uint64_t r = gather(L, lds32(c));
+#pragma unroll 1
     for (uint32_t o = 1; o < ar; ++o) r = fold_step(op, r, gather(L, lds32(c + 4 * o)));
     const uint64_t y = r & wmask(lds32(s_w + 4 * j) & 127u);
     scatter(L, (out_cls << 30) | (out_byte0 + j * ((uint32_t)LT << out_cls)), y);
@@ -326,47 +387,16 @@ __device__ __noinline__ uint64_t run_generic(uint8_t* tb, uint32_t lin, uint32_t
   return hacc;
 }
 
-template <int LT, bool HASH>
-__device__ __forceinline__ uint64_t dispatch_run(uint8_t* tb, uint32_t lin, uint32_t meta, uint32_t s_c, uint32_t s_w,
-                                                 uint32_t s_k, uint32_t out_byte0, uint32_t n) {
-  const uint32_t op = meta & 0xffu, ar = (meta >> 8) & 0xffu, cls = (meta >> 16) & 3u;
-#define RS_SEG(OPC, N) run_segment<LT, HASH, OPC, N>(tb, lin, s_c, s_w, s_k, cls, out_byte0, n)
-#define RS_FOLD(OPC)                                    \
-  case OPC:                                             \
-    if (ar == 2) return RS_SEG(OPC, 2);                 \
-    if (ar == 3) return RS_SEG(OPC, 3);                 \
-    return run_generic<LT, HASH>(tb, lin, s_c, s_w, s_k, meta, out_byte0, n);
-  switch (op) {
-    RS_FOLD(RS_OP_AND)
-    RS_FOLD(RS_OP_OR)
-    RS_FOLD(RS_OP_XOR)
-    RS_FOLD(RS_OP_ADD)
-    RS_FOLD(RS_OP_SUB)
-    RS_FOLD(RS_OP_MUL)
-    case RS_OP_EQ: return RS_SEG(RS_OP_EQ, 2);
-    case RS_OP_LT: return RS_SEG(RS_OP_LT, 2);
-    case RS_OP_CAT: return RS_SEG(RS_OP_CAT, 2);
-    case RS_OP_NOT: return RS_SEG(RS_OP_NOT, 1);
-    case RS_OP_SHL: return RS_SEG(RS_OP_SHL, 1);
-    case RS_OP_SHR: return RS_SEG(RS_OP_SHR, 1);
-    case RS_OP_BITS: return RS_SEG(RS_OP_BITS, 1);
-    case RS_OP_MUX: return RS_SEG(RS_OP_MUX, 3);
-    default: return RS_SEG(OP_COPY, 1);
-  }
-#undef RS_FOLD
-#undef RS_SEG
-}
-
 __device__ __forceinline__ void chunk_of(uint32_t n, uint32_t part, uint32_t nparts, uint32_t& b, uint32_t& e) {
   const uint32_t c = (n + nparts - 1) / nparts;
   b = min(n, part * c);
   e = min(n, b + c);
 }
 
-// OPS stage: the sub-warp's contiguous chunk of the stage's ops, run by run.
+// OPS stage: the sub-warp's contiguous chunk of the stage's ops, run by run
+// (a run fixes arity and out class; the opcode rides in each param word).
 template <int LT, bool HASH>
-__device__ __forceinline__ uint64_t stage_ops(uint8_t* tb, uint32_t lin, const uint8_t* buf, uint32_t sub,
-                                              uint32_t nsub) {
+__device__ __forceinline__ uint64_t stage_ops(const Lane& L, const uint8_t* buf, uint32_t sub, uint32_t nsub) {
   const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
   uint32_t b, e;
   chunk_of(h->n, sub, nsub, b, e);
@@ -379,13 +409,20 @@ __device__ __forceinline__ uint64_t stage_ops(uint8_t* tb, uint32_t lin, const u
     if (runs[mid].op_begin <= b) lo = mid; else hi = mid - 1;
   }
   const uint32_t base = smem_addr(buf);
+#pragma unroll 1
   for (uint32_t r = lo; b < e; ++r) {
     const StageRun R = runs[r];
     const uint32_t se = min(e, R.op_begin + R.count);
     const uint32_t ar = (R.meta >> 8) & 0xffu, k = b - R.op_begin, cls = (R.meta >> 16) & 3u;
-    const uint64_t hh = dispatch_run<LT, HASH>(tb, lin, R.meta, base + h->off_c + 4 * (R.coord_begin + k * ar),
-                                               base + h->off_w + 4 * b, base + h->off_k + 8 * b,
-                                               R.out_row0 + k * ((uint32_t)LT << cls), se - b);
+    const uint32_t s_c = base + h->off_c + 4 * (R.coord_begin + k * ar);
+    const uint32_t s_w = base + h->off_w + 4 * b, s_k = base + h->off_k + 8 * b;
+    const uint32_t ob = R.out_row0 + k * ((uint32_t)LT << cls);
+    uint64_t hh;
+    const uint32_t op = R.meta & 0xffu;
+    if (ar == 2) hh = seg_loop<LT, HASH, 2>(L, op, s_c, s_w, s_k, cls, ob, se - b);
+    else if (ar == 1) hh = seg_loop<LT, HASH, 1>(L, op, s_c, s_w, s_k, cls, ob, se - b);
+    else if (ar == 3) hh = seg_loop<LT, HASH, 3>(L, op, s_c, s_w, s_k, cls, ob, se - b);
+    else hh = seg_generic<LT, HASH>(L, s_c, s_w, s_k, R.meta, ob, se - b);
     if constexpr (HASH) hacc += hh;
     b = se;
   }
@@ -395,11 +432,11 @@ __device__ __forceinline__ uint64_t stage_ops(uint8_t* tb, uint32_t lin, const u
 // LATCH stage: tmp = LI[next] & M(w_r); LI[r] = tmp.  One pass is hazard-free
 // because every next row is an op row (compiler identity copies; reading R8).
 template <int LT, bool HASH>
-__device__ __noinline__ uint64_t stage_latch(uint8_t* tb, uint32_t lin, uint32_t s_c, uint32_t s_w, uint32_t s_k,
-                                             uint32_t b, uint32_t e) {
+__device__ __forceinline__ uint64_t stage_latch(const Lane& L, uint32_t s_c, uint32_t s_w, uint32_t s_k, uint32_t b,
+                                                uint32_t e) {
   constexpr int U = 8;
-  const Lane L = make_lane(tb, lin);
   uint64_t h = 0;
+#pragma unroll 1
   for (uint32_t j = b; j < e; j += U) {
     uint64_t v[U];
 #pragma unroll
@@ -418,13 +455,13 @@ __device__ __noinline__ uint64_t stage_latch(uint8_t* tb, uint32_t lin, uint32_t
 
 // INJECT stage: LI[in_k] = stimulus & M(w_k) (or the staged value).
 template <int LT, bool HASH>
-__device__ __noinline__ uint64_t stage_inject(uint8_t* tb, uint32_t lin, uint32_t s_c, uint32_t s_w, uint32_t s_k,
-                                              uint32_t first, uint32_t b, uint32_t e,
-                                              const uint64_t* __restrict__ stage, uint32_t n_inputs,
-                                              uint32_t n_lanes, uint64_t seed, uint64_t glane, uint64_t cycle_or_slot,
-                                              int staged, uint32_t lane, bool valid) {
-  const Lane L = make_lane(tb, lin);
+__device__ __forceinline__ uint64_t stage_inject(const Lane& L, uint32_t s_c, uint32_t s_w, uint32_t s_k,
+                                                 uint32_t first, uint32_t b, uint32_t e,
+                                                 const uint64_t* __restrict__ stage, uint32_t n_inputs,
+                                                 uint32_t n_lanes, uint64_t seed, uint64_t glane,
+                                                 uint64_t cycle_or_slot, int staged, uint32_t lane, bool valid) {
   uint64_t h = 0;
+#pragma unroll 1
   for (uint32_t j = b; j < e; ++j) {
     const uint32_t k = first + j;
     uint64_t v;
@@ -440,7 +477,7 @@ __device__ __noinline__ uint64_t stage_inject(uint8_t* tb, uint32_t lin, uint32_
 }
 
 template <int LT, bool HASH>
-__global__ void __launch_bounds__(1024, 1) k_lanes(const StepArgs a) {
+__global__ void __launch_bounds__(RS_LANES_MAX_THREADS, 1) k_lanes(const StepArgs a) {
   constexpr int LTL = (LT == 32) ? 5 : (LT == 16) ? 4 : (LT == 8) ? 3 : (LT == 4) ? 2 : (LT == 2) ? 1 : 0;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
@@ -454,6 +491,7 @@ __global__ void __launch_bounds__(1024, 1) k_lanes(const StepArgs a) {
   const uint32_t lane = tile * LT + lin;
   const bool valid = lane < a.n_lanes;
   uint8_t* tb = a.state + (size_t)tile * a.tile_bytes;
+  const Lane L = make_lane(tb, lin);
 
   if (threadIdx.x == 0) {
     mbar_init(&mbar[0], 1);
@@ -481,13 +519,13 @@ __global__ void __launch_bounds__(1024, 1) k_lanes(const StepArgs a) {
     const uint32_t base = smem_addr(buf);
     const uint32_t type = h->type;
     if (type == ST_OPS) {
-      const uint64_t hh = stage_ops<LT, HASH>(tb, lin, buf, sub, nsub);
+      const uint64_t hh = stage_ops<LT, HASH>(L, buf, sub, nsub);
       if constexpr (HASH) hacc += hh;
     } else if (type == ST_LATCH) {
       uint32_t b, e;
       chunk_of(h->n, sub, nsub, b, e);
       if (b < e) {
-        const uint64_t hh = stage_latch<LT, HASH>(tb, lin, base + h->off_c, base + h->off_w, base + h->off_k, b, e);
+        const uint64_t hh = stage_latch<LT, HASH>(L, base + h->off_c, base + h->off_w, base + h->off_k, b, e);
         if constexpr (HASH) hr += hh;
       }
     } else if (type == ST_INJECT) {
@@ -495,7 +533,7 @@ __global__ void __launch_bounds__(1024, 1) k_lanes(const StepArgs a) {
       chunk_of(h->n, sub, nsub, b, e);
       if (b < e) {
         const uint64_t c = a.cycle0 + cyc;
-        const uint64_t hh = stage_inject<LT, HASH>(tb, lin, base + h->off_c, base + h->off_w, base + h->off_k, h->first,
+        const uint64_t hh = stage_inject<LT, HASH>(L, base + h->off_c, base + h->off_w, base + h->off_k, h->first,
                                                    b, e, a.stage, a.g.n_inputs, a.n_lanes, a.seed, a.lane0 + lane,
                                                    a.staged ? c % a.stage_cap : c, a.staged, lane, valid);
         if constexpr (HASH) hacc += hh;

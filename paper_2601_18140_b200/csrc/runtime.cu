@@ -348,13 +348,14 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
   }
   // launch shape
   if (o.threads) {
-    if (o.threads % 32 || o.threads > 1024 || o.threads < s->LT) { delete s; return set_err(RS_E_INVALID_ARG, "threads must be a multiple of 32 in [32, 1024]"); }
+    if (o.threads % 32 || o.threads > (g->cg.mode == RS_MODE_SINGLE ? 1024u : (uint32_t)RS_LANES_MAX_THREADS) ||
+        o.threads < s->LT) { delete s; return set_err(RS_E_INVALID_ARG, "threads must be a multiple of 32 in [32, 1024]"); }
     s->threads = o.threads;
   } else if (g->cg.mode == RS_MODE_SINGLE) {
     s->threads = 1024;
   } else {
     const uint32_t per_sm = (s->n_tiles + g->sm_count - 1) / g->sm_count;
-    uint32_t th = 1024 / std::max<uint32_t>(1, per_sm);
+    uint32_t th = RS_LANES_MAX_THREADS / std::max<uint32_t>(1, per_sm);
     th = std::max<uint32_t>(64, th & ~31u);
     s->threads = th;
   }
@@ -565,6 +566,7 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
     }
     hout = s->hbuf;
   }
+  (void)cudaGetLastError();  // clear a stale non-sticky error of an unrelated earlier call
   StepArgs a = base_args(s);
   a.cycle0 = s->cycle;
   a.n_cycles = n_cycles;

@@ -14,7 +14,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "librtlsim.so")
+LIB_PATH = os.environ.get("RTLSIM_LIB") or os.path.join(_HERE, "lib", "librtlsim.so")
 
 RS_MODE_LANES, RS_MODE_SINGLE = 0, 1
 RS_MEM_NONE, RS_MEM_HOST, RS_MEM_DEVICE = 0, 1, 2
@@ -73,7 +73,8 @@ def lib() -> C.CDLL:
     """Load librtlsim.so (building it first if the sources are newer)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH) or os.environ.get("RTLSIM_AUTOBUILD", "1") == "1":
+        if "RTLSIM_LIB" not in os.environ and (not os.path.exists(LIB_PATH) or
+                                               os.environ.get("RTLSIM_AUTOBUILD", "1") == "1"):
             from . import build as _b
             _b.build()
         L = C.CDLL(LIB_PATH)
