@@ -339,12 +339,14 @@ inline uint32_t al16(uint32_t x) { return (x + 15u) & ~15u; }
 struct StageWriter {
   std::vector<uint8_t>* blob;
   std::vector<StageRef>* table;
-  void emit(StageHdr h, const uint32_t* w, const uint64_t* k, const uint32_t* c, const StageRun* runs) {
+  void emit(StageHdr h, const uint32_t* w, const uint64_t* k, const uint32_t* c, const StageRun* runs,
+            const uint32_t* items = nullptr) {
     h.off_w = al16((uint32_t)sizeof(StageHdr));
     h.off_k = al16(h.off_w + 4 * h.n);
     h.off_c = al16(h.off_k + 8 * h.n);
     h.off_runs = al16(h.off_c + 4 * h.n_coords);
-    h.bytes = al16(h.off_runs + (uint32_t)sizeof(StageRun) * h.n_runs);
+    h.off_items = al16(h.off_runs + (uint32_t)sizeof(StageRun) * h.n_runs);
+    h.bytes = al16(h.off_items + 4 * h.n_items);
     const size_t base = (blob->size() + 15) & ~(size_t)15;
     blob->resize(base + h.bytes, 0);
     uint8_t* p = blob->data() + base;
@@ -355,17 +357,23 @@ struct StageWriter {
     }
     if (h.n_coords) std::memcpy(p + h.off_c, c, 4ull * h.n_coords);
     if (h.n_runs) std::memcpy(p + h.off_runs, runs, sizeof(StageRun) * h.n_runs);
+    if (h.n_items) std::memcpy(p + h.off_items, items, 4ull * h.n_items);
     table->push_back({base, h.bytes, h.type});
   }
 };
 
+// Upper bound of a stage's bytes (OPS items bounded by n / kBatch + n_runs).
 uint32_t stage_size(uint32_t n, uint32_t n_coords, uint32_t n_runs) {
   uint32_t off_w = al16((uint32_t)sizeof(StageHdr));
   uint32_t off_k = al16(off_w + 4 * n);
   uint32_t off_c = al16(off_k + 8 * n);
   uint32_t off_r = al16(off_c + 4 * n_coords);
-  return al16(off_r + (uint32_t)sizeof(StageRun) * n_runs);
+  uint32_t off_i = al16(off_r + (uint32_t)sizeof(StageRun) * n_runs);
+  const uint32_t items = n_runs ? n / kBatch + n_runs : 0;
+  return al16(off_i + 4 * items);
 }
+
+constexpr uint32_t kMaxStageOps = 8191;   // 13-bit op field of a work item
 }  // namespace
 
 void build_stages(const CompiledGraph& g, uint32_t stage_bytes, std::vector<uint8_t>* blob,
@@ -400,7 +408,9 @@ void build_stages(const CompiledGraph& g, uint32_t stage_bytes, std::vector<uint
         while (rr + 1 < g.level_run_begin[l + 1] && g.runs[rr + 1].op_begin <= e) ++rr;
         const bool new_run = (e == j) || (g.runs[rr].op_begin == e);
         const uint32_t ar = g.coord_off[e + 1] - g.coord_off[e];
-        if (stage_size(e - j + 1, ncoords + ar, nruns + (new_run ? 1 : 0)) > stage_bytes && e > j) break;
+        if ((stage_size(e - j + 1, ncoords + ar, nruns + (new_run ? 1 : 0)) > stage_bytes || e - j >= kMaxStageOps) &&
+            e > j)
+          break;
         nruns += new_run ? 1 : 0;
         ncoords += ar;
         ++e;
@@ -420,6 +430,13 @@ void build_stages(const CompiledGraph& g, uint32_t stage_bytes, std::vector<uint
         runs.push_back(sr);
         k = se;
       }
+      // work items: run-aligned batches of <= kBatch ops
+      std::vector<uint32_t> items;
+      for (uint32_t q = 0; q < runs.size(); ++q)
+        for (uint32_t o = 0; o < runs[q].count; o += kBatch) {
+          const uint32_t cnt = std::min(kBatch, runs[q].count - o);
+          items.push_back((q << 16) | ((cnt - 1) << 13) | (runs[q].op_begin + o));
+        }
       StageHdr h{};
       h.type = ST_OPS;
       h.n = e - j;
@@ -427,7 +444,8 @@ void build_stages(const CompiledGraph& g, uint32_t stage_bytes, std::vector<uint
       h.n_coords = g.coord_off[e] - g.coord_off[j];
       h.first = j;
       h.level = l;
-      W.emit(h, &g.opw[j], &g.opk[j], &g.coord[g.coord_off[j]], runs.data());
+      h.n_items = (uint32_t)items.size();
+      W.emit(h, &g.opw[j], &g.opk[j], &g.coord[g.coord_off[j]], runs.data(), items.data());
       j = e;
     }
   }

@@ -125,8 +125,13 @@ struct StageHdr {          // first 64 bytes of a stage block
   uint32_t off_c;          // u32[..]: op operand coords | input coords | (next, reg) coord pairs
   uint32_t off_runs;       // StageRun[n_runs]
   uint32_t bytes;
-  uint32_t pad[5];
+  uint32_t n_items;        // OPS: work items (run-aligned batches of <= kBatch ops)
+  uint32_t off_items;      // u32[n_items]: run << 16 | (count - 1) << 13 | first op (stage-relative)
+  uint32_t pad[3];
 };
+
+// Ops per work item of an OPS stage (the gather batch of the lane kernel).
+constexpr uint32_t kBatch = 4;
 
 struct StageRun {          // a run clipped to the stage; indices relative to the stage
   uint32_t op_begin;

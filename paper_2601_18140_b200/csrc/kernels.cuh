@@ -221,9 +221,7 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
 // of the row's lane 0 inside the tile; rows are 8-byte aligned).
 struct Lane {
   uint8_t* tb;     // tile base
-  uint32_t loff;   // byte c = (lin << c) & ~3  (lane byte offset rounded to the 32-bit word)
-  uint32_t sel0;   // PRMT selector extracting this lane's u8 from its word
-  uint32_t sel1;   // ... its u16
+  uint32_t loff;   // byte c = lin << c: the lane's byte offset inside a class-c row
   uint32_t lin;
 };
 
@@ -231,28 +229,27 @@ __device__ __forceinline__ Lane make_lane(uint8_t* tb, uint32_t lin) {
   Lane L;
   L.tb = tb;
   L.lin = lin;
-  L.loff = ((lin & ~3u)) | (((lin << 1) & ~3u) << 8) | ((lin << 2) << 16) | ((lin << 3) << 24);
-  L.sel0 = 0x4440u | (lin & 3u);
-  const uint32_t b = (lin << 1) & 3u;
-  L.sel1 = 0x4400u | ((b + 1u) << 4) | b;
+  L.loff = lin | ((lin << 1) << 8) | ((lin << 2) << 16) | ((lin << 3) << 24);
   return L;
 }
 
-// Branch-free gather of one operand: one 32-bit word (classes 0-2, the lane's
-// bytes picked by PRMT afterwards) or one 64-bit word (class 3), selected by a
-// predicate -- no control flow, so a batch's loads are all in flight together.
+// Branch-free gather of one operand: four predicated, zero-extending loads
+// (u8 / u16 / u32 / u64) into the same register pair, exactly one of them
+// enabled by the operand's class -- no control flow and nothing to extract
+// afterwards, so all of a batch's loads are in flight together.
 __device__ __forceinline__ uint64_t gather(const Lane& L, uint32_t c) {
   const uint32_t cls = c >> 30;
-  const uint32_t byte = (c & ROW_MASK) + __byte_perm(L.loff, 0u, cls | 0x4440u);
-  const uint8_t* p = L.tb + byte;
+  const uint8_t* p = L.tb + ((c & ROW_MASK) + __byte_perm(L.loff, 0u, cls | 0x4440u));
   uint32_t lo, hi = 0;
-  asm("{\n .reg .pred p3;\n setp.eq.u32 p3, %2, 3;\n"
-      " @p3 ld.global.v2.u32 {%0, %1}, [%3];\n"
-      " @!p3 ld.global.u32 %0, [%3];\n}"
+  asm("{\n .reg .pred q0, q1, q2, q3;\n"
+      " setp.eq.u32 q0, %2, 0;\n setp.eq.u32 q1, %2, 1;\n setp.eq.u32 q2, %2, 2;\n setp.eq.u32 q3, %2, 3;\n"
+      " @q0 ld.global.u8 %0, [%3];\n"
+      " @q1 ld.global.u16 %0, [%3];\n"
+      " @q2 ld.global.u32 %0, [%3];\n"
+      " @q3 ld.global.v2.u32 {%0, %1}, [%3];\n}"
       : "=r"(lo), "+r"(hi)
       : "r"(cls), "l"(p));
-  const uint32_t s = (cls >= 2u) ? 0x3210u : (cls ? L.sel1 : L.sel0);
-  return ((uint64_t)hi << 32) | __byte_perm(lo, 0u, s);
+  return ((uint64_t)hi << 32) | lo;
 }
 
 // Store to a bound coordinate (class varies per value: latch / inject).
@@ -312,58 +309,55 @@ __device__ __forceinline__ void batch_compute(uint32_t op, const uint64_t (&x)[U
   for (int u = 0; u < U; ++u) y[u] &= wmask(pw[u] & 127u);
 }
 
-// n ops of one run (opcode op, arity A in 1..3, out class out_cls),
-// descriptors in shared memory (s_c: first coord, s_w: first param word,
-// s_k: first hash weight), outputs at consecutive rows from out_byte0.  U
-// ops' operands are gathered with branch-free loads before any is computed
-// (memory-level parallelism).
+// One work item: cnt <= U ops of one run (opcode op, arity A in 1..3, out
+// class out_cls), descriptors in shared memory (s_c: first coord, s_w: first
+// param word, s_k: first hash weight), outputs at consecutive rows from
+// out_byte0.  All operands of the batch are gathered (branch-free; tail slots
+// re-read op 0) before any op is computed: memory-level parallelism.
 template <int LT, bool HASH, int A>
-__device__ __forceinline__ uint64_t seg_loop(const Lane& L, uint32_t op, uint32_t s_c, uint32_t s_w, uint32_t s_k,
-                                             uint32_t out_cls, uint32_t out_byte0, uint32_t n) {
-  constexpr int U = (A <= 2) ? RS_U2 : RS_U3;
+__device__ __forceinline__ uint64_t batch_ops(const Lane& L, uint32_t op, uint32_t s_c, uint32_t s_w, uint32_t s_k,
+                                              uint32_t out_cls, uint32_t out_byte0, uint32_t cnt) {
+  constexpr int U = (int)kBatch;
+  uint64_t x[U][A];
+  uint32_t pw[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint32_t uu = (uint32_t)u < cnt ? (uint32_t)u : 0u;
+#pragma unroll
+    for (int o = 0; o < A; ++o) x[u][o] = gather(L, lds32(s_c + 4 * (uu * A + o)));
+    pw[u] = lds32(s_w + 4 * uu);
+  }
+  uint64_t y[U];
+  batch_compute<U, A>(op, x, pw, y);
   uint64_t hacc = 0;
+  if constexpr (HASH) {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if ((uint32_t)u < cnt) hacc += y[u] * lds64(s_k + 8 * u);
+  }
   uint8_t* ob = L.tb + out_byte0 + (L.lin << out_cls);
   const uint32_t ostride = (uint32_t)LT << out_cls;
-#pragma unroll 1
-  for (uint32_t j = 0; j < n; j += U, s_c += 4 * U * A, s_w += 4 * U, s_k += 8 * U, ob += U * ostride) {
-    uint64_t x[U][A];
-    uint32_t pw[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const bool v = j + u < n;
-#pragma unroll
-      for (int o = 0; o < A; ++o) x[u][o] = v ? gather(L, lds32(s_c + 4 * (u * A + o))) : 0ull;
-      pw[u] = v ? lds32(s_w + 4 * u) : 1u;
-    }
-    uint64_t y[U];
-    batch_compute<U, A>(op, x, pw, y);
-    if constexpr (HASH) {
+  switch (out_cls) {
+    case 0:
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (j + u < n) hacc += y[u] * lds64(s_k + 8 * u);
-    }
-    switch (out_cls) {
-      case 0:
+        if ((uint32_t)u < cnt) ob[u * ostride] = (uint8_t)y[u];
+      break;
+    case 1:
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (j + u < n) ob[u * ostride] = (uint8_t)y[u];
-        break;
-      case 1:
+      for (int u = 0; u < U; ++u)
+        if ((uint32_t)u < cnt) *reinterpret_cast<uint16_t*>(ob + u * ostride) = (uint16_t)y[u];
+      break;
+    case 2:
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (j + u < n) *reinterpret_cast<uint16_t*>(ob + u * ostride) = (uint16_t)y[u];
-        break;
-      case 2:
+      for (int u = 0; u < U; ++u)
+        if ((uint32_t)u < cnt) *reinterpret_cast<uint32_t*>(ob + u * ostride) = (uint32_t)y[u];
+      break;
+    default:
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (j + u < n) *reinterpret_cast<uint32_t*>(ob + u * ostride) = (uint32_t)y[u];
-        break;
-      default:
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (j + u < n) *reinterpret_cast<uint64_t*>(ob + u * ostride) = y[u];
-        break;
-    }
+      for (int u = 0; u < U; ++u)
+        if ((uint32_t)u < cnt) *reinterpret_cast<uint64_t*>(ob + u * ostride) = y[u];
+      break;
   }
   return hacc;
 }
@@ -393,38 +387,31 @@ __device__ __forceinline__ void chunk_of(uint32_t n, uint32_t part, uint32_t npa
   e = min(n, b + c);
 }
 
-// OPS stage: the sub-warp's contiguous chunk of the stage's ops, run by run
-// (a run fixes arity and out class; the opcode rides in each param word).
+// OPS stage: the stage's work items (run-aligned batches of <= kBatch ops)
+// dealt round-robin to the sub-warps, so every sub-warp gets an even mix of
+// arities and classes (static balance; no atomics).
 template <int LT, bool HASH>
 __device__ __forceinline__ uint64_t stage_ops(const Lane& L, const uint8_t* buf, uint32_t sub, uint32_t nsub) {
   const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
-  uint32_t b, e;
-  chunk_of(h->n, sub, nsub, b, e);
-  uint64_t hacc = 0;
-  if (b >= e) return 0;
   const StageRun* runs = reinterpret_cast<const StageRun*>(buf + h->off_runs);
-  uint32_t lo = 0, hi = h->n_runs - 1;
-  while (lo < hi) {  // last run with op_begin <= b
-    const uint32_t mid = (lo + hi + 1) >> 1;
-    if (runs[mid].op_begin <= b) lo = mid; else hi = mid - 1;
-  }
-  const uint32_t base = smem_addr(buf);
+  const uint32_t* items = reinterpret_cast<const uint32_t*>(buf + h->off_items);
+  const uint32_t base = smem_addr(buf), n_items = h->n_items;
+  const uint32_t s_c0 = base + h->off_c, s_w0 = base + h->off_w, s_k0 = base + h->off_k;
+  uint64_t hacc = 0;
 #pragma unroll 1
-  for (uint32_t r = lo; b < e; ++r) {
-    const StageRun R = runs[r];
-    const uint32_t se = min(e, R.op_begin + R.count);
-    const uint32_t ar = (R.meta >> 8) & 0xffu, k = b - R.op_begin, cls = (R.meta >> 16) & 3u;
-    const uint32_t s_c = base + h->off_c + 4 * (R.coord_begin + k * ar);
-    const uint32_t s_w = base + h->off_w + 4 * b, s_k = base + h->off_k + 8 * b;
+  for (uint32_t it = sub; it < n_items; it += nsub) {
+    const uint32_t w = items[it];
+    const StageRun R = runs[w >> 16];
+    const uint32_t b = w & 0x1FFFu, cnt = ((w >> 13) & 7u) + 1u;
+    const uint32_t ar = (R.meta >> 8) & 0xffu, k = b - R.op_begin, cls = (R.meta >> 16) & 3u, op = R.meta & 0xffu;
+    const uint32_t s_c = s_c0 + 4 * (R.coord_begin + k * ar);
     const uint32_t ob = R.out_row0 + k * ((uint32_t)LT << cls);
     uint64_t hh;
-    const uint32_t op = R.meta & 0xffu;
-    if (ar == 2) hh = seg_loop<LT, HASH, 2>(L, op, s_c, s_w, s_k, cls, ob, se - b);
-    else if (ar == 1) hh = seg_loop<LT, HASH, 1>(L, op, s_c, s_w, s_k, cls, ob, se - b);
-    else if (ar == 3) hh = seg_loop<LT, HASH, 3>(L, op, s_c, s_w, s_k, cls, ob, se - b);
-    else hh = seg_generic<LT, HASH>(L, s_c, s_w, s_k, R.meta, ob, se - b);
+    if (ar == 2) hh = batch_ops<LT, HASH, 2>(L, op, s_c, s_w0 + 4 * b, s_k0 + 8 * b, cls, ob, cnt);
+    else if (ar == 1) hh = batch_ops<LT, HASH, 1>(L, op, s_c, s_w0 + 4 * b, s_k0 + 8 * b, cls, ob, cnt);
+    else if (ar == 3) hh = batch_ops<LT, HASH, 3>(L, op, s_c, s_w0 + 4 * b, s_k0 + 8 * b, cls, ob, cnt);
+    else hh = seg_generic<LT, HASH>(L, s_c, s_w0 + 4 * b, s_k0 + 8 * b, R.meta, ob, cnt);
     if constexpr (HASH) hacc += hh;
-    b = se;
   }
   return hacc;
 }
