@@ -467,43 +467,51 @@ template <int LT, bool HASH>
 __global__ void __launch_bounds__(RS_LANES_MAX_THREADS, 1) k_lanes(const StepArgs a) {
   constexpr int LTL = (LT == 32) ? 5 : (LT == 16) ? 4 : (LT == 8) ? 3 : (LT == 4) ? 2 : (LT == 2) ? 1 : 0;
   extern __shared__ __align__(128) uint8_t smem[];
+  // shared memory: [mbarriers | stage buffer 0 | stage buffer 1 | red[2][T] | hr[T] | hp[T]]
+  // red: per-thread hash partials of a cycle (double buffered, reduced per lane);
+  // hr / hp: per-thread register terms of the next / current cycle.  Kept in
+  // shared memory, not registers: the hot loop needs every register it has.
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
-  uint8_t* bufs[2] = {smem + 128, smem + 128 + a.stage_bytes};
-  uint64_t* red = reinterpret_cast<uint64_t*>(smem + 128 + 2 * (size_t)a.stage_bytes);  // [2][nsub][LT]
+  const uint32_t T = blockDim.x, tid = threadIdx.x;
+  uint64_t* red = reinterpret_cast<uint64_t*>(smem + 128 + 2 * (size_t)a.stage_bytes);
+  uint64_t* hr_s = red + 2 * T;
+  uint64_t* hp_s = red + 3 * T;
 
-  const uint32_t tile = blockIdx.x;
-  const uint32_t lin = threadIdx.x & (LT - 1);
-  const uint32_t sub = threadIdx.x >> LTL;
-  const uint32_t nsub = blockDim.x >> LTL;
-  const uint32_t lane = tile * LT + lin;
-  const bool valid = lane < a.n_lanes;
-  uint8_t* tb = a.state + (size_t)tile * a.tile_bytes;
-  const Lane L = make_lane(tb, lin);
+  const uint32_t lin = tid & (LT - 1);
+  const uint32_t sub = tid >> LTL;
+  const uint32_t nsub = T >> LTL;
+  const Lane L = make_lane(a.state + (size_t)blockIdx.x * a.tile_bytes, lin);
 
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
     mbar_fence_init();
   }
+  if constexpr (HASH) {
+    const uint32_t lane = blockIdx.x * LT + lin;
+    hr_s[tid] = 0;
+    hp_s[tid] = (sub == 0 && lane < a.n_lanes) ? a.hcarry_in[lane] : 0ull;
+  }
   __syncthreads();
   const uint32_t S = a.n_stages;
-  const uint64_t total = (uint64_t)a.n_cycles * S;
-  auto issue = [&](uint32_t idx, int b) {
-    const StageRef r = a.stage_tab[idx];
-    tma_load_1d(bufs[b], a.stage_blob + r.off, r.bytes, &mbar[b]);
-  };
-  if (threadIdx.x == 0 && total) issue(0, 0);
+  const uint32_t total = a.n_cycles * S;  // host keeps n_cycles * S < 2^31
+  if (tid == 0 && total) {
+    const StageRef r = a.stage_tab[0];
+    tma_load_1d(smem + 128, a.stage_blob + r.off, r.bytes, &mbar[0]);
+  }
 
-  uint64_t hacc = 0, hr = 0;
-  uint64_t hr_prev = (HASH && sub == 0 && valid) ? a.hcarry_in[lane] : 0ull;
+  uint64_t hacc = 0;
   uint32_t s = 0, cyc = 0;
-  for (uint64_t gi = 0; gi < total; ++gi) {
-    const int bsel = (int)(gi & 1);
-    if (threadIdx.x == 0 && gi + 1 < total) issue(s + 1 == S ? 0 : s + 1, bsel ^ 1);
-    mbar_wait(&mbar[bsel], (uint32_t)((gi >> 1) & 1));
-    const uint8_t* buf = bufs[bsel];
+#pragma unroll 1
+  for (uint32_t gi = 0; gi < total; ++gi) {
+    const uint32_t bsel = gi & 1u;
+    if (tid == 0 && gi + 1 < total) {
+      const StageRef r = a.stage_tab[s + 1 == S ? 0 : s + 1];
+      tma_load_1d(smem + 128 + (bsel ^ 1u) * a.stage_bytes, a.stage_blob + r.off, r.bytes, &mbar[bsel ^ 1u]);
+    }
+    mbar_wait(&mbar[bsel], (gi >> 1) & 1u);
+    const uint8_t* buf = smem + 128 + bsel * a.stage_bytes;
     const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
-    const uint32_t base = smem_addr(buf);
     const uint32_t type = h->type;
     if (type == ST_OPS) {
       const uint64_t hh = stage_ops<LT, HASH>(L, buf, sub, nsub);
@@ -512,36 +520,40 @@ __global__ void __launch_bounds__(RS_LANES_MAX_THREADS, 1) k_lanes(const StepArg
       uint32_t b, e;
       chunk_of(h->n, sub, nsub, b, e);
       if (b < e) {
+        const uint32_t base = smem_addr(buf);
         const uint64_t hh = stage_latch<LT, HASH>(L, base + h->off_c, base + h->off_w, base + h->off_k, b, e);
-        if constexpr (HASH) hr += hh;
+        if constexpr (HASH) hr_s[tid] += hh;
       }
     } else if (type == ST_INJECT) {
       uint32_t b, e;
       chunk_of(h->n, sub, nsub, b, e);
       if (b < e) {
+        const uint32_t base = smem_addr(buf), lane = blockIdx.x * LT + lin;
         const uint64_t c = a.cycle0 + cyc;
         const uint64_t hh = stage_inject<LT, HASH>(L, base + h->off_c, base + h->off_w, base + h->off_k, h->first,
                                                    b, e, a.stage, a.g.n_inputs, a.n_lanes, a.seed, a.lane0 + lane,
-                                                   a.staged ? c % a.stage_cap : c, a.staged, lane, valid);
+                                                   a.staged ? c % a.stage_cap : c, a.staged, lane, lane < a.n_lanes);
         if constexpr (HASH) hacc += hh;
       }
     }
     const bool eoc = (s + 1 == S);
     if constexpr (HASH) {
       if (eoc) {
-        red[((cyc & 1) * nsub + sub) * LT + lin] = hacc + hr_prev;
-        hr_prev = hr;
-        hr = 0;
+        red[(cyc & 1u) * T + tid] = hacc + hp_s[tid];
+        hp_s[tid] = hr_s[tid];
+        hr_s[tid] = 0;
         hacc = 0;
       }
     }
     __syncthreads();
     if constexpr (HASH) {
-      if (eoc && sub == 0 && a.hashes != nullptr) {
-        const uint64_t* rr = red + (cyc & 1) * nsub * LT + lin;
+      const uint32_t lane = blockIdx.x * LT + lin;
+      if (eoc && sub == 0 && a.hashes != nullptr && lane < a.n_lanes) {
+        const uint64_t* rr = red + (cyc & 1u) * T + lin;
         uint64_t sum = a.g.const_hash;
+#pragma unroll 4
         for (uint32_t i = 0; i < nsub; ++i) sum += rr[i * LT];
-        if (valid) a.hashes[(size_t)cyc * a.n_lanes + lane] = sum;
+        a.hashes[(size_t)cyc * a.n_lanes + lane] = sum;
       }
     }
     if (eoc) {
@@ -552,14 +564,12 @@ __global__ void __launch_bounds__(RS_LANES_MAX_THREADS, 1) k_lanes(const StepArg
     }
   }
   if constexpr (HASH) {
-    // register term of the hash of the next cycle
-    const uint32_t bb = a.n_cycles & 1u;
-    red[(bb * nsub + sub) * LT + lin] = hr_prev;
+    // register term of the hash of the next cycle (hp_s holds the last commit's partials)
     __syncthreads();
-    if (sub == 0 && valid) {
-      const uint64_t* rr = red + bb * nsub * LT + lin;
+    const uint32_t lane = blockIdx.x * LT + lin;
+    if (sub == 0 && lane < a.n_lanes) {
       uint64_t sum = 0;
-      for (uint32_t i = 0; i < nsub; ++i) sum += rr[i * LT];
+      for (uint32_t i = 0; i < nsub; ++i) sum += hp_s[i * LT + lin];
       a.hcarry_out[lane] = sum;
     }
   }

@@ -166,7 +166,7 @@ void put(std::vector<uint8_t>& blob, size_t& off, const std::vector<T>& v, size_
 constexpr uint32_t kStageBytes = 48 * 1024;
 
 size_t lanes_smem(uint32_t stage_bytes, uint32_t threads) {
-  return 128 + 2ull * stage_bytes + 2ull * threads * sizeof(uint64_t);
+  return 128 + 2ull * stage_bytes + 4ull * threads * sizeof(uint64_t);
 }
 
 int choose_lt(uint32_t n_lanes, int sms) {
@@ -544,6 +544,17 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
     return set_err(RS_E_INVALID_ARG, "bad hashes_mem %d", hashes_mem);
   if (hashes_mem != RS_MEM_NONE && !hashes && n_cycles) return set_err(RS_E_INVALID_ARG, "NULL hashes");
   if (n_cycles == 0) return RS_OK;
+  if (s->g->cg.mode == RS_MODE_LANES && (uint64_t)n_cycles * s->n_stages >= (1ull << 31)) {
+    // the kernel counts stages in 32 bits: split very long runs
+    const uint32_t chunk = (uint32_t)((1ull << 31) / s->n_stages) - 1;
+    for (uint32_t done = 0; done < n_cycles;) {
+      const uint32_t n = std::min(chunk, n_cycles - done);
+      rs_status st = rs_step_cycles(s, n, hashes ? hashes + (size_t)done * s->n_lanes : nullptr, hashes_mem);
+      if (st != RS_OK) return st;
+      done += n;
+    }
+    return RS_OK;
+  }
   if (s->staged && (s->cycle < s->st_lo || s->cycle + n_cycles > s->st_hi))
     return set_err(RS_E_STATE, "cycles [%llu, %llu) are not staged (window [%llu, %llu))",
                    (unsigned long long)s->cycle, (unsigned long long)(s->cycle + n_cycles),
