@@ -221,7 +221,8 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
 // of the row's lane 0 inside the tile; rows are 8-byte aligned).
 struct Lane {
   uint8_t* tb;     // tile base
-  uint32_t loff;   // byte c = lin << c: the lane's byte offset inside a class-c row
+  uint32_t off8;   // byte c = (lin << c) & ~7: the lane's container's 8-byte word inside a class-c row
+  uint32_t sh8;    // byte c = ((lin << c) & 7) * 8: bit offset of the container inside that word
   uint32_t lin;
 };
 
@@ -229,28 +230,31 @@ __device__ __forceinline__ Lane make_lane(uint8_t* tb, uint32_t lin) {
   Lane L;
   L.tb = tb;
   L.lin = lin;
-  L.loff = lin | ((lin << 1) << 8) | ((lin << 2) << 16) | ((lin << 3) << 24);
+  L.off8 = (lin & ~7u) | (((lin << 1) & ~7u) << 8) | (((lin << 2) & ~7u) << 16) | (((lin << 3) & ~7u) << 24);
+  L.sh8 = ((lin & 7u) << 3) | ((((lin << 1) & 7u) << 3) << 8) | ((((lin << 2) & 7u) << 3) << 16);
   return L;
 }
 
-// Branch-free gather of one operand: four predicated, zero-extending loads
-// (u8 / u16 / u32 / u64) into the same register pair, exactly one of them
-// enabled by the operand's class -- no control flow and nothing to extract
-// afterwards, so all of a batch's loads are in flight together.
-__device__ __forceinline__ uint64_t gather(const Lane& L, uint32_t c) {
+// Gather, part 1: one aligned 64-bit load per operand -- the word that holds
+// this lane's container, whatever the class -- so a batch issues exactly one
+// load per operand, with no branches and no register reused between loads.
+__device__ __forceinline__ uint64_t gather_raw(const Lane& L, uint32_t c) {
   const uint32_t cls = c >> 30;
-  const uint8_t* p = L.tb + ((c & ROW_MASK) + __byte_perm(L.loff, 0u, cls | 0x4440u));
-  uint32_t lo, hi = 0;
-  asm("{\n .reg .pred q0, q1, q2, q3;\n"
-      " setp.eq.u32 q0, %2, 0;\n setp.eq.u32 q1, %2, 1;\n setp.eq.u32 q2, %2, 2;\n setp.eq.u32 q3, %2, 3;\n"
-      " @q0 ld.global.u8 %0, [%3];\n"
-      " @q1 ld.global.u16 %0, [%3];\n"
-      " @q2 ld.global.u32 %0, [%3];\n"
-      " @q3 ld.global.v2.u32 {%0, %1}, [%3];\n}"
-      : "=r"(lo), "+r"(hi)
-      : "r"(cls), "l"(p));
-  return ((uint64_t)hi << 32) | lo;
+  const uint8_t* p = L.tb + ((c & ROW_MASK) + __byte_perm(L.off8, 0u, cls | 0x4440u));
+  return *reinterpret_cast<const uint64_t*>(p);
 }
+
+// Gather, part 2 (after every load of the batch is in flight): shift the
+// lane's container down and mask it to its class width.
+__device__ __forceinline__ uint64_t gather_fix(const Lane& L, uint32_t c, uint64_t w) {
+  const uint32_t cls = c >> 30;
+  const uint32_t sh = __byte_perm(L.sh8, 0u, cls | 0x4440u);
+  const uint64_t v = w >> sh;
+  const uint32_t m32 = 0xFFFFFFFFu >> (32u - (8u << min(cls, 2u)));
+  return cls == 3u ? w : (uint64_t)((uint32_t)v & m32);
+}
+
+__device__ __forceinline__ uint64_t gather(const Lane& L, uint32_t c) { return gather_fix(L, c, gather_raw(L, c)); }
 
 // Store to a bound coordinate (class varies per value: latch / inject).
 __device__ __forceinline__ void scatter(const Lane& L, uint32_t c, uint64_t v) {
@@ -319,14 +323,22 @@ __device__ __forceinline__ uint64_t batch_ops(const Lane& L, uint32_t op, uint32
                                               uint32_t out_cls, uint32_t out_byte0, uint32_t cnt) {
   constexpr int U = (int)kBatch;
   uint64_t x[U][A];
+  uint32_t cc[U][A];
   uint32_t pw[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const uint32_t uu = (uint32_t)u < cnt ? (uint32_t)u : 0u;
 #pragma unroll
-    for (int o = 0; o < A; ++o) x[u][o] = gather(L, lds32(s_c + 4 * (uu * A + o)));
+    for (int o = 0; o < A; ++o) {
+      cc[u][o] = lds32(s_c + 4 * (uu * A + o));
+      x[u][o] = gather_raw(L, cc[u][o]);
+    }
     pw[u] = lds32(s_w + 4 * uu);
   }
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int o = 0; o < A; ++o) x[u][o] = gather_fix(L, cc[u][o], x[u][o]);
   uint64_t y[U];
   batch_compute<U, A>(op, x, pw, y);
   uint64_t hacc = 0;
@@ -426,13 +438,16 @@ __device__ __forceinline__ uint64_t stage_latch(const Lane& L, uint32_t s_c, uin
 #pragma unroll 1
   for (uint32_t j = b; j < e; j += U) {
     uint64_t v[U];
+    uint32_t cc[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (j + u < e) v[u] = gather(L, lds32(s_c + 8 * (j + u)));
+    for (int u = 0; u < U; ++u) {
+      cc[u] = lds32(s_c + 8 * min(j + u, e - 1));
+      v[u] = gather_raw(L, cc[u]);
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (j + u < e) {
-        const uint64_t x = v[u] & wmask(lds32(s_w + 4 * (j + u)));
+        const uint64_t x = gather_fix(L, cc[u], v[u]) & wmask(lds32(s_w + 4 * (j + u)));
         scatter(L, lds32(s_c + 8 * (j + u) + 4), x);
         if constexpr (HASH) h += x * lds64(s_k + 8 * (j + u));
       }
