@@ -26,14 +26,8 @@
 
 // Build-time tuning knobs (ops gathered per batch for arity <= 2 / 3, and the
 // CTA size the lane kernel's register budget is compiled for).
-#ifndef RS_U2
-#define RS_U2 4
-#endif
-#ifndef RS_U3
-#define RS_U3 2
-#endif
 #ifndef RS_LANES_MAX_THREADS
-#define RS_LANES_MAX_THREADS 1024
+#define RS_LANES_MAX_THREADS 512
 #endif
 
 namespace rtlsim {
@@ -215,379 +209,6 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(dst)),
       "l"(src), "r"(bytes), "r"(smem_addr(bar))
       : "memory");
-}
-
-// Per-thread lane constants for bound coordinates ((class << 30) | byte offset
-// of the row's lane 0 inside the tile; rows are 8-byte aligned).
-struct Lane {
-  uint8_t* tb;     // tile base
-  uint32_t off8;   // byte c = (lin << c) & ~7: the lane's container's 8-byte word inside a class-c row
-  uint32_t sh8;    // byte c = ((lin << c) & 7) * 8: bit offset of the container inside that word
-  uint32_t lin;
-};
-
-__device__ __forceinline__ Lane make_lane(uint8_t* tb, uint32_t lin) {
-  Lane L;
-  L.tb = tb;
-  L.lin = lin;
-  L.off8 = (lin & ~7u) | (((lin << 1) & ~7u) << 8) | (((lin << 2) & ~7u) << 16) | (((lin << 3) & ~7u) << 24);
-  L.sh8 = ((lin & 7u) << 3) | ((((lin << 1) & 7u) << 3) << 8) | ((((lin << 2) & 7u) << 3) << 16);
-  return L;
-}
-
-// Gather, part 1: one aligned 64-bit load per operand -- the word that holds
-// this lane's container, whatever the class -- so a batch issues exactly one
-// load per operand, with no branches and no register reused between loads.
-__device__ __forceinline__ uint64_t gather_raw(const Lane& L, uint32_t c) {
-  const uint32_t cls = c >> 30;
-  const uint8_t* p = L.tb + ((c & ROW_MASK) + __byte_perm(L.off8, 0u, cls | 0x4440u));
-  return *reinterpret_cast<const uint64_t*>(p);
-}
-
-// Gather, part 2 (after every load of the batch is in flight): shift the
-// lane's container down and mask it to its class width.
-__device__ __forceinline__ uint64_t gather_fix(const Lane& L, uint32_t c, uint64_t w) {
-  const uint32_t cls = c >> 30;
-  const uint32_t sh = __byte_perm(L.sh8, 0u, cls | 0x4440u);
-  const uint64_t v = w >> sh;
-  const uint32_t m32 = 0xFFFFFFFFu >> (32u - (8u << min(cls, 2u)));
-  return cls == 3u ? w : (uint64_t)((uint32_t)v & m32);
-}
-
-__device__ __forceinline__ uint64_t gather(const Lane& L, uint32_t c) { return gather_fix(L, c, gather_raw(L, c)); }
-
-// Store to a bound coordinate (class varies per value: latch / inject).
-__device__ __forceinline__ void scatter(const Lane& L, uint32_t c, uint64_t v) {
-  const uint32_t cls = c >> 30;
-  uint8_t* p = L.tb + (c & ROW_MASK) + (L.lin << cls);
-  switch (cls) {
-    case 0: *p = (uint8_t)v; break;
-    case 1: *reinterpret_cast<uint16_t*>(p) = (uint16_t)v; break;
-    case 2: *reinterpret_cast<uint32_t*>(p) = (uint32_t)v; break;
-    default: *reinterpret_cast<uint64_t*>(p) = v; break;
-  }
-}
-
-// op_u / op_r / op_s of Cascade 1 for a batch of U ops of one run (same
-// opcode and arity): one uniform switch per batch, the batch's U ops
-// unrolled inside each case; only the opcodes of arity A are instantiated.
-// Per-op parameters come from the param words (compiler.hpp pack_pw).
-template <int U, int A>
-__device__ __forceinline__ void batch_compute(uint32_t op, const uint64_t (&x)[U][A], const uint32_t (&pw)[U],
-                                              uint64_t (&y)[U]) {
-#define RS_EACH(EXPR) _Pragma("unroll") for (int u = 0; u < U; ++u) { y[u] = (EXPR); } break;
-  if constexpr (A == 1) {
-    switch (op) {
-      case RS_OP_NOT: RS_EACH(~x[u][0])
-      case RS_OP_SHL: RS_EACH(((pw[u] >> 7) & 127u) >= 64 ? 0ull : (x[u][0] << ((pw[u] >> 7) & 127u)))
-      case RS_OP_SHR: RS_EACH(((pw[u] >> 7) & 127u) >= 64 ? 0ull : (x[u][0] >> ((pw[u] >> 7) & 127u)))
-      case RS_OP_BITS: RS_EACH((x[u][0] >> ((pw[u] >> 14) & 63u)) &
-                               wmask(((pw[u] >> 7) & 127u) - ((pw[u] >> 14) & 63u) + 1u))
-      default: RS_EACH(x[u][0])  // OP_COPY
-    }
-  } else if constexpr (A == 2) {
-    switch (op) {
-      case RS_OP_AND: RS_EACH(x[u][0] & x[u][1])
-      case RS_OP_OR: RS_EACH(x[u][0] | x[u][1])
-      case RS_OP_XOR: RS_EACH(x[u][0] ^ x[u][1])
-      case RS_OP_ADD: RS_EACH(x[u][0] + x[u][1])
-      case RS_OP_SUB: RS_EACH(x[u][0] - x[u][1])
-      case RS_OP_MUL: RS_EACH(x[u][0] * x[u][1])
-      case RS_OP_EQ: RS_EACH(x[u][0] == x[u][1] ? 1ull : 0ull)
-      case RS_OP_LT: RS_EACH(x[u][0] < x[u][1] ? 1ull : 0ull)
-      default: RS_EACH(((pw[u] >> 7) & 127u) >= 64 ? x[u][1] : ((x[u][0] << ((pw[u] >> 7) & 127u)) | x[u][1]))  // CAT
-    }
-  } else {
-    switch (op) {
-      case RS_OP_AND: RS_EACH(x[u][0] & x[u][1] & x[u][2])
-      case RS_OP_OR: RS_EACH(x[u][0] | x[u][1] | x[u][2])
-      case RS_OP_XOR: RS_EACH(x[u][0] ^ x[u][1] ^ x[u][2])
-      case RS_OP_ADD: RS_EACH(x[u][0] + x[u][1] + x[u][2])
-      case RS_OP_SUB: RS_EACH(x[u][0] - x[u][1] - x[u][2])
-      case RS_OP_MUL: RS_EACH(x[u][0] * x[u][1] * x[u][2])
-      default: RS_EACH(x[u][0] != 0 ? x[u][1] : x[u][2])  // MUX
-    }
-  }
-#undef RS_EACH
-#pragma unroll
-  for (int u = 0; u < U; ++u) y[u] &= wmask(pw[u] & 127u);
-}
-
-// One work item: cnt <= U ops of one run (opcode op, arity A in 1..3, out
-// class out_cls), descriptors in shared memory (s_c: first coord, s_w: first
-// param word, s_k: first hash weight), outputs at consecutive rows from
-// out_byte0.  All operands of the batch are gathered (branch-free; tail slots
-// re-read op 0) before any op is computed: memory-level parallelism.
-template <int LT, bool HASH, int A>
-__device__ __forceinline__ uint64_t batch_ops(const Lane& L, uint32_t op, uint32_t s_c, uint32_t s_w, uint32_t s_k,
-                                              uint32_t out_cls, uint32_t out_byte0, uint32_t cnt) {
-  constexpr int U = (int)kBatch;
-  uint64_t x[U][A];
-  uint32_t cc[U][A];
-  uint32_t pw[U];
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const uint32_t uu = (uint32_t)u < cnt ? (uint32_t)u : 0u;
-#pragma unroll
-    for (int o = 0; o < A; ++o) {
-      cc[u][o] = lds32(s_c + 4 * (uu * A + o));
-      x[u][o] = gather_raw(L, cc[u][o]);
-    }
-    pw[u] = lds32(s_w + 4 * uu);
-  }
-#pragma unroll
-  for (int u = 0; u < U; ++u)
-#pragma unroll
-    for (int o = 0; o < A; ++o) x[u][o] = gather_fix(L, cc[u][o], x[u][o]);
-  uint64_t y[U];
-  batch_compute<U, A>(op, x, pw, y);
-  uint64_t hacc = 0;
-  if constexpr (HASH) {
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if ((uint32_t)u < cnt) hacc += y[u] * lds64(s_k + 8 * u);
-  }
-  uint8_t* ob = L.tb + out_byte0 + (L.lin << out_cls);
-  const uint32_t ostride = (uint32_t)LT << out_cls;
-  switch (out_cls) {
-    case 0:
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if ((uint32_t)u < cnt) ob[u * ostride] = (uint8_t)y[u];
-      break;
-    case 1:
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if ((uint32_t)u < cnt) *reinterpret_cast<uint16_t*>(ob + u * ostride) = (uint16_t)y[u];
-      break;
-    case 2:
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if ((uint32_t)u < cnt) *reinterpret_cast<uint32_t*>(ob + u * ostride) = (uint32_t)y[u];
-      break;
-    default:
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if ((uint32_t)u < cnt) *reinterpret_cast<uint64_t*>(ob + u * ostride) = y[u];
-      break;
-  }
-  return hacc;
-}
-
-// Folds with more than 3 operands (left fold over the O rank; rare).
-template <int LT, bool HASH>
-__device__ __forceinline__ uint64_t seg_generic(const Lane& L, uint32_t s_c, uint32_t s_w, uint32_t s_k, uint32_t meta,
-                                                uint32_t out_byte0, uint32_t n) {
-  const uint32_t op = meta & 0xffu, ar = (meta >> 8) & 0xffu, out_cls = (meta >> 16) & 3u;
-  uint64_t hacc = 0;
-#pragma unroll 1
-  for (uint32_t j = 0; j < n; ++j) {
-    const uint32_t c = s_c + 4 * j * ar;
-    uint64_t r = gather(L, lds32(c));
-#pragma unroll 1
-    for (uint32_t o = 1; o < ar; ++o) r = fold_step(op, r, gather(L, lds32(c + 4 * o)));
-    const uint64_t y = r & wmask(lds32(s_w + 4 * j) & 127u);
-    scatter(L, (out_cls << 30) | (out_byte0 + j * ((uint32_t)LT << out_cls)), y);
-    if constexpr (HASH) hacc += y * lds64(s_k + 8 * j);
-  }
-  return hacc;
-}
-
-__device__ __forceinline__ void chunk_of(uint32_t n, uint32_t part, uint32_t nparts, uint32_t& b, uint32_t& e) {
-  const uint32_t c = (n + nparts - 1) / nparts;
-  b = min(n, part * c);
-  e = min(n, b + c);
-}
-
-// OPS stage: the stage's work items (run-aligned batches of <= kBatch ops)
-// dealt round-robin to the sub-warps, so every sub-warp gets an even mix of
-// arities and classes (static balance; no atomics).
-template <int LT, bool HASH>
-__device__ __forceinline__ uint64_t stage_ops(const Lane& L, const uint8_t* buf, uint32_t sub, uint32_t nsub) {
-  const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
-  const StageRun* runs = reinterpret_cast<const StageRun*>(buf + h->off_runs);
-  const uint32_t* items = reinterpret_cast<const uint32_t*>(buf + h->off_items);
-  const uint32_t base = smem_addr(buf), n_items = h->n_items;
-  const uint32_t s_c0 = base + h->off_c, s_w0 = base + h->off_w, s_k0 = base + h->off_k;
-  uint64_t hacc = 0;
-#pragma unroll 1
-  for (uint32_t it = sub; it < n_items; it += nsub) {
-    const uint32_t w = items[it];
-    const StageRun R = runs[w >> 16];
-    const uint32_t b = w & 0x1FFFu, cnt = ((w >> 13) & 7u) + 1u;
-    const uint32_t ar = (R.meta >> 8) & 0xffu, k = b - R.op_begin, cls = (R.meta >> 16) & 3u, op = R.meta & 0xffu;
-    const uint32_t s_c = s_c0 + 4 * (R.coord_begin + k * ar);
-    const uint32_t ob = R.out_row0 + k * ((uint32_t)LT << cls);
-    uint64_t hh;
-    if (ar == 2) hh = batch_ops<LT, HASH, 2>(L, op, s_c, s_w0 + 4 * b, s_k0 + 8 * b, cls, ob, cnt);
-    else if (ar == 1) hh = batch_ops<LT, HASH, 1>(L, op, s_c, s_w0 + 4 * b, s_k0 + 8 * b, cls, ob, cnt);
-    else if (ar == 3) hh = batch_ops<LT, HASH, 3>(L, op, s_c, s_w0 + 4 * b, s_k0 + 8 * b, cls, ob, cnt);
-    else hh = seg_generic<LT, HASH>(L, s_c, s_w0 + 4 * b, s_k0 + 8 * b, R.meta, ob, cnt);
-    if constexpr (HASH) hacc += hh;
-  }
-  return hacc;
-}
-
-// LATCH stage: tmp = LI[next] & M(w_r); LI[r] = tmp.  One pass is hazard-free
-// because every next row is an op row (compiler identity copies; reading R8).
-template <int LT, bool HASH>
-__device__ __forceinline__ uint64_t stage_latch(const Lane& L, uint32_t s_c, uint32_t s_w, uint32_t s_k, uint32_t b,
-                                                uint32_t e) {
-  constexpr int U = 8;
-  uint64_t h = 0;
-#pragma unroll 1
-  for (uint32_t j = b; j < e; j += U) {
-    uint64_t v[U];
-    uint32_t cc[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      cc[u] = lds32(s_c + 8 * min(j + u, e - 1));
-      v[u] = gather_raw(L, cc[u]);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (j + u < e) {
-        const uint64_t x = gather_fix(L, cc[u], v[u]) & wmask(lds32(s_w + 4 * (j + u)));
-        scatter(L, lds32(s_c + 8 * (j + u) + 4), x);
-        if constexpr (HASH) h += x * lds64(s_k + 8 * (j + u));
-      }
-  }
-  return h;
-}
-
-// INJECT stage: LI[in_k] = stimulus & M(w_k) (or the staged value).
-template <int LT, bool HASH>
-__device__ __forceinline__ uint64_t stage_inject(const Lane& L, uint32_t s_c, uint32_t s_w, uint32_t s_k,
-                                                 uint32_t first, uint32_t b, uint32_t e,
-                                                 const uint64_t* __restrict__ stage, uint32_t n_inputs,
-                                                 uint32_t n_lanes, uint64_t seed, uint64_t glane,
-                                                 uint64_t cycle_or_slot, int staged, uint32_t lane, bool valid) {
-  uint64_t h = 0;
-#pragma unroll 1
-  for (uint32_t j = b; j < e; ++j) {
-    const uint32_t k = first + j;
-    uint64_t v;
-    if (staged)
-      v = valid ? __ldg(stage + (cycle_or_slot * n_inputs + k) * n_lanes + lane) : 0ull;
-    else
-      v = d_stimulus(seed, k, cycle_or_slot, glane);
-    v &= wmask(lds32(s_w + 4 * j));
-    scatter(L, lds32(s_c + 4 * j), v);
-    if constexpr (HASH) h += v * lds64(s_k + 8 * j);
-  }
-  return h;
-}
-
-template <int LT, bool HASH>
-__global__ void __launch_bounds__(RS_LANES_MAX_THREADS, 1) k_lanes(const StepArgs a) {
-  constexpr int LTL = (LT == 32) ? 5 : (LT == 16) ? 4 : (LT == 8) ? 3 : (LT == 4) ? 2 : (LT == 2) ? 1 : 0;
-  extern __shared__ __align__(128) uint8_t smem[];
-  // shared memory: [mbarriers | stage buffer 0 | stage buffer 1 | red[2][T] | hr[T] | hp[T]]
-  // red: per-thread hash partials of a cycle (double buffered, reduced per lane);
-  // hr / hp: per-thread register terms of the next / current cycle.  Kept in
-  // shared memory, not registers: the hot loop needs every register it has.
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
-  const uint32_t T = blockDim.x, tid = threadIdx.x;
-  uint64_t* red = reinterpret_cast<uint64_t*>(smem + 128 + 2 * (size_t)a.stage_bytes);
-  uint64_t* hr_s = red + 2 * T;
-  uint64_t* hp_s = red + 3 * T;
-
-  const uint32_t lin = tid & (LT - 1);
-  const uint32_t sub = tid >> LTL;
-  const uint32_t nsub = T >> LTL;
-  const Lane L = make_lane(a.state + (size_t)blockIdx.x * a.tile_bytes, lin);
-
-  if (tid == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
-    mbar_fence_init();
-  }
-  if constexpr (HASH) {
-    const uint32_t lane = blockIdx.x * LT + lin;
-    hr_s[tid] = 0;
-    hp_s[tid] = (sub == 0 && lane < a.n_lanes) ? a.hcarry_in[lane] : 0ull;
-  }
-  __syncthreads();
-  const uint32_t S = a.n_stages;
-  const uint32_t total = a.n_cycles * S;  // host keeps n_cycles * S < 2^31
-  if (tid == 0 && total) {
-    const StageRef r = a.stage_tab[0];
-    tma_load_1d(smem + 128, a.stage_blob + r.off, r.bytes, &mbar[0]);
-  }
-
-  uint64_t hacc = 0;
-  uint32_t s = 0, cyc = 0;
-#pragma unroll 1
-  for (uint32_t gi = 0; gi < total; ++gi) {
-    const uint32_t bsel = gi & 1u;
-    if (tid == 0 && gi + 1 < total) {
-      const StageRef r = a.stage_tab[s + 1 == S ? 0 : s + 1];
-      tma_load_1d(smem + 128 + (bsel ^ 1u) * a.stage_bytes, a.stage_blob + r.off, r.bytes, &mbar[bsel ^ 1u]);
-    }
-    mbar_wait(&mbar[bsel], (gi >> 1) & 1u);
-    const uint8_t* buf = smem + 128 + bsel * a.stage_bytes;
-    const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
-    const uint32_t type = h->type;
-    if (type == ST_OPS) {
-      const uint64_t hh = stage_ops<LT, HASH>(L, buf, sub, nsub);
-      if constexpr (HASH) hacc += hh;
-    } else if (type == ST_LATCH) {
-      uint32_t b, e;
-      chunk_of(h->n, sub, nsub, b, e);
-      if (b < e) {
-        const uint32_t base = smem_addr(buf);
-        const uint64_t hh = stage_latch<LT, HASH>(L, base + h->off_c, base + h->off_w, base + h->off_k, b, e);
-        if constexpr (HASH) hr_s[tid] += hh;
-      }
-    } else if (type == ST_INJECT) {
-      uint32_t b, e;
-      chunk_of(h->n, sub, nsub, b, e);
-      if (b < e) {
-        const uint32_t base = smem_addr(buf), lane = blockIdx.x * LT + lin;
-        const uint64_t c = a.cycle0 + cyc;
-        const uint64_t hh = stage_inject<LT, HASH>(L, base + h->off_c, base + h->off_w, base + h->off_k, h->first,
-                                                   b, e, a.stage, a.g.n_inputs, a.n_lanes, a.seed, a.lane0 + lane,
-                                                   a.staged ? c % a.stage_cap : c, a.staged, lane, lane < a.n_lanes);
-        if constexpr (HASH) hacc += hh;
-      }
-    }
-    const bool eoc = (s + 1 == S);
-    if constexpr (HASH) {
-      if (eoc) {
-        red[(cyc & 1u) * T + tid] = hacc + hp_s[tid];
-        hp_s[tid] = hr_s[tid];
-        hr_s[tid] = 0;
-        hacc = 0;
-      }
-    }
-    __syncthreads();
-    if constexpr (HASH) {
-      const uint32_t lane = blockIdx.x * LT + lin;
-      if (eoc && sub == 0 && a.hashes != nullptr && lane < a.n_lanes) {
-        const uint64_t* rr = red + (cyc & 1u) * T + lin;
-        uint64_t sum = a.g.const_hash;
-#pragma unroll 4
-        for (uint32_t i = 0; i < nsub; ++i) sum += rr[i * LT];
-        a.hashes[(size_t)cyc * a.n_lanes + lane] = sum;
-      }
-    }
-    if (eoc) {
-      s = 0;
-      ++cyc;
-    } else {
-      ++s;
-    }
-  }
-  if constexpr (HASH) {
-    // register term of the hash of the next cycle (hp_s holds the last commit's partials)
-    __syncthreads();
-    const uint32_t lane = blockIdx.x * LT + lin;
-    if (sub == 0 && lane < a.n_lanes) {
-      uint64_t sum = 0;
-      for (uint32_t i = 0; i < nsub; ++i) sum += hp_s[i * LT + lin];
-      a.hcarry_out[lane] = sum;
-    }
-  }
 }
 
 // ------------------------------------------------------------------ single-lane mode

@@ -1,0 +1,479 @@
+// lanes.cuh -- the lane-mode step kernel (k_lanes): many independent
+// stimulus lanes, one CTA per lane tile of LT lanes, every thread owning P
+// adjacent lanes of its tile.
+//
+// Per cycle the CTA walks a fixed stage schedule (compiler.hpp build_stages):
+//   INJECT chunks | OPS chunks level by level | LATCH chunks,
+// each stage's descriptors brought into shared memory by one TMA bulk copy
+// issued a stage ahead; __syncthreads after every stage is the level barrier
+// (the iterative rank I of Cascade 1).
+//
+// Inside an OPS stage the work items -- run-aligned batches of kBatch ops of
+// one (opcode, arity, out class) run, PAPER.md Format c -- are
+// dealt round-robin to sub-warps of LT/P threads.  A sub-warp gathers every
+// operand of its batch (eq:split_einsum1) with one aligned 64-bit
+// load per operand (plus one per extra lane for 64-bit operands) before
+// computing any op (op_u / op_r / op_s, eq:step4c / eq:step5b): the PSU
+// partial S unrolling of P:1204-1209, used here for memory-level parallelism.
+// The per-op decode (descriptors, addresses, run bookkeeping) is paid once
+// per thread for P lanes.
+#pragma once
+#include "kernels.cuh"
+
+#ifndef RS_P
+#define RS_P 2
+#endif
+
+namespace rtlsim {
+
+__device__ __forceinline__ void chunk_of(uint32_t n, uint32_t part, uint32_t nparts, uint32_t& b, uint32_t& e) {
+  const uint32_t c = (n + nparts - 1) / nparts;
+  b = min(n, part * c);
+  e = min(n, b + c);
+}
+
+// Per-thread constants.  Bound coordinates are (class << 30) | byte offset of
+// the row's lane 0 inside the tile (rows are 8-byte aligned).
+template <int P>
+struct LaneP {
+  uint8_t* tb;       // tile base
+  uint32_t lin;      // thread index inside its sub-warp; owns tile lanes lin*P .. lin*P+P-1
+  uint32_t off8;     // byte c: ((lin*P) << c) & ~7 -- the 8-byte word holding the thread's first lane
+  uint32_t sh8[P];   // byte c (c <= 2): bit offset of lane p's container inside that word
+};
+
+template <int P>
+__device__ __forceinline__ LaneP<P> make_lanep(uint8_t* tb, uint32_t lin) {
+  LaneP<P> L;
+  L.tb = tb;
+  L.lin = lin;
+  const uint32_t l0 = lin * P;
+  L.off8 = 0;
+#pragma unroll
+  for (uint32_t c = 0; c < 4; ++c) L.off8 |= (((l0 << c) & ~7u) & 0xFFu) << (8 * c);
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    L.sh8[p] = 0;
+#pragma unroll
+    for (uint32_t c = 0; c < 3; ++c) L.sh8[p] |= ((((l0 + p) << c) & 7u) * 8u) << (8 * c);
+  }
+  return L;
+}
+
+__device__ __forceinline__ uint32_t cls_sel(uint32_t c) { return (c >> 30) | 0x4440u; }
+
+// Gather, part 1: the aligned 64-bit word holding the thread's first lane of
+// operand coordinate c (all P lanes for classes <= 32 bit), plus, for 64-bit
+// operands only, the next P-1 words -- each in its own register, so no load
+// waits for another.
+template <int P>
+__device__ __forceinline__ void gather_raw(const LaneP<P>& L, uint32_t c, uint64_t (&w)[P]) {
+  const uint8_t* q = L.tb + ((c & ROW_MASK) + __byte_perm(L.off8, 0u, cls_sel(c)));
+  w[0] = *reinterpret_cast<const uint64_t*>(q);
+#pragma unroll
+  for (int p = 1; p < P; ++p) {
+    w[p] = 0;
+    if ((c >> 30) == 3u) w[p] = *reinterpret_cast<const uint64_t*>(q + 8 * p);
+  }
+}
+
+// Gather, part 2 (after the batch's loads are all in flight): lane p's value.
+template <int P>
+__device__ __forceinline__ void gather_fix(const LaneP<P>& L, uint32_t c, const uint64_t (&w)[P], uint64_t (&x)[P]) {
+  const uint32_t cls = c >> 30, s = cls_sel(c);
+  const uint32_t m32 = 0xFFFFFFFFu >> __byte_perm(0x00001018u, 0u, s);  // 0xFF / 0xFFFF / ~0
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const uint32_t v = (uint32_t)(w[0] >> __byte_perm(L.sh8[p], 0u, s)) & m32;
+    x[p] = cls == 3u ? w[p] : (uint64_t)v;
+  }
+}
+
+// Store the thread's P lanes of one value row (class cls, row byte offset rb).
+template <int P>
+__device__ __forceinline__ void store_lanes(const LaneP<P>& L, uint32_t cls, uint32_t rb, const uint64_t (&y)[P]) {
+  uint8_t* q = L.tb + rb + ((L.lin * P) << cls);
+  if constexpr (P == 2) {
+    switch (cls) {
+      case 0: *reinterpret_cast<uint16_t*>(q) = (uint16_t)(((uint32_t)y[1] << 8) | ((uint32_t)y[0] & 0xFFu)); break;
+      case 1: *reinterpret_cast<uint32_t*>(q) = ((uint32_t)y[1] << 16) | ((uint32_t)y[0] & 0xFFFFu); break;
+      case 2: *reinterpret_cast<uint64_t*>(q) = (y[1] << 32) | (y[0] & 0xFFFFFFFFull); break;
+      default: *reinterpret_cast<ulonglong2*>(q) = make_ulonglong2(y[0], y[1]); break;
+    }
+  } else {
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      uint8_t* r = q + (p << cls);
+      switch (cls) {
+        case 0: *r = (uint8_t)y[p]; break;
+        case 1: *reinterpret_cast<uint16_t*>(r) = (uint16_t)y[p]; break;
+        case 2: *reinterpret_cast<uint32_t*>(r) = (uint32_t)y[p]; break;
+        default: *reinterpret_cast<uint64_t*>(r) = y[p]; break;
+      }
+    }
+  }
+}
+
+// op_u / op_r / op_s of Cascade 1 for the U ops x P lanes of a batch of one
+// run: one uniform switch per batch, the batch unrolled inside each case; only
+// the opcodes of arity A are instantiated.  Parameters come from the param
+// words (compiler.hpp pack_pw).
+template <int U, int A, int P>
+__device__ __forceinline__ void batch_compute(uint32_t op, const uint64_t (&x)[U][A][P], const uint32_t (&pw)[U],
+                                              uint64_t (&y)[U][P]) {
+#define RS_EACH(EXPR)                                   \
+  _Pragma("unroll") for (int u = 0; u < U; ++u) {       \
+    _Pragma("unroll") for (int p = 0; p < P; ++p) {     \
+      y[u][p] = (EXPR);                                 \
+    }                                                   \
+  }                                                     \
+  break;
+#define X0 x[u][0][p]
+#define X1 x[u][A > 1 ? 1 : 0][p]
+#define X2 x[u][A > 2 ? 2 : 0][p]
+#define P0 ((pw[u] >> 7) & 127u)
+#define P1 ((pw[u] >> 14) & 63u)
+  if constexpr (A == 1) {
+    switch (op) {
+      case RS_OP_NOT: RS_EACH(~X0)
+      case RS_OP_SHL: RS_EACH(P0 >= 64 ? 0ull : (X0 << P0))
+      case RS_OP_SHR: RS_EACH(P0 >= 64 ? 0ull : (X0 >> P0))
+      case RS_OP_BITS: RS_EACH((X0 >> P1) & wmask(P0 - P1 + 1u))
+      default: RS_EACH(X0)  // OP_COPY
+    }
+  } else if constexpr (A == 2) {
+    switch (op) {
+      case RS_OP_AND: RS_EACH(X0 & X1)
+      case RS_OP_OR: RS_EACH(X0 | X1)
+      case RS_OP_XOR: RS_EACH(X0 ^ X1)
+      case RS_OP_ADD: RS_EACH(X0 + X1)
+      case RS_OP_SUB: RS_EACH(X0 - X1)
+      case RS_OP_MUL: RS_EACH(X0 * X1)
+      case RS_OP_EQ: RS_EACH(X0 == X1 ? 1ull : 0ull)
+      case RS_OP_LT: RS_EACH(X0 < X1 ? 1ull : 0ull)
+      default: RS_EACH(P0 >= 64 ? X1 : ((X0 << P0) | X1))  // CAT
+    }
+  } else {
+    switch (op) {
+      case RS_OP_AND: RS_EACH(X0 & X1 & X2)
+      case RS_OP_OR: RS_EACH(X0 | X1 | X2)
+      case RS_OP_XOR: RS_EACH(X0 ^ X1 ^ X2)
+      case RS_OP_ADD: RS_EACH(X0 + X1 + X2)
+      case RS_OP_SUB: RS_EACH(X0 - X1 - X2)
+      case RS_OP_MUL: RS_EACH(X0 * X1 * X2)
+      default: RS_EACH(X0 != 0 ? X1 : X2)  // MUX
+    }
+  }
+#undef RS_EACH
+#undef X0
+#undef X1
+#undef X2
+#undef P0
+#undef P1
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint64_t m = wmask(pw[u] & 127u);
+#pragma unroll
+    for (int p = 0; p < P; ++p) y[u][p] &= m;
+  }
+}
+
+// One work item: cnt <= kBatch ops of one run (opcode op, arity A in 1..3,
+// out class out_cls); descriptors in shared memory (s_c: first coord, s_w:
+// first param word, s_k: first hash weight); outputs at consecutive rows
+// from out_byte0.  Tail slots re-read op 0 (no branches in the gather).
+template <int LT, int P, bool HASH, int A>
+__device__ __forceinline__ void batch_ops(const LaneP<P>& L, uint32_t op, uint32_t s_c, uint32_t s_w, uint32_t s_k,
+                                          uint32_t out_cls, uint32_t out_byte0, uint32_t cnt, uint64_t (&hacc)[P]) {
+  constexpr int U = (int)kBatch;
+  uint64_t x[U][A][P];
+  uint32_t cc[U][A];
+  uint32_t pw[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint32_t uu = (uint32_t)u < cnt ? (uint32_t)u : 0u;
+#pragma unroll
+    for (int o = 0; o < A; ++o) {
+      cc[u][o] = lds32(s_c + 4 * (uu * A + o));
+      gather_raw<P>(L, cc[u][o], x[u][o]);
+    }
+    pw[u] = lds32(s_w + 4 * uu);
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int o = 0; o < A; ++o) {
+      uint64_t w[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) w[p] = x[u][o][p];
+      gather_fix<P>(L, cc[u][o], w, x[u][o]);
+    }
+  uint64_t y[U][P];
+  batch_compute<U, A, P>(op, x, pw, y);
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    if ((uint32_t)u < cnt) {
+      if constexpr (HASH) {
+        const uint64_t k = lds64(s_k + 8 * u);
+#pragma unroll
+        for (int p = 0; p < P; ++p) hacc[p] += y[u][p] * k;
+      }
+      store_lanes<P>(L, out_cls, out_byte0 + u * ((uint32_t)LT << out_cls), y[u]);
+    }
+  }
+}
+
+// Folds with more than 3 operands (left fold over the O rank; rare).
+template <int LT, int P, bool HASH>
+__device__ __forceinline__ void seg_generic(const LaneP<P>& L, uint32_t s_c, uint32_t s_w, uint32_t s_k, uint32_t meta,
+                                            uint32_t out_byte0, uint32_t n, uint64_t (&hacc)[P]) {
+  const uint32_t op = meta & 0xffu, ar = (meta >> 8) & 0xffu, out_cls = (meta >> 16) & 3u;
+#pragma unroll 1
+  for (uint32_t j = 0; j < n; ++j) {
+    const uint32_t c0 = s_c + 4 * j * ar;
+    uint64_t w[P], r[P], x[P];
+    uint32_t c = lds32(c0);
+    gather_raw<P>(L, c, w);
+    gather_fix<P>(L, c, w, r);
+#pragma unroll 1
+    for (uint32_t o = 1; o < ar; ++o) {
+      c = lds32(c0 + 4 * o);
+      gather_raw<P>(L, c, w);
+      gather_fix<P>(L, c, w, x);
+#pragma unroll
+      for (int p = 0; p < P; ++p) r[p] = fold_step(op, r[p], x[p]);
+    }
+    const uint64_t m = wmask(lds32(s_w + 4 * j) & 127u);
+#pragma unroll
+    for (int p = 0; p < P; ++p) r[p] &= m;
+    if constexpr (HASH) {
+      const uint64_t k = lds64(s_k + 8 * j);
+#pragma unroll
+      for (int p = 0; p < P; ++p) hacc[p] += r[p] * k;
+    }
+    store_lanes<P>(L, out_cls, out_byte0 + j * ((uint32_t)LT << out_cls), r);
+  }
+}
+
+// OPS stage: the stage's work items dealt round-robin to the sub-warps (an
+// even mix of arities and classes per sub-warp; no atomics).
+template <int LT, int P, bool HASH>
+__device__ __forceinline__ void stage_ops(const LaneP<P>& L, const uint8_t* buf, uint32_t sub, uint32_t nsub,
+                                          uint64_t (&hacc)[P]) {
+  const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
+  const StageRun* runs = reinterpret_cast<const StageRun*>(buf + h->off_runs);
+  const uint32_t* items = reinterpret_cast<const uint32_t*>(buf + h->off_items);
+  const uint32_t base = smem_addr(buf), n_items = h->n_items;
+  const uint32_t s_c0 = base + h->off_c, s_w0 = base + h->off_w, s_k0 = base + h->off_k;
+#pragma unroll 1
+  for (uint32_t it = sub; it < n_items; it += nsub) {
+    const uint32_t w = items[it];
+    const StageRun R = runs[w >> 16];
+    const uint32_t b = w & 0x1FFFu, cnt = ((w >> 13) & 7u) + 1u;
+    const uint32_t ar = (R.meta >> 8) & 0xffu, k = b - R.op_begin, cls = (R.meta >> 16) & 3u, op = R.meta & 0xffu;
+    const uint32_t s_c = s_c0 + 4 * (R.coord_begin + k * ar);
+    const uint32_t ob = R.out_row0 + k * ((uint32_t)LT << cls);
+    if (ar == 2) batch_ops<LT, P, HASH, 2>(L, op, s_c, s_w0 + 4 * b, s_k0 + 8 * b, cls, ob, cnt, hacc);
+    else if (ar == 1) batch_ops<LT, P, HASH, 1>(L, op, s_c, s_w0 + 4 * b, s_k0 + 8 * b, cls, ob, cnt, hacc);
+    else if (ar == 3) batch_ops<LT, P, HASH, 3>(L, op, s_c, s_w0 + 4 * b, s_k0 + 8 * b, cls, ob, cnt, hacc);
+    else seg_generic<LT, P, HASH>(L, s_c, s_w0 + 4 * b, s_k0 + 8 * b, R.meta, ob, cnt, hacc);
+  }
+}
+
+// LATCH stage: tmp = LI[next] & M(w_r); LI[r] = tmp.  One pass is hazard-free
+// because every next row is an op row (compiler identity copies; reading R8).
+template <int LT, int P, bool HASH>
+__device__ __forceinline__ void stage_latch(const LaneP<P>& L, uint32_t s_c, uint32_t s_w, uint32_t s_k, uint32_t b,
+                                            uint32_t e, uint64_t (&hr)[P]) {
+  constexpr int U = 4;
+#pragma unroll 1
+  for (uint32_t j = b; j < e; j += U) {
+    uint64_t v[U][P];
+    uint32_t cc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      cc[u] = lds32(s_c + 8 * min(j + u, e - 1));
+      gather_raw<P>(L, cc[u], v[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (j + u < e) {
+        uint64_t x[P];
+        gather_fix<P>(L, cc[u], v[u], x);
+        const uint64_t m = wmask(lds32(s_w + 4 * (j + u)));
+#pragma unroll
+        for (int p = 0; p < P; ++p) x[p] &= m;
+        const uint32_t rc = lds32(s_c + 8 * (j + u) + 4);
+        store_lanes<P>(L, rc >> 30, rc & ROW_MASK, x);
+        if constexpr (HASH) {
+          const uint64_t k = lds64(s_k + 8 * (j + u));
+#pragma unroll
+          for (int p = 0; p < P; ++p) hr[p] += x[p] * k;
+        }
+      }
+    }
+  }
+}
+
+// INJECT stage: LI[in_k] = stimulus & M(w_k) (or the staged value).
+template <int LT, int P, bool HASH>
+__device__ __forceinline__ void stage_inject(const LaneP<P>& L, uint32_t s_c, uint32_t s_w, uint32_t s_k,
+                                             uint32_t first, uint32_t b, uint32_t e, const StepArgs& a, uint32_t lane,
+                                             uint64_t cycle, uint64_t (&hacc)[P]) {
+#pragma unroll 1
+  for (uint32_t j = b; j < e; ++j) {
+    const uint32_t k = first + j;
+    const uint64_t m = wmask(lds32(s_w + 4 * j));
+    uint64_t v[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      if (a.staged)
+        v[p] = lane + p < a.n_lanes
+                   ? __ldg(a.stage + ((cycle % a.stage_cap) * a.g.n_inputs + k) * a.n_lanes + lane + p)
+                   : 0ull;
+      else
+        v[p] = d_stimulus(a.seed, k, cycle, a.lane0 + lane + p);
+      v[p] &= m;
+    }
+    const uint32_t c = lds32(s_c + 4 * j);
+    store_lanes<P>(L, c >> 30, c & ROW_MASK, v);
+    if constexpr (HASH) {
+      const uint64_t kk = lds64(s_k + 8 * j);
+#pragma unroll
+      for (int p = 0; p < P; ++p) hacc[p] += v[p] * kk;
+    }
+  }
+}
+
+// Shared-memory bytes the lane kernel needs beyond its two stage buffers.
+__host__ __device__ constexpr size_t lanes_smem_extra(uint32_t threads) { return 4ull * threads * RS_P * 8; }
+
+template <int LT, bool HASH>
+__global__ void __launch_bounds__(RS_LANES_MAX_THREADS, 1) k_lanes(const StepArgs a) {
+  constexpr int P = RS_P;
+  constexpr int LTS = LT / P;  // threads per sub-warp (one op at a time)
+  constexpr int LTSL = (LTS == 32) ? 5 : (LTS == 16) ? 4 : (LTS == 8) ? 3 : (LTS == 4) ? 2 : (LTS == 2) ? 1 : 0;
+  static_assert(LT % P == 0 && (1 << LTSL) == LTS, "lane tile / lanes per thread");
+  extern __shared__ __align__(128) uint8_t smem[];
+  // shared memory: [mbarriers | stage buffer 0 | stage buffer 1 | red[2][T*P] | hr[T*P] | hp[T*P]]
+  // red: per-(thread, lane) hash partials of a cycle (double buffered, then
+  // reduced per lane); hr / hp: register terms of the next / current cycle.
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
+  const uint32_t T = blockDim.x, tid = threadIdx.x;
+  uint64_t* red = reinterpret_cast<uint64_t*>(smem + 128 + 2 * (size_t)a.stage_bytes);
+  uint64_t* hr_s = red + 2 * T * P;
+  uint64_t* hp_s = red + 3 * T * P;
+
+  const uint32_t lin = tid & (LTS - 1);
+  const uint32_t sub = tid >> LTSL;
+  const uint32_t nsub = T >> LTSL;
+  const uint32_t lane = blockIdx.x * LT + lin * P;  // first lane of this thread (allocation-relative)
+  const LaneP<P> L = make_lanep<P>(a.state + (size_t)blockIdx.x * a.tile_bytes, lin);
+
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    mbar_fence_init();
+  }
+  if constexpr (HASH) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      hr_s[tid * P + p] = 0;
+      hp_s[tid * P + p] = (sub == 0 && lane + p < a.n_lanes) ? a.hcarry_in[lane + p] : 0ull;
+    }
+  }
+  __syncthreads();
+  const uint32_t S = a.n_stages;
+  const uint32_t total = a.n_cycles * S;  // host keeps n_cycles * S < 2^31
+  if (tid == 0 && total) {
+    const StageRef r = a.stage_tab[0];
+    tma_load_1d(smem + 128, a.stage_blob + r.off, r.bytes, &mbar[0]);
+  }
+
+  uint64_t hacc[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) hacc[p] = 0;
+  uint32_t s = 0, cyc = 0;
+#pragma unroll 1
+  for (uint32_t gi = 0; gi < total; ++gi) {
+    const uint32_t bsel = gi & 1u;
+    if (tid == 0 && gi + 1 < total) {
+      const StageRef r = a.stage_tab[s + 1 == S ? 0 : s + 1];
+      tma_load_1d(smem + 128 + (bsel ^ 1u) * a.stage_bytes, a.stage_blob + r.off, r.bytes, &mbar[bsel ^ 1u]);
+    }
+    mbar_wait(&mbar[bsel], (gi >> 1) & 1u);
+    const uint8_t* buf = smem + 128 + bsel * a.stage_bytes;
+    const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
+    const uint32_t type = h->type;
+    if (type == ST_OPS) {
+      stage_ops<LT, P, HASH>(L, buf, sub, nsub, hacc);
+    } else if (type == ST_LATCH) {
+      uint32_t b, e;
+      chunk_of(h->n, sub, nsub, b, e);
+      if (b < e) {
+        const uint32_t base = smem_addr(buf);
+        uint64_t hr[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) hr[p] = 0;
+        stage_latch<LT, P, HASH>(L, base + h->off_c, base + h->off_w, base + h->off_k, b, e, hr);
+        if constexpr (HASH) {
+#pragma unroll
+          for (int p = 0; p < P; ++p) hr_s[tid * P + p] += hr[p];
+        }
+      }
+    } else if (type == ST_INJECT) {
+      uint32_t b, e;
+      chunk_of(h->n, sub, nsub, b, e);
+      if (b < e) {
+        const uint32_t base = smem_addr(buf);
+        stage_inject<LT, P, HASH>(L, base + h->off_c, base + h->off_w, base + h->off_k, h->first, b, e, a, lane,
+                                  a.cycle0 + cyc, hacc);
+      }
+    }
+    const bool eoc = (s + 1 == S);
+    if constexpr (HASH) {
+      if (eoc) {
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          red[(cyc & 1u) * T * P + tid * P + p] = hacc[p] + hp_s[tid * P + p];
+          hp_s[tid * P + p] = hr_s[tid * P + p];
+          hr_s[tid * P + p] = 0;
+          hacc[p] = 0;
+        }
+      }
+    }
+    __syncthreads();
+    if constexpr (HASH) {
+      if (eoc && sub == 0 && a.hashes != nullptr) {
+        const uint64_t* rr = red + (cyc & 1u) * T * P + lin * P;
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          uint64_t sum = a.g.const_hash;
+#pragma unroll 4
+          for (uint32_t i = 0; i < nsub; ++i) sum += rr[i * LTS * P + p];
+          if (lane + p < a.n_lanes) a.hashes[(size_t)cyc * a.n_lanes + lane + p] = sum;
+        }
+      }
+    }
+    if (eoc) {
+      s = 0;
+      ++cyc;
+    } else {
+      ++s;
+    }
+  }
+  if constexpr (HASH) {
+    // register term of the hash of the next cycle (hp_s holds the last commit's partials)
+    __syncthreads();
+    if (sub == 0) {
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        uint64_t sum = 0;
+        for (uint32_t i = 0; i < nsub; ++i) sum += hp_s[(i * LTS + lin) * P + p];
+        if (lane + p < a.n_lanes) a.hcarry_out[lane + p] = sum;
+      }
+    }
+  }
+}
+
+}  // namespace rtlsim

@@ -13,6 +13,7 @@
 #include "../../include/rtlsim.h"
 #include "compiler.hpp"
 #include "kernels.cuh"
+#include "lanes.cuh"
 
 using namespace rtlsim;
 
@@ -166,7 +167,7 @@ void put(std::vector<uint8_t>& blob, size_t& off, const std::vector<T>& v, size_
 constexpr uint32_t kStageBytes = 48 * 1024;
 
 size_t lanes_smem(uint32_t stage_bytes, uint32_t threads) {
-  return 128 + 2ull * stage_bytes + 4ull * threads * sizeof(uint64_t);
+  return 128 + 2ull * stage_bytes + lanes_smem_extra(threads);
 }
 
 int choose_lt(uint32_t n_lanes, int sms) {
