@@ -199,6 +199,11 @@ uint64_t rs_launch_count(const rs_lanes* s);
 /* Chosen launch shape: lane tile, threads per CTA, CTAs. */
 rs_status rs_launch_shape(const rs_lanes* s, uint32_t* lane_tile, uint32_t* threads, uint32_t* ctas);
 rs_status rs_sync(rs_lanes* s);
+/* Diagnostics (builds with -DRS_TRACE only, else RS_E_UNSUPPORTED): the first
+ * call arms a per-stage clock64 trace of CTA 0; later calls copy up to n u64
+ * stamps to host `out` (layout: per stage [top, after stage wait, after
+ * barrier, work end of each warp]). */
+rs_status rs_debug_trace(rs_lanes* s, uint64_t* out, uint64_t n);
 
 #ifdef __cplusplus
 }

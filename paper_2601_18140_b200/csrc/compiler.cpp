@@ -187,7 +187,9 @@ rs_status compile_graph(const rs_graph_desc* d, uint32_t mode, CompiledGraph* ou
   std::vector<uint32_t> order(NT);
   std::iota(order.begin(), order.end(), 0u);
   auto key = [&](uint32_t t) -> uint64_t {
-    return ((uint64_t)op_level(t) << 32) | ((uint64_t)op_code(t) << 16) | ((uint64_t)op_arity(t) << 8) |
+    // arity first: consecutive work items then share the gather code path, so
+    // sub-warps of one warp stay converged even across short runs
+    return ((uint64_t)op_level(t) << 32) | ((uint64_t)op_arity(t) << 16) | ((uint64_t)op_code(t) << 8) |
            width_class(op_width(t));
   };
   std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return key(a) < key(b); });

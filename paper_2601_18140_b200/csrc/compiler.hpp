@@ -131,7 +131,10 @@ struct StageHdr {          // first 64 bytes of a stage block
 };
 
 // Ops per work item of an OPS stage (the gather batch of the lane kernel).
-constexpr uint32_t kBatch = 4;
+#ifndef RS_BATCH
+#define RS_BATCH 4
+#endif
+constexpr uint32_t kBatch = RS_BATCH;   // <= 8 (3-bit count field of a work item)
 
 struct StageRun {          // a run clipped to the stage; indices relative to the stage
   uint32_t op_begin;

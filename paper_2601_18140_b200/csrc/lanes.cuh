@@ -396,12 +396,21 @@ __global__ void __launch_bounds__(RS_LANES_MAX_THREADS, 1) k_lanes(const StepArg
   uint32_t s = 0, cyc = 0;
 #pragma unroll 1
   for (uint32_t gi = 0; gi < total; ++gi) {
+#ifdef RS_TRACE
+    // stamps per stage (CTA 0): [0] loop top, [1] after the stage-buffer wait,
+    // [2] after the barrier, [3 + w] warp w's work end
+    unsigned long long* tr = (blockIdx.x == 0 && gi < 4096) ? a.trace + (size_t)gi * (3 + T / 32) : nullptr;
+    if (tr && tid == 0) tr[0] = clock64();
+#endif
     const uint32_t bsel = gi & 1u;
     if (tid == 0 && gi + 1 < total) {
       const StageRef r = a.stage_tab[s + 1 == S ? 0 : s + 1];
       tma_load_1d(smem + 128 + (bsel ^ 1u) * a.stage_bytes, a.stage_blob + r.off, r.bytes, &mbar[bsel ^ 1u]);
     }
     mbar_wait(&mbar[bsel], (gi >> 1) & 1u);
+#ifdef RS_TRACE
+    if (tr && tid == 0) tr[1] = clock64();
+#endif
     const uint8_t* buf = smem + 128 + bsel * a.stage_bytes;
     const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
     const uint32_t type = h->type;
@@ -442,7 +451,13 @@ __global__ void __launch_bounds__(RS_LANES_MAX_THREADS, 1) k_lanes(const StepArg
         }
       }
     }
+#ifdef RS_TRACE
+    if (tr && (tid & 31) == 0) tr[3 + tid / 32] = clock64();
+#endif
     __syncthreads();
+#ifdef RS_TRACE
+    if (tr && tid == 0) tr[2] = clock64();
+#endif
     if constexpr (HASH) {
       if (eoc && sub == 0 && a.hashes != nullptr) {
         const uint64_t* rr = red + (cyc & 1u) * T * P + lin * P;

@@ -93,6 +93,7 @@ struct rs_lanes {
   size_t hbuf_cap = 0;
   unsigned long long* bar = nullptr;
   uint64_t launches = 0;
+  unsigned long long* trace = nullptr;  // RS_TRACE builds only
   size_t total_bytes = 0;
 };
 
@@ -119,6 +120,7 @@ StepArgs base_args(const rs_lanes* s) {
   a.stage_tab = s->stage_tab;
   a.n_stages = s->n_stages;
   a.stage_bytes = s->g->stage_bytes;
+  a.trace = s->trace;
   return a;
 }
 
@@ -708,6 +710,24 @@ rs_status rs_set_cycle(rs_lanes* s, uint64_t cycle) {
 }
 
 uint64_t rs_launch_count(const rs_lanes* s) { return s ? s->launches : 0; }
+
+rs_status rs_debug_trace(rs_lanes* s, uint64_t* out, uint64_t n) {
+#ifdef RS_TRACE
+  if (!s || !out) return set_err(RS_E_INVALID_ARG, "NULL argument");
+  const uint64_t cap = 4096ull * (3 + 1024 / 32);
+  if (!s->trace) {
+    CU(cudaMalloc(&s->trace, cap * 8));
+    CU(cudaMemset(s->trace, 0, cap * 8));
+    return RS_OK;  // first call arms the buffer; step, then call again to read
+  }
+  CU(cudaStreamSynchronize(s->stream));
+  CU(cudaMemcpy(out, s->trace, std::min(n, cap) * 8, cudaMemcpyDeviceToHost));
+  return RS_OK;
+#else
+  (void)s; (void)out; (void)n;
+  return set_err(RS_E_UNSUPPORTED, "built without RS_TRACE");
+#endif
+}
 
 rs_status rs_launch_shape(const rs_lanes* s, uint32_t* lt, uint32_t* threads, uint32_t* ctas) {
   if (!s) return set_err(RS_E_INVALID_ARG, "NULL lanes");

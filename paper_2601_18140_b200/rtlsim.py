@@ -25,7 +25,7 @@ STATUS = {0: "RS_OK", -1: "RS_E_INVALID_ARG", -2: "RS_E_GRAPH", -3: "RS_E_CAPACI
 EXPORTS = ["rs_version", "rs_last_error", "rs_load_graph", "rs_graph_info_get", "rs_free_graph",
            "rs_alloc_lanes", "rs_free_lanes", "rs_lanes_bytes", "rs_set_input_seed", "rs_set_inputs",
            "rs_step_cycles", "rs_read_signals", "rs_write_registers", "rs_get_cycle", "rs_set_cycle",
-           "rs_launch_count", "rs_launch_shape", "rs_sync", "rs_graph_export"]
+           "rs_launch_count", "rs_launch_shape", "rs_sync", "rs_graph_export", "rs_debug_trace"]
 RS_DEVICE_NONE = -1
 EXPORT = {"runs": (0, np.uint32), "level_run_begin": (1, np.uint32), "level_op_begin": (2, np.uint32),
           "opw": (3, np.uint32), "opk": (4, np.uint64), "coord_off": (5, np.uint32), "coord": (6, np.uint32),
@@ -99,6 +99,7 @@ def lib() -> C.CDLL:
             "rs_launch_shape": (i32, [vp, C.POINTER(u32), C.POINTER(u32), C.POINTER(u32)]),
             "rs_sync": (i32, [vp]),
             "rs_graph_export": (i32, [vp, u32, vp, C.POINTER(u64)]),
+            "rs_debug_trace": (i32, [vp, vp, u64]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)

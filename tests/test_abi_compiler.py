@@ -198,7 +198,7 @@ def test_format_runs_sorted_and_stats(rs):
     lrb = g.export("level_run_begin")
     assert info["n_levels"] == 20 and info["n_runs"] == runs.shape[0]
     for lev in range(20):
-        keys = [(int(m) & 0xFF, (int(m) >> 8) & 0xFF, (int(m) >> 16) & 3) for m in runs[lrb[lev]:lrb[lev + 1], 4]]
+        keys = [((int(m) >> 8) & 0xFF, int(m) & 0xFF, (int(m) >> 16) & 3) for m in runs[lrb[lev]:lrb[lev + 1], 4]]
         assert keys == sorted(keys) and len(set(keys)) == len(keys)
     # B_alg per lane-cycle equals the SURVEY §8(d) formula recomputed here
     cls_b = lambda w: 1 if w <= 8 else 2 if w <= 16 else 4 if w <= 32 else 8
