@@ -163,6 +163,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--lane-tile", type=int, default=0)
     ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--cluster", type=int, default=0)
     ap.add_argument("--ref-step-s", type=float, default=4.0)
     args = ap.parse_args()
 
@@ -194,7 +195,8 @@ def main():
     stream = torch.cuda.Stream()
     g = rs.Graph(circ, device=local, mode="single" if single else "lanes")
     info = g.info()
-    L = rs.Lanes(g, lanes, lane0=rank * lanes, lane_tile=args.lane_tile, threads=args.threads, stream=stream)
+    L = rs.Lanes(g, lanes, lane0=rank * lanes, lane_tile=args.lane_tile, threads=args.threads, stream=stream,
+                 cluster=args.cluster)
     L.set_seed(cfg.stim_seed)
     hashes = None if args.no_hash else torch.empty(cycles * lanes, dtype=torch.int64, device="cuda")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
@@ -250,7 +252,7 @@ def main():
     e2e = None
     if not args.no_e2e and rank == 0 or (not args.no_e2e and world > 1):
         chunk = min(cycles, max(1, (256 << 20) // max(1, 8 * circ.n_inputs * lanes)))
-        Ls = rs.Lanes(g, lanes, lane0=rank * lanes, lane_tile=args.lane_tile, threads=args.threads,
+        Ls = rs.Lanes(g, lanes, lane0=rank * lanes, lane_tile=args.lane_tile, threads=args.threads, cluster=args.cluster,
                       stage_cycles=chunk, stream=stream)
         rng = np.random.default_rng(rank)
         host_in = torch.from_numpy(rng.integers(0, 2**63, size=(chunk, circ.n_inputs, lanes),

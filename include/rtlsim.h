@@ -119,7 +119,8 @@ typedef struct {
   uint32_t lane_tile;      /* RS_MODE_LANES: lanes per CTA tile, 0 = auto, else 8, 16 or 32 */
   uint32_t threads;        /* threads per CTA, 0 = auto (multiple of 32, <= 1024) */
   uint32_t stage_cycles;   /* capacity (cycles) of the staged-input ring, 0 = none */
-  uint32_t unroll_hint;    /* reserved, 0 */
+  uint32_t cluster;        /* RS_MODE_LANES: CTAs (a thread-block cluster on as many SMs) sharing one
+                              lane tile, 0 = auto, else 1, 2, 4 or 8 */
   void* stream;            /* cudaStream_t to run on; NULL = a stream the library creates */
 } rs_lane_opts;
 
@@ -196,8 +197,10 @@ rs_status rs_get_cycle(const rs_lanes* s, uint64_t* cycle);
 rs_status rs_set_cycle(rs_lanes* s, uint64_t cycle);
 /* Kernel launches issued by this allocation so far (evidence counter). */
 uint64_t rs_launch_count(const rs_lanes* s);
-/* Chosen launch shape: lane tile, threads per CTA, CTAs. */
-rs_status rs_launch_shape(const rs_lanes* s, uint32_t* lane_tile, uint32_t* threads, uint32_t* ctas);
+/* Chosen launch shape: lane tile, threads per CTA, CTAs, CTAs per cluster
+ * (any output pointer may be NULL). */
+rs_status rs_launch_shape(const rs_lanes* s, uint32_t* lane_tile, uint32_t* threads, uint32_t* ctas,
+                          uint32_t* cluster);
 rs_status rs_sync(rs_lanes* s);
 /* Diagnostics (builds with -DRS_TRACE only, else RS_E_UNSUPPORTED): the first
  * call arms a per-stage clock64 trace of CTA 0; later calls copy up to n u64

@@ -75,6 +75,7 @@ struct StepArgs {
   const StageRef* stage_tab;
   uint32_t n_stages;
   uint32_t stage_bytes;        // shared-memory bytes per stage buffer
+  uint32_t cluster;            // lane mode: CTAs (one cluster) sharing one lane tile
   unsigned long long* trace;   // RS_TRACE builds: per-stage clock64 stamps of CTA 0 (tools/, not the product)
 };
 

@@ -345,30 +345,59 @@ __device__ __forceinline__ void stage_inject(const LaneP<P>& L, uint32_t s_c, ui
   }
 }
 
-// Shared-memory bytes the lane kernel needs beyond its two stage buffers.
-__host__ __device__ constexpr size_t lanes_smem_extra(uint32_t threads) { return 4ull * threads * RS_P * 8; }
+// Shared-memory bytes the lane kernel needs beyond its two stage buffers:
+// red[2][T*P] + hr[T*P] + hp[T*P] (u64) + lsum[3][32] (u64, cluster partials).
+__host__ __device__ constexpr size_t lanes_smem_extra(uint32_t threads) {
+  return 4ull * threads * RS_P * 8 + 3ull * 32 * 8;
+}
+
+// Level barrier: CTA barrier, or a cluster barrier when one lane tile is
+// spread over a thread-block cluster (arrive.release / wait.acquire: the
+// state other CTAs of the cluster wrote in this stage is visible after it).
+__device__ __forceinline__ void stage_barrier(uint32_t cs) {
+  if (cs > 1) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  } else {
+    __syncthreads();
+  }
+}
+
+// Generic address of the same shared-memory object in CTA `rank` of the cluster.
+__device__ __forceinline__ const uint64_t* dsmem(const uint64_t* p, uint32_t rank) {
+  uint32_t a = smem_addr(p), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  uint64_t out;
+  asm volatile("{ .reg .u64 t; cvt.u64.u32 t, %1; cvta.shared::cluster.u64 %0, t; }" : "=l"(out) : "r"(r));
+  return reinterpret_cast<const uint64_t*>(out);
+}
 
 template <int LT, bool HASH>
 __global__ void __launch_bounds__(RS_LANES_MAX_THREADS, 1) k_lanes(const StepArgs a) {
   constexpr int P = RS_P;
   constexpr int LTS = LT / P;  // threads per sub-warp (one op at a time)
   constexpr int LTSL = (LTS == 32) ? 5 : (LTS == 16) ? 4 : (LTS == 8) ? 3 : (LTS == 4) ? 2 : (LTS == 2) ? 1 : 0;
-  static_assert(LT % P == 0 && (1 << LTSL) == LTS, "lane tile / lanes per thread");
+  static_assert(LT % P == 0 && (1 << LTSL) == LTS && LT <= 32, "lane tile / lanes per thread");
   extern __shared__ __align__(128) uint8_t smem[];
-  // shared memory: [mbarriers | stage buffer 0 | stage buffer 1 | red[2][T*P] | hr[T*P] | hp[T*P]]
-  // red: per-(thread, lane) hash partials of a cycle (double buffered, then
-  // reduced per lane); hr / hp: register terms of the next / current cycle.
+  // shared memory: [mbarriers | stage buffer 0 | stage buffer 1 | red[2][T*P] | hr[T*P] | hp[T*P] | lsum[3][32]]
+  // red: per-(thread, lane) hash partials of a cycle (double buffered, reduced
+  // per lane); hr / hp: register terms of the next / current cycle; lsum: this
+  // CTA's per-lane partial of a cycle (two parities) and of the carry, summed
+  // across the cluster through distributed shared memory.
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
   const uint32_t T = blockDim.x, tid = threadIdx.x;
   uint64_t* red = reinterpret_cast<uint64_t*>(smem + 128 + 2 * (size_t)a.stage_bytes);
   uint64_t* hr_s = red + 2 * T * P;
   uint64_t* hp_s = red + 3 * T * P;
+  uint64_t* lsum = red + 4 * T * P;
 
+  const uint32_t CS = a.cluster;
+  const uint32_t rank = blockIdx.x % CS, tile = blockIdx.x / CS;
   const uint32_t lin = tid & (LTS - 1);
   const uint32_t sub = tid >> LTSL;
   const uint32_t nsub = T >> LTSL;
-  const uint32_t lane = blockIdx.x * LT + lin * P;  // first lane of this thread (allocation-relative)
-  const LaneP<P> L = make_lanep<P>(a.state + (size_t)blockIdx.x * a.tile_bytes, lin);
+  const uint32_t gsub = rank * nsub + sub, ngsub = CS * nsub;  // sub-warp index across the cluster
+  const uint32_t lane = tile * LT + lin * P;  // first lane of this thread (allocation-relative)
+  const LaneP<P> L = make_lanep<P>(a.state + (size_t)tile * a.tile_bytes, lin);
 
   if (tid == 0) {
     mbar_init(&mbar[0], 1);
@@ -379,7 +408,7 @@ __global__ void __launch_bounds__(RS_LANES_MAX_THREADS, 1) k_lanes(const StepArg
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       hr_s[tid * P + p] = 0;
-      hp_s[tid * P + p] = (sub == 0 && lane + p < a.n_lanes) ? a.hcarry_in[lane + p] : 0ull;
+      hp_s[tid * P + p] = (gsub == 0 && lane + p < a.n_lanes) ? a.hcarry_in[lane + p] : 0ull;
     }
   }
   __syncthreads();
@@ -389,11 +418,13 @@ __global__ void __launch_bounds__(RS_LANES_MAX_THREADS, 1) k_lanes(const StepArg
     const StageRef r = a.stage_tab[0];
     tma_load_1d(smem + 128, a.stage_blob + r.off, r.bytes, &mbar[0]);
   }
+  if (CS > 1) stage_barrier(CS);  // every CTA of the cluster has started (DSMEM use below)
 
   uint64_t hacc[P];
 #pragma unroll
   for (int p = 0; p < P; ++p) hacc[p] = 0;
   uint32_t s = 0, cyc = 0;
+  int pend = -1;  // cycle whose cluster-wide hash is still to be summed (CS > 1)
 #pragma unroll 1
   for (uint32_t gi = 0; gi < total; ++gi) {
 #ifdef RS_TRACE
@@ -415,10 +446,10 @@ __global__ void __launch_bounds__(RS_LANES_MAX_THREADS, 1) k_lanes(const StepArg
     const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
     const uint32_t type = h->type;
     if (type == ST_OPS) {
-      stage_ops<LT, P, HASH>(L, buf, sub, nsub, hacc);
+      stage_ops<LT, P, HASH>(L, buf, gsub, ngsub, hacc);
     } else if (type == ST_LATCH) {
       uint32_t b, e;
-      chunk_of(h->n, sub, nsub, b, e);
+      chunk_of(h->n, gsub, ngsub, b, e);
       if (b < e) {
         const uint32_t base = smem_addr(buf);
         uint64_t hr[P];
@@ -432,7 +463,7 @@ __global__ void __launch_bounds__(RS_LANES_MAX_THREADS, 1) k_lanes(const StepArg
       }
     } else if (type == ST_INJECT) {
       uint32_t b, e;
-      chunk_of(h->n, sub, nsub, b, e);
+      chunk_of(h->n, gsub, ngsub, b, e);
       if (b < e) {
         const uint32_t base = smem_addr(buf);
         stage_inject<LT, P, HASH>(L, base + h->off_c, base + h->off_w, base + h->off_k, h->first, b, e, a, lane,
@@ -454,21 +485,38 @@ __global__ void __launch_bounds__(RS_LANES_MAX_THREADS, 1) k_lanes(const StepArg
 #ifdef RS_TRACE
     if (tr && (tid & 31) == 0) tr[3 + tid / 32] = clock64();
 #endif
-    __syncthreads();
+    stage_barrier(CS);
 #ifdef RS_TRACE
     if (tr && tid == 0) tr[2] = clock64();
 #endif
     if constexpr (HASH) {
-      if (eoc && sub == 0 && a.hashes != nullptr) {
-        const uint64_t* rr = red + (cyc & 1u) * T * P + lin * P;
+      if (sub == 0 && a.hashes != nullptr) {
+        // the cluster's partials of cycle `pend` were all written before this barrier
+        if (pend >= 0 && rank == 0) {
+          const uint32_t pb = (uint32_t)pend & 1u;
 #pragma unroll
-        for (int p = 0; p < P; ++p) {
-          uint64_t sum = a.g.const_hash;
+          for (int p = 0; p < P; ++p) {
+            uint64_t sum = a.g.const_hash + lsum[pb * 32 + lin * P + p];
+            for (uint32_t r = 1; r < CS; ++r) sum += dsmem(lsum, r)[pb * 32 + lin * P + p];
+            if (lane + p < a.n_lanes) a.hashes[(size_t)pend * a.n_lanes + lane + p] = sum;
+          }
+        }
+        if (eoc) {
+          const uint64_t* rr = red + (cyc & 1u) * T * P + lin * P;
+#pragma unroll
+          for (int p = 0; p < P; ++p) {
+            uint64_t sum = 0;
 #pragma unroll 4
-          for (uint32_t i = 0; i < nsub; ++i) sum += rr[i * LTS * P + p];
-          if (lane + p < a.n_lanes) a.hashes[(size_t)cyc * a.n_lanes + lane + p] = sum;
+            for (uint32_t i = 0; i < nsub; ++i) sum += rr[i * LTS * P + p];
+            if (CS == 1) {
+              if (lane + p < a.n_lanes) a.hashes[(size_t)cyc * a.n_lanes + lane + p] = sum + a.g.const_hash;
+            } else {
+              lsum[(cyc & 1u) * 32 + lin * P + p] = sum;
+            }
+          }
         }
       }
+      if (CS > 1) pend = eoc ? (int)cyc : -1;  // any older pending cycle was summed above
     }
     if (eoc) {
       s = 0;
@@ -485,9 +533,25 @@ __global__ void __launch_bounds__(RS_LANES_MAX_THREADS, 1) k_lanes(const StepArg
       for (int p = 0; p < P; ++p) {
         uint64_t sum = 0;
         for (uint32_t i = 0; i < nsub; ++i) sum += hp_s[(i * LTS + lin) * P + p];
-        if (lane + p < a.n_lanes) a.hcarry_out[lane + p] = sum;
+        lsum[64 + lin * P + p] = sum;
       }
     }
+    stage_barrier(CS);
+    if (sub == 0 && rank == 0) {
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        uint64_t sum = lsum[64 + lin * P + p];
+        for (uint32_t r = 1; r < CS; ++r) sum += dsmem(lsum, r)[64 + lin * P + p];
+        if (lane + p < a.n_lanes) a.hcarry_out[lane + p] = sum;
+        if (pend >= 0 && a.hashes != nullptr) {  // last cycle's cluster-wide hash
+          const uint32_t pb = (uint32_t)pend & 1u;
+          uint64_t hs = a.g.const_hash + lsum[pb * 32 + lin * P + p];
+          for (uint32_t r = 1; r < CS; ++r) hs += dsmem(lsum, r)[pb * 32 + lin * P + p];
+          if (lane + p < a.n_lanes) a.hashes[(size_t)pend * a.n_lanes + lane + p] = hs;
+        }
+      }
+    }
+    if (CS > 1) stage_barrier(CS);  // keep every CTA's shared memory alive until rank 0 has read it
   }
 }
 

@@ -68,7 +68,7 @@ struct rs_graph {
 
 struct rs_lanes {
   rs_graph* g = nullptr;
-  uint32_t n_lanes = 0, LT = 1, n_tiles = 1, threads = 1024, ctas = 1;
+  uint32_t n_lanes = 0, LT = 1, n_tiles = 1, threads = 1024, ctas = 1, cluster = 1;
   uint64_t lane0 = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -121,6 +121,7 @@ StepArgs base_args(const rs_lanes* s) {
   a.n_stages = s->n_stages;
   a.stage_bytes = s->g->stage_bytes;
   a.trace = s->trace;
+  a.cluster = s->cluster;
   return a;
 }
 
@@ -172,12 +173,25 @@ size_t lanes_smem(uint32_t stage_bytes, uint32_t threads) {
   return 128 + 2ull * stage_bytes + lanes_smem_extra(threads);
 }
 
-int choose_lt(uint32_t n_lanes, int sms) {
-  for (int lt : {32, 16, 8}) {
-    const uint64_t tiles = (n_lanes + lt - 1) / lt;
-    if (tiles * 10 >= (uint64_t)sms * 8) return lt;   // >= 80% of the SMs busy
+// Lane tile and cluster size: the widest tile (32 lanes: every warp
+// instruction does 32 lanes of work), spread over the fewest CTAs of a
+// cluster that keeps >= 80% of the SMs busy; narrower tiles only when even an
+// 8-CTA cluster per 32-lane tile cannot fill the GPU.
+void choose_tiling(uint32_t n_lanes, int sms, uint32_t want_lt, uint32_t want_cs, uint32_t* lt, uint32_t* cs) {
+  for (uint32_t t : {32u, 16u, 8u}) {
+    if (want_lt && t != want_lt) continue;
+    const uint64_t tiles = (n_lanes + t - 1) / t;
+    for (uint32_t c : {1u, 2u, 4u, 8u}) {
+      if (want_cs && c != want_cs) continue;
+      if (tiles * c * 10 >= (uint64_t)sms * 8 || (want_lt && want_cs) || (t == 8 && c == 8)) {
+        *lt = t;
+        *cs = c;
+        return;
+      }
+    }
   }
-  return 8;
+  *lt = want_lt ? want_lt : 8;
+  *cs = want_cs ? want_cs : 8;
 }
 
 }  // namespace
@@ -344,9 +358,18 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     s->LT = 1;
     s->n_tiles = 1;
   } else {
-    uint32_t lt = o.lane_tile ? o.lane_tile : (uint32_t)choose_lt(n_lanes, g->sm_count);
-    if (lt != 8 && lt != 16 && lt != 32) { delete s; return set_err(RS_E_INVALID_ARG, "lane_tile must be 8, 16 or 32"); }
+    if (o.lane_tile && o.lane_tile != 8 && o.lane_tile != 16 && o.lane_tile != 32) {
+      delete s;
+      return set_err(RS_E_INVALID_ARG, "lane_tile must be 8, 16 or 32");
+    }
+    if (o.cluster && o.cluster != 1 && o.cluster != 2 && o.cluster != 4 && o.cluster != 8) {
+      delete s;
+      return set_err(RS_E_INVALID_ARG, "cluster must be 1, 2, 4 or 8");
+    }
+    uint32_t lt, cs;
+    choose_tiling(n_lanes, g->sm_count, o.lane_tile, o.cluster, &lt, &cs);
     s->LT = lt;
+    s->cluster = cs;
     s->n_tiles = (n_lanes + lt - 1) / lt;
   }
   // launch shape
@@ -357,7 +380,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
   } else if (g->cg.mode == RS_MODE_SINGLE) {
     s->threads = 1024;
   } else {
-    const uint32_t per_sm = (s->n_tiles + g->sm_count - 1) / g->sm_count;
+    const uint32_t per_sm = (s->n_tiles * s->cluster + g->sm_count - 1) / g->sm_count;
     uint32_t th = RS_LANES_MAX_THREADS / std::max<uint32_t>(1, per_sm);
     th = std::max<uint32_t>(64, th & ~31u);
     s->threads = th;
@@ -374,7 +397,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     const uint32_t maxc = (uint32_t)std::max(1, occ) * g->sm_count;
     s->ctas = std::max<uint32_t>(1, std::min(ctas, maxc));
   } else {
-    s->ctas = s->n_tiles;
+    s->ctas = s->n_tiles * s->cluster;
   }
   // state: [n_tiles][class 0 rows x LT | class 1 | class 2 | class 3], regions 128-B aligned
   uint64_t off = 0;
@@ -602,24 +625,29 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
   } else {
     a.hcarry_out = a.hcarry_in;
     const size_t smem = lanes_smem(s->g->stage_bytes, s->threads);
-    const dim3 grid(s->n_tiles), block(s->threads);
+    const void* fns[] = {(const void*)k_lanes<32, true>, (const void*)k_lanes<32, false>,
+                         (const void*)k_lanes<16, true>, (const void*)k_lanes<16, false>,
+                         (const void*)k_lanes<8, true>,  (const void*)k_lanes<8, false>};
     static size_t attr_set = 0;
     if (attr_set < smem) {
-      const void* fns[] = {(const void*)k_lanes<32, true>, (const void*)k_lanes<32, false>,
-                           (const void*)k_lanes<16, true>, (const void*)k_lanes<16, false>,
-                           (const void*)k_lanes<8, true>,  (const void*)k_lanes<8, false>};
       for (const void* f : fns) CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       attr_set = smem;
     }
-    switch (s->LT * 2 + (hash ? 1 : 0)) {
-      case 65: k_lanes<32, true><<<grid, block, smem, s->stream>>>(a); break;
-      case 64: k_lanes<32, false><<<grid, block, smem, s->stream>>>(a); break;
-      case 33: k_lanes<16, true><<<grid, block, smem, s->stream>>>(a); break;
-      case 32: k_lanes<16, false><<<grid, block, smem, s->stream>>>(a); break;
-      case 17: k_lanes<8, true><<<grid, block, smem, s->stream>>>(a); break;
-      default: k_lanes<8, false><<<grid, block, smem, s->stream>>>(a); break;
-    }
-    cudaError_t e = cudaGetLastError();
+    const int fi = (s->LT == 32 ? 0 : s->LT == 16 ? 2 : 4) + (hash ? 0 : 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(s->n_tiles * s->cluster);
+    cfg.blockDim = dim3(s->threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = s->cluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    void* args[] = {&a};
+    cudaError_t e = cudaLaunchKernelExC(&cfg, fns[fi], args);
     if (e != cudaSuccess) return set_err(RS_E_CUDA, "k_lanes launch: %s", cudaGetErrorString(e));
   }
   s->launches++;
@@ -729,7 +757,8 @@ rs_status rs_debug_trace(rs_lanes* s, uint64_t* out, uint64_t n) {
 #endif
 }
 
-rs_status rs_launch_shape(const rs_lanes* s, uint32_t* lt, uint32_t* threads, uint32_t* ctas) {
+rs_status rs_launch_shape(const rs_lanes* s, uint32_t* lt, uint32_t* threads, uint32_t* ctas, uint32_t* cluster) {
+  if (s && cluster) *cluster = s->cluster;
   if (!s) return set_err(RS_E_INVALID_ARG, "NULL lanes");
   if (lt) *lt = s->LT;
   if (threads) *threads = s->threads;

@@ -63,7 +63,7 @@ class GraphInfo(C.Structure):
 
 class LaneOpts(C.Structure):
     _fields_ = [("lane0", C.c_uint64), ("lane_tile", C.c_uint32), ("threads", C.c_uint32),
-                ("stage_cycles", C.c_uint32), ("unroll_hint", C.c_uint32), ("stream", C.c_void_p)]
+                ("stage_cycles", C.c_uint32), ("cluster", C.c_uint32), ("stream", C.c_void_p)]
 
 
 _lib = None
@@ -96,7 +96,7 @@ def lib() -> C.CDLL:
             "rs_get_cycle": (i32, [vp, C.POINTER(u64)]),
             "rs_set_cycle": (i32, [vp, u64]),
             "rs_launch_count": (u64, [vp]),
-            "rs_launch_shape": (i32, [vp, C.POINTER(u32), C.POINTER(u32), C.POINTER(u32)]),
+            "rs_launch_shape": (i32, [vp, C.POINTER(u32), C.POINTER(u32), C.POINTER(u32), C.POINTER(u32)]),
             "rs_sync": (i32, [vp]),
             "rs_graph_export": (i32, [vp, u32, vp, C.POINTER(u64)]),
             "rs_debug_trace": (i32, [vp, vp, u64]),
@@ -194,12 +194,12 @@ class Lanes:
     lane0 .. lane0 + n_lanes - 1)."""
 
     def __init__(self, graph: Graph, n_lanes: int, lane0: int = 0, lane_tile: int = 0, threads: int = 0,
-                 stage_cycles: int = 0, stream=None):
+                 stage_cycles: int = 0, stream=None, cluster: int = 0):
         self.graph = graph
         self.n_lanes = n_lanes
         self.lane0 = lane0
         st = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
-        self.opts = LaneOpts(lane0, lane_tile, threads, stage_cycles, 0, st)
+        self.opts = LaneOpts(lane0, lane_tile, threads, stage_cycles, cluster, st)
         h = C.c_void_p()
         _check(lib().rs_alloc_lanes(graph.h, n_lanes, C.byref(self.opts), C.byref(h)))
         self.h = h
@@ -269,9 +269,9 @@ class Lanes:
         return int(lib().rs_launch_count(self.h))
 
     def shape(self):
-        lt, th, ct = C.c_uint32(), C.c_uint32(), C.c_uint32()
-        _check(lib().rs_launch_shape(self.h, C.byref(lt), C.byref(th), C.byref(ct)))
-        return {"lane_tile": lt.value, "threads": th.value, "ctas": ct.value}
+        lt, th, ct, cs = C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_uint32()
+        _check(lib().rs_launch_shape(self.h, C.byref(lt), C.byref(th), C.byref(ct), C.byref(cs)))
+        return {"lane_tile": lt.value, "threads": th.value, "ctas": ct.value, "cluster": cs.value}
 
     def nbytes(self) -> int:
         return int(lib().rs_lanes_bytes(self.h))

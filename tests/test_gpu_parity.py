@@ -17,9 +17,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def run_gpu(rs, c, n_cycles, n_lanes=1, seed=0, mode="lanes", lane0=0, lane_tile=0, threads=0,
-            staged=None, chunks=None, final=True):
+            staged=None, chunks=None, final=True, cluster=0):
     g = rs.Graph(c, device=0, mode=mode)
-    L = rs.Lanes(g, n_lanes, lane0=lane0, lane_tile=lane_tile, threads=threads,
+    L = rs.Lanes(g, n_lanes, lane0=lane0, lane_tile=lane_tile, threads=threads, cluster=cluster,
                  stage_cycles=(n_cycles if staged is not None else 0))
     if staged is not None:
         L.set_inputs(0, staged)
@@ -79,10 +79,11 @@ def test_c1_full(rs, mode):
     check(rs, config_circuit("C1"), cfg.cycles, 1, seed=cfg.stim_seed, mode=mode)
 
 
-@pytest.mark.parametrize("lt", [8, 16, 32])
-def test_c2_structure_ragged_lanes(rs, lt):
-    """Full C2 circuit, 37 lanes (ragged last tile), 25 cycles, each lane tile."""
-    check(rs, config_circuit("C2"), 25, 37, seed=CONFIGS["C2"].stim_seed, lane_tile=lt)
+@pytest.mark.parametrize("lt,cs", [(8, 1), (16, 1), (32, 1), (32, 4), (16, 2), (8, 8)])
+def test_c2_structure_ragged_lanes(rs, lt, cs):
+    """Full C2 circuit, 37 lanes (ragged last tile), 25 cycles, each lane tile,
+    one CTA or a thread-block cluster per tile."""
+    check(rs, config_circuit("C2"), 25, 37, seed=CONFIGS["C2"].stim_seed, lane_tile=lt, cluster=cs)
 
 
 def test_c2_threads_variants(rs):

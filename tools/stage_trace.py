@@ -52,6 +52,8 @@ def main():
     tot = np.diff(rows[:, 0])
     print(f"per stage (cycles): total {np.mean(tot):.0f}  wait {np.mean(wait):.0f}  "
           f"work max {np.mean(work_max):.0f} min {np.mean(work_min):.0f}  barrier-after-max {np.mean(bar):.0f}")
+    per_warp = (rows[:, 3:] - rows[:, 1:2]).mean(axis=0)
+    print("mean work end per warp:", " ".join(f"{v:.0f}" for v in per_warp))
     for i in range(min(S, 60)):
         idx = np.arange(i, len(rows) - 1, S)
         print(f"  stage {i:3d}: total {np.mean(tot[idx]) if len(idx) else 0:8.0f} wait {np.mean(wait[idx]):7.0f} "
