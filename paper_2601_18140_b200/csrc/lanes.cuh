@@ -170,11 +170,77 @@ __device__ __forceinline__ void batch_compute(uint32_t op, const uint64_t (&x)[U
 #undef X2
 #undef P0
 #undef P1
+}
+
+// Mask to the out width, hash, store: once per batch per out class (uniform
+// over the run).  Out classes <= 32 bit take a 32-bit path: 32-bit mask, a
+// 32 x 64-bit hash multiply, and the P lanes packed into one store.
+template <int LT, int P, bool HASH, int U>
+__device__ __forceinline__ void batch_store(const LaneP<P>& L, uint32_t out_cls, uint32_t out_byte0, uint32_t cnt,
+                                            uint32_t s_k, const uint32_t (&pw)[U], const uint64_t (&y)[U][P],
+                                            uint64_t (&hacc)[P]) {
+  uint8_t* ob = L.tb + out_byte0 + ((L.lin * P) << out_cls);
+  const uint32_t ostride = (uint32_t)LT << out_cls;
+  if (out_cls < 3u) {
+    uint32_t v[U][P];
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const uint64_t m = wmask(pw[u] & 127u);
+    for (int u = 0; u < U; ++u) {
+      const uint32_t m32 = 0xFFFFFFFFu >> (32u - (pw[u] & 127u));  // w_out <= 32
 #pragma unroll
-    for (int p = 0; p < P; ++p) y[u][p] &= m;
+      for (int p = 0; p < P; ++p) v[u][p] = (uint32_t)y[u][p] & m32;
+    }
+    if constexpr (HASH) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if ((uint32_t)u < cnt) {
+          const uint64_t k = lds64(s_k + 8 * u);
+#pragma unroll
+          for (int p = 0; p < P; ++p) hacc[p] += (uint64_t)v[u][p] * k;
+        }
+    }
+    if (out_cls == 0u) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if ((uint32_t)u < cnt) {
+          if constexpr (P == 2) *reinterpret_cast<uint16_t*>(ob + u * ostride) = (uint16_t)(v[u][0] | (v[u][1] << 8));
+          else _Pragma("unroll") for (int p = 0; p < P; ++p) ob[u * ostride + p] = (uint8_t)v[u][p];
+        }
+    } else if (out_cls == 1u) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if ((uint32_t)u < cnt) {
+          if constexpr (P == 2) *reinterpret_cast<uint32_t*>(ob + u * ostride) = v[u][0] | (v[u][1] << 16);
+          else _Pragma("unroll") for (int p = 0; p < P; ++p)
+              reinterpret_cast<uint16_t*>(ob + u * ostride)[p] = (uint16_t)v[u][p];
+        }
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if ((uint32_t)u < cnt) {
+          if constexpr (P == 2)
+            *reinterpret_cast<uint2*>(ob + u * ostride) = make_uint2(v[u][0], v[u][1]);
+          else _Pragma("unroll") for (int p = 0; p < P; ++p)
+              reinterpret_cast<uint32_t*>(ob + u * ostride)[p] = v[u][p];
+        }
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if ((uint32_t)u < cnt) {
+        const uint64_t m = wmask(pw[u] & 127u);
+        uint64_t z[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) z[p] = y[u][p] & m;
+        if constexpr (HASH) {
+          const uint64_t k = lds64(s_k + 8 * u);
+#pragma unroll
+          for (int p = 0; p < P; ++p) hacc[p] += z[p] * k;
+        }
+        if constexpr (P == 2)
+          *reinterpret_cast<ulonglong2*>(ob + u * ostride) = make_ulonglong2(z[0], z[1]);
+        else _Pragma("unroll") for (int p = 0; p < P; ++p)
+            reinterpret_cast<uint64_t*>(ob + u * ostride)[p] = z[p];
+      }
   }
 }
 
@@ -210,17 +276,7 @@ __device__ __forceinline__ void batch_ops(const LaneP<P>& L, uint32_t op, uint32
     }
   uint64_t y[U][P];
   batch_compute<U, A, P>(op, x, pw, y);
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    if ((uint32_t)u < cnt) {
-      if constexpr (HASH) {
-        const uint64_t k = lds64(s_k + 8 * u);
-#pragma unroll
-        for (int p = 0; p < P; ++p) hacc[p] += y[u][p] * k;
-      }
-      store_lanes<P>(L, out_cls, out_byte0 + u * ((uint32_t)LT << out_cls), y[u]);
-    }
-  }
+  batch_store<LT, P, HASH, U>(L, out_cls, out_byte0, cnt, s_k, pw, y, hacc);
 }
 
 // Folds with more than 3 operands (left fold over the O rank; rare).
