@@ -478,4 +478,99 @@ void build_stages(const CompiledGraph& g, uint32_t stage_bytes, std::vector<uint
   }
 }
 
+bool build_single_slices(const CompiledGraph& g, uint32_t G, uint32_t max_bytes, std::vector<uint8_t>* blob,
+                         std::vector<uint64_t>* slice_off) {
+  blob->clear();
+  slice_off->assign(G, 0);
+  auto chunk = [](uint32_t n, uint32_t part, uint32_t parts, uint32_t& b, uint32_t& e) {
+    const uint32_t c = (n + parts - 1) / parts;
+    b = std::min(n, part * c);
+    e = std::min(n, b + c);
+  };
+  for (uint32_t cta = 0; cta < G; ++cta) {
+    std::vector<SliceLvl> lv(g.n_levels);
+    std::vector<SliceSeg> seg;
+    std::vector<uint32_t> pw, coords, latch, inj;
+    std::vector<uint16_t> cofs;
+    for (uint32_t l = 0; l < g.n_levels; ++l) {
+      const uint32_t ob = g.level_op_begin[l], oe = g.level_op_begin[l + 1];
+      uint32_t b, e;
+      chunk(oe - ob, cta, G, b, e);
+      b += ob;
+      e += ob;
+      SliceLvl& L = lv[l];
+      L = SliceLvl{};
+      L.op_begin = b;
+      L.n = e - b;
+      L.pw_base = (uint32_t)pw.size();
+      L.coord_base = (uint32_t)coords.size();
+      L.seg_begin = (uint32_t)seg.size();
+      for (uint32_t r = g.level_run_begin[l]; r < g.level_run_begin[l + 1]; ++r) {
+        const DevRun& R = g.runs[r];
+        const uint32_t s0 = std::max(b, R.op_begin), s1 = std::min(e, R.op_begin + R.count);
+        if (s0 >= s1) continue;
+        SliceSeg sg{};
+        sg.first = s0 - b;
+        sg.count = s1 - s0;
+        sg.out_coord0 = make_coord((R.meta >> 16) & 3u, R.out_row0 + (s0 - R.op_begin));
+        seg.push_back(sg);
+      }
+      L.n_seg = (uint32_t)seg.size() - L.seg_begin;
+      for (uint32_t j = b; j < e; ++j) {
+        pw.push_back(g.opw[j]);
+        const uint32_t off = (uint32_t)coords.size() - L.coord_base;
+        if (off > 0xFFFFu) return false;
+        cofs.push_back((uint16_t)off);
+        for (uint32_t k = g.coord_off[j]; k < g.coord_off[j + 1]; ++k) coords.push_back(g.coord[k]);
+      }
+    }
+    uint32_t rb, re, ib, ie;
+    chunk(g.n_regs, cta, G, rb, re);
+    chunk(g.n_inputs, cta, G, ib, ie);
+    for (uint32_t i = rb; i < re; ++i) {
+      latch.push_back(g.reg_next_coord[i]);
+      latch.push_back(g.reg_coord[i]);
+      latch.push_back(g.reg_w[i]);
+    }
+    for (uint32_t i = ib; i < ie; ++i) {
+      inj.push_back(g.in_coord[i]);
+      inj.push_back(g.in_w[i]);
+    }
+    SliceHdr h{};
+    h.n_levels = g.n_levels;
+    h.off_lvl = al16((uint32_t)sizeof(SliceHdr));
+    h.off_seg = al16(h.off_lvl + (uint32_t)(lv.size() * sizeof(SliceLvl)));
+    h.off_pw = al16(h.off_seg + (uint32_t)(seg.size() * sizeof(SliceSeg)));
+    h.off_cofs = al16(h.off_pw + 4u * (uint32_t)pw.size());
+    h.off_coord = al16(h.off_cofs + 2u * (uint32_t)cofs.size());
+    h.off_latch = al16(h.off_coord + 4u * (uint32_t)coords.size());
+    h.off_inj = al16(h.off_latch + 4u * (uint32_t)latch.size());
+    h.bytes = al16(h.off_inj + 4u * (uint32_t)inj.size());
+    h.latch_first = rb;
+    h.n_latch = re - rb;
+    h.inj_first = ib;
+    h.n_inj = ie - ib;
+    if (h.bytes > max_bytes) {
+      blob->clear();
+      return false;
+    }
+    const size_t base = (blob->size() + 127) & ~(size_t)127;
+    blob->resize(base + h.bytes, 0);
+    uint8_t* p = blob->data() + base;
+    std::memcpy(p, &h, sizeof h);
+    auto put = [&](uint32_t off, const void* src, size_t n) {
+      if (n) std::memcpy(p + off, src, n);
+    };
+    put(h.off_lvl, lv.data(), lv.size() * sizeof(SliceLvl));
+    put(h.off_seg, seg.data(), seg.size() * sizeof(SliceSeg));
+    put(h.off_pw, pw.data(), pw.size() * 4);
+    put(h.off_cofs, cofs.data(), cofs.size() * 2);
+    put(h.off_coord, coords.data(), coords.size() * 4);
+    put(h.off_latch, latch.data(), latch.size() * 4);
+    put(h.off_inj, inj.data(), inj.size() * 4);
+    (*slice_off)[cta] = base;
+  }
+  return true;
+}
+
 }  // namespace rtlsim

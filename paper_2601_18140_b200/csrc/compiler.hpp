@@ -155,4 +155,37 @@ struct StageRef {
 void build_stages(const CompiledGraph& g, uint32_t stage_bytes, std::vector<uint8_t>* blob,
                   std::vector<StageRef>* table);
 
+// ---------------------------------------------------------------- single-lane slices
+// Single-lane mode: CTA g of a G-CTA persistent grid owns a fixed contiguous
+// chunk of every level's ops (and of the registers / inputs); its descriptors
+// stay resident in shared memory for the whole launch.  Layout of one slice
+// (16-byte aligned sections, offsets in SliceHdr):
+//   SliceLvl[n_levels] | SliceSeg[...] | pw u32[ops] | cofs u16[ops] | coords u32[...]
+//   | latch {next coord, reg coord, width} u32x3[n_latch] | inject {coord, width} u32x2[n_inj]
+struct SliceHdr {
+  uint32_t bytes;
+  uint32_t n_levels;
+  uint32_t off_lvl, off_seg, off_pw, off_cofs, off_coord, off_latch, off_inj;
+  uint32_t latch_first, n_latch;   // registers [latch_first, latch_first + n_latch)
+  uint32_t inj_first, n_inj;       // inputs [inj_first, inj_first + n_inj)
+  uint32_t pad[3];
+};
+struct SliceLvl {
+  uint32_t op_begin;   // global op index of the chunk's first op (hash weights)
+  uint32_t n;          // ops in the chunk
+  uint32_t pw_base;    // index of its first op in the slice's pw / cofs arrays
+  uint32_t coord_base; // index of its first coord in the slice's coords array
+  uint32_t seg_begin, n_seg;
+  uint32_t pad[2];
+};
+struct SliceSeg {      // a run piece inside a chunk: outputs are consecutive rows of one class
+  uint32_t first;      // chunk-relative index of the piece's first op
+  uint32_t count;
+  uint32_t out_coord0; // (class << 30) | row of the first op's output
+  uint32_t pad;
+};
+// Returns false (and builds nothing) if a slice would exceed max_bytes.
+bool build_single_slices(const CompiledGraph& g, uint32_t G, uint32_t max_bytes, std::vector<uint8_t>* blob,
+                         std::vector<uint64_t>* slice_off);
+
 }  // namespace rtlsim

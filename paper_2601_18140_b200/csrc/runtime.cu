@@ -14,6 +14,7 @@
 #include "compiler.hpp"
 #include "kernels.cuh"
 #include "lanes.cuh"
+#include "single.cuh"
 
 using namespace rtlsim;
 
@@ -94,6 +95,11 @@ struct rs_lanes {
   unsigned long long* bar = nullptr;
   uint64_t launches = 0;
   unsigned long long* trace = nullptr;  // RS_TRACE builds only
+  // single-lane mode: per-CTA graph slices resident in shared memory (single.cuh)
+  void* dslices = nullptr;               // blob, then u64 offsets per CTA
+  const uint8_t* slice_blob = nullptr;
+  const uint64_t* slice_off = nullptr;
+  uint32_t slice_max = 0;
   size_t total_bytes = 0;
 };
 
@@ -390,12 +396,48 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     uint32_t maxops = 0;
     for (uint32_t l = 0; l < g->cg.n_levels; ++l)
       maxops = std::max(maxops, g->cg.level_op_begin[l + 1] - g->cg.level_op_begin[l]);
-    const uint32_t need = std::max(work, maxops);
-    uint32_t ctas = (need + s->threads - 1) / s->threads;
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_single<true>, s->threads, 0);
-    const uint32_t maxc = (uint32_t)std::max(1, occ) * g->sm_count;
-    s->ctas = std::max<uint32_t>(1, std::min(ctas, maxc));
+    // resident-slice kernel (single.cuh): fewest CTAs whose graph slices fit in shared memory
+    const CompiledGraph& cg = g->cg;
+    const uint64_t est = 6ull * cg.n_ops_total() + 4ull * cg.coord.size() + 12ull * cg.n_regs + 8ull * cg.n_inputs;
+    const uint32_t kMaxSlice = 200 * 1024;
+    uint32_t G = (uint32_t)std::max<uint64_t>({1, (est + kMaxSlice / 2) / (kMaxSlice * 3 / 4), (maxops + 1023) / 1024});
+    G = std::min<uint32_t>(G, (uint32_t)g->sm_count);
+    std::vector<uint8_t> sblob;
+    std::vector<uint64_t> soff;
+    bool ok = false;
+    while (true) {
+      ok = build_single_slices(cg, G, kMaxSlice, &sblob, &soff);
+      if (ok || G >= (uint32_t)g->sm_count) break;
+      G = std::min<uint32_t>((uint32_t)g->sm_count, G + std::max<uint32_t>(1, G / 4));
+    }
+    if (ok && !o.threads) {
+      const uint32_t chunk = std::max<uint32_t>(1, (maxops + G - 1) / G);
+      s->threads = std::min<uint32_t>(1024, std::max<uint32_t>(32, (chunk + 31) & ~31u));
+    }
+    if (ok) {
+      uint32_t smax = 0;
+      for (uint32_t i = 0; i < G; ++i) smax = std::max(smax, reinterpret_cast<const SliceHdr*>(sblob.data() + soff[i])->bytes);
+      const size_t off_off = (sblob.size() + 255) & ~(size_t)255;
+      cudaError_t e2 = cudaMalloc(&s->dslices, off_off + G * 8);
+      if (e2 == cudaSuccess) e2 = cudaMemcpy(s->dslices, sblob.data(), sblob.size(), cudaMemcpyHostToDevice);
+      if (e2 == cudaSuccess) e2 = cudaMemcpy((uint8_t*)s->dslices + off_off, soff.data(), G * 8, cudaMemcpyHostToDevice);
+      if (e2 != cudaSuccess) {
+        delete s;
+        return set_err(RS_E_OOM, "single-lane slices: %s", cudaGetErrorString(e2));
+      }
+      s->slice_blob = (const uint8_t*)s->dslices;
+      s->slice_off = (const uint64_t*)((const uint8_t*)s->dslices + off_off);
+      s->slice_max = smax;
+      s->ctas = G;
+      s->total_bytes += off_off + G * 8;
+    } else {  // graph too large for resident slices: descriptors streamed from global memory
+      const uint32_t need = std::max(work, maxops);
+      uint32_t ctas = (need + s->threads - 1) / s->threads;
+      int occ = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_single<true>, s->threads, 0);
+      const uint32_t maxc = (uint32_t)std::max(1, occ) * g->sm_count;
+      s->ctas = std::max<uint32_t>(1, std::min(ctas, maxc));
+    }
   } else {
     s->ctas = s->n_tiles * s->cluster;
   }
@@ -505,6 +547,7 @@ void rs_free_lanes(rs_lanes* s) {
   if (s->stream) cudaStreamSynchronize(s->stream);
   if (s->state_mem) cudaFree(s->state_mem);
   if (s->dstages) cudaFree(s->dstages);
+  if (s->dslices) cudaFree(s->dslices);
   if (s->hcarry) cudaFree(s->hcarry);
   if (s->bar) cudaFree(s->bar);
   if (s->stage) cudaFree(s->stage);
@@ -617,9 +660,20 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
       if (hout) CU(cudaMemsetAsync(hout, 0, hn * 8, s->stream));
     }
     CU(cudaMemsetAsync(s->bar, 0, 8, s->stream));
-    void* args[] = {&a};
-    cudaError_t e = hash ? cudaLaunchCooperativeKernel((const void*)k_single<true>, s->ctas, s->threads, args, 0, s->stream)
-                         : cudaLaunchCooperativeKernel((const void*)k_single<false>, s->ctas, s->threads, args, 0, s->stream);
+    cudaError_t e;
+    if (s->slice_blob) {
+      SingleArgs sa{a, s->slice_blob, s->slice_off, s->slice_max};
+      void* args[] = {&sa};
+      const bool grid = s->ctas > 1;
+      const void* fn = grid ? (hash ? (const void*)k_single2<true, true> : (const void*)k_single2<true, false>)
+                            : (hash ? (const void*)k_single2<false, true> : (const void*)k_single2<false, false>);
+      CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->slice_max));
+      e = cudaLaunchCooperativeKernel(fn, s->ctas, s->threads, args, s->slice_max, s->stream);
+    } else {
+      void* args[] = {&a};
+      e = hash ? cudaLaunchCooperativeKernel((const void*)k_single<true>, s->ctas, s->threads, args, 0, s->stream)
+               : cudaLaunchCooperativeKernel((const void*)k_single<false>, s->ctas, s->threads, args, 0, s->stream);
+    }
     if (e != cudaSuccess) return set_err(RS_E_CUDA, "k_single launch: %s", cudaGetErrorString(e));
     if (hash) s->hc_cur = 1 - s->hc_cur;
   } else {

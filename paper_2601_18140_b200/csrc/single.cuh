@@ -1,0 +1,219 @@
+// single.cuh -- single-lane step kernel (RS_MODE_SINGLE; configs C1, C5).
+//
+// One lane has no lane parallelism; the parallel axis is the ops of a level
+// (the S rank of Cascade 1).  A persistent grid of G CTAs (cooperative launch:
+// all co-resident) walks the cycle; CTA g owns a fixed contiguous chunk of
+// every level's ops, registers and inputs, whose descriptors (param words,
+// operand coordinates, output run pieces) it copies into shared memory once per
+// launch (compiler.hpp build_single_slices) -- the per-level critical path is
+// then one state gather (L2) plus one grid barrier.  The grid barrier is a
+// release-add / acquire-poll on one counter; with G == 1 it is __syncthreads
+// and the state is read through L1.
+#pragma once
+#include "kernels.cuh"
+
+namespace rtlsim {
+
+struct SingleArgs {
+  StepArgs a;
+  const uint8_t* slice_blob;
+  const uint64_t* slice_off;
+  uint32_t slice_max;  // bytes of the largest slice (dynamic shared memory)
+};
+
+__device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Grid barrier; before it, each warp's lane 0 has put the warp's hash partial
+// in wsum[warp] (or 0): the CTA's sum is added to *hsum (relaxed atomic) by
+// thread 0 on the way in.
+template <bool GRID>
+__device__ __forceinline__ void single_barrier(unsigned long long* bar, unsigned long long& target, uint64_t* wsum,
+                                               unsigned long long* hsum) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (hsum) {
+      uint64_t s = 0;
+      for (uint32_t w = 0; w < (blockDim.x + 31) / 32; ++w) s += wsum[w];
+      atomicAdd(hsum, (unsigned long long)s);
+    }
+    if constexpr (GRID) {
+      target += gridDim.x;
+      red_release_add(bar, 1ull);
+      while (ld_acquire(bar) < target) {
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void warp_partial(uint64_t v, uint64_t* wsum) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = v;
+}
+
+template <bool GRID>
+struct SState {
+  uint8_t* base;
+  uint64_t r1, r2, r3;  // class region offsets (class 0 region starts at 0 after rebasing)
+  __device__ __forceinline__ uint8_t* addr(uint32_t c) const {
+    const uint32_t cls = c >> 30;
+    const uint64_t reg = cls == 0 ? 0 : cls == 1 ? r1 : cls == 2 ? r2 : r3;
+    return base + reg + ((uint64_t)(c & ROW_MASK) << cls);
+  }
+  __device__ __forceinline__ uint64_t ld(uint32_t c) const {
+    const uint8_t* p = addr(c);
+    if constexpr (GRID) {
+      switch (c >> 30) {
+        case 0: return __ldcg(p);
+        case 1: return __ldcg(reinterpret_cast<const uint16_t*>(p));
+        case 2: return __ldcg(reinterpret_cast<const uint32_t*>(p));
+        default: return __ldcg(reinterpret_cast<const uint64_t*>(p));
+      }
+    } else {
+      switch (c >> 30) {
+        case 0: return *p;
+        case 1: return *reinterpret_cast<const uint16_t*>(p);
+        case 2: return *reinterpret_cast<const uint32_t*>(p);
+        default: return *reinterpret_cast<const uint64_t*>(p);
+      }
+    }
+  }
+  __device__ __forceinline__ void st(uint32_t c, uint64_t v) const {
+    uint8_t* p = addr(c);
+    switch (c >> 30) {
+      case 0: *p = (uint8_t)v; break;
+      case 1: *reinterpret_cast<uint16_t*>(p) = (uint16_t)v; break;
+      case 2: *reinterpret_cast<uint32_t*>(p) = (uint32_t)v; break;
+      default: *reinterpret_cast<uint64_t*>(p) = v; break;
+    }
+  }
+};
+
+// One op of a level chunk: gather (eq:split_einsum1), op_u / op_r / op_s.
+template <bool GRID>
+__device__ __forceinline__ uint64_t single_eval(const SState<GRID>& S, uint32_t pw, const uint32_t* cp) {
+  const uint32_t op = (pw >> 22) & 15u, n = pw >> 26, p0 = (pw >> 7) & 127u;
+  uint64_t x0 = S.ld(cp[0]), x1 = 0, x2 = 0;
+  if (n >= 2) x1 = S.ld(cp[1]);
+  if (n >= 3) x2 = S.ld(cp[2]);
+  uint64_t r;
+  switch (op) {
+    case RS_OP_AND: r = x0 & x1; if (n >= 3) r &= x2; break;
+    case RS_OP_OR: r = x0 | x1; if (n >= 3) r |= x2; break;
+    case RS_OP_XOR: r = x0 ^ x1; if (n >= 3) r ^= x2; break;
+    case RS_OP_ADD: r = x0 + x1; if (n >= 3) r += x2; break;
+    case RS_OP_SUB: r = x0 - x1; if (n >= 3) r -= x2; break;
+    case RS_OP_MUL: r = x0 * x1; if (n >= 3) r *= x2; break;
+    case RS_OP_EQ: r = x0 == x1 ? 1ull : 0ull; break;
+    case RS_OP_LT: r = x0 < x1 ? 1ull : 0ull; break;
+    case RS_OP_NOT: r = ~x0; break;
+    case RS_OP_SHL: r = p0 >= 64 ? 0ull : (x0 << p0); break;
+    case RS_OP_SHR: r = p0 >= 64 ? 0ull : (x0 >> p0); break;
+    case RS_OP_BITS: {
+      const uint32_t lo = (pw >> 14) & 63u;
+      r = (x0 >> lo) & wmask(p0 - lo + 1u);
+      break;
+    }
+    case RS_OP_CAT: r = p0 >= 64 ? x1 : ((x0 << p0) | x1); break;
+    case RS_OP_MUX: r = x0 != 0 ? x1 : x2; break;
+    default: r = x0; break;  // OP_COPY
+  }
+  if (n > 3 && op <= RS_OP_MUL)  // rare long folds (left fold over the O rank)
+    for (uint32_t o = 3; o < n; ++o) r = fold_step(op, r, S.ld(cp[o]));
+  return r & wmask(pw & 127u);
+}
+
+template <bool GRID, bool HASH>
+__global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
+  const StepArgs& a = sa.a;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t wsum[32];
+  const uint32_t tid = threadIdx.x, T = blockDim.x;
+  {  // this CTA's slice of the graph, resident for the whole launch
+    const uint8_t* src = sa.slice_blob + sa.slice_off[blockIdx.x];
+    const uint32_t bytes = reinterpret_cast<const SliceHdr*>(src)->bytes;
+    for (uint32_t i = tid * 16; i < bytes; i += T * 16)
+      *reinterpret_cast<uint4*>(smem + i) = __ldg(reinterpret_cast<const uint4*>(src + i));
+  }
+  if (tid < 32) wsum[tid] = 0;
+  __syncthreads();
+  const SliceHdr* h = reinterpret_cast<const SliceHdr*>(smem);
+  const SliceLvl* lvl = reinterpret_cast<const SliceLvl*>(smem + h->off_lvl);
+  const SliceSeg* seg = reinterpret_cast<const SliceSeg*>(smem + h->off_seg);
+  const uint32_t* pws = reinterpret_cast<const uint32_t*>(smem + h->off_pw);
+  const uint16_t* cofs = reinterpret_cast<const uint16_t*>(smem + h->off_cofs);
+  const uint32_t* crd = reinterpret_cast<const uint32_t*>(smem + h->off_coord);
+  const uint32_t* lat = reinterpret_cast<const uint32_t*>(smem + h->off_latch);
+  const uint32_t* inj = reinterpret_cast<const uint32_t*>(smem + h->off_inj);
+
+  SState<GRID> S;
+  S.base = a.state + a.region[0];
+  S.r1 = a.region[1] - a.region[0];
+  S.r2 = a.region[2] - a.region[0];
+  S.r3 = a.region[3] - a.region[0];
+  unsigned long long target = 0;
+  uint64_t hacc = (HASH && blockIdx.x == 0 && tid == 0) ? a.hcarry_in[0] + a.g.const_hash : 0ull;
+
+  auto inject = [&](uint64_t cyc) -> uint64_t {
+    uint64_t hh = 0;
+    for (uint32_t i = tid; i < h->n_inj; i += T) {
+      const uint32_t k = h->inj_first + i;
+      uint64_t v = a.staged ? __ldg(a.stage + (size_t)(cyc % a.stage_cap) * a.g.n_inputs + k)
+                            : d_stimulus(a.seed, k, cyc, a.lane0);
+      v &= wmask(inj[2 * i + 1]);
+      S.st(inj[2 * i], v);
+      if (HASH) hh += v * __ldg(a.g.in_k + k);
+    }
+    return hh;
+  };
+  if (a.n_cycles == 0) return;
+  hacc += inject(a.cycle0);
+  single_barrier<GRID>(a.bar, target, wsum, nullptr);
+  uint64_t hr = 0;
+#pragma unroll 1
+  for (uint32_t cyc = 0; cyc < a.n_cycles; ++cyc) {
+#pragma unroll 1
+    for (uint32_t l = 0; l < h->n_levels; ++l) {
+      const SliceLvl L = lvl[l];
+#pragma unroll 1
+      for (uint32_t t = tid; t < L.n; t += T) {
+        const uint64_t k = HASH ? __ldg(a.g.opk + L.op_begin + t) : 0ull;  // off the dependency chain
+        const uint32_t pw = pws[L.pw_base + t];
+        const uint64_t y = single_eval<GRID>(S, pw, crd + L.coord_base + cofs[L.pw_base + t]);
+        uint32_t si = L.seg_begin;
+        while (t >= seg[si].first + seg[si].count) ++si;
+        S.st(seg[si].out_coord0 + (t - seg[si].first), y);
+        if (HASH) hacc += y * k;
+      }
+      single_barrier<GRID>(a.bar, target, wsum, nullptr);
+    }
+    hr = 0;
+#pragma unroll 1
+    for (uint32_t i = tid; i < h->n_latch; i += T) {
+      const uint64_t x = S.ld(lat[3 * i]) & wmask(lat[3 * i + 2]);
+      S.st(lat[3 * i + 1], x);
+      if (HASH) hr += x * __ldg(a.g.reg_k + h->latch_first + i);
+    }
+    uint64_t hin = 0;
+    if (cyc + 1 < a.n_cycles) hin = inject(a.cycle0 + cyc + 1);
+    if (HASH) {
+      warp_partial(hacc, wsum);
+      hacc = hr + hin + ((blockIdx.x == 0 && tid == 0) ? a.g.const_hash : 0ull);
+    }
+    single_barrier<GRID>(a.bar, target, wsum, (HASH && a.hashes) ? (unsigned long long*)(a.hashes + cyc) : nullptr);
+  }
+  if (HASH) {
+    warp_partial(hr, wsum);
+    __syncthreads();
+    if (tid == 0) {
+      uint64_t s = 0;
+      for (uint32_t w = 0; w < (T + 31) / 32; ++w) s += wsum[w];
+      atomicAdd((unsigned long long*)a.hcarry_out, (unsigned long long)s);
+    }
+  }
+}
+
+}  // namespace rtlsim
