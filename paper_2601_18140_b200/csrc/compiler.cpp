@@ -513,14 +513,12 @@ bool build_single_slices(const CompiledGraph& g, uint32_t G, uint32_t max_bytes,
         sg.first = s0 - b;
         sg.count = s1 - s0;
         sg.out_coord0 = make_coord((R.meta >> 16) & 3u, R.out_row0 + (s0 - R.op_begin));
+        sg.coord0 = g.coord_off[s0] - g.coord_off[b];
         seg.push_back(sg);
       }
       L.n_seg = (uint32_t)seg.size() - L.seg_begin;
       for (uint32_t j = b; j < e; ++j) {
         pw.push_back(g.opw[j]);
-        const uint32_t off = (uint32_t)coords.size() - L.coord_base;
-        if (off > 0xFFFFu) return false;
-        cofs.push_back((uint16_t)off);
         for (uint32_t k = g.coord_off[j]; k < g.coord_off[j + 1]; ++k) coords.push_back(g.coord[k]);
       }
     }

@@ -178,11 +178,11 @@ struct SliceLvl {
   uint32_t seg_begin, n_seg;
   uint32_t pad[2];
 };
-struct SliceSeg {      // a run piece inside a chunk: outputs are consecutive rows of one class
+struct SliceSeg {      // a run piece inside a chunk: one arity, outputs consecutive rows of one class
   uint32_t first;      // chunk-relative index of the piece's first op
   uint32_t count;
   uint32_t out_coord0; // (class << 30) | row of the first op's output
-  uint32_t pad;
+  uint32_t coord0;     // first coord of the piece, relative to the level's coord_base (arity-strided)
 };
 // Returns false (and builds nothing) if a slice would exceed max_bytes.
 bool build_single_slices(const CompiledGraph& g, uint32_t G, uint32_t max_bytes, std::vector<uint8_t>* blob,

@@ -398,7 +398,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
       maxops = std::max(maxops, g->cg.level_op_begin[l + 1] - g->cg.level_op_begin[l]);
     // resident-slice kernel (single.cuh): fewest CTAs whose graph slices fit in shared memory
     const CompiledGraph& cg = g->cg;
-    const uint64_t est = 6ull * cg.n_ops_total() + 4ull * cg.coord.size() + 12ull * cg.n_regs + 8ull * cg.n_inputs;
+    const uint64_t est = 4ull * cg.n_ops_total() + 4ull * cg.coord.size() + 12ull * cg.n_regs + 8ull * cg.n_inputs;
     const uint32_t kMaxSlice = 200 * 1024;
     uint32_t G = (uint32_t)std::max<uint64_t>({1, (est + kMaxSlice / 2) / (kMaxSlice * 3 / 4), (maxops + 1023) / 1024});
     G = std::min<uint32_t>(G, (uint32_t)g->sm_count);
@@ -662,13 +662,16 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
     CU(cudaMemsetAsync(s->bar, 0, 8, s->stream));
     cudaError_t e;
     if (s->slice_blob) {
-      SingleArgs sa{a, s->slice_blob, s->slice_off, s->slice_max};
-      void* args[] = {&sa};
       const bool grid = s->ctas > 1;
+      const uint32_t smax = (s->slice_max + 127u) & ~127u;
+      const uint32_t st_smem =
+          (!grid && smax + s->tile_bytes <= 200u * 1024u) ? (uint32_t)s->tile_bytes : 0u;
+      SingleArgs sa{a, s->slice_blob, s->slice_off, smax, st_smem};
+      void* args[] = {&sa};
       const void* fn = grid ? (hash ? (const void*)k_single2<true, true> : (const void*)k_single2<true, false>)
                             : (hash ? (const void*)k_single2<false, true> : (const void*)k_single2<false, false>);
-      CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->slice_max));
-      e = cudaLaunchCooperativeKernel(fn, s->ctas, s->threads, args, s->slice_max, s->stream);
+      CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smax + st_smem)));
+      e = cudaLaunchCooperativeKernel(fn, s->ctas, s->threads, args, smax + st_smem, s->stream);
     } else {
       void* args[] = {&a};
       e = hash ? cudaLaunchCooperativeKernel((const void*)k_single<true>, s->ctas, s->threads, args, 0, s->stream)

@@ -18,7 +18,8 @@ struct SingleArgs {
   StepArgs a;
   const uint8_t* slice_blob;
   const uint64_t* slice_off;
-  uint32_t slice_max;  // bytes of the largest slice (dynamic shared memory)
+  uint32_t slice_max;    // bytes of the largest slice (128-aligned; dynamic shared memory)
+  uint32_t state_smem;   // single-CTA launches: bytes of signal state kept in shared memory (0 = off)
 };
 
 __device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v) {
@@ -144,13 +145,20 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
   const SliceLvl* lvl = reinterpret_cast<const SliceLvl*>(smem + h->off_lvl);
   const SliceSeg* seg = reinterpret_cast<const SliceSeg*>(smem + h->off_seg);
   const uint32_t* pws = reinterpret_cast<const uint32_t*>(smem + h->off_pw);
-  const uint16_t* cofs = reinterpret_cast<const uint16_t*>(smem + h->off_cofs);
   const uint32_t* crd = reinterpret_cast<const uint32_t*>(smem + h->off_coord);
   const uint32_t* lat = reinterpret_cast<const uint32_t*>(smem + h->off_latch);
   const uint32_t* inj = reinterpret_cast<const uint32_t*>(smem + h->off_inj);
 
+  // single CTA with a small state: the whole signal state lives in shared memory
+  uint8_t* st_base = a.state;
+  if (!GRID && sa.state_smem) {
+    st_base = smem + sa.slice_max;
+    for (uint32_t i = tid * 16; i < sa.state_smem; i += T * 16)
+      *reinterpret_cast<uint4*>(st_base + i) = *reinterpret_cast<const uint4*>(a.state + i);
+    __syncthreads();
+  }
   SState<GRID> S;
-  S.base = a.state + a.region[0];
+  S.base = st_base + a.region[0];
   S.r1 = a.region[1] - a.region[0];
   S.r2 = a.region[2] - a.region[0];
   S.r3 = a.region[3] - a.region[0];
@@ -182,10 +190,11 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
       for (uint32_t t = tid; t < L.n; t += T) {
         const uint64_t k = HASH ? __ldg(a.g.opk + L.op_begin + t) : 0ull;  // off the dependency chain
         const uint32_t pw = pws[L.pw_base + t];
-        const uint64_t y = single_eval<GRID>(S, pw, crd + L.coord_base + cofs[L.pw_base + t]);
         uint32_t si = L.seg_begin;
         while (t >= seg[si].first + seg[si].count) ++si;
-        S.st(seg[si].out_coord0 + (t - seg[si].first), y);
+        const SliceSeg G_ = seg[si];
+        const uint64_t y = single_eval<GRID>(S, pw, crd + L.coord_base + G_.coord0 + (t - G_.first) * (pw >> 26));
+        S.st(G_.out_coord0 + (t - G_.first), y);
         if (HASH) hacc += y * k;
       }
       single_barrier<GRID>(a.bar, target, wsum, nullptr);
@@ -213,6 +222,11 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
       for (uint32_t w = 0; w < (T + 31) / 32; ++w) s += wsum[w];
       atomicAdd((unsigned long long*)a.hcarry_out, (unsigned long long)s);
     }
+  }
+  if (!GRID && sa.state_smem) {  // write the state back
+    __syncthreads();
+    for (uint32_t i = tid * 16; i < sa.state_smem; i += T * 16)
+      *reinterpret_cast<uint4*>(a.state + i) = *reinterpret_cast<const uint4*>(st_base + i);
   }
 }
 
