@@ -399,7 +399,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     // resident-slice kernel (single.cuh): fewest CTAs whose graph slices fit in shared memory
     const CompiledGraph& cg = g->cg;
     const uint64_t est = 4ull * cg.n_ops_total() + 4ull * cg.coord.size() + 12ull * cg.n_regs + 8ull * cg.n_inputs;
-    const uint32_t kMaxSlice = 200 * 1024;
+    const uint32_t kMaxSlice = 212 * 1024;  // + static shared memory stays below the 227 KB per-CTA limit
     uint32_t G = (uint32_t)std::max<uint64_t>({1, (est + kMaxSlice / 2) / (kMaxSlice * 3 / 4), (maxops + 1023) / 1024});
     G = std::min<uint32_t>(G, (uint32_t)g->sm_count);
     std::vector<uint8_t> sblob;

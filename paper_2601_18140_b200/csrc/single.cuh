@@ -165,6 +165,7 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
   unsigned long long target = 0;
   uint64_t hacc = (HASH && blockIdx.x == 0 && tid == 0) ? a.hcarry_in[0] + a.g.const_hash : 0ull;
 
+  const uint64_t kinj = (HASH && tid < h->n_inj) ? __ldg(a.g.in_k + h->inj_first + tid) : 0ull;
   auto inject = [&](uint64_t cyc) -> uint64_t {
     uint64_t hh = 0;
     for (uint32_t i = tid; i < h->n_inj; i += T) {
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
                             : d_stimulus(a.seed, k, cyc, a.lane0);
       v &= wmask(inj[2 * i + 1]);
       S.st(inj[2 * i], v);
-      if (HASH) hh += v * __ldg(a.g.in_k + k);
+      if (HASH) hh += v * (i == tid ? kinj : __ldg(a.g.in_k + k));
     }
     return hh;
   };
@@ -181,14 +182,25 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
   hacc += inject(a.cycle0);
   single_barrier<GRID>(a.bar, target, wsum, nullptr);
   uint64_t hr = 0;
+  // hash weights are software-pipelined one level ahead: with few warps per
+  // SM an exposed global load per level would dominate the level's latency
+  auto kload = [&](uint32_t l) -> uint64_t {
+    if (!HASH || l >= h->n_levels) return 0ull;
+    const SliceLvl& L = lvl[l];
+    return tid < L.n ? __ldg(a.g.opk + L.op_begin + tid) : 0ull;
+  };
+  uint64_t knext = kload(0);
+  const uint64_t klat = (HASH && tid < h->n_latch) ? __ldg(a.g.reg_k + h->latch_first + tid) : 0ull;
 #pragma unroll 1
   for (uint32_t cyc = 0; cyc < a.n_cycles; ++cyc) {
 #pragma unroll 1
     for (uint32_t l = 0; l < h->n_levels; ++l) {
       const SliceLvl L = lvl[l];
+      const uint64_t kcur = knext;
+      knext = kload(l + 1 < h->n_levels ? l + 1 : 0);
 #pragma unroll 1
       for (uint32_t t = tid; t < L.n; t += T) {
-        const uint64_t k = HASH ? __ldg(a.g.opk + L.op_begin + t) : 0ull;  // off the dependency chain
+        const uint64_t k = !HASH ? 0ull : (t == tid ? kcur : __ldg(a.g.opk + L.op_begin + t));
         const uint32_t pw = pws[L.pw_base + t];
         uint32_t si = L.seg_begin;
         while (t >= seg[si].first + seg[si].count) ++si;
@@ -204,7 +216,7 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
     for (uint32_t i = tid; i < h->n_latch; i += T) {
       const uint64_t x = S.ld(lat[3 * i]) & wmask(lat[3 * i + 2]);
       S.st(lat[3 * i + 1], x);
-      if (HASH) hr += x * __ldg(a.g.reg_k + h->latch_first + i);
+      if (HASH) hr += x * (i == tid ? klat : __ldg(a.g.reg_k + h->latch_first + i));
     }
     uint64_t hin = 0;
     if (cyc + 1 < a.n_cycles) hin = inject(a.cycle0 + cyc + 1);
