@@ -494,10 +494,21 @@ bool build_single_slices(const CompiledGraph& g, uint32_t G, uint32_t max_bytes,
     std::vector<uint16_t> cofs;
     for (uint32_t l = 0; l < g.n_levels; ++l) {
       const uint32_t ob = g.level_op_begin[l], oe = g.level_op_begin[l + 1];
-      uint32_t b, e;
-      chunk(oe - ob, cta, G, b, e);
-      b += ob;
-      e += ob;
+      // chunk boundaries balanced by weight 1 + arity (ops are sorted by arity
+      // inside a level, so equal op counts would give the last CTAs all the
+      // 3-operand ops: unequal work and shared memory)
+      auto wpos = [&](uint32_t j) -> uint64_t { return (uint64_t)(j - ob) + (g.coord_off[j] - g.coord_off[ob]); };
+      const uint64_t W = wpos(oe);
+      auto cut = [&](uint32_t part) -> uint32_t {
+        const uint64_t target = (W * part + G - 1) / G;
+        uint32_t lo = ob, hi = oe;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) / 2;
+          if (wpos(mid) < target) lo = mid + 1; else hi = mid;
+        }
+        return lo;
+      };
+      const uint32_t b = cut(cta), e = cut(cta + 1);
       SliceLvl& L = lv[l];
       L = SliceLvl{};
       L.op_begin = b;

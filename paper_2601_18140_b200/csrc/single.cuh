@@ -210,6 +210,9 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
         if (HASH) hacc += y * k;
       }
       single_barrier<GRID>(a.bar, target, wsum, nullptr);
+#ifdef RS_TRACE
+      if (blockIdx.x == 0 && tid == 0 && a.trace && cyc < 8) a.trace[cyc * 64 + l] = clock64();
+#endif
     }
     hr = 0;
 #pragma unroll 1
@@ -224,7 +227,13 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
       warp_partial(hacc, wsum);
       hacc = hr + hin + ((blockIdx.x == 0 && tid == 0) ? a.g.const_hash : 0ull);
     }
+#ifdef RS_TRACE
+    if (blockIdx.x == 0 && tid == 0 && a.trace && cyc < 8) a.trace[cyc * 64 + 60] = clock64();
+#endif
     single_barrier<GRID>(a.bar, target, wsum, (HASH && a.hashes) ? (unsigned long long*)(a.hashes + cyc) : nullptr);
+#ifdef RS_TRACE
+    if (blockIdx.x == 0 && tid == 0 && a.trace && cyc < 8) a.trace[cyc * 64 + 61] = clock64();
+#endif
   }
   if (HASH) {
     warp_partial(hr, wsum);
