@@ -64,6 +64,21 @@ struct SState {
     const uint64_t reg = cls == 0 ? 0 : cls == 1 ? r1 : cls == 2 ? r2 : r3;
     return base + reg + ((uint64_t)(c & ROW_MASK) << cls);
   }
+  // Branch-free gather (threads of a warp hold different ops, so a per-class
+  // switch would diverge and serialize the warp's loads): load the aligned
+  // 64-bit word holding the container, then shift and mask it.
+  __device__ __forceinline__ uint64_t word(uint32_t c) const {
+    const uintptr_t p = reinterpret_cast<uintptr_t>(addr(c));
+    const uint64_t* q = reinterpret_cast<const uint64_t*>(p & ~(uintptr_t)7);
+    if constexpr (GRID) return __ldcg(q);
+    else return *q;
+  }
+  __device__ __forceinline__ uint64_t fix(uint32_t c, uint64_t w) const {
+    const uint32_t cls = c >> 30;
+    const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(addr(c)) & 7u) * 8u;
+    const uint64_t v = w >> sh;
+    return cls == 3u ? w : (v & (0xFFFFFFFFull >> (32u - (8u << min(cls, 2u)))));
+  }
   __device__ __forceinline__ uint64_t ld(uint32_t c) const {
     const uint8_t* p = addr(c);
     if constexpr (GRID) {
@@ -97,9 +112,10 @@ struct SState {
 template <bool GRID>
 __device__ __forceinline__ uint64_t single_eval(const SState<GRID>& S, uint32_t pw, const uint32_t* cp) {
   const uint32_t op = (pw >> 22) & 15u, n = pw >> 26, p0 = (pw >> 7) & 127u;
-  uint64_t x0 = S.ld(cp[0]), x1 = 0, x2 = 0;
-  if (n >= 2) x1 = S.ld(cp[1]);
-  if (n >= 3) x2 = S.ld(cp[2]);
+  // all operand loads first (convergent, predicated by arity), then the fix-ups
+  const uint32_t c0 = cp[0], c1 = n >= 2 ? cp[1] : c0, c2 = n >= 3 ? cp[2] : c0;
+  const uint64_t w0 = S.word(c0), w1 = S.word(c1), w2 = S.word(c2);
+  const uint64_t x0 = S.fix(c0, w0), x1 = S.fix(c1, w1), x2 = S.fix(c2, w2);
   uint64_t r;
   switch (op) {
     case RS_OP_AND: r = x0 & x1; if (n >= 3) r &= x2; break;
@@ -202,9 +218,12 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
       for (uint32_t t = tid; t < L.n; t += T) {
         const uint64_t k = !HASH ? 0ull : (t == tid ? kcur : __ldg(a.g.opk + L.op_begin + t));
         const uint32_t pw = pws[L.pw_base + t];
-        uint32_t si = L.seg_begin;
-        while (t >= seg[si].first + seg[si].count) ++si;
-        const SliceSeg G_ = seg[si];
+        uint32_t lo = L.seg_begin, hi = L.seg_begin + L.n_seg - 1;  // last piece with first <= t
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi + 1) >> 1;
+          if (seg[mid].first <= t) lo = mid; else hi = mid - 1;
+        }
+        const SliceSeg G_ = seg[lo];
         const uint64_t y = single_eval<GRID>(S, pw, crd + L.coord_base + G_.coord0 + (t - G_.first) * (pw >> 26));
         S.st(G_.out_coord0 + (t - G_.first), y);
         if (HASH) hacc += y * k;
