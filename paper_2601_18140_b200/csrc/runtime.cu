@@ -412,7 +412,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     }
     if (ok && !o.threads) {
       const uint32_t chunk = std::max<uint32_t>(1, (maxops + G - 1) / G);
-      s->threads = std::min<uint32_t>(1024, std::max<uint32_t>(32, (chunk + 31) & ~31u));
+      s->threads = std::min<uint32_t>(1024, 32u * chunk);  // up to one op per warp (single.cuh op slots)
     }
     if (ok) {
       uint32_t smax = 0;

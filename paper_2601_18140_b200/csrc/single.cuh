@@ -198,12 +198,17 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
   hacc += inject(a.cycle0);
   single_barrier<GRID>(a.bar, target, wsum, nullptr);
   uint64_t hr = 0;
+  // op slot of this thread: ops are dealt to warps first (op t -> warp t % W,
+  // lane t / W), so a level with few ops puts one op per warp -- the warps run
+  // their ops' code paths in parallel instead of one warp diverging over them
+  const uint32_t W = (T + 31) / 32;
+  const uint32_t top = (tid & 31u) * W + (tid >> 5);
   // hash weights are software-pipelined one level ahead: with few warps per
   // SM an exposed global load per level would dominate the level's latency
   auto kload = [&](uint32_t l) -> uint64_t {
     if (!HASH || l >= h->n_levels) return 0ull;
     const SliceLvl& L = lvl[l];
-    return tid < L.n ? __ldg(a.g.opk + L.op_begin + tid) : 0ull;
+    return top < L.n ? __ldg(a.g.opk + L.op_begin + top) : 0ull;
   };
   uint64_t knext = kload(0);
   const uint64_t klat = (HASH && tid < h->n_latch) ? __ldg(a.g.reg_k + h->latch_first + tid) : 0ull;
@@ -215,8 +220,8 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
       const uint64_t kcur = knext;
       knext = kload(l + 1 < h->n_levels ? l + 1 : 0);
 #pragma unroll 1
-      for (uint32_t t = tid; t < L.n; t += T) {
-        const uint64_t k = !HASH ? 0ull : (t == tid ? kcur : __ldg(a.g.opk + L.op_begin + t));
+      for (uint32_t t = top; t < L.n; t += T) {
+        const uint64_t k = !HASH ? 0ull : (t == top ? kcur : __ldg(a.g.opk + L.op_begin + t));
         const uint32_t pw = pws[L.pw_base + t];
         uint32_t lo = L.seg_begin, hi = L.seg_begin + L.n_seg - 1;  // last piece with first <= t
         while (lo < hi) {
