@@ -176,9 +176,8 @@ def main():
     import torch
     from paper_2601_18140_b200 import rtlsim as rs
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2601_18140_b200 import dist as D
+    rank, world, local = D.env_rank()
     if world != args.gpus:
         print(f"warning: WORLD_SIZE={world} but --gpus={args.gpus}", file=sys.stderr)
     torch.cuda.set_device(local)
@@ -192,10 +191,11 @@ def main():
     if single:
         lanes = 1
     cycles = args.cycles or cfg.cycles
+    shard = D.shard_weak(rank, world, lanes)      # global lanes [lane0, lane0 + lanes)
     stream = torch.cuda.Stream()
     g = rs.Graph(circ, device=local, mode="single" if single else "lanes")
     info = g.info()
-    L = rs.Lanes(g, lanes, lane0=rank * lanes, lane_tile=args.lane_tile, threads=args.threads, stream=stream,
+    L = rs.Lanes(g, lanes, lane0=shard.lane0, lane_tile=args.lane_tile, threads=args.threads, stream=stream,
                  cluster=args.cluster)
     L.set_seed(cfg.stim_seed)
     hashes = None if args.no_hash else torch.empty(cycles * lanes, dtype=torch.int64, device="cuda")
@@ -228,10 +228,7 @@ def main():
         launches = L.launches - launches0
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = float(sum(step_ms))
-    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    total_ms = D.max_over_ranks(total_ms, dist, device="cuda")
     lane_cycles = lanes * world * cycles * args.steps
     value = lane_cycles / (total_ms / 1e3)
 
@@ -250,9 +247,9 @@ def main():
     # end to end through the public API with host buffers: staged inputs H2D
     # from pinned memory, hashes D2H, every chunk.
     e2e = None
-    if not args.no_e2e and rank == 0 or (not args.no_e2e and world > 1):
+    if not args.no_e2e:
         chunk = min(cycles, max(1, (256 << 20) // max(1, 8 * circ.n_inputs * lanes)))
-        Ls = rs.Lanes(g, lanes, lane0=rank * lanes, lane_tile=args.lane_tile, threads=args.threads, cluster=args.cluster,
+        Ls = rs.Lanes(g, lanes, lane0=shard.lane0, lane_tile=args.lane_tile, threads=args.threads, cluster=args.cluster,
                       stage_cycles=chunk, stream=stream)
         rng = np.random.default_rng(rank)
         host_in = torch.from_numpy(rng.integers(0, 2**63, size=(chunk, circ.n_inputs, lanes),
@@ -278,10 +275,7 @@ def main():
             e2e_step()
         torch.cuda.synchronize()
         el = time.perf_counter() - t0
-        te = torch.tensor([el], dtype=torch.float64, device="cuda")
-        if dist is not None:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        el = float(te.item())
+        el = D.max_over_ranks(el, dist, device="cuda")
         e2e = {"value": lanes * world * cycles * e2e_steps / el, "unit": UNIT,
                "h2d_bytes_per_step": int(cycles * circ.n_inputs * lanes * 8),
                "d2h_bytes_per_step": int(cycles * lanes * 8), "steps": e2e_steps,
