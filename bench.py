@@ -164,6 +164,7 @@ def main():
     ap.add_argument("--lane-tile", type=int, default=0)
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--cluster", type=int, default=0)
+    ap.add_argument("--parts", type=int, default=0, help="C1/C5: level-cut partitions emulated on this GPU")
     ap.add_argument("--ref-step-s", type=float, default=4.0)
     args = ap.parse_args()
 
@@ -196,7 +197,7 @@ def main():
     g = rs.Graph(circ, device=local, mode="single" if single else "lanes")
     info = g.info()
     L = rs.Lanes(g, lanes, lane0=shard.lane0, lane_tile=args.lane_tile, threads=args.threads, stream=stream,
-                 cluster=args.cluster)
+                 cluster=args.cluster, parts=args.parts)
     L.set_seed(cfg.stim_seed)
     hashes = None if args.no_hash else torch.empty(cycles * lanes, dtype=torch.int64, device="cuda")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
@@ -250,7 +251,7 @@ def main():
     if not args.no_e2e:
         chunk = min(cycles, max(1, (256 << 20) // max(1, 8 * circ.n_inputs * lanes)))
         Ls = rs.Lanes(g, lanes, lane0=shard.lane0, lane_tile=args.lane_tile, threads=args.threads, cluster=args.cluster,
-                      stage_cycles=chunk, stream=stream)
+                      stage_cycles=chunk, stream=stream, parts=args.parts)
         rng = np.random.default_rng(rank)
         host_in = torch.from_numpy(rng.integers(0, 2**63, size=(chunk, circ.n_inputs, lanes),
                                                 dtype=np.int64)).pin_memory()
@@ -300,6 +301,7 @@ def main():
                        "lanes_per_gpu": lanes, "cycles_per_step": cycles, "hash": not args.no_hash,
                        "l2": "flushed (256 MB write) before every timed step",
                        "mode": "single" if single else "lanes", "launch": L.shape(),
+                       **({"level_cut_parts": args.parts} if args.parts > 1 else {}),
                        "state_bytes_per_gpu": info["state_bytes_per_lane"] * lanes},
             "op_evals_per_s": value * circ.n_ops,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -122,6 +122,14 @@ typedef struct {
   uint32_t cluster;        /* RS_MODE_LANES: CTAs (a thread-block cluster on as many SMs) sharing one
                               lane tile, 0 = auto, else 1, 2, 4 or 8 */
   void* stream;            /* cudaStream_t to run on; NULL = a stream the library creates */
+  uint32_t parts;          /* RS_MODE_SINGLE level cut: 0/1 = off, else 2..8 partitions,
+                              each owning a contiguous level range (balanced by op weight) and a full
+                              state replica; partitions hand each cycle on through release/acquire
+                              flags and push the signals a later partition reads (cut signals, register
+                              values) into its replica.  On one device the partitions are CTA groups of
+                              one cooperative launch.  RS_E_CAPACITY if the slices do not fit
+                              co-resident, RS_E_INVALID_ARG if parts > n_levels or > 8. */
+  uint32_t pad_;
 } rs_lane_opts;
 
 typedef struct rs_graph rs_graph;
@@ -156,6 +164,13 @@ enum {
 };
 rs_status rs_graph_export(const rs_graph* g, uint32_t what, void* out, uint64_t* count);
 void rs_free_graph(rs_graph* g);
+
+/* Level ranges of a `parts`-way level cut (rs_lane_opts.parts):
+ * partition k owns levels [cut[k], cut[k+1]); cut[0] = 0, cut[parts] = n_levels,
+ * every range non-empty, boundaries balanced by op weight (1 + arity).  `cut`
+ * is caller-owned host memory of parts + 1 entries.  Host-only (works on a
+ * RS_DEVICE_NONE graph).  RS_E_INVALID_ARG if parts is 0, > 8 or > n_levels. */
+rs_status rs_level_cut(const rs_graph* g, uint32_t parts, uint32_t* cut);
 
 /* Allocate the signal state for n_lanes lanes (RS_MODE_SINGLE: n_lanes must
  * be 1), initialised to: registers = init & M(w), constants = value, all

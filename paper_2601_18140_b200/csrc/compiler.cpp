@@ -478,106 +478,194 @@ void build_stages(const CompiledGraph& g, uint32_t stage_bytes, std::vector<uint
   }
 }
 
-bool build_single_slices(const CompiledGraph& g, uint32_t G, uint32_t max_bytes, std::vector<uint8_t>* blob,
-                         std::vector<uint64_t>* slice_off) {
+std::vector<uint32_t> level_cut(const CompiledGraph& g, uint32_t P) {
+  // cumulative op weight (1 + arity) at each level boundary
+  const uint32_t nl = g.n_levels;
+  auto wl = [&](uint32_t l) -> uint64_t {
+    const uint32_t o = g.level_op_begin[l];
+    return (uint64_t)o + g.coord_off[o];
+  };
+  const uint64_t W = wl(nl);
+  std::vector<uint32_t> cut(P + 1, nl);
+  cut[0] = 0;
+  for (uint32_t k = 1; k < P; ++k) {
+    const uint64_t target = (W * k + P / 2) / P;
+    uint32_t l = cut[k - 1] + 1;                      // every partition gets >= 1 level
+    while (l < nl - (P - 1 - k) && wl(l) < target) ++l;
+    cut[k] = std::min(l, nl - (P - k));
+  }
+  return cut;
+}
+
+void row_owner(const CompiledGraph& g, const std::vector<uint32_t>& cut, std::vector<uint8_t> owner[4]) {
+  for (int c = 0; c < 4; ++c) owner[c].assign(g.rows[c], 0);
+  uint32_t k = 0;
+  for (uint32_t l = 0; l < g.n_levels; ++l) {
+    while (l >= cut[k + 1]) ++k;
+    for (uint32_t r = g.level_run_begin[l]; r < g.level_run_begin[l + 1]; ++r) {
+      const DevRun& R = g.runs[r];
+      const uint32_t cls = (R.meta >> 16) & 3u;
+      for (uint32_t i = 0; i < R.count; ++i) owner[cls][R.out_row0 + i] = (uint8_t)k;
+    }
+  }
+}
+
+bool build_single_slices(const CompiledGraph& g, uint32_t P, uint32_t Gp, uint32_t max_bytes,
+                         std::vector<uint8_t>* blob, std::vector<uint64_t>* slice_off) {
   blob->clear();
-  slice_off->assign(G, 0);
+  slice_off->assign((size_t)P * Gp, 0);
+  if (P == 0 || P > kMaxParts || P > std::max<uint32_t>(1, g.n_levels)) return false;
   auto chunk = [](uint32_t n, uint32_t part, uint32_t parts, uint32_t& b, uint32_t& e) {
     const uint32_t c = (n + parts - 1) / parts;
     b = std::min(n, part * c);
     e = std::min(n, b + c);
   };
-  for (uint32_t cta = 0; cta < G; ++cta) {
-    std::vector<SliceLvl> lv(g.n_levels);
-    std::vector<SliceSeg> seg;
-    std::vector<uint32_t> pw, coords, latch, inj;
-    std::vector<uint16_t> cofs;
+  const std::vector<uint32_t> cut = level_cut(g, P);
+  std::vector<uint8_t> owner[4];
+  row_owner(g, cut, owner);
+  auto own_of = [&](uint32_t c) -> uint32_t { return owner[c >> 30][c & ROW_MASK]; };
+  // register owner = partition producing its next value (an op row: the
+  // compiler routes source next values through identity copies at level 0)
+  std::vector<uint32_t> reg_owner(g.n_regs);
+  for (uint32_t i = 0; i < g.n_regs; ++i) reg_owner[i] = own_of(g.reg_next_coord[i]);
+  // cut signals: producer partition -> (coord -> consumer mask)
+  std::vector<std::vector<std::pair<uint32_t, uint32_t>>> push(P);
+  if (P > 1) {
+    std::vector<uint32_t> mask[4];
+    for (int c = 0; c < 4; ++c) mask[c].assign(g.rows[c], 0);
+    uint32_t k = 0;
     for (uint32_t l = 0; l < g.n_levels; ++l) {
-      const uint32_t ob = g.level_op_begin[l], oe = g.level_op_begin[l + 1];
-      // chunk boundaries balanced by weight 1 + arity (ops are sorted by arity
-      // inside a level, so equal op counts would give the last CTAs all the
-      // 3-operand ops: unequal work and shared memory)
-      auto wpos = [&](uint32_t j) -> uint64_t { return (uint64_t)(j - ob) + (g.coord_off[j] - g.coord_off[ob]); };
-      const uint64_t W = wpos(oe);
-      auto cut = [&](uint32_t part) -> uint32_t {
-        const uint64_t target = (W * part + G - 1) / G;
-        uint32_t lo = ob, hi = oe;
-        while (lo < hi) {
-          const uint32_t mid = (lo + hi) / 2;
-          if (wpos(mid) < target) lo = mid + 1; else hi = mid;
+      while (l >= cut[k + 1]) ++k;
+      for (uint32_t j = g.level_op_begin[l]; j < g.level_op_begin[l + 1]; ++j)
+        for (uint32_t q = g.coord_off[j]; q < g.coord_off[j + 1]; ++q) {
+          const uint32_t c = g.coord[q];
+          mask[c >> 30][c & ROW_MASK] |= 1u << k;
         }
-        return lo;
+    }
+    for (uint32_t i = 0; i < g.n_regs; ++i) {  // partitions after the owner latch it locally
+      const uint32_t c = g.reg_next_coord[i];
+      for (uint32_t m = reg_owner[i] + 1; m < P; ++m) mask[c >> 30][c & ROW_MASK] |= 1u << m;
+    }
+    // only op rows produced by an earlier partition travel; sources are in every replica
+    std::vector<uint8_t> is_op[4];
+    for (int c = 0; c < 4; ++c) is_op[c].assign(g.rows[c], 0);
+    for (const DevRun& R : g.runs)
+      for (uint32_t i = 0; i < R.count; ++i) is_op[(R.meta >> 16) & 3u][R.out_row0 + i] = 1;
+    for (uint32_t c = 0; c < 4; ++c)
+      for (uint32_t r = 0; r < g.rows[c]; ++r) {
+        if (!is_op[c][r]) continue;
+        const uint32_t k0 = owner[c][r];
+        const uint32_t m = mask[c][r] & ~((2u << k0) - 1u);  // consumers after the producer
+        if (m) push[k0].push_back({make_coord(c, r), m});
+      }
+  }
+  for (uint32_t k = 0; k < P; ++k) {
+    // latch list of partition k: registers owned by partitions <= k
+    std::vector<uint32_t> regs;
+    for (uint32_t i = 0; i < g.n_regs; ++i)
+      if (reg_owner[i] <= k) regs.push_back(i);
+    for (uint32_t cta = 0; cta < Gp; ++cta) {
+      std::vector<SliceLvl> lv(cut[k + 1] - cut[k]);
+      std::vector<SliceSeg> seg;
+      std::vector<uint32_t> pw, coords, latch, inj, pu;
+      for (uint32_t l = cut[k]; l < cut[k + 1]; ++l) {
+        const uint32_t ob = g.level_op_begin[l], oe = g.level_op_begin[l + 1];
+        // chunk boundaries balanced by weight 1 + arity (ops are sorted by arity
+        // inside a level, so equal op counts would give the last CTAs all the
+        // 3-operand ops: unequal work and shared memory)
+        auto wpos = [&](uint32_t j) -> uint64_t { return (uint64_t)(j - ob) + (g.coord_off[j] - g.coord_off[ob]); };
+        const uint64_t W = wpos(oe);
+        auto cutw = [&](uint32_t part) -> uint32_t {
+          const uint64_t target = (W * part + Gp - 1) / Gp;
+          uint32_t lo = ob, hi = oe;
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi) / 2;
+            if (wpos(mid) < target) lo = mid + 1; else hi = mid;
+          }
+          return lo;
+        };
+        const uint32_t b = cutw(cta), e = cutw(cta + 1);
+        SliceLvl& L = lv[l - cut[k]];
+        L = SliceLvl{};
+        L.op_begin = b;
+        L.n = e - b;
+        L.pw_base = (uint32_t)pw.size();
+        L.coord_base = (uint32_t)coords.size();
+        L.seg_begin = (uint32_t)seg.size();
+        for (uint32_t r = g.level_run_begin[l]; r < g.level_run_begin[l + 1]; ++r) {
+          const DevRun& R = g.runs[r];
+          const uint32_t s0 = std::max(b, R.op_begin), s1 = std::min(e, R.op_begin + R.count);
+          if (s0 >= s1) continue;
+          SliceSeg sg{};
+          sg.first = s0 - b;
+          sg.count = s1 - s0;
+          sg.out_coord0 = make_coord((R.meta >> 16) & 3u, R.out_row0 + (s0 - R.op_begin));
+          sg.coord0 = g.coord_off[s0] - g.coord_off[b];
+          seg.push_back(sg);
+        }
+        L.n_seg = (uint32_t)seg.size() - L.seg_begin;
+        for (uint32_t j = b; j < e; ++j) {
+          pw.push_back(g.opw[j]);
+          for (uint32_t q = g.coord_off[j]; q < g.coord_off[j + 1]; ++q) coords.push_back(g.coord[q]);
+        }
+      }
+      uint32_t rb, re, ib, ie, pb, pe;
+      chunk((uint32_t)regs.size(), cta, Gp, rb, re);
+      chunk(g.n_inputs, cta, Gp, ib, ie);
+      chunk((uint32_t)push[k].size(), cta, Gp, pb, pe);
+      for (uint32_t q = rb; q < re; ++q) {
+        const uint32_t i = regs[q];
+        const uint32_t own = reg_owner[i] == k ? 1u : 0u;
+        const uint32_t dmask = own ? ((1u << k) - 1u) : 0u;  // earlier replicas are done with the cycle
+        latch.push_back(g.reg_next_coord[i]);
+        latch.push_back(g.reg_coord[i]);
+        latch.push_back(g.reg_w[i] | (own << 7) | (dmask << 8));
+        latch.push_back(i);
+      }
+      for (uint32_t i = ib; i < ie; ++i) {
+        inj.push_back(g.in_coord[i]);
+        inj.push_back(g.in_w[i]);
+      }
+      for (uint32_t i = pb; i < pe; ++i) {
+        pu.push_back(push[k][i].first);
+        pu.push_back(push[k][i].second);
+      }
+      SliceHdr h{};
+      h.n_levels = (uint32_t)lv.size();
+      h.off_lvl = al16((uint32_t)sizeof(SliceHdr));
+      h.off_seg = al16(h.off_lvl + (uint32_t)(lv.size() * sizeof(SliceLvl)));
+      h.off_pw = al16(h.off_seg + (uint32_t)(seg.size() * sizeof(SliceSeg)));
+      h.off_coord = al16(h.off_pw + 4u * (uint32_t)pw.size());
+      h.head_bytes = al16(h.off_coord + 4u * (uint32_t)coords.size());
+      h.off_push = h.head_bytes;
+      h.off_latch = al16(h.off_push + 4u * (uint32_t)pu.size());
+      h.off_inj = al16(h.off_latch + 4u * (uint32_t)latch.size());
+      h.bytes = al16(h.off_inj + 4u * (uint32_t)inj.size());
+      h.n_push = pe - pb;
+      h.n_latch = re - rb;
+      h.inj_first = ib;
+      h.n_inj = ie - ib;
+      h.part = k;
+      if (h.head_bytes > max_bytes) {
+        blob->clear();
+        return false;
+      }
+      const size_t base = (blob->size() + 127) & ~(size_t)127;
+      blob->resize(base + h.bytes, 0);
+      uint8_t* p = blob->data() + base;
+      std::memcpy(p, &h, sizeof h);
+      auto put = [&](uint32_t off, const void* src, size_t n) {
+        if (n) std::memcpy(p + off, src, n);
       };
-      const uint32_t b = cut(cta), e = cut(cta + 1);
-      SliceLvl& L = lv[l];
-      L = SliceLvl{};
-      L.op_begin = b;
-      L.n = e - b;
-      L.pw_base = (uint32_t)pw.size();
-      L.coord_base = (uint32_t)coords.size();
-      L.seg_begin = (uint32_t)seg.size();
-      for (uint32_t r = g.level_run_begin[l]; r < g.level_run_begin[l + 1]; ++r) {
-        const DevRun& R = g.runs[r];
-        const uint32_t s0 = std::max(b, R.op_begin), s1 = std::min(e, R.op_begin + R.count);
-        if (s0 >= s1) continue;
-        SliceSeg sg{};
-        sg.first = s0 - b;
-        sg.count = s1 - s0;
-        sg.out_coord0 = make_coord((R.meta >> 16) & 3u, R.out_row0 + (s0 - R.op_begin));
-        sg.coord0 = g.coord_off[s0] - g.coord_off[b];
-        seg.push_back(sg);
-      }
-      L.n_seg = (uint32_t)seg.size() - L.seg_begin;
-      for (uint32_t j = b; j < e; ++j) {
-        pw.push_back(g.opw[j]);
-        for (uint32_t k = g.coord_off[j]; k < g.coord_off[j + 1]; ++k) coords.push_back(g.coord[k]);
-      }
+      put(h.off_lvl, lv.data(), lv.size() * sizeof(SliceLvl));
+      put(h.off_seg, seg.data(), seg.size() * sizeof(SliceSeg));
+      put(h.off_pw, pw.data(), pw.size() * 4);
+      put(h.off_push, pu.data(), pu.size() * 4);
+      put(h.off_coord, coords.data(), coords.size() * 4);
+      put(h.off_latch, latch.data(), latch.size() * 4);
+      put(h.off_inj, inj.data(), inj.size() * 4);
+      (*slice_off)[(size_t)k * Gp + cta] = base;
     }
-    uint32_t rb, re, ib, ie;
-    chunk(g.n_regs, cta, G, rb, re);
-    chunk(g.n_inputs, cta, G, ib, ie);
-    for (uint32_t i = rb; i < re; ++i) {
-      latch.push_back(g.reg_next_coord[i]);
-      latch.push_back(g.reg_coord[i]);
-      latch.push_back(g.reg_w[i]);
-    }
-    for (uint32_t i = ib; i < ie; ++i) {
-      inj.push_back(g.in_coord[i]);
-      inj.push_back(g.in_w[i]);
-    }
-    SliceHdr h{};
-    h.n_levels = g.n_levels;
-    h.off_lvl = al16((uint32_t)sizeof(SliceHdr));
-    h.off_seg = al16(h.off_lvl + (uint32_t)(lv.size() * sizeof(SliceLvl)));
-    h.off_pw = al16(h.off_seg + (uint32_t)(seg.size() * sizeof(SliceSeg)));
-    h.off_cofs = al16(h.off_pw + 4u * (uint32_t)pw.size());
-    h.off_coord = al16(h.off_cofs + 2u * (uint32_t)cofs.size());
-    h.off_latch = al16(h.off_coord + 4u * (uint32_t)coords.size());
-    h.off_inj = al16(h.off_latch + 4u * (uint32_t)latch.size());
-    h.bytes = al16(h.off_inj + 4u * (uint32_t)inj.size());
-    h.latch_first = rb;
-    h.n_latch = re - rb;
-    h.inj_first = ib;
-    h.n_inj = ie - ib;
-    if (h.bytes > max_bytes) {
-      blob->clear();
-      return false;
-    }
-    const size_t base = (blob->size() + 127) & ~(size_t)127;
-    blob->resize(base + h.bytes, 0);
-    uint8_t* p = blob->data() + base;
-    std::memcpy(p, &h, sizeof h);
-    auto put = [&](uint32_t off, const void* src, size_t n) {
-      if (n) std::memcpy(p + off, src, n);
-    };
-    put(h.off_lvl, lv.data(), lv.size() * sizeof(SliceLvl));
-    put(h.off_seg, seg.data(), seg.size() * sizeof(SliceSeg));
-    put(h.off_pw, pw.data(), pw.size() * 4);
-    put(h.off_cofs, cofs.data(), cofs.size() * 2);
-    put(h.off_coord, coords.data(), coords.size() * 4);
-    put(h.off_latch, latch.data(), latch.size() * 4);
-    put(h.off_inj, inj.data(), inj.size() * 4);
-    (*slice_off)[cta] = base;
   }
   return true;
 }

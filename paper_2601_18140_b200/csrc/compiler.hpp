@@ -160,16 +160,34 @@ void build_stages(const CompiledGraph& g, uint32_t stage_bytes, std::vector<uint
 // chunk of every level's ops (and of the registers / inputs); its descriptors
 // stay resident in shared memory for the whole launch.  Layout of one slice
 // (16-byte aligned sections, offsets in SliceHdr):
-//   SliceLvl[n_levels] | SliceSeg[...] | pw u32[ops] | cofs u16[ops] | coords u32[...]
-//   | latch {next coord, reg coord, width} u32x3[n_latch] | inject {coord, width} u32x2[n_inj]
+//   head: SliceLvl[n_levels] | SliceSeg[...] | pw u32[ops] | coords u32[...]
+//   tail: push {coord, dmask} u32x2[n_push]
+//         | latch {next coord, reg coord, w | own << 7 | dmask << 8, reg index} u32x4[n_latch]
+//         | inject {coord, width} u32x2[n_inj]
+// The head (read every level) must fit shared memory; the tail (read once
+// per cycle, coalesced) is copied there too when every slice fits whole,
+// else it is streamed from global memory (L2).
+//
+// Level cut: with P > 1 partitions, partition k owns the
+// contiguous level range [level_cut[k], level_cut[k+1]) (balanced by op
+// weight) and keeps a full replica of the signal state.  Its slices hold
+// only its levels; its latch list holds every register whose next value is
+// produced by a partition <= k (the register's owner), own == 1 for its own
+// registers, whose new value it also pushes to the replicas in dmask (the
+// partitions < k, which have finished the cycle); its push list holds the
+// op outputs it produces that a later partition reads (operands, or the next
+// value of a register that partition latches), dmask = the consumers.
 struct SliceHdr {
   uint32_t bytes;
   uint32_t n_levels;
-  uint32_t off_lvl, off_seg, off_pw, off_cofs, off_coord, off_latch, off_inj;
-  uint32_t latch_first, n_latch;   // registers [latch_first, latch_first + n_latch)
+  uint32_t off_lvl, off_seg, off_pw, off_push, off_coord, off_latch, off_inj;
+  uint32_t n_push, n_latch;
   uint32_t inj_first, n_inj;       // inputs [inj_first, inj_first + n_inj)
-  uint32_t pad[3];
+  uint32_t part;                   // level-cut partition of the slice
+  uint32_t head_bytes;             // bytes of the head (= off_push)
+  uint32_t pad;
 };
+constexpr uint32_t kMaxParts = 8;
 struct SliceLvl {
   uint32_t op_begin;   // global op index of the chunk's first op (hash weights)
   uint32_t n;          // ops in the chunk
@@ -184,8 +202,13 @@ struct SliceSeg {      // a run piece inside a chunk: one arity, outputs consecu
   uint32_t out_coord0; // (class << 30) | row of the first op's output
   uint32_t coord0;     // first coord of the piece, relative to the level's coord_base (arity-strided)
 };
-// Returns false (and builds nothing) if a slice would exceed max_bytes.
-bool build_single_slices(const CompiledGraph& g, uint32_t G, uint32_t max_bytes, std::vector<uint8_t>* blob,
-                         std::vector<uint64_t>* slice_off);
+// Level ranges of P partitions balanced by op weight (1 + arity): [cut[k], cut[k+1]).
+std::vector<uint32_t> level_cut(const CompiledGraph& g, uint32_t P);
+// Partition (of `cut`) that produces each signal row, per class (sources: 0).
+void row_owner(const CompiledGraph& g, const std::vector<uint32_t>& cut, std::vector<uint8_t> owner[4]);
+// Slices of P partitions x Gp CTAs (partition-major).  Returns false (and
+// builds nothing) if a slice head would exceed max_bytes.
+bool build_single_slices(const CompiledGraph& g, uint32_t P, uint32_t Gp, uint32_t max_bytes,
+                         std::vector<uint8_t>* blob, std::vector<uint64_t>* slice_off);
 
 }  // namespace rtlsim

@@ -100,10 +100,17 @@ struct rs_lanes {
   const uint8_t* slice_blob = nullptr;
   const uint64_t* slice_off = nullptr;
   uint32_t slice_max = 0;
+  // level cut: parts partitions x gp CTAs, replica k = tile k of state_mem
+  uint32_t parts = 1, gp = 1;
+  bool tail_global = false;
+  std::vector<uint8_t> sig_part;         // canonical id -> partition whose replica holds it
   size_t total_bytes = 0;
 };
 
 namespace {
+
+constexpr size_t kBarBytes = 1024;      // partition k's grid barrier at u64 [4k]; level-cut flags at [kFlagOffset + k]
+constexpr size_t kFlagOffset = 64;
 
 StepArgs base_args(const rs_lanes* s) {
   StepArgs a{};
@@ -335,6 +342,16 @@ rs_status rs_graph_export(const rs_graph* g, uint32_t what, void* out, uint64_t*
   return RS_OK;
 }
 
+rs_status rs_level_cut(const rs_graph* g, uint32_t parts, uint32_t* cut) {
+  if (!g || !cut) return set_err(RS_E_INVALID_ARG, "NULL argument");
+  if (parts == 0 || parts > kMaxParts || parts > std::max<uint32_t>(1, g->cg.n_levels))
+    return set_err(RS_E_INVALID_ARG, "parts = %u: must be in [1, min(%u, n_levels = %u)]", parts, kMaxParts,
+                   g->cg.n_levels);
+  const std::vector<uint32_t> c = level_cut(g->cg, parts);
+  std::memcpy(cut, c.data(), c.size() * 4);
+  return RS_OK;
+}
+
 void rs_free_graph(rs_graph* g) {
   if (!g) return;
   if (g->dmem) {
@@ -362,8 +379,18 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
   s->lane0 = o.lane0;
   if (g->cg.mode == RS_MODE_SINGLE) {
     s->LT = 1;
-    s->n_tiles = 1;
+    s->parts = std::max<uint32_t>(1, o.parts);
+    if (s->parts > kMaxParts || s->parts > std::max<uint32_t>(1, g->cg.n_levels)) {
+      const uint32_t p = s->parts;
+      delete s;
+      return set_err(RS_E_INVALID_ARG, "parts = %u: must be <= %u and <= n_levels (%u)", p, kMaxParts, g->cg.n_levels);
+    }
+    s->n_tiles = s->parts;  // one state replica per partition (lane index = replica in the aux kernels)
   } else {
+    if (o.parts > 1) {
+      delete s;
+      return set_err(RS_E_INVALID_ARG, "parts (level cut) applies to RS_MODE_SINGLE only");
+    }
     if (o.lane_tile && o.lane_tile != 8 && o.lane_tile != 16 && o.lane_tile != 32) {
       delete s;
       return set_err(RS_E_INVALID_ARG, "lane_tile must be 8, 16 or 32");
@@ -400,23 +427,44 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     const CompiledGraph& cg = g->cg;
     const uint64_t est = 4ull * cg.n_ops_total() + 4ull * cg.coord.size() + 12ull * cg.n_regs + 8ull * cg.n_inputs;
     const uint32_t kMaxSlice = 212 * 1024;  // + static shared memory stays below the 227 KB per-CTA limit
-    uint32_t G = (uint32_t)std::max<uint64_t>({1, (est + kMaxSlice / 2) / (kMaxSlice * 3 / 4), (maxops + 1023) / 1024});
-    G = std::min<uint32_t>(G, (uint32_t)g->sm_count);
+    const uint32_t P = s->parts, maxG = (uint32_t)g->sm_count / P;
+    uint32_t G = (uint32_t)std::max<uint64_t>({1, (est + kMaxSlice / 2) / (kMaxSlice * 3 / 4) / P, (maxops + 1023) / 1024});
+    G = std::min<uint32_t>(G, maxG);
     std::vector<uint8_t> sblob;
     std::vector<uint64_t> soff;
     bool ok = false;
-    while (true) {
-      ok = build_single_slices(cg, G, kMaxSlice, &sblob, &soff);
-      if (ok || G >= (uint32_t)g->sm_count) break;
-      G = std::min<uint32_t>((uint32_t)g->sm_count, G + std::max<uint32_t>(1, G / 4));
+    while (true) {  // G = CTAs per partition
+      ok = build_single_slices(cg, P, G, kMaxSlice, &sblob, &soff);
+      if (ok || G >= maxG) break;
+      G = std::min<uint32_t>(maxG, G + std::max<uint32_t>(1, G / 4));
+    }
+    if (!ok && P > 1) {
+      delete s;
+      return set_err(RS_E_CAPACITY, "level cut: %u partitions' slices do not fit %u co-resident CTAs", P, maxG * P);
     }
     if (ok && !o.threads) {
       const uint32_t chunk = std::max<uint32_t>(1, (maxops + G - 1) / G);
       s->threads = std::min<uint32_t>(1024, 32u * chunk);  // up to one op per warp (single.cuh op slots)
     }
+    if (ok && P > 1) {
+      std::vector<uint8_t> owner[4];
+      row_owner(cg, level_cut(cg, P), owner);
+      s->sig_part.assign(cg.n_signals, 0);
+      for (uint32_t id = 0; id < cg.n_signals; ++id)
+        if (cg.sig_kind[id] == 3) s->sig_part[id] = owner[cg.sig_coord[id] >> 30][cg.sig_coord[id] & ROW_MASK];
+    }
     if (ok) {
-      uint32_t smax = 0;
-      for (uint32_t i = 0; i < G; ++i) smax = std::max(smax, reinterpret_cast<const SliceHdr*>(sblob.data() + soff[i])->bytes);
+      s->gp = G;
+      G *= P;
+      uint32_t smax = 0, hmax = 0;
+      for (uint32_t i = 0; i < G; ++i) {
+        const SliceHdr* sh = reinterpret_cast<const SliceHdr*>(sblob.data() + soff[i]);
+        smax = std::max(smax, sh->bytes);
+        hmax = std::max(hmax, sh->head_bytes);
+      }
+      // tails (latch / push / inject lists) stay in global memory unless every slice fits whole
+      s->tail_global = smax > kMaxSlice;
+      if (s->tail_global) smax = hmax;
       const size_t off_off = (sblob.size() + 255) & ~(size_t)255;
       cudaError_t e2 = cudaMalloc(&s->dslices, off_off + G * 8);
       if (e2 == cudaSuccess) e2 = cudaMemcpy(s->dslices, sblob.data(), sblob.size(), cudaMemcpyHostToDevice);
@@ -481,7 +529,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
   }
   const size_t lanes_pad = (size_t)s->n_tiles * s->LT;
   if ((e = cudaMalloc(&s->hcarry, 2 * lanes_pad * sizeof(uint64_t))) != cudaSuccess ||
-      (e = cudaMalloc(&s->bar, 256)) != cudaSuccess) {
+      (e = cudaMalloc(&s->bar, kBarBytes)) != cudaSuccess) {
     rs_free_lanes(s);
     return set_err(RS_E_OOM, "cudaMalloc: %s", cudaGetErrorString(e));
   }
@@ -493,7 +541,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     }
     s->stage_cap = o.stage_cycles;
   }
-  s->total_bytes += s->state_bytes + 2 * lanes_pad * 8 + 256 +
+  s->total_bytes += s->state_bytes + 2 * lanes_pad * 8 + kBarBytes +
                    (size_t)s->stage_cap * std::max<uint32_t>(1, g->cg.n_inputs) * n_lanes * 8;
   if (o.stream) {
     s->stream = (cudaStream_t)o.stream;
@@ -659,14 +707,24 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
       CU(cudaMemsetAsync(a.hcarry_out, 0, 8, s->stream));
       if (hout) CU(cudaMemsetAsync(hout, 0, hn * 8, s->stream));
     }
-    CU(cudaMemsetAsync(s->bar, 0, 8, s->stream));
+    CU(cudaMemsetAsync(s->bar, 0, kBarBytes, s->stream));
     cudaError_t e;
     if (s->slice_blob) {
       const bool grid = s->ctas > 1;
       const uint32_t smax = (s->slice_max + 127u) & ~127u;
       const uint32_t st_smem =
           (!grid && smax + s->tile_bytes <= 200u * 1024u) ? (uint32_t)s->tile_bytes : 0u;
-      SingleArgs sa{a, s->slice_blob, s->slice_off, smax, st_smem};
+      SingleArgs sa{};
+      sa.a = a;
+      sa.slice_blob = s->slice_blob;
+      sa.slice_off = s->slice_off;
+      sa.slice_max = smax;
+      sa.state_smem = s->parts > 1 ? 0u : st_smem;
+      sa.parts = s->parts;
+      sa.tail_global = s->tail_global ? 1u : 0u;
+      sa.gp = s->gp;
+      sa.flags = s->bar + kFlagOffset;
+      for (uint32_t k = 0; k < s->parts; ++k) sa.rep[k] = (uint8_t*)s->state_mem + (size_t)k * s->tile_bytes;
       void* args[] = {&sa};
       const void* fn = grid ? (hash ? (const void*)k_single2<true, true> : (const void*)k_single2<true, false>)
                             : (hash ? (const void*)k_single2<false, true> : (const void*)k_single2<false, false>);
@@ -729,22 +787,28 @@ rs_status rs_read_signals(rs_lanes* s, const uint32_t* ids, uint32_t n_ids, uint
   }
   rs_status st = set_device(s->g);
   if (st != RS_OK) return st;
-  const size_t n = (size_t)n_ids * n_lanes;
+  // level cut: read every replica (the aux kernels see replica k as lane k), keep the producer's
+  const uint32_t P = s->parts;
+  const uint32_t rb = P > 1 ? 0 : lane_begin, rn = P > 1 ? P : n_lanes;
+  const size_t n = (size_t)n_ids * rn;
   void* tmp = nullptr;
   CU(cudaMalloc(&tmp, n * 8 + n_ids * 4 + 8));
   uint64_t* dout = (uint64_t*)tmp;
   uint32_t* dco = (uint32_t*)(dout + n);
+  std::vector<uint64_t> all(P > 1 ? n : 0);
   cudaError_t e = cudaMemcpyAsync(dco, coords.data(), n_ids * 4, cudaMemcpyHostToDevice, s->stream);
   if (e == cudaSuccess) {
     StepArgs a = base_args(s);
-    k_read<<<(unsigned)std::min<size_t>(8192, (n + 255) / 256), 256, 0, s->stream>>>(a, dco, n_ids, lane_begin, n_lanes, dout);
+    k_read<<<(unsigned)std::min<size_t>(8192, (n + 255) / 256), 256, 0, s->stream>>>(a, dco, n_ids, rb, rn, dout);
     s->launches++;
     e = cudaGetLastError();
   }
-  if (e == cudaSuccess) e = cudaMemcpyAsync(out, dout, n * 8, cudaMemcpyDeviceToHost, s->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(P > 1 ? all.data() : out, dout, n * 8, cudaMemcpyDeviceToHost, s->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
   cudaFree(tmp);
   if (e != cudaSuccess) return set_err(RS_E_CUDA, "read_signals: %s", cudaGetErrorString(e));
+  if (P > 1)
+    for (uint32_t i = 0; i < n_ids; ++i) out[i] = all[(size_t)i * P + s->sig_part[ids[i]]];
   return RS_OK;
 }
 
@@ -762,7 +826,17 @@ rs_status rs_write_registers(rs_lanes* s, const uint32_t* reg_ids, uint32_t n, u
   }
   rs_status st = set_device(s->g);
   if (st != RS_OK) return st;
-  const size_t nv = (size_t)n * n_lanes;
+  // level cut: every replica holds every register
+  const uint32_t P = s->parts;
+  const uint32_t wb = P > 1 ? 0 : lane_begin, wn = P > 1 ? P : n_lanes;
+  std::vector<uint64_t> rv;
+  if (P > 1) {
+    rv.resize((size_t)n * P);
+    for (uint32_t i = 0; i < n; ++i)
+      for (uint32_t k = 0; k < P; ++k) rv[(size_t)i * P + k] = values[i];
+    values = rv.data();
+  }
+  const size_t nv = (size_t)n * wn;
   void* tmp = nullptr;
   CU(cudaMalloc(&tmp, nv * 8 + cw.size() * 4 + 8));
   uint64_t* dv = (uint64_t*)tmp;
@@ -771,7 +845,7 @@ rs_status rs_write_registers(rs_lanes* s, const uint32_t* reg_ids, uint32_t n, u
   if (e == cudaSuccess) e = cudaMemcpyAsync(dc, cw.data(), cw.size() * 4, cudaMemcpyHostToDevice, s->stream);
   if (e == cudaSuccess) {
     StepArgs a = base_args(s);
-    k_write<<<(unsigned)std::min<size_t>(8192, (nv + 255) / 256), 256, 0, s->stream>>>(a, dc, dc + n, n, lane_begin, n_lanes, dv);
+    k_write<<<(unsigned)std::min<size_t>(8192, (nv + 255) / 256), 256, 0, s->stream>>>(a, dc, dc + n, n, wb, wn, dv);
     s->launches++;
     e = cudaGetLastError();
   }

@@ -20,6 +20,13 @@ struct SingleArgs {
   const uint64_t* slice_off;
   uint32_t slice_max;    // bytes of the largest slice (128-aligned; dynamic shared memory)
   uint32_t state_smem;   // single-CTA launches: bytes of signal state kept in shared memory (0 = off)
+  // level cut (compiler.hpp SliceHdr): CTAs [k*gp, (k+1)*gp)
+  // run partition k on replica rep[k]; partition k publishes "cycle c done"
+  // as flags[k] = c + 1 (launch-relative).  parts == 1: plain single-lane.
+  uint32_t parts, gp;
+  uint32_t tail_global;  // slice tails (push / latch / inject lists) read from global memory
+  unsigned long long* flags;
+  uint8_t* rep[kMaxParts];
 };
 
 __device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v) {
@@ -30,8 +37,8 @@ __device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned 
 // in wsum[warp] (or 0): the CTA's sum is added to *hsum (relaxed atomic) by
 // thread 0 on the way in.
 template <bool GRID>
-__device__ __forceinline__ void single_barrier(unsigned long long* bar, unsigned long long& target, uint64_t* wsum,
-                                               unsigned long long* hsum) {
+__device__ __forceinline__ void single_barrier(unsigned long long* bar, unsigned long long& target, uint32_t nctas,
+                                               uint64_t* wsum, unsigned long long* hsum) {
   __syncthreads();
   if (threadIdx.x == 0) {
     if (hsum) {
@@ -40,7 +47,7 @@ __device__ __forceinline__ void single_barrier(unsigned long long* bar, unsigned
       atomicAdd(hsum, (unsigned long long)s);
     }
     if constexpr (GRID) {
-      target += gridDim.x;
+      target += nctas;
       red_release_add(bar, 1ull);
       while (ld_acquire(bar) < target) {
       }
@@ -143,6 +150,10 @@ __device__ __forceinline__ uint64_t single_eval(const SState<GRID>& S, uint32_t 
   return r & wmask(pw & 127u);
 }
 
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 template <bool GRID, bool HASH>
 __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
   const StepArgs& a = sa.a;
@@ -151,7 +162,8 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
   const uint32_t tid = threadIdx.x, T = blockDim.x;
   {  // this CTA's slice of the graph, resident for the whole launch
     const uint8_t* src = sa.slice_blob + sa.slice_off[blockIdx.x];
-    const uint32_t bytes = reinterpret_cast<const SliceHdr*>(src)->bytes;
+    const SliceHdr* sh = reinterpret_cast<const SliceHdr*>(src);
+    const uint32_t bytes = sa.tail_global ? sh->head_bytes : sh->bytes;
     for (uint32_t i = tid * 16; i < bytes; i += T * 16)
       *reinterpret_cast<uint4*>(smem + i) = __ldg(reinterpret_cast<const uint4*>(src + i));
   }
@@ -162,11 +174,16 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
   const SliceSeg* seg = reinterpret_cast<const SliceSeg*>(smem + h->off_seg);
   const uint32_t* pws = reinterpret_cast<const uint32_t*>(smem + h->off_pw);
   const uint32_t* crd = reinterpret_cast<const uint32_t*>(smem + h->off_coord);
-  const uint32_t* lat = reinterpret_cast<const uint32_t*>(smem + h->off_latch);
-  const uint32_t* inj = reinterpret_cast<const uint32_t*>(smem + h->off_inj);
+  const uint8_t* tail = sa.tail_global ? sa.slice_blob + sa.slice_off[blockIdx.x] : smem;
+  const uint32_t* lat = reinterpret_cast<const uint32_t*>(tail + h->off_latch);
+  const uint32_t* inj = reinterpret_cast<const uint32_t*>(tail + h->off_inj);
+  const uint32_t* psh = reinterpret_cast<const uint32_t*>(tail + h->off_push);
+  const uint32_t part = h->part, P = sa.parts;
+  const bool lead = blockIdx.x == 0;               // adds the launch-wide hash terms
+  unsigned long long* bar = a.bar + 4 * part;      // partition-local grid barrier
 
   // single CTA with a small state: the whole signal state lives in shared memory
-  uint8_t* st_base = a.state;
+  uint8_t* st_base = P > 1 ? sa.rep[part] : a.state;
   if (!GRID && sa.state_smem) {
     st_base = smem + sa.slice_max;
     for (uint32_t i = tid * 16; i < sa.state_smem; i += T * 16)
@@ -178,10 +195,23 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
   S.r1 = a.region[1] - a.region[0];
   S.r2 = a.region[2] - a.region[0];
   S.r3 = a.region[3] - a.region[0];
+  // the same signal in replica m (level cut): same offset from the replica base
+  auto peer = [&](uint32_t c, uint32_t m) -> uint8_t* { return sa.rep[m] + (S.addr(c) - st_base); };
+  auto peer_st = [&](uint32_t c, uint32_t m, uint64_t v) {
+    uint8_t* q = peer(c, m);
+    switch (c >> 30) {
+      case 0: *q = (uint8_t)v; break;
+      case 1: *reinterpret_cast<uint16_t*>(q) = (uint16_t)v; break;
+      case 2: *reinterpret_cast<uint32_t*>(q) = (uint32_t)v; break;
+      default: *reinterpret_cast<uint64_t*>(q) = v; break;
+    }
+  };
   unsigned long long target = 0;
-  uint64_t hacc = (HASH && blockIdx.x == 0 && tid == 0) ? a.hcarry_in[0] + a.g.const_hash : 0ull;
+  uint64_t hacc = (HASH && lead && tid == 0) ? a.hcarry_in[0] + a.g.const_hash : 0ull;
 
-  const uint64_t kinj = (HASH && tid < h->n_inj) ? __ldg(a.g.in_k + h->inj_first + tid) : 0ull;
+  // inputs are injected into every replica; partition 0 hashes them
+  const bool hin_on = HASH && part == 0;
+  const uint64_t kinj = (hin_on && tid < h->n_inj) ? __ldg(a.g.in_k + h->inj_first + tid) : 0ull;
   auto inject = [&](uint64_t cyc) -> uint64_t {
     uint64_t hh = 0;
     for (uint32_t i = tid; i < h->n_inj; i += T) {
@@ -190,13 +220,13 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
                             : d_stimulus(a.seed, k, cyc, a.lane0);
       v &= wmask(inj[2 * i + 1]);
       S.st(inj[2 * i], v);
-      if (HASH) hh += v * (i == tid ? kinj : __ldg(a.g.in_k + k));
+      if (hin_on) hh += v * (i == tid ? kinj : __ldg(a.g.in_k + k));
     }
     return hh;
   };
   if (a.n_cycles == 0) return;
   hacc += inject(a.cycle0);
-  single_barrier<GRID>(a.bar, target, wsum, nullptr);
+  single_barrier<GRID>(bar, target, sa.gp, wsum, nullptr);
   uint64_t hr = 0;
   // op slot of this thread: ops are dealt to warps first (op t -> warp t % W,
   // lane t / W), so a level with few ops puts one op per warp -- the warps run
@@ -211,9 +241,18 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
     return top < L.n ? __ldg(a.g.opk + L.op_begin + top) : 0ull;
   };
   uint64_t knext = kload(0);
-  const uint64_t klat = (HASH && tid < h->n_latch) ? __ldg(a.g.reg_k + h->latch_first + tid) : 0ull;
+  const uint64_t klat = (HASH && tid < h->n_latch && (lat[4 * tid + 2] & 128u)) ? __ldg(a.g.reg_k + lat[4 * tid + 3]) : 0ull;
 #pragma unroll 1
   for (uint32_t cyc = 0; cyc < a.n_cycles; ++cyc) {
+    if (P > 1) {  // token ring: partition k runs cycle c after k-1 finished it; 0 after P-1 finished c-1
+      if (tid == 0) {
+        const unsigned long long* f = sa.flags + (part == 0 ? P - 1 : part - 1);
+        const unsigned long long want = part == 0 ? cyc : cyc + 1;
+        while (ld_acquire(f) < want) {
+        }
+      }
+      __syncthreads();
+    }
 #pragma unroll 1
     for (uint32_t l = 0; l < h->n_levels; ++l) {
       const SliceLvl L = lvl[l];
@@ -233,7 +272,7 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
         S.st(G_.out_coord0 + (t - G_.first), y);
         if (HASH) hacc += y * k;
       }
-      single_barrier<GRID>(a.bar, target, wsum, nullptr);
+      single_barrier<GRID>(bar, target, sa.gp, wsum, nullptr);
 #ifdef RS_TRACE
       if (blockIdx.x == 0 && tid == 0 && a.trace && cyc < 8) a.trace[cyc * 64 + l] = clock64();
 #endif
@@ -241,20 +280,33 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
     hr = 0;
 #pragma unroll 1
     for (uint32_t i = tid; i < h->n_latch; i += T) {
-      const uint64_t x = S.ld(lat[3 * i]) & wmask(lat[3 * i + 2]);
-      S.st(lat[3 * i + 1], x);
-      if (HASH) hr += x * (i == tid ? klat : __ldg(a.g.reg_k + h->latch_first + i));
+      const uint32_t wf = lat[4 * i + 2];
+      const uint64_t x = S.ld(lat[4 * i]) & wmask(wf & 127u);
+      S.st(lat[4 * i + 1], x);
+      if (wf & 128u) {  // own register: hash it; publish it to the replicas that finished the cycle
+        if (HASH) hr += x * (i == tid ? klat : __ldg(a.g.reg_k + lat[4 * i + 3]));
+        for (uint32_t m = wf >> 8; m; m &= m - 1) peer_st(lat[4 * i + 1], __ffs(m) - 1, x);
+      }
+    }
+    if (P > 1) {  // cut signals to the later partitions that read them
+#pragma unroll 1
+      for (uint32_t i = tid; i < h->n_push; i += T) {
+        const uint32_t c = psh[2 * i];
+        const uint64_t v = S.ld(c);
+        for (uint32_t m = psh[2 * i + 1]; m; m &= m - 1) peer_st(c, __ffs(m) - 1, v);
+      }
     }
     uint64_t hin = 0;
     if (cyc + 1 < a.n_cycles) hin = inject(a.cycle0 + cyc + 1);
     if (HASH) {
       warp_partial(hacc, wsum);
-      hacc = hr + hin + ((blockIdx.x == 0 && tid == 0) ? a.g.const_hash : 0ull);
+      hacc = hr + hin + ((lead && tid == 0) ? a.g.const_hash : 0ull);
     }
 #ifdef RS_TRACE
     if (blockIdx.x == 0 && tid == 0 && a.trace && cyc < 8) a.trace[cyc * 64 + 60] = clock64();
 #endif
-    single_barrier<GRID>(a.bar, target, wsum, (HASH && a.hashes) ? (unsigned long long*)(a.hashes + cyc) : nullptr);
+    single_barrier<GRID>(bar, target, sa.gp, wsum, (HASH && a.hashes) ? (unsigned long long*)(a.hashes + cyc) : nullptr);
+    if (P > 1 && tid == 0 && blockIdx.x == part * sa.gp) st_release(sa.flags + part, cyc + 1);
 #ifdef RS_TRACE
     if (blockIdx.x == 0 && tid == 0 && a.trace && cyc < 8) a.trace[cyc * 64 + 61] = clock64();
 #endif

@@ -25,7 +25,8 @@ STATUS = {0: "RS_OK", -1: "RS_E_INVALID_ARG", -2: "RS_E_GRAPH", -3: "RS_E_CAPACI
 EXPORTS = ["rs_version", "rs_last_error", "rs_load_graph", "rs_graph_info_get", "rs_free_graph",
            "rs_alloc_lanes", "rs_free_lanes", "rs_lanes_bytes", "rs_set_input_seed", "rs_set_inputs",
            "rs_step_cycles", "rs_read_signals", "rs_write_registers", "rs_get_cycle", "rs_set_cycle",
-           "rs_launch_count", "rs_launch_shape", "rs_sync", "rs_graph_export", "rs_debug_trace"]
+           "rs_launch_count", "rs_launch_shape", "rs_sync", "rs_graph_export", "rs_debug_trace",
+           "rs_level_cut"]
 RS_DEVICE_NONE = -1
 EXPORT = {"runs": (0, np.uint32), "level_run_begin": (1, np.uint32), "level_op_begin": (2, np.uint32),
           "opw": (3, np.uint32), "opk": (4, np.uint64), "coord_off": (5, np.uint32), "coord": (6, np.uint32),
@@ -63,7 +64,8 @@ class GraphInfo(C.Structure):
 
 class LaneOpts(C.Structure):
     _fields_ = [("lane0", C.c_uint64), ("lane_tile", C.c_uint32), ("threads", C.c_uint32),
-                ("stage_cycles", C.c_uint32), ("cluster", C.c_uint32), ("stream", C.c_void_p)]
+                ("stage_cycles", C.c_uint32), ("cluster", C.c_uint32), ("stream", C.c_void_p),
+                ("parts", C.c_uint32), ("pad_", C.c_uint32)]
 
 
 _lib = None
@@ -100,6 +102,7 @@ def lib() -> C.CDLL:
             "rs_sync": (i32, [vp]),
             "rs_graph_export": (i32, [vp, u32, vp, C.POINTER(u64)]),
             "rs_debug_trace": (i32, [vp, vp, u64]),
+            "rs_level_cut": (i32, [vp, u32, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -177,6 +180,12 @@ class Graph:
         out = out[:n.value]
         return out.reshape(-1, 5) if what == "runs" else out
 
+    def level_cut(self, parts: int) -> np.ndarray:
+        """rs_level_cut: level boundaries [parts + 1] of a parts-way level cut."""
+        out = np.zeros(parts + 1, dtype=np.uint32)
+        _check(lib().rs_level_cut(self.h, parts, _ptr(out)))
+        return out
+
     def close(self):
         if getattr(self, "h", None):
             lib().rs_free_graph(self.h)
@@ -194,12 +203,12 @@ class Lanes:
     lane0 .. lane0 + n_lanes - 1)."""
 
     def __init__(self, graph: Graph, n_lanes: int, lane0: int = 0, lane_tile: int = 0, threads: int = 0,
-                 stage_cycles: int = 0, stream=None, cluster: int = 0):
+                 stage_cycles: int = 0, stream=None, cluster: int = 0, parts: int = 0):
         self.graph = graph
         self.n_lanes = n_lanes
         self.lane0 = lane0
         st = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
-        self.opts = LaneOpts(lane0, lane_tile, threads, stage_cycles, cluster, st)
+        self.opts = LaneOpts(lane0, lane_tile, threads, stage_cycles, cluster, st, parts, 0)
         h = C.c_void_p()
         _check(lib().rs_alloc_lanes(graph.h, n_lanes, C.byref(self.opts), C.byref(h)))
         self.h = h

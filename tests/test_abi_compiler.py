@@ -218,3 +218,28 @@ def test_identity_copy_for_register_chains(rs):
     assert g.info()["n_copy_ops"] == 5            # next(r0) = input, next(r_k) = register
     c2, _, _ = cf.swap(8, 1, 2)
     assert _graph(rs, c2).info()["n_copy_ops"] == 2
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_level_cut_ranges(rs, name):
+    """rs_level_cut: contiguous non-empty level ranges
+    covering all levels, balanced by op weight to within one level's weight."""
+    c = config_circuit(name, **({"n_ops": 30000, "n_regs": 3000} if name == "C3" else {}))
+    g = rs.Graph(c, device=rs.RS_DEVICE_NONE, mode="single")
+    nl = g.info()["n_levels"]
+    lob = g.export("level_op_begin").astype(np.int64)
+    co = g.export("coord_off").astype(np.int64)
+    wl = lob + co[lob]                       # cumulative weight (1 + arity) at level boundaries
+    for parts in (1, 2, 3, 4, 8):
+        if parts > nl:
+            continue
+        cut = g.level_cut(parts).astype(np.int64)
+        assert cut[0] == 0 and cut[-1] == nl and np.all(np.diff(cut) >= 1)
+        w = np.diff(wl[cut])
+        assert w.sum() == wl[-1]
+        maxlvl = np.diff(wl).max()
+        assert np.all(np.abs(w - wl[-1] / parts) <= maxlvl + 1), (parts, w.tolist())
+    with pytest.raises(rs.RtlSimError):
+        g.level_cut(0)
+    with pytest.raises(rs.RtlSimError):
+        g.level_cut(9)
