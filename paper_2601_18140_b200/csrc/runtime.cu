@@ -164,6 +164,7 @@ void bind_stages(const rs_graph* g, uint32_t LT, const uint64_t* region, std::ve
 
 rs_status set_device(const rs_graph* g) {
   CU(cudaSetDevice(g->device));
+  (void)cudaGetLastError();  // a stale non-sticky error of an unrelated earlier call must not surface here
   return RS_OK;
 }
 
@@ -796,17 +797,25 @@ rs_status rs_read_signals(rs_lanes* s, const uint32_t* ids, uint32_t n_ids, uint
   uint64_t* dout = (uint64_t*)tmp;
   uint32_t* dco = (uint32_t*)(dout + n);
   std::vector<uint64_t> all(P > 1 ? n : 0);
+  const char* what = "ids H2D";
   cudaError_t e = cudaMemcpyAsync(dco, coords.data(), n_ids * 4, cudaMemcpyHostToDevice, s->stream);
   if (e == cudaSuccess) {
     StepArgs a = base_args(s);
+    what = "k_read launch";
     k_read<<<(unsigned)std::min<size_t>(8192, (n + 255) / 256), 256, 0, s->stream>>>(a, dco, n_ids, rb, rn, dout);
     s->launches++;
     e = cudaGetLastError();
   }
-  if (e == cudaSuccess) e = cudaMemcpyAsync(P > 1 ? all.data() : out, dout, n * 8, cudaMemcpyDeviceToHost, s->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+  if (e == cudaSuccess) {
+    what = "D2H";
+    e = cudaMemcpyAsync(P > 1 ? all.data() : out, dout, n * 8, cudaMemcpyDeviceToHost, s->stream);
+  }
+  if (e == cudaSuccess) {
+    what = "sync";
+    e = cudaStreamSynchronize(s->stream);
+  }
   cudaFree(tmp);
-  if (e != cudaSuccess) return set_err(RS_E_CUDA, "read_signals: %s", cudaGetErrorString(e));
+  if (e != cudaSuccess) return set_err(RS_E_CUDA, "read_signals (%s): %s", what, cudaGetErrorString(e));
   if (P > 1)
     for (uint32_t i = 0; i < n_ids; ++i) out[i] = all[(size_t)i * P + s->sig_part[ids[i]]];
   return RS_OK;

@@ -1,0 +1,15 @@
+#!/bin/bash
+# One GPU session: parity tests, bench lines, ncu launch list + one full capture.
+cd "$GRAFT_REPO_ROOT"; O=gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $O/smi.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
+timeout 600 python bench.py > $O/bench_C2.json 2> $O/bench_C2.err
+timeout 600 python bench.py --config C3 --cycles 1000 --steps 3 --no-e2e > $O/bench_C3.json 2> $O/bench_C3.err
+timeout 300 python bench.py --config C5 --cycles 2000 --steps 3 --no-e2e --no-cpu > $O/bench_C5.json 2> $O/bench_C5.err
+timeout 300 python bench.py --config C1 --cycles 1000 --steps 3 --no-e2e --no-cpu > $O/bench_C1.json 2> $O/bench_C1.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_C2.csv \
+   python bench.py --steps 2 --warmup 3 --cycles 1000 --no-cpu > $O/ncu_launch.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_lanes -s 3 -c 1 -o $O/k_lanes_C2 -f \
+   python bench.py --steps 1 --warmup 3 --cycles 200 --no-cpu --no-e2e > $O/ncu_full.log 2>&1
+echo done
