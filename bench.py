@@ -164,6 +164,7 @@ def main():
     ap.add_argument("--lane-tile", type=int, default=0)
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--cluster", type=int, default=0)
+    ap.add_argument("--kernel", type=int, default=0, help="lane kernel: 0 auto, 1 lane/thread, 2 two lanes/thread")
     ap.add_argument("--parts", type=int, default=0, help="C1/C5: level-cut partitions emulated on this GPU")
     ap.add_argument("--ref-step-s", type=float, default=4.0)
     args = ap.parse_args()
@@ -197,7 +198,7 @@ def main():
     g = rs.Graph(circ, device=local, mode="single" if single else "lanes")
     info = g.info()
     L = rs.Lanes(g, lanes, lane0=shard.lane0, lane_tile=args.lane_tile, threads=args.threads, stream=stream,
-                 cluster=args.cluster, parts=args.parts)
+                 cluster=args.cluster, parts=args.parts, kernel=args.kernel)
     L.set_seed(cfg.stim_seed)
     hashes = None if args.no_hash else torch.empty(cycles * lanes, dtype=torch.int64, device="cuda")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
@@ -251,7 +252,7 @@ def main():
     if not args.no_e2e:
         chunk = min(cycles, max(1, (256 << 20) // max(1, 8 * circ.n_inputs * lanes)))
         Ls = rs.Lanes(g, lanes, lane0=shard.lane0, lane_tile=args.lane_tile, threads=args.threads, cluster=args.cluster,
-                      stage_cycles=chunk, stream=stream, parts=args.parts)
+                      stage_cycles=chunk, stream=stream, parts=args.parts, kernel=args.kernel)
         rng = np.random.default_rng(rank)
         host_in = torch.from_numpy(rng.integers(0, 2**63, size=(chunk, circ.n_inputs, lanes),
                                                 dtype=np.int64)).pin_memory()

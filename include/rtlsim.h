@@ -129,7 +129,10 @@ typedef struct {
                               values) into its replica.  On one device the partitions are CTA groups of
                               one cooperative launch.  RS_E_CAPACITY if the slices do not fit
                               co-resident, RS_E_INVALID_ARG if parts > n_levels or > 8. */
-  uint32_t pad_;
+  uint32_t kernel;         /* RS_MODE_LANES step kernel: 0 = auto (1), 1 = one lane per thread (a tile's LT
+                              lanes are one sub-warp, operand container widths dispatched by a uniform
+                              branch), 2 = two lanes per thread (aligned 64-bit word gathers + extraction);
+                              results are identical.  RS_E_INVALID_ARG otherwise. */
 } rs_lane_opts;
 
 typedef struct rs_graph rs_graph;
@@ -216,6 +219,8 @@ uint64_t rs_launch_count(const rs_lanes* s);
  * (any output pointer may be NULL). */
 rs_status rs_launch_shape(const rs_lanes* s, uint32_t* lane_tile, uint32_t* threads, uint32_t* ctas,
                           uint32_t* cluster);
+/* Lane-mode step kernel in use (rs_lane_opts.kernel: 1 or 2); 0 for single-lane mode or NULL. */
+uint32_t rs_lanes_kernel(const rs_lanes* s);
 rs_status rs_sync(rs_lanes* s);
 /* Diagnostics (builds with -DRS_TRACE only, else RS_E_UNSUPPORTED): the first
  * call arms a per-stage clock64 trace of CTA 0; later calls copy up to n u64

@@ -14,6 +14,7 @@
 #include "compiler.hpp"
 #include "kernels.cuh"
 #include "lanes.cuh"
+#include "lanes_t.cuh"
 #include "single.cuh"
 
 using namespace rtlsim;
@@ -69,7 +70,7 @@ struct rs_graph {
 
 struct rs_lanes {
   rs_graph* g = nullptr;
-  uint32_t n_lanes = 0, LT = 1, n_tiles = 1, threads = 1024, ctas = 1, cluster = 1;
+  uint32_t n_lanes = 0, LT = 1, n_tiles = 1, threads = 1024, ctas = 1, cluster = 1, variant = 1;
   uint64_t lane0 = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -187,24 +188,30 @@ size_t lanes_smem(uint32_t stage_bytes, uint32_t threads) {
   return 128 + 2ull * stage_bytes + lanes_smem_extra(threads);
 }
 
-// Lane tile and cluster size: the widest tile (32 lanes: every warp
-// instruction does 32 lanes of work), spread over the fewest CTAs of a
-// cluster that keeps >= 80% of the SMs busy; narrower tiles only when even an
-// 8-CTA cluster per 32-lane tile cannot fill the GPU.
-void choose_tiling(uint32_t n_lanes, int sms, uint32_t want_lt, uint32_t want_cs, uint32_t* lt, uint32_t* cs) {
-  for (uint32_t t : {32u, 16u, 8u}) {
+// Lane tile and cluster size: the widest tile (most lanes per warp
+// instruction), spread over the fewest CTAs of a cluster that keeps >= 80% of
+// the SMs busy; narrower tiles only when even an 8-CTA cluster per tile
+// cannot fill the GPU.  Kernel 1 tiles are 32 * P lanes (P = 1, 2, 4 lanes per
+// thread), kernel 2 tiles 8, 16 or 32 lanes.
+void choose_tiling(uint32_t kernel, uint32_t n_lanes, int sms, uint32_t want_lt, uint32_t want_cs, uint32_t* lt,
+                   uint32_t* cs) {
+  const uint32_t k1[3] = {128u, 64u, 32u}, k2[3] = {32u, 16u, 8u};
+  const uint32_t* cand = kernel == 1 ? k1 : k2;
+  const uint32_t smallest = cand[2];
+  for (int i = 0; i < 3; ++i) {
+    const uint32_t t = cand[i];
     if (want_lt && t != want_lt) continue;
     const uint64_t tiles = (n_lanes + t - 1) / t;
     for (uint32_t c : {1u, 2u, 4u, 8u}) {
       if (want_cs && c != want_cs) continue;
-      if (tiles * c * 10 >= (uint64_t)sms * 8 || (want_lt && want_cs) || (t == 8 && c == 8)) {
+      if (tiles * c * 10 >= (uint64_t)sms * 8 || (want_lt && want_cs) || (t == smallest && c == 8)) {
         *lt = t;
         *cs = c;
         return;
       }
     }
   }
-  *lt = want_lt ? want_lt : 8;
+  *lt = want_lt ? want_lt : smallest;
   *cs = want_cs ? want_cs : 8;
 }
 
@@ -392,16 +399,23 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
       delete s;
       return set_err(RS_E_INVALID_ARG, "parts (level cut) applies to RS_MODE_SINGLE only");
     }
-    if (o.lane_tile && o.lane_tile != 8 && o.lane_tile != 16 && o.lane_tile != 32) {
+    const uint32_t kern = o.kernel == 2 ? 2u : 1u;
+    if (o.lane_tile && (kern == 2 ? (o.lane_tile != 8 && o.lane_tile != 16 && o.lane_tile != 32)
+                                  : (o.lane_tile != 32 && o.lane_tile != 64 && o.lane_tile != 128))) {
       delete s;
-      return set_err(RS_E_INVALID_ARG, "lane_tile must be 8, 16 or 32");
+      return set_err(RS_E_INVALID_ARG, "lane_tile must be 32, 64 or 128 (kernel 1) or 8, 16 or 32 (kernel 2)");
     }
     if (o.cluster && o.cluster != 1 && o.cluster != 2 && o.cluster != 4 && o.cluster != 8) {
       delete s;
       return set_err(RS_E_INVALID_ARG, "cluster must be 1, 2, 4 or 8");
     }
+    if (o.kernel > 2) {
+      delete s;
+      return set_err(RS_E_INVALID_ARG, "kernel must be 0, 1 or 2");
+    }
+    s->variant = kern;
     uint32_t lt, cs;
-    choose_tiling(n_lanes, g->sm_count, o.lane_tile, o.cluster, &lt, &cs);
+    choose_tiling(kern, n_lanes, g->sm_count, o.lane_tile, o.cluster, &lt, &cs);
     s->LT = lt;
     s->cluster = cs;
     s->n_tiles = (n_lanes + lt - 1) / lt;
@@ -409,7 +423,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
   // launch shape
   if (o.threads) {
     if (o.threads % 32 || o.threads > (g->cg.mode == RS_MODE_SINGLE ? 1024u : (uint32_t)RS_LANES_MAX_THREADS) ||
-        o.threads < s->LT) { delete s; return set_err(RS_E_INVALID_ARG, "threads must be a multiple of 32 in [32, 1024]"); }
+        o.threads < (s->variant == 1 ? 32u : s->LT)) { delete s; return set_err(RS_E_INVALID_ARG, "threads must be a multiple of 32 in [32, 1024]"); }
     s->threads = o.threads;
   } else if (g->cg.mode == RS_MODE_SINGLE) {
     s->threads = 1024;
@@ -740,16 +754,21 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
     if (hash) s->hc_cur = 1 - s->hc_cur;
   } else {
     a.hcarry_out = a.hcarry_in;
-    const size_t smem = lanes_smem(s->g->stage_bytes, s->threads);
+    const size_t smem = s->variant == 1 ? 128 + 2ull * s->g->stage_bytes + lanes_t_smem_extra(s->threads, s->LT / 32)
+                                        : lanes_smem(s->g->stage_bytes, s->threads);
     const void* fns[] = {(const void*)k_lanes<32, true>, (const void*)k_lanes<32, false>,
                          (const void*)k_lanes<16, true>, (const void*)k_lanes<16, false>,
-                         (const void*)k_lanes<8, true>,  (const void*)k_lanes<8, false>};
+                         (const void*)k_lanes<8, true>,  (const void*)k_lanes<8, false>,
+                         (const void*)k_lanes_t<1, true>, (const void*)k_lanes_t<1, false>,
+                         (const void*)k_lanes_t<2, true>, (const void*)k_lanes_t<2, false>,
+                         (const void*)k_lanes_t<4, true>, (const void*)k_lanes_t<4, false>};
     static size_t attr_set = 0;
     if (attr_set < smem) {
       for (const void* f : fns) CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       attr_set = smem;
     }
-    const int fi = (s->LT == 32 ? 0 : s->LT == 16 ? 2 : 4) + (hash ? 0 : 1);
+    const int fi = (s->variant == 1 ? 6 + (s->LT == 32 ? 0 : s->LT == 64 ? 2 : 4)
+                                    : (s->LT == 32 ? 0 : s->LT == 16 ? 2 : 4)) + (hash ? 0 : 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(s->n_tiles * s->cluster);
     cfg.blockDim = dim3(s->threads);
@@ -896,6 +915,8 @@ rs_status rs_debug_trace(rs_lanes* s, uint64_t* out, uint64_t n) {
   return set_err(RS_E_UNSUPPORTED, "built without RS_TRACE");
 #endif
 }
+
+uint32_t rs_lanes_kernel(const rs_lanes* s) { return s ? (s->g->cg.mode == RS_MODE_LANES ? s->variant : 0u) : 0u; }
 
 rs_status rs_launch_shape(const rs_lanes* s, uint32_t* lt, uint32_t* threads, uint32_t* ctas, uint32_t* cluster) {
   if (s && cluster) *cluster = s->cluster;

@@ -25,7 +25,7 @@ STATUS = {0: "RS_OK", -1: "RS_E_INVALID_ARG", -2: "RS_E_GRAPH", -3: "RS_E_CAPACI
 EXPORTS = ["rs_version", "rs_last_error", "rs_load_graph", "rs_graph_info_get", "rs_free_graph",
            "rs_alloc_lanes", "rs_free_lanes", "rs_lanes_bytes", "rs_set_input_seed", "rs_set_inputs",
            "rs_step_cycles", "rs_read_signals", "rs_write_registers", "rs_get_cycle", "rs_set_cycle",
-           "rs_launch_count", "rs_launch_shape", "rs_sync", "rs_graph_export", "rs_debug_trace",
+           "rs_launch_count", "rs_launch_shape", "rs_lanes_kernel", "rs_sync", "rs_graph_export", "rs_debug_trace",
            "rs_level_cut"]
 RS_DEVICE_NONE = -1
 EXPORT = {"runs": (0, np.uint32), "level_run_begin": (1, np.uint32), "level_op_begin": (2, np.uint32),
@@ -65,7 +65,7 @@ class GraphInfo(C.Structure):
 class LaneOpts(C.Structure):
     _fields_ = [("lane0", C.c_uint64), ("lane_tile", C.c_uint32), ("threads", C.c_uint32),
                 ("stage_cycles", C.c_uint32), ("cluster", C.c_uint32), ("stream", C.c_void_p),
-                ("parts", C.c_uint32), ("pad_", C.c_uint32)]
+                ("parts", C.c_uint32), ("kernel", C.c_uint32)]
 
 
 _lib = None
@@ -98,6 +98,7 @@ def lib() -> C.CDLL:
             "rs_get_cycle": (i32, [vp, C.POINTER(u64)]),
             "rs_set_cycle": (i32, [vp, u64]),
             "rs_launch_count": (u64, [vp]),
+            "rs_lanes_kernel": (u32, [vp]),
             "rs_launch_shape": (i32, [vp, C.POINTER(u32), C.POINTER(u32), C.POINTER(u32), C.POINTER(u32)]),
             "rs_sync": (i32, [vp]),
             "rs_graph_export": (i32, [vp, u32, vp, C.POINTER(u64)]),
@@ -203,12 +204,12 @@ class Lanes:
     lane0 .. lane0 + n_lanes - 1)."""
 
     def __init__(self, graph: Graph, n_lanes: int, lane0: int = 0, lane_tile: int = 0, threads: int = 0,
-                 stage_cycles: int = 0, stream=None, cluster: int = 0, parts: int = 0):
+                 stage_cycles: int = 0, stream=None, cluster: int = 0, parts: int = 0, kernel: int = 0):
         self.graph = graph
         self.n_lanes = n_lanes
         self.lane0 = lane0
         st = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
-        self.opts = LaneOpts(lane0, lane_tile, threads, stage_cycles, cluster, st, parts, 0)
+        self.opts = LaneOpts(lane0, lane_tile, threads, stage_cycles, cluster, st, parts, kernel)
         h = C.c_void_p()
         _check(lib().rs_alloc_lanes(graph.h, n_lanes, C.byref(self.opts), C.byref(h)))
         self.h = h
@@ -280,7 +281,8 @@ class Lanes:
     def shape(self):
         lt, th, ct, cs = C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_uint32()
         _check(lib().rs_launch_shape(self.h, C.byref(lt), C.byref(th), C.byref(ct), C.byref(cs)))
-        return {"lane_tile": lt.value, "threads": th.value, "ctas": ct.value, "cluster": cs.value}
+        return {"lane_tile": lt.value, "threads": th.value, "ctas": ct.value, "cluster": cs.value,
+                "kernel": int(lib().rs_lanes_kernel(self.h))}
 
     def nbytes(self) -> int:
         return int(lib().rs_lanes_bytes(self.h))

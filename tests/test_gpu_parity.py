@@ -17,10 +17,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def run_gpu(rs, c, n_cycles, n_lanes=1, seed=0, mode="lanes", lane0=0, lane_tile=0, threads=0,
-            staged=None, chunks=None, final=True, cluster=0, parts=0):
+            staged=None, chunks=None, final=True, cluster=0, parts=0, kernel=0):
     g = rs.Graph(c, device=0, mode=mode)
     L = rs.Lanes(g, n_lanes, lane0=lane0, lane_tile=lane_tile, threads=threads, cluster=cluster,
-                 stage_cycles=(n_cycles if staged is not None else 0), parts=parts)
+                 stage_cycles=(n_cycles if staged is not None else 0), parts=parts, kernel=kernel)
     if staged is not None:
         L.set_inputs(0, staged)
     else:
@@ -79,21 +79,27 @@ def test_c1_full(rs, mode):
     check(rs, config_circuit("C1"), cfg.cycles, 1, seed=cfg.stim_seed, mode=mode)
 
 
-@pytest.mark.parametrize("lt,cs", [(8, 1), (16, 1), (32, 1), (32, 4), (16, 2), (8, 8)])
-def test_c2_structure_ragged_lanes(rs, lt, cs):
+@pytest.mark.parametrize("kernel,lt,cs", [(2, 8, 1), (2, 16, 1), (2, 32, 1), (2, 32, 4), (2, 16, 2), (2, 8, 8),
+                                          (1, 32, 1), (1, 64, 1), (1, 128, 1), (1, 32, 4), (1, 64, 2),
+                                          (1, 128, 8)])
+def test_c2_structure_ragged_lanes(rs, lt, cs, kernel):
     """Full C2 circuit, 37 lanes (ragged last tile), 25 cycles, each lane tile,
-    one CTA or a thread-block cluster per tile."""
-    check(rs, config_circuit("C2"), 25, 37, seed=CONFIGS["C2"].stim_seed, lane_tile=lt, cluster=cs)
+    one CTA or a thread-block cluster per tile, both lane kernels."""
+    check(rs, config_circuit("C2"), 25, 37, seed=CONFIGS["C2"].stim_seed, lane_tile=lt, cluster=cs,
+          kernel=kernel)
 
 
 def test_c2_threads_variants(rs):
     c = config_circuit("C2", n_ops=5000, n_levels=40, n_regs=500)
     for th in (64, 256, 512):
-        check(rs, c, 12, 40, seed=7, threads=th, lane_tile=8)
+        check(rs, c, 12, 40, seed=7, threads=th, lane_tile=8, kernel=2)
+    for th in (32, 96, 768):
+        check(rs, c, 12, 70, seed=7, threads=th, lane_tile=64, kernel=1)
 
 
-def test_c3_structure(rs):
-    check(rs, config_circuit("C3"), 6, 40, seed=CONFIGS["C3"].stim_seed)
+@pytest.mark.parametrize("kernel", [1, 2])
+def test_c3_structure(rs, kernel):
+    check(rs, config_circuit("C3"), 6, 40, seed=CONFIGS["C3"].stim_seed, kernel=kernel)
 
 
 def test_c5_structure_single_lane(rs):
@@ -107,7 +113,7 @@ def test_fuzz_corpus(rs):
     wide folds, permuted ids; 60 cycles, both modes."""
     for seed in range(200):
         c = fuzz_circuit(seed)
-        check(rs, c, 60, 3, seed=seed)
+        check(rs, c, 60, 3, seed=seed, kernel=1 + seed % 2)
         if seed % 4 == 0:
             check(rs, c, 60, 1, seed=seed, mode="single")
 

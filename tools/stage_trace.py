@@ -21,10 +21,13 @@ from synth import CONFIGS, config_circuit  # noqa: E402
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "C2"
     cycles = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+    kernel = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+    lt = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+    cs = int(sys.argv[5]) if len(sys.argv) > 5 else 0
     cfg = CONFIGS[name]
     c = config_circuit(name)
     g = rs.Graph(c)
-    L = rs.Lanes(g, cfg.lanes)
+    L = rs.Lanes(g, cfg.lanes, kernel=kernel, lane_tile=lt, cluster=cs)
     L.set_seed(cfg.stim_seed)
     buf = np.zeros(4096 * 35, dtype=np.uint64)
     L.step(2)                                     # warm
