@@ -129,10 +129,13 @@ typedef struct {
                               values) into its replica.  On one device the partitions are CTA groups of
                               one cooperative launch.  RS_E_CAPACITY if the slices do not fit
                               co-resident, RS_E_INVALID_ARG if parts > n_levels or > 8. */
-  uint32_t kernel;         /* RS_MODE_LANES step kernel: 0 = auto (1), 1 = one lane per thread (a tile's LT
-                              lanes are one sub-warp, operand container widths dispatched by a uniform
-                              branch), 2 = two lanes per thread (aligned 64-bit word gathers + extraction);
-                              results are identical.  RS_E_INVALID_ARG otherwise. */
+  uint32_t kernel;         /* RS_MODE_LANES step kernel (results identical): 0 = auto (2 below 2048
+                              lanes, else 1); 1 = tile-interleaved: tile = 32 * P lanes (P = 1, 2, 4),
+                              thread t owns lanes t + 32k, one op per warp, operand container widths
+                              dispatched once per op through a jump table on the class signature;
+                              2 = two adjacent lanes per thread, 8/16/32-lane tiles, aligned 64-bit
+                              word gathers + extraction.  lane_tile must match (32/64/128 for 1,
+                              8/16/32 for 2).  RS_E_INVALID_ARG otherwise. */
 } rs_lane_opts;
 
 typedef struct rs_graph rs_graph;

@@ -399,7 +399,10 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
       delete s;
       return set_err(RS_E_INVALID_ARG, "parts (level cut) applies to RS_MODE_SINGLE only");
     }
-    const uint32_t kern = o.kernel == 2 ? 2u : 1u;
+    // auto: lane-poor allocations (< 2048 lanes: per-level work per SM is a few
+    // hundred lane-ops, latency-bound) take kernel 2's 8..32-lane tiles; lane-rich
+    // ones kernel 1's 32 * P-lane tiles (P = 4 amortizes the per-op decode).
+    const uint32_t kern = o.kernel ? o.kernel : (n_lanes < 2048u ? 2u : 1u);
     if (o.lane_tile && (kern == 2 ? (o.lane_tile != 8 && o.lane_tile != 16 && o.lane_tile != 32)
                                   : (o.lane_tile != 32 && o.lane_tile != 64 && o.lane_tile != 128))) {
       delete s;
