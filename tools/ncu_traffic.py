@@ -29,7 +29,9 @@ rd, wr = num("dram__bytes_read.sum"), num("dram__bytes_write.sum")
 out = {"report": os.path.basename(rep), "config": cfg, "lanes": lanes, "cycles": cycles, "kernel": kernel,
        "dram_bytes_read": rd, "dram_bytes_write": wr,
        "dram_bytes_per_lane_cycle": (rd + wr) / (lanes * cycles),
-       "gpu_time_ms": num("gpu__time_duration.sum") / 1e6 if d["gpu__time_duration.sum"][1] == "ns" else None,
+       "gpu_time_ms": float(d["gpu__time_duration.sum"][0].replace(",", "")) *
+                      {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "nsecond": 1e-6}.get(
+                          d["gpu__time_duration.sum"][1], float("nan")),
        "note": "ncu --set full (cache control all: caches flushed before the captured launch)"}
 path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", f"traffic_{cfg}.json")
 json.dump(out, open(path, "w"), indent=1)
