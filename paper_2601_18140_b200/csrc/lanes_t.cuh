@@ -363,10 +363,18 @@ __global__ void __launch_bounds__(RS_LANES_MAX_THREADS, 1) k_lanes_t(const StepA
   __syncthreads();
   const uint32_t S = a.n_stages;
   const uint32_t total = a.n_cycles * S;  // host keeps n_cycles * S < 2^31
-  if (tid == 0 && total) {
+  if (tid == T - 1 && total) {
     const StageRef r = a.stage_tab[0];
     tma_load_1d(smem + 128, a.stage_blob + r.off, r.bytes, &mbar[0]);
   }
+  // thread 0 keeps the reference of the next stage to prefetch in registers,
+  // loaded a stage ahead (a global load on the critical path of warp 0 otherwise)
+  // The stage prefetch (a ~500-cycle proxy fence + TMA issue) is done by the
+  // CTA's LAST thread: work items are dealt from warp 0 up, so the last warp
+  // is the least loaded and the issue latency stays off the critical path.
+  const uint32_t producer = T - 1;
+  StageRef nref{};
+  if (tid == producer && total > 1) nref = a.stage_tab[S > 1 ? 1 : 0];
   if (CS > 1) stage_barrier(CS);  // every CTA of the cluster has started (DSMEM use below)
 
   uint64_t hacc[P];
@@ -383,9 +391,10 @@ __global__ void __launch_bounds__(RS_LANES_MAX_THREADS, 1) k_lanes_t(const StepA
     if (tr && tid == 0) tr[0] = clock64();
 #endif
     const uint32_t bsel = gi & 1u;
-    if (tid == 0 && gi + 1 < total) {
-      const StageRef r = a.stage_tab[s + 1 == S ? 0 : s + 1];
-      tma_load_1d(smem + 128 + (bsel ^ 1u) * a.stage_bytes, a.stage_blob + r.off, r.bytes, &mbar[bsel ^ 1u]);
+    if (tid == producer && gi + 1 < total) {
+      tma_load_1d(smem + 128 + (bsel ^ 1u) * a.stage_bytes, a.stage_blob + nref.off, nref.bytes, &mbar[bsel ^ 1u]);
+      const uint32_t s2 = (s + 2) % S;  // the stage after the one just requested
+      nref = a.stage_tab[s2];
     }
     mbar_wait(&mbar[bsel], (gi >> 1) & 1u);
 #ifdef RS_TRACE

@@ -904,7 +904,7 @@ uint64_t rs_launch_count(const rs_lanes* s) { return s ? s->launches : 0; }
 rs_status rs_debug_trace(rs_lanes* s, uint64_t* out, uint64_t n) {
 #ifdef RS_TRACE
   if (!s || !out) return set_err(RS_E_INVALID_ARG, "NULL argument");
-  const uint64_t cap = 4096ull * (3 + 1024 / 32);
+  const uint64_t cap = 4096ull * (3 + 1024 / 32) + 4096ull * 16;  // stage stamps + extra stamps
   if (!s->trace) {
     CU(cudaMalloc(&s->trace, cap * 8));
     CU(cudaMemset(s->trace, 0, cap * 8));

@@ -29,7 +29,7 @@ def main():
     g = rs.Graph(c)
     L = rs.Lanes(g, cfg.lanes, kernel=kernel, lane_tile=lt, cluster=cs)
     L.set_seed(cfg.stim_seed)
-    buf = np.zeros(4096 * 35, dtype=np.uint64)
+    buf = np.zeros(4096 * 35 + 4096 * 16, dtype=np.uint64)
     L.step(2)                                     # warm
     rs._check(rs.lib().rs_debug_trace(L.h, buf.ctypes.data, buf.size))   # arm
     L.step(cycles)
@@ -57,6 +57,10 @@ def main():
           f"work max {np.mean(work_max):.0f} min {np.mean(work_min):.0f}  barrier-after-max {np.mean(bar):.0f}")
     per_warp = (rows[:, 3:] - rows[:, 1:2]).mean(axis=0)
     print("mean work end per warp:", " ".join(f"{v:.0f}" for v in per_warp))
+    ex = buf[4096 * 35:].reshape(4096, 16)[:len(rows)].astype(np.int64)
+    if (ex[:, 0] != 0).all():
+        print(f"extra stamp 0: {(ex[:, 0] - rows[:, 0]).mean():.0f} cycles after the loop top, "
+              f"{(rows[:, 1] - ex[:, 0]).mean():.0f} before the end of the stage-buffer wait")
     for i in range(min(S, 60)):
         idx = np.arange(i, len(rows) - 1, S)
         print(f"  stage {i:3d}: total {np.mean(tot[idx]) if len(idx) else 0:8.0f} wait {np.mean(wait[idx]):7.0f} "
