@@ -113,10 +113,16 @@ def cpu_sample_plan(circ, target_s, cores):
     (calibrated with a short run)."""
     import oracle
     lanes = max(1, cores)
-    t = time.perf_counter()
-    oracle.simulate(circ, 2, seed=1, n_lanes=lanes, threads=cores)
-    per_cycle = max((time.perf_counter() - t) / 2, 1e-6)
-    cycles = int(max(2, min(100000, target_s / per_cycle)))
+    n = 2
+    while True:  # calibrate on at least ~0.2 s of work (tiny circuits run thousands of cycles per ms)
+        t = time.perf_counter()
+        oracle.simulate(circ, n, seed=1, n_lanes=lanes, threads=cores)
+        dt = time.perf_counter() - t
+        if dt > 0.2 or n >= 1 << 20:
+            break
+        n *= 8
+    per_cycle = max(dt / n, 1e-9)
+    cycles = int(max(2, min(10_000_000, target_s / per_cycle)))
     return lanes, cycles
 
 
@@ -291,7 +297,7 @@ def main():
         nl, nc = cpu_sample_plan(circ, 10.0, cores)
         rate, dt = oracle_rate(circ, cfg.stim_seed, nl, nc, threads=cores)
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"{nl} lanes x {nc} cycles of {args.config} ({dt:.1f} s)"}
+               "sample": f"{nl} lanes x {nc} cycles of {args.config} ({dt:.2f} s)"}
 
     if rank == 0:
         line = {

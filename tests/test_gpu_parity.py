@@ -278,3 +278,18 @@ def test_c4_c5_full_size_sampled(rs):
     H, F, _ = run_gpu(rs, c, 10, 1, seed=CONFIGS["C5"].stim_seed, mode="single", final=True)
     r = oracle.simulate(c, 10, seed=CONFIGS["C5"].stim_seed, final=True)
     assert np.array_equal(H, r.hashes) and np.array_equal(F, r.final_state)
+
+
+def test_auto_kernel_choice(rs):
+    """rs_lane_opts.kernel = 0: kernel 2 below 2048 lanes, kernel 1 (32 * P-lane tiles) above."""
+    c = config_circuit("C2", n_ops=2000, n_levels=10, n_regs=100)
+    g = rs.Graph(c)
+    a = rs.Lanes(g, 1024)
+    b = rs.Lanes(g, 4096)
+    assert a.shape()["kernel"] == 2 and a.shape()["lane_tile"] in (8, 16, 32)
+    assert b.shape()["kernel"] == 1 and b.shape()["lane_tile"] in (32, 64, 128)
+    for L in (a, b):
+        L.set_seed(3)
+        h = L.step(3, hashes="host")
+        r = oracle.simulate(c, 3, seed=3, lanes=[0, L.n_lanes - 1], threads=2)
+        assert np.array_equal(h[:, [0, L.n_lanes - 1]], r.hashes)

@@ -18,7 +18,7 @@ def main():
     g = rs.Graph(c, mode="single")
     L = rs.Lanes(g, 1)
     L.set_seed(CONFIGS[name].stim_seed)
-    buf = np.zeros(4096 * 35, dtype=np.uint64)
+    buf = np.zeros(4096 * 35 + 4096 * 16, dtype=np.uint64)
     L.step(2, hashes="host")
     rs._check(rs.lib().rs_debug_trace(L.h, buf.ctypes.data, buf.size))  # arm
     L.step(6, hashes="host")
