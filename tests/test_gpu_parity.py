@@ -139,10 +139,11 @@ def test_closed_forms_on_gpu(rs):
     check(rs, c, 40, 1, staged=vals)
 
 
-def test_chunking_and_hash_toggle(rs):
+@pytest.mark.parametrize("kernel", [1, 2])
+def test_chunking_and_hash_toggle(rs, kernel):
     c = config_circuit("C2", n_ops=4000, n_levels=20, n_regs=400)
     g = rs.Graph(c)
-    L = rs.Lanes(g, 50)
+    L = rs.Lanes(g, 50, kernel=kernel)
     L.set_seed(11)
     h1 = L.step(7, hashes="host")
     L.step(5)                                             # hash off: carry must be refreshed
@@ -156,13 +157,14 @@ def test_chunking_and_hash_toggle(rs):
     assert L.cycle == 21
 
 
-def test_staged_inputs_chunks(rs):
+@pytest.mark.parametrize("kernel", [1, 2])
+def test_staged_inputs_chunks(rs, kernel):
     c = config_circuit("C2", n_ops=3000, n_levels=15, n_regs=300)
     rng = np.random.default_rng(3)
-    n, nl = 30, 33
+    n, nl = 30, 33 if kernel == 2 else 130
     vals = rng.integers(0, 2**63, size=(n, c.n_inputs, nl), dtype=np.int64).astype(np.uint64) * np.uint64(3)
     g = rs.Graph(c)
-    L = rs.Lanes(g, nl, stage_cycles=8)
+    L = rs.Lanes(g, nl, stage_cycles=8, kernel=kernel)
     hs = []
     for c0 in range(0, n, 6):
         L.set_inputs(c0, vals[c0:c0 + 6])
@@ -174,15 +176,16 @@ def test_staged_inputs_chunks(rs):
     assert e.value.name == "RS_E_STATE"
 
 
-def test_checkpoint_restore(rs):
+@pytest.mark.parametrize("kernel", [1, 2])
+def test_checkpoint_restore(rs, kernel):
     c = config_circuit("C2", n_ops=3000, n_levels=15, n_regs=300)
     full = oracle.simulate(c, 20, seed=5, n_lanes=24)
     g = rs.Graph(c)
-    a = rs.Lanes(g, 24)
+    a = rs.Lanes(g, 24, kernel=kernel)
     a.set_seed(5)
     h0 = a.step(10, hashes="host")
     regs = a.read(c.reg_id)
-    b = rs.Lanes(g, 24)
+    b = rs.Lanes(g, 24, kernel=3 - kernel)   # restored into the other lane kernel's layout
     b.set_seed(5)
     b.write_registers(c.reg_id, regs)
     b.cycle = 10
@@ -202,6 +205,9 @@ def test_lane_sharding_invariance(rs):
     Hb, Fb, _ = run_gpu(rs, c, 15, 37, seed=9, lane0=37)
     assert np.array_equal(Hf, np.concatenate([Ha, Hb], axis=1))
     assert np.array_equal(Ff, np.concatenate([Fa, Fb], axis=1))
+    # the same partition across the two lane kernels (shards may run different layouts)
+    Hc, Fc, _ = run_gpu(rs, c, 15, 37, seed=9, lane0=37, kernel=1)
+    assert np.array_equal(Hb, Hc) and np.array_equal(Fb, Fc)
 
 
 def test_error_statuses(rs):
