@@ -173,6 +173,7 @@ def main():
     ap.add_argument("--kernel", type=int, default=0, help="lane kernel: 0 auto, 1 lane/thread, 2 two lanes/thread")
     ap.add_argument("--parts", type=int, default=0, help="C1/C5: level-cut partitions emulated on this GPU")
     ap.add_argument("--ref-step-s", type=float, default=4.0)
+    ap.add_argument("--watch", type=int, default=0, help="waveform capture of N signals during the timed steps")
     args = ap.parse_args()
 
     from synth import CONFIGS, config_circuit
@@ -206,6 +207,9 @@ def main():
     L = rs.Lanes(g, lanes, lane0=shard.lane0, lane_tile=args.lane_tile, threads=args.threads, stream=stream,
                  cluster=args.cluster, parts=args.parts, kernel=args.kernel)
     L.set_seed(cfg.stim_seed)
+    if args.watch:
+        wids = np.linspace(0, circ.n_signals - 1, args.watch).astype(np.uint32)
+        L.watch(wids, capacity=1 << 26)
     hashes = None if args.no_hash else torch.empty(cycles * lanes, dtype=torch.int64, device="cuda")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
 
@@ -309,7 +313,8 @@ def main():
                        "l2": "flushed (256 MB write) before every timed step",
                        "mode": "single" if single else "lanes", "launch": L.shape(),
                        **({"level_cut_parts": args.parts} if args.parts > 1 else {}),
-                       "state_bytes_per_gpu": info["state_bytes_per_lane"] * lanes},
+                       "state_bytes_per_gpu": info["state_bytes_per_lane"] * lanes,
+                       **({"watched_signals": args.watch} if args.watch else {})},
             "op_evals_per_s": value * circ.n_ops,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,

@@ -225,6 +225,32 @@ rs_status rs_launch_shape(const rs_lanes* s, uint32_t* lane_tile, uint32_t* thre
 /* Lane-mode step kernel in use (rs_lane_opts.kernel: 1 or 2); 0 for single-lane mode or NULL. */
 uint32_t rs_lanes_kernel(const rs_lanes* s);
 rs_status rs_sync(rs_lanes* s);
+/* ---- Waveform capture (§6.2: the
+ * DMI dumps waveforms of selected signals).  rs_watch selects up to 2^16
+ * canonical signal ids of a RS_MODE_LANES allocation; every later
+ * rs_step_cycles then records, fused into the step kernel (one extra stage per
+ * cycle, after the last level and before the register commit), a CHANGE
+ * record for each (watched signal, lane) whose value after the combinational
+ * evaluation of cycle c -- the snapshot the per-cycle hash covers -- differs
+ * from its value at cycle c - 1, and for every (signal, lane) at the first
+ * stepped cycle after rs_watch.  Records are appended to a device buffer of
+ * `capacity` records in no particular order; records beyond capacity are
+ * counted as dropped.  n_ids = 0 stops watching (and frees the buffers).
+ * RS_E_RANGE for an unknown id, RS_E_UNSUPPORTED in RS_MODE_SINGLE. */
+typedef struct {
+  uint64_t cycle;   /* absolute cycle */
+  uint64_t lane;    /* global lane id (rs_lane_opts.lane0 + allocation lane) */
+  uint32_t watch;   /* index into the rs_watch id list */
+  uint32_t pad_;
+  uint64_t value;   /* the signal's value at that cycle (masked to its width) */
+} rs_change;
+rs_status rs_watch(rs_lanes* s, const uint32_t* ids, uint32_t n_ids, uint64_t capacity);
+/* Copy the records collected so far to host memory `out` (up to cap; caller-
+ * owned) and clear the buffer; *n_out = records copied, *dropped = records
+ * lost to capacity since the last read (either pointer may be NULL).
+ * Synchronises the lanes' stream. */
+rs_status rs_wave_read(rs_lanes* s, rs_change* out, uint64_t cap, uint64_t* n_out, uint64_t* dropped);
+
 /* Diagnostics (builds with -DRS_TRACE only, else RS_E_UNSUPPORTED): the first
  * call arms a per-stage clock64 trace of CTA 0; later calls copy up to n u64
  * stamps to host `out` (layout: per stage [top, after stage wait, after

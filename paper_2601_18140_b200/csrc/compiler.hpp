@@ -111,7 +111,7 @@ rs_status compile_graph(const rs_graph_desc* d, uint32_t mode, CompiledGraph* ou
 // with a CTA barrier after every stage.  A level larger than one stage is
 // split into several OPS stages (barrier after each; only the last one ends
 // the level, but an extra barrier is harmless).
-enum StageType : uint32_t { ST_INJECT = 1, ST_OPS = 2, ST_LATCH = 3, ST_NOP = 4 };
+enum StageType : uint32_t { ST_INJECT = 1, ST_OPS = 2, ST_LATCH = 3, ST_NOP = 4, ST_WATCH = 6 };
 
 struct StageHdr {          // first 64 bytes of a stage block
   uint32_t type;

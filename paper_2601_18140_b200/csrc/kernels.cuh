@@ -77,6 +77,12 @@ struct StepArgs {
   uint32_t stage_bytes;        // shared-memory bytes per stage buffer
   uint32_t cluster;            // lane mode: CTAs (one cluster) sharing one lane tile
   unsigned long long* trace;   // RS_TRACE builds: per-stage clock64 stamps of CTA 0 (tools/, not the product)
+  // waveform capture (rs_watch): previous values [n_watch][lanes_pad], change records, record counter
+  uint64_t* wave_prev;
+  uint64_t* wave_rec;          // [capacity][4] u64: cycle, lane, watch, value
+  unsigned long long* wave_count;
+  uint64_t wave_cap;
+  uint64_t wave_first;         // records are unconditional at this absolute cycle
 };
 
 // ------------------------------------------------------------------ helpers
@@ -211,6 +217,53 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(dst)),
       "l"(src), "r"(bytes), "r"(smem_addr(bar))
       : "memory");
+}
+
+// WATCH stage (waveform capture, rs_watch): for watches [b, e) of the stage and
+// the thread's lanes (tile-relative ids lanes[0..n)), compare each value with
+// the previous cycle's and append a change record; the records of a warp are
+// reserved with one atomic.  coords: the watched signals' bound coordinates.
+template <int N>
+__device__ __forceinline__ void stage_watch(const StepArgs& a, const uint8_t* tb, const uint32_t* coords, uint32_t b,
+                                            uint32_t e, const uint32_t (&lanes)[N], uint32_t tile, uint64_t cycle) {
+  const size_t lanes_pad = (size_t)gridDim.x / a.cluster * a.LT;
+#pragma unroll 1
+  for (uint32_t j = b; j < e; ++j) {
+    const uint32_t c = coords[j], cls = c >> 30;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const uint32_t l = tile * a.LT + lanes[k];  // allocation lane
+      const uint8_t* p = tb + (c & ROW_MASK) + ((size_t)lanes[k] << cls);
+      uint64_t v;
+      switch (cls) {
+        case 0: v = *p; break;
+        case 1: v = *reinterpret_cast<const uint16_t*>(p); break;
+        case 2: v = *reinterpret_cast<const uint32_t*>(p); break;
+        default: v = *reinterpret_cast<const uint64_t*>(p); break;
+      }
+      uint64_t* prev = a.wave_prev + (size_t)j * lanes_pad + l;
+      const bool rec = l < a.n_lanes && (cycle == a.wave_first || *prev != v);
+      *prev = v;
+      // one atomic per warp and step: the leader reserves the warp's records
+      const uint32_t am = __activemask();
+      const uint32_t m = __ballot_sync(am, rec);
+      if (m == 0u) continue;
+      const uint32_t me = threadIdx.x & 31u, leader = __ffs(m) - 1;
+      unsigned long long base = 0;
+      if (me == leader) base = atomicAdd(a.wave_count, (unsigned long long)__popc(m));
+      base = __shfl_sync(am, base, leader);
+      if (rec) {
+        const unsigned long long i = base + __popc(m & ((1u << me) - 1u));
+        if (i < a.wave_cap) {
+          uint64_t* r = a.wave_rec + 4 * i;
+          r[0] = cycle;
+          r[1] = a.lane0 + l;
+          r[2] = j;
+          r[3] = v;
+        }
+      }
+    }
+  }
 }
 
 // ------------------------------------------------------------------ single-lane mode

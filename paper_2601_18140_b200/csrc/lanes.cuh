@@ -537,6 +537,15 @@ __global__ void __launch_bounds__(RS_LANES_MAX_THREADS, 1) k_lanes(const StepArg
         stage_inject<LT, P, HASH>(L, base + h->off_c, base + h->off_w, base + h->off_k, h->first, b, e, a, lane,
                                   a.cycle0 + cyc, hacc);
       }
+    } else if (type == ST_WATCH) {
+      uint32_t b, e;
+      chunk_of(h->n, gsub, ngsub, b, e);
+      uint32_t ln[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) ln[p] = lin * P + p;
+      if (b < e)
+        stage_watch<P>(a, a.state + (size_t)tile * a.tile_bytes, reinterpret_cast<const uint32_t*>(buf + h->off_c), b,
+                       e, ln, tile, a.cycle0 + cyc);
     }
     const bool eoc = (s + 1 == S);
     if constexpr (HASH) {

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -106,6 +107,14 @@ struct rs_lanes {
   bool tail_global = false;
   std::vector<uint8_t> sig_part;         // canonical id -> partition whose replica holds it
   size_t total_bytes = 0;
+  size_t sched_bytes = 0;                // device bytes of the bound stage schedule
+  // waveform capture (rs_watch)
+  std::vector<uint32_t> watch;           // canonical ids
+  uint64_t* wave_prev = nullptr;         // [n_watch][lanes_pad]
+  uint64_t* wave_rec = nullptr;          // [wave_cap][4]
+  unsigned long long* wave_count = nullptr;
+  uint64_t wave_cap = 0;
+  uint64_t wave_first = 0;
 };
 
 namespace {
@@ -136,6 +145,11 @@ StepArgs base_args(const rs_lanes* s) {
   a.stage_bytes = s->g->stage_bytes;
   a.trace = s->trace;
   a.cluster = s->cluster;
+  a.wave_prev = s->wave_prev;
+  a.wave_rec = s->wave_rec;
+  a.wave_count = s->wave_count;
+  a.wave_cap = s->wave_cap;
+  a.wave_first = s->wave_first;
   return a;
 }
 
@@ -161,6 +175,52 @@ void bind_stages(const rs_graph* g, uint32_t LT, const uint64_t* region, std::ve
       runs[i].out_row0 = bind((cls << 30) | runs[i].out_row0) & ROW_MASK;
     }
   }
+}
+
+// Bind the graph's schedule to the allocation and upload it; with watched
+// signals (rs_watch) a WATCH stage is spliced in before the register commit.
+rs_status upload_schedule(rs_lanes* s) {
+  const rs_graph* g = s->g;
+  std::vector<uint8_t> bound;
+  bind_stages(g, s->LT, s->region, &bound);
+  std::vector<StageRef> tab = g->stage_tab;
+  if (!s->watch.empty()) {
+    StageHdr h{};
+    h.type = ST_WATCH;
+    h.n = h.n_coords = (uint32_t)s->watch.size();
+    h.off_c = (uint32_t)((sizeof(StageHdr) + 15) & ~(size_t)15);
+    h.bytes = (uint32_t)((h.off_c + 4ull * h.n + 15) & ~15ull);
+    const size_t base = (bound.size() + 15) & ~(size_t)15;
+    bound.resize(base + h.bytes, 0);
+    std::memcpy(bound.data() + base, &h, sizeof h);
+    uint32_t* c = reinterpret_cast<uint32_t*>(bound.data() + base + h.off_c);
+    for (uint32_t i = 0; i < h.n; ++i) {
+      const uint32_t co = g->cg.sig_coord[s->watch[i]], cls = co >> 30;
+      c[i] = (cls << 30) | (uint32_t)(s->region[cls] + ((uint64_t)(co & ROW_MASK) * s->LT << cls));
+    }
+    size_t at = 0;
+    while (at < tab.size() && tab[at].type != ST_LATCH) ++at;
+    tab.insert(tab.begin() + at, StageRef{base, h.bytes, ST_WATCH});
+  }
+  const size_t tab_off = (bound.size() + 255) & ~(size_t)255;
+  const size_t nbytes = tab_off + tab.size() * sizeof(StageRef);
+  if (s->dstages) {
+    CU(cudaStreamSynchronize(s->stream));
+    cudaFree(s->dstages);
+    s->dstages = nullptr;
+    s->total_bytes -= s->sched_bytes;
+  }
+  cudaError_t e = cudaMalloc(&s->dstages, nbytes);
+  if (e == cudaSuccess) e = cudaMemcpy(s->dstages, bound.data(), bound.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = cudaMemcpy((uint8_t*)s->dstages + tab_off, tab.data(), tab.size() * sizeof(StageRef), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return set_err(RS_E_OOM, "stage schedule (%zu B): %s", nbytes, cudaGetErrorString(e));
+  s->stage_blob = (const uint8_t*)s->dstages;
+  s->stage_tab = (const StageRef*)((const uint8_t*)s->dstages + tab_off);
+  s->n_stages = (uint32_t)tab.size();
+  s->sched_bytes = nbytes;
+  s->total_bytes += nbytes;
+  return RS_OK;
 }
 
 rs_status set_device(const rs_graph* g) {
@@ -527,23 +587,10 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     return set_err(RS_E_OOM, "cudaMalloc state (%zu B): %s", s->state_bytes, cudaGetErrorString(e));
   }
   if (g->cg.mode == RS_MODE_LANES) {
-    std::vector<uint8_t> bound;
-    bind_stages(g, s->LT, s->region, &bound);
-    const size_t tab_off = (bound.size() + 255) & ~(size_t)255;
-    const size_t nbytes = tab_off + g->stage_tab.size() * sizeof(StageRef);
-    e = cudaMalloc(&s->dstages, nbytes);
-    if (e == cudaSuccess) e = cudaMemcpy(s->dstages, bound.data(), bound.size(), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess)
-      e = cudaMemcpy((uint8_t*)s->dstages + tab_off, g->stage_tab.data(), g->stage_tab.size() * sizeof(StageRef),
-                     cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) {
+    if ((st = upload_schedule(s)) != RS_OK) {
       rs_free_lanes(s);
-      return set_err(RS_E_OOM, "stage schedule (%zu B): %s", nbytes, cudaGetErrorString(e));
+      return st;
     }
-    s->stage_blob = (const uint8_t*)s->dstages;
-    s->stage_tab = (const StageRef*)((const uint8_t*)s->dstages + tab_off);
-    s->n_stages = (uint32_t)g->stage_tab.size();
-    s->total_bytes += nbytes;
   }
   const size_t lanes_pad = (size_t)s->n_tiles * s->LT;
   if ((e = cudaMalloc(&s->hcarry, 2 * lanes_pad * sizeof(uint64_t))) != cudaSuccess ||
@@ -618,6 +665,9 @@ void rs_free_lanes(rs_lanes* s) {
   if (s->bar) cudaFree(s->bar);
   if (s->stage) cudaFree(s->stage);
   if (s->hbuf) cudaFree(s->hbuf);
+  if (s->wave_prev) cudaFree(s->wave_prev);
+  if (s->wave_rec) cudaFree(s->wave_rec);
+  if (s->wave_count) cudaFree(s->wave_count);
   if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
   if (s->g) s->g->live_lanes--;
   delete s;
@@ -917,6 +967,54 @@ rs_status rs_debug_trace(rs_lanes* s, uint64_t* out, uint64_t n) {
   (void)s; (void)out; (void)n;
   return set_err(RS_E_UNSUPPORTED, "built without RS_TRACE");
 #endif
+}
+
+rs_status rs_watch(rs_lanes* s, const uint32_t* ids, uint32_t n_ids, uint64_t capacity) {
+  if (!s || (n_ids && !ids)) return set_err(RS_E_INVALID_ARG, "NULL argument");
+  if (s->g->cg.mode != RS_MODE_LANES) return set_err(RS_E_UNSUPPORTED, "waveform capture needs RS_MODE_LANES");
+  if (n_ids > 8192u) return set_err(RS_E_INVALID_ARG, "at most 8192 watched signals (got %u)", n_ids);
+  if (n_ids && capacity == 0) return set_err(RS_E_INVALID_ARG, "capacity must be >= 1");
+  for (uint32_t i = 0; i < n_ids; ++i)
+    if (ids[i] >= s->g->cg.n_signals) return set_err(RS_E_RANGE, "signal id %u out of range", ids[i]);
+  rs_status st = set_device(s->g);
+  if (st != RS_OK) return st;
+  CU(cudaStreamSynchronize(s->stream));
+  if (s->wave_prev) cudaFree(s->wave_prev);
+  if (s->wave_rec) cudaFree(s->wave_rec);
+  if (s->wave_count) cudaFree(s->wave_count);
+  s->wave_prev = nullptr;
+  s->wave_rec = nullptr;
+  s->wave_count = nullptr;
+  s->wave_cap = 0;
+  s->watch.assign(ids, ids + n_ids);
+  if (n_ids) {
+    const size_t lanes_pad = (size_t)s->n_tiles * s->LT;
+    CU(cudaMalloc(&s->wave_prev, (size_t)n_ids * lanes_pad * 8));
+    CU(cudaMalloc(&s->wave_rec, capacity * 32));
+    CU(cudaMalloc(&s->wave_count, 8));
+    CU(cudaMemset(s->wave_count, 0, 8));
+    s->wave_cap = capacity;
+    s->wave_first = s->cycle;
+  }
+  return upload_schedule(s);
+}
+
+rs_status rs_wave_read(rs_lanes* s, rs_change* out, uint64_t cap, uint64_t* n_out, uint64_t* dropped) {
+  if (!s || (cap && !out)) return set_err(RS_E_INVALID_ARG, "NULL argument");
+  if (n_out) *n_out = 0;
+  if (dropped) *dropped = 0;
+  if (!s->wave_count) return RS_OK;
+  rs_status st = set_device(s->g);
+  if (st != RS_OK) return st;
+  unsigned long long cnt = 0;
+  CU(cudaMemcpyAsync(&cnt, s->wave_count, 8, cudaMemcpyDeviceToHost, s->stream));
+  CU(cudaStreamSynchronize(s->stream));
+  const uint64_t have = std::min<uint64_t>(cnt, s->wave_cap), n = std::min<uint64_t>(have, cap);
+  if (n) CU(cudaMemcpy(out, s->wave_rec, n * 32, cudaMemcpyDeviceToHost));
+  CU(cudaMemset(s->wave_count, 0, 8));
+  if (n_out) *n_out = n;
+  if (dropped) *dropped = cnt - n;
+  return RS_OK;
 }
 
 uint32_t rs_lanes_kernel(const rs_lanes* s) { return s ? (s->g->cg.mode == RS_MODE_LANES ? s->variant : 0u) : 0u; }

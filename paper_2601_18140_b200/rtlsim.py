@@ -25,7 +25,7 @@ STATUS = {0: "RS_OK", -1: "RS_E_INVALID_ARG", -2: "RS_E_GRAPH", -3: "RS_E_CAPACI
 EXPORTS = ["rs_version", "rs_last_error", "rs_load_graph", "rs_graph_info_get", "rs_free_graph",
            "rs_alloc_lanes", "rs_free_lanes", "rs_lanes_bytes", "rs_set_input_seed", "rs_set_inputs",
            "rs_step_cycles", "rs_read_signals", "rs_write_registers", "rs_get_cycle", "rs_set_cycle",
-           "rs_launch_count", "rs_launch_shape", "rs_lanes_kernel", "rs_sync", "rs_graph_export", "rs_debug_trace",
+           "rs_launch_count", "rs_launch_shape", "rs_lanes_kernel", "rs_watch", "rs_wave_read", "rs_sync", "rs_graph_export", "rs_debug_trace",
            "rs_level_cut"]
 RS_DEVICE_NONE = -1
 EXPORT = {"runs": (0, np.uint32), "level_run_begin": (1, np.uint32), "level_op_begin": (2, np.uint32),
@@ -99,6 +99,8 @@ def lib() -> C.CDLL:
             "rs_set_cycle": (i32, [vp, u64]),
             "rs_launch_count": (u64, [vp]),
             "rs_lanes_kernel": (u32, [vp]),
+            "rs_watch": (i32, [vp, vp, u32, u64]),
+            "rs_wave_read": (i32, [vp, vp, u64, C.POINTER(u64), C.POINTER(u64)]),
             "rs_launch_shape": (i32, [vp, C.POINTER(u32), C.POINTER(u32), C.POINTER(u32), C.POINTER(u32)]),
             "rs_sync": (i32, [vp]),
             "rs_graph_export": (i32, [vp, u32, vp, C.POINTER(u64)]),
@@ -283,6 +285,23 @@ class Lanes:
         _check(lib().rs_launch_shape(self.h, C.byref(lt), C.byref(th), C.byref(ct), C.byref(cs)))
         return {"lane_tile": lt.value, "threads": th.value, "ctas": ct.value, "cluster": cs.value,
                 "kernel": int(lib().rs_lanes_kernel(self.h))}
+
+    # ---- waveform capture (rs_watch / rs_wave_read)
+    CHANGE = np.dtype([("cycle", np.uint64), ("lane", np.uint64), ("watch", np.uint32), ("pad_", np.uint32),
+                       ("value", np.uint64)])
+
+    def watch(self, ids: Sequence[int], capacity: int = 1 << 20) -> None:
+        """Record value changes of the canonical signals ``ids`` from the next stepped cycle on."""
+        ids_a = _arr(ids, np.uint32)
+        _check(lib().rs_watch(self.h, _ptr(ids_a) if ids_a.size else None, ids_a.shape[0], capacity))
+        self.watched = ids_a
+
+    def wave_read(self, cap: int = 1 << 20):
+        """Drain the change records: (structured array cycle/lane/watch/value, dropped count)."""
+        out = np.zeros(max(cap, 1), dtype=self.CHANGE)
+        n, d = C.c_uint64(), C.c_uint64()
+        _check(lib().rs_wave_read(self.h, _ptr(out), cap, C.byref(n), C.byref(d)))
+        return out[:n.value], d.value
 
     def nbytes(self) -> int:
         return int(lib().rs_lanes_bytes(self.h))

@@ -243,3 +243,21 @@ def test_level_cut_ranges(rs, name):
         g.level_cut(0)
     with pytest.raises(rs.RtlSimError):
         g.level_cut(9)
+
+
+def test_vcd_writer_format():
+    """VCD text of hand-made change records (wave.py; no GPU)."""
+    from paper_2601_18140_b200 import rtlsim as rs
+    from paper_2601_18140_b200.wave import changes_from_trace, vcd_string
+    rec = np.zeros(5, dtype=rs.Lanes.CHANGE)
+    rec["cycle"] = [0, 0, 3, 3, 1]
+    rec["lane"] = [7, 7, 7, 8, 7]
+    rec["watch"] = [0, 1, 1, 1, 0]
+    rec["value"] = [1, 5, 6, 9, 0]
+    txt = vcd_string(rec, [1, 4], lane=7, names=["clk_en", "cnt"])
+    assert "$var wire 1 ! clk_en $end" in txt and '$var wire 4 " cnt $end' in txt
+    body = txt.split("$enddefinitions $end\n")[1]
+    assert body == '#0\n1!\nb101 "\n#1\n0!\n#3\nb110 "\n'
+    # change-set semantics: first cycle always, then only differences
+    tr = np.array([[[1, 2]], [[1, 3]], [[4, 3]]], dtype=np.uint64)   # [cycle][watch][lane]
+    assert changes_from_trace(tr, 10, [0, 1]) == {(10, 0, 0, 1), (10, 1, 0, 2), (11, 1, 0, 3), (12, 0, 0, 4)}

@@ -299,3 +299,42 @@ def test_auto_kernel_choice(rs):
         h = L.step(3, hashes="host")
         r = oracle.simulate(c, 3, seed=3, lanes=[0, L.n_lanes - 1], threads=2)
         assert np.array_equal(h[:, [0, L.n_lanes - 1]], r.hashes)
+
+
+@pytest.mark.parametrize("kernel", [1, 2])
+def test_waveform_changes(rs, kernel):
+    """Waveform capture (rs_watch): the fused per-cycle change
+    records equal the change set of the oracle's per-cycle trace of the same
+    signals (ops, inputs, registers of every width class), across step chunks
+    and a re-armed watch."""
+    from paper_2601_18140_b200.wave import changes_from_trace
+    c = config_circuit("C2", n_ops=3000, n_levels=15, n_regs=300)
+    rng = np.random.default_rng(kernel)
+    ids = sorted(set(rng.choice(c.n_signals, 40, replace=False).tolist()) | {int(c.input_id[0]), int(c.reg_id[0])})
+    nl = 45 if kernel == 2 else 140
+    g = rs.Graph(c)
+    L = rs.Lanes(g, nl, lane0=1000, kernel=kernel)
+    L.set_seed(4)
+    L.step(3)                                  # not watched
+    L.watch(ids, capacity=1 << 20)
+    L.step(5)
+    L.step(7, hashes="host")
+    rec, dropped = L.wave_read()
+    assert dropped == 0
+    got = {(int(r["cycle"]), int(r["lane"]), int(r["watch"]), int(r["value"])) for r in rec}
+    assert len(got) == len(rec)
+    lanes = list(range(1000, 1000 + nl))
+    tr = oracle.simulate(c, 15, seed=4, lane0=1000, n_lanes=nl, watch=ids, hashes=False).trace
+    assert got == changes_from_trace(tr[3:], 3, lanes)
+    # re-arm on a subset: records restart from the current cycle
+    L.watch(ids[:5], capacity=64)
+    L.step(4)
+    rec, dropped = L.wave_read()
+    exp = changes_from_trace(
+        oracle.simulate(c, 19, seed=4, lane0=1000, n_lanes=nl, watch=ids[:5], hashes=False).trace[15:], 15, lanes)
+    assert len(rec) == 64 and dropped == len(exp) - 64
+    got = {(int(r["cycle"]), int(r["lane"]), int(r["watch"]), int(r["value"])) for r in rec}
+    assert got <= exp
+    L.watch([])
+    L.step(2)
+    assert L.wave_read()[0].shape[0] == 0
