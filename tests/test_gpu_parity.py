@@ -338,3 +338,21 @@ def test_waveform_changes(rs, kernel):
     L.watch([])
     L.step(2)
     assert L.wave_read()[0].shape[0] == 0
+
+
+def test_watch_errors(rs):
+    c = config_circuit("C1")
+    g = rs.Graph(c)
+    L = rs.Lanes(g, 4)
+    with pytest.raises(rs.RtlSimError) as e:
+        L.watch([c.n_signals])
+    assert e.value.name == "RS_E_RANGE"
+    with pytest.raises(rs.RtlSimError) as e:
+        L.watch([0], capacity=0)
+    assert e.value.name == "RS_E_INVALID_ARG"
+    gs = rs.Graph(c, mode="single")
+    Ls = rs.Lanes(gs, 1)
+    with pytest.raises(rs.RtlSimError) as e:
+        Ls.watch([0])
+    assert e.value.name == "RS_E_UNSUPPORTED"
+    assert L.wave_read()[0].shape[0] == 0           # nothing watched: empty
