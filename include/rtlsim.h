@@ -260,135 +260,4 @@ rs_status rs_debug_trace(rs_lanes* s, uint64_t* out, uint64_t n);
 #ifdef __cplusplus
 }
 #endif
-#endif  uint32_t kernel;         /* RS_MODE_LANES step kernel (results identical): 0 = auto (2 below 2048
-                              lanes, else 1); 1 = tile-interleaved: tile = 32 * P lanes (P = 1, 2, 4),
-                              thread t owns lanes t + 32k, one op per warp, operand container widths
-                              dispatched once per op through a jump table on the class signature;
-                              2 = two adjacent lanes per thread, 8/16/32-lane tiles, aligned 64-bit
-                              word gathers + extraction.  lane_tile must match (32/64/128 for 1,
-                              8/16/32 for 2).  RS_E_INVALID_ARG otherwise. */
-} rs_lane_opts;
-
-typedef struct rs_graph rs_graph;
-typedef struct rs_lanes rs_lanes;
-
-const char* rs_version(void);
-/* Thread-local message for the last non-RS_OK status (never NULL). */
-const char* rs_last_error(void);
-
-/* device value for rs_load_graph: compile and validate only (no device
- * memory; the handle supports rs_graph_info_get / rs_graph_export and
- * rs_free_graph only -- rs_alloc_lanes returns RS_E_STATE). */
-#define RS_DEVICE_NONE (-1)
-
-/* Validate + compile the circuit into the GPU graph format (levelize, insert
- * identity copies for register->source next edges, group each level by
- * (opcode, arity, width class) as in PAPER.md Format c P:1123-1129, renumber
- * signals so op outputs are implicit, pack operand coords as int32) and copy
- * it to `device`.  mode: RS_MODE_LANES or RS_MODE_SINGLE. */
-rs_status rs_load_graph(const rs_graph_desc* desc, int device, uint32_t mode, rs_graph** out);
-rs_status rs_graph_info_get(const rs_graph* g, rs_graph_info* out);
-
-/* Copy one array of the compiled graph format to host memory `out` (or,
- * with out == NULL, only report its element count in *count).  Element
- * types: RUNS = 5 x u32 per run {op_begin, count, coord_begin, out_row0,
- * meta = opcode | arity<<8 | out_class<<16}; OPK = u64; all others u32.
- * For inspection and tests of the format; never needed to simulate. */
-enum {
-  RS_EXPORT_RUNS = 0, RS_EXPORT_LEVEL_RUN_BEGIN = 1, RS_EXPORT_LEVEL_OP_BEGIN = 2, RS_EXPORT_OPW = 3,
-  RS_EXPORT_OPK = 4, RS_EXPORT_COORD_OFF = 5, RS_EXPORT_COORD = 6, RS_EXPORT_SIG_COORD = 7,
-  RS_EXPORT_REG_COORD = 8, RS_EXPORT_REG_NEXT_COORD = 9, RS_EXPORT_IN_COORD = 10
-};
-rs_status rs_graph_export(const rs_graph* g, uint32_t what, void* out, uint64_t* count);
-void rs_free_graph(rs_graph* g);
-
-/* Level ranges of a `parts`-way level cut (rs_lane_opts.parts):
- * partition k owns levels [cut[k], cut[k+1]); cut[0] = 0, cut[parts] = n_levels,
- * every range non-empty, boundaries balanced by op weight (1 + arity).  `cut`
- * is caller-owned host memory of parts + 1 entries.  Host-only (works on a
- * RS_DEVICE_NONE graph).  RS_E_INVALID_ARG if parts is 0, > 8 or > n_levels. */
-rs_status rs_level_cut(const rs_graph* g, uint32_t parts, uint32_t* cut);
-
-/* Allocate the signal state for n_lanes lanes (RS_MODE_SINGLE: n_lanes must
- * be 1), initialised to: registers = init & M(w), constants = value, all
- * other signals 0; the absolute cycle counter = 0; input source = seed 0. */
-rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts, rs_lanes** out);
-void rs_free_lanes(rs_lanes* s);
-/* Device bytes held by this allocation. */
-uint64_t rs_lanes_bytes(const rs_lanes* s);
-
-/* Input source = counter-based stimulus of (seed, input k, absolute cycle,
- * global lane) (reading R13). */
-rs_status rs_set_input_seed(rs_lanes* s, uint64_t seed);
-/* Input source = staged values for absolute cycles [first_cycle,
- * first_cycle + n_cycles): values[n_cycles][n_inputs][n_lanes] (u64, masked to
- * each input's width when injected), host (on_device = 0) or device memory
- * of the lanes' device (on_device = 1).  n_cycles <= stage_cycles.  The
- * ring keeps the last stage_cycles staged cycles. Async on the stream. */
-rs_status rs_set_inputs(rs_lanes* s, uint64_t first_cycle, uint32_t n_cycles,
-                        const uint64_t* values, int on_device);
-
-/* Advance n_cycles cycles.  hashes: RS_MEM_NONE (no hash computed, pointer
- * ignored), RS_MEM_DEVICE ([n_cycles][n_lanes] u64 on the lanes' device) or
- * RS_MEM_HOST ([n_cycles][n_lanes] u64 host; the call synchronises).
- * H[c][l] = sum over all canonical signals of value * K_s mod 2^64, taken
- * after the combinational evaluation of cycle c and before the commit. */
-rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int hashes_mem);
-
-/* Read canonical signals ids[n_ids] for lanes [lane_begin, lane_begin+n_lanes)
- * (allocation-relative) into out[n_ids][n_lanes] (host).  Registers hold the
- * committed values; other signals hold the values of the last cycle. Syncs. */
-rs_status rs_read_signals(rs_lanes* s, const uint32_t* ids, uint32_t n_ids,
-                          uint32_t lane_begin, uint32_t n_lanes, uint64_t* out);
-/* Checkpoint restore: overwrite registers reg_ids[n] (canonical ids of
- * registers) for lanes [lane_begin, lane_begin+n_lanes) from values[n][n_lanes]
- * (host, masked).  RS_E_RANGE if an id is not a register. Syncs. */
-rs_status rs_write_registers(rs_lanes* s, const uint32_t* reg_ids, uint32_t n,
-                             uint32_t lane_begin, uint32_t n_lanes, const uint64_t* values);
-rs_status rs_get_cycle(const rs_lanes* s, uint64_t* cycle);
-rs_status rs_set_cycle(rs_lanes* s, uint64_t cycle);
-/* Kernel launches issued by this allocation so far (evidence counter). */
-uint64_t rs_launch_count(const rs_lanes* s);
-/* Chosen launch shape: lane tile, threads per CTA, CTAs, CTAs per cluster
- * (any output pointer may be NULL). */
-rs_status rs_launch_shape(const rs_lanes* s, uint32_t* lane_tile, uint32_t* threads, uint32_t* ctas,
-                          uint32_t* cluster);
-/* Lane-mode step kernel in use (rs_lane_opts.kernel: 1 or 2); 0 for single-lane mode or NULL. */
-uint32_t rs_lanes_kernel(const rs_lanes* s);
-rs_status rs_sync(rs_lanes* s);
-/* ---- Waveform capture (§6.2: the
- * DMI dumps waveforms of selected signals).  rs_watch selects up to 2^16
- * canonical signal ids of a RS_MODE_LANES allocation; every later
- * rs_step_cycles then records, fused into the step kernel (one extra stage per
- * cycle, after the last level and before the register commit), a CHANGE
- * record for each (watched signal, lane) whose value after the combinational
- * evaluation of cycle c -- the snapshot the per-cycle hash covers -- differs
- * from its value at cycle c - 1, and for every (signal, lane) at the first
- * stepped cycle after rs_watch.  Records are appended to a device buffer of
- * `capacity` records in no particular order; records beyond capacity are
- * counted as dropped.  n_ids = 0 stops watching (and frees the buffers).
- * RS_E_RANGE for an unknown id, RS_E_UNSUPPORTED in RS_MODE_SINGLE. */
-typedef struct {
-  uint64_t cycle;   /* absolute cycle */
-  uint64_t lane;    /* global lane id (rs_lane_opts.lane0 + allocation lane) */
-  uint32_t watch;   /* index into the rs_watch id list */
-  uint32_t pad_;
-  uint64_t value;   /* the signal's value at that cycle (masked to its width) */
-} rs_change;
-rs_status rs_watch(rs_lanes* s, const uint32_t* ids, uint32_t n_ids, uint64_t capacity);
-/* Copy the records collected so far to host memory `out` (up to cap; caller-
- * owned) and clear the buffer; *n_out = records copied, *dropped = records
- * lost to capacity since the last read (either pointer may be NULL).
- * Synchronises the lanes' stream. */
-rs_status rs_wave_read(rs_lanes* s, rs_change* out, uint64_t cap, uint64_t* n_out, uint64_t* dropped);
-
-/* Diagnostics (builds with -DRS_TRACE only, else RS_E_UNSUPPORTED): the first
- * call arms a per-stage clock64 trace of CTA 0; later calls copy up to n u64
- * stamps to host `out` (layout: per stage [top, after stage wait, after
- * barrier, work end of each warp]). */
-rs_status rs_debug_trace(rs_lanes* s, uint64_t* out, uint64_t n);
-
-#ifdef __cplusplus
-}
-#endif
 #endif
