@@ -232,13 +232,18 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
   // lane t / W), so a level with few ops puts one op per warp -- the warps run
   // their ops' code paths in parallel instead of one warp diverging over them
   const uint32_t W = (T + 31) / 32;
-  const uint32_t top = (tid & 31u) * W + (tid >> 5);
+  const uint32_t top_w = (tid & 31u) * W + (tid >> 5);
+  // ...but a level with more than two ops per warp is dealt densely (op t ->
+  // thread t): consecutive ops share a run (opcode, arity, class), so a warp's
+  // threads mostly take one code path, and far fewer warp instructions issue
+  auto slot = [&](uint32_t n) -> uint32_t { return n > 2 * W ? tid : top_w; };
   // hash weights are software-pipelined one level ahead: with few warps per
   // SM an exposed global load per level would dominate the level's latency
   auto kload = [&](uint32_t l) -> uint64_t {
     if (!HASH || l >= h->n_levels) return 0ull;
     const SliceLvl& L = lvl[l];
-    return top < L.n ? __ldg(a.g.opk + L.op_begin + top) : 0ull;
+    const uint32_t t0 = slot(L.n);
+    return t0 < L.n ? __ldg(a.g.opk + L.op_begin + t0) : 0ull;
   };
   uint64_t knext = kload(0);
   const uint64_t klat = (HASH && tid < h->n_latch && (lat[4 * tid + 2] & 128u)) ? __ldg(a.g.reg_k + lat[4 * tid + 3]) : 0ull;
@@ -259,6 +264,7 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
       const uint64_t kcur = knext;
       knext = kload(l + 1 < h->n_levels ? l + 1 : 0);
 #pragma unroll 1
+      const uint32_t top = slot(L.n);
       for (uint32_t t = top; t < L.n; t += T) {
         const uint64_t k = !HASH ? 0ull : (t == top ? kcur : __ldg(a.g.opk + L.op_begin + t));
         const uint32_t pw = pws[L.pw_base + t];
