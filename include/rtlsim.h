@@ -136,6 +136,18 @@ typedef struct {
                               2 = two adjacent lanes per thread, 8/16/32-lane tiles, aligned 64-bit
                               word gathers + extraction.  lane_tile must match (32/64/128 for 1,
                               8/16/32 for 2).  RS_E_INVALID_ARG otherwise. */
+  uint32_t repcut;         /* RS_MODE_SINGLE replicated cut (App. C, Cascade 2; SURVEY.md §8(f)
+                              NEXT-2): 0/1 = off, else P partitions = CTAs of one cooperative launch; the
+                              registers are cut into P contiguous blocks, partition p evaluates the cone of
+                              its registers' next values (shared logic replicated) on its own state replica
+                              with CTA barriers only, and after each cycle pushes its registers' new values
+                              to the partitions that read them (the Register Update Map).  Pays off on
+                              designs whose cones barely overlap (e.g. multi-core SoCs).  RS_E_INVALID_ARG
+                              if P > n_regs, > 255, > the SMs of the device, or combined with parts.
+                              Each partition keeps its working set (op descriptors + a compact copy of the
+                              signals it touches) in shared memory when it fits (k_repcut_smem), else works
+                              on its state replica in global memory (k_repcut). */
+  uint32_t repcut_global;  /* 1: force the global-replica RepCut kernel even if the slices fit shared memory */
 } rs_lane_opts;
 
 typedef struct rs_graph rs_graph;
@@ -170,6 +182,12 @@ enum {
 };
 rs_status rs_graph_export(const rs_graph* g, uint32_t what, void* out, uint64_t* count);
 void rs_free_graph(rs_graph* g);
+
+/* RepCut plan statistics for P partitions (host-only; works on a RS_DEVICE_NONE
+ * graph): *ops_total = sum of the partitions' op counts (replication factor =
+ * ops_total / ops), *max_ops = the largest partition, *push = (register,
+ * reader) pairs of the Register Update Map.  Any output may be NULL. */
+rs_status rs_repcut_stats(const rs_graph* g, uint32_t P, uint64_t* ops_total, uint32_t* max_ops, uint64_t* push);
 
 /* Level ranges of a `parts`-way level cut (rs_lane_opts.parts):
  * partition k owns levels [cut[k], cut[k+1]); cut[0] = 0, cut[parts] = n_levels,
@@ -222,7 +240,9 @@ uint64_t rs_launch_count(const rs_lanes* s);
  * (any output pointer may be NULL). */
 rs_status rs_launch_shape(const rs_lanes* s, uint32_t* lane_tile, uint32_t* threads, uint32_t* ctas,
                           uint32_t* cluster);
-/* Lane-mode step kernel in use (rs_lane_opts.kernel: 1 or 2); 0 for single-lane mode or NULL. */
+/* Step kernel in use: lane mode 1 or 2 (rs_lane_opts.kernel); single-lane mode 3 = RepCut with
+ * shared-memory slices (k_repcut_smem), 4 = RepCut on global replicas (k_repcut), 0 = the
+ * level-synchronous single-lane kernel (or NULL). */
 uint32_t rs_lanes_kernel(const rs_lanes* s);
 rs_status rs_sync(rs_lanes* s);
 /* ---- Waveform capture (§6.2: the

@@ -670,4 +670,294 @@ bool build_single_slices(const CompiledGraph& g, uint32_t P, uint32_t Gp, uint32
   return true;
 }
 
+bool build_repcut(const CompiledGraph& g, uint32_t P, RepCutPlan* out, std::string* err) {
+  const uint32_t NT = g.n_ops_total(), NL = g.n_levels, R = g.n_regs;
+  if (P == 0 || P > 255 || (R && P > R) || (!R && P > 1)) {
+    *err = "repcut: partitions must be in [1, min(255, n_regs)]";
+    return false;
+  }
+  // producing op of every (class, row); -1 = a source
+  std::vector<int32_t> prod[4];
+  for (int c = 0; c < 4; ++c) prod[c].assign(g.rows[c], -1);
+  for (const DevRun& r : g.runs) {
+    const uint32_t cls = (r.meta >> 16) & 3u;
+    for (uint32_t k = 0; k < r.count; ++k) prod[cls][r.out_row0 + k] = (int32_t)(r.op_begin + k);
+  }
+  auto producer = [&](uint32_t c) -> int32_t { return prod[c >> 30][c & ROW_MASK]; };
+  // register blocks
+  std::vector<uint32_t> reg_part(R);
+  for (uint32_t i = 0; i < R; ++i) reg_part[i] = (uint32_t)((uint64_t)i * P / R);
+  // cones: member[p] bitmaps over ops
+  std::vector<std::vector<uint8_t>> member(P, std::vector<uint8_t>(NT, 0));
+  std::vector<uint32_t> stack;
+  auto close = [&](uint32_t p, int32_t j0) {
+    if (j0 < 0 || member[p][j0]) return;
+    stack.assign(1, (uint32_t)j0);
+    member[p][j0] = 1;
+    while (!stack.empty()) {
+      const uint32_t j = stack.back();
+      stack.pop_back();
+      for (uint32_t a = g.coord_off[j]; a < g.coord_off[j + 1]; ++a) {
+        const int32_t q = producer(g.coord[a]);
+        if (q >= 0 && !member[p][q]) {
+          member[p][q] = 1;
+          stack.push_back((uint32_t)q);
+        }
+      }
+    }
+  };
+  for (uint32_t i = 0; i < R; ++i) close(reg_part[i], producer(g.reg_next_coord[i]));
+  std::vector<int32_t> owner(NT, -1);
+  for (uint32_t j = 0; j < NT; ++j)
+    for (uint32_t p = 0; p < P && owner[j] < 0; ++p)
+      if (member[p][j]) owner[j] = (int32_t)p;
+  // ops outside every register cone (dead logic: its values are still hashed
+  // and readable) join the partition of their first operand's producer (the
+  // producers have lower device indices -- level order -- so they already have
+  // an owner), else of their first register operand, else j mod P; with their
+  // cone, so they replicate and push no more than they must
+  std::unordered_map<uint32_t, uint32_t> reg_of_coord;
+  for (uint32_t i = 0; i < R; ++i) reg_of_coord[g.reg_coord[i]] = i;
+  for (uint32_t j = 0; j < NT; ++j)
+    if (owner[j] < 0) {
+      int32_t p = -1;
+      for (uint32_t a = g.coord_off[j]; a < g.coord_off[j + 1] && p < 0; ++a) {
+        const int32_t q = producer(g.coord[a]);
+        if (q >= 0) p = owner[q];
+      }
+      for (uint32_t a = g.coord_off[j]; a < g.coord_off[j + 1] && p < 0; ++a) {
+        auto it = reg_of_coord.find(g.coord[a]);
+        if (it != reg_of_coord.end()) p = (int32_t)reg_part[it->second];
+      }
+      if (p < 0) p = (int32_t)(j % P);
+      close((uint32_t)p, (int32_t)j);
+      owner[j] = p;
+    }
+  RepCutPlan& o = *out;
+  o = RepCutPlan{};
+  o.P = P;
+  o.lvl_begin.assign((size_t)P * (NL + 1), 0);
+  for (uint32_t p = 0; p < P; ++p) {
+    uint32_t cnt = 0;
+    for (uint32_t l = 0; l < NL; ++l) {
+      o.lvl_begin[(size_t)p * (NL + 1) + l] = (uint32_t)o.ops.size();
+      for (uint32_t j = g.level_op_begin[l]; j < g.level_op_begin[l + 1]; ++j)
+        if (member[p][j]) {
+          o.ops.push_back(j | ((uint32_t)(owner[j] == (int32_t)p) << 31));
+          ++cnt;
+        }
+    }
+    o.lvl_begin[(size_t)p * (NL + 1) + NL] = (uint32_t)o.ops.size();
+    o.ops_total += cnt;
+    o.max_ops = std::max(o.max_ops, cnt);
+  }
+  // own registers and the Register Update Map (push to the partitions that read a register)
+  o.reg_begin.assign(P + 1, 0);
+  for (uint32_t i = 0; i < R; ++i) o.reg_begin[reg_part[i] + 1]++;
+  for (uint32_t p = 0; p < P; ++p) o.reg_begin[p + 1] += o.reg_begin[p];
+  o.regs.resize(R);
+  {
+    std::vector<uint32_t> fill(o.reg_begin.begin(), o.reg_begin.end() - 1);
+    for (uint32_t i = 0; i < R; ++i) o.regs[fill[reg_part[i]]++] = i;
+  }
+  std::vector<std::vector<uint8_t>> reads(P, std::vector<uint8_t>(R, 0));
+  for (uint32_t p = 0; p < P; ++p)
+    for (uint32_t j = 0; j < NT; ++j)
+      if (member[p][j])
+        for (uint32_t a = g.coord_off[j]; a < g.coord_off[j + 1]; ++a) {
+          auto it = reg_of_coord.find(g.coord[a]);
+          if (it != reg_of_coord.end()) reads[p][it->second] = 1;
+        }
+  o.push_begin.assign(P + 1, 0);
+  for (uint32_t p = 0; p < P; ++p) {
+    o.push_begin[p] = (uint32_t)(o.push.size() / 2);
+    for (uint32_t k = o.reg_begin[p]; k < o.reg_begin[p + 1]; ++k) {
+      const uint32_t i = o.regs[k];
+      for (uint32_t q = 0; q < P; ++q)
+        if (q != p && reads[q][i]) {
+          o.push.push_back(i);
+          o.push.push_back(q);
+        }
+    }
+  }
+  o.push_begin[P] = (uint32_t)(o.push.size() / 2);
+  // read-back: the replica holding each signal's value
+  o.sig_owner.assign(g.n_signals, 0);
+  for (uint32_t s = 0; s < g.n_signals; ++s) {
+    if (g.sig_kind[s] == 1) {
+      o.sig_owner[s] = (uint8_t)reg_part[g.sig_reg_index[s]];
+    } else if (g.sig_kind[s] == 3) {
+      const int32_t j = producer(g.sig_coord[s]);
+      o.sig_owner[s] = (uint8_t)(j >= 0 ? owner[j] : 0);
+    }
+  }
+  return true;
+}
+
+
+bool build_repcut_slices(const CompiledGraph& g, const RepCutPlan& plan, uint32_t max_smem,
+                         std::vector<uint8_t>* blob, std::vector<uint64_t>* slice_off,
+                         std::vector<uint64_t>* op_k, std::vector<uint8_t>* in_owner, std::string* err) {
+  const uint32_t P = plan.P, NL = g.n_levels, NT = g.n_ops_total(), R = g.n_regs, NI = g.n_inputs;
+  blob->clear();
+  slice_off->assign(P, 0);
+  op_k->clear();
+  if (R >= (1u << 24)) {
+    *err = "repcut slices: more than 2^24 registers";
+    return false;
+  }
+  in_owner->assign(NI, 0);
+  // output coord of every op
+  std::vector<uint32_t> out_coord(NT, 0);
+  for (const DevRun& r : g.runs) {
+    const uint32_t cls = (r.meta >> 16) & 3u;
+    for (uint32_t k = 0; k < r.count; ++k) out_coord[r.op_begin + k] = (cls << 30) | (r.out_row0 + k);
+  }
+  std::unordered_map<uint32_t, uint32_t> reg_of_coord, in_of_coord;
+  for (uint32_t i = 0; i < R; ++i) reg_of_coord[g.reg_coord[i]] = i;
+  for (uint32_t k = 0; k < NI; ++k) in_of_coord[g.in_coord[k]] = k;
+  // who reads each input; its owner is the lowest reader (none: partition 0)
+  std::vector<std::vector<uint8_t>> reads_in(P, std::vector<uint8_t>(NI, 0));
+  for (uint32_t p = 0; p < P; ++p)
+    for (uint32_t x = plan.lvl_begin[(size_t)p * (NL + 1)]; x < plan.lvl_begin[(size_t)p * (NL + 1) + NL]; ++x) {
+      const uint32_t j = plan.ops[x] & 0x7FFFFFFFu;
+      for (uint32_t a = g.coord_off[j]; a < g.coord_off[j + 1]; ++a) {
+        auto it = in_of_coord.find(g.coord[a]);
+        if (it != in_of_coord.end()) reads_in[p][it->second] = 1;
+      }
+    }
+  for (uint32_t k = 0; k < NI; ++k) {
+    uint32_t o = 0;
+    while (o < P && !reads_in[o][k]) ++o;
+    (*in_owner)[k] = (uint8_t)(o < P ? o : 0);
+  }
+  std::vector<uint32_t> reg_owner(R, 0);
+  for (uint32_t p = 0; p < P; ++p)
+    for (uint32_t k = plan.reg_begin[p]; k < plan.reg_begin[p + 1]; ++k) reg_owner[plan.regs[k]] = p;
+  auto align16 = [](size_t n) { return (n + 15) & ~(size_t)15; };
+  for (uint32_t p = 0; p < P; ++p) {
+    const uint32_t* lb = plan.lvl_begin.data() + (size_t)p * (NL + 1);
+    // ---- local signal set, by class
+    std::vector<uint32_t> sigs;
+    for (uint32_t x = lb[0]; x < lb[NL]; ++x) {
+      const uint32_t j = plan.ops[x] & 0x7FFFFFFFu;
+      sigs.push_back(out_coord[j]);
+      for (uint32_t a = g.coord_off[j]; a < g.coord_off[j + 1]; ++a) sigs.push_back(g.coord[a]);
+    }
+    for (uint32_t k = plan.reg_begin[p]; k < plan.reg_begin[p + 1]; ++k) {
+      sigs.push_back(g.reg_coord[plan.regs[k]]);
+      sigs.push_back(g.reg_next_coord[plan.regs[k]]);
+    }
+    for (uint32_t k = 0; k < NI; ++k)
+      if (reads_in[p][k] || (*in_owner)[k] == p) sigs.push_back(g.in_coord[k]);
+    std::sort(sigs.begin(), sigs.end());
+    sigs.erase(std::unique(sigs.begin(), sigs.end()), sigs.end());
+    std::unordered_map<uint32_t, uint32_t> local;
+    local.reserve(sigs.size() * 2);
+    uint32_t off = 0, bnd[4] = {0, 0, 0, 0};
+    for (int cls = 3; cls >= 0; --cls) {
+      bnd[cls] = off;
+      for (uint32_t c : sigs)
+        if ((c >> 30) == (uint32_t)cls) {
+          local[c] = off;
+          off += 1u << cls;
+        }
+    }
+    const uint32_t state_bytes = (uint32_t)align16(off + 8);  // + 8: the aligned-word gather may read past the end
+    if (off > 65535u) {
+      *err = "repcut slice " + std::to_string(p) + ": local state of " + std::to_string(off) + " bytes > 64 KiB";
+      return false;
+    }
+    auto L = [&](uint32_t c) -> uint16_t { return (uint16_t)local.at(c); };
+    // ---- sections
+    const uint32_t n_ops = lb[NL] - lb[0];
+    std::vector<uint32_t> lvl(NL + 1), pw(n_ops);
+    std::vector<uint16_t> cw((size_t)n_ops * 4), ovf;
+    uint32_t max_level = 0;
+    for (uint32_t l = 0; l <= NL; ++l) lvl[l] = lb[l] - lb[0];
+    for (uint32_t l = 0; l < NL; ++l) max_level = std::max(max_level, lb[l + 1] - lb[l]);
+    for (uint32_t x = lb[0]; x < lb[NL]; ++x) {
+      const uint32_t i = x - lb[0], j = plan.ops[x] & 0x7FFFFFFFu;
+      const uint32_t n = g.coord_off[j + 1] - g.coord_off[j];
+      pw[i] = g.opw[j];
+      cw[4 * i] = L(out_coord[j]);
+      const uint32_t* cp = g.coord.data() + g.coord_off[j];
+      cw[4 * i + 1] = L(cp[0]);
+      cw[4 * i + 2] = n >= 2 ? L(cp[1]) : cw[4 * i + 1];
+      if (n <= 3) {
+        cw[4 * i + 3] = n >= 3 ? L(cp[2]) : cw[4 * i + 1];
+      } else {
+        if (ovf.size() + n > 65535u) {
+          *err = "repcut slice: too many long-fold operands";
+          return false;
+        }
+        cw[4 * i + 3] = (uint16_t)ovf.size();
+        for (uint32_t o = 2; o < n; ++o) ovf.push_back(L(cp[o]));
+      }
+      op_k->push_back((plan.ops[x] >> 31) ? g.opk[j] : 0ull);
+    }
+    std::vector<uint32_t> commit, pull, inj, map;
+    for (uint32_t k = plan.reg_begin[p]; k < plan.reg_begin[p + 1]; ++k) {
+      const uint32_t r = plan.regs[k];
+      commit.push_back(L(g.reg_coord[r]) | ((uint32_t)L(g.reg_next_coord[r]) << 16));
+      commit.push_back(r | (g.reg_w[r] << 24));
+    }
+    for (uint32_t c : sigs) {
+      auto it = reg_of_coord.find(c);
+      if (it != reg_of_coord.end()) {
+        const uint32_t r = it->second;
+        if (reg_owner[r] != p) {
+          pull.push_back(L(c));
+          pull.push_back(r);
+        }
+      }
+      map.push_back(L(c));
+      map.push_back(c);
+    }
+    for (uint32_t k = 0; k < NI; ++k)
+      if (reads_in[p][k] || (*in_owner)[k] == p) {
+        inj.push_back(L(g.in_coord[k]) | (g.in_w[k] << 16) | ((uint32_t)((*in_owner)[k] == p) << 23));
+        inj.push_back(k);
+      }
+    RepSliceHdr h{};
+    size_t o = align16(sizeof(RepSliceHdr));
+    h.off_lvl = (uint32_t)o; o = align16(o + lvl.size() * 4);
+    h.off_pw = (uint32_t)o; o = align16(o + pw.size() * 4);
+    h.off_cw = (uint32_t)o; o = align16(o + cw.size() * 2);
+    h.off_ovf = (uint32_t)o; o = align16(o + ovf.size() * 2);
+    h.off_commit = (uint32_t)o; o = align16(o + commit.size() * 4);
+    h.off_pull = (uint32_t)o; o = align16(o + pull.size() * 4);
+    h.off_inj = (uint32_t)o; o = align16(o + inj.size() * 4);
+    h.smem_bytes = (uint32_t)o;
+    h.state_off = (uint32_t)o;
+    h.state_bytes = state_bytes;
+    h.off_map = (uint32_t)o; o = align16(o + map.size() * 4);
+    h.b1 = bnd[2]; h.b2 = bnd[1]; h.b3 = bnd[0];
+    h.n_levels = NL; h.n_ops = n_ops; h.max_level = max_level;
+    h.n_commit = (uint32_t)commit.size() / 2; h.n_pull = (uint32_t)pull.size() / 2;
+    h.n_inj = (uint32_t)inj.size() / 2; h.n_map = (uint32_t)map.size() / 2;
+    h.k_base = (uint32_t)(op_k->size() - n_ops);
+    if ((size_t)h.smem_bytes + state_bytes > max_smem) {
+      *err = "repcut slice " + std::to_string(p) + ": " + std::to_string(h.smem_bytes + state_bytes) +
+             " bytes of shared memory > " + std::to_string(max_smem);
+      return false;
+    }
+    const size_t base = align16(blob->size());
+    (*slice_off)[p] = base;
+    blob->resize(base + o, 0);
+    uint8_t* b = blob->data() + base;
+    std::memcpy(b, &h, sizeof h);
+    auto cp = [&](uint32_t at, const void* src, size_t n) { if (n) std::memcpy(b + at, src, n); };
+    cp(h.off_lvl, lvl.data(), lvl.size() * 4);
+    cp(h.off_pw, pw.data(), pw.size() * 4);
+    cp(h.off_cw, cw.data(), cw.size() * 2);
+    cp(h.off_ovf, ovf.data(), ovf.size() * 2);
+    cp(h.off_commit, commit.data(), commit.size() * 4);
+    cp(h.off_pull, pull.data(), pull.size() * 4);
+    cp(h.off_inj, inj.data(), inj.size() * 4);
+    cp(h.off_map, map.data(), map.size() * 4);
+  }
+  return true;
+}
+
 }  // namespace rtlsim

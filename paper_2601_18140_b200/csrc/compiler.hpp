@@ -211,4 +211,66 @@ void row_owner(const CompiledGraph& g, const std::vector<uint32_t>& cut, std::ve
 bool build_single_slices(const CompiledGraph& g, uint32_t P, uint32_t Gp, uint32_t max_bytes,
                          std::vector<uint8_t>* blob, std::vector<uint64_t>* slice_off);
 
+// ---------------------------------------------------------------- RepCut
+// Replicated-cut partitioning for single-lane simulation (SURVEY.md §8(f)
+// NEXT-2; App. C, Cascade 2 P:2021-2078): registers are split into P
+// contiguous blocks; partition p evaluates the combinational cone of its
+// registers' next values (ops shared between cones are replicated), keeps its
+// own state replica, and after every cycle pushes each of its registers'
+// new values into the replicas of the partitions that read it -- the Register
+// Update Map (RUM) of Cascade 2's last Einsum.  Every op is hashed by exactly
+// one partition (its lowest-numbered holder); ops outside every cone are
+// given to partition (op index mod P) with their own cones.
+struct RepCutPlan {
+  uint32_t P = 0;
+  std::vector<uint32_t> lvl_begin;   // [P][n_levels + 1]: offsets into ops (partition-major)
+  std::vector<uint32_t> ops;         // device op index | owned << 31, per partition in level order
+  std::vector<uint32_t> reg_begin;   // [P + 1]
+  std::vector<uint32_t> regs;        // register indices, partition-major
+  std::vector<uint32_t> push_begin;  // [P + 1]
+  std::vector<uint32_t> push;        // (register index, reader partition) pairs, by owner partition
+  std::vector<uint8_t> sig_owner;    // [n_signals]: the partition whose replica holds the signal's value
+  uint64_t ops_total = 0;            // sum of partition op counts (replication = ops_total / n_ops_total)
+  uint32_t max_ops = 0;              // largest partition
+};
+// Returns false (with *err) if P is 0, > 255 or > the number of registers.
+bool build_repcut(const CompiledGraph& g, uint32_t P, RepCutPlan* out, std::string* err);
+
+// Partition-local RepCut slices (repcut.cuh k_repcut_smem): partition p keeps
+// the values of the signals it touches (its ops' outputs and operands, its
+// registers, the inputs it reads or owns) in shared memory, renumbered into a
+// compact local state of byte offsets < 64 KiB -- u64 region first, then u32,
+// u16, u8, so an offset's width class follows from three comparisons -- and
+// its op descriptors next to them.  Registers cross partitions through a
+// global mailbox (value by register index): owners post after the commit,
+// readers pull after the one grid barrier per cycle.  Layout of one slice
+// (16-byte aligned sections, offsets relative to the slice; the smem part is
+// [0, smem_bytes), the map is read from global memory at launch start / end):
+//   lvl u32[n_levels + 1] | pw u32[ops] | cw u16x4[ops] {out, c0, c1, c2 | ovf index}
+//   | ovf u16[...] (operands 2.. of ops with arity > 3) | commit u32x2[n_commit]
+//   {reg | next << 16, register index} | pull u32x2[n_pull] {local, register index}
+//   | inject u32x2[n_inj] {local | width << 16 | owned << 23, input index}
+//   | (state: state_bytes at state_off, not in the blob) | map u32x2[n_map] {local, coord}
+struct RepSliceHdr {
+  uint32_t smem_bytes;    // bytes copied to shared memory (16-aligned)
+  uint32_t state_off;     // shared-memory offset of the local state (16-aligned; = smem_bytes)
+  uint32_t state_bytes;   // 16-aligned
+  uint32_t b1, b2, b3;    // local offsets where the u32 / u16 / u8 regions start
+  uint32_t n_levels, n_ops;
+  uint32_t off_lvl, off_pw, off_cw, off_ovf;
+  uint32_t off_commit, n_commit, off_pull, n_pull;
+  uint32_t off_inj, n_inj, off_map, n_map;
+  uint32_t k_base;        // first entry of the partition in the op hash-weight array
+  uint32_t max_level;     // largest level of the partition (ops)
+  uint32_t pad[2];
+};
+// Builds the P slices of `plan` (blob, slice offsets) and the per-partition op
+// hash weights (owned ops: opk, else 0) in slice op order.  in_owner[k] = the
+// partition that hashes input k (and whose replica holds it for read-back).
+// Returns false (with *err) if a slice's smem part + local state exceeds
+// max_smem or its local state exceeds 64 KiB.
+bool build_repcut_slices(const CompiledGraph& g, const RepCutPlan& plan, uint32_t max_smem,
+                         std::vector<uint8_t>* blob, std::vector<uint64_t>* slice_off,
+                         std::vector<uint64_t>* op_k, std::vector<uint8_t>* in_owner, std::string* err);
+
 }  // namespace rtlsim

@@ -109,6 +109,17 @@ struct TileP {
   uint16_t* p1;
   uint32_t* p2;
   uint64_t* p3;
+  // plain (L1-cached) load: state written by this CTA, or published to it
+  // through an acquire (RepCut replicas)
+  __device__ __forceinline__ uint64_t ld(uint32_t c) const {
+    const size_t r = (size_t)(c & ROW_MASK) * LT;
+    switch (c >> 30) {
+      case 0: return p0[r];
+      case 1: return p1[r];
+      case 2: return p2[r];
+      default: return p3[r];
+    }
+  }
   // L2-coherent load (single-lane mode: other SMs write the state)
   __device__ __forceinline__ uint64_t ld_cg(uint32_t c) const {
     const size_t r = (size_t)(c & ROW_MASK) * LT;
@@ -300,28 +311,30 @@ __device__ __forceinline__ uint64_t block_sum(uint64_t v, uint64_t* sm) {
   return s;
 }
 
+template <bool CG = true>
 __device__ __forceinline__ uint64_t single_op(const StepArgs& a, const TileP<1>& t, uint32_t j) {
+  auto L = [&](uint32_t c) -> uint64_t { return CG ? t.ld_cg(c) : t.ld(c); };
   const uint32_t pw = __ldg(a.g.opw + j);
   const uint32_t op = (pw >> 22) & 15u, n = pw >> 26;
   const uint32_t* cp = a.g.coord + __ldg(a.g.coord_off + j);
   uint64_t x[3];
   switch (op) {
     case RS_OP_AND: case RS_OP_OR: case RS_OP_XOR: case RS_OP_ADD: case RS_OP_SUB: case RS_OP_MUL: {
-      uint64_t r = t.ld_cg(__ldg(cp));
-      for (uint32_t o = 1; o < n; ++o) r = fold_step(op, r, t.ld_cg(__ldg(cp + o)));
+      uint64_t r = L(__ldg(cp));
+      for (uint32_t o = 1; o < n; ++o) r = fold_step(op, r, L(__ldg(cp + o)));
       return r & wmask(pw & 127u);
     }
-    case RS_OP_EQ: x[0] = t.ld_cg(__ldg(cp)); x[1] = t.ld_cg(__ldg(cp + 1)); return apply_op<RS_OP_EQ, 2>(x, pw);
-    case RS_OP_LT: x[0] = t.ld_cg(__ldg(cp)); x[1] = t.ld_cg(__ldg(cp + 1)); return apply_op<RS_OP_LT, 2>(x, pw);
-    case RS_OP_CAT: x[0] = t.ld_cg(__ldg(cp)); x[1] = t.ld_cg(__ldg(cp + 1)); return apply_op<RS_OP_CAT, 2>(x, pw);
-    case RS_OP_NOT: x[0] = t.ld_cg(__ldg(cp)); return apply_op<RS_OP_NOT, 1>(x, pw);
-    case RS_OP_SHL: x[0] = t.ld_cg(__ldg(cp)); return apply_op<RS_OP_SHL, 1>(x, pw);
-    case RS_OP_SHR: x[0] = t.ld_cg(__ldg(cp)); return apply_op<RS_OP_SHR, 1>(x, pw);
-    case RS_OP_BITS: x[0] = t.ld_cg(__ldg(cp)); return apply_op<RS_OP_BITS, 1>(x, pw);
+    case RS_OP_EQ: x[0] = L(__ldg(cp)); x[1] = L(__ldg(cp + 1)); return apply_op<RS_OP_EQ, 2>(x, pw);
+    case RS_OP_LT: x[0] = L(__ldg(cp)); x[1] = L(__ldg(cp + 1)); return apply_op<RS_OP_LT, 2>(x, pw);
+    case RS_OP_CAT: x[0] = L(__ldg(cp)); x[1] = L(__ldg(cp + 1)); return apply_op<RS_OP_CAT, 2>(x, pw);
+    case RS_OP_NOT: x[0] = L(__ldg(cp)); return apply_op<RS_OP_NOT, 1>(x, pw);
+    case RS_OP_SHL: x[0] = L(__ldg(cp)); return apply_op<RS_OP_SHL, 1>(x, pw);
+    case RS_OP_SHR: x[0] = L(__ldg(cp)); return apply_op<RS_OP_SHR, 1>(x, pw);
+    case RS_OP_BITS: x[0] = L(__ldg(cp)); return apply_op<RS_OP_BITS, 1>(x, pw);
     case RS_OP_MUX:
-      x[0] = t.ld_cg(__ldg(cp)); x[1] = t.ld_cg(__ldg(cp + 1)); x[2] = t.ld_cg(__ldg(cp + 2));
+      x[0] = L(__ldg(cp)); x[1] = L(__ldg(cp + 1)); x[2] = L(__ldg(cp + 2));
       return apply_op<RS_OP_MUX, 3>(x, pw);
-    default: x[0] = t.ld_cg(__ldg(cp)); return apply_op<OP_COPY, 1>(x, pw);
+    default: x[0] = L(__ldg(cp)); return apply_op<OP_COPY, 1>(x, pw);
   }
 }
 

@@ -1,0 +1,262 @@
+// repcut.cuh -- replicated-cut single-lane kernel (k_repcut; rs_lane_opts.repcut).
+//
+// The RepCut cascade (App. C, Cascade 2 P:2021-2078; SURVEY.md §8(f)
+// NEXT-2): partition p = CTA p of a cooperative launch owns a block of the
+// registers and evaluates the combinational cone of their next values
+// (compiler.hpp build_repcut: shared logic replicated) on its OWN state
+// replica, so the levels of a cycle need only CTA barriers -- no grid barrier
+// per level as in single.cuh.  After the register commit, the Register Update
+// Map (Cascade 2's last Einsum, LI_{c+1} = LI_{c,I} . RUM) pushes every
+// register's new value into the replicas of the partitions that read it, with
+// one grid barrier on each side of the push.  Hash terms (reading R12) are
+// added by the one partition that owns each op (inputs: partition 0).
+#pragma once
+#include "kernels.cuh"
+
+namespace rtlsim {
+
+struct RepArgs {
+  StepArgs a;
+  const uint32_t* lvl_begin;   // [P][n_levels + 1]
+  const uint32_t* ops;         // op index | owned << 31
+  const uint32_t* reg_begin;   // [P + 1]
+  const uint32_t* regs;
+  const uint32_t* push_begin;  // [P + 1]
+  const uint32_t* push;        // (register, reader partition) pairs
+};
+
+template <bool HASH>
+__global__ void __launch_bounds__(1024, 1) k_repcut(const RepArgs ra) {
+  const StepArgs& a = ra.a;
+  __shared__ uint64_t wsum[32];
+  const uint32_t p = blockIdx.x, tid = threadIdx.x, T = blockDim.x, NL = a.g.n_levels;
+  const TileP<1> t = tile_ptrs<1>(a, p, 0);  // this partition's replica (replica p = tile p)
+  const uint32_t* lb = ra.lvl_begin + (size_t)p * (NL + 1);
+  unsigned long long target = 0;
+#pragma unroll 1
+  for (uint32_t cyc = 0; cyc < a.n_cycles; ++cyc) {
+    const uint64_t cycle = a.cycle0 + cyc;
+    uint64_t hacc = 0;
+    // input injection into every replica (partition 0 hashes the inputs)
+#pragma unroll 1
+    for (uint32_t k = tid; k < a.g.n_inputs; k += T) {
+      uint64_t v = a.staged ? __ldg(a.stage + (size_t)(cycle % a.stage_cap) * a.g.n_inputs + k)
+                            : d_stimulus(a.seed, k, cycle, a.lane0);
+      v &= wmask(__ldg(a.g.in_w + k));
+      t.stc(__ldg(a.g.in_coord + k), v);
+      if (HASH && p == 0) hacc += v * __ldg(a.g.in_k + k);
+    }
+    __syncthreads();
+    // the partition's cone, level by level, CTA barriers only
+#pragma unroll 1
+    for (uint32_t l = 0; l < NL; ++l) {
+#pragma unroll 1
+      for (uint32_t i = lb[l] + tid; i < lb[l + 1]; i += T) {
+        const uint32_t e = __ldg(ra.ops + i), j = e & 0x7FFFFFFFu;
+        const uint64_t y = single_op<false>(a, t, j);
+        t.stc(__ldg(a.g.out_coord + j), y);
+        if (HASH && (e >> 31)) hacc += y * __ldg(a.g.opk + j);
+      }
+      __syncthreads();
+    }
+    // commit of the partition's registers (their pre-commit values are this cycle's hash terms)
+#pragma unroll 1
+    for (uint32_t k = ra.reg_begin[p] + tid; k < ra.reg_begin[p + 1]; k += T) {
+      const uint32_t r = __ldg(ra.regs + k), rc = __ldg(a.g.reg_coord + r);
+      if (HASH) hacc += t.ld(rc) * __ldg(a.g.reg_k + r);
+      t.stc(rc, t.ld(__ldg(a.g.reg_next_coord + r)) & wmask(__ldg(a.g.reg_w + r)));
+    }
+    if (HASH) {
+      const uint64_t s = block_sum(hacc, wsum) + (p == 0 ? a.g.const_hash : 0ull);
+      if (tid == 0 && a.hashes) atomicAdd((unsigned long long*)(a.hashes + cyc), (unsigned long long)s);
+    }
+    grid_barrier(a.bar, target);  // every partition has finished reading this cycle's register values
+    // Register Update Map: new register values into the replicas that read them
+#pragma unroll 1
+    for (uint32_t k = ra.push_begin[p] + tid; k < ra.push_begin[p + 1]; k += T) {
+      const uint32_t r = __ldg(ra.push + 2 * k), q = __ldg(ra.push + 2 * k + 1), rc = __ldg(a.g.reg_coord + r);
+      tile_ptrs<1>(a, q, 0).stc(rc, t.ld(rc));
+    }
+    grid_barrier(a.bar, target);  // pushes visible before the next cycle's reads
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_repcut_smem: the same cascade with each partition's working set resident
+// in its SM (compiler.hpp RepSliceHdr): the op descriptors and a compact local
+// copy of the signals it touches live in shared memory for the whole launch,
+// so a level is shared-memory loads + ALU + one CTA barrier.  Registers cross
+// partitions through a global mailbox indexed by register (double-buffered by
+// cycle parity): owners post at the commit, readers pull after the single
+// grid barrier of the cycle -- the Register Update Map as a pull.  The local
+// state is loaded from / written back to replica p at launch start / end, so
+// read-back, checkpoint and the aux kernels see the usual replicas.
+struct RepSmemArgs {
+  StepArgs a;
+  const uint8_t* blob;
+  const uint64_t* slice_off;
+  const uint64_t* op_k;   // per-partition op hash weights in slice op order (0: not owned)
+  uint64_t* mail;         // [2][n_regs]
+};
+
+struct LocalState {
+  uint8_t* s;
+  uint32_t b1, b2, b3;
+  __device__ __forceinline__ uint32_t cls(uint32_t o) const { return o < b1 ? 3u : o < b2 ? 2u : o < b3 ? 1u : 0u; }
+  // branch-free gather: the aligned 64-bit word holding the value, shifted and masked
+  __device__ __forceinline__ uint64_t ld(uint32_t o) const {
+    const uint64_t w = *reinterpret_cast<const uint64_t*>(s + (o & ~7u));
+    const uint32_t c = cls(o);
+    const uint64_t v = w >> ((o & 7u) * 8u);
+    return c == 3u ? w : (v & (0xFFFFFFFFull >> (32u - (8u << c))));
+  }
+  __device__ __forceinline__ void st(uint32_t o, uint64_t v) const {
+    switch (cls(o)) {
+      case 0: s[o] = (uint8_t)v; break;
+      case 1: *reinterpret_cast<uint16_t*>(s + o) = (uint16_t)v; break;
+      case 2: *reinterpret_cast<uint32_t*>(s + o) = (uint32_t)v; break;
+      default: *reinterpret_cast<uint64_t*>(s + o) = v; break;
+    }
+  }
+};
+
+__device__ __forceinline__ uint64_t rep_eval(const LocalState& S, uint32_t pw, uint2 cw, const uint16_t* ovf) {
+  const uint32_t op = (pw >> 22) & 15u, n = pw >> 26, p0 = (pw >> 7) & 127u;
+  const uint32_t c0 = cw.x >> 16, c1 = cw.y & 0xFFFFu, c2 = n > 3 ? c0 : cw.y >> 16;
+  const uint64_t x0 = S.ld(c0), x1 = S.ld(c1), x2 = S.ld(c2);
+  uint64_t r;
+  switch (op) {
+    case RS_OP_AND: r = x0 & x1; if (n == 3) r &= x2; break;
+    case RS_OP_OR: r = x0 | x1; if (n == 3) r |= x2; break;
+    case RS_OP_XOR: r = x0 ^ x1; if (n == 3) r ^= x2; break;
+    case RS_OP_ADD: r = x0 + x1; if (n == 3) r += x2; break;
+    case RS_OP_SUB: r = x0 - x1; if (n == 3) r -= x2; break;
+    case RS_OP_MUL: r = x0 * x1; if (n == 3) r *= x2; break;
+    case RS_OP_EQ: r = x0 == x1 ? 1ull : 0ull; break;
+    case RS_OP_LT: r = x0 < x1 ? 1ull : 0ull; break;
+    case RS_OP_NOT: r = ~x0; break;
+    case RS_OP_SHL: r = p0 >= 64 ? 0ull : (x0 << p0); break;
+    case RS_OP_SHR: r = p0 >= 64 ? 0ull : (x0 >> p0); break;
+    case RS_OP_BITS: {
+      const uint32_t lo = (pw >> 14) & 63u;
+      r = (x0 >> lo) & wmask(p0 - lo + 1u);
+      break;
+    }
+    case RS_OP_CAT: r = p0 >= 64 ? x1 : ((x0 << p0) | x1); break;
+    case RS_OP_MUX: r = x0 != 0 ? x1 : x2; break;
+    default: r = x0; break;  // OP_COPY
+  }
+  if (n > 3 && op <= RS_OP_MUL)  // rare long folds: operands 2.. in the overflow list
+    for (uint32_t o = 2; o < n; ++o) r = fold_step(op, r, S.ld(ovf[(cw.y >> 16) + o - 2]));
+  return r & wmask(pw & 127u);
+}
+
+template <bool HASH>
+__global__ void __launch_bounds__(1024, 1) k_repcut_smem(const RepSmemArgs ra) {
+  const StepArgs& a = ra.a;
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint64_t wsum[32];
+  const uint32_t p = blockIdx.x, tid = threadIdx.x, T = blockDim.x, R = a.g.n_regs;
+  const uint8_t* src = ra.blob + ra.slice_off[p];
+  {
+    const uint32_t sb = reinterpret_cast<const RepSliceHdr*>(src)->smem_bytes;
+    for (uint32_t i = tid * 16; i < sb; i += T * 16)
+      *reinterpret_cast<uint4*>(smem + i) = __ldg(reinterpret_cast<const uint4*>(src + i));
+  }
+  __syncthreads();
+  const RepSliceHdr& h = *reinterpret_cast<const RepSliceHdr*>(smem);
+  const uint32_t* lvl = reinterpret_cast<const uint32_t*>(smem + h.off_lvl);
+  const uint32_t* pws = reinterpret_cast<const uint32_t*>(smem + h.off_pw);
+  const uint2* cws = reinterpret_cast<const uint2*>(smem + h.off_cw);
+  const uint16_t* ovf = reinterpret_cast<const uint16_t*>(smem + h.off_ovf);
+  const uint32_t* com = reinterpret_cast<const uint32_t*>(smem + h.off_commit);
+  const uint32_t* pul = reinterpret_cast<const uint32_t*>(smem + h.off_pull);
+  const uint32_t* inj = reinterpret_cast<const uint32_t*>(smem + h.off_inj);
+  const uint32_t* map = reinterpret_cast<const uint32_t*>(src + h.off_map);
+  const uint64_t* opk = ra.op_k + h.k_base;
+  LocalState S{smem + h.state_off, h.b1, h.b2, h.b3};
+  const TileP<1> t = tile_ptrs<1>(a, p, 0);
+  for (uint32_t i = tid; i < h.n_map; i += T) S.st(map[2 * i], t.ld(map[2 * i + 1]));
+  if (a.n_cycles == 0) return;
+  const uint32_t NL = h.n_levels;
+  // hash weights are software-pipelined one level ahead (an exposed L2 load per
+  // level would dominate a level of shared-memory work); the registers' once
+  auto kload = [&](uint32_t l) -> uint64_t {
+    if (!HASH) return 0ull;
+    const uint32_t i = lvl[l] + tid;
+    return i < lvl[l + 1] ? __ldg(opk + i) : 0ull;
+  };
+  const uint64_t kreg = (HASH && tid < h.n_commit) ? __ldg(a.g.reg_k + (com[2 * tid + 1] & 0xFFFFFFu)) : 0ull;
+  unsigned long long target = 0;
+  uint64_t hacc = 0;
+  __syncthreads();
+#pragma unroll 1
+  for (uint32_t cyc = 0; cyc < a.n_cycles; ++cyc) {
+    const uint64_t cycle = a.cycle0 + cyc;
+    uint64_t knext = NL ? kload(0) : 0ull;
+#pragma unroll 1
+    for (uint32_t i = tid; i < h.n_inj; i += T) {
+      const uint32_t e = inj[2 * i], k = inj[2 * i + 1];
+      uint64_t v = a.staged ? __ldg(a.stage + (size_t)(cycle % a.stage_cap) * a.g.n_inputs + k)
+                            : d_stimulus(a.seed, k, cycle, a.lane0);
+      v &= wmask((e >> 16) & 127u);
+      S.st(e & 0xFFFFu, v);
+      if (HASH && (e >> 23)) hacc += v * __ldg(a.g.in_k + k);
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (uint32_t l = 0; l < NL; ++l) {
+      const uint32_t b = lvl[l], e = lvl[l + 1];
+      const uint64_t kcur = knext;
+      if (l + 1 < NL) knext = kload(l + 1);
+#pragma unroll 1
+      for (uint32_t i = b + tid; i < e; i += T) {
+        const uint32_t pw = pws[i];
+        const uint2 cw = cws[i];
+        const uint64_t y = rep_eval(S, pw, cw, ovf);
+        S.st(cw.x & 0xFFFFu, y);
+        if (HASH) hacc += y * (i == b + tid ? kcur : __ldg(opk + i));
+      }
+      __syncthreads();
+#ifdef RS_TRACE
+      if (p == 0 && tid == 0 && a.trace && cyc < 8 && l < 60) a.trace[cyc * 64 + l] = clock64();
+#endif
+    }
+    // commit: the pre-commit values are this cycle's register hash terms
+    uint64_t* mail = ra.mail + (size_t)(cyc & 1u) * R;
+#pragma unroll 1
+    for (uint32_t i = tid; i < h.n_commit; i += T) {
+      const uint32_t e = com[2 * i], rw = com[2 * i + 1], r = rw & 0xFFFFFFu;
+      const uint64_t nv = S.ld(e >> 16) & wmask(rw >> 24);
+      if (HASH) hacc += S.ld(e & 0xFFFFu) * (i == tid ? kreg : __ldg(a.g.reg_k + r));
+      S.st(e & 0xFFFFu, nv);
+      mail[r] = nv;
+    }
+    if (HASH) {
+      const uint64_t s = block_sum(hacc, wsum) + (p == 0 ? a.g.const_hash : 0ull);
+      if (tid == 0 && a.hashes) atomicAdd((unsigned long long*)(a.hashes + cyc), (unsigned long long)s);
+      hacc = 0;
+    }
+#ifdef RS_TRACE
+    if (p == 0 && tid == 0 && a.trace && cyc < 8) a.trace[cyc * 64 + 60] = clock64();
+#endif
+    grid_barrier(a.bar, target);
+#ifdef RS_TRACE
+    if (p == 0 && tid == 0 && a.trace && cyc < 8) a.trace[cyc * 64 + 61] = clock64();
+#endif
+    // Register Update Map: pull the new values of the registers this partition reads
+#pragma unroll 1
+    for (uint32_t i = tid; i < h.n_pull; i += T) S.st(pul[2 * i], __ldcg(mail + pul[2 * i + 1]));
+#ifdef RS_TRACE
+    __syncthreads();
+    if (p == 0 && tid == 0 && a.trace && cyc < 8) a.trace[cyc * 64 + 62] = clock64();
+#endif
+  }
+  __syncthreads();
+  for (uint32_t i = tid; i < h.n_map; i += T) {
+    const uint32_t c = map[2 * i + 1];
+    t.stc(c, S.ld(map[2 * i]));
+  }
+}
+
+}  // namespace rtlsim

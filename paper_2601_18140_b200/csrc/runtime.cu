@@ -17,6 +17,7 @@
 #include "lanes.cuh"
 #include "lanes_t.cuh"
 #include "single.cuh"
+#include "repcut.cuh"
 
 using namespace rtlsim;
 
@@ -107,6 +108,14 @@ struct rs_lanes {
   bool tail_global = false;
   std::vector<uint8_t> sig_part;         // canonical id -> partition whose replica holds it
   size_t total_bytes = 0;
+  // RepCut (rs_lane_opts.repcut): device plan arrays
+  bool repcut = false;
+  void* drep = nullptr;
+  RepArgs rep{};
+  bool rep_smem = false;      // k_repcut_smem (partition-local shared-memory slices)
+  void* rep_mail = nullptr;   // [2][n_regs] register mailbox
+  RepSmemArgs reps{};
+  uint32_t rep_smem_bytes = 0;
   size_t sched_bytes = 0;                // device bytes of the bound stage schedule
   // waveform capture (rs_watch)
   std::vector<uint32_t> watch;           // canonical ids
@@ -410,6 +419,17 @@ rs_status rs_graph_export(const rs_graph* g, uint32_t what, void* out, uint64_t*
   return RS_OK;
 }
 
+rs_status rs_repcut_stats(const rs_graph* g, uint32_t P, uint64_t* ops_total, uint32_t* max_ops, uint64_t* push) {
+  if (!g) return set_err(RS_E_INVALID_ARG, "NULL graph");
+  RepCutPlan plan;
+  std::string err;
+  if (!build_repcut(g->cg, P, &plan, &err)) return set_err(RS_E_INVALID_ARG, "%s", err.c_str());
+  if (ops_total) *ops_total = plan.ops_total;
+  if (max_ops) *max_ops = plan.max_ops;
+  if (push) *push = plan.push.size() / 2;
+  return RS_OK;
+}
+
 rs_status rs_level_cut(const rs_graph* g, uint32_t parts, uint32_t* cut) {
   if (!g || !cut) return set_err(RS_E_INVALID_ARG, "NULL argument");
   if (parts == 0 || parts > kMaxParts || parts > std::max<uint32_t>(1, g->cg.n_levels))
@@ -445,7 +465,17 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
   s->g = g;
   s->n_lanes = n_lanes;
   s->lane0 = o.lane0;
-  if (g->cg.mode == RS_MODE_SINGLE) {
+  if (g->cg.mode == RS_MODE_SINGLE && o.repcut > 1) {
+    if (o.parts > 1 || o.repcut > (uint32_t)g->sm_count) {
+      delete s;
+      return set_err(RS_E_INVALID_ARG, "repcut = %u: must be <= %d SMs and not combined with parts", o.repcut,
+                     g->sm_count);
+    }
+    s->LT = 1;
+    s->repcut = true;
+    s->parts = o.repcut;   // one state replica per partition: the aux kernels' replica machinery
+    s->n_tiles = o.repcut;
+  } else if (g->cg.mode == RS_MODE_SINGLE) {
     s->LT = 1;
     s->parts = std::max<uint32_t>(1, o.parts);
     if (s->parts > kMaxParts || s->parts > std::max<uint32_t>(1, g->cg.n_levels)) {
@@ -496,7 +526,96 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     th = std::max<uint32_t>(64, th & ~31u);
     s->threads = th;
   }
-  if (g->cg.mode == RS_MODE_SINGLE) {
+  if (s->repcut) {
+    RepCutPlan plan;
+    std::string err;
+    if (!build_repcut(g->cg, s->parts, &plan, &err)) {
+      delete s;
+      return set_err(RS_E_INVALID_ARG, "%s", err.c_str());
+    }
+    s->threads = o.threads ? o.threads : 1024;
+    s->ctas = s->parts;
+    s->sig_part = plan.sig_owner;
+    std::vector<uint8_t> blob;
+    size_t off = 0, o_lb, o_ops, o_rb, o_regs, o_pb, o_push;
+    std::vector<uint8_t> sblob, in_owner;
+    std::vector<uint64_t> sl_off, op_k;
+    const uint32_t max_smem = 227u * 1024u - 2048u;  // static shared memory of k_repcut_smem
+    if (!o.repcut_global && build_repcut_slices(g->cg, plan, max_smem, &sblob, &sl_off, &op_k, &in_owner, &err)) {
+      s->rep_smem = true;
+      uint32_t max_level = 0;
+      for (uint32_t p = 0; p < s->parts; ++p) {
+        const RepSliceHdr* h = reinterpret_cast<const RepSliceHdr*>(sblob.data() + sl_off[p]);
+        s->rep_smem_bytes = std::max(s->rep_smem_bytes, h->smem_bytes + h->state_bytes);
+        max_level = std::max(max_level, h->max_level);
+      }
+      // one op per thread per level where possible (the hash weights are prefetched for one)
+      if (!o.threads) s->threads = std::min<uint32_t>(1024, std::max<uint32_t>(128, (max_level + 31) / 32 * 32));
+      size_t o_bl;
+      put(blob, off, sblob, &o_bl);
+      size_t o_so, o_k;
+      put(blob, off, sl_off, &o_so);
+      put(blob, off, op_k, &o_k);
+      s->reps.blob = (const uint8_t*)(uintptr_t)o_bl;
+      s->reps.slice_off = (const uint64_t*)(uintptr_t)o_so;
+      s->reps.op_k = (const uint64_t*)(uintptr_t)o_k;
+      // inputs read back from the replica of the partition that injects and hashes them
+      for (uint32_t sg = 0; sg < g->cg.n_signals; ++sg)
+        if (g->cg.sig_kind[sg] == 0) {
+          const uint32_t c = g->cg.sig_coord[sg];
+          for (uint32_t k = 0; k < g->cg.n_inputs; ++k)
+            if (g->cg.in_coord[k] == c) {
+              s->sig_part[sg] = in_owner[k];
+              break;
+            }
+        }
+    }
+    put(blob, off, plan.lvl_begin, &o_lb);
+    put(blob, off, plan.ops, &o_ops);
+    put(blob, off, plan.reg_begin, &o_rb);
+    put(blob, off, plan.regs, &o_regs);
+    put(blob, off, plan.push_begin, &o_pb);
+    put(blob, off, plan.push, &o_push);
+    blob.resize(std::max<size_t>(off, 256));
+    cudaError_t e2 = cudaMalloc(&s->drep, blob.size());
+    if (e2 == cudaSuccess) e2 = cudaMemcpy(s->drep, blob.data(), blob.size(), cudaMemcpyHostToDevice);
+    if (e2 != cudaSuccess) {
+      delete s;
+      return set_err(RS_E_OOM, "repcut plan: %s", cudaGetErrorString(e2));
+    }
+    const uint8_t* b = (const uint8_t*)s->drep;
+    s->rep.lvl_begin = (const uint32_t*)(b + o_lb);
+    s->rep.ops = (const uint32_t*)(b + o_ops);
+    s->rep.reg_begin = (const uint32_t*)(b + o_rb);
+    s->rep.regs = (const uint32_t*)(b + o_regs);
+    s->rep.push_begin = (const uint32_t*)(b + o_pb);
+    s->rep.push = (const uint32_t*)(b + o_push);
+    s->total_bytes += blob.size();
+    if (s->rep_smem) {
+      s->reps.blob = b + (uintptr_t)s->reps.blob;
+      s->reps.slice_off = (const uint64_t*)(b + (uintptr_t)s->reps.slice_off);
+      s->reps.op_k = (const uint64_t*)(b + (uintptr_t)s->reps.op_k);
+      e2 = cudaMalloc(&s->rep_mail, std::max<size_t>(16, 16ull * g->cg.n_regs));
+      if (e2 != cudaSuccess) {
+        cudaFree(s->drep);
+        delete s;
+        return set_err(RS_E_OOM, "repcut mailbox: %s", cudaGetErrorString(e2));
+      }
+      s->reps.mail = (uint64_t*)s->rep_mail;
+      s->total_bytes += 16ull * g->cg.n_regs;
+      e2 = cudaFuncSetAttribute((const void*)k_repcut_smem<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)s->rep_smem_bytes);
+      if (e2 == cudaSuccess)
+        e2 = cudaFuncSetAttribute((const void*)k_repcut_smem<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)s->rep_smem_bytes);
+      if (e2 != cudaSuccess) {
+        cudaFree(s->drep);
+        cudaFree(s->rep_mail);
+        delete s;
+        return set_err(RS_E_CUDA, "repcut smem attribute: %s", cudaGetErrorString(e2));
+      }
+    }
+  } else if (g->cg.mode == RS_MODE_SINGLE) {
     const uint32_t work = std::max<uint32_t>(1, std::max(g->cg.n_inputs, g->cg.n_regs));
     uint32_t maxops = 0;
     for (uint32_t l = 0; l < g->cg.n_levels; ++l)
@@ -668,6 +787,8 @@ void rs_free_lanes(rs_lanes* s) {
   if (s->wave_prev) cudaFree(s->wave_prev);
   if (s->wave_rec) cudaFree(s->wave_rec);
   if (s->wave_count) cudaFree(s->wave_count);
+  if (s->drep) cudaFree(s->drep);
+  if (s->rep_mail) cudaFree(s->rep_mail);
   if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
   if (s->g) s->g->live_lanes--;
   delete s;
@@ -777,7 +898,19 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
     }
     CU(cudaMemsetAsync(s->bar, 0, kBarBytes, s->stream));
     cudaError_t e;
-    if (s->slice_blob) {
+    if (s->repcut && s->rep_smem) {
+      RepSmemArgs ra = s->reps;
+      ra.a = a;
+      void* args[] = {&ra};
+      e = cudaLaunchCooperativeKernel(hash ? (const void*)k_repcut_smem<true> : (const void*)k_repcut_smem<false>,
+                                      s->ctas, s->threads, args, s->rep_smem_bytes, s->stream);
+    } else if (s->repcut) {
+      RepArgs ra = s->rep;
+      ra.a = a;
+      void* args[] = {&ra};
+      e = cudaLaunchCooperativeKernel(hash ? (const void*)k_repcut<true> : (const void*)k_repcut<false>, s->ctas,
+                                      s->threads, args, 0, s->stream);
+    } else if (s->slice_blob) {
       const bool grid = s->ctas > 1;
       const uint32_t smax = (s->slice_max + 127u) & ~127u;
       const uint32_t st_smem =
@@ -1017,7 +1150,11 @@ rs_status rs_wave_read(rs_lanes* s, rs_change* out, uint64_t cap, uint64_t* n_ou
   return RS_OK;
 }
 
-uint32_t rs_lanes_kernel(const rs_lanes* s) { return s ? (s->g->cg.mode == RS_MODE_LANES ? s->variant : 0u) : 0u; }
+uint32_t rs_lanes_kernel(const rs_lanes* s) {
+  if (!s) return 0u;
+  if (s->g->cg.mode == RS_MODE_LANES) return s->variant;
+  return s->repcut ? (s->rep_smem ? 3u : 4u) : 0u;
+}
 
 rs_status rs_launch_shape(const rs_lanes* s, uint32_t* lt, uint32_t* threads, uint32_t* ctas, uint32_t* cluster) {
   if (s && cluster) *cluster = s->cluster;

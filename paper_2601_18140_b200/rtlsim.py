@@ -25,7 +25,7 @@ STATUS = {0: "RS_OK", -1: "RS_E_INVALID_ARG", -2: "RS_E_GRAPH", -3: "RS_E_CAPACI
 EXPORTS = ["rs_version", "rs_last_error", "rs_load_graph", "rs_graph_info_get", "rs_free_graph",
            "rs_alloc_lanes", "rs_free_lanes", "rs_lanes_bytes", "rs_set_input_seed", "rs_set_inputs",
            "rs_step_cycles", "rs_read_signals", "rs_write_registers", "rs_get_cycle", "rs_set_cycle",
-           "rs_launch_count", "rs_launch_shape", "rs_lanes_kernel", "rs_watch", "rs_wave_read", "rs_sync", "rs_graph_export", "rs_debug_trace",
+           "rs_launch_count", "rs_launch_shape", "rs_lanes_kernel", "rs_repcut_stats", "rs_watch", "rs_wave_read", "rs_sync", "rs_graph_export", "rs_debug_trace",
            "rs_level_cut"]
 RS_DEVICE_NONE = -1
 EXPORT = {"runs": (0, np.uint32), "level_run_begin": (1, np.uint32), "level_op_begin": (2, np.uint32),
@@ -65,7 +65,8 @@ class GraphInfo(C.Structure):
 class LaneOpts(C.Structure):
     _fields_ = [("lane0", C.c_uint64), ("lane_tile", C.c_uint32), ("threads", C.c_uint32),
                 ("stage_cycles", C.c_uint32), ("cluster", C.c_uint32), ("stream", C.c_void_p),
-                ("parts", C.c_uint32), ("kernel", C.c_uint32)]
+                ("parts", C.c_uint32), ("kernel", C.c_uint32),
+                ("repcut", C.c_uint32), ("repcut_global", C.c_uint32)]
 
 
 _lib = None
@@ -99,6 +100,7 @@ def lib() -> C.CDLL:
             "rs_set_cycle": (i32, [vp, u64]),
             "rs_launch_count": (u64, [vp]),
             "rs_lanes_kernel": (u32, [vp]),
+            "rs_repcut_stats": (i32, [vp, u32, C.POINTER(u64), C.POINTER(u32), C.POINTER(u64)]),
             "rs_watch": (i32, [vp, vp, u32, u64]),
             "rs_wave_read": (i32, [vp, vp, u64, C.POINTER(u64), C.POINTER(u64)]),
             "rs_launch_shape": (i32, [vp, C.POINTER(u32), C.POINTER(u32), C.POINTER(u32), C.POINTER(u32)]),
@@ -183,6 +185,12 @@ class Graph:
         out = out[:n.value]
         return out.reshape(-1, 5) if what == "runs" else out
 
+    def repcut_stats(self, parts: int) -> dict:
+        """rs_repcut_stats: replication of a parts-way RepCut plan."""
+        t, m, p = C.c_uint64(), C.c_uint32(), C.c_uint64()
+        _check(lib().rs_repcut_stats(self.h, parts, C.byref(t), C.byref(m), C.byref(p)))
+        return {"ops_total": t.value, "max_ops": m.value, "push": p.value}
+
     def level_cut(self, parts: int) -> np.ndarray:
         """rs_level_cut: level boundaries [parts + 1] of a parts-way level cut."""
         out = np.zeros(parts + 1, dtype=np.uint32)
@@ -206,12 +214,13 @@ class Lanes:
     lane0 .. lane0 + n_lanes - 1)."""
 
     def __init__(self, graph: Graph, n_lanes: int, lane0: int = 0, lane_tile: int = 0, threads: int = 0,
-                 stage_cycles: int = 0, stream=None, cluster: int = 0, parts: int = 0, kernel: int = 0):
+                 stage_cycles: int = 0, stream=None, cluster: int = 0, parts: int = 0, kernel: int = 0,
+                 repcut: int = 0, repcut_global: bool = False):
         self.graph = graph
         self.n_lanes = n_lanes
         self.lane0 = lane0
         st = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
-        self.opts = LaneOpts(lane0, lane_tile, threads, stage_cycles, cluster, st, parts, kernel)
+        self.opts = LaneOpts(lane0, lane_tile, threads, stage_cycles, cluster, st, parts, kernel, repcut, int(repcut_global))
         h = C.c_void_p()
         _check(lib().rs_alloc_lanes(graph.h, n_lanes, C.byref(self.opts), C.byref(h)))
         self.h = h

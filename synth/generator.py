@@ -257,3 +257,51 @@ def fuzz_circuit(seed: int) -> Circuit:
                     20_000 + seed, 1, 100, n_consts=int(rng.integers(0, 4)),
                     reg_next_source_p=0.2)
     return generate(cfg, permute=bool(seed % 2))
+
+
+def multicore_circuit(n_cores: int = 16, ops_per_core: int = 12_500, n_levels: int = 60,
+                      regs_per_core: int = 1_250, inputs_per_core: int = 8, cross_p: float = 0.01,
+                      seed: int = 106, base: str = "C3") -> Circuit:
+    """A partition-friendly single-design circuit for the RepCut path (SURVEY.md
+    §8(f) NEXT-2; App. C, Cascade 2): ``n_cores`` independent
+    ``base``-shaped random cores, like the paper's multi-core RocketChip
+    configurations (r1..r24), coupled only through registers: each
+    non-anchor operand is, with probability ``cross_p``, replaced by a register
+    of another core.  Cores are laid out one after the other (their inputs,
+    registers and ops keep per-core contiguous ids), so a register partition by
+    contiguous index ranges follows the cores and needs no op replication."""
+    cfg = CONFIGS[base]
+    parts = [generate(cfg, n_ops=ops_per_core, n_levels=n_levels, n_regs=regs_per_core,
+                      n_inputs=inputs_per_core, seed=seed * 1000 + k) for k in range(n_cores)]
+    off = np.cumsum([0] + [p.n_signals for p in parts])
+    width = np.concatenate([p.width for p in parts])
+    cat = lambda f: np.concatenate([getattr(p, f).astype(np.int64) + off[k] for k, p in enumerate(parts)])
+    input_id, reg_id, reg_next_id = cat("input_id"), cat("reg_id"), cat("reg_next_id")
+    out_id, arg_id = cat("out_id"), cat("arg_id")
+    const_id = cat("const_id") if sum(p.n_consts for p in parts) else np.zeros(0, np.int64)
+    arg_off = np.zeros(1, dtype=np.int64)
+    for p in parts:
+        arg_off = np.concatenate([arg_off, arg_off[-1] + p.arg_off[1:].astype(np.int64)])
+    opcode = np.concatenate([p.opcode for p in parts])
+    param = np.concatenate([p.param for p in parts])
+    level = np.concatenate([p.level for p in parts])
+    rng = np.random.default_rng(seed)
+    # cross-core coupling through registers: operand o >= 1 of an op (never the
+    # anchor, so the levels stay exact) becomes a register of another core
+    core_of_op = np.repeat(np.arange(n_cores), [p.n_ops for p in parts])
+    ar = np.diff(arg_off)
+    pos_in_op = np.arange(arg_id.shape[0]) - np.repeat(arg_off[:-1], ar)
+    anchor = np.where(np.repeat(opcode == MUX, ar), 1, 0)      # per operand: the op's anchor position
+    cand = np.nonzero((pos_in_op != anchor) & (rng.random(arg_id.shape[0]) < cross_p))[0]
+    if n_cores > 1 and cand.size:
+        core = np.repeat(core_of_op, ar)[cand]
+        other = (core + rng.integers(1, n_cores, size=cand.size)) % n_cores
+        pick = rng.integers(0, regs_per_core, size=cand.size)
+        arg_id[cand] = reg_id[other * regs_per_core + pick]
+    return Circuit(
+        width=width.astype(np.uint8), input_id=input_id.astype(np.uint32), reg_id=reg_id.astype(np.uint32),
+        reg_next_id=reg_next_id.astype(np.uint32), reg_init=np.concatenate([p.reg_init for p in parts]),
+        const_id=const_id.astype(np.uint32), const_val=np.concatenate([p.const_val for p in parts]),
+        opcode=opcode, out_id=out_id.astype(np.uint32), arg_off=arg_off.astype(np.uint32),
+        arg_id=arg_id.astype(np.uint32), param=param, level=level, name=f"multicore{n_cores}x{ops_per_core}",
+        meta={"struct_seed": seed, "stim_seed": 206, "lanes": 1, "cycles": 10_000}).normalized()

@@ -261,3 +261,35 @@ def test_vcd_writer_format():
     # change-set semantics: first cycle always, then only differences
     tr = np.array([[[1, 2]], [[1, 3]], [[4, 3]]], dtype=np.uint64)   # [cycle][watch][lane]
     assert changes_from_trace(tr, 10, [0, 1]) == {(10, 0, 0, 1), (10, 1, 0, 2), (11, 1, 0, 3), (12, 0, 0, 4)}
+
+
+def test_repcut_plan_stats(rs):
+    """rs_repcut_stats (App. C, Cascade 2):
+    one partition holds every op once and pushes nothing; a multi-core design
+    with no cross-core edges, cut at its core boundaries, replicates nothing
+    and pushes nothing; coupling through registers adds pushes; replication is
+    bounded by P copies of the graph."""
+    from synth import multicore_circuit
+    c = multicore_circuit(4, 600, 10, 60, 4, cross_p=0.0, seed=5)
+    g = rs.Graph(c, device=rs.RS_DEVICE_NONE, mode="single")
+    n = g.info()
+    total = n["n_ops"] + n["n_copy_ops"]
+    one = g.repcut_stats(1)
+    assert one == {"ops_total": total, "max_ops": total, "push": 0}
+    four = g.repcut_stats(4)
+    assert four["ops_total"] == total and four["push"] == 0
+    assert four["max_ops"] < total
+    two = g.repcut_stats(2)
+    assert two["ops_total"] == total and two["push"] == 0
+    cc = multicore_circuit(4, 600, 10, 60, 4, cross_p=0.02, seed=5)
+    gc = rs.Graph(cc, device=rs.RS_DEVICE_NONE, mode="single")
+    tc = gc.info()["n_ops"] + gc.info()["n_copy_ops"]
+    for P in (2, 3, 4, 7):
+        st = gc.repcut_stats(P)
+        assert tc <= st["ops_total"] <= P * tc
+        assert -(-st["ops_total"] // P) <= st["max_ops"] <= tc
+        assert st["push"] > 0
+    with pytest.raises(rs.RtlSimError):
+        gc.repcut_stats(0)
+    with pytest.raises(rs.RtlSimError):
+        gc.repcut_stats(256)

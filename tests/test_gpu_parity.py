@@ -17,10 +17,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def run_gpu(rs, c, n_cycles, n_lanes=1, seed=0, mode="lanes", lane0=0, lane_tile=0, threads=0,
-            staged=None, chunks=None, final=True, cluster=0, parts=0, kernel=0):
+            staged=None, chunks=None, final=True, cluster=0, parts=0, kernel=0, repcut=0,
+            repcut_global=False):
     g = rs.Graph(c, device=0, mode=mode)
     L = rs.Lanes(g, n_lanes, lane0=lane0, lane_tile=lane_tile, threads=threads, cluster=cluster,
-                 stage_cycles=(n_cycles if staged is not None else 0), parts=parts, kernel=kernel)
+                 stage_cycles=(n_cycles if staged is not None else 0), parts=parts, kernel=kernel,
+                 repcut=repcut, repcut_global=repcut_global)
     if staged is not None:
         L.set_inputs(0, staged)
     else:
