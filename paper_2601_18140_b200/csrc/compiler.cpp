@@ -876,8 +876,21 @@ bool build_repcut_slices(const CompiledGraph& g, const RepCutPlan& plan, uint32_
     uint32_t max_level = 0;
     for (uint32_t l = 0; l <= NL; ++l) lvl[l] = lb[l] - lb[0];
     for (uint32_t l = 0; l < NL; ++l) max_level = std::max(max_level, lb[l + 1] - lb[l]);
-    for (uint32_t x = lb[0]; x < lb[NL]; ++x) {
-      const uint32_t i = x - lb[0], j = plan.ops[x] & 0x7FFFFFFFu;
+    // within a level, ops by (output class, opcode, arity): the warps of a
+    // level then mostly store one width and take one path
+    std::vector<uint32_t> order(lb[NL] - lb[0]);
+    for (uint32_t l = 0; l < NL; ++l) {
+      auto first = order.begin() + (lb[l] - lb[0]), last = order.begin() + (lb[l + 1] - lb[0]);
+      std::iota(first, last, lb[l]);
+      auto key = [&](uint32_t x) {
+        const uint32_t j = plan.ops[x] & 0x7FFFFFFFu;
+        return ((out_coord[j] >> 30) << 16) | (((g.opw[j] >> 22) & 15u) << 8) | (g.opw[j] >> 26);
+      };
+      std::stable_sort(first, last, [&](uint32_t u, uint32_t v) { return key(u) < key(v); });
+    }
+    for (uint32_t x0 = lb[0]; x0 < lb[NL]; ++x0) {
+      const uint32_t x = order[x0 - lb[0]];
+      const uint32_t i = x0 - lb[0], j = plan.ops[x] & 0x7FFFFFFFu;
       const uint32_t n = g.coord_off[j + 1] - g.coord_off[j];
       pw[i] = g.opw[j];
       cw[4 * i] = L(out_coord[j]);

@@ -110,44 +110,52 @@ struct LocalState {
     const uint64_t v = w >> ((o & 7u) * 8u);
     return c == 3u ? w : (v & (0xFFFFFFFFull >> (32u - (8u << c))));
   }
+  // branch-free store: four predicated st.shared (a switch compiles to an
+  // indirect branch, which splits warps whose ops write several widths)
   __device__ __forceinline__ void st(uint32_t o, uint64_t v) const {
-    switch (cls(o)) {
-      case 0: s[o] = (uint8_t)v; break;
-      case 1: *reinterpret_cast<uint16_t*>(s + o) = (uint16_t)v; break;
-      case 2: *reinterpret_cast<uint32_t*>(s + o) = (uint32_t)v; break;
-      default: *reinterpret_cast<uint64_t*>(s + o) = v; break;
-    }
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(s + o), c = cls(o);
+    asm volatile(
+        "{\n\t.reg .pred q0, q1, q2, q3;\n\t"
+        "setp.eq.u32 q0, %2, 0;\n\tsetp.eq.u32 q1, %2, 1;\n\tsetp.eq.u32 q2, %2, 2;\n\tsetp.eq.u32 q3, %2, 3;\n\t"
+        "@q0 st.shared.u8 [%0], %1;\n\t@q1 st.shared.u16 [%0], %1;\n\t"
+        "@q2 st.shared.u32 [%0], %1;\n\t@q3 st.shared.u64 [%0], %1;\n\t}"
+        :: "r"(a), "l"(v), "r"(c) : "memory");
   }
 };
 
+// One op, branch-free: a partition's level mixes many opcodes (its ops are a
+// sparse subset of the level's runs), and a switch compiles to an indirect
+// branch that splits a warp into serialized paths (measured: 2240 vs 1186
+// cycles per level on the 16-core design); every candidate result is computed
+// instead (a few dozen ALU instructions) and the op's one is picked by a
+// selection tree on the opcode bits (depth 4; a 14-deep select chain: 1275).
 __device__ __forceinline__ uint64_t rep_eval(const LocalState& S, uint32_t pw, uint2 cw, const uint16_t* ovf) {
   const uint32_t op = (pw >> 22) & 15u, n = pw >> 26, p0 = (pw >> 7) & 127u;
   const uint32_t c0 = cw.x >> 16, c1 = cw.y & 0xFFFFu, c2 = n > 3 ? c0 : cw.y >> 16;
   const uint64_t x0 = S.ld(c0), x1 = S.ld(c1), x2 = S.ld(c2);
+  const bool three = n == 3;
+  const uint64_t z = three ? x2 : 0ull;
+  const uint32_t sh = p0 >= 64 ? 63u : p0;
+  const uint64_t shl = p0 >= 64 ? 0ull : (x0 << sh), shr = p0 >= 64 ? 0ull : (x0 >> sh);
+  const uint32_t lo = (pw >> 14) & 63u;
   uint64_t r;
-  switch (op) {
-    case RS_OP_AND: r = x0 & x1; if (n == 3) r &= x2; break;
-    case RS_OP_OR: r = x0 | x1; if (n == 3) r |= x2; break;
-    case RS_OP_XOR: r = x0 ^ x1; if (n == 3) r ^= x2; break;
-    case RS_OP_ADD: r = x0 + x1; if (n == 3) r += x2; break;
-    case RS_OP_SUB: r = x0 - x1; if (n == 3) r -= x2; break;
-    case RS_OP_MUL: r = x0 * x1; if (n == 3) r *= x2; break;
-    case RS_OP_EQ: r = x0 == x1 ? 1ull : 0ull; break;
-    case RS_OP_LT: r = x0 < x1 ? 1ull : 0ull; break;
-    case RS_OP_NOT: r = ~x0; break;
-    case RS_OP_SHL: r = p0 >= 64 ? 0ull : (x0 << p0); break;
-    case RS_OP_SHR: r = p0 >= 64 ? 0ull : (x0 >> p0); break;
-    case RS_OP_BITS: {
-      const uint32_t lo = (pw >> 14) & 63u;
-      r = (x0 >> lo) & wmask(p0 - lo + 1u);
-      break;
-    }
-    case RS_OP_CAT: r = p0 >= 64 ? x1 : ((x0 << p0) | x1); break;
-    case RS_OP_MUX: r = x0 != 0 ? x1 : x2; break;
-    default: r = x0; break;  // OP_COPY
+  {  // selection tree on the opcode bits (depth 4 instead of a 14-deep chain)
+    const uint64_t a0 = x0 & x1 & (three ? x2 : ~0ull), a1 = x0 | x1 | z, a2 = x0 ^ x1 ^ z, a3 = ~x0;
+    const uint64_t a4 = x0 + x1 + z, a5 = x0 - x1 - z, a6 = x0 * x1 * (three ? x2 : 1ull);
+    const uint64_t a7 = (uint64_t)(x0 == x1), a8 = (uint64_t)(x0 < x1), a9 = shl, a10 = shr;
+    const uint64_t a11 = (x0 >> lo) & wmask(p0 - lo + 1u), a12 = p0 >= 64 ? x1 : (shl | x1);
+    const uint64_t a13 = x0 != 0 ? x1 : x2, a14 = x0;
+    const bool b0 = op & 1u, b1 = op & 2u, b2 = op & 4u, b3 = op & 8u;
+    const uint64_t s01 = b0 ? a1 : a0, s23 = b0 ? a3 : a2, s45 = b0 ? a5 : a4, s67 = b0 ? a7 : a6;
+    const uint64_t s89 = b0 ? a9 : a8, sab = b0 ? a11 : a10, scd = b0 ? a13 : a12, sef = a14;
+    const uint64_t t0 = b1 ? s23 : s01, t1 = b1 ? s67 : s45, t2 = b1 ? sab : s89, t3 = b1 ? sef : scd;
+    const uint64_t u0 = b2 ? t1 : t0, u1 = b2 ? t3 : t2;
+    r = b3 ? u1 : u0;
   }
-  if (n > 3 && op <= RS_OP_MUL)  // rare long folds: operands 2.. in the overflow list
+  if (n > 3) {  // rare long folds (op <= RS_OP_MUL): operands 2.. in the overflow list
+    r = fold_step(op, x0, x1);
     for (uint32_t o = 2; o < n; ++o) r = fold_step(op, r, S.ld(ovf[(cw.y >> 16) + o - 2]));
+  }
   return r & wmask(pw & 127u);
 }
 
@@ -204,9 +212,10 @@ __global__ void __launch_bounds__(1024, 1) k_repcut_smem(const RepSmemArgs ra) {
       if (HASH && (e >> 23)) hacc += v * __ldg(a.g.in_k + k);
     }
     __syncthreads();
+    uint32_t b = NL ? lvl[0] : 0u, e = NL ? lvl[1] : 0u;  // level bounds, loaded a level ahead
 #pragma unroll 1
     for (uint32_t l = 0; l < NL; ++l) {
-      const uint32_t b = lvl[l], e = lvl[l + 1];
+      const uint32_t en = lvl[l + 2 <= NL ? l + 2 : NL];
       const uint64_t kcur = knext;
       if (l + 1 < NL) knext = kload(l + 1);
 #pragma unroll 1
@@ -221,6 +230,8 @@ __global__ void __launch_bounds__(1024, 1) k_repcut_smem(const RepSmemArgs ra) {
 #ifdef RS_TRACE
       if (p == 0 && tid == 0 && a.trace && cyc < 8 && l < 60) a.trace[cyc * 64 + l] = clock64();
 #endif
+      b = e;
+      e = en;
     }
     // commit: the pre-commit values are this cycle's register hash terms
     uint64_t* mail = ra.mail + (size_t)(cyc & 1u) * R;
