@@ -160,7 +160,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5", "MC16"],
+                    help="BASELINE configs; MC16 = synth.multicore_circuit() (16 cores x 12.5k ops, the RepCut "
+                         "workload of SURVEY.md §8(f) NEXT-2)")
     ap.add_argument("--cycles", type=int, default=0, help="cycles per step (default: the config's)")
     ap.add_argument("--lanes", type=int, default=0, help="lanes per GPU (default: the config's)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -172,13 +174,20 @@ def main():
     ap.add_argument("--cluster", type=int, default=0)
     ap.add_argument("--kernel", type=int, default=0, help="lane kernel: 0 auto, 1 lane/thread, 2 two lanes/thread")
     ap.add_argument("--parts", type=int, default=0, help="C1/C5: level-cut partitions emulated on this GPU")
+    ap.add_argument("--repcut", type=int, default=0, help="single-lane configs: RepCut partitions (rs_lane_opts.repcut)")
     ap.add_argument("--ref-step-s", type=float, default=4.0)
     ap.add_argument("--watch", type=int, default=0, help="waveform capture of N signals during the timed steps")
     args = ap.parse_args()
 
-    from synth import CONFIGS, config_circuit
-    cfg = CONFIGS[args.config]
-    circ = config_circuit(args.config)
+    from synth import CONFIGS, config_circuit, multicore_circuit
+    if args.config == "MC16":
+        import types
+        circ = multicore_circuit()
+        cfg = types.SimpleNamespace(name="MC16", lanes=1, cycles=2000, stim_seed=circ.meta["stim_seed"],
+                                    n_levels=60)
+    else:
+        cfg = CONFIGS[args.config]
+        circ = config_circuit(args.config)
     if args.impl == "reference":
         return run_reference(args, cfg, circ)
 
@@ -195,7 +204,7 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    single = args.config in ("C1", "C5")
+    single = args.config in ("C1", "C5", "MC16")
     lanes = args.lanes or cfg.lanes
     if single:
         lanes = 1
@@ -205,7 +214,7 @@ def main():
     g = rs.Graph(circ, device=local, mode="single" if single else "lanes")
     info = g.info()
     L = rs.Lanes(g, lanes, lane0=shard.lane0, lane_tile=args.lane_tile, threads=args.threads, stream=stream,
-                 cluster=args.cluster, parts=args.parts, kernel=args.kernel)
+                 cluster=args.cluster, parts=args.parts, kernel=args.kernel, repcut=args.repcut)
     L.set_seed(cfg.stim_seed)
     if args.watch:
         wids = np.linspace(0, circ.n_signals - 1, args.watch).astype(np.uint32)
@@ -244,6 +253,8 @@ def main():
     lane_cycles = lanes * world * cycles * args.steps
     value = lane_cycles / (total_ms / 1e3)
 
+    kid = L.shape()["kernel"]
+    kernel_name = {1: "k_lanes_t", 2: "k_lanes", 3: "k_repcut_smem", 4: "k_repcut"}.get(kid, "k_single")
     # roofline of the dominant (only) kernel: algorithmic bytes per launch / launch duration
     bytes_per_cycle = lanes * info["alg_bytes_per_lane_cycle"] + info["graph_alg_bytes"]
     alg_bytes = bytes_per_cycle * cycles
@@ -262,7 +273,8 @@ def main():
     if not args.no_e2e:
         chunk = min(cycles, max(1, (256 << 20) // max(1, 8 * circ.n_inputs * lanes)))
         Ls = rs.Lanes(g, lanes, lane0=shard.lane0, lane_tile=args.lane_tile, threads=args.threads, cluster=args.cluster,
-                      stage_cycles=chunk, stream=stream, parts=args.parts, kernel=args.kernel)
+                      stage_cycles=chunk, stream=stream, parts=args.parts, kernel=args.kernel,
+                      repcut=args.repcut)
         rng = np.random.default_rng(rank)
         host_in = torch.from_numpy(rng.integers(0, 2**63, size=(chunk, circ.n_inputs, lanes),
                                                 dtype=np.int64)).pin_memory()
@@ -313,6 +325,7 @@ def main():
                        "l2": "flushed (256 MB write) before every timed step",
                        "mode": "single" if single else "lanes", "launch": L.shape(),
                        **({"level_cut_parts": args.parts} if args.parts > 1 else {}),
+                       **({"repcut_partitions": args.repcut} if args.repcut > 1 else {}),
                        "state_bytes_per_gpu": info["state_bytes_per_lane"] * lanes,
                        **({"watched_signals": args.watch} if args.watch else {})},
             "op_evals_per_s": value * circ.n_ops,
@@ -320,7 +333,7 @@ def main():
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "alg_bytes_per_launch": alg_bytes,
                          "alg_bytes_per_lane_cycle": info["alg_bytes_per_lane_cycle"],
-                         "kernel": "k_lanes" if not single else "k_single"},
+                         "kernel": kernel_name},
             "clocks": clk.summary(),
             "gpu_launches": launches,
             "step_ms": step_ms,

@@ -914,6 +914,8 @@ bool build_repcut_slices(const CompiledGraph& g, const RepCutPlan& plan, uint32_
       const uint32_t r = plan.regs[k];
       commit.push_back(L(g.reg_coord[r]) | ((uint32_t)L(g.reg_next_coord[r]) << 16));
       commit.push_back(r | (g.reg_w[r] << 24));
+      commit.push_back((uint32_t)g.reg_k[r]);
+      commit.push_back((uint32_t)(g.reg_k[r] >> 32));
     }
     for (uint32_t c : sigs) {
       auto it = reg_of_coord.find(c);
@@ -929,8 +931,11 @@ bool build_repcut_slices(const CompiledGraph& g, const RepCutPlan& plan, uint32_
     }
     for (uint32_t k = 0; k < NI; ++k)
       if (reads_in[p][k] || (*in_owner)[k] == p) {
-        inj.push_back(L(g.in_coord[k]) | (g.in_w[k] << 16) | ((uint32_t)((*in_owner)[k] == p) << 23));
+        const bool own = (*in_owner)[k] == p;
+        inj.push_back(L(g.in_coord[k]) | (g.in_w[k] << 16));
         inj.push_back(k);
+        inj.push_back(own ? (uint32_t)g.in_k[k] : 0u);
+        inj.push_back(own ? (uint32_t)(g.in_k[k] >> 32) : 0u);
       }
     RepSliceHdr h{};
     size_t o = align16(sizeof(RepSliceHdr));
@@ -941,14 +946,20 @@ bool build_repcut_slices(const CompiledGraph& g, const RepCutPlan& plan, uint32_
     h.off_commit = (uint32_t)o; o = align16(o + commit.size() * 4);
     h.off_pull = (uint32_t)o; o = align16(o + pull.size() * 4);
     h.off_inj = (uint32_t)o; o = align16(o + inj.size() * 4);
+    // the op hash weights join the slice when they fit (else read from global memory)
+    h.off_kop = (uint32_t)o;
+    if (o + (size_t)n_ops * 8 + state_bytes <= max_smem) {
+      h.kop_smem = 1;
+      o = align16(o + (size_t)n_ops * 8);
+    }
     h.smem_bytes = (uint32_t)o;
     h.state_off = (uint32_t)o;
     h.state_bytes = state_bytes;
     h.off_map = (uint32_t)o; o = align16(o + map.size() * 4);
     h.b1 = bnd[2]; h.b2 = bnd[1]; h.b3 = bnd[0];
     h.n_levels = NL; h.n_ops = n_ops; h.max_level = max_level;
-    h.n_commit = (uint32_t)commit.size() / 2; h.n_pull = (uint32_t)pull.size() / 2;
-    h.n_inj = (uint32_t)inj.size() / 2; h.n_map = (uint32_t)map.size() / 2;
+    h.n_commit = (uint32_t)commit.size() / 4; h.n_pull = (uint32_t)pull.size() / 2;
+    h.n_inj = (uint32_t)inj.size() / 4; h.n_map = (uint32_t)map.size() / 2;
     h.k_base = (uint32_t)(op_k->size() - n_ops);
     if ((size_t)h.smem_bytes + state_bytes > max_smem) {
       *err = "repcut slice " + std::to_string(p) + ": " + std::to_string(h.smem_bytes + state_bytes) +
@@ -968,6 +979,7 @@ bool build_repcut_slices(const CompiledGraph& g, const RepCutPlan& plan, uint32_
     cp(h.off_commit, commit.data(), commit.size() * 4);
     cp(h.off_pull, pull.data(), pull.size() * 4);
     cp(h.off_inj, inj.data(), inj.size() * 4);
+    if (h.kop_smem) cp(h.off_kop, op_k->data() + h.k_base, (size_t)n_ops * 8);
     cp(h.off_map, map.data(), map.size() * 4);
   }
   return true;

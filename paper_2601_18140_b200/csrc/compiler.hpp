@@ -247,9 +247,11 @@ bool build_repcut(const CompiledGraph& g, uint32_t P, RepCutPlan* out, std::stri
 // (16-byte aligned sections, offsets relative to the slice; the smem part is
 // [0, smem_bytes), the map is read from global memory at launch start / end):
 //   lvl u32[n_levels + 1] | pw u32[ops] | cw u16x4[ops] {out, c0, c1, c2 | ovf index}
-//   | ovf u16[...] (operands 2.. of ops with arity > 3) | commit u32x2[n_commit]
-//   {reg | next << 16, register index} | pull u32x2[n_pull] {local, register index}
-//   | inject u32x2[n_inj] {local | width << 16 | owned << 23, input index}
+//   | ovf u16[...] (operands 2.. of ops with arity > 3) | commit u32x4[n_commit]
+//   {reg | next << 16, register index | width << 24, hash weight lo, hi}
+//   | pull u32x2[n_pull] {local, register index}
+//   | inject u32x4[n_inj] {local | width << 16, input index, hash weight lo, hi (0: not owned)}
+//   | [kop u64[ops]: the op hash weights, when they fit]
 //   | (state: state_bytes at state_off, not in the blob) | map u32x2[n_map] {local, coord}
 struct RepSliceHdr {
   uint32_t smem_bytes;    // bytes copied to shared memory (16-aligned)
@@ -262,7 +264,8 @@ struct RepSliceHdr {
   uint32_t off_inj, n_inj, off_map, n_map;
   uint32_t k_base;        // first entry of the partition in the op hash-weight array
   uint32_t max_level;     // largest level of the partition (ops)
-  uint32_t pad[2];
+  uint32_t off_kop;       // u64[ops]: op hash weights in shared memory (kop_smem), else in global memory
+  uint32_t kop_smem;
 };
 // Builds the P slices of `plan` (blob, slice offsets) and the per-partition op
 // hash weights (owned ops: opk, else 0) in slice op order.  in_owner[k] = the

@@ -101,19 +101,28 @@ struct RepSmemArgs {
 
 struct LocalState {
   uint8_t* s;
+  uint32_t sa;          // shared-window address of s
   uint32_t b1, b2, b3;
-  __device__ __forceinline__ uint32_t cls(uint32_t o) const { return o < b1 ? 3u : o < b2 ? 2u : o < b3 ? 1u : 0u; }
-  // branch-free gather: the aligned 64-bit word holding the value, shifted and masked
-  __device__ __forceinline__ uint64_t ld(uint32_t o) const {
-    const uint64_t w = *reinterpret_cast<const uint64_t*>(s + (o & ~7u));
-    const uint32_t c = cls(o);
-    const uint64_t v = w >> ((o & 7u) * 8u);
-    return c == 3u ? w : (v & (0xFFFFFFFFull >> (32u - (8u << c))));
+  // width class of a local offset: the u64 region comes first, then u32, u16, u8
+  __device__ __forceinline__ uint32_t cls(uint32_t o) const {
+    return (uint32_t)(o < b1) + (uint32_t)(o < b2) + (uint32_t)(o < b3);
   }
-  // branch-free store: four predicated st.shared (a switch compiles to an
-  // indirect branch, which splits warps whose ops write several widths)
+  // branch-free gather and store: one predicated ld/st.shared per width class,
+  // exactly one of which is on (a switch compiles to an indirect branch that
+  // splits a warp whose operands have several widths)
+  __device__ __forceinline__ uint64_t ld(uint32_t o) const {
+    uint64_t v;
+    asm volatile(
+        "{\n\t.reg .pred q1, q2, q3, p16, p32;\n\t.reg .u32 t;\n\t"
+        "setp.lt.u32 q3, %1, %2;\n\tsetp.lt.u32 q2, %1, %3;\n\tsetp.lt.u32 q1, %1, %4;\n\t"
+        "xor.pred p16, q1, q2;\n\txor.pred p32, q2, q3;\n\tmov.u32 t, 0;\n\t"
+        "@!q1 ld.shared.u8 t, [%5];\n\t@p16 ld.shared.u16 t, [%5];\n\t@p32 ld.shared.u32 t, [%5];\n\t"
+        "cvt.u64.u32 %0, t;\n\t@q3 ld.shared.u64 %0, [%5];\n\t}"
+        : "=l"(v) : "r"(o), "r"(b1), "r"(b2), "r"(b3), "r"(sa + o) : "memory");
+    return v;
+  }
   __device__ __forceinline__ void st(uint32_t o, uint64_t v) const {
-    const uint32_t a = (uint32_t)__cvta_generic_to_shared(s + o), c = cls(o);
+    const uint32_t c = cls(o), a = sa + o;
     asm volatile(
         "{\n\t.reg .pred q0, q1, q2, q3;\n\t"
         "setp.eq.u32 q0, %2, 0;\n\tsetp.eq.u32 q1, %2, 1;\n\tsetp.eq.u32 q2, %2, 2;\n\tsetp.eq.u32 q3, %2, 3;\n\t"
@@ -159,7 +168,7 @@ __device__ __forceinline__ uint64_t rep_eval(const LocalState& S, uint32_t pw, u
   return r & wmask(pw & 127u);
 }
 
-template <bool HASH>
+template <bool HASH, bool ONE>
 __global__ void __launch_bounds__(1024, 1) k_repcut_smem(const RepSmemArgs ra) {
   const StepArgs& a = ra.a;
   extern __shared__ __align__(16) uint8_t smem[];
@@ -182,49 +191,56 @@ __global__ void __launch_bounds__(1024, 1) k_repcut_smem(const RepSmemArgs ra) {
   const uint32_t* inj = reinterpret_cast<const uint32_t*>(smem + h.off_inj);
   const uint32_t* map = reinterpret_cast<const uint32_t*>(src + h.off_map);
   const uint64_t* opk = ra.op_k + h.k_base;
-  LocalState S{smem + h.state_off, h.b1, h.b2, h.b3};
+  LocalState S{smem + h.state_off, (uint32_t)__cvta_generic_to_shared(smem + h.state_off), h.b1, h.b2, h.b3};
   const TileP<1> t = tile_ptrs<1>(a, p, 0);
   for (uint32_t i = tid; i < h.n_map; i += T) S.st(map[2 * i], t.ld(map[2 * i + 1]));
   if (a.n_cycles == 0) return;
   const uint32_t NL = h.n_levels;
-  // hash weights are software-pipelined one level ahead (an exposed L2 load per
-  // level would dominate a level of shared-memory work); the registers' once
+  // op hash weights, loaded two levels ahead for the thread's (first) op of
+  // the level: from shared memory when they fit in the slice, else from global
+  // memory (an exposed L2 load per level would dominate a level's work)
+  const bool ksm = h.kop_smem != 0;
+  const uint64_t* kop = ksm ? reinterpret_cast<const uint64_t*>(smem + h.off_kop) : opk;
   auto kload = [&](uint32_t l) -> uint64_t {
-    if (!HASH) return 0ull;
+    if (!HASH || l >= NL) return 0ull;
     const uint32_t i = lvl[l] + tid;
-    return i < lvl[l + 1] ? __ldg(opk + i) : 0ull;
+    return i < lvl[l + 1] ? (ksm ? kop[i] : __ldg(opk + i)) : 0ull;
   };
-  const uint64_t kreg = (HASH && tid < h.n_commit) ? __ldg(a.g.reg_k + (com[2 * tid + 1] & 0xFFFFFFu)) : 0ull;
   unsigned long long target = 0;
   uint64_t hacc = 0;
   __syncthreads();
 #pragma unroll 1
   for (uint32_t cyc = 0; cyc < a.n_cycles; ++cyc) {
     const uint64_t cycle = a.cycle0 + cyc;
-    uint64_t knext = NL ? kload(0) : 0ull;
+    uint64_t k0 = kload(0), k1 = kload(1);
 #pragma unroll 1
     for (uint32_t i = tid; i < h.n_inj; i += T) {
-      const uint32_t e = inj[2 * i], k = inj[2 * i + 1];
-      uint64_t v = a.staged ? __ldg(a.stage + (size_t)(cycle % a.stage_cap) * a.g.n_inputs + k)
-                            : d_stimulus(a.seed, k, cycle, a.lane0);
-      v &= wmask((e >> 16) & 127u);
-      S.st(e & 0xFFFFu, v);
-      if (HASH && (e >> 23)) hacc += v * __ldg(a.g.in_k + k);
+      const uint4 e = *reinterpret_cast<const uint4*>(inj + 4 * i);
+      uint64_t v = a.staged ? __ldg(a.stage + (size_t)(cycle % a.stage_cap) * a.g.n_inputs + e.y)
+                            : d_stimulus(a.seed, e.y, cycle, a.lane0);
+      v &= wmask((e.x >> 16) & 127u);
+      S.st(e.x & 0xFFFFu, v);
+      if (HASH) hacc += v * (((uint64_t)e.w << 32) | e.z);
     }
     __syncthreads();
     uint32_t b = NL ? lvl[0] : 0u, e = NL ? lvl[1] : 0u;  // level bounds, loaded a level ahead
 #pragma unroll 1
     for (uint32_t l = 0; l < NL; ++l) {
       const uint32_t en = lvl[l + 2 <= NL ? l + 2 : NL];
-      const uint64_t kcur = knext;
-      if (l + 1 < NL) knext = kload(l + 1);
+      const uint64_t kcur = k0;
+      k0 = k1;
+      k1 = kload(l + 2);
+      const auto do_op = [&](uint32_t i, uint64_t k) {
+        const uint64_t y = rep_eval(S, pws[i], cws[i], ovf);
+        S.st(cws[i].x & 0xFFFFu, y);
+        if (HASH) hacc += y * k;
+      };
+      if (ONE) {  // the launch has a thread for every op of every level
+        if (b + tid < e) do_op(b + tid, kcur);
+      } else {
+        if (b + tid < e) do_op(b + tid, kcur);
 #pragma unroll 1
-      for (uint32_t i = b + tid; i < e; i += T) {
-        const uint32_t pw = pws[i];
-        const uint2 cw = cws[i];
-        const uint64_t y = rep_eval(S, pw, cw, ovf);
-        S.st(cw.x & 0xFFFFu, y);
-        if (HASH) hacc += y * (i == b + tid ? kcur : __ldg(opk + i));
+        for (uint32_t i = b + tid + T; i < e; i += T) do_op(i, HASH ? (ksm ? kop[i] : __ldg(opk + i)) : 0ull);
       }
       __syncthreads();
 #ifdef RS_TRACE
@@ -237,10 +253,11 @@ __global__ void __launch_bounds__(1024, 1) k_repcut_smem(const RepSmemArgs ra) {
     uint64_t* mail = ra.mail + (size_t)(cyc & 1u) * R;
 #pragma unroll 1
     for (uint32_t i = tid; i < h.n_commit; i += T) {
-      const uint32_t e = com[2 * i], rw = com[2 * i + 1], r = rw & 0xFFFFFFu;
-      const uint64_t nv = S.ld(e >> 16) & wmask(rw >> 24);
-      if (HASH) hacc += S.ld(e & 0xFFFFu) * (i == tid ? kreg : __ldg(a.g.reg_k + r));
-      S.st(e & 0xFFFFu, nv);
+      const uint4 e = *reinterpret_cast<const uint4*>(com + 4 * i);
+      const uint32_t r = e.y & 0xFFFFFFu;
+      const uint64_t nv = S.ld(e.x >> 16) & wmask(e.y >> 24);
+      if (HASH) hacc += S.ld(e.x & 0xFFFFu) * (((uint64_t)e.w << 32) | e.z);
+      S.st(e.x & 0xFFFFu, nv);
       mail[r] = nv;
     }
     if (HASH) {

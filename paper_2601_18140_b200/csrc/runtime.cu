@@ -114,6 +114,7 @@ struct rs_lanes {
   RepArgs rep{};
   bool rep_smem = false;      // k_repcut_smem (partition-local shared-memory slices)
   void* rep_mail = nullptr;   // [2][n_regs] register mailbox
+  bool rep_one = false;       // threads >= every partition level: one op per thread
   RepSmemArgs reps{};
   uint32_t rep_smem_bytes = 0;
   size_t sched_bytes = 0;                // device bytes of the bound stage schedule
@@ -551,6 +552,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
       }
       // one op per thread per level where possible (the hash weights are prefetched for one)
       if (!o.threads) s->threads = std::min<uint32_t>(1024, std::max<uint32_t>(128, (max_level + 31) / 32 * 32));
+      s->rep_one = s->threads >= max_level;
       size_t o_bl;
       put(blob, off, sblob, &o_bl);
       size_t o_so, o_k;
@@ -603,11 +605,12 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
       }
       s->reps.mail = (uint64_t*)s->rep_mail;
       s->total_bytes += 16ull * g->cg.n_regs;
-      e2 = cudaFuncSetAttribute((const void*)k_repcut_smem<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)s->rep_smem_bytes);
-      if (e2 == cudaSuccess)
-        e2 = cudaFuncSetAttribute((const void*)k_repcut_smem<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)s->rep_smem_bytes);
+      const void* fns[] = {(const void*)k_repcut_smem<true, true>, (const void*)k_repcut_smem<true, false>,
+                           (const void*)k_repcut_smem<false, true>, (const void*)k_repcut_smem<false, false>};
+      for (const void* f : fns)
+        if (e2 == cudaSuccess)
+          e2 = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->rep_smem_bytes);
+
       if (e2 != cudaSuccess) {
         cudaFree(s->drep);
         cudaFree(s->rep_mail);
@@ -902,8 +905,9 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
       RepSmemArgs ra = s->reps;
       ra.a = a;
       void* args[] = {&ra};
-      e = cudaLaunchCooperativeKernel(hash ? (const void*)k_repcut_smem<true> : (const void*)k_repcut_smem<false>,
-                                      s->ctas, s->threads, args, s->rep_smem_bytes, s->stream);
+      const void* fn = hash ? (s->rep_one ? (const void*)k_repcut_smem<true, true> : (const void*)k_repcut_smem<true, false>)
+                            : (s->rep_one ? (const void*)k_repcut_smem<false, true> : (const void*)k_repcut_smem<false, false>);
+      e = cudaLaunchCooperativeKernel(fn, s->ctas, s->threads, args, s->rep_smem_bytes, s->stream);
     } else if (s->repcut) {
       RepArgs ra = s->rep;
       ra.a = a;

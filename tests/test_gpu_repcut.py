@@ -44,6 +44,14 @@ def test_multicore_repcut(rs, cross_p, gl):
         check(rs, c, 40, 1, seed=11, mode="single", repcut=P, repcut_global=gl)
 
 
+@pytest.mark.parametrize("threads", [32, 64, 1024])
+def test_repcut_threads(rs, threads):
+    """Fewer threads than a level's ops (each thread loops over several ops,
+    hash weights fetched per op) and more."""
+    c = multicore_circuit(4, 2000, 12, 100, 4, cross_p=0.02, seed=4)
+    check(rs, c, 25, 1, seed=8, mode="single", repcut=4, threads=threads)
+
+
 @pytest.mark.parametrize("gl", GL)
 def test_repcut_fuzz(rs, gl):
     for s in range(60):

@@ -1,7 +1,7 @@
 #!/bin/bash
 # k_repcut_smem level timing for eval variants (trace builds)
 cd "$GRAFT_REPO_ROOT"
-for v in _TREE _TREE2; do
+for v in ""; do
   export RTLSIM_LIB=paper_2601_18140_b200/lib/librtlsim_trace$v.so
   echo "=== variant $v"
   for a in "16 0 1" "16 0 0"; do
