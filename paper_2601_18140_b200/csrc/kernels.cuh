@@ -27,7 +27,7 @@
 // Build-time tuning knobs (ops gathered per batch for arity <= 2 / 3, and the
 // CTA size the lane kernel's register budget is compiled for).
 #ifndef RS_LANES_MAX_THREADS
-#define RS_LANES_MAX_THREADS 768
+#define RS_LANES_MAX_THREADS 640
 #endif
 
 namespace rtlsim {

@@ -165,7 +165,10 @@ __device__ __forceinline__ void batch_store_t(const LaneT& L, uint32_t out_cls, 
 // parallelism); U * A * P values live in registers.
 template <int A, int P>
 struct BatchU {
-  static constexpr int value = (P == 4) ? 2 : (P == 2 && A == 3) ? 2 : 4;
+#ifndef RS_BATCHU_P4
+#define RS_BATCHU_P4 2
+#endif
+  static constexpr int value = (P == 4) ? RS_BATCHU_P4 : (P == 2 && A == 3) ? 2 : 4;
 };
 
 // cnt <= U ops of one run: op = opcode, outputs from coordinate ob (rows LT << out_cls apart).

@@ -95,7 +95,7 @@ def test_c2_threads_variants(rs):
     c = config_circuit("C2", n_ops=5000, n_levels=40, n_regs=500)
     for th in (64, 256, 512):
         check(rs, c, 12, 40, seed=7, threads=th, lane_tile=8, kernel=2)
-    for th in (32, 96, 768):
+    for th in (32, 96, 640):
         check(rs, c, 12, 70, seed=7, threads=th, lane_tile=64, kernel=1)
 
 
