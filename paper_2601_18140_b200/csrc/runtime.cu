@@ -76,6 +76,7 @@ struct rs_lanes {
   uint64_t lane0 = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  bool counted = false;       // counted in g->live_lanes (a fully built allocation)
   void* state_mem = nullptr;       // [n_tiles][tile_bytes]
   size_t state_bytes = 0;
   uint64_t tile_bytes = 0;
@@ -468,7 +469,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
   s->lane0 = o.lane0;
   if (g->cg.mode == RS_MODE_SINGLE && o.repcut > 1) {
     if (o.parts > 1 || o.repcut > (uint32_t)g->sm_count) {
-      delete s;
+      rs_free_lanes(s);  // partially built: frees what exists
       return set_err(RS_E_INVALID_ARG, "repcut = %u: must be <= %d SMs and not combined with parts", o.repcut,
                      g->sm_count);
     }
@@ -481,13 +482,13 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     s->parts = std::max<uint32_t>(1, o.parts);
     if (s->parts > kMaxParts || s->parts > std::max<uint32_t>(1, g->cg.n_levels)) {
       const uint32_t p = s->parts;
-      delete s;
+      rs_free_lanes(s);  // partially built: frees what exists
       return set_err(RS_E_INVALID_ARG, "parts = %u: must be <= %u and <= n_levels (%u)", p, kMaxParts, g->cg.n_levels);
     }
     s->n_tiles = s->parts;  // one state replica per partition (lane index = replica in the aux kernels)
   } else {
     if (o.parts > 1) {
-      delete s;
+      rs_free_lanes(s);  // partially built: frees what exists
       return set_err(RS_E_INVALID_ARG, "parts (level cut) applies to RS_MODE_SINGLE only");
     }
     // auto: lane-poor allocations (< 2048 lanes: per-level work per SM is a few
@@ -496,15 +497,15 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     const uint32_t kern = o.kernel ? o.kernel : (n_lanes < 2048u ? 2u : 1u);
     if (o.lane_tile && (kern == 2 ? (o.lane_tile != 8 && o.lane_tile != 16 && o.lane_tile != 32)
                                   : (o.lane_tile != 32 && o.lane_tile != 64 && o.lane_tile != 128))) {
-      delete s;
+      rs_free_lanes(s);  // partially built: frees what exists
       return set_err(RS_E_INVALID_ARG, "lane_tile must be 32, 64 or 128 (kernel 1) or 8, 16 or 32 (kernel 2)");
     }
     if (o.cluster && o.cluster != 1 && o.cluster != 2 && o.cluster != 4 && o.cluster != 8) {
-      delete s;
+      rs_free_lanes(s);  // partially built: frees what exists
       return set_err(RS_E_INVALID_ARG, "cluster must be 1, 2, 4 or 8");
     }
     if (o.kernel > 2) {
-      delete s;
+      rs_free_lanes(s);  // partially built: frees what exists
       return set_err(RS_E_INVALID_ARG, "kernel must be 0, 1 or 2");
     }
     s->variant = kern;
@@ -517,7 +518,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
   // launch shape
   if (o.threads) {
     if (o.threads % 32 || o.threads > (g->cg.mode == RS_MODE_SINGLE ? 1024u : (uint32_t)RS_LANES_MAX_THREADS) ||
-        o.threads < (s->variant == 1 ? 32u : s->LT)) { delete s; return set_err(RS_E_INVALID_ARG, "threads must be a multiple of 32 in [32, 1024]"); }
+        o.threads < (s->variant == 1 ? 32u : s->LT)) { rs_free_lanes(s); return set_err(RS_E_INVALID_ARG, "threads must be a multiple of 32 in [32, 1024]"); }
     s->threads = o.threads;
   } else if (g->cg.mode == RS_MODE_SINGLE) {
     s->threads = 1024;
@@ -531,7 +532,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     RepCutPlan plan;
     std::string err;
     if (!build_repcut(g->cg, s->parts, &plan, &err)) {
-      delete s;
+      rs_free_lanes(s);  // partially built: frees what exists
       return set_err(RS_E_INVALID_ARG, "%s", err.c_str());
     }
     s->threads = o.threads ? o.threads : 1024;
@@ -582,7 +583,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     cudaError_t e2 = cudaMalloc(&s->drep, blob.size());
     if (e2 == cudaSuccess) e2 = cudaMemcpy(s->drep, blob.data(), blob.size(), cudaMemcpyHostToDevice);
     if (e2 != cudaSuccess) {
-      delete s;
+      rs_free_lanes(s);  // partially built: frees what exists
       return set_err(RS_E_OOM, "repcut plan: %s", cudaGetErrorString(e2));
     }
     const uint8_t* b = (const uint8_t*)s->drep;
@@ -600,7 +601,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
       e2 = cudaMalloc(&s->rep_mail, std::max<size_t>(16, 16ull * g->cg.n_regs));
       if (e2 != cudaSuccess) {
         cudaFree(s->drep);
-        delete s;
+        rs_free_lanes(s);  // partially built: frees what exists
         return set_err(RS_E_OOM, "repcut mailbox: %s", cudaGetErrorString(e2));
       }
       s->reps.mail = (uint64_t*)s->rep_mail;
@@ -614,7 +615,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
       if (e2 != cudaSuccess) {
         cudaFree(s->drep);
         cudaFree(s->rep_mail);
-        delete s;
+        rs_free_lanes(s);  // partially built: frees what exists
         return set_err(RS_E_CUDA, "repcut smem attribute: %s", cudaGetErrorString(e2));
       }
     }
@@ -639,7 +640,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
       G = std::min<uint32_t>(maxG, G + std::max<uint32_t>(1, G / 4));
     }
     if (!ok && P > 1) {
-      delete s;
+      rs_free_lanes(s);  // partially built: frees what exists
       return set_err(RS_E_CAPACITY, "level cut: %u partitions' slices do not fit %u co-resident CTAs", P, maxG * P);
     }
     if (ok && !o.threads) {
@@ -670,7 +671,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
       if (e2 == cudaSuccess) e2 = cudaMemcpy(s->dslices, sblob.data(), sblob.size(), cudaMemcpyHostToDevice);
       if (e2 == cudaSuccess) e2 = cudaMemcpy((uint8_t*)s->dslices + off_off, soff.data(), G * 8, cudaMemcpyHostToDevice);
       if (e2 != cudaSuccess) {
-        delete s;
+        rs_free_lanes(s);  // partially built: frees what exists
         return set_err(RS_E_OOM, "single-lane slices: %s", cudaGetErrorString(e2));
       }
       s->slice_blob = (const uint8_t*)s->dslices;
@@ -698,14 +699,14 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
   }
   s->tile_bytes = std::max<uint64_t>((off + 127) & ~(uint64_t)127, 128);
   if (g->cg.mode == RS_MODE_LANES && s->tile_bytes >= (1ull << 30)) {
-    delete s;
+    rs_free_lanes(s);  // partially built: frees what exists
     return set_err(RS_E_CAPACITY, "a lane tile needs %llu B of state (limit 2^30); use a smaller lane_tile",
                    (unsigned long long)s->tile_bytes);
   }
   s->state_bytes = (size_t)s->tile_bytes * s->n_tiles;
   cudaError_t e;
   if ((e = cudaMalloc(&s->state_mem, s->state_bytes)) != cudaSuccess) {
-    delete s;
+    rs_free_lanes(s);  // partially built: frees what exists
     return set_err(RS_E_OOM, "cudaMalloc state (%zu B): %s", s->state_bytes, cudaGetErrorString(e));
   }
   if (g->cg.mode == RS_MODE_LANES) {
@@ -772,6 +773,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     return set_err(RS_E_CUDA, "state init: %s", cudaGetErrorString(e));
   }
   g->live_lanes++;
+  s->counted = true;
   *out = s;
   return RS_OK;
 }
@@ -793,7 +795,7 @@ void rs_free_lanes(rs_lanes* s) {
   if (s->drep) cudaFree(s->drep);
   if (s->rep_mail) cudaFree(s->rep_mail);
   if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
-  if (s->g) s->g->live_lanes--;
+  if (s->g && s->counted) s->g->live_lanes--;
   delete s;
 }
 
