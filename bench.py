@@ -254,7 +254,7 @@ def main():
     value = lane_cycles / (total_ms / 1e3)
 
     kid = L.shape()["kernel"]
-    kernel_name = {1: "k_lanes_t", 2: "k_lanes", 3: "k_repcut_smem", 4: "k_repcut"}.get(kid, "k_single")
+    kernel_name = {1: "k_lanes_t", 2: "k_lanes", 3: "k_repcut_smem", 4: "k_repcut", 5: "k_single2"}.get(kid, "?")
     # roofline of the dominant (only) kernel: algorithmic bytes per launch / launch duration
     bytes_per_cycle = lanes * info["alg_bytes_per_lane_cycle"] + info["graph_alg_bytes"]
     alg_bytes = bytes_per_cycle * cycles
@@ -325,7 +325,7 @@ def main():
                        "l2": "flushed (256 MB write) before every timed step",
                        "mode": "single" if single else "lanes", "launch": L.shape(),
                        **({"level_cut_parts": args.parts} if args.parts > 1 else {}),
-                       **({"repcut_partitions": args.repcut} if args.repcut > 1 else {}),
+                       **({"repcut_partitions": args.repcut} if args.repcut >= 1 else {}),
                        "state_bytes_per_gpu": info["state_bytes_per_lane"] * lanes,
                        **({"watched_signals": args.watch} if args.watch else {})},
             "op_evals_per_s": value * circ.n_ops,

@@ -135,9 +135,13 @@ typedef struct {
                               dispatched once per op through a jump table on the class signature;
                               2 = two adjacent lanes per thread, 8/16/32-lane tiles, aligned 64-bit
                               word gathers + extraction.  lane_tile must match (32/64/128 for 1,
-                              8/16/32 for 2).  RS_E_INVALID_ARG otherwise. */
+                              8/16/32 for 2).  RS_E_INVALID_ARG otherwise.
+                              RS_MODE_SINGLE: 0 = auto (RepCut with one partition when the whole design
+                              fits one SM's shared memory, else the level-synchronous grid); 3 = RepCut,
+                              shared-memory slices; 4 = RepCut, global replicas; 5 = level-synchronous
+                              grid (k_single2; the level cut uses it). */
   uint32_t repcut;         /* RS_MODE_SINGLE replicated cut (App. C, Cascade 2; SURVEY.md §8(f)
-                              NEXT-2): 0/1 = off, else P partitions = CTAs of one cooperative launch; the
+                              NEXT-2): 0 = off, else P >= 1 partitions = CTAs of one cooperative launch; the
                               registers are cut into P contiguous blocks, partition p evaluates the cone of
                               its registers' next values (shared logic replicated) on its own state replica
                               with CTA barriers only, and after each cycle pushes its registers' new values
@@ -146,7 +150,8 @@ typedef struct {
                               if P > n_regs, > 255, > the SMs of the device, or combined with parts.
                               Each partition keeps its working set (op descriptors + a compact copy of the
                               signals it touches) in shared memory when it fits (k_repcut_smem), else works
-                              on its state replica in global memory (k_repcut). */
+                              on its state replica in global memory (k_repcut).  P = 1 runs a design that
+                              fits one SM's shared memory on a single CTA with CTA barriers only. */
   uint32_t repcut_global;  /* 1: force the global-replica RepCut kernel even if the slices fit shared memory */
 } rs_lane_opts;
 
@@ -241,8 +246,8 @@ uint64_t rs_launch_count(const rs_lanes* s);
 rs_status rs_launch_shape(const rs_lanes* s, uint32_t* lane_tile, uint32_t* threads, uint32_t* ctas,
                           uint32_t* cluster);
 /* Step kernel in use: lane mode 1 or 2 (rs_lane_opts.kernel); single-lane mode 3 = RepCut with
- * shared-memory slices (k_repcut_smem), 4 = RepCut on global replicas (k_repcut), 0 = the
- * level-synchronous single-lane kernel (or NULL). */
+ * shared-memory slices (k_repcut_smem), 4 = RepCut on global replicas (k_repcut), 5 = the
+ * level-synchronous single-lane grid (k_single2, also the level cut); 0 for NULL. */
 uint32_t rs_lanes_kernel(const rs_lanes* s);
 rs_status rs_sync(rs_lanes* s);
 /* ---- Waveform capture (§6.2: the

@@ -451,6 +451,9 @@ void rs_free_graph(rs_graph* g) {
   delete g;
 }
 
+// dynamic shared memory a RepCut slice may take (227 KiB less k_repcut_smem's static shared memory)
+constexpr uint32_t kRepSmemMax = 227u * 1024u - 2048u;
+
 rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts, rs_lanes** out) {
   if (!g || !out) return set_err(RS_E_INVALID_ARG, "NULL graph/out");
   *out = nullptr;
@@ -467,10 +470,33 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
   s->g = g;
   s->n_lanes = n_lanes;
   s->lane0 = o.lane0;
-  if (g->cg.mode == RS_MODE_SINGLE && o.repcut > 1) {
+  if (g->cg.mode == RS_MODE_SINGLE && o.kernel && o.kernel != 3 && o.kernel != 4 && o.kernel != 5) {
+    rs_free_lanes(s);
+    return set_err(RS_E_INVALID_ARG, "single-lane kernel must be 0 (auto), 3 (RepCut, shared memory), 4 (RepCut, "
+                                     "global replicas) or 5 (level-synchronous grid)");
+  }
+  if (g->cg.mode == RS_MODE_SINGLE && (o.kernel == 3 || o.kernel == 4) && !o.repcut) o.repcut = 1;
+  if (g->cg.mode == RS_MODE_SINGLE && o.kernel == 4) o.repcut_global = 1;
+  if (g->cg.mode == RS_MODE_SINGLE && o.kernel == 5 && o.repcut) {
+    rs_free_lanes(s);
+    return set_err(RS_E_INVALID_ARG, "kernel 5 (level-synchronous) excludes repcut");
+  }
+  // auto: a design whose whole working set fits one SM's shared memory runs as
+  // RepCut with one partition (one CTA, CTA barriers only; C1: 4.9 vs 17 us per
+  // cycle on the level-synchronous grid)
+  if (g->cg.mode == RS_MODE_SINGLE && o.kernel == 0 && o.repcut == 0 && o.parts <= 1 &&
+      (size_t)g->cg.n_ops_total() * 12 < kRepSmemMax && g->cg.n_regs >= 1) {
+    RepCutPlan plan;
+    std::string err;
+    std::vector<uint8_t> b1, b2;
+    std::vector<uint64_t> b3, b4;
+    if (build_repcut(g->cg, 1, &plan, &err) && build_repcut_slices(g->cg, plan, kRepSmemMax, &b1, &b3, &b4, &b2, &err))
+      o.repcut = 1;
+  }
+  if (g->cg.mode == RS_MODE_SINGLE && o.repcut >= 1) {
     if (o.parts > 1 || o.repcut > (uint32_t)g->sm_count) {
       rs_free_lanes(s);  // partially built: frees what exists
-      return set_err(RS_E_INVALID_ARG, "repcut = %u: must be <= %d SMs and not combined with parts", o.repcut,
+      return set_err(RS_E_INVALID_ARG, "repcut = %u: must be <= %d SMs and not combined with parts (level cut)", o.repcut,
                      g->sm_count);
     }
     s->LT = 1;
@@ -542,8 +568,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     size_t off = 0, o_lb, o_ops, o_rb, o_regs, o_pb, o_push;
     std::vector<uint8_t> sblob, in_owner;
     std::vector<uint64_t> sl_off, op_k;
-    const uint32_t max_smem = 227u * 1024u - 2048u;  // static shared memory of k_repcut_smem
-    if (!o.repcut_global && build_repcut_slices(g->cg, plan, max_smem, &sblob, &sl_off, &op_k, &in_owner, &err)) {
+    if (!o.repcut_global && build_repcut_slices(g->cg, plan, kRepSmemMax, &sblob, &sl_off, &op_k, &in_owner, &err)) {
       s->rep_smem = true;
       uint32_t max_level = 0;
       for (uint32_t p = 0; p < s->parts; ++p) {
@@ -1159,7 +1184,7 @@ rs_status rs_wave_read(rs_lanes* s, rs_change* out, uint64_t cap, uint64_t* n_ou
 uint32_t rs_lanes_kernel(const rs_lanes* s) {
   if (!s) return 0u;
   if (s->g->cg.mode == RS_MODE_LANES) return s->variant;
-  return s->repcut ? (s->rep_smem ? 3u : 4u) : 0u;
+  return s->repcut ? (s->rep_smem ? 3u : 4u) : 5u;
 }
 
 rs_status rs_launch_shape(const rs_lanes* s, uint32_t* lt, uint32_t* threads, uint32_t* ctas, uint32_t* cluster) {

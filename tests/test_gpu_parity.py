@@ -50,10 +50,10 @@ def check(rs, c, n_cycles, n_lanes=1, seed=0, mode="lanes", **kw):
 
 def test_paper_example_both_modes(rs):
     c, outs = cf.paper_example(two_muls=True)
-    for mode in ("lanes", "single"):
-        H, F, _ = run_gpu(rs, c, 2, mode=mode)
+    for mode, kernel in (("lanes", 0), ("single", 0), ("single", 5)):
+        H, F, _ = run_gpu(rs, c, 2, mode=mode, kernel=kernel)
         assert [int(F[o, 0]) for o in outs] == [4, 8]
-        check(rs, c, 2, mode=mode)
+        check(rs, c, 2, mode=mode, kernel=kernel)
 
 
 def test_stimulus_matches_golden(rs):
@@ -75,10 +75,14 @@ def test_stimulus_matches_golden(rs):
                 assert int(vals[row["k"], row["lane"]]) == int(row["value"]), row
 
 
-@pytest.mark.parametrize("mode", ["lanes", "single"])
-def test_c1_full(rs, mode):
+@pytest.mark.parametrize("mode,kernel", [("lanes", 0), ("single", 0), ("single", 3), ("single", 4), ("single", 5)])
+def test_c1_full(rs, mode, kernel):
+    """C1 in every mode; single lane: auto (RepCut, one partition, since C1 fits
+    one SM's shared memory), RepCut shared-memory / global, level-synchronous."""
     cfg = CONFIGS["C1"]
-    check(rs, config_circuit("C1"), cfg.cycles, 1, seed=cfg.stim_seed, mode=mode)
+    L = check(rs, config_circuit("C1"), cfg.cycles, 1, seed=cfg.stim_seed, mode=mode, kernel=kernel)
+    if mode == "single":
+        assert L.shape()["kernel"] == (kernel or 3)
 
 
 @pytest.mark.parametrize("kernel,lt,cs", [(2, 8, 1), (2, 16, 1), (2, 32, 1), (2, 32, 4), (2, 16, 2), (2, 8, 8),
@@ -117,7 +121,7 @@ def test_fuzz_corpus(rs):
         c = fuzz_circuit(seed)
         check(rs, c, 60, 3, seed=seed, kernel=1 + seed % 2)
         if seed % 4 == 0:
-            check(rs, c, 60, 1, seed=seed, mode="single")
+            check(rs, c, 60, 1, seed=seed, mode="single", kernel=5 if seed % 8 else 0)
 
 
 def test_closed_forms_on_gpu(rs):
@@ -127,10 +131,11 @@ def test_closed_forms_on_gpu(rs):
     c, s = cf.lfsr(16, (16, 14, 13, 11), seed=1)
     H, F, L = run_gpu(rs, c, 65535, 2)
     assert (F[s] == 1).all()                             # period 2^16 - 1
-    H1, F1, _ = run_gpu(rs, c, 65535, 1, mode="single", final=True)
-    assert int(F1[s, 0]) == 1
     r0 = oracle.simulate(c, 65535, n_lanes=1)
-    assert np.array_equal(H1, r0.hashes) and np.array_equal(H[:, :1], r0.hashes)
+    for kernel in (0, 5):
+        H1, F1, _ = run_gpu(rs, c, 65535, 1, mode="single", final=True, kernel=kernel)
+        assert int(F1[s, 0]) == 1
+        assert np.array_equal(H1, r0.hashes) and np.array_equal(H[:, :1], r0.hashes)
     c, a, b, out = cf.ripple_adder(8)
     A = np.repeat(np.arange(256, dtype=np.uint64), 256)
     B = np.tile(np.arange(256, dtype=np.uint64), 256)
@@ -250,8 +255,8 @@ def test_degenerate_graphs(rs):
     b.op("add", [k, k2], 64)
     b.op("cat", [k2, k], 64)
     c = b.build()
-    for mode in ("lanes", "single"):
-        check(rs, c, 3, 1, mode=mode)
+    for mode, kernel in (("lanes", 0), ("single", 0), ("single", 5)):
+        check(rs, c, 3, 1, mode=mode, kernel=kernel)
 
 
 @pytest.mark.slow

@@ -28,7 +28,7 @@ def kernel_of(rs, c, **kw):
 
 
 @pytest.mark.parametrize("gl", GL)
-@pytest.mark.parametrize("P", [2, 3, 8, 32])
+@pytest.mark.parametrize("P", [1, 2, 3, 8, 32])
 def test_c1_repcut(rs, P, gl):
     cfg = CONFIGS["C1"]
     c = config_circuit("C1")
@@ -40,7 +40,7 @@ def test_c1_repcut(rs, P, gl):
 @pytest.mark.parametrize("cross_p", [0.0, 0.02, 0.3])
 def test_multicore_repcut(rs, cross_p, gl):
     c = multicore_circuit(4, 500, 12, 50, 4, cross_p=cross_p, seed=9)
-    for P in (2, 4, 5):
+    for P in (1, 2, 4, 5):
         check(rs, c, 40, 1, seed=11, mode="single", repcut=P, repcut_global=gl)
 
 
@@ -57,7 +57,7 @@ def test_repcut_fuzz(rs, gl):
     for s in range(60):
         c = fuzz_circuit(8000 + s)
         R = len(c.reg_id)
-        for P in sorted({2, 3, 7}):
+        for P in sorted({1, 2, 3, 7}):
             if P <= R:
                 check(rs, c, 12, 1, seed=s, mode="single", repcut=P, repcut_global=gl)
 

@@ -52,7 +52,7 @@ def main():
     for parts in (2, 4):
         if parts <= info["n_levels"]:
             res[f"level_cut{parts}"] = timed(c, n, parts=parts)
-    for P in (2, 4, 8, 16, 32, 64, 128, 148):
+    for P in (1, 2, 4, 8, 16, 32, 64, 128, 148):
         if P > len(c.reg_id):
             continue
         st = gh.repcut_stats(P)
