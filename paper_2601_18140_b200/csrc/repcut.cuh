@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(1024, 1) k_repcut_smem(const RepSmemArgs ra) {
       const uint64_t nv = S.ld(e.x >> 16) & wmask(e.y >> 24);
       if (HASH) hacc += S.ld(e.x & 0xFFFFu) * (((uint64_t)e.w << 32) | e.z);
       S.st(e.x & 0xFFFFu, nv);
-      mail[r] = nv;
+      if (gridDim.x > 1) mail[r] = nv;  // one partition: nobody pulls
     }
     if (HASH) {
       const uint64_t s = block_sum(hacc, wsum) + (p == 0 ? a.g.const_hash : 0ull);
