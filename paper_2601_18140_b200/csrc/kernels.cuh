@@ -311,6 +311,34 @@ __device__ __forceinline__ uint64_t block_sum(uint64_t v, uint64_t* sm) {
   return s;
 }
 
+// op_u / op_r / op_s for an op of arity <= 3 (n = pw >> 26), branch-free: the
+// ops of a warp may have different opcodes (single-lane mode deals a level's
+// ops to threads), and a switch compiles to an indirect branch that splits the
+// warp into serialized paths; every candidate result is computed and the op's
+// one is picked by a selection tree on the opcode bits (depth 4).  Unmasked;
+// folds with n > 3 are the caller's.
+__device__ __forceinline__ uint64_t select_op(uint32_t pw, uint64_t x0, uint64_t x1, uint64_t x2) {
+  const uint32_t op = (pw >> 22) & 15u, n = pw >> 26, p0 = (pw >> 7) & 127u;
+  const bool three = n == 3;
+  const uint64_t z = three ? x2 : 0ull;
+  const uint32_t sh = p0 >= 64 ? 63u : p0;
+  const uint64_t shl = p0 >= 64 ? 0ull : (x0 << sh), shr = p0 >= 64 ? 0ull : (x0 >> sh);
+  const uint32_t lo = (pw >> 14) & 63u;
+  {  // selection tree on the opcode bits (depth 4 instead of a 14-deep chain)
+    const uint64_t a0 = x0 & x1 & (three ? x2 : ~0ull), a1 = x0 | x1 | z, a2 = x0 ^ x1 ^ z, a3 = ~x0;
+    const uint64_t a4 = x0 + x1 + z, a5 = x0 - x1 - z, a6 = x0 * x1 * (three ? x2 : 1ull);
+    const uint64_t a7 = (uint64_t)(x0 == x1), a8 = (uint64_t)(x0 < x1), a9 = shl, a10 = shr;
+    const uint64_t a11 = (x0 >> lo) & wmask(p0 - lo + 1u), a12 = p0 >= 64 ? x1 : (shl | x1);
+    const uint64_t a13 = x0 != 0 ? x1 : x2, a14 = x0;
+    const bool b0 = op & 1u, b1 = op & 2u, b2 = op & 4u, b3 = op & 8u;
+    const uint64_t s01 = b0 ? a1 : a0, s23 = b0 ? a3 : a2, s45 = b0 ? a5 : a4, s67 = b0 ? a7 : a6;
+    const uint64_t s89 = b0 ? a9 : a8, sab = b0 ? a11 : a10, scd = b0 ? a13 : a12, sef = a14;
+    const uint64_t t0 = b1 ? s23 : s01, t1 = b1 ? s67 : s45, t2 = b1 ? sab : s89, t3 = b1 ? sef : scd;
+    const uint64_t u0 = b2 ? t1 : t0, u1 = b2 ? t3 : t2;
+    return b3 ? u1 : u0;
+  }
+}
+
 template <bool CG = true>
 __device__ __forceinline__ uint64_t single_op(const StepArgs& a, const TileP<1>& t, uint32_t j) {
   auto L = [&](uint32_t c) -> uint64_t { return CG ? t.ld_cg(c) : t.ld(c); };

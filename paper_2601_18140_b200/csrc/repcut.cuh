@@ -132,35 +132,14 @@ struct LocalState {
   }
 };
 
-// One op, branch-free: a partition's level mixes many opcodes (its ops are a
-// sparse subset of the level's runs), and a switch compiles to an indirect
-// branch that splits a warp into serialized paths (measured: 2240 vs 1186
-// cycles per level on the 16-core design); every candidate result is computed
-// instead (a few dozen ALU instructions) and the op's one is picked by a
-// selection tree on the opcode bits (depth 4; a 14-deep select chain: 1275).
+// One op (kernels.cuh select_op: branch-free; on the 16-core design a switch
+// cost 2,240 cycles per level, a 14-deep select chain 1,275, the selection
+// tree 1,186 -- a partition's level mixes many opcodes).
 __device__ __forceinline__ uint64_t rep_eval(const LocalState& S, uint32_t pw, uint2 cw, const uint16_t* ovf) {
-  const uint32_t op = (pw >> 22) & 15u, n = pw >> 26, p0 = (pw >> 7) & 127u;
+  const uint32_t op = (pw >> 22) & 15u, n = pw >> 26;
   const uint32_t c0 = cw.x >> 16, c1 = cw.y & 0xFFFFu, c2 = n > 3 ? c0 : cw.y >> 16;
   const uint64_t x0 = S.ld(c0), x1 = S.ld(c1), x2 = S.ld(c2);
-  const bool three = n == 3;
-  const uint64_t z = three ? x2 : 0ull;
-  const uint32_t sh = p0 >= 64 ? 63u : p0;
-  const uint64_t shl = p0 >= 64 ? 0ull : (x0 << sh), shr = p0 >= 64 ? 0ull : (x0 >> sh);
-  const uint32_t lo = (pw >> 14) & 63u;
-  uint64_t r;
-  {  // selection tree on the opcode bits (depth 4 instead of a 14-deep chain)
-    const uint64_t a0 = x0 & x1 & (three ? x2 : ~0ull), a1 = x0 | x1 | z, a2 = x0 ^ x1 ^ z, a3 = ~x0;
-    const uint64_t a4 = x0 + x1 + z, a5 = x0 - x1 - z, a6 = x0 * x1 * (three ? x2 : 1ull);
-    const uint64_t a7 = (uint64_t)(x0 == x1), a8 = (uint64_t)(x0 < x1), a9 = shl, a10 = shr;
-    const uint64_t a11 = (x0 >> lo) & wmask(p0 - lo + 1u), a12 = p0 >= 64 ? x1 : (shl | x1);
-    const uint64_t a13 = x0 != 0 ? x1 : x2, a14 = x0;
-    const bool b0 = op & 1u, b1 = op & 2u, b2 = op & 4u, b3 = op & 8u;
-    const uint64_t s01 = b0 ? a1 : a0, s23 = b0 ? a3 : a2, s45 = b0 ? a5 : a4, s67 = b0 ? a7 : a6;
-    const uint64_t s89 = b0 ? a9 : a8, sab = b0 ? a11 : a10, scd = b0 ? a13 : a12, sef = a14;
-    const uint64_t t0 = b1 ? s23 : s01, t1 = b1 ? s67 : s45, t2 = b1 ? sab : s89, t3 = b1 ? sef : scd;
-    const uint64_t u0 = b2 ? t1 : t0, u1 = b2 ? t3 : t2;
-    r = b3 ? u1 : u0;
-  }
+  uint64_t r = select_op(pw, x0, x1, x2);
   if (n > 3) {  // rare long folds (op <= RS_OP_MUL): operands 2.. in the overflow list
     r = fold_step(op, x0, x1);
     for (uint32_t o = 2; o < n; ++o) r = fold_step(op, r, S.ld(ovf[(cw.y >> 16) + o - 2]));
@@ -171,7 +150,7 @@ __device__ __forceinline__ uint64_t rep_eval(const LocalState& S, uint32_t pw, u
 template <bool HASH, bool ONE>
 __global__ void __launch_bounds__(1024, 1) k_repcut_smem(const RepSmemArgs ra) {
   const StepArgs& a = ra.a;
-  extern __shared__ __align__(16) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t wsum[32];
   const uint32_t p = blockIdx.x, tid = threadIdx.x, T = blockDim.x, R = a.g.n_regs;
   const uint8_t* src = ra.blob + ra.slice_off[p];

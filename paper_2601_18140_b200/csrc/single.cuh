@@ -263,8 +263,8 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
       const SliceLvl L = lvl[l];
       const uint64_t kcur = knext;
       knext = kload(l + 1 < h->n_levels ? l + 1 : 0);
-#pragma unroll 1
       const uint32_t top = slot(L.n);
+#pragma unroll 1
       for (uint32_t t = top; t < L.n; t += T) {
         const uint64_t k = !HASH ? 0ull : (t == top ? kcur : __ldg(a.g.opk + L.op_begin + t));
         const uint32_t pw = pws[L.pw_base + t];
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
       }
       single_barrier<GRID>(bar, target, sa.gp, wsum, nullptr);
 #ifdef RS_TRACE
-      if (blockIdx.x == 0 && tid == 0 && a.trace && cyc < 8) a.trace[cyc * 64 + l] = clock64();
+      if (blockIdx.x == 0 && tid == 0 && a.trace && cyc < 8 && l < 60) a.trace[cyc * 64 + l] = clock64();
 #endif
     }
     hr = 0;
