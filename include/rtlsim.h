@@ -116,8 +116,11 @@ typedef struct {
 /* Options for rs_alloc_lanes (NULL -> all defaults). */
 typedef struct {
   uint64_t lane0;          /* global index of this allocation's first lane (stimulus, hashes) */
-  uint32_t lane_tile;      /* RS_MODE_LANES: lanes per CTA tile, 0 = auto, else 8, 16 or 32 */
-  uint32_t threads;        /* threads per CTA, 0 = auto (multiple of 32, <= 1024) */
+  uint32_t lane_tile;      /* RS_MODE_LANES: lanes per CTA tile, 0 = auto, else 8, 16 or 32 (kernel 2)
+                              or 32, 64 or 128 (kernel 1) */
+  uint32_t threads;        /* threads per CTA, 0 = auto; a multiple of 32, <= 640 in RS_MODE_LANES (the
+                              register budget the lane kernels are compiled for: RS_LANES_MAX_THREADS),
+                              <= 1024 in RS_MODE_SINGLE */
   uint32_t stage_cycles;   /* capacity (cycles) of the staged-input ring, 0 = none */
   uint32_t cluster;        /* RS_MODE_LANES: CTAs (a thread-block cluster on as many SMs) sharing one
                               lane tile, 0 = auto, else 1, 2, 4 or 8 */
@@ -144,8 +147,8 @@ typedef struct {
                               NEXT-2): 0 = off, else P >= 1 partitions = CTAs of one cooperative launch; the
                               registers are cut into P contiguous blocks, partition p evaluates the cone of
                               its registers' next values (shared logic replicated) on its own state replica
-                              with CTA barriers only, and after each cycle pushes its registers' new values
-                              to the partitions that read them (the Register Update Map).  Pays off on
+                              with CTA barriers only, and after each cycle delivers its registers' new
+                              values to the partitions that read them (the Register Update Map).  Pays off on
                               designs whose cones barely overlap (e.g. multi-core SoCs).  RS_E_INVALID_ARG
                               if P > n_regs, > 255, > the SMs of the device, or combined with parts.
                               Each partition keeps its working set (op descriptors + a compact copy of the
