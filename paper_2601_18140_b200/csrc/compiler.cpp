@@ -358,8 +358,8 @@ struct StageWriter {
       std::memcpy(p + h.off_k, k, 8ull * h.n);
     }
     if (h.n_coords) std::memcpy(p + h.off_c, c, 4ull * h.n_coords);
-    if (h.n_runs) std::memcpy(p + h.off_runs, runs, sizeof(StageRun) * h.n_runs);
-    if (h.n_items) std::memcpy(p + h.off_items, items, 4ull * h.n_items);
+    if (h.n_runs && runs) std::memcpy(p + h.off_runs, runs, sizeof(StageRun) * h.n_runs);
+    if (h.n_items && items) std::memcpy(p + h.off_items, items, 4ull * h.n_items);
     table->push_back({base, h.bytes, h.type});
   }
 };
