@@ -353,11 +353,9 @@ struct StageWriter {
     blob->resize(base + h.bytes, 0);
     uint8_t* p = blob->data() + base;
     std::memcpy(p, &h, sizeof h);
-    if (h.n) {
-      std::memcpy(p + h.off_w, w, 4ull * h.n);
-      std::memcpy(p + h.off_k, k, 8ull * h.n);
-    }
-    if (h.n_coords) std::memcpy(p + h.off_c, c, 4ull * h.n_coords);
+    if (h.n && w) std::memcpy(p + h.off_w, w, 4ull * h.n);
+    if (h.n && k) std::memcpy(p + h.off_k, k, 8ull * h.n);
+    if (h.n_coords && c) std::memcpy(p + h.off_c, c, 4ull * h.n_coords);
     if (h.n_runs && runs) std::memcpy(p + h.off_runs, runs, sizeof(StageRun) * h.n_runs);
     if (h.n_items && items) std::memcpy(p + h.off_items, items, 4ull * h.n_items);
     table->push_back({base, h.bytes, h.type});
