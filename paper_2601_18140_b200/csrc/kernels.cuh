@@ -27,7 +27,10 @@
 // Build-time tuning knobs (ops gathered per batch for arity <= 2 / 3, and the
 // CTA size the lane kernel's register budget is compiled for).
 #ifndef RS_LANES_MAX_THREADS
-#define RS_LANES_MAX_THREADS 640
+#define RS_LANES_MAX_THREADS 640    // kernel 2 (k_lanes): 96 registers
+#endif
+#ifndef RS_LANES_T_MAX_THREADS
+#define RS_LANES_T_MAX_THREADS 768  // kernel 1 (k_lanes_t): 80 registers, 3-operand batches of 1 op at P = 4
 #endif
 
 namespace rtlsim {

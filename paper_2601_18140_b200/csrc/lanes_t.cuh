@@ -168,7 +168,10 @@ struct BatchU {
 #ifndef RS_BATCHU_P4
 #define RS_BATCHU_P4 2
 #endif
-  static constexpr int value = (P == 4) ? RS_BATCHU_P4 : (P == 2 && A == 3) ? 2 : 4;
+#ifndef RS_BATCHU_P4_A3
+#define RS_BATCHU_P4_A3 1  // keeps k_lanes_t<4, 1> at 80 registers without spills (768-thread CTAs)
+#endif
+  static constexpr int value = (P == 4) ? (A == 3 ? RS_BATCHU_P4_A3 : RS_BATCHU_P4) : (P == 2 && A == 3) ? 2 : 4;
 };
 
 // cnt <= U ops of one run: op = opcode, outputs from coordinate ob (rows LT << out_cls apart).
@@ -327,7 +330,7 @@ __host__ __device__ constexpr size_t lanes_t_smem_extra(uint32_t threads, uint32
 }
 
 template <int P, bool HASH>
-__global__ void __launch_bounds__(RS_LANES_MAX_THREADS, 1) k_lanes_t(const StepArgs a) {
+__global__ void __launch_bounds__(RS_LANES_T_MAX_THREADS, 1) k_lanes_t(const StepArgs a) {
   constexpr uint32_t LT = 32u * P;
   extern __shared__ __align__(128) uint8_t smem[];
   // [mbarriers | stage buffer 0 | stage buffer 1 | red[2][T*P] | hr[T*P] | hp[T*P] | lsum[3][LT]]

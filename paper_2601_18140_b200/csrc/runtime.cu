@@ -543,14 +543,20 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
   }
   // launch shape
   if (o.threads) {
-    if (o.threads % 32 || o.threads > (g->cg.mode == RS_MODE_SINGLE ? 1024u : (uint32_t)RS_LANES_MAX_THREADS) ||
-        o.threads < (s->variant == 1 ? 32u : s->LT)) { rs_free_lanes(s); return set_err(RS_E_INVALID_ARG, "threads must be a multiple of 32 in [32, 1024]"); }
+    const uint32_t tmax = g->cg.mode == RS_MODE_SINGLE ? 1024u
+                          : s->variant == 1            ? (uint32_t)RS_LANES_T_MAX_THREADS
+                                                       : (uint32_t)RS_LANES_MAX_THREADS;
+    if (o.threads % 32 || o.threads > tmax || o.threads < (s->variant == 1 ? 32u : s->LT)) {
+      rs_free_lanes(s);
+      return set_err(RS_E_INVALID_ARG, "threads must be a multiple of 32 in [32, %u] for this kernel", tmax);
+    }
     s->threads = o.threads;
   } else if (g->cg.mode == RS_MODE_SINGLE) {
     s->threads = 1024;
   } else {
     const uint32_t per_sm = (s->n_tiles * s->cluster + g->sm_count - 1) / g->sm_count;
-    uint32_t th = RS_LANES_MAX_THREADS / std::max<uint32_t>(1, per_sm);
+    const uint32_t tmax = s->variant == 1 ? (uint32_t)RS_LANES_T_MAX_THREADS : (uint32_t)RS_LANES_MAX_THREADS;
+    uint32_t th = tmax / std::max<uint32_t>(1, per_sm);
     th = std::max<uint32_t>(64, th & ~31u);
     s->threads = th;
   }
