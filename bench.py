@@ -273,7 +273,7 @@ def main():
     if not args.no_e2e:
         chunk = min(cycles, max(1, (256 << 20) // max(1, 8 * circ.n_inputs * lanes)))
         Ls = rs.Lanes(g, lanes, lane0=shard.lane0, lane_tile=args.lane_tile, threads=args.threads, cluster=args.cluster,
-                      stage_cycles=chunk, stream=stream, parts=args.parts, kernel=args.kernel,
+                      stage_cycles=2 * chunk, stream=stream, parts=args.parts, kernel=args.kernel,
                       repcut=args.repcut)
         rng = np.random.default_rng(rank)
         host_in = torch.from_numpy(rng.integers(0, 2**63, size=(chunk, circ.n_inputs, lanes),
@@ -283,10 +283,16 @@ def main():
         h_np = host_h.numpy().view(np.uint64)
 
         def e2e_step():
-            done = 0
+            # double-buffered ring: chunk k+1's inputs are copied (the library's copy
+            # stream) while chunk k is simulated; hashes come back per chunk
+            c0, done, staged = Ls.cycle, 0, min(chunk, cycles)
+            Ls.set_inputs(c0, in_np[:staged])
             while done < cycles:
                 n = min(chunk, cycles - done)
-                Ls.set_inputs(Ls.cycle, in_np[:n])
+                if staged < cycles:
+                    n2 = min(chunk, cycles - staged)
+                    Ls.set_inputs(c0 + staged, in_np[:n2])
+                    staged += n2
                 Ls.step(n, hashes=h_np[:n] if n == chunk else np.ascontiguousarray(h_np[:n]))
                 done += n
 
@@ -303,8 +309,8 @@ def main():
         e2e = {"value": lanes * world * cycles * e2e_steps / el, "unit": UNIT,
                "h2d_bytes_per_step": int(cycles * circ.n_inputs * lanes * 8),
                "d2h_bytes_per_step": int(cycles * lanes * 8), "steps": e2e_steps,
-               "path": "rs_set_inputs(host pinned) + rs_step_cycles(hashes=HOST) per chunk of "
-                       f"{chunk} cycles"}
+               "path": "rs_set_inputs(host pinned, next chunk, copy stream) + rs_step_cycles(hashes=HOST) "
+                       f"per chunk of {chunk} cycles (2-chunk ring)"}
         Ls.close()
 
     cpu = None

@@ -219,7 +219,12 @@ rs_status rs_set_input_seed(rs_lanes* s, uint64_t seed);
  * first_cycle + n_cycles): values[n_cycles][n_inputs][n_lanes] (u64, masked to
  * each input's width when injected), host (on_device = 0) or device memory
  * of the lanes' device (on_device = 1).  n_cycles <= stage_cycles.  The
- * ring keeps the last stage_cycles staged cycles. Async on the stream. */
+ * ring keeps the last stage_cycles staged cycles.  Asynchronous, on a copy
+ * stream of the allocation: the copy waits for the last launch that read the
+ * ring slots it overwrites, and a later rs_step_cycles waits for the copies
+ * of its cycles only -- so with a ring of two chunks the next chunk's
+ * transfer overlaps the current chunk's simulation.  Pinned host memory must
+ * stay valid until the step that reads it has run (rs_sync covers both). */
 rs_status rs_set_inputs(rs_lanes* s, uint64_t first_cycle, uint32_t n_cycles,
                         const uint64_t* values, int on_device);
 

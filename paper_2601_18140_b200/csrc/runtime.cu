@@ -94,6 +94,16 @@ struct rs_lanes {
   uint64_t* stage = nullptr;
   uint32_t stage_cap = 0;
   uint64_t st_lo = 0, st_hi = 0;    // staged window [st_lo, st_hi)
+  // staged-input copies run on their own stream so the next chunk's transfer
+  // overlaps the current chunk's step: a copy waits for the last launch that
+  // read the ring slots it overwrites; a step waits for the copies before it
+  cudaStream_t cstream = nullptr;
+  struct CycleRec { uint64_t c0 = 0, c1 = 0; cudaEvent_t ev = nullptr; };
+  CycleRec lrec[4];                 // the last 4 launches (cycles read)
+  uint64_t lrec_n = 0;
+  CycleRec crec[4];                 // the last 4 copies (cycles written)
+  uint64_t crec_n = 0;
+  uint64_t crec_waited = 0;         // copies [0, crec_waited) are ordered before the lanes' stream
   uint64_t* hbuf = nullptr;         // device hash temp for host outputs
   size_t hbuf_cap = 0;
   unsigned long long* bar = nullptr;
@@ -825,6 +835,14 @@ void rs_free_lanes(rs_lanes* s) {
   if (s->wave_count) cudaFree(s->wave_count);
   if (s->drep) cudaFree(s->drep);
   if (s->rep_mail) cudaFree(s->rep_mail);
+  if (s->cstream) {
+    cudaStreamSynchronize(s->cstream);
+    cudaStreamDestroy(s->cstream);
+  }
+  for (auto& r : s->lrec)
+    if (r.ev) cudaEventDestroy(r.ev);
+  for (auto& r : s->crec)
+    if (r.ev) cudaEventDestroy(r.ev);
   if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
   if (s->g && s->counted) s->g->live_lanes--;
   delete s;
@@ -849,13 +867,50 @@ rs_status rs_set_inputs(rs_lanes* s, uint64_t first_cycle, uint32_t n_cycles, co
   const uint32_t NI = s->g->cg.n_inputs;
   const size_t per = (size_t)NI * s->n_lanes;
   const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  if (!s->cstream) CU(cudaStreamCreateWithFlags(&s->cstream, cudaStreamNonBlocking));
+  if (n_cycles && per) {
+    // the ring slots of cycles [first_cycle, +n_cycles) may still be read by a
+    // recorded launch: wait for the latest launch whose cycles share a slot
+    // (launches run in order on the lanes' stream); launches evicted from the
+    // record ring are older than its oldest entry, which then stands for them
+    const uint64_t cap = s->stage_cap;
+    auto shares_slot = [&](uint64_t a0, uint64_t la, uint64_t b0, uint64_t lb) {
+      if (!la || !lb) return false;
+      if (la >= cap || lb >= cap) return true;
+      a0 %= cap;
+      b0 %= cap;
+      return (b0 + cap - a0) % cap < la || (a0 + cap - b0) % cap < lb;
+    };
+    const uint64_t kept = std::min<uint64_t>(s->lrec_n, 4);
+    cudaEvent_t wait = nullptr;
+    for (uint64_t j = 0; j < kept && !wait; ++j) {  // newest first
+      const auto& r = s->lrec[(s->lrec_n - 1 - j) % 4];
+      if (shares_slot(r.c0, r.c1 - r.c0, first_cycle, n_cycles)) wait = r.ev;
+    }
+    if (!wait && s->lrec_n > 4) wait = s->lrec[(s->lrec_n - kept) % 4].ev;
+    if (wait) CU(cudaStreamWaitEvent(s->cstream, wait, 0));
+  }
   uint32_t done = 0;
   while (done < n_cycles && per) {
     const uint64_t c = first_cycle + done;
     const uint32_t slot = (uint32_t)(c % s->stage_cap);
     const uint32_t n = std::min<uint32_t>(n_cycles - done, s->stage_cap - slot);
-    CU(cudaMemcpyAsync(s->stage + (size_t)slot * per, values + (size_t)done * per, (size_t)n * per * 8, kind, s->stream));
+    CU(cudaMemcpyAsync(s->stage + (size_t)slot * per, values + (size_t)done * per, (size_t)n * per * 8, kind,
+                       s->cstream));
     done += n;
+  }
+  if (n_cycles && per) {
+    auto& r = s->crec[s->crec_n % 4];
+    if (s->crec_n >= 4 && s->crec_waited < s->crec_n - 3) {
+      // the record about to be reused was never waited for: order it now
+      CU(cudaStreamWaitEvent(s->stream, r.ev, 0));
+      s->crec_waited = s->crec_n - 3;
+    }
+    if (!r.ev) CU(cudaEventCreateWithFlags(&r.ev, cudaEventDisableTiming));
+    r.c0 = first_cycle;
+    r.c1 = first_cycle + n_cycles;
+    CU(cudaEventRecord(r.ev, s->cstream));
+    s->crec_n++;
   }
   // staged window
   if (s->staged && first_cycle <= s->st_hi && first_cycle >= s->st_lo) {
@@ -920,6 +975,20 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
     hout = s->hbuf;
   }
   (void)cudaGetLastError();  // clear a stale non-sticky error of an unrelated earlier call
+  if (s->staged && s->crec_waited < s->crec_n) {
+    // the newest copy that wrote any of this launch's cycles must come first
+    // (copies run in order on the copy stream, so it stands for older ones);
+    // copies of later cycles (the next chunk) keep running beside the launch
+    const uint64_t c0 = s->cycle, c1 = s->cycle + n_cycles;
+    for (uint64_t j = s->crec_n; j > s->crec_waited; --j) {
+      const auto& r = s->crec[(j - 1) % 4];
+      if (r.c0 < c1 && c0 < r.c1) {
+        CU(cudaStreamWaitEvent(s->stream, r.ev, 0));
+        s->crec_waited = j;
+        break;
+      }
+    }
+  }
   StepArgs a = base_args(s);
   a.cycle0 = s->cycle;
   a.n_cycles = n_cycles;
@@ -1009,6 +1078,14 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
     if (e != cudaSuccess) return set_err(RS_E_CUDA, "k_lanes launch: %s", cudaGetErrorString(e));
   }
   s->launches++;
+  if (s->staged) {  // which cycles (ring slots) this launch reads, for later rs_set_inputs
+    auto& r = s->lrec[s->lrec_n % 4];
+    if (!r.ev) CU(cudaEventCreateWithFlags(&r.ev, cudaEventDisableTiming));
+    r.c0 = s->cycle;
+    r.c1 = s->cycle + n_cycles;
+    CU(cudaEventRecord(r.ev, s->stream));
+    s->lrec_n++;
+  }
   if (!hash) s->hc_valid = false;
   s->cycle += n_cycles;
   if (hashes_mem == RS_MEM_HOST) {
@@ -1206,6 +1283,7 @@ rs_status rs_sync(rs_lanes* s) {
   if (!s) return set_err(RS_E_INVALID_ARG, "NULL lanes");
   rs_status st = set_device(s->g);
   if (st != RS_OK) return st;
+  if (s->cstream) CU(cudaStreamSynchronize(s->cstream));
   CU(cudaStreamSynchronize(s->stream));
   return RS_OK;
 }

@@ -164,6 +164,30 @@ def test_chunking_and_hash_toggle(rs, kernel):
     assert L.cycle == 21
 
 
+@pytest.mark.parametrize("mode,kernel", [("lanes", 1), ("lanes", 2), ("single", 0), ("single", 5)])
+def test_staged_inputs_pipelined(rs, mode, kernel):
+    """The next chunk is staged (copy stream) before the current one is stepped,
+    with a ring of two chunks: every copy must wait for the launch that last
+    read its slots, every step for the copies before it."""
+    c = config_circuit("C2", n_ops=3000, n_levels=15, n_regs=300) if mode == "lanes" else config_circuit("C1")
+    rng = np.random.default_rng(5)
+    n, ch = 60, 6
+    nl = (130 if kernel == 1 else 33) if mode == "lanes" else 1
+    vals = rng.integers(0, 2**63, size=(n, c.n_inputs, nl), dtype=np.int64).astype(np.uint64)
+    g = rs.Graph(c, mode=mode)
+    L = rs.Lanes(g, nl, stage_cycles=2 * ch, kernel=kernel)
+    L.set_inputs(0, vals[0:ch])
+    hs = []
+    for c0 in range(0, n, ch):
+        if c0 + ch < n:
+            L.set_inputs(c0 + ch, vals[c0 + ch:c0 + 2 * ch])
+        hs.append(L.step(ch, hashes="host"))
+    r = oracle.simulate(c, n, n_lanes=nl, staged=vals)
+    assert np.array_equal(np.concatenate(hs), r.hashes)
+    F = L.read(list(range(c.n_signals)))
+    assert np.array_equal(F, oracle.simulate(c, n, n_lanes=nl, staged=vals, final=True).final_state)
+
+
 @pytest.mark.parametrize("kernel", [1, 2])
 def test_staged_inputs_chunks(rs, kernel):
     c = config_circuit("C2", n_ops=3000, n_levels=15, n_regs=300)
