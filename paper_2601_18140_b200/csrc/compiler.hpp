@@ -132,7 +132,7 @@ struct StageHdr {          // first 64 bytes of a stage block
 
 // Ops per work item of an OPS stage (the gather batch of the lane kernel).
 #ifndef RS_BATCH
-#define RS_BATCH 4
+#define RS_BATCH 2
 #endif
 constexpr uint32_t kBatch = RS_BATCH;   // <= 8 (3-bit count field of a work item)
 

@@ -171,7 +171,8 @@ struct BatchU {
 #ifndef RS_BATCHU_P4_A3
 #define RS_BATCHU_P4_A3 1  // keeps k_lanes_t<4, 1> at 80 registers without spills (768-thread CTAs)
 #endif
-  static constexpr int value = (P == 4) ? (A == 3 ? RS_BATCHU_P4_A3 : RS_BATCHU_P4) : (P == 2 && A == 3) ? 2 : 4;
+  static constexpr int raw = (P == 4) ? (A == 3 ? RS_BATCHU_P4_A3 : RS_BATCHU_P4) : (P == 2 && A == 3) ? 2 : 4;
+  static constexpr int value = raw < (int)kBatch ? raw : (int)kBatch;  // a work item has <= kBatch ops
 };
 
 // cnt <= U ops of one run: op = opcode, outputs from coordinate ob (rows LT << out_cls apart).
