@@ -362,21 +362,21 @@ struct StageWriter {
   }
 };
 
-// Upper bound of a stage's bytes (OPS items bounded by n / kBatch + n_runs).
-uint32_t stage_size(uint32_t n, uint32_t n_coords, uint32_t n_runs) {
+// Upper bound of a stage's bytes (OPS items bounded by n / batch + n_runs).
+uint32_t stage_size(uint32_t n, uint32_t n_coords, uint32_t n_runs, uint32_t batch) {
   uint32_t off_w = al16((uint32_t)sizeof(StageHdr));
   uint32_t off_k = al16(off_w + 4 * n);
   uint32_t off_c = al16(off_k + 8 * n);
   uint32_t off_r = al16(off_c + 4 * n_coords);
   uint32_t off_i = al16(off_r + (uint32_t)sizeof(StageRun) * n_runs);
-  const uint32_t items = n_runs ? n / kBatch + n_runs : 0;
+  const uint32_t items = n_runs ? n / batch + n_runs : 0;
   return al16(off_i + 4 * items);
 }
 
 constexpr uint32_t kMaxStageOps = 8191;   // 13-bit op field of a work item
 }  // namespace
 
-void build_stages(const CompiledGraph& g, uint32_t stage_bytes, std::vector<uint8_t>* blob,
+void build_stages(const CompiledGraph& g, uint32_t stage_bytes, uint32_t batch, std::vector<uint8_t>* blob,
                   std::vector<StageRef>* table) {
   blob->clear();
   table->clear();
@@ -386,7 +386,7 @@ void build_stages(const CompiledGraph& g, uint32_t stage_bytes, std::vector<uint
     uint32_t i = 0;
     while (i < g.n_inputs) {
       uint32_t n = 0;
-      while (i + n < g.n_inputs && stage_size(n + 1, n + 1, 0) <= stage_bytes) ++n;
+      while (i + n < g.n_inputs && stage_size(n + 1, n + 1, 0, batch) <= stage_bytes) ++n;
       StageHdr h{};
       h.type = ST_INJECT;
       h.n = n;
@@ -408,7 +408,7 @@ void build_stages(const CompiledGraph& g, uint32_t stage_bytes, std::vector<uint
         while (rr + 1 < g.level_run_begin[l + 1] && g.runs[rr + 1].op_begin <= e) ++rr;
         const bool new_run = (e == j) || (g.runs[rr].op_begin == e);
         const uint32_t ar = g.coord_off[e + 1] - g.coord_off[e];
-        if ((stage_size(e - j + 1, ncoords + ar, nruns + (new_run ? 1 : 0)) > stage_bytes || e - j >= kMaxStageOps) &&
+        if ((stage_size(e - j + 1, ncoords + ar, nruns + (new_run ? 1 : 0), batch) > stage_bytes || e - j >= kMaxStageOps) &&
             e > j)
           break;
         nruns += new_run ? 1 : 0;
@@ -430,11 +430,11 @@ void build_stages(const CompiledGraph& g, uint32_t stage_bytes, std::vector<uint
         runs.push_back(sr);
         k = se;
       }
-      // work items: run-aligned batches of <= kBatch ops
+      // work items: run-aligned batches of <= batch ops
       std::vector<uint32_t> items;
       for (uint32_t q = 0; q < runs.size(); ++q)
-        for (uint32_t o = 0; o < runs[q].count; o += kBatch) {
-          const uint32_t cnt = std::min(kBatch, runs[q].count - o);
+        for (uint32_t o = 0; o < runs[q].count; o += batch) {
+          const uint32_t cnt = std::min(batch, runs[q].count - o);
           items.push_back((q << 16) | ((cnt - 1) << 13) | (runs[q].op_begin + o));
         }
       StageHdr h{};
@@ -454,7 +454,7 @@ void build_stages(const CompiledGraph& g, uint32_t stage_bytes, std::vector<uint
     uint32_t i = 0;
     while (i < g.n_regs) {
       uint32_t n = 0;
-      while (i + n < g.n_regs && stage_size(n + 1, 2 * (n + 1), 0) <= stage_bytes) ++n;
+      while (i + n < g.n_regs && stage_size(n + 1, 2 * (n + 1), 0, batch) <= stage_bytes) ++n;
       std::vector<uint32_t> pairs(2 * n);
       for (uint32_t q = 0; q < n; ++q) {
         pairs[2 * q] = g.reg_next_coord[i + q];

@@ -125,16 +125,19 @@ struct StageHdr {          // first 64 bytes of a stage block
   uint32_t off_c;          // u32[..]: op operand coords | input coords | (next, reg) coord pairs
   uint32_t off_runs;       // StageRun[n_runs]
   uint32_t bytes;
-  uint32_t n_items;        // OPS: work items (run-aligned batches of <= kBatch ops)
+  uint32_t n_items;        // OPS: work items (run-aligned batches of <= `batch` ops)
   uint32_t off_items;      // u32[n_items]: run << 16 | (count - 1) << 13 | first op (stage-relative)
   uint32_t pad[3];
 };
 
-// Ops per work item of an OPS stage (the gather batch of the lane kernel).
+// Ops per work item of an OPS stage: kernel 2's gather batch (its items never
+// hold more), and kernel 1's default; kernel 1 takes items of kBatchWide ops
+// when a CTA has many ops per level (build_stages' `batch`; runtime.cu).
 #ifndef RS_BATCH
 #define RS_BATCH 2
 #endif
 constexpr uint32_t kBatch = RS_BATCH;   // <= 8 (3-bit count field of a work item)
+constexpr uint32_t kBatchWide = 4;
 
 struct StageRun {          // a run clipped to the stage; indices relative to the stage
   uint32_t op_begin;
@@ -152,7 +155,7 @@ struct StageRef {
 };
 
 // Build the per-cycle stage schedule with blocks of at most stage_bytes.
-void build_stages(const CompiledGraph& g, uint32_t stage_bytes, std::vector<uint8_t>* blob,
+void build_stages(const CompiledGraph& g, uint32_t stage_bytes, uint32_t batch, std::vector<uint8_t>* blob,
                   std::vector<StageRef>* table);
 
 // ---------------------------------------------------------------- single-lane slices

@@ -65,8 +65,11 @@ struct rs_graph {
   int live_lanes = 0;
   // lane mode stage schedule (compiler.hpp build_stages)
   // (host copy; every allocation binds it to its own layout, see bind_stages)
-  std::vector<uint8_t> stage_blob;
-  std::vector<StageRef> stage_tab;
+  // lane-mode stage schedules, by work-item size: [0] kBatch ops (built at
+  // load), [1] kBatchWide ops (built on first use)
+  std::vector<uint8_t> stage_blob[2];
+  std::vector<StageRef> stage_tab[2];
+  bool stages_built[2] = {false, false};
   uint32_t stage_bytes = 0;
 };
 
@@ -94,6 +97,7 @@ struct rs_lanes {
   uint64_t* stage = nullptr;
   uint32_t stage_cap = 0;
   uint64_t st_lo = 0, st_hi = 0;    // staged window [st_lo, st_hi)
+  uint32_t batch_idx = 0;           // rs_graph stage schedule in use (work-item size)
   // staged-input copies run on their own stream so the next chunk's transfer
   // overlaps the current chunk's step: a copy waits for the last launch that
   // read the ring slots it overwrites; a step waits for the copies before it
@@ -178,13 +182,13 @@ StepArgs base_args(const rs_lanes* s) {
 // coordinate (class << 30 | row) becomes (class << 30 | byte offset of the
 // row's lane 0 inside a tile); run out rows become byte offsets.  Requires
 // tile_bytes < 2^30.
-void bind_stages(const rs_graph* g, uint32_t LT, const uint64_t* region, std::vector<uint8_t>* out) {
-  *out = g->stage_blob;
+void bind_stages(const rs_graph* g, uint32_t bi, uint32_t LT, const uint64_t* region, std::vector<uint8_t>* out) {
+  *out = g->stage_blob[bi];
   auto bind = [&](uint32_t c) -> uint32_t {
     const uint32_t cls = c >> 30, row = c & ROW_MASK;
     return (cls << 30) | (uint32_t)(region[cls] + ((uint64_t)row * LT << cls));
   };
-  for (const StageRef& r : g->stage_tab) {
+  for (const StageRef& r : g->stage_tab[bi]) {
     uint8_t* p = out->data() + r.off;
     StageHdr h;
     std::memcpy(&h, p, sizeof h);
@@ -203,8 +207,8 @@ void bind_stages(const rs_graph* g, uint32_t LT, const uint64_t* region, std::ve
 rs_status upload_schedule(rs_lanes* s) {
   const rs_graph* g = s->g;
   std::vector<uint8_t> bound;
-  bind_stages(g, s->LT, s->region, &bound);
-  std::vector<StageRef> tab = g->stage_tab;
+  bind_stages(g, s->batch_idx, s->LT, s->region, &bound);
+  std::vector<StageRef> tab = g->stage_tab[s->batch_idx];
   if (!s->watch.empty()) {
     StageHdr h{};
     h.type = ST_WATCH;
@@ -382,7 +386,8 @@ rs_status rs_load_graph(const rs_graph_desc* desc, int device, uint32_t mode, rs
   cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, device);
   if (mode == RS_MODE_LANES) {
     g->stage_bytes = kStageBytes;
-    build_stages(cg, g->stage_bytes, &g->stage_blob, &g->stage_tab);
+    build_stages(cg, g->stage_bytes, kBatch, &g->stage_blob[0], &g->stage_tab[0]);
+    g->stages_built[0] = true;
   }
   *out = g;
   return RS_OK;
@@ -751,6 +756,17 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     return set_err(RS_E_OOM, "cudaMalloc state (%zu B): %s", s->state_bytes, cudaGetErrorString(e));
   }
   if (g->cg.mode == RS_MODE_LANES) {
+    // work items: kernel 1 takes kBatchWide-op items when its CTAs have many ops
+    // per level (C4: ~6,700; fewer, longer items cut the per-item decode), else
+    // kBatch-op items (more items to deal when a level is short: C3 ~470)
+    const uint64_t ops_per_cta_level =
+        g->cg.n_levels ? (uint64_t)g->cg.n_ops_total() / g->cg.n_levels / std::max<uint32_t>(1, s->cluster) : 0;
+    s->batch_idx = (s->variant == 1 && ops_per_cta_level >= 2048) ? 1u : 0u;
+    if (!g->stages_built[s->batch_idx]) {
+      build_stages(g->cg, g->stage_bytes, s->batch_idx ? kBatchWide : kBatch, &g->stage_blob[s->batch_idx],
+                   &g->stage_tab[s->batch_idx]);
+      g->stages_built[s->batch_idx] = true;
+    }
     if ((st = upload_schedule(s)) != RS_OK) {
       rs_free_lanes(s);
       return st;

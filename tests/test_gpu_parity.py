@@ -164,6 +164,14 @@ def test_chunking_and_hash_toggle(rs, kernel):
     assert L.cycle == 21
 
 
+@pytest.mark.parametrize("cluster", [1, 2])
+def test_wide_work_items(rs, cluster):
+    """Kernel 1 with kBatchWide-op work items (>= 2,048 ops per CTA and level:
+    cluster 1) and with kBatch-op items (cluster 2), ragged lanes."""
+    c = config_circuit("C3", n_ops=60000, n_levels=20, n_regs=3000)
+    check(rs, c, 5, 70, seed=9, kernel=1, lane_tile=64, cluster=cluster)
+
+
 @pytest.mark.parametrize("mode,kernel", [("lanes", 1), ("lanes", 2), ("single", 0), ("single", 5)])
 def test_staged_inputs_pipelined(rs, mode, kernel):
     """The next chunk is staged (copy stream) before the current one is stepped,
