@@ -137,7 +137,10 @@ struct StageHdr {          // first 64 bytes of a stage block
 #define RS_BATCH 2
 #endif
 constexpr uint32_t kBatch = RS_BATCH;   // <= 8 (3-bit count field of a work item)
-constexpr uint32_t kBatchWide = 4;
+#ifndef RS_BATCH_WIDE
+#define RS_BATCH_WIDE 4
+#endif
+constexpr uint32_t kBatchWide = RS_BATCH_WIDE;  // <= 8
 
 struct StageRun {          // a run clipped to the stage; indices relative to the stage
   uint32_t op_begin;
