@@ -1,15 +1,20 @@
-// repcut.cuh -- replicated-cut single-lane kernel (k_repcut; rs_lane_opts.repcut).
+// repcut.cuh -- replicated-cut single-lane kernels (rs_lane_opts.repcut; the
+// single-lane auto choice with one partition when a design fits one SM).
 //
 // The RepCut cascade (App. C, Cascade 2 P:2021-2078; SURVEY.md §8(f)
 // NEXT-2): partition p = CTA p of a cooperative launch owns a block of the
 // registers and evaluates the combinational cone of their next values
-// (compiler.hpp build_repcut: shared logic replicated) on its OWN state
-// replica, so the levels of a cycle need only CTA barriers -- no grid barrier
+// (compiler.hpp build_repcut: shared logic replicated) on its OWN copy of the
+// state, so the levels of a cycle need only CTA barriers -- no grid barrier
 // per level as in single.cuh.  After the register commit, the Register Update
-// Map (Cascade 2's last Einsum, LI_{c+1} = LI_{c,I} . RUM) pushes every
-// register's new value into the replicas of the partitions that read it, with
-// one grid barrier on each side of the push.  Hash terms (reading R12) are
-// added by the one partition that owns each op (inputs: partition 0).
+// Map (Cascade 2's last Einsum, LI_{c+1} = LI_{c,I} . RUM) delivers every
+// register's new value to the partitions that read it.  Hash terms (reading
+// R12) are added by the one partition that owns each op.
+//   k_repcut      -- state replicas in global memory; RUM as a push between two
+//                    grid barriers (inputs hashed by partition 0);
+//   k_repcut_smem -- working set in shared memory; RUM as a pull through a
+//                    mailbox after one grid barrier (inputs hashed by their
+//                    lowest reader).
 #pragma once
 #include "kernels.cuh"
 
