@@ -3,6 +3,7 @@
 //   * L2 capacity attributes, L2-resident and HBM read bandwidth
 //   * dependent-load latency (L2 hit, HBM)
 //   * __syncthreads, barrier.cluster and grid-barrier (atomic flag) latency
+//   * 64-bit integer multiply-add and 64-bit logic throughput (the op and hash ALU work)
 // Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/microbench tools/microbench.cu
 // Prints one JSON object.
 #include <cooperative_groups.h>
@@ -38,6 +39,26 @@ __global__ void k_chase(const uint32_t* __restrict__ next, uint32_t start, int s
   const unsigned long long t1 = clock64();
   cyc[0] = t1 - t0;
   sink[0] = i;
+}
+
+// 8 independent chains per thread: a = a * b + c (64-bit; the fused hash term) or
+// a = (a ^ b) & c | d (64-bit logic; the op evaluation), iters rounds.
+template <int KIND>
+__global__ void k_alu64(int iters, uint64_t seed, uint64_t* out) {
+  uint64_t a[8], b = seed * 0x9E3779B97F4A7C15ull + threadIdx.x, c = b ^ 0x5EEDull, d = ~b;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = b + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (KIND == 0) a[k] = a[k] * b + c;
+      else a[k] = ((a[k] ^ b) & c) | (d + a[k]);
+    }
+  }
+  uint64_t r = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) r ^= a[k];
+  if (r == 42) out[0] = r;
 }
 
 __global__ void k_syncthreads(int iters, unsigned long long* cyc) {
@@ -182,6 +203,31 @@ int main() {
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost));
     printf(", \"grid%d_cg_sync_cycles\": %.1f", grid, c / (double)it);
+  }
+  {  // 64-bit ALU throughput, whole GPU (ops per second, one op = one 64-bit multiply-add / logic step)
+    uint64_t* out;
+    CK(cudaMalloc(&out, 8));
+    const int iters = 1 << 14, blocks = sms * 8, threads = 256;
+    for (int kind = 0; kind < 2; ++kind) {
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      auto launch = [&]() {
+        if (kind == 0) k_alu64<0><<<blocks, threads>>>(iters, 3, out);
+        else k_alu64<1><<<blocks, threads>>>(iters, 3, out);
+      };
+      launch();
+      CK(cudaDeviceSynchronize());
+      cudaEventRecord(e0);
+      launch();
+      cudaEventRecord(e1);
+      CK(cudaEventSynchronize(e1));
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      const double ops = (double)blocks * threads * iters * 8;
+      printf(", \"%s_gops\": %.1f", kind == 0 ? "int64_madd" : "int64_logic", ops / (ms * 1e-3) / 1e9);
+    }
+    cudaFree(out);
   }
   printf("}\n");
   return 0;
