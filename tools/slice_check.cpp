@@ -38,7 +38,7 @@ int main(int argc, char** argv) {
   if (rtlsim::compile_graph(&d, RS_MODE_SINGLE, &g, &err) != RS_OK) { printf("compile: %s\n", err.c_str()); return 1; }
   std::vector<uint8_t> blob;
   std::vector<uint64_t> off;
-  bool ok = rtlsim::build_single_slices(g, G, 1u << 30, &blob, &off);
+  bool ok = rtlsim::build_single_slices(g, 1, G, 1u << 30, &blob, &off);  // one partition (no level cut)
   uint32_t mx = 0, mn = ~0u;
   for (unsigned i = 0; i < G; ++i) {
     const auto* h = reinterpret_cast<const rtlsim::SliceHdr*>(blob.data() + off[i]);
@@ -47,8 +47,8 @@ int main(int argc, char** argv) {
   printf("G=%u ok=%d slice bytes min %u max %u (levels %u)\n", G, ok, mn, mx, g.n_levels);
   for (unsigned i = 0; i < G; i += (G > 8 ? G / 8 : 1)) {
     const auto* h = reinterpret_cast<const rtlsim::SliceHdr*>(blob.data() + off[i]);
-    printf("  cta %u: bytes %u lvl@%u seg@%u pw@%u cofs@%u coord@%u latch@%u inj@%u\n", i, h->bytes, h->off_lvl, h->off_seg,
-           h->off_pw, h->off_cofs, h->off_coord, h->off_latch, h->off_inj);
+    printf("  cta %u: bytes %u (head %u) lvl@%u seg@%u pw@%u coord@%u push@%u latch@%u inj@%u\n", i, h->bytes,
+           h->head_bytes, h->off_lvl, h->off_seg, h->off_pw, h->off_coord, h->off_push, h->off_latch, h->off_inj);
   }
   return 0;
 }
