@@ -1,0 +1,68 @@
+"""Randomised parity sweep: fuzz-corpus circuits under random launch options
+(lane kernel, tile, cluster, threads; single-lane kernel, RepCut partitions,
+level cut), hashes and final state vs the oracle.
+
+    python tools/stress_fuzz.py [n_cases] [seed]
+"""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import oracle  # noqa: E402
+from paper_2601_18140_b200 import rtlsim as rs  # noqa: E402
+from synth import fuzz_circuit  # noqa: E402
+
+
+def main():
+    n_cases = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+    rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 11)
+    bad = 0
+    for it in range(n_cases):
+        seed = int(rng.integers(0, 100000))
+        c = fuzz_circuit(seed)
+        cycles = int(rng.integers(1, 40))
+        if rng.random() < 0.6:
+            mode = "lanes"
+            kernel = int(rng.integers(1, 3))
+            lt = int(rng.choice([32, 64, 128] if kernel == 1 else [8, 16, 32]))
+            cs = int(rng.choice([1, 2, 4]))
+            nl = int(rng.integers(1, 300))
+            th = int(rng.choice([0, 64, 128, 256]))
+            if kernel == 2 and th and th < lt:
+                th = 0
+            opts = dict(kernel=kernel, lane_tile=lt, cluster=cs, threads=th)
+        else:
+            mode, nl = "single", 1
+            g0 = rs.Graph(c, device=rs.RS_DEVICE_NONE, mode="single")
+            nlev, nreg = g0.info()["n_levels"], len(c.reg_id)
+            g0.close()
+            pick = rng.integers(0, 4)
+            if pick == 0 or nreg == 0:
+                opts = dict(kernel=5)
+            elif pick == 1:
+                opts = dict(repcut=int(rng.integers(1, min(nreg, 8) + 1)))
+            elif pick == 2:
+                opts = dict(repcut=int(rng.integers(1, min(nreg, 8) + 1)), repcut_global=True)
+            else:
+                opts = dict(kernel=5, parts=int(rng.integers(1, min(max(nlev, 1), 4) + 1)))
+        g = rs.Graph(c, device=0, mode=mode)
+        L = rs.Lanes(g, nl, **opts)
+        L.set_seed(seed)
+        H = L.step(cycles, hashes="host")
+        F = L.read(list(range(c.n_signals)))
+        r = oracle.simulate(c, cycles, seed=seed, n_lanes=nl, final=True, threads=8)
+        ok = np.array_equal(H, r.hashes) and np.array_equal(F, r.final_state)
+        bad += not ok
+        if not ok or it % 20 == 0:
+            print(f"case {it}: seed {seed} {mode} lanes {nl} cycles {cycles} {opts} shape {L.shape()} -> "
+                  f"{'ok' if ok else 'MISMATCH'}", flush=True)
+        L.close()
+        g.close()
+    print("cases", n_cases, "mismatches", bad)
+    sys.exit(1 if bad else 0)
+
+
+if __name__ == "__main__":
+    main()
