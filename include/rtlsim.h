@@ -224,7 +224,9 @@ rs_status rs_set_input_seed(rs_lanes* s, uint64_t seed);
  * ring slots it overwrites, and a later rs_step_cycles waits for the copies
  * of its cycles only -- so with a ring of two chunks the next chunk's
  * transfer overlaps the current chunk's simulation.  Pinned host memory must
- * stay valid until the step that reads it has run (rs_sync covers both). */
+ * stay valid until the step that reads it has run (rs_sync covers both);
+ * device values are copied after all work already queued on the lanes'
+ * stream (so a producer kernel on that stream is complete). */
 rs_status rs_set_inputs(rs_lanes* s, uint64_t first_cycle, uint32_t n_cycles,
                         const uint64_t* values, int on_device);
 

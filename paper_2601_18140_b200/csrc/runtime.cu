@@ -108,6 +108,7 @@ struct rs_lanes {
   CycleRec crec[4];                 // the last 4 copies (cycles written)
   uint64_t crec_n = 0;
   uint64_t crec_waited = 0;         // copies [0, crec_waited) are ordered before the lanes' stream
+  cudaEvent_t ev_order = nullptr;   // device-to-device staging follows the lanes' stream
   uint64_t* hbuf = nullptr;         // device hash temp for host outputs
   size_t hbuf_cap = 0;
   unsigned long long* bar = nullptr;
@@ -859,6 +860,7 @@ void rs_free_lanes(rs_lanes* s) {
     if (r.ev) cudaEventDestroy(r.ev);
   for (auto& r : s->crec)
     if (r.ev) cudaEventDestroy(r.ev);
+  if (s->ev_order) cudaEventDestroy(s->ev_order);
   if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
   if (s->g && s->counted) s->g->live_lanes--;
   delete s;
@@ -905,6 +907,13 @@ rs_status rs_set_inputs(rs_lanes* s, uint64_t first_cycle, uint32_t n_cycles, co
     }
     if (!wait && s->lrec_n > 4) wait = s->lrec[(s->lrec_n - kept) % 4].ev;
     if (wait) CU(cudaStreamWaitEvent(s->cstream, wait, 0));
+    if (on_device) {
+      // device values may be produced by work queued on the lanes' stream
+      // (the caller's): the copy follows everything queued there so far
+      if (!s->ev_order) CU(cudaEventCreateWithFlags(&s->ev_order, cudaEventDisableTiming));
+      CU(cudaEventRecord(s->ev_order, s->stream));
+      CU(cudaStreamWaitEvent(s->cstream, s->ev_order, 0));
+    }
   }
   uint32_t done = 0;
   while (done < n_cycles && per) {

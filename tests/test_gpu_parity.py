@@ -196,6 +196,27 @@ def test_staged_inputs_pipelined(rs, mode, kernel):
     assert np.array_equal(F, oracle.simulate(c, n, n_lanes=nl, staged=vals, final=True).final_state)
 
 
+def test_staged_inputs_from_device_stream(rs):
+    """Device-resident stimulus produced by kernels on the lanes' stream and
+    staged right away (no host sync): the copy must follow that work."""
+    import torch
+    c = config_circuit("C2", n_ops=2000, n_levels=10, n_regs=200)
+    n, nl = 24, 96
+    vals = np.random.default_rng(2).integers(0, 2**62, size=(n, c.n_inputs, nl), dtype=np.int64)
+    st = torch.cuda.Stream()
+    g = rs.Graph(c)
+    L = rs.Lanes(g, nl, stage_cycles=n, stream=st, kernel=2)
+    with torch.cuda.stream(st):
+        base = torch.from_numpy(vals).cuda()
+        for _ in range(8):                 # a queue of kernels producing the values
+            base = base * 3 - base * 2
+        t = base.view(torch.uint64) if hasattr(torch, "uint64") else base
+        L.set_inputs(0, t)
+        H = L.step(n, hashes="host")
+    r = oracle.simulate(c, n, n_lanes=nl, staged=vals.astype(np.uint64))
+    assert np.array_equal(H, r.hashes)
+
+
 @pytest.mark.parametrize("kernel", [1, 2])
 def test_staged_inputs_chunks(rs, kernel):
     c = config_circuit("C2", n_ops=3000, n_levels=15, n_regs=300)
