@@ -261,17 +261,19 @@ rs_status rs_launch_shape(const rs_lanes* s, uint32_t* lane_tile, uint32_t* thre
 uint32_t rs_lanes_kernel(const rs_lanes* s);
 rs_status rs_sync(rs_lanes* s);
 /* ---- Waveform capture (§6.2: the
- * DMI dumps waveforms of selected signals).  rs_watch selects up to 2^16
- * canonical signal ids of a RS_MODE_LANES allocation; every later
- * rs_step_cycles then records, fused into the step kernel (one extra stage per
- * cycle, after the last level and before the register commit), a CHANGE
+ * DMI dumps waveforms of selected signals).  rs_watch selects up to 8192
+ * canonical signal ids of an allocation; every later rs_step_cycles then
+ * records, fused into the step kernel (lane mode: one extra stage per cycle;
+ * single lane: a pass over the watched signals, plus one grid barrier on the
+ * level-synchronous grid, after the last level and before the commit), a CHANGE
  * record for each (watched signal, lane) whose value after the combinational
  * evaluation of cycle c -- the snapshot the per-cycle hash covers -- differs
  * from its value at cycle c - 1, and for every (signal, lane) at the first
  * stepped cycle after rs_watch.  Records are appended to a device buffer of
  * `capacity` records in no particular order; records beyond capacity are
  * counted as dropped.  n_ids = 0 stops watching (and frees the buffers).
- * RS_E_RANGE for an unknown id, RS_E_UNSUPPORTED in RS_MODE_SINGLE. */
+ * RS_E_RANGE for an unknown id; RS_E_UNSUPPORTED for a level cut (parts > 1)
+ * or the global-replica RepCut kernel. */
 typedef struct {
   uint64_t cycle;   /* absolute cycle */
   uint64_t lane;    /* global lane id (rs_lane_opts.lane0 + allocation lane) */

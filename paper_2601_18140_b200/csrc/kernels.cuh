@@ -86,7 +86,30 @@ struct StepArgs {
   unsigned long long* wave_count;
   uint64_t wave_cap;
   uint64_t wave_first;         // records are unconditional at this absolute cycle
+  // single-lane waveform capture: watch entries (k_single2: signal coords;
+  // k_repcut_smem: per-partition {local offset, watch index} pairs from
+  // watch_begin[p]), 0 entries = off
+  const uint32_t* watch_ent;
+  const uint32_t* watch_begin;
+  uint32_t n_watch;
 };
+
+// One watched value of the single lane (watch index j) at `cycle`: a change
+// record when it differs from the previous cycle's (always at wave_first).
+__device__ __forceinline__ void watch_single(const StepArgs& a, uint32_t j, uint64_t v, uint64_t cycle) {
+  uint64_t* prev = a.wave_prev + j;
+  const bool rec = cycle == a.wave_first || *prev != v;
+  *prev = v;
+  if (!rec) return;
+  const unsigned long long i = atomicAdd(a.wave_count, 1ull);
+  if (i < a.wave_cap) {
+    uint64_t* r = a.wave_rec + 4 * i;
+    r[0] = cycle;
+    r[1] = a.lane0;
+    r[2] = j;
+    r[3] = v;
+  }
+}
 
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ uint64_t wmask(uint32_t w) { return ~0ull >> (64u - w); }  // w in 1..64

@@ -233,6 +233,12 @@ __global__ void __launch_bounds__(1024, 1) k_repcut_smem(const RepSmemArgs ra) {
       b = e;
       e = en;
     }
+    if (a.n_watch) {  // waveform (rs_watch): this partition's watched signals, before the commit
+#pragma unroll 1
+      for (uint32_t i = a.watch_begin[p] + tid; i < a.watch_begin[p + 1]; i += T)
+        watch_single(a, a.watch_ent[2 * i + 1], S.ld(a.watch_ent[2 * i]), cycle);
+      __syncthreads();
+    }
     // commit: the pre-commit values are this cycle's register hash terms
     uint64_t* mail = ra.mail + (size_t)(cyc & 1u) * R;
 #pragma unroll 1

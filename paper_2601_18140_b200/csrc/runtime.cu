@@ -80,6 +80,9 @@ struct rs_lanes {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   bool counted = false;       // counted in g->live_lanes (a fully built allocation)
+  void* dwatch = nullptr;      // single-lane watch entries (device)
+  const uint32_t* watch_ent = nullptr;
+  const uint32_t* watch_begin = nullptr;
   void* state_mem = nullptr;       // [n_tiles][tile_bytes]
   size_t state_bytes = 0;
   uint64_t tile_bytes = 0;
@@ -176,6 +179,9 @@ StepArgs base_args(const rs_lanes* s) {
   a.wave_count = s->wave_count;
   a.wave_cap = s->wave_cap;
   a.wave_first = s->wave_first;
+  a.watch_ent = s->watch_ent;
+  a.watch_begin = s->watch_begin;
+  a.n_watch = s->g->cg.mode == RS_MODE_SINGLE ? (uint32_t)s->watch.size() : 0u;
   return a;
 }
 
@@ -852,6 +858,7 @@ void rs_free_lanes(rs_lanes* s) {
   if (s->wave_count) cudaFree(s->wave_count);
   if (s->drep) cudaFree(s->drep);
   if (s->rep_mail) cudaFree(s->rep_mail);
+  if (s->dwatch) cudaFree(s->dwatch);
   if (s->cstream) {
     cudaStreamSynchronize(s->cstream);
     cudaStreamDestroy(s->cstream);
@@ -1243,7 +1250,11 @@ rs_status rs_debug_trace(rs_lanes* s, uint64_t* out, uint64_t n) {
 
 rs_status rs_watch(rs_lanes* s, const uint32_t* ids, uint32_t n_ids, uint64_t capacity) {
   if (!s || (n_ids && !ids)) return set_err(RS_E_INVALID_ARG, "NULL argument");
-  if (s->g->cg.mode != RS_MODE_LANES) return set_err(RS_E_UNSUPPORTED, "waveform capture needs RS_MODE_LANES");
+  const bool single = s->g->cg.mode == RS_MODE_SINGLE;
+  if (single && (s->parts > 1 && !s->repcut))
+    return set_err(RS_E_UNSUPPORTED, "waveform capture with a level cut (parts > 1) is not supported");
+  if (single && s->repcut && !s->rep_smem)
+    return set_err(RS_E_UNSUPPORTED, "waveform capture needs the shared-memory RepCut kernel (not repcut_global)");
   if (n_ids > 8192u) return set_err(RS_E_INVALID_ARG, "at most 8192 watched signals (got %u)", n_ids);
   if (n_ids && capacity == 0) return set_err(RS_E_INVALID_ARG, "capacity must be >= 1");
   for (uint32_t i = 0; i < n_ids; ++i)
@@ -1268,7 +1279,53 @@ rs_status rs_watch(rs_lanes* s, const uint32_t* ids, uint32_t n_ids, uint64_t ca
     s->wave_cap = capacity;
     s->wave_first = s->cycle;
   }
-  return upload_schedule(s);
+  if (!single) return upload_schedule(s);
+  // single lane: k_single2 reads the watched signals' coordinates; a RepCut
+  // partition reads its own watched signals (those whose value its replica
+  // holds, sig_part) from its local state: their local offsets come from the
+  // partition's (local, coord) map, sorted by coord, in the device slice blob
+  if (s->dwatch) cudaFree(s->dwatch);
+  s->dwatch = nullptr;
+  s->watch_ent = s->watch_begin = nullptr;
+  if (!n_ids) return RS_OK;
+  std::vector<uint32_t> ent, begin;
+  if (!s->repcut) {
+    for (uint32_t i = 0; i < n_ids; ++i) ent.push_back(s->g->cg.sig_coord[ids[i]]);
+  } else {
+    const uint32_t P = s->parts;
+    std::vector<uint64_t> soff(P);
+    CU(cudaMemcpy(soff.data(), s->reps.slice_off, P * 8, cudaMemcpyDeviceToHost));
+    begin.assign(P + 1, 0);
+    for (uint32_t p = 0; p < P; ++p) {
+      begin[p] = (uint32_t)(ent.size() / 2);
+      RepSliceHdr h;
+      CU(cudaMemcpy(&h, s->reps.blob + soff[p], sizeof h, cudaMemcpyDeviceToHost));
+      std::vector<uint32_t> map(2ull * h.n_map);
+      if (h.n_map) CU(cudaMemcpy(map.data(), s->reps.blob + soff[p] + h.off_map, map.size() * 4, cudaMemcpyDeviceToHost));
+      for (uint32_t j = 0; j < n_ids; ++j) {
+        const uint32_t sig = ids[j];
+        if ((s->sig_part.empty() ? 0u : s->sig_part[sig]) != p) continue;
+        const uint32_t c = s->g->cg.sig_coord[sig];
+        uint32_t lo = 0, hi = h.n_map;  // first map entry with coord >= c
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) / 2;
+          if (map[2 * mid + 1] < c) lo = mid + 1; else hi = mid;
+        }
+        if (lo == h.n_map || map[2 * lo + 1] != c)
+          return set_err(RS_E_STATE, "signal %u is not in its partition's local state", sig);
+        ent.push_back(map[2 * lo]);
+        ent.push_back(j);
+      }
+    }
+    begin[P] = (uint32_t)(ent.size() / 2);
+  }
+  const size_t eb = ent.size() * 4, off_b = (eb + 255) & ~(size_t)255;
+  CU(cudaMalloc(&s->dwatch, off_b + std::max<size_t>(4, begin.size() * 4)));
+  if (eb) CU(cudaMemcpy(s->dwatch, ent.data(), eb, cudaMemcpyHostToDevice));
+  if (!begin.empty()) CU(cudaMemcpy((uint8_t*)s->dwatch + off_b, begin.data(), begin.size() * 4, cudaMemcpyHostToDevice));
+  s->watch_ent = (const uint32_t*)s->dwatch;
+  s->watch_begin = begin.empty() ? nullptr : (const uint32_t*)((uint8_t*)s->dwatch + off_b);
+  return RS_OK;
 }
 
 rs_status rs_wave_read(rs_lanes* s, rs_change* out, uint64_t cap, uint64_t* n_out, uint64_t* dropped) {

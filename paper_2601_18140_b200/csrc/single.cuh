@@ -283,6 +283,12 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
       if (blockIdx.x == 0 && tid == 0 && a.trace && cyc < 8 && l < 60) a.trace[cyc * 64 + l] = clock64();
 #endif
     }
+    if (a.n_watch) {  // waveform (rs_watch): the snapshot the hash covers, before the commit
+#pragma unroll 1
+      for (uint32_t i = blockIdx.x * T + tid; i < a.n_watch; i += gridDim.x * T)
+        watch_single(a, i, S.ld(a.watch_ent[i]), a.cycle0 + cyc);
+      single_barrier<GRID>(bar, target, sa.gp, wsum, nullptr);  // no latch before every watched value is read
+    }
     hr = 0;
 #pragma unroll 1
     for (uint32_t i = tid; i < h->n_latch; i += T) {

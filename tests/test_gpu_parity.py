@@ -400,6 +400,36 @@ def test_waveform_changes(rs, kernel):
     assert L.wave_read()[0].shape[0] == 0
 
 
+@pytest.mark.parametrize("kw", [dict(kernel=5), dict(), dict(repcut=3), dict(kernel=5, name="C5s")])
+def test_waveform_single_lane(rs, kw):
+    """Single-lane waveform capture: the level-synchronous grid and RepCut
+    (shared-memory slices; watched signals read by the partition that holds
+    them) record exactly the oracle trace's changes."""
+    from paper_2601_18140_b200.wave import changes_from_trace
+    kw = dict(kw)
+    name = kw.pop("name", "C1")
+    c = config_circuit("C1") if name == "C1" else config_circuit("C5", n_ops=20000, n_levels=30, n_regs=2000)
+    rng = np.random.default_rng(3)
+    ids = sorted(set(rng.choice(c.n_signals, 30, replace=False).tolist()) | {int(c.input_id[0]), int(c.reg_id[0])})
+    g = rs.Graph(c, mode="single")
+    L = rs.Lanes(g, 1, **kw)
+    L.set_seed(6)
+    L.step(2)
+    L.watch(ids, capacity=1 << 16)
+    L.step(4)
+    L.step(9, hashes="host")
+    rec, dropped = L.wave_read()
+    assert dropped == 0
+    got = {(int(r["cycle"]), int(r["lane"]), int(r["watch"]), int(r["value"])) for r in rec}
+    assert len(got) == len(rec)
+    tr = oracle.simulate(c, 15, seed=6, n_lanes=1, watch=ids, hashes=False).trace
+    assert got == changes_from_trace(tr[2:], 2, [0])
+    H = oracle.simulate(c, 15, seed=6, n_lanes=1).hashes
+    L2 = rs.Lanes(g, 1, **kw)
+    L2.set_seed(6)
+    assert np.array_equal(L2.step(15, hashes="host"), H)
+
+
 def test_watch_errors(rs):
     c = config_circuit("C1")
     g = rs.Graph(c)
@@ -411,8 +441,9 @@ def test_watch_errors(rs):
         L.watch([0], capacity=0)
     assert e.value.name == "RS_E_INVALID_ARG"
     gs = rs.Graph(c, mode="single")
-    Ls = rs.Lanes(gs, 1)
-    with pytest.raises(rs.RtlSimError) as e:
-        Ls.watch([0])
-    assert e.value.name == "RS_E_UNSUPPORTED"
+    for kw in (dict(parts=2), dict(repcut=2, repcut_global=True)):
+        Ls = rs.Lanes(gs, 1, **kw)
+        with pytest.raises(rs.RtlSimError) as e:
+            Ls.watch([0])
+        assert e.value.name == "RS_E_UNSUPPORTED"
     assert L.wave_read()[0].shape[0] == 0           # nothing watched: empty
