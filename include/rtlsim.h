@@ -155,7 +155,9 @@ typedef struct {
                               signals it touches) in shared memory when it fits (k_repcut_smem), else works
                               on its state replica in global memory (k_repcut).  P = 1 runs a design that
                               fits one SM's shared memory on a single CTA with CTA barriers only. */
-  uint32_t repcut_global;  /* 1: force the global-replica RepCut kernel even if the slices fit shared memory */
+  uint32_t repcut_global;  /* RepCut kernel choice: 0 = auto (shared-memory slices with 8-byte signal
+                              slots if they fit, else width-packed slots, else global replicas);
+                              1 = global replicas; 2 = width-packed shared-memory slices */
 } rs_lane_opts;
 
 typedef struct rs_graph rs_graph;

@@ -793,7 +793,7 @@ bool build_repcut(const CompiledGraph& g, uint32_t P, RepCutPlan* out, std::stri
 }
 
 
-bool build_repcut_slices(const CompiledGraph& g, const RepCutPlan& plan, uint32_t max_smem,
+bool build_repcut_slices(const CompiledGraph& g, const RepCutPlan& plan, uint32_t max_smem, bool wide,
                          std::vector<uint8_t>* blob, std::vector<uint64_t>* slice_off,
                          std::vector<uint64_t>* op_k, std::vector<uint8_t>* in_owner, std::string* err) {
   const uint32_t P = plan.P, NL = g.n_levels, NT = g.n_ops_total(), R = g.n_regs, NI = g.n_inputs;
@@ -856,10 +856,14 @@ bool build_repcut_slices(const CompiledGraph& g, const RepCutPlan& plan, uint32_
     for (int cls = 3; cls >= 0; --cls) {
       bnd[cls] = off;
       for (uint32_t c : sigs)
-        if ((c >> 30) == (uint32_t)cls) {
+        if ((c >> 30) == (uint32_t)cls || (wide && cls == 3)) {
           local[c] = off;
-          off += 1u << cls;
+          off += wide ? 8u : 1u << cls;
         }
+      if (wide) {  // one region of 8-byte slots: every offset reads as class 3
+        bnd[2] = bnd[1] = bnd[0] = off;
+        break;
+      }
     }
     const uint32_t state_bytes = (uint32_t)align16(off + 8);  // + 8: the aligned-word gather may read past the end
     if (off > 65535u) {
@@ -955,7 +959,7 @@ bool build_repcut_slices(const CompiledGraph& g, const RepCutPlan& plan, uint32_
     h.state_bytes = state_bytes;
     h.off_map = (uint32_t)o; o = align16(o + map.size() * 4);
     h.b1 = bnd[2]; h.b2 = bnd[1]; h.b3 = bnd[0];
-    h.n_levels = NL; h.n_ops = n_ops; h.max_level = max_level;
+    h.n_levels = NL; h.n_ops = n_ops; h.max_level = max_level; h.wide = wide ? 1u : 0u;
     h.n_commit = (uint32_t)commit.size() / 4; h.n_pull = (uint32_t)pull.size() / 2;
     h.n_inj = (uint32_t)inj.size() / 4; h.n_map = (uint32_t)map.size() / 2;
     h.k_base = (uint32_t)(op_k->size() - n_ops);

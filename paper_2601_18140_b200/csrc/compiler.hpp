@@ -272,13 +272,16 @@ struct RepSliceHdr {
   uint32_t max_level;     // largest level of the partition (ops)
   uint32_t off_kop;       // u64[ops]: op hash weights in shared memory (kop_smem), else in global memory
   uint32_t kop_smem;
+  uint32_t wide;          // every local signal in an 8-byte slot (no width-class logic in the gathers)
+  uint32_t pad_[3];
 };
 // Builds the P slices of `plan` (blob, slice offsets) and the per-partition op
 // hash weights (owned ops: opk, else 0) in slice op order.  in_owner[k] = the
 // partition that hashes input k (and whose replica holds it for read-back).
 // Returns false (with *err) if a slice's smem part + local state exceeds
 // max_smem or its local state exceeds 64 KiB.
-bool build_repcut_slices(const CompiledGraph& g, const RepCutPlan& plan, uint32_t max_smem,
+// wide: 8-byte slots for every local signal (faster gathers; fails sooner).
+bool build_repcut_slices(const CompiledGraph& g, const RepCutPlan& plan, uint32_t max_smem, bool wide,
                          std::vector<uint8_t>* blob, std::vector<uint64_t>* slice_off,
                          std::vector<uint64_t>* op_k, std::vector<uint8_t>* in_owner, std::string* err);
 

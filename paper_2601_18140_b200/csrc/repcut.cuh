@@ -104,6 +104,7 @@ struct RepSmemArgs {
   uint64_t* mail;         // [2][n_regs]
 };
 
+template <bool WIDE>
 struct LocalState {
   uint8_t* s;
   uint32_t sa;          // shared-window address of s
@@ -117,6 +118,10 @@ struct LocalState {
   // splits a warp whose operands have several widths)
   __device__ __forceinline__ uint64_t ld(uint32_t o) const {
     uint64_t v;
+    if constexpr (WIDE) {  // every signal in an 8-byte slot
+      asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(sa + o) : "memory");
+      return v;
+    }
     asm volatile(
         "{\n\t.reg .pred q1, q2, q3, p16, p32;\n\t.reg .u32 t;\n\t"
         "setp.lt.u32 q3, %1, %2;\n\tsetp.lt.u32 q2, %1, %3;\n\tsetp.lt.u32 q1, %1, %4;\n\t"
@@ -127,6 +132,10 @@ struct LocalState {
     return v;
   }
   __device__ __forceinline__ void st(uint32_t o, uint64_t v) const {
+    if constexpr (WIDE) {
+      asm volatile("st.shared.u64 [%0], %1;" ::"r"(sa + o), "l"(v) : "memory");
+      return;
+    }
     const uint32_t c = cls(o), a = sa + o;
     asm volatile(
         "{\n\t.reg .pred q0, q1, q2, q3;\n\t"
@@ -140,7 +149,8 @@ struct LocalState {
 // One op (kernels.cuh select_op: branch-free; on the 16-core design a switch
 // cost 2,240 cycles per level, a 14-deep select chain 1,275, the selection
 // tree 1,186 -- a partition's level mixes many opcodes).
-__device__ __forceinline__ uint64_t rep_eval(const LocalState& S, uint32_t pw, uint2 cw, const uint16_t* ovf) {
+template <bool WIDE>
+__device__ __forceinline__ uint64_t rep_eval(const LocalState<WIDE>& S, uint32_t pw, uint2 cw, const uint16_t* ovf) {
   const uint32_t op = (pw >> 22) & 15u, n = pw >> 26;
   const uint32_t c0 = cw.x >> 16, c1 = cw.y & 0xFFFFu, c2 = n > 3 ? c0 : cw.y >> 16;
   const uint64_t x0 = S.ld(c0), x1 = S.ld(c1), x2 = S.ld(c2);
@@ -152,7 +162,7 @@ __device__ __forceinline__ uint64_t rep_eval(const LocalState& S, uint32_t pw, u
   return r & wmask(pw & 127u);
 }
 
-template <bool HASH, bool ONE>
+template <bool HASH, bool ONE, bool WIDE>
 __global__ void __launch_bounds__(1024, 1) k_repcut_smem(const RepSmemArgs ra) {
   const StepArgs& a = ra.a;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -175,7 +185,7 @@ __global__ void __launch_bounds__(1024, 1) k_repcut_smem(const RepSmemArgs ra) {
   const uint32_t* inj = reinterpret_cast<const uint32_t*>(smem + h.off_inj);
   const uint32_t* map = reinterpret_cast<const uint32_t*>(src + h.off_map);
   const uint64_t* opk = ra.op_k + h.k_base;
-  LocalState S{smem + h.state_off, (uint32_t)__cvta_generic_to_shared(smem + h.state_off), h.b1, h.b2, h.b3};
+  LocalState<WIDE> S{smem + h.state_off, (uint32_t)__cvta_generic_to_shared(smem + h.state_off), h.b1, h.b2, h.b3};
   const TileP<1> t = tile_ptrs<1>(a, p, 0);
   for (uint32_t i = tid; i < h.n_map; i += T) S.st(map[2 * i], t.ld(map[2 * i + 1]));
   if (a.n_cycles == 0) return;

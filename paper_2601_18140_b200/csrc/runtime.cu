@@ -134,6 +134,7 @@ struct rs_lanes {
   bool rep_smem = false;      // k_repcut_smem (partition-local shared-memory slices)
   void* rep_mail = nullptr;   // [2][n_regs] register mailbox
   bool rep_one = false;       // threads >= every partition level: one op per thread
+  bool rep_wide = false;      // slices with 8-byte signal slots
   RepSmemArgs reps{};
   uint32_t rep_smem_bytes = 0;
   size_t sched_bytes = 0;                // device bytes of the bound stage schedule
@@ -499,6 +500,10 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
   }
   if (g->cg.mode == RS_MODE_SINGLE && (o.kernel == 3 || o.kernel == 4) && !o.repcut) o.repcut = 1;
   if (g->cg.mode == RS_MODE_SINGLE && o.kernel == 4) o.repcut_global = 1;
+  if (o.repcut_global > 2) {
+    rs_free_lanes(s);
+    return set_err(RS_E_INVALID_ARG, "repcut_global must be 0, 1 or 2");
+  }
   if (g->cg.mode == RS_MODE_SINGLE && o.kernel == 5 && o.repcut) {
     rs_free_lanes(s);
     return set_err(RS_E_INVALID_ARG, "kernel 5 (level-synchronous) excludes repcut");
@@ -512,7 +517,8 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     std::string err;
     std::vector<uint8_t> b1, b2;
     std::vector<uint64_t> b3, b4;
-    if (build_repcut(g->cg, 1, &plan, &err) && build_repcut_slices(g->cg, plan, kRepSmemMax, &b1, &b3, &b4, &b2, &err))
+    if (build_repcut(g->cg, 1, &plan, &err) &&
+        build_repcut_slices(g->cg, plan, kRepSmemMax, false, &b1, &b3, &b4, &b2, &err))
       o.repcut = 1;
   }
   if (g->cg.mode == RS_MODE_SINGLE && o.repcut >= 1) {
@@ -596,7 +602,14 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     size_t off = 0, o_lb, o_ops, o_rb, o_regs, o_pb, o_push;
     std::vector<uint8_t> sblob, in_owner;
     std::vector<uint64_t> sl_off, op_k;
-    if (!o.repcut_global && build_repcut_slices(g->cg, plan, kRepSmemMax, &sblob, &sl_off, &op_k, &in_owner, &err)) {
+    bool fits = false;
+    if (o.repcut_global != 1) {  // 8-byte slots if every partition still fits, else width-packed
+      fits = o.repcut_global != 2 &&
+             build_repcut_slices(g->cg, plan, kRepSmemMax, true, &sblob, &sl_off, &op_k, &in_owner, &err);
+      if (fits) s->rep_wide = true;
+      else fits = build_repcut_slices(g->cg, plan, kRepSmemMax, false, &sblob, &sl_off, &op_k, &in_owner, &err);
+    }
+    if (fits) {
       s->rep_smem = true;
       uint32_t max_level = 0;
       for (uint32_t p = 0; p < s->parts; ++p) {
@@ -659,8 +672,10 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
       }
       s->reps.mail = (uint64_t*)s->rep_mail;
       s->total_bytes += 16ull * g->cg.n_regs;
-      const void* fns[] = {(const void*)k_repcut_smem<true, true>, (const void*)k_repcut_smem<true, false>,
-                           (const void*)k_repcut_smem<false, true>, (const void*)k_repcut_smem<false, false>};
+      const void* fns[] = {(const void*)k_repcut_smem<true, true, true>,   (const void*)k_repcut_smem<true, false, true>,
+                           (const void*)k_repcut_smem<false, true, true>,  (const void*)k_repcut_smem<false, false, true>,
+                           (const void*)k_repcut_smem<true, true, false>,  (const void*)k_repcut_smem<true, false, false>,
+                           (const void*)k_repcut_smem<false, true, false>, (const void*)k_repcut_smem<false, false, false>};
       for (const void* f : fns)
         if (e2 == cudaSuccess)
           e2 = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->rep_smem_bytes);
@@ -1039,8 +1054,11 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
       RepSmemArgs ra = s->reps;
       ra.a = a;
       void* args[] = {&ra};
-      const void* fn = hash ? (s->rep_one ? (const void*)k_repcut_smem<true, true> : (const void*)k_repcut_smem<true, false>)
-                            : (s->rep_one ? (const void*)k_repcut_smem<false, true> : (const void*)k_repcut_smem<false, false>);
+      const void* fns[] = {(const void*)k_repcut_smem<true, true, true>,   (const void*)k_repcut_smem<true, false, true>,
+                           (const void*)k_repcut_smem<false, true, true>,  (const void*)k_repcut_smem<false, false, true>,
+                           (const void*)k_repcut_smem<true, true, false>,  (const void*)k_repcut_smem<true, false, false>,
+                           (const void*)k_repcut_smem<false, true, false>, (const void*)k_repcut_smem<false, false, false>};
+      const void* fn = fns[(s->rep_wide ? 0 : 4) + (hash ? 0 : 2) + (s->rep_one ? 0 : 1)];
       e = cudaLaunchCooperativeKernel(fn, s->ctas, s->threads, args, s->rep_smem_bytes, s->stream);
     } else if (s->repcut) {
       RepArgs ra = s->rep;

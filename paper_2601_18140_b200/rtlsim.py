@@ -215,7 +215,7 @@ class Lanes:
 
     def __init__(self, graph: Graph, n_lanes: int, lane0: int = 0, lane_tile: int = 0, threads: int = 0,
                  stage_cycles: int = 0, stream=None, cluster: int = 0, parts: int = 0, kernel: int = 0,
-                 repcut: int = 0, repcut_global: bool = False):
+                 repcut: int = 0, repcut_global: int = 0):
         self.graph = graph
         self.n_lanes = n_lanes
         self.lane0 = lane0

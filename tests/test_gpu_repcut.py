@@ -15,7 +15,7 @@ from tests.test_gpu_parity import check, run_gpu
 pytestmark = pytest.mark.gpu
 
 
-GL = [False, True]   # k_repcut_smem (shared-memory slices) / k_repcut (global replicas)
+GL = [0, 1, 2]   # shared-memory slices (8-byte slots when they fit) / global replicas / width-packed slices
 
 
 def kernel_of(rs, c, **kw):
@@ -32,7 +32,7 @@ def kernel_of(rs, c, **kw):
 def test_c1_repcut(rs, P, gl):
     cfg = CONFIGS["C1"]
     c = config_circuit("C1")
-    assert kernel_of(rs, c, repcut=P, repcut_global=gl) == (4 if gl else 3)
+    assert kernel_of(rs, c, repcut=P, repcut_global=gl) == (4 if gl == 1 else 3)
     check(rs, c, cfg.cycles, 1, seed=cfg.stim_seed, mode="single", repcut=P, repcut_global=gl)
 
 
