@@ -38,13 +38,15 @@ def main():
             g0 = rs.Graph(c, device=rs.RS_DEVICE_NONE, mode="single")
             nlev, nreg = g0.info()["n_levels"], len(c.reg_id)
             g0.close()
-            pick = rng.integers(0, 4)
+            pick = rng.integers(0, 5)
             if pick == 0 or nreg == 0:
                 opts = dict(kernel=5)
             elif pick == 1:
                 opts = dict(repcut=int(rng.integers(1, min(nreg, 8) + 1)))
             elif pick == 2:
-                opts = dict(repcut=int(rng.integers(1, min(nreg, 8) + 1)), repcut_global=True)
+                opts = dict(repcut=int(rng.integers(1, min(nreg, 8) + 1)), repcut_global=1)
+            elif pick == 3:
+                opts = dict(repcut=int(rng.integers(1, min(nreg, 8) + 1)), repcut_global=2)
             else:
                 opts = dict(kernel=5, parts=int(rng.integers(1, min(max(nlev, 1), 4) + 1)))
         g = rs.Graph(c, device=0, mode=mode)
