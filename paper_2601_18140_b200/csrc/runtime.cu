@@ -1104,10 +1104,13 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
                          (const void*)k_lanes_t<1, true>, (const void*)k_lanes_t<1, false>,
                          (const void*)k_lanes_t<2, true>, (const void*)k_lanes_t<2, false>,
                          (const void*)k_lanes_t<4, true>, (const void*)k_lanes_t<4, false>};
-    static size_t attr_set = 0;
-    if (attr_set < smem) {
+    // the dynamic shared-memory limit is a per-device function attribute: raise it
+    // once per device to the largest size any allocation there has needed
+    static thread_local size_t attr_set[64] = {};
+    size_t& have = attr_set[s->g->device & 63];
+    if (have < smem) {
       for (const void* f : fns) CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr_set = smem;
+      have = smem;
     }
     const int fi = (s->variant == 1 ? 6 + (s->LT == 32 ? 0 : s->LT == 64 ? 2 : 4)
                                     : (s->LT == 32 ? 0 : s->LT == 16 ? 2 : 4)) + (hash ? 0 : 1);
