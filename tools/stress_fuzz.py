@@ -15,9 +15,41 @@ from paper_2601_18140_b200 import rtlsim as rs  # noqa: E402
 from synth import fuzz_circuit  # noqa: E402
 
 
+def big_cases(n_cases, rng):
+    """C3-shaped circuits of random size (wide-level kernel-1 paths, 4-op items,
+    clusters), a few cycles, random lane counts."""
+    from synth import config_circuit
+    bad = 0
+    for it in range(n_cases):
+        n_ops = int(rng.integers(5000, 90000))
+        n_levels = int(rng.integers(5, 40))
+        c = config_circuit("C3", n_ops=n_ops, n_levels=n_levels, n_regs=max(1, n_ops // 10))
+        kernel = int(rng.integers(1, 3))
+        lt = int(rng.choice([32, 64, 128] if kernel == 1 else [8, 16, 32]))
+        cs = int(rng.choice([1, 2, 4]))
+        nl = int(rng.integers(1, 400))
+        seed = int(rng.integers(0, 1000))
+        g = rs.Graph(c, device=0)
+        L = rs.Lanes(g, nl, kernel=kernel, lane_tile=lt, cluster=cs)
+        L.set_seed(seed)
+        H = L.step(3, hashes="host")
+        r = oracle.simulate(c, 3, seed=seed, n_lanes=nl, threads=8)
+        ok = np.array_equal(H, r.hashes)
+        bad += not ok
+        print(f"big {it}: ops {n_ops} levels {n_levels} lanes {nl} kernel {kernel} lt {lt} cs {cs} "
+              f"shape {L.shape()} -> {'ok' if ok else 'MISMATCH'}", flush=True)
+        L.close()
+        g.close()
+    return bad
+
+
 def main():
     n_cases = int(sys.argv[1]) if len(sys.argv) > 1 else 200
     rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 11)
+    if len(sys.argv) > 3 and sys.argv[3] == "big":
+        bad = big_cases(n_cases, rng)
+        print("cases", n_cases, "mismatches", bad)
+        sys.exit(1 if bad else 0)
     bad = 0
     for it in range(n_cases):
         seed = int(rng.integers(0, 100000))
