@@ -293,3 +293,29 @@ def test_repcut_plan_stats(rs):
         gc.repcut_stats(0)
     with pytest.raises(rs.RtlSimError):
         gc.repcut_stats(256)
+
+
+def test_header_is_plain_c():
+    """include/rtlsim.h is a C ABI: it compiles as C99 (no C++ or torch types),
+    and a C program can link the library's entry points."""
+    import shutil
+    import subprocess
+    import tempfile
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("no C compiler")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([gcc, "-fsyntax-only", "-std=c99", "-Wall", "-Werror", "-x", "c",
+                        os.path.join(root, "include", "rtlsim.h")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    src = """#include "rtlsim.h"
+int main(void) { rs_graph* g = 0; rs_graph_desc d = {0};
+  rs_status s = rs_load_graph(&d, RS_DEVICE_NONE, RS_MODE_LANES, &g);
+  return s == RS_OK ? 0 : (rs_last_error() ? 0 : 1); }"""
+    lib = os.path.join(root, "paper_2601_18140_b200", "lib")
+    with tempfile.TemporaryDirectory() as d:
+        c = os.path.join(d, "t.c")
+        open(c, "w").write(src)
+        r = subprocess.run([gcc, "-std=c99", "-I", os.path.join(root, "include"), c, "-L", lib, "-lrtlsim",
+                            "-Wl,-rpath," + lib, "-o", os.path.join(d, "t")], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
