@@ -1,23 +1,37 @@
 #!/usr/bin/env python
 """Benchmark: simulated lane-cycles/s of the B200 RTeAAL Sim hot path.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl reference]
 
 One step = one rs_step_cycles launch over the config's full cycle count for
 this rank's lanes (inject -> every level's gather/op/write -> hash -> commit,
-all cycles), hashes on.  N > 1 runs under torchrun, one process per GPU;
-each rank simulates its own `lanes` global lanes (weak scaling: lanes are
-independent units, no data-path collective).  Timing: CUDA events on the
-launching stream around each step, barrier + synchronize on both sides of
-the timed region, max over ranks; L2 flushed (256 MB write) before every
-timed step.  `--impl reference` times the CPU oracle (test infrastructure,
-oracle/) on the host cores over a bounded sample of the same workload.
+all cycles), hashes on.  Default workload: C3, the largest BASELINE.json
+config that fits one GPU (4,096 lanes x 10,000 cycles).
+
+N > 1: one process per GPU.  Under torchrun the ranks come from the
+environment; a plain `python bench.py --gpus N` re-executes itself under
+torch.distributed.run.  Lane configs are split into contiguous global lane
+ranges [d*L/N, (d+1)*L/N) (`--scaling strong`, the default)
+or give every rank the config's lane count (`--scaling weak`).  There is no
+data-path collective: lanes are independent; a gloo process group carries the
+barriers around the timed region and the max-over-ranks reduction only (so it
+also works with several ranks on one device).  Single-lane configs (C1, C5,
+MC16) run one independent replica per rank at N > 1.
+
+Timing: CUDA events on the launching stream around each step, barrier +
+synchronize on both sides of the timed region, max over ranks; L2 flushed
+(256 MB write) before every timed step.  `value` = all ranks' lane-cycles /
+the max-over-ranks device time of the K steps; `ms_per_step_median` is the
+median step.  A hash-off pass (pure throughput) follows.
+`--impl reference` times the CPU oracle (test infrastructure, oracle/) on
+the host cores over a bounded sample of the same workload.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -30,6 +44,11 @@ sys.path.insert(0, ROOT)
 
 METRIC = "simulated lane-cycles/s and op-evals/s at 1/2/4/8 B200; % of BW roofline"
 UNIT = "lane-cycles/s"
+SINGLE = ("C1", "C5", "MC16")
+# per-config roofline bound (SURVEY.md §8(d) "Roofline quantities"): HBM when the
+# per-GPU state exceeds L2 (C3, C4); L2 when state + graph fit (C2); single-lane
+# configs are latency-bound (reported against HBM, with the latency floor in DESIGN.md)
+BOUND = {"C1": "hbm", "C2": "l2", "C3": "hbm", "C4": "hbm", "C5": "hbm", "MC16": "hbm"}
 
 
 def load_peaks():
@@ -38,6 +57,33 @@ def load_peaks():
         d = json.load(open(p))
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_l2_peak():
+    """Measured L2 read bandwidth at a 64 MiB working set (tools/microbench.cu on a
+    B200, stored in profiles/)."""
+    for rnd in ("r02", "r01"):
+        p = os.path.join(ROOT, "profiles", rnd, "microbench.json")
+        if os.path.exists(p):
+            d = json.load(open(p))
+            return float(d["read_bw_gbs"]["64_MiB"]), f"measured L2 read BW at 64 MiB (profiles/{rnd}/microbench.json)"
+    return None, "unmeasured"
+
+
+def load_traffic(cfg_name, lanes, cycles, kernel):
+    """DRAM bytes of the dominant kernel per launch, scaled from the stored ncu --set
+    full capture of the same kernel (profiles/<round>/traffic_<cfg>.json); tagged as stored."""
+    for rnd in ("r02", "r01", ""):
+        p = os.path.join(ROOT, "profiles", rnd, f"traffic_{cfg_name}.json")
+        if os.path.exists(p):
+            t = json.load(open(p))
+            per = t.get("dram_bytes_per_lane_cycle")
+            if not per:
+                return None, None
+            src = (f"stored: {os.path.relpath(p, ROOT)} (ncu --set full, kernel {t.get('kernel')}, "
+                   f"{t.get('lanes')} lanes x {t.get('cycles')} cycles), scaled to this launch")
+            return per * lanes * cycles, src
+    return None, None
 
 
 class ClockSampler:
@@ -95,9 +141,12 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def workload(cfg_name, lanes, cycles, n_ops, n_levels, n_gpus):
-    return (f"{cfg_name}: {n_ops} ops / {n_levels} levels, {lanes} lanes per GPU x {cycles} cycles "
-            f"per step, {n_gpus} GPU(s), synthetic seeded circuit + stimulus")
+def workload(cfg_name, total_lanes, lanes_rank, cycles, n_ops, n_levels, n_gpus, scaling):
+    if cfg_name in SINGLE:
+        return (f"{cfg_name}: {n_ops} ops / {n_levels} levels, 1 lane x {cycles} cycles per step"
+                + (f", {n_gpus} independent replicas" if n_gpus > 1 else "") + ", synthetic seeded circuit + stimulus")
+    return (f"{cfg_name}: {n_ops} ops / {n_levels} levels, {total_lanes} lanes x {cycles} cycles per step, "
+            f"{n_gpus} GPU(s) ({lanes_rank} lanes per GPU, {scaling} scaling), synthetic seeded circuit + stimulus")
 
 
 def oracle_rate(circ, seed, n_lanes, n_cycles, lane0=0, threads=1):
@@ -126,8 +175,20 @@ def cpu_sample_plan(circ, target_s, cores):
     return lanes, cycles
 
 
+def get_config(name):
+    from synth import CONFIGS, config_circuit, multicore_circuit
+    if name == "MC16":
+        import types
+        circ = multicore_circuit()
+        cfg = types.SimpleNamespace(name="MC16", lanes=1, cycles=2000, stim_seed=circ.meta["stim_seed"], n_levels=60)
+    else:
+        cfg = CONFIGS[name]
+        circ = config_circuit(name)
+    return cfg, circ
+
+
 def run_reference(args, cfg, circ):
-    """--impl reference: the oracle (as it stands) on the host cores."""
+    """--impl reference: the oracle (as it stands) on the host cores; rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
@@ -140,12 +201,14 @@ def run_reference(args, cfg, circ):
         _, dt = oracle_rate(circ, cfg.stim_seed, lanes, cycles, lane0=k * lanes, threads=cores)
         tot += dt
     value = lanes * cycles * args.steps / tot
+    total_lanes = 1 if args.config in SINGLE else (args.lanes or cfg.lanes)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
-        "data": "synthetic",
-        "config": {"workload": workload(cfg.name, cfg.lanes, cfg.cycles, circ.n_ops, cfg.n_levels, args.gpus)},
+        "higher_is_better": True, "scaling": "weak" if args.config in SINGLE else args.scaling,
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": workload(cfg.name, total_lanes, total_lanes, args.cycles or cfg.cycles, circ.n_ops,
+                                        cfg.n_levels, args.gpus, args.scaling)},
         "op_evals_per_s": value * circ.n_ops,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                          "sample": f"{lanes} lanes x {cycles} cycles per step (one lane per thread)"},
@@ -155,18 +218,57 @@ def run_reference(args, cfg, circ):
     return 0
 
 
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def spawn_ranks(n):
+    """Re-execute this command under torch.distributed.run with n ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def time_steps(L, stream, cycles, hashes, steps, flush, barrier, torch):
+    evs = []
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    l0 = L.launches
+    for _ in range(steps):
+        flush.fill_(1)                          # L2 flush between timed steps
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        L.step(cycles, hashes=hashes)
+        e1.record(stream)
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in evs], L.launches - l0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5", "MC16"],
+    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4", "C5", "MC16"],
                     help="BASELINE configs; MC16 = synth.multicore_circuit() (16 cores x 12.5k ops, the RepCut "
                          "workload of SURVEY.md §8(f) NEXT-2)")
     ap.add_argument("--cycles", type=int, default=0, help="cycles per step (default: the config's)")
-    ap.add_argument("--lanes", type=int, default=0, help="lanes per GPU (default: the config's)")
+    ap.add_argument("--lanes", type=int, default=0, help="total lanes (strong) / lanes per GPU (weak); "
+                                                         "default: the config's")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--no-hash", action="store_true")
+    ap.add_argument("--no-hash", action="store_true", help="time the hash-off step as the headline")
+    ap.add_argument("--no-hash-off-pass", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--lane-tile", type=int, default=0)
@@ -179,47 +281,51 @@ def main():
     ap.add_argument("--watch", type=int, default=0, help="waveform capture of N signals during the timed steps")
     args = ap.parse_args()
 
-    from synth import CONFIGS, config_circuit, multicore_circuit
-    if args.config == "MC16":
-        import types
-        circ = multicore_circuit()
-        cfg = types.SimpleNamespace(name="MC16", lanes=1, cycles=2000, stim_seed=circ.meta["stim_seed"],
-                                    n_levels=60)
-    else:
-        cfg = CONFIGS[args.config]
-        circ = config_circuit(args.config)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
+
+    cfg, circ = get_config(args.config)
     if args.impl == "reference":
         return run_reference(args, cfg, circ)
 
     import torch
+    import torch.distributed as tdist
+    from paper_2601_18140_b200 import dist as D
     from paper_2601_18140_b200 import rtlsim as rs
 
-    from paper_2601_18140_b200 import dist as D
     rank, world, local = D.env_rank()
-    if world != args.gpus:
-        print(f"warning: WORLD_SIZE={world} but --gpus={args.gpus}", file=sys.stderr)
-    torch.cuda.set_device(local)
+    ndev = max(1, torch.cuda.device_count())
+    dev = local % ndev                    # more ranks than GPUs: ranks share devices (independent lanes)
+    torch.cuda.set_device(dev)
     dist = None
     if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        tdist.init_process_group("gloo")  # barriers + timing reduction only; no data-path collective
+        dist = tdist
 
-    single = args.config in ("C1", "C5", "MC16")
-    lanes = args.lanes or cfg.lanes
-    if single:
-        lanes = 1
+    single = args.config in SINGLE
     cycles = args.cycles or cfg.cycles
-    shard = D.shard_weak(rank, world, lanes)      # global lanes [lane0, lane0 + lanes)
+    if single:
+        shard = D.Shard(rank, world, 0, 1)
+        total_lanes = 1
+    elif args.scaling == "strong":
+        total_lanes = args.lanes or cfg.lanes
+        shard = D.shard_strong(rank, world, total_lanes)
+    else:
+        shard = D.shard_weak(rank, world, args.lanes or cfg.lanes)
+        total_lanes = shard.n_lanes * world
+    lanes = shard.n_lanes
     stream = torch.cuda.Stream()
-    g = rs.Graph(circ, device=local, mode="single" if single else "lanes")
+    g = rs.Graph(circ, device=dev, mode="single" if single else "lanes")
     info = g.info()
-    L = rs.Lanes(g, lanes, lane0=shard.lane0, lane_tile=args.lane_tile, threads=args.threads, stream=stream,
-                 cluster=args.cluster, parts=args.parts, kernel=args.kernel, repcut=args.repcut)
+    mk = dict(lane0=shard.lane0, lane_tile=args.lane_tile, threads=args.threads, stream=stream,
+              cluster=args.cluster, parts=args.parts, kernel=args.kernel, repcut=args.repcut)
+    L = rs.Lanes(g, lanes, **mk)
     L.set_seed(cfg.stim_seed)
     if args.watch:
         wids = np.linspace(0, circ.n_signals - 1, args.watch).astype(np.uint32)
         L.watch(wids, capacity=1 << 26)
-    hashes = None if args.no_hash else torch.empty(cycles * lanes, dtype=torch.int64, device="cuda")
+    hbuf = torch.empty(cycles * lanes, dtype=torch.int64, device="cuda")
+    hashes = None if args.no_hash else hbuf
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
 
     def barrier():
@@ -229,52 +335,42 @@ def main():
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             L.step(cycles, hashes=hashes)
-        torch.cuda.synchronize()
-        barrier()
-        torch.cuda.synchronize()
-        launches0 = L.launches
-        evs = []
-        with ClockSampler(local) as clk:
-            for _ in range(args.steps):
-                flush.fill_(1)                          # L2 flush between timed steps
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                L.step(cycles, hashes=hashes)
-                e1.record(stream)
-                evs.append((e0, e1))
-            torch.cuda.synchronize()
-        barrier()
-        torch.cuda.synchronize()
-        launches = L.launches - launches0
-    step_ms = [a.elapsed_time(b) for a, b in evs]
-    total_ms = float(sum(step_ms))
-    total_ms = D.max_over_ranks(total_ms, dist, device="cuda")
-    lane_cycles = lanes * world * cycles * args.steps
-    value = lane_cycles / (total_ms / 1e3)
+        with ClockSampler(dev) as clk:
+            step_ms, launches = time_steps(L, stream, cycles, hashes, args.steps, flush, barrier, torch)
+        hash_off = None
+        if not args.no_hash and not args.no_hash_off_pass:
+            n_off = max(1, min(args.steps, 3))
+            L.step(cycles)                                   # warm the hash-off variant
+            off_ms, _ = time_steps(L, stream, cycles, None, n_off, flush, barrier, torch)
+            hash_off = off_ms
+    total_ms = D.max_over_ranks(float(sum(step_ms)), dist)
+    med_ms = D.max_over_ranks(float(np.median(step_ms)), dist)
+    all_lane_cycles = (total_lanes * world if single else total_lanes) * cycles * args.steps
+    value = all_lane_cycles / (total_ms / 1e3)
 
     kid = L.shape()["kernel"]
     kernel_name = {1: "k_lanes_t", 2: "k_lanes", 3: "k_repcut_smem", 4: "k_repcut", 5: "k_single2"}.get(kid, "?")
     # roofline of the dominant (only) kernel: algorithmic bytes per launch / launch duration
+    # (this rank's launch; the max-over-ranks time)
     bytes_per_cycle = lanes * info["alg_bytes_per_lane_cycle"] + info["graph_alg_bytes"]
     alg_bytes = bytes_per_cycle * cycles
     kern_s = (total_ms / args.steps) / 1e3
-    peak, peak_src = load_peaks()
+    bound = BOUND[args.config]
+    if bound == "l2":
+        peak, peak_src = load_l2_peak()
+        if peak is None:
+            bound = "hbm"
+    if bound == "hbm":
+        peak, peak_src = load_peaks()
     achieved = alg_bytes / kern_s / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
-    if os.path.exists(tp):
-        tj = json.load(open(tp))
-        traffic = tj.get("dram_bytes_per_lane_cycle", 0) * lanes * cycles or None
+    traffic, traffic_src = load_traffic(args.config, lanes, cycles, kid)
 
-    # end to end through the public API with host buffers: staged inputs H2D
-    # from pinned memory, hashes D2H, every chunk.
+    # end to end through the public API with host buffers: staged inputs H2D from
+    # pinned memory and hashes D2H, every chunk, inside the timed region.
     e2e = None
     if not args.no_e2e:
         chunk = min(cycles, max(1, (256 << 20) // max(1, 8 * circ.n_inputs * lanes)))
-        Ls = rs.Lanes(g, lanes, lane0=shard.lane0, lane_tile=args.lane_tile, threads=args.threads, cluster=args.cluster,
-                      stage_cycles=2 * chunk, stream=stream, parts=args.parts, kernel=args.kernel,
-                      repcut=args.repcut)
+        Ls = rs.Lanes(g, lanes, stage_cycles=2 * chunk, **mk)
         rng = np.random.default_rng(rank)
         host_in = torch.from_numpy(rng.integers(0, 2**63, size=(chunk, circ.n_inputs, lanes),
                                                 dtype=np.int64)).pin_memory()
@@ -305,8 +401,9 @@ def main():
             e2e_step()
         torch.cuda.synchronize()
         el = time.perf_counter() - t0
-        el = D.max_over_ranks(el, dist, device="cuda")
-        e2e = {"value": lanes * world * cycles * e2e_steps / el, "unit": UNIT,
+        barrier()
+        el = D.max_over_ranks(el, dist)
+        e2e = {"value": (total_lanes * world if single else total_lanes) * cycles * e2e_steps / el, "unit": UNIT,
                "h2d_bytes_per_step": int(cycles * circ.n_inputs * lanes * 8),
                "d2h_bytes_per_step": int(cycles * lanes * 8), "steps": e2e_steps,
                "path": "rs_set_inputs(host pinned, next chunk, copy stream) + rs_step_cycles(hashes=HOST) "
@@ -322,28 +419,39 @@ def main():
                "sample": f"{nl} lanes x {nc} cycles of {args.config} ({dt:.2f} s)"}
 
     if rank == 0:
+        scaling = "weak" if (single or args.scaling == "weak") else "strong"
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": workload(args.config, lanes, cycles, circ.n_ops, info["n_levels"], world),
-                       "lanes_per_gpu": lanes, "cycles_per_step": cycles, "hash": not args.no_hash,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "ms_per_step_median": med_ms,
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic",
+            "config": {"workload": workload(args.config, total_lanes, lanes, cycles, circ.n_ops, info["n_levels"],
+                                            world, scaling),
+                       "lanes_total": total_lanes, "lanes_per_gpu": lanes, "cycles_per_step": cycles,
+                       "hash": not args.no_hash,
                        "l2": "flushed (256 MB write) before every timed step",
                        "mode": "single" if single else "lanes", "launch": L.shape(),
+                       "collective": "none on the data path (gloo barrier + max-over-ranks timing only)",
+                       **({"devices": ndev} if world > 1 else {}),
                        **({"level_cut_parts": args.parts} if args.parts > 1 else {}),
                        **({"repcut_partitions": args.repcut} if args.repcut >= 1 else {}),
                        "state_bytes_per_gpu": info["state_bytes_per_lane"] * lanes,
                        **({"watched_signals": args.watch} if args.watch else {})},
             "op_evals_per_s": value * circ.n_ops,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "alg_bytes_per_launch": alg_bytes,
+            "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "peak_source": peak_src, "alg_bytes_per_launch": alg_bytes,
                          "alg_bytes_per_lane_cycle": info["alg_bytes_per_lane_cycle"],
-                         "kernel": kernel_name},
+                         "graph_alg_bytes": info["graph_alg_bytes"], "kernel": kernel_name},
             "clocks": clk.summary(),
             "gpu_launches": launches,
             "step_ms": step_ms,
         }
+        if hash_off:
+            off_med = float(np.median(hash_off))
+            line["hash_off"] = {"value": (total_lanes * world if single else total_lanes) * cycles / (off_med / 1e3),
+                                "ms_per_step_median": off_med, "steps": len(hash_off),
+                                "roofline_frac": alg_bytes / (off_med / 1e3) / 1e9 / peak}
         if e2e:
             line["e2e"] = e2e
         if cpu:

@@ -666,8 +666,8 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
       s->reps.op_k = (const uint64_t*)(b + (uintptr_t)s->reps.op_k);
       e2 = cudaMalloc(&s->rep_mail, std::max<size_t>(16, 16ull * g->cg.n_regs));
       if (e2 != cudaSuccess) {
-        cudaFree(s->drep);
-        rs_free_lanes(s);  // partially built: frees what exists
+        s->rep_mail = nullptr;
+        rs_free_lanes(s);  // partially built: frees what exists (drep included)
         return set_err(RS_E_OOM, "repcut mailbox: %s", cudaGetErrorString(e2));
       }
       s->reps.mail = (uint64_t*)s->rep_mail;
@@ -676,14 +676,14 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
                            (const void*)k_repcut_smem<false, true, true>,  (const void*)k_repcut_smem<false, false, true>,
                            (const void*)k_repcut_smem<true, true, false>,  (const void*)k_repcut_smem<true, false, false>,
                            (const void*)k_repcut_smem<false, true, false>, (const void*)k_repcut_smem<false, false, false>};
+      // the dynamic shared-memory cap is a per-function attribute (process-wide):
+      // checked here, and set again before every launch (rs_step_cycles), so a later
+      // allocation with smaller slices cannot lower it under this one
       for (const void* f : fns)
         if (e2 == cudaSuccess)
           e2 = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->rep_smem_bytes);
-
       if (e2 != cudaSuccess) {
-        cudaFree(s->drep);
-        cudaFree(s->rep_mail);
-        rs_free_lanes(s);  // partially built: frees what exists
+        rs_free_lanes(s);  // partially built: frees what exists (drep, rep_mail included)
         return set_err(RS_E_CUDA, "repcut smem attribute: %s", cudaGetErrorString(e2));
       }
     }
@@ -1059,6 +1059,7 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
                            (const void*)k_repcut_smem<true, true, false>,  (const void*)k_repcut_smem<true, false, false>,
                            (const void*)k_repcut_smem<false, true, false>, (const void*)k_repcut_smem<false, false, false>};
       const void* fn = fns[(s->rep_wide ? 0 : 4) + (hash ? 0 : 2) + (s->rep_one ? 0 : 1)];
+      CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->rep_smem_bytes));
       e = cudaLaunchCooperativeKernel(fn, s->ctas, s->threads, args, s->rep_smem_bytes, s->stream);
     } else if (s->repcut) {
       RepArgs ra = s->rep;
@@ -1296,7 +1297,8 @@ rs_status rs_watch(rs_lanes* s, const uint32_t* ids, uint32_t n_ids, uint64_t ca
     CU(cudaMalloc(&s->wave_prev, (size_t)n_ids * lanes_pad * 8));
     CU(cudaMalloc(&s->wave_rec, capacity * 32));
     CU(cudaMalloc(&s->wave_count, 8));
-    CU(cudaMemset(s->wave_count, 0, 8));
+    // on the lanes' stream (non-blocking: a legacy-stream memset would not be ordered with the steps)
+    CU(cudaMemsetAsync(s->wave_count, 0, 8, s->stream));
     s->wave_cap = capacity;
     s->wave_first = s->cycle;
   }
@@ -1360,8 +1362,10 @@ rs_status rs_wave_read(rs_lanes* s, rs_change* out, uint64_t cap, uint64_t* n_ou
   CU(cudaMemcpyAsync(&cnt, s->wave_count, 8, cudaMemcpyDeviceToHost, s->stream));
   CU(cudaStreamSynchronize(s->stream));
   const uint64_t have = std::min<uint64_t>(cnt, s->wave_cap), n = std::min<uint64_t>(have, cap);
-  if (n) CU(cudaMemcpy(out, s->wave_rec, n * 32, cudaMemcpyDeviceToHost));
-  CU(cudaMemset(s->wave_count, 0, 8));
+  if (n) CU(cudaMemcpyAsync(out, s->wave_rec, n * 32, cudaMemcpyDeviceToHost, s->stream));
+  // reset on the lanes' stream, ordered before the next step's records
+  CU(cudaMemsetAsync(s->wave_count, 0, 8, s->stream));
+  CU(cudaStreamSynchronize(s->stream));
   if (n_out) *n_out = n;
   if (dropped) *dropped = cnt - n;
   return RS_OK;
