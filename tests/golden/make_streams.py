@@ -8,7 +8,7 @@ the bench's launch configuration on the GPU box and compare every sampled
     python tests/golden/make_streams.py C3 C4 C5 [--threads T]
 
   C3  64 lanes spread over the 4,096 (first / last lane of each of the 8
-      512-lane shards of §8(e)'s 8-GPU split, plus 48 evenly spaced) x all
+      512-lane shards of §8(e)'s 8-GPU split, plus evenly spaced ones) x all
       10,000 cycles                         -> streams/C3_sampled.npz
   C4  64 lanes: 8 per 1,024-lane shard (first two, last two, four spread)
       x all 2,000 cycles                    -> streams/C4_sampled.npz
@@ -42,9 +42,13 @@ def sample_lanes(name):
     n = CONFIGS[name].lanes
     shard = n // 8
     if name == "C3":
-        s = set(np.linspace(0, n - 1, 48).astype(int).tolist())
+        s = set()
         for d in range(8):
             s |= {d * shard, d * shard + shard - 1}
+        for x in np.linspace(0, n - 1, 64).astype(int).tolist():
+            if len(s) >= 64:
+                break
+            s.add(x)
         return sorted(s)
     s = set()
     for d in range(8):

@@ -32,7 +32,8 @@ out = {"report": os.path.basename(rep), "config": cfg, "lanes": lanes, "cycles":
        "gpu_time_ms": float(d["gpu__time_duration.sum"][0].replace(",", "")) *
                       {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "nsecond": 1e-6}.get(
                           d["gpu__time_duration.sum"][1], float("nan")),
-       "note": "ncu --set full (cache control all: caches flushed before the captured launch)"}
-path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", f"traffic_{cfg}.json")
+       "note": "ncu --set full --clock-control none (cache control all: caches flushed before the captured launch)"}
+path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                    os.environ.get("RS_PROFILE_ROUND", "r02"), f"traffic_{cfg}.json")
 json.dump(out, open(path, "w"), indent=1)
 print(json.dumps(out))
