@@ -111,6 +111,8 @@ typedef struct {
   uint64_t graph_alg_bytes;       /* G: int32 operand coords + one u32 param word per op */
   uint64_t alg_bytes_per_lane_cycle;  /* SURVEY §8(d) B_alg per lane per cycle, excluding G */
   uint64_t identity_ops_naive;    /* copies a naive §4.2 construction would need */
+  uint32_t rows_bit;              /* class-0 rows [0, rows_bit) are the 1-bit signals (bit planes in lane kernel 3) */
+  uint32_t pad_;
 } rs_graph_info;
 
 /* Options for rs_alloc_lanes (NULL -> all defaults). */

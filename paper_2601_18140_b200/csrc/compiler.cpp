@@ -183,24 +183,42 @@ rs_status compile_graph(const rs_graph_desc* d, uint32_t mode, CompiledGraph* ou
   };
   auto op_level = [&](uint32_t t) -> uint32_t { return t < NO ? lev[t] : 0; };
 
-  // ---- group each level by (opcode, arity, out class): Format-c swizzle
+  // ---- group each level by (opcode, arity, kind, out class): Format-c swizzle.
+  // kind (bit-sliced lane kernel, lanes_b.cuh): 0 = a 1-bit result whose
+  // operands are all 1-bit (evaluated on 32-lane bit-plane words), 1 = another
+  // 1-bit result, 2 = a wider result; the other kernels ignore it.
+  auto op_kind = [&](uint32_t t) -> uint32_t {
+    if (op_width(t) != 1) return 2;
+    if (t >= NO) return d->width[copies[t - NO].src] == 1 ? 0 : 1;
+    for (uint32_t a = d->arg_off[t]; a < d->arg_off[t + 1]; ++a)
+      if (d->width[d->arg_id[a]] != 1) return 1;
+    return 0;
+  };
   std::vector<uint32_t> order(NT);
   std::iota(order.begin(), order.end(), 0u);
+  std::vector<uint8_t> kind(NT);
+  for (uint32_t t = 0; t < NT; ++t) kind[t] = (uint8_t)op_kind(t);
   auto key = [&](uint32_t t) -> uint64_t {
     // arity first: consecutive work items then share the gather code path, so
     // sub-warps of one warp stay converged even across short runs
     return ((uint64_t)op_level(t) << 32) | ((uint64_t)op_arity(t) << 16) | ((uint64_t)op_code(t) << 8) |
-           width_class(op_width(t));
+           ((uint64_t)kind[t] << 4) | width_class(op_width(t));
   };
   std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return key(a) < key(b); });
 
-  // ---- rows: per class, [consts][inputs][registers][ops in device order]
+  // ---- rows: per class, [consts][inputs][registers][ops in device order];
+  // class 0 holds every 1-bit signal first (rows [0, rows_bit)), so a lane
+  // allocation may keep them as bit planes (lanes_b.cuh)
   std::vector<uint32_t> sig_coord(NS + g.n_copy, 0);
-  uint32_t rows[4] = {0, 0, 0, 0};
+  uint32_t n_bit = 0;
+  for (uint32_t s = 0; s < NS; ++s) n_bit += d->width[s] == 1;
+  for (const Copy& c : copies) n_bit += d->width[c.src] == 1;
+  uint32_t rows[4] = {0, 0, 0, 0}, bit_row = 0;
+  rows[0] = n_bit;
   auto assign = [&](uint32_t sig, uint32_t w) -> bool {
     const uint32_t c = width_class(w);
     if (rows[c] >= MAX_ROWS) return false;
-    sig_coord[sig] = make_coord(c, rows[c]++);
+    sig_coord[sig] = make_coord(c, w == 1 ? bit_row++ : rows[c]++);
     return true;
   };
   for (uint32_t i = 0; i < d->n_consts; ++i)
@@ -232,8 +250,8 @@ rs_status compile_graph(const rs_graph_desc* d, uint32_t mode, CompiledGraph* ou
       r.count = (uint32_t)(e - i);
       r.coord_begin = 0;  // filled below
       const uint32_t cls = width_class(op_width(t0));
-      r.out_row0 = rows[cls];
-      r.meta = op_code(t0) | (op_arity(t0) << 8) | (cls << 16);
+      r.out_row0 = op_width(t0) == 1 ? bit_row : rows[cls];
+      r.meta = op_code(t0) | (op_arity(t0) << 8) | (cls << 16) | ((uint32_t)kind[t0] << 18);
       for (size_t k = i; k < e; ++k) {
         const uint32_t t = order[k];
         const uint32_t sig = t < NO ? d->out_id[t] : NS + (t - NO);
@@ -247,6 +265,8 @@ rs_status compile_graph(const rs_graph_desc* d, uint32_t mode, CompiledGraph* ou
     g.level_op_begin[n_levels] = NT;
   }
   for (int c = 0; c < 4; ++c) g.rows[c] = rows[c];
+  g.rows_bit = n_bit;
+  if (bit_row != n_bit) return fail(err, RS_E_GRAPH, "internal: 1-bit rows %llu != %llu", bit_row, n_bit);
 
   // ---- per-op arrays in device order
   size_t run_i = 0;
@@ -716,6 +736,8 @@ bool build_repcut(const CompiledGraph& g, uint32_t P, RepCutPlan* out, std::stri
   // cone, so they replicate and push no more than they must
   std::unordered_map<uint32_t, uint32_t> reg_of_coord;
   for (uint32_t i = 0; i < R; ++i) reg_of_coord[g.reg_coord[i]] = i;
+  std::unordered_map<uint32_t, uint32_t> in_of_coord;
+  for (uint32_t i = 0; i < g.n_inputs; ++i) in_of_coord[g.in_coord[i]] = i;
   for (uint32_t j = 0; j < NT; ++j)
     if (owner[j] < 0) {
       int32_t p = -1;
@@ -726,6 +748,12 @@ bool build_repcut(const CompiledGraph& g, uint32_t P, RepCutPlan* out, std::stri
       for (uint32_t a = g.coord_off[j]; a < g.coord_off[j + 1] && p < 0; ++a) {
         auto it = reg_of_coord.find(g.coord[a]);
         if (it != reg_of_coord.end()) p = (int32_t)reg_part[it->second];
+      }
+      // inputs, like registers, in contiguous index blocks (a multi-core design's
+      // inputs follow its module order)
+      for (uint32_t a = g.coord_off[j]; a < g.coord_off[j + 1] && p < 0; ++a) {
+        auto it = in_of_coord.find(g.coord[a]);
+        if (it != in_of_coord.end()) p = (int32_t)((uint64_t)it->second * P / g.n_inputs);
       }
       if (p < 0) p = (int32_t)(j % P);
       close((uint32_t)p, (int32_t)j);

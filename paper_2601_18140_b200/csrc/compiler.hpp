@@ -40,12 +40,12 @@ inline uint32_t pack_pw(uint32_t w_out, uint32_t p0, uint32_t p1, uint32_t cls, 
          ((op & 15u) << 22) | ((arity & 63u) << 26);
 }
 
-struct DevRun {            // one (level, opcode, arity, out class) run
+struct DevRun {            // one (level, opcode, arity, kind, out class) run
   uint32_t op_begin;       // index of the run's first op in the per-op arrays
   uint32_t count;
   uint32_t coord_begin;    // index of the first operand coord
   uint32_t out_row0;       // first output row in the out class array
-  uint32_t meta;           // opcode | arity << 8 | out_cls << 16
+  uint32_t meta;           // opcode | arity << 8 | out_cls << 16 | kind << 18 (kind: 0 all-1-bit, 1 1-bit out, 2 wider)
 };
 
 struct CompiledGraph {
@@ -53,6 +53,7 @@ struct CompiledGraph {
   uint32_t n_signals = 0, n_inputs = 0, n_regs = 0, n_consts = 0;
   uint32_t n_ops = 0, n_copy = 0, n_levels = 0;
   uint32_t rows[4] = {0, 0, 0, 0};
+  uint32_t rows_bit = 0;            // class-0 rows [0, rows_bit) are exactly the 1-bit signals
   // per-op arrays in device order (level-major, run-major)
   std::vector<uint32_t> opw;        // param word
   std::vector<uint64_t> opk;        // hash weight of the op's output (0 for copies)

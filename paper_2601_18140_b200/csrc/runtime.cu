@@ -417,6 +417,8 @@ rs_status rs_graph_info_get(const rs_graph* g, rs_graph_info* o) {
   o->graph_alg_bytes = cg.graph_alg_bytes;
   o->alg_bytes_per_lane_cycle = cg.alg_bytes_per_lane_cycle;
   o->identity_ops_naive = cg.identity_ops_naive;
+  o->rows_bit = cg.rows_bit;
+  o->pad_ = 0;
   return RS_OK;
 }
 

@@ -58,7 +58,7 @@ class GraphInfo(C.Structure):
         ("n_runs", C.c_uint32), ("n_coords", C.c_uint32), ("rows", C.c_uint32 * 4),
         ("state_bytes_per_lane", C.c_uint64), ("graph_device_bytes", C.c_uint64),
         ("graph_alg_bytes", C.c_uint64), ("alg_bytes_per_lane_cycle", C.c_uint64),
-        ("identity_ops_naive", C.c_uint64),
+        ("identity_ops_naive", C.c_uint64), ("rows_bit", C.c_uint32), ("pad_", C.c_uint32),
     ]
 
 

@@ -198,7 +198,9 @@ def test_format_runs_sorted_and_stats(rs):
     lrb = g.export("level_run_begin")
     assert info["n_levels"] == 20 and info["n_runs"] == runs.shape[0]
     for lev in range(20):
-        keys = [((int(m) >> 8) & 0xFF, int(m) & 0xFF, (int(m) >> 16) & 3) for m in runs[lrb[lev]:lrb[lev + 1], 4]]
+        # (arity, opcode, kind, out class); kind 0 = 1-bit result of 1-bit operands, 1 = other 1-bit, 2 = wider
+        keys = [((int(m) >> 8) & 0xFF, int(m) & 0xFF, (int(m) >> 18) & 3, (int(m) >> 16) & 3)
+                for m in runs[lrb[lev]:lrb[lev + 1], 4]]
         assert keys == sorted(keys) and len(set(keys)) == len(keys)
     # B_alg per lane-cycle equals the SURVEY §8(d) formula recomputed here
     cls_b = lambda w: 1 if w <= 8 else 2 if w <= 16 else 4 if w <= 32 else 8
@@ -209,6 +211,13 @@ def test_format_runs_sorted_and_stats(rs):
     assert info["graph_alg_bytes"] == 4 * len(c.arg_id) + 4 * c.n_ops
     assert info["state_bytes_per_lane"] == sum(W)
     assert info["identity_ops_naive"] > 0
+    # class-0 rows [0, rows_bit) are exactly the 1-bit signals (bit-plane layout of lane kernel 3)
+    sc = g.export("sig_coord")
+    nb = int(sum(1 for w in c.width if int(w) == 1))
+    assert info["rows_bit"] == nb
+    for s_, w in enumerate(c.width):
+        co = int(sc[s_])
+        assert ((co >> 30) == 0 and (co & 0x3FFFFFFF) < nb) == (int(w) == 1)
 
 
 def test_identity_copy_for_register_chains(rs):
