@@ -92,6 +92,13 @@ struct StepArgs {
   const uint32_t* watch_ent;
   const uint32_t* watch_begin;
   uint32_t n_watch;
+  // bit-sliced lane kernel (lanes_b.cuh) allocations: class-0 rows [0, rows_bit)
+  // (the 1-bit signals) are bit planes at region_b + row * 16 inside a tile (word k
+  // = lanes 32k..32k+31); region[0] is then biased by -rows_bit * LT so that
+  // region[0] + row * LT addresses the u8 rows [rows_bit, rows[0])
+  uint32_t bitplane;
+  uint32_t rows_bit;
+  uint64_t region_b;
 };
 
 // One watched value of the single lane (watch index j) at `cycle`: a change
@@ -476,14 +483,38 @@ __device__ __forceinline__ void st_any(uint8_t* p, uint32_t cls, uint64_t v) {
   }
 }
 
+// Bit-plane word and bit of (coordinate, lane) in a bit-sliced allocation, or
+// nullptr when the row is a container row.
+__device__ __forceinline__ uint32_t* bit_word(const StepArgs& a, uint32_t c, uint32_t lane, uint32_t& bit) {
+  if (!a.bitplane || (c >> 30) != 0u || (c & ROW_MASK) >= a.rows_bit) return nullptr;
+  const uint32_t tile = lane / a.LT, lin = lane % a.LT;
+  bit = lin & 31u;
+  return reinterpret_cast<uint32_t*>(a.state + (size_t)tile * a.tile_bytes + a.region_b + (size_t)(c & ROW_MASK) * 16 +
+                                     (lin >> 5) * 4);
+}
+__device__ __forceinline__ uint64_t ld_sig(const StepArgs& a, uint32_t c, uint32_t lane) {
+  uint32_t bit;
+  if (const uint32_t* w = bit_word(a, c, lane, bit)) return (*w >> bit) & 1u;
+  return ld_any(row_addr(a, c, lane), c >> 30);
+}
+// one lane of a bit plane is one bit of a word other lanes share: atomic
+__device__ __forceinline__ void st_sig(const StepArgs& a, uint32_t c, uint32_t lane, uint64_t v) {
+  uint32_t bit;
+  if (uint32_t* w = bit_word(a, c, lane, bit)) {
+    if (v & 1u) atomicOr(w, 1u << bit);
+    else atomicAnd(w, ~(1u << bit));
+    return;
+  }
+  st_any(row_addr(a, c, lane), c >> 30, v);
+}
+
 // Fill every lane (padded lanes included) of the given rows with a value
 // (constants, register init).
 __global__ void k_broadcast(StepArgs a, uint32_t n_lanes_pad, const uint32_t* coords, const uint64_t* vals, uint32_t n) {
   for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < (uint64_t)n * n_lanes_pad;
        idx += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t i = (uint32_t)(idx / n_lanes_pad), l = (uint32_t)(idx % n_lanes_pad);
-    const uint32_t c = coords[i];
-    st_any(row_addr(a, c, l), c >> 30, vals[i]);
+    st_sig(a, coords[i], l, vals[i]);
   }
 }
 
@@ -493,8 +524,7 @@ __global__ void k_read(StepArgs a, const uint32_t* coords, uint32_t n_ids, uint3
   for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < (uint64_t)n_ids * n;
        idx += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t i = (uint32_t)(idx / n), l = (uint32_t)(idx % n);
-    const uint32_t c = coords[i];
-    out[idx] = ld_any(row_addr(a, c, lane_begin + l), c >> 30);
+    out[idx] = ld_sig(a, coords[i], lane_begin + l);
   }
 }
 
@@ -503,8 +533,7 @@ __global__ void k_write(StepArgs a, const uint32_t* coords, const uint32_t* widt
   for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < (uint64_t)n_ids * n;
        idx += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t i = (uint32_t)(idx / n), l = (uint32_t)(idx % n);
-    const uint32_t c = coords[i];
-    st_any(row_addr(a, c, lane_begin + l), c >> 30, vals[idx] & wmask(widths[i]));
+    st_sig(a, coords[i], lane_begin + l, vals[idx] & wmask(widths[i]));
   }
 }
 
@@ -512,10 +541,7 @@ __global__ void k_write(StepArgs a, const uint32_t* coords, const uint32_t* widt
 __global__ void k_reg_hash(StepArgs a, uint32_t n_lanes, uint64_t* hcarry) {
   for (uint32_t l = blockIdx.x * blockDim.x + threadIdx.x; l < n_lanes; l += gridDim.x * blockDim.x) {
     uint64_t h = 0;
-    for (uint32_t j = 0; j < a.g.n_regs; ++j) {
-      const uint32_t c = a.g.reg_coord[j];
-      h += ld_any(row_addr(a, c, l), c >> 30) * a.g.reg_k[j];
-    }
+    for (uint32_t j = 0; j < a.g.n_regs; ++j) h += ld_sig(a, a.g.reg_coord[j], l) * a.g.reg_k[j];
     hcarry[l] = h;
   }
 }

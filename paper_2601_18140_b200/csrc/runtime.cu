@@ -16,6 +16,7 @@
 #include "kernels.cuh"
 #include "lanes.cuh"
 #include "lanes_t.cuh"
+#include "lanes_b.cuh"
 #include "single.cuh"
 #include "repcut.cuh"
 
@@ -87,6 +88,7 @@ struct rs_lanes {
   size_t state_bytes = 0;
   uint64_t tile_bytes = 0;
   uint64_t region[4] = {0, 0, 0, 0};
+  uint64_t region_b = 0;           // kernel 6: bit-plane region (1-bit rows) inside a tile
   void* dstages = nullptr;         // bound stage schedule: blob, then table
   const uint8_t* stage_blob = nullptr;
   const StageRef* stage_tab = nullptr;
@@ -183,6 +185,9 @@ StepArgs base_args(const rs_lanes* s) {
   a.watch_ent = s->watch_ent;
   a.watch_begin = s->watch_begin;
   a.n_watch = s->g->cg.mode == RS_MODE_SINGLE ? (uint32_t)s->watch.size() : 0u;
+  a.bitplane = s->variant == 6 ? 1u : 0u;
+  a.rows_bit = s->g->cg.rows_bit;
+  a.region_b = s->region_b;
   return a;
 }
 
@@ -210,12 +215,55 @@ void bind_stages(const rs_graph* g, uint32_t bi, uint32_t LT, const uint64_t* re
   }
 }
 
+// Bit-sliced allocations (kernel 6, lanes_b.cuh): coordinate -> tile byte offset
+// of the row's lane-0 container | class (0..3), or of its first word | 4 for the
+// 1-bit rows (bit planes, 16 bytes per row).
+uint32_t bind_b(const rs_lanes* s, uint32_t c) {
+  const uint32_t cls = c >> 30, row = c & ROW_MASK;
+  if (cls == 0 && row < s->g->cg.rows_bit) return (uint32_t)(s->region_b + 16ull * row) | kClsBit;
+  return (uint32_t)(s->region[cls] + ((uint64_t)row * s->LT << cls)) | cls;
+}
+
+void bind_stages_b(const rs_lanes* s, std::vector<uint8_t>* out) {
+  const rs_graph* g = s->g;
+  *out = g->stage_blob[s->batch_idx];
+  for (const StageRef& r : g->stage_tab[s->batch_idx]) {
+    uint8_t* p = out->data() + r.off;
+    StageHdr h;
+    std::memcpy(&h, p, sizeof h);
+    uint32_t* c = reinterpret_cast<uint32_t*>(p + h.off_c);
+    if (h.type == ST_OPS) {
+      // param words get the operand class signature sum_o class(o) * 5^o in bits [26:20]
+      uint32_t* w = reinterpret_cast<uint32_t*>(p + h.off_w);
+      const StageRun* runs = reinterpret_cast<const StageRun*>(p + h.off_runs);
+      for (uint32_t i = 0; i < h.n_runs; ++i) {
+        const uint32_t ar = (runs[i].meta >> 8) & 0xffu;
+        for (uint32_t j = 0; j < runs[i].count; ++j) {
+          uint32_t sig = 0, m = 1;
+          for (uint32_t o = 0; o < ar && o < 3; ++o, m *= 5) sig += (bind_b(s, c[runs[i].coord_begin + j * ar + o]) & 7u) * m;
+          uint32_t& pw = w[runs[i].op_begin + j];
+          pw = (pw & 0xFFFFFu) | ((ar <= 3 ? sig : 0u) << 20);
+        }
+      }
+    }
+    for (uint32_t i = 0; i < h.n_coords; ++i) c[i] = bind_b(s, c[i]);
+    StageRun* runs = reinterpret_cast<StageRun*>(p + h.off_runs);
+    for (uint32_t i = 0; i < h.n_runs; ++i) {
+      const uint32_t cls = (runs[i].meta >> 16) & 3u;
+      runs[i].out_row0 = bind_b(s, (cls << 30) | runs[i].out_row0);
+    }
+  }
+}
+
 // Bind the graph's schedule to the allocation and upload it; with watched
 // signals (rs_watch) a WATCH stage is spliced in before the register commit.
 rs_status upload_schedule(rs_lanes* s) {
   const rs_graph* g = s->g;
   std::vector<uint8_t> bound;
-  bind_stages(g, s->batch_idx, s->LT, s->region, &bound);
+  if (s->variant == 6)
+    bind_stages_b(s, &bound);
+  else
+    bind_stages(g, s->batch_idx, s->LT, s->region, &bound);
   std::vector<StageRef> tab = g->stage_tab[s->batch_idx];
   if (!s->watch.empty()) {
     StageHdr h{};
@@ -229,7 +277,8 @@ rs_status upload_schedule(rs_lanes* s) {
     uint32_t* c = reinterpret_cast<uint32_t*>(bound.data() + base + h.off_c);
     for (uint32_t i = 0; i < h.n; ++i) {
       const uint32_t co = g->cg.sig_coord[s->watch[i]], cls = co >> 30;
-      c[i] = (cls << 30) | (uint32_t)(s->region[cls] + ((uint64_t)(co & ROW_MASK) * s->LT << cls));
+      c[i] = s->variant == 6 ? bind_b(s, co)
+                             : (cls << 30) | (uint32_t)(s->region[cls] + ((uint64_t)(co & ROW_MASK) * s->LT << cls));
     }
     size_t at = 0;
     while (at < tab.size() && tab[at].type != ST_LATCH) ++at;
@@ -288,10 +337,11 @@ size_t lanes_smem(uint32_t stage_bytes, uint32_t threads) {
 // thread), kernel 2 tiles 8, 16 or 32 lanes.
 void choose_tiling(uint32_t kernel, uint32_t n_lanes, int sms, uint32_t want_lt, uint32_t want_cs, uint32_t* lt,
                    uint32_t* cs) {
-  const uint32_t k1[3] = {128u, 64u, 32u}, k2[3] = {32u, 16u, 8u};
-  const uint32_t* cand = kernel == 1 ? k1 : k2;
-  const uint32_t smallest = cand[2];
-  for (int i = 0; i < 3; ++i) {
+  const uint32_t k1[3] = {128u, 64u, 32u}, k2[3] = {32u, 16u, 8u}, k6[2] = {128u, 64u};
+  const uint32_t* cand = kernel == 1 ? k1 : kernel == 6 ? k6 : k2;
+  const int nc = kernel == 6 ? 2 : 3;
+  const uint32_t smallest = cand[nc - 1];
+  for (int i = 0; i < nc; ++i) {
     const uint32_t t = cand[i];
     if (want_lt && t != want_lt) continue;
     const uint64_t tiles = (n_lanes + t - 1) / t;
@@ -551,18 +601,20 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     // hundred lane-ops, latency-bound) take kernel 2's 8..32-lane tiles; lane-rich
     // ones kernel 1's 32 * P-lane tiles (P = 4 amortizes the per-op decode).
     const uint32_t kern = o.kernel ? o.kernel : (n_lanes < 2048u ? 2u : 1u);
-    if (o.lane_tile && (kern == 2 ? (o.lane_tile != 8 && o.lane_tile != 16 && o.lane_tile != 32)
-                                  : (o.lane_tile != 32 && o.lane_tile != 64 && o.lane_tile != 128))) {
+    if (o.lane_tile && (kern == 2   ? (o.lane_tile != 8 && o.lane_tile != 16 && o.lane_tile != 32)
+                        : kern == 6 ? (o.lane_tile != 64 && o.lane_tile != 128)
+                                    : (o.lane_tile != 32 && o.lane_tile != 64 && o.lane_tile != 128))) {
       rs_free_lanes(s);  // partially built: frees what exists
-      return set_err(RS_E_INVALID_ARG, "lane_tile must be 32, 64 or 128 (kernel 1) or 8, 16 or 32 (kernel 2)");
+      return set_err(RS_E_INVALID_ARG, "lane_tile must be 32, 64 or 128 (kernel 1), 8, 16 or 32 (kernel 2) or "
+                                       "64 or 128 (kernel 6)");
     }
     if (o.cluster && o.cluster != 1 && o.cluster != 2 && o.cluster != 4 && o.cluster != 8) {
       rs_free_lanes(s);  // partially built: frees what exists
       return set_err(RS_E_INVALID_ARG, "cluster must be 1, 2, 4 or 8");
     }
-    if (o.kernel > 2) {
+    if (o.kernel > 2 && o.kernel != 6) {
       rs_free_lanes(s);  // partially built: frees what exists
-      return set_err(RS_E_INVALID_ARG, "kernel must be 0, 1 or 2");
+      return set_err(RS_E_INVALID_ARG, "lane kernel must be 0, 1, 2 or 6");
     }
     s->variant = kern;
     uint32_t lt, cs;
@@ -575,8 +627,9 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
   if (o.threads) {
     const uint32_t tmax = g->cg.mode == RS_MODE_SINGLE ? 1024u
                           : s->variant == 1            ? (uint32_t)RS_LANES_T_MAX_THREADS
+                          : s->variant == 6            ? (uint32_t)RS_LANES_B_MAX_THREADS
                                                        : (uint32_t)RS_LANES_MAX_THREADS;
-    if (o.threads % 32 || o.threads > tmax || o.threads < (s->variant == 1 ? 32u : s->LT)) {
+    if (o.threads % 32 || o.threads > tmax || o.threads < (s->variant != 2 ? 32u : s->LT)) {
       rs_free_lanes(s);
       return set_err(RS_E_INVALID_ARG, "threads must be a multiple of 32 in [32, %u] for this kernel", tmax);
     }
@@ -585,7 +638,9 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     s->threads = 1024;
   } else {
     const uint32_t per_sm = (s->n_tiles * s->cluster + g->sm_count - 1) / g->sm_count;
-    const uint32_t tmax = s->variant == 1 ? (uint32_t)RS_LANES_T_MAX_THREADS : (uint32_t)RS_LANES_MAX_THREADS;
+    const uint32_t tmax = s->variant == 1   ? (uint32_t)RS_LANES_T_MAX_THREADS
+                          : s->variant == 6 ? (uint32_t)RS_LANES_B_MAX_THREADS
+                                            : (uint32_t)RS_LANES_MAX_THREADS;
     uint32_t th = tmax / std::max<uint32_t>(1, per_sm);
     th = std::max<uint32_t>(64, th & ~31u);
     s->threads = th;
@@ -762,13 +817,29 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
   }
   // state: [n_tiles][class 0 rows x LT | class 1 | class 2 | class 3], regions 128-B aligned
   uint64_t off = 0;
-  for (int c = 0; c < 4; ++c) {
+  if (s->variant == 6) {
+    // bit-sliced tile: [bit planes: rows_bit x 16 B | u8 rows [rows_bit, rows[0]) | u16 | u32 | u64];
+    // region[0] is biased so region[0] + row * LT addresses u8 row `row` (>= rows_bit)
+    const uint32_t nb = g->cg.rows_bit;
+    s->region_b = 0;
+    off = 16ull * nb;
     off = (off + 127) & ~(uint64_t)127;
-    s->region[c] = off;
-    off += (uint64_t)g->cg.rows[c] * s->LT * (1u << c);
+    s->region[0] = off - (uint64_t)nb * s->LT;
+    off += (uint64_t)(g->cg.rows[0] - nb) * s->LT;
+    for (int c = 1; c < 4; ++c) {
+      off = (off + 127) & ~(uint64_t)127;
+      s->region[c] = off;
+      off += (uint64_t)g->cg.rows[c] * s->LT * (1u << c);
+    }
+  } else {
+    for (int c = 0; c < 4; ++c) {
+      off = (off + 127) & ~(uint64_t)127;
+      s->region[c] = off;
+      off += (uint64_t)g->cg.rows[c] * s->LT * (1u << c);
+    }
   }
   s->tile_bytes = std::max<uint64_t>((off + 127) & ~(uint64_t)127, 128);
-  if (g->cg.mode == RS_MODE_LANES && s->tile_bytes >= (1ull << 30)) {
+  if (g->cg.mode == RS_MODE_LANES && s->tile_bytes >= (s->variant == 6 ? (1ull << 32) : (1ull << 30))) {
     rs_free_lanes(s);  // partially built: frees what exists
     return set_err(RS_E_CAPACITY, "a lane tile needs %llu B of state (limit 2^30); use a smaller lane_tile",
                    (unsigned long long)s->tile_bytes);
@@ -785,7 +856,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     // kBatch-op items (more items to deal when a level is short: C3 ~470)
     const uint64_t ops_per_cta_level =
         g->cg.n_levels ? (uint64_t)g->cg.n_ops_total() / g->cg.n_levels / std::max<uint32_t>(1, s->cluster) : 0;
-    s->batch_idx = (s->variant == 1 && ops_per_cta_level >= 2048) ? 1u : 0u;
+    s->batch_idx = (s->variant != 2 && ops_per_cta_level >= 2048) ? 1u : 0u;
     if (!g->stages_built[s->batch_idx]) {
       build_stages(g->cg, g->stage_bytes, s->batch_idx ? kBatchWide : kBatch, &g->stage_blob[s->batch_idx],
                    &g->stage_tab[s->batch_idx]);
@@ -1099,14 +1170,16 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
     if (hash) s->hc_cur = 1 - s->hc_cur;
   } else {
     a.hcarry_out = a.hcarry_in;
-    const size_t smem = s->variant == 1 ? 128 + 2ull * s->g->stage_bytes + lanes_t_smem_extra(s->threads, s->LT / 32)
+    const size_t smem = s->variant != 2 ? 128 + 2ull * s->g->stage_bytes + lanes_t_smem_extra(s->threads, s->LT / 32)
                                         : lanes_smem(s->g->stage_bytes, s->threads);
     const void* fns[] = {(const void*)k_lanes<32, true>, (const void*)k_lanes<32, false>,
                          (const void*)k_lanes<16, true>, (const void*)k_lanes<16, false>,
                          (const void*)k_lanes<8, true>,  (const void*)k_lanes<8, false>,
                          (const void*)k_lanes_t<1, true>, (const void*)k_lanes_t<1, false>,
                          (const void*)k_lanes_t<2, true>, (const void*)k_lanes_t<2, false>,
-                         (const void*)k_lanes_t<4, true>, (const void*)k_lanes_t<4, false>};
+                         (const void*)k_lanes_t<4, true>, (const void*)k_lanes_t<4, false>,
+                         (const void*)k_lanes_b<2, true>, (const void*)k_lanes_b<2, false>,
+                         (const void*)k_lanes_b<4, true>, (const void*)k_lanes_b<4, false>};
     // the dynamic shared-memory limit is a per-device function attribute: raise it
     // once per device to the largest size any allocation there has needed
     static thread_local size_t attr_set[64] = {};
@@ -1115,8 +1188,9 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
       for (const void* f : fns) CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       have = smem;
     }
-    const int fi = (s->variant == 1 ? 6 + (s->LT == 32 ? 0 : s->LT == 64 ? 2 : 4)
-                                    : (s->LT == 32 ? 0 : s->LT == 16 ? 2 : 4)) + (hash ? 0 : 1);
+    const int fi = (s->variant == 1   ? 6 + (s->LT == 32 ? 0 : s->LT == 64 ? 2 : 4)
+                    : s->variant == 6 ? 12 + (s->LT == 64 ? 0 : 2)
+                                      : (s->LT == 32 ? 0 : s->LT == 16 ? 2 : 4)) + (hash ? 0 : 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(s->n_tiles * s->cluster);
     cfg.blockDim = dim3(s->threads);

@@ -87,7 +87,8 @@ def test_c1_full(rs, mode, kernel):
 
 @pytest.mark.parametrize("kernel,lt,cs", [(2, 8, 1), (2, 16, 1), (2, 32, 1), (2, 32, 4), (2, 16, 2), (2, 8, 8),
                                           (1, 32, 1), (1, 64, 1), (1, 128, 1), (1, 32, 4), (1, 64, 2),
-                                          (1, 128, 8)])
+                                          (1, 128, 8), (6, 64, 1), (6, 128, 1), (6, 64, 2), (6, 128, 4),
+                                          (6, 128, 8)])
 def test_c2_structure_ragged_lanes(rs, lt, cs, kernel):
     """Full C2 circuit, 37 lanes (ragged last tile), 25 cycles, each lane tile,
     one CTA or a thread-block cluster per tile, both lane kernels."""
@@ -101,9 +102,11 @@ def test_c2_threads_variants(rs):
         check(rs, c, 12, 40, seed=7, threads=th, lane_tile=8, kernel=2)
     for th in (32, 96, 640):
         check(rs, c, 12, 70, seed=7, threads=th, lane_tile=64, kernel=1)
+    for th in (32, 160, 768):
+        check(rs, c, 12, 200, seed=7, threads=th, lane_tile=128, kernel=6)
 
 
-@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("kernel", [1, 2, 6])
 def test_c3_structure(rs, kernel):
     check(rs, config_circuit("C3"), 6, 40, seed=CONFIGS["C3"].stim_seed, kernel=kernel)
 
@@ -119,7 +122,7 @@ def test_fuzz_corpus(rs):
     wide folds, permuted ids; 60 cycles, both modes."""
     for seed in range(200):
         c = fuzz_circuit(seed)
-        check(rs, c, 60, 3, seed=seed, kernel=1 + seed % 2)
+        check(rs, c, 60, 3, seed=seed, kernel=(1, 2, 6)[seed % 3])
         if seed % 4 == 0:
             check(rs, c, 60, 1, seed=seed, mode="single", kernel=5 if seed % 8 else 0)
 
@@ -146,7 +149,7 @@ def test_closed_forms_on_gpu(rs):
     check(rs, c, 40, 1, staged=vals)
 
 
-@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("kernel", [1, 2, 6])
 def test_chunking_and_hash_toggle(rs, kernel):
     c = config_circuit("C2", n_ops=4000, n_levels=20, n_regs=400)
     g = rs.Graph(c)
@@ -164,15 +167,16 @@ def test_chunking_and_hash_toggle(rs, kernel):
     assert L.cycle == 21
 
 
+@pytest.mark.parametrize("kernel", [1, 6])
 @pytest.mark.parametrize("cluster", [1, 2])
-def test_wide_work_items(rs, cluster):
-    """Kernel 1 with kBatchWide-op work items (>= 2,048 ops per CTA and level:
-    cluster 1) and with kBatch-op items (cluster 2), ragged lanes."""
+def test_wide_work_items(rs, cluster, kernel):
+    """Kernels 1 and 6 with kBatchWide-op work items (>= 2,048 ops per CTA and
+    level: cluster 1) and with kBatch-op items (cluster 2), ragged lanes."""
     c = config_circuit("C3", n_ops=60000, n_levels=20, n_regs=3000)
-    check(rs, c, 5, 70, seed=9, kernel=1, lane_tile=64, cluster=cluster)
+    check(rs, c, 5, 70, seed=9, kernel=kernel, lane_tile=64, cluster=cluster)
 
 
-@pytest.mark.parametrize("mode,kernel", [("lanes", 1), ("lanes", 2), ("single", 0), ("single", 5)])
+@pytest.mark.parametrize("mode,kernel", [("lanes", 1), ("lanes", 2), ("lanes", 6), ("single", 0), ("single", 5)])
 def test_staged_inputs_pipelined(rs, mode, kernel):
     """The next chunk is staged (copy stream) before the current one is stepped,
     with a ring of two chunks: every copy must wait for the launch that last
@@ -180,7 +184,7 @@ def test_staged_inputs_pipelined(rs, mode, kernel):
     c = config_circuit("C2", n_ops=3000, n_levels=15, n_regs=300) if mode == "lanes" else config_circuit("C1")
     rng = np.random.default_rng(5)
     n, ch = 60, 6
-    nl = (130 if kernel == 1 else 33) if mode == "lanes" else 1
+    nl = (33 if kernel == 2 else 130) if mode == "lanes" else 1
     vals = rng.integers(0, 2**63, size=(n, c.n_inputs, nl), dtype=np.int64).astype(np.uint64)
     g = rs.Graph(c, mode=mode)
     L = rs.Lanes(g, nl, stage_cycles=2 * ch, kernel=kernel)
@@ -217,7 +221,7 @@ def test_staged_inputs_from_device_stream(rs):
     assert np.array_equal(H, r.hashes)
 
 
-@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("kernel", [1, 2, 6])
 def test_staged_inputs_chunks(rs, kernel):
     c = config_circuit("C2", n_ops=3000, n_levels=15, n_regs=300)
     rng = np.random.default_rng(3)
@@ -236,7 +240,7 @@ def test_staged_inputs_chunks(rs, kernel):
     assert e.value.name == "RS_E_STATE"
 
 
-@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("kernel", [1, 2, 6])
 def test_checkpoint_restore(rs, kernel):
     c = config_circuit("C2", n_ops=3000, n_levels=15, n_regs=300)
     full = oracle.simulate(c, 20, seed=5, n_lanes=24)
@@ -245,7 +249,7 @@ def test_checkpoint_restore(rs, kernel):
     a.set_seed(5)
     h0 = a.step(10, hashes="host")
     regs = a.read(c.reg_id)
-    b = rs.Lanes(g, 24, kernel=3 - kernel)   # restored into the other lane kernel's layout
+    b = rs.Lanes(g, 24, kernel={1: 2, 2: 6, 6: 1}[kernel])   # restored into another lane kernel's layout
     b.set_seed(5)
     b.write_registers(c.reg_id, regs)
     b.cycle = 10
@@ -268,6 +272,8 @@ def test_lane_sharding_invariance(rs):
     # the same partition across the two lane kernels (shards may run different layouts)
     Hc, Fc, _ = run_gpu(rs, c, 15, 37, seed=9, lane0=37, kernel=1)
     assert np.array_equal(Hb, Hc) and np.array_equal(Fb, Fc)
+    Hd, Fd, _ = run_gpu(rs, c, 15, 37, seed=9, lane0=37, kernel=6)
+    assert np.array_equal(Hb, Hd) and np.array_equal(Fb, Fd)
 
 
 def test_error_statuses(rs):
@@ -361,7 +367,7 @@ def test_auto_kernel_choice(rs):
         assert np.array_equal(h[:, [0, L.n_lanes - 1]], r.hashes)
 
 
-@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("kernel", [1, 2, 6])
 def test_waveform_changes(rs, kernel):
     """Waveform capture (rs_watch): the fused per-cycle change
     records equal the change set of the oracle's per-cycle trace of the same
