@@ -225,28 +225,139 @@ __device__ __forceinline__ void word_ops(const LaneB& L, uint32_t op, uint32_t a
   }
 }
 
+// Low 32 bits of an op's result (reading R1 semantics before the final mask):
+// and / or / xor / add / sub / mul / not / shl / cat / mux / copy need only the
+// low 32 bits of their operands (a mux's selector is tested on all 64); eq, lt,
+// shr and bits read whole operands.
+template <int OP, int A>
+__device__ __forceinline__ uint32_t low32(const uint64_t* x, uint32_t pw) {
+  const uint32_t p0 = (pw >> 7) & 127u;
+  const uint32_t x0 = (uint32_t)x[0], x1 = (uint32_t)x[A > 1 ? 1 : 0], x2 = (uint32_t)x[A > 2 ? 2 : 0];
+  if constexpr (OP == RS_OP_AND) return A == 3 ? x0 & x1 & x2 : x0 & x1;
+  else if constexpr (OP == RS_OP_OR) return A == 3 ? x0 | x1 | x2 : x0 | x1;
+  else if constexpr (OP == RS_OP_XOR) return A == 3 ? x0 ^ x1 ^ x2 : x0 ^ x1;
+  else if constexpr (OP == RS_OP_ADD) return A == 3 ? x0 + x1 + x2 : x0 + x1;
+  else if constexpr (OP == RS_OP_SUB) return A == 3 ? x0 - x1 - x2 : x0 - x1;
+  else if constexpr (OP == RS_OP_MUL) return A == 3 ? x0 * x1 * x2 : x0 * x1;
+  else if constexpr (OP == RS_OP_NOT) return ~x0;
+  else if constexpr (OP == RS_OP_SHL) return p0 >= 32u ? 0u : x0 << p0;
+  else if constexpr (OP == RS_OP_SHR) return p0 >= 64u ? 0u : (uint32_t)(x[0] >> p0);
+  else if constexpr (OP == RS_OP_BITS) {
+    const uint32_t lo = (pw >> 14) & 63u, n = p0 - lo + 1u;
+    return (uint32_t)(x[0] >> lo) & (n >= 32u ? 0xFFFFFFFFu : ((1u << n) - 1u));
+  } else if constexpr (OP == RS_OP_CAT) return p0 >= 32u ? x1 : ((x0 << p0) | x1);
+  else if constexpr (OP == RS_OP_EQ) return x[0] == x[1 % A] ? 1u : 0u;
+  else if constexpr (OP == RS_OP_LT) return x[0] < x[1 % A] ? 1u : 0u;
+  else if constexpr (OP == RS_OP_MUX) return x[0] != 0ull ? x1 : x2;
+  else return x0;  // OP_COPY
+}
+
+enum : uint32_t { OC_BIT = 0, OC_NARROW = 1, OC_WIDE = 2 };
+
+// Compute, mask, hash and store one op (opcode OP, A operands, result kind OC:
+// a bit plane, a <= 32-bit container or a 64-bit one) for the thread's P lanes.
+template <int P, bool HASH, int A, int OP, int OC>
+__device__ __forceinline__ void op_tail(const LaneB& L, const uint64_t (&x)[A][P], uint32_t pw, uint32_t s_k,
+                                        uint32_t oc, uint64_t (&hacc)[P]) {
+  if constexpr (OC == OC_WIDE) {
+    uint64_t v[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      uint64_t xs[A];
+#pragma unroll
+      for (int o = 0; o < A; ++o) xs[o] = x[o][k];
+      v[k] = apply_op<OP, A>(xs, pw);  // masked to w_out
+    }
+    if constexpr (HASH) hash_add<P>(hacc, v, lds64(s_k));
+    uint64_t* q = reinterpret_cast<uint64_t*>(const_cast<uint8_t*>(L.tb) + (oc + ((L.lin << 3) - 3u)));
+#pragma unroll
+    for (int k = 0; k < P; ++k) q[32 * k] = v[k];
+  } else {
+    uint32_t y[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      uint64_t xs[A];
+#pragma unroll
+      for (int o = 0; o < A; ++o) xs[o] = x[o][k];
+      y[k] = low32<OP, A>(xs, pw);
+    }
+    if constexpr (OC == OC_BIT) {
+      uint32_t w[P];
+#pragma unroll
+      for (int k = 0; k < P; ++k) w[k] = __ballot_sync(0xffffffffu, y[k] & 1u);
+      if constexpr (HASH) {
+        const uint64_t K = lds64(s_k);
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+          if (y[k] & 1u) hacc[k] += K;
+      }
+      stwords<P>(L, oc, w);
+    } else {
+      const uint32_t m = 0xFFFFFFFFu >> (32u - (pw & 127u));  // w_out <= 32
+#pragma unroll
+      for (int k = 0; k < P; ++k) y[k] &= m;
+      if constexpr (HASH) {
+        const uint64_t K = lds64(s_k);
+        const uint32_t klo = (uint32_t)K, khi = (uint32_t)(K >> 32);
+#pragma unroll
+        for (int k = 0; k < P; ++k) hacc[k] += (uint64_t)y[k] * klo + ((uint64_t)(y[k] * khi) << 32);
+      }
+      const uint32_t cls = oc & 7u;
+      uint8_t* q = const_cast<uint8_t*>(L.tb) + (oc + ((L.lin << cls) - cls));
+      if (cls == 0u) {
+#pragma unroll
+        for (int k = 0; k < P; ++k) q[32 * k] = (uint8_t)y[k];
+      } else if (cls == 1u) {
+#pragma unroll
+        for (int k = 0; k < P; ++k) reinterpret_cast<uint16_t*>(q)[32 * k] = (uint16_t)y[k];
+      } else {
+#pragma unroll
+        for (int k = 0; k < P; ++k) reinterpret_cast<uint32_t*>(q)[32 * k] = y[k];
+      }
+    }
+  }
+}
+
 // cnt ops of one run (kind 1 / 2), gathered op by op through the class
-// signature (pw bits [26:20]), computed, masked, hashed and stored.
+// signature (pw bits [26:20]), then one jump on (opcode, result kind) into the
+// specialised compute / mask / hash / store tail.
 template <int P, bool HASH, int A>
 __device__ __forceinline__ void lane_ops(const LaneB& L, uint32_t op, uint32_t s_c, uint32_t s_w, uint32_t s_k,
                                          uint32_t ob, uint32_t ostride, uint32_t cnt, uint64_t (&hacc)[P]) {
+  const uint32_t ocls = ob & 7u;
+  const uint32_t sel = op * 3u + (ocls == kClsBit ? OC_BIT : ocls == 3u ? OC_WIDE : OC_NARROW);
 #pragma unroll 1
   for (uint32_t j = 0; j < cnt; ++j) {
     uint32_t c[A];
 #pragma unroll
     for (int o = 0; o < A; ++o) c[o] = lds32(s_c + 4 * (j * A + o));
     const uint32_t pw = lds32(s_w + 4 * j);
-    uint64_t x[1][A][P];
-    gather_b<A, P>(L, (pw >> 20) & 127u, c, x[0]);
-    const uint32_t pwa[1] = {pw};
-    uint64_t y[1][P];
-    batch_compute<1, A, P>(op, x, pwa, y);
-    const uint64_t m = wmask(pw & 127u);
-    uint64_t v[P];
-#pragma unroll
-    for (int k = 0; k < P; ++k) v[k] = y[0][k] & m;
-    if constexpr (HASH) hash_add<P>(hacc, v, lds64(s_k + 8 * j));
-    stb<P>(L, ob + ostride * j, v);
+    uint64_t x[A][P];
+    gather_b<A, P>(L, (pw >> 20) & 127u, c, x);
+    const uint32_t oc = ob + ostride * j, sk = s_k + 8 * j;
+#define RS_T(OPC)                                                                         \
+  case OPC * 3 + OC_BIT: op_tail<P, HASH, A, OPC, OC_BIT>(L, x, pw, sk, oc, hacc); break;      \
+  case OPC * 3 + OC_NARROW: op_tail<P, HASH, A, OPC, OC_NARROW>(L, x, pw, sk, oc, hacc); break; \
+  case OPC * 3 + OC_WIDE: op_tail<P, HASH, A, OPC, OC_WIDE>(L, x, pw, sk, oc, hacc); break;
+    if constexpr (A == 1) {
+      switch (sel) {
+        RS_T(RS_OP_NOT) RS_T(RS_OP_SHL) RS_T(RS_OP_SHR) RS_T(RS_OP_BITS) RS_T(OP_COPY)
+        default: break;
+      }
+    } else if constexpr (A == 2) {
+      switch (sel) {
+        RS_T(RS_OP_AND) RS_T(RS_OP_OR) RS_T(RS_OP_XOR) RS_T(RS_OP_ADD) RS_T(RS_OP_SUB) RS_T(RS_OP_MUL)
+        RS_T(RS_OP_EQ) RS_T(RS_OP_LT) RS_T(RS_OP_CAT)
+        default: break;
+      }
+    } else {
+      switch (sel) {
+        RS_T(RS_OP_AND) RS_T(RS_OP_OR) RS_T(RS_OP_XOR) RS_T(RS_OP_ADD) RS_T(RS_OP_SUB) RS_T(RS_OP_MUL)
+        RS_T(RS_OP_MUX)
+        default: break;
+      }
+    }
+#undef RS_T
   }
 }
 
