@@ -140,6 +140,13 @@ __device__ __forceinline__ void stb(const LaneB& L, uint32_t c, const uint64_t (
   }
 }
 
+// hacc += K when bit `lin` of word w is set (a 1-bit value's hash term): one
+// predicate and a predicated 64-bit add
+__device__ __forceinline__ void hash_bit(uint64_t& hacc, uint32_t w, uint32_t bitmask, uint64_t K) {
+  asm("{\n .reg .pred p;\n .reg .u32 t;\n and.b32 t, %1, %2;\n setp.ne.u32 p, t, 0;\n @p add.u64 %0, %0, %3;\n}"
+      : "+l"(hacc) : "r"(w), "r"(bitmask), "l"(K));
+}
+
 template <int P>
 __device__ __forceinline__ void hash_add(uint64_t (&hacc)[P], const uint64_t (&v)[P], uint64_t K) {
 #pragma unroll
@@ -217,9 +224,9 @@ __device__ __forceinline__ void word_ops(const LaneB& L, uint32_t op, uint32_t a
     }
     if constexpr (HASH) {
       const uint64_t K = lds64(s_k + 8 * j);
+      const uint32_t bm = 1u << L.lin;
 #pragma unroll
-      for (int k = 0; k < P; ++k)
-        if ((r[k] >> L.lin) & 1u) hacc[k] += K;
+      for (int k = 0; k < P; ++k) hash_bit(hacc[k], r[k], bm, K);
     }
     stwords<P>(L, ob + 16u * j, r);
   }
@@ -288,8 +295,7 @@ __device__ __forceinline__ void op_tail(const LaneB& L, const uint64_t (&x)[A][P
       if constexpr (HASH) {
         const uint64_t K = lds64(s_k);
 #pragma unroll
-        for (int k = 0; k < P; ++k)
-          if (y[k] & 1u) hacc[k] += K;
+        for (int k = 0; k < P; ++k) hash_bit(hacc[k], y[k], 1u, K);
       }
       stwords<P>(L, oc, w);
     } else {
@@ -318,14 +324,21 @@ __device__ __forceinline__ void op_tail(const LaneB& L, const uint64_t (&x)[A][P
   }
 }
 
+// Dense tail index of (opcode, result kind) per arity, written into param word
+// bits [31:27] at bind time (runtime.cu bind_stages_b) so the tail dispatch is
+// one jump-table branch.
+__host__ __device__ constexpr int tail_op_index(int A, int op) {
+  return A == 1 ? (op == RS_OP_NOT ? 0 : op == RS_OP_SHL ? 1 : op == RS_OP_SHR ? 2 : op == RS_OP_BITS ? 3 : 4)
+       : A == 2 ? (op <= RS_OP_XOR ? op : op <= RS_OP_LT ? op - 1 : 8)  // and or xor | add sub mul eq lt | cat
+                : (op <= RS_OP_XOR ? op : op <= RS_OP_MUL ? op - 1 : 6);  // and or xor | add sub mul | mux
+}
+
 // cnt ops of one run (kind 1 / 2), gathered op by op through the class
-// signature (pw bits [26:20]), then one jump on (opcode, result kind) into the
-// specialised compute / mask / hash / store tail.
+// signature (pw bits [26:20]), then one jump on (opcode, result kind) (pw bits
+// [31:27]) into the specialised compute / mask / hash / store tail.
 template <int P, bool HASH, int A>
-__device__ __forceinline__ void lane_ops(const LaneB& L, uint32_t op, uint32_t s_c, uint32_t s_w, uint32_t s_k,
-                                         uint32_t ob, uint32_t ostride, uint32_t cnt, uint64_t (&hacc)[P]) {
-  const uint32_t ocls = ob & 7u;
-  const uint32_t sel = op * 3u + (ocls == kClsBit ? OC_BIT : ocls == 3u ? OC_WIDE : OC_NARROW);
+__device__ __forceinline__ void lane_ops(const LaneB& L, uint32_t s_c, uint32_t s_w, uint32_t s_k, uint32_t ob,
+                                         uint32_t ostride, uint32_t cnt, uint64_t (&hacc)[P]) {
 #pragma unroll 1
   for (uint32_t j = 0; j < cnt; ++j) {
     uint32_t c[A];
@@ -335,25 +348,25 @@ __device__ __forceinline__ void lane_ops(const LaneB& L, uint32_t op, uint32_t s
     uint64_t x[A][P];
     gather_b<A, P>(L, (pw >> 20) & 127u, c, x);
     const uint32_t oc = ob + ostride * j, sk = s_k + 8 * j;
-#define RS_T(OPC)                                                                         \
-  case OPC * 3 + OC_BIT: op_tail<P, HASH, A, OPC, OC_BIT>(L, x, pw, sk, oc, hacc); break;      \
-  case OPC * 3 + OC_NARROW: op_tail<P, HASH, A, OPC, OC_NARROW>(L, x, pw, sk, oc, hacc); break; \
-  case OPC * 3 + OC_WIDE: op_tail<P, HASH, A, OPC, OC_WIDE>(L, x, pw, sk, oc, hacc); break;
+#define RS_T(I, OPC)                                                                              \
+  case 3 * I + OC_BIT: op_tail<P, HASH, A, OPC, OC_BIT>(L, x, pw, sk, oc, hacc); break;             \
+  case 3 * I + OC_NARROW: op_tail<P, HASH, A, OPC, OC_NARROW>(L, x, pw, sk, oc, hacc); break;       \
+  case 3 * I + OC_WIDE: op_tail<P, HASH, A, OPC, OC_WIDE>(L, x, pw, sk, oc, hacc); break;
     if constexpr (A == 1) {
-      switch (sel) {
-        RS_T(RS_OP_NOT) RS_T(RS_OP_SHL) RS_T(RS_OP_SHR) RS_T(RS_OP_BITS) RS_T(OP_COPY)
+      switch (pw >> 27) {
+        RS_T(0, RS_OP_NOT) RS_T(1, RS_OP_SHL) RS_T(2, RS_OP_SHR) RS_T(3, RS_OP_BITS) RS_T(4, OP_COPY)
         default: break;
       }
     } else if constexpr (A == 2) {
-      switch (sel) {
-        RS_T(RS_OP_AND) RS_T(RS_OP_OR) RS_T(RS_OP_XOR) RS_T(RS_OP_ADD) RS_T(RS_OP_SUB) RS_T(RS_OP_MUL)
-        RS_T(RS_OP_EQ) RS_T(RS_OP_LT) RS_T(RS_OP_CAT)
+      switch (pw >> 27) {
+        RS_T(0, RS_OP_AND) RS_T(1, RS_OP_OR) RS_T(2, RS_OP_XOR) RS_T(3, RS_OP_ADD) RS_T(4, RS_OP_SUB)
+        RS_T(5, RS_OP_MUL) RS_T(6, RS_OP_EQ) RS_T(7, RS_OP_LT) RS_T(8, RS_OP_CAT)
         default: break;
       }
     } else {
-      switch (sel) {
-        RS_T(RS_OP_AND) RS_T(RS_OP_OR) RS_T(RS_OP_XOR) RS_T(RS_OP_ADD) RS_T(RS_OP_SUB) RS_T(RS_OP_MUL)
-        RS_T(RS_OP_MUX)
+      switch (pw >> 27) {
+        RS_T(0, RS_OP_AND) RS_T(1, RS_OP_OR) RS_T(2, RS_OP_XOR) RS_T(3, RS_OP_ADD) RS_T(4, RS_OP_SUB)
+        RS_T(5, RS_OP_MUL) RS_T(6, RS_OP_MUX)
         default: break;
       }
     }
@@ -408,11 +421,11 @@ __device__ __forceinline__ void stage_ops_b(const LaneB& L, const uint8_t* buf, 
     if (kind == 0u) {
       word_ops<P, HASH>(L, op, ar, s_c, s_w, s_k, ob, cnt, hacc);
     } else if (ar == 2) {
-      lane_ops<P, HASH, 2>(L, op, s_c, s_w, s_k, ob, ostride, cnt, hacc);
+      lane_ops<P, HASH, 2>(L, s_c, s_w, s_k, ob, ostride, cnt, hacc);
     } else if (ar == 1) {
-      lane_ops<P, HASH, 1>(L, op, s_c, s_w, s_k, ob, ostride, cnt, hacc);
+      lane_ops<P, HASH, 1>(L, s_c, s_w, s_k, ob, ostride, cnt, hacc);
     } else if (ar == 3) {
-      lane_ops<P, HASH, 3>(L, op, s_c, s_w, s_k, ob, ostride, cnt, hacc);
+      lane_ops<P, HASH, 3>(L, s_c, s_w, s_k, ob, ostride, cnt, hacc);
     } else {
       fold_ops<P, HASH>(L, op, ar, s_c, s_w, s_k, ob, ostride, cnt, hacc);
     }

@@ -241,8 +241,12 @@ void bind_stages_b(const rs_lanes* s, std::vector<uint8_t>* out) {
         for (uint32_t j = 0; j < runs[i].count; ++j) {
           uint32_t sig = 0, m = 1;
           for (uint32_t o = 0; o < ar && o < 3; ++o, m *= 5) sig += (bind_b(s, c[runs[i].coord_begin + j * ar + o]) & 7u) * m;
+          // bits [31:27]: dense (opcode, result kind) tail index (lanes_b.cuh tail_op_index)
+          const uint32_t op = runs[i].meta & 0xffu, ocls = (runs[i].meta >> 16) & 3u;
+          const uint32_t kind = ((runs[i].meta >> 18) & 3u) < 2u ? OC_BIT : ocls == 3u ? OC_WIDE : OC_NARROW;
+          const uint32_t tail = ar <= 3 ? 3u * (uint32_t)tail_op_index((int)ar, (int)op) + kind : 0u;
           uint32_t& pw = w[runs[i].op_begin + j];
-          pw = (pw & 0xFFFFFu) | ((ar <= 3 ? sig : 0u) << 20);
+          pw = (pw & 0xFFFFFu) | ((ar <= 3 ? sig : 0u) << 20) | (tail << 27);
         }
       }
     }
