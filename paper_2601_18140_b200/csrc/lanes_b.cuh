@@ -398,6 +398,29 @@ __device__ __forceinline__ void fold_ops(const LaneB& L, uint32_t op, uint32_t a
   }
 }
 
+// Prefetch into L1 the operand rows of work item `it` (this warp's next item):
+// thread t touches 128-byte line t of each row segment of the tile, so the
+// gathers of that item hit L1 instead of waiting on L2 / HBM (memory-level
+// parallelism across items without holding values in registers).
+template <int P>
+__device__ __forceinline__ void prefetch_item(const LaneB& L, const uint32_t* items, const StageRun* runs,
+                                              uint32_t s_c0, uint32_t it) {
+  const uint32_t w = items[it];
+  const StageRun R = runs[w >> 16];
+  const uint32_t b = w & 0x1FFFu, cnt = ((w >> 13) & 7u) + 1u, ar = (R.meta >> 8) & 0xffu;
+  const uint32_t n = min(cnt * ar, 12u);
+  const uint32_t s_c = s_c0 + 4 * (R.coord_begin + (b - R.op_begin) * ar);
+#pragma unroll 1
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t c = lds32(s_c + 4 * i), cls = c & 7u;
+    const uint32_t lines = cls == kClsBit ? 1u : max(1u, (uint32_t)(P << cls) >> 2);  // (32 * P << cls) / 128
+    if (L.lin < lines) {
+      const uint8_t* p = L.tb + ((c & ~15u) + 128u * L.lin);
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+    }
+  }
+}
+
 template <int P, bool HASH>
 __device__ __forceinline__ void stage_ops_b(const LaneB& L, const uint8_t* buf, uint32_t w0, uint32_t nw,
                                             uint64_t (&hacc)[P]) {
@@ -407,8 +430,14 @@ __device__ __forceinline__ void stage_ops_b(const LaneB& L, const uint8_t* buf, 
   const uint32_t* items = reinterpret_cast<const uint32_t*>(buf + h->off_items);
   const uint32_t base = smem_addr(buf), n_items = h->n_items;
   const uint32_t s_c0 = base + h->off_c, s_w0 = base + h->off_w, s_k0 = base + h->off_k;
+#ifndef RS_NO_PREFETCH
+  if (w0 < n_items) prefetch_item<P>(L, items, runs, s_c0, w0);
+#endif
 #pragma unroll 1
   for (uint32_t it = w0; it < n_items; it += nw) {
+#ifndef RS_NO_PREFETCH
+    if (it + nw < n_items) prefetch_item<P>(L, items, runs, s_c0, it + nw);
+#endif
     const uint32_t w = items[it];
     const StageRun R = runs[w >> 16];
     const uint32_t b = w & 0x1FFFu, cnt = ((w >> 13) & 7u) + 1u;
