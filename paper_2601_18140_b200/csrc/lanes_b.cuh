@@ -26,7 +26,7 @@
 #include "lanes_t.cuh"
 
 #ifndef RS_LANES_B_MAX_THREADS
-#define RS_LANES_B_MAX_THREADS 768
+#define RS_LANES_B_MAX_THREADS 1024
 #endif
 
 namespace rtlsim {
@@ -536,18 +536,27 @@ __device__ __forceinline__ void stage_watch_b(const StepArgs& a, const LaneB& L,
   }
 }
 
+// Shared-memory bytes beyond the two stage buffers: per-lane hash partials,
+// scyc[4][LT] (the CTA's op / input terms of a cycle, by cycle mod 4) and
+// sreg[4][LT] (its register terms), summed with shared-memory atomics -- no
+// per-thread partial arrays, so the CTA can run 1,024 threads.
+__host__ __device__ constexpr size_t lanes_b_smem_extra(uint32_t P) { return 2ull * 4 * 32 * P * 8; }
+
 template <int P, bool HASH>
 __global__ void __launch_bounds__(RS_LANES_B_MAX_THREADS, 1) k_lanes_b(const StepArgs a) {
   constexpr uint32_t LT = 32u * P;
   extern __shared__ __align__(128) uint8_t smem[];
-  // [mbarriers | stage buffer 0 | stage buffer 1 | red[2][T*P] | hr[T*P] | hp[T*P] | lsum[3][LT]]
-  // (the hash partials exactly as in k_lanes_t)
+  // [mbarriers | stage buffer 0 | stage buffer 1 | scyc[4][LT] | sreg[4][LT]]
+  // Hash of cycle c (reading R12) = const + sum over the cluster's CTAs of
+  // scyc[c % 4] (ops and inputs of cycle c) + sreg[c % 4] (registers committed
+  // by the latch of cycle c - 1; slot 0 starts from the carry).  Every thread
+  // adds its partials with atomics at the cycle's last stage; after that
+  // stage's barrier the cluster's rank 0 sums the slots of all its CTAs
+  // (distributed shared memory); slot (c + 2) % 4 is cleared at cycle c.
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
   const uint32_t T = blockDim.x, tid = threadIdx.x;
-  uint64_t* red = reinterpret_cast<uint64_t*>(smem + 128 + 2 * (size_t)a.stage_bytes);
-  uint64_t* hr_s = red + 2 * T * P;
-  uint64_t* hp_s = red + 3 * T * P;
-  uint64_t* lsum = red + 4 * T * P;
+  uint64_t* scyc = reinterpret_cast<uint64_t*>(smem + 128 + 2 * (size_t)a.stage_bytes);
+  uint64_t* sreg = scyc + 4 * LT;
 
   const uint32_t CS = a.cluster;
   const uint32_t rank = blockIdx.x % CS, tile = blockIdx.x / CS;
@@ -562,11 +571,9 @@ __global__ void __launch_bounds__(RS_LANES_B_MAX_THREADS, 1) k_lanes_b(const Ste
     mbar_fence_init();
   }
   if constexpr (HASH) {
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-      const uint32_t l = lane + 32 * k;
-      hr_s[tid * P + k] = 0;
-      hp_s[tid * P + k] = (gw == 0 && l < a.n_lanes) ? a.hcarry_in[l] : 0ull;
+    for (uint32_t i = tid; i < 8 * LT; i += T) {
+      const uint32_t l = tile * LT + (i % LT);
+      scyc[i] = (i == 4 * LT + (i % LT) && rank == 0 && l < a.n_lanes) ? a.hcarry_in[l] : 0ull;  // sreg[0]
     }
   }
   __syncthreads();
@@ -585,7 +592,6 @@ __global__ void __launch_bounds__(RS_LANES_B_MAX_THREADS, 1) k_lanes_b(const Ste
 #pragma unroll
   for (int k = 0; k < P; ++k) hacc[k] = 0;
   uint32_t s = 0, cyc = 0;
-  int pend = -1;
 #pragma unroll 1
   for (uint32_t gi = 0; gi < total; ++gi) {
     const uint32_t bsel = gi & 1u;
@@ -609,8 +615,9 @@ __global__ void __launch_bounds__(RS_LANES_B_MAX_THREADS, 1) k_lanes_b(const Ste
         for (int k = 0; k < P; ++k) hr[k] = 0;
         stage_latch_b<P, HASH>(L, base + h->off_c, base + h->off_w, base + h->off_k, b, e, hr);
         if constexpr (HASH) {
+          uint64_t* sr = sreg + ((cyc + 1u) & 3u) * LT;
 #pragma unroll
-          for (int k = 0; k < P; ++k) hr_s[tid * P + k] += hr[k];
+          for (int k = 0; k < P; ++k) atomicAdd((unsigned long long*)&sr[lin + 32 * k], (unsigned long long)hr[k]);
         }
       }
     } else if (type == ST_INJECT) {
@@ -630,44 +637,36 @@ __global__ void __launch_bounds__(RS_LANES_B_MAX_THREADS, 1) k_lanes_b(const Ste
     const bool eoc = (s + 1 == S);
     if constexpr (HASH) {
       if (eoc) {
+        uint64_t* sc = scyc + (cyc & 3u) * LT;
 #pragma unroll
         for (int k = 0; k < P; ++k) {
-          red[(cyc & 1u) * T * P + tid * P + k] = hacc[k] + hp_s[tid * P + k];
-          hp_s[tid * P + k] = hr_s[tid * P + k];
-          hr_s[tid * P + k] = 0;
+          if (hacc[k]) atomicAdd((unsigned long long*)&sc[lin + 32 * k], (unsigned long long)hacc[k]);
           hacc[k] = 0;
+        }
+        if (warp == nwarp - 1) {  // clear the slots of cycle c + 2 (read two cycles ago)
+#pragma unroll
+          for (int k = 0; k < P; ++k) {
+            scyc[((cyc + 2u) & 3u) * LT + lin + 32 * k] = 0;
+            sreg[((cyc + 2u) & 3u) * LT + lin + 32 * k] = 0;
+          }
         }
       }
     }
     stage_barrier(CS);
     if constexpr (HASH) {
-      if (warp == 0 && a.hashes != nullptr) {
-        if (pend >= 0 && rank == 0) {
-          const uint32_t pb = (uint32_t)pend & 1u;
+      if (eoc && warp == 0 && rank == 0 && a.hashes != nullptr) {
+        const uint32_t sl = (cyc & 3u) * LT;
 #pragma unroll
-          for (int k = 0; k < P; ++k) {
-            const uint32_t li = lin + 32 * k;
-            uint64_t sum = a.g.const_hash + lsum[pb * LT + li];
-            for (uint32_t r = 1; r < CS; ++r) sum += dsmem(lsum, r)[pb * LT + li];
-            if (lane + 32 * k < a.n_lanes) a.hashes[(size_t)pend * a.n_lanes + lane + 32 * k] = sum;
+        for (int k = 0; k < P; ++k) {
+          const uint32_t li = lin + 32 * k;
+          uint64_t sum = a.g.const_hash + scyc[sl + li] + sreg[sl + li];
+          for (uint32_t r = 1; r < CS; ++r) {
+            const uint64_t* pc = dsmem(scyc, r);
+            sum += pc[sl + li] + pc[4 * LT + sl + li];
           }
-        }
-        if (eoc) {
-          const uint64_t* rr = red + (cyc & 1u) * T * P + lin * P;
-#pragma unroll
-          for (int k = 0; k < P; ++k) {
-            uint64_t sum = 0;
-#pragma unroll 4
-            for (uint32_t i = 0; i < nwarp; ++i) sum += rr[i * 32 * P + k];
-            if (CS == 1) {
-              if (lane + 32 * k < a.n_lanes) a.hashes[(size_t)cyc * a.n_lanes + lane + 32 * k] = sum + a.g.const_hash;
-            } else {
-              lsum[(cyc & 1u) * LT + lin + 32 * k] = sum;
-            }
-          }
+          if (lane + 32 * k < a.n_lanes) a.hashes[(size_t)cyc * a.n_lanes + lane + 32 * k] = sum;
         }
       }
-      if (CS > 1) pend = eoc ? (int)cyc : -1;
     }
     if (eoc) {
       s = 0;
@@ -677,32 +676,19 @@ __global__ void __launch_bounds__(RS_LANES_B_MAX_THREADS, 1) k_lanes_b(const Ste
     }
   }
   if constexpr (HASH) {
-    __syncthreads();
-    if (warp == 0) {
-#pragma unroll
-      for (int k = 0; k < P; ++k) {
-        uint64_t sum = 0;
-        for (uint32_t i = 0; i < nwarp; ++i) sum += hp_s[(i * 32 + lin) * P + k];
-        lsum[2 * LT + lin + 32 * k] = sum;
-      }
-    }
+    // register term of the next cycle: sreg[cyc % 4] over the cluster
     stage_barrier(CS);
     if (warp == 0 && rank == 0) {
+      const uint32_t sl = (cyc & 3u) * LT;
 #pragma unroll
       for (int k = 0; k < P; ++k) {
         const uint32_t li = lin + 32 * k, l = lane + 32 * k;
-        uint64_t sum = lsum[2 * LT + li];
-        for (uint32_t r = 1; r < CS; ++r) sum += dsmem(lsum, r)[2 * LT + li];
+        uint64_t sum = sreg[sl + li];
+        for (uint32_t r = 1; r < CS; ++r) sum += dsmem(sreg, r)[sl + li];
         if (l < a.n_lanes) a.hcarry_out[l] = sum;
-        if (pend >= 0 && a.hashes != nullptr) {
-          const uint32_t pb = (uint32_t)pend & 1u;
-          uint64_t hs = a.g.const_hash + lsum[pb * LT + li];
-          for (uint32_t r = 1; r < CS; ++r) hs += dsmem(lsum, r)[pb * LT + li];
-          if (l < a.n_lanes) a.hashes[(size_t)pend * a.n_lanes + l] = hs;
-        }
       }
     }
-    if (CS > 1) stage_barrier(CS);
+    if (CS > 1) stage_barrier(CS);  // keep every CTA's shared memory alive until rank 0 has read it
   }
 }
 

@@ -1174,8 +1174,9 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
     if (hash) s->hc_cur = 1 - s->hc_cur;
   } else {
     a.hcarry_out = a.hcarry_in;
-    const size_t smem = s->variant != 2 ? 128 + 2ull * s->g->stage_bytes + lanes_t_smem_extra(s->threads, s->LT / 32)
-                                        : lanes_smem(s->g->stage_bytes, s->threads);
+    const size_t smem = s->variant == 6   ? 128 + 2ull * s->g->stage_bytes + lanes_b_smem_extra(s->LT / 32)
+                        : s->variant == 1 ? 128 + 2ull * s->g->stage_bytes + lanes_t_smem_extra(s->threads, s->LT / 32)
+                                          : lanes_smem(s->g->stage_bytes, s->threads);
     const void* fns[] = {(const void*)k_lanes<32, true>, (const void*)k_lanes<32, false>,
                          (const void*)k_lanes<16, true>, (const void*)k_lanes<16, false>,
                          (const void*)k_lanes<8, true>,  (const void*)k_lanes<8, false>,
