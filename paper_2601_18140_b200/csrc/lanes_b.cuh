@@ -26,7 +26,7 @@
 #include "lanes_t.cuh"
 
 #ifndef RS_LANES_B_MAX_THREADS
-#define RS_LANES_B_MAX_THREADS 1024
+#define RS_LANES_B_MAX_THREADS 768
 #endif
 
 namespace rtlsim {
