@@ -268,6 +268,8 @@ def main():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-hash", action="store_true", help="time the hash-off step as the headline")
+    ap.add_argument("--no-passes", action="store_true",
+                    help="compile without the constant / copy propagation passes (RS_LOAD_PASSES)")
     ap.add_argument("--no-hash-off-pass", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -315,8 +317,9 @@ def main():
         total_lanes = shard.n_lanes * world
     lanes = shard.n_lanes
     stream = torch.cuda.Stream()
-    g = rs.Graph(circ, device=dev, mode="single" if single else "lanes")
+    g = rs.Graph(circ, device=dev, mode="single" if single else "lanes", passes=not args.no_passes)
     info = g.info()
+    info0 = rs.Graph(circ, device=rs.RS_DEVICE_NONE, mode="single" if single else "lanes").info()
     mk = dict(lane0=shard.lane0, lane_tile=args.lane_tile, threads=args.threads, stream=stream,
               cluster=args.cluster, parts=args.parts, kernel=args.kernel, repcut=args.repcut)
     L = rs.Lanes(g, lanes, **mk)
@@ -436,12 +439,16 @@ def main():
                        **({"level_cut_parts": args.parts} if args.parts > 1 else {}),
                        **({"repcut_partitions": args.repcut} if args.repcut >= 1 else {}),
                        "state_bytes_per_gpu": info["state_bytes_per_lane"] * lanes,
+                       "graph_passes": None if args.no_passes else {
+                           "ops_evaluated": info["n_ops"], "aliases": info["n_alias"],
+                           "folded": info["n_folded"], "mux_chains_counted": info["n_mux_chain"]},
                        **({"watched_signals": args.watch} if args.watch else {})},
             "op_evals_per_s": value * circ.n_ops,
             "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "peak_source": peak_src, "alg_bytes_per_launch": alg_bytes,
                          "alg_bytes_per_lane_cycle": info["alg_bytes_per_lane_cycle"],
+                         "alg_bytes_per_lane_cycle_without_passes": info0["alg_bytes_per_lane_cycle"],
                          "graph_alg_bytes": info["graph_alg_bytes"], "kernel": kernel_name},
             "clocks": clk.summary(),
             "gpu_launches": launches,

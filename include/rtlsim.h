@@ -63,6 +63,15 @@ enum {
   RS_MODE_LANES = 0,   /* many lanes: a CTA owns a lane tile; CTA barrier between levels */
   RS_MODE_SINGLE = 1   /* one lane: ops of a level spread over the grid; grid barrier between levels */
 };
+/* Flag OR-ed into rs_load_graph's mode: run the compiler's data-level graph passes
+ * (§6.1, App. B.1) --
+ * constant propagation (ops of constant operands, and a few absorbing cases, become
+ * constant signals) and copy propagation (an op whose result always equals an
+ * operand's value becomes an alias of it: no row, no evaluation; reads of it read
+ * the operand, and its hash weight is folded into the operand's, so every result
+ * -- hashes, rs_read_signals, waveforms -- is unchanged).  rs_graph_info reports
+ * what was removed. */
+#define RS_LOAD_PASSES 0x100u
 
 /* Where a pointer lives. */
 enum { RS_MEM_NONE = 0, RS_MEM_HOST = 1, RS_MEM_DEVICE = 2 };
@@ -111,8 +120,10 @@ typedef struct {
   uint64_t graph_alg_bytes;       /* G: int32 operand coords + one u32 param word per op */
   uint64_t alg_bytes_per_lane_cycle;  /* SURVEY §8(d) B_alg per lane per cycle, excluding G */
   uint64_t identity_ops_naive;    /* copies a naive §4.2 construction would need */
-  uint32_t rows_bit;              /* class-0 rows [0, rows_bit) are the 1-bit signals (bit planes in lane kernel 3) */
-  uint32_t pad_;
+  uint32_t rows_bit;              /* class-0 rows [0, rows_bit) are the 1-bit signals (bit planes in lane kernel 6) */
+  uint32_t n_alias;               /* RS_LOAD_PASSES: ops removed by copy propagation (signals aliased) */
+  uint32_t n_folded;              /* RS_LOAD_PASSES: ops removed by constant propagation */
+  uint32_t n_mux_chain;           /* RS_LOAD_PASSES: muxes whose else-branch is another mux (counted, not fused) */
 } rs_graph_info;
 
 /* Options for rs_alloc_lanes (NULL -> all defaults). */

@@ -38,7 +38,10 @@ rs_status fail(std::string* err, rs_status st, const char* fmt, unsigned long lo
 
 }  // namespace
 
-rs_status compile_graph(const rs_graph_desc* d, uint32_t mode, CompiledGraph* out, std::string* err) {
+// alias (optional, graph passes): alias[s] != s marks signal s as an alias of
+// alias[s] -- no driver, no row, its hash weight added to its representative's.
+static rs_status compile_core(const rs_graph_desc* d, uint32_t mode, CompiledGraph* out, std::string* err,
+                              const std::vector<uint32_t>* alias, const std::vector<uint32_t>* cat_wb = nullptr) {
   if (!d || !out) return fail(err, RS_E_INVALID_ARG, "NULL desc or out");
   if (mode != RS_MODE_LANES && mode != RS_MODE_SINGLE)
     return fail(err, RS_E_INVALID_ARG, "unknown mode %llu", mode);
@@ -79,8 +82,14 @@ rs_status compile_graph(const rs_graph_desc* d, uint32_t mode, CompiledGraph* ou
     if (!claim(d->const_id[i], -4)) return fail(err, RS_E_GRAPH, "const %llu: bad id or multiple drivers", i);
   for (uint32_t j = 0; j < NO; ++j)
     if (!claim(d->out_id[j], j)) return fail(err, RS_E_GRAPH, "op %llu: bad out id or multiple drivers", j);
+  auto is_alias = [&](uint32_t s) -> bool { return alias && (*alias)[s] != s; };
   for (uint32_t s = 0; s < NS; ++s)
-    if (drv[s] == -1) return fail(err, RS_E_GRAPH, "signal %llu has no driver", s);
+    if (drv[s] == -1 && !is_alias(s)) return fail(err, RS_E_GRAPH, "signal %llu has no driver", s);
+  // hash weights (reading R12): an alias's weight moves to its representative
+  std::vector<uint64_t> W(NS);
+  for (uint32_t s = 0; s < NS; ++s) W[s] = is_alias(s) ? 0ull : hash_weight(s);
+  for (uint32_t s = 0; s < NS; ++s)
+    if (is_alias(s)) W[(*alias)[s]] += hash_weight(s);
   for (uint32_t i = 0; i < d->n_regs; ++i)
     if (d->reg_next_id[i] >= NS) return fail(err, RS_E_GRAPH, "register %llu: next id out of range", i);
 
@@ -211,7 +220,7 @@ rs_status compile_graph(const rs_graph_desc* d, uint32_t mode, CompiledGraph* ou
   // allocation may keep them as bit planes (lanes_b.cuh)
   std::vector<uint32_t> sig_coord(NS + g.n_copy, 0);
   uint32_t n_bit = 0;
-  for (uint32_t s = 0; s < NS; ++s) n_bit += d->width[s] == 1;
+  for (uint32_t s = 0; s < NS; ++s) n_bit += d->width[s] == 1 && !is_alias(s);
   for (const Copy& c : copies) n_bit += d->width[c.src] == 1;
   uint32_t rows[4] = {0, 0, 0, 0}, bit_row = 0;
   rows[0] = n_bit;
@@ -266,6 +275,8 @@ rs_status compile_graph(const rs_graph_desc* d, uint32_t mode, CompiledGraph* ou
   }
   for (int c = 0; c < 4; ++c) g.rows[c] = rows[c];
   g.rows_bit = n_bit;
+  for (uint32_t s = 0; s < NS; ++s)
+    if (is_alias(s)) sig_coord[s] = sig_coord[(*alias)[s]];
   if (bit_row != n_bit) return fail(err, RS_E_GRAPH, "internal: 1-bit rows %llu != %llu", bit_row, n_bit);
 
   // ---- per-op arrays in device order
@@ -280,9 +291,9 @@ rs_status compile_graph(const rs_graph_desc* d, uint32_t mode, CompiledGraph* ou
       const uint32_t a0 = d->arg_off[t];
       if (op == RS_OP_SHL || op == RS_OP_SHR) p0 = std::min<uint32_t>(d->param[2 * t], 64u);
       if (op == RS_OP_BITS) { p0 = d->param[2 * t]; p1 = d->param[2 * t + 1]; }
-      if (op == RS_OP_CAT) p0 = d->width[d->arg_id[a0 + 1]];
+      if (op == RS_OP_CAT) p0 = cat_wb ? (*cat_wb)[t] : d->width[d->arg_id[a0 + 1]];
       for (uint32_t a = a0; a < a0 + n; ++a) g.coord.push_back(sig_coord[d->arg_id[a]]);
-      g.opk.push_back(hash_weight(d->out_id[t]));
+      g.opk.push_back(W[d->out_id[t]]);
     } else {
       g.coord.push_back(sig_coord[copies[t - NO].src]);
       g.opk.push_back(0);
@@ -297,7 +308,7 @@ rs_status compile_graph(const rs_graph_desc* d, uint32_t mode, CompiledGraph* ou
     const uint32_t s = d->input_id[i];
     g.in_coord.push_back(sig_coord[s]);
     g.in_w.push_back(d->width[s]);
-    g.in_k.push_back(hash_weight(s));
+    g.in_k.push_back(W[s]);
     B += 1ull << width_class(d->width[s]);
   }
   for (uint32_t i = 0; i < d->n_regs; ++i) {
@@ -306,10 +317,10 @@ rs_status compile_graph(const rs_graph_desc* d, uint32_t mode, CompiledGraph* ou
     g.reg_coord.push_back(sig_coord[s]);
     g.reg_next_coord.push_back(sig_coord[reg_src[i]]);
     g.reg_w.push_back(w);
-    g.reg_k.push_back(hash_weight(s));
+    g.reg_k.push_back(W[s]);
     const uint64_t init = (d->reg_init ? d->reg_init[i] : 0) & width_mask(w);
     g.reg_init.push_back(init);
-    g.init_reg_hash += init * hash_weight(s);
+    g.init_reg_hash += init * W[s];
     B += (1ull << width_class(w)) + (1ull << width_class(d->width[d->reg_next_id[i]]));
   }
   for (uint32_t i = 0; i < d->n_consts; ++i) {
@@ -317,7 +328,7 @@ rs_status compile_graph(const rs_graph_desc* d, uint32_t mode, CompiledGraph* ou
     const uint64_t v = d->const_val[i] & width_mask(d->width[s]);
     g.const_coord.push_back(sig_coord[s]);
     g.const_val.push_back(v);
-    g.const_hash += v * hash_weight(s);
+    g.const_hash += v * W[s];
   }
   // canonical maps
   g.sig_coord.assign(sig_coord.begin(), sig_coord.begin() + NS);
@@ -326,6 +337,14 @@ rs_status compile_graph(const rs_graph_desc* d, uint32_t mode, CompiledGraph* ou
   for (uint32_t i = 0; i < d->n_inputs; ++i) g.sig_kind[d->input_id[i]] = 0;
   for (uint32_t i = 0; i < d->n_regs; ++i) { g.sig_kind[d->reg_id[i]] = 1; g.sig_reg_index[d->reg_id[i]] = (int32_t)i; }
   for (uint32_t i = 0; i < d->n_consts; ++i) g.sig_kind[d->const_id[i]] = 2;
+  g.sig_rep.resize(NS);
+  for (uint32_t s = 0; s < NS; ++s) {
+    g.sig_rep[s] = alias ? (*alias)[s] : s;
+    if (is_alias(s)) {  // read back like its representative
+      g.sig_kind[s] = g.sig_kind[(*alias)[s]];
+      g.sig_reg_index[s] = g.sig_reg_index[(*alias)[s]];
+    }
+  }
 
   // ---- statistics: B_alg per lane-cycle, G, naive identity count
   uint64_t G = 0;
@@ -352,6 +371,47 @@ rs_status compile_graph(const rs_graph_desc* d, uint32_t mode, CompiledGraph* ou
       if (last[s] - plev[s] - 1 > 0) ids += (uint64_t)(last[s] - plev[s] - 1);
     g.identity_ops_naive = ids;
   }
+  return RS_OK;
+}
+
+rs_status compile_graph(const rs_graph_desc* d, uint32_t mode, CompiledGraph* out, std::string* err) {
+  if (!(mode & RS_LOAD_PASSES)) return compile_core(d, mode, out, err, nullptr);
+  mode &= ~RS_LOAD_PASSES;
+  // validate the circuit as given (drivers, arities, params, loops) first
+  rs_status st = compile_core(d, mode, out, err, nullptr);
+  if (st != RS_OK) return st;
+  // a topological order: the ops by their (valid) levels
+  const uint32_t NO = d->n_ops, NS = d->n_signals;
+  std::vector<int64_t> drv(NS, -1);
+  for (uint32_t j = 0; j < NO; ++j) drv[d->out_id[j]] = j;
+  std::vector<uint32_t> lev(NO, 0), topo(NO);
+  {
+    // ASAP levels by a Kahn sweep over the producers (the core run proved acyclicity)
+    std::vector<uint32_t> indeg(NO, 0), off(NS + 1, 0);
+    for (uint32_t j = 0; j < NO; ++j)
+      for (uint32_t a = d->arg_off[j]; a < d->arg_off[j + 1]; ++a)
+        if (drv[d->arg_id[a]] >= 0) { indeg[j]++; off[d->arg_id[a] + 1]++; }
+    for (uint32_t s2 = 0; s2 < NS; ++s2) off[s2 + 1] += off[s2];
+    std::vector<uint32_t> users(off[NS]), fill(off.begin(), off.end() - 1);
+    for (uint32_t j = 0; j < NO; ++j)
+      for (uint32_t a = d->arg_off[j]; a < d->arg_off[j + 1]; ++a)
+        if (drv[d->arg_id[a]] >= 0) users[fill[d->arg_id[a]]++] = j;
+    size_t h = 0, t = 0;
+    for (uint32_t j = 0; j < NO; ++j) if (indeg[j] == 0) topo[t++] = j;
+    while (h < t) {
+      const uint32_t j = topo[h++], o = d->out_id[j];
+      for (uint32_t u = off[o]; u < off[o + 1]; ++u)
+        if (--indeg[users[u]] == 0) topo[t++] = users[u];
+    }
+  }
+  PassResult pr;
+  run_passes(d, drv, topo, &pr);
+  st = compile_core(&pr.desc, mode, out, err, &pr.rep, &pr.cat_wb);
+  if (st != RS_OK) return st;
+  out->n_alias = pr.n_alias;
+  out->n_folded = (uint32_t)pr.folded.size();
+  out->n_mux_chain = pr.n_mux_chain;
+  out->n_ops_input = NO;
   return RS_OK;
 }
 

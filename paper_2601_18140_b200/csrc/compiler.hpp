@@ -54,6 +54,10 @@ struct CompiledGraph {
   uint32_t n_ops = 0, n_copy = 0, n_levels = 0;
   uint32_t rows[4] = {0, 0, 0, 0};
   uint32_t rows_bit = 0;            // class-0 rows [0, rows_bit) are exactly the 1-bit signals
+  // graph passes (RS_LOAD_PASSES): canonical id -> representative (itself, or the
+  // signal an alias reads), ops removed as aliases / folded to constants, mux chains
+  std::vector<uint32_t> sig_rep;
+  uint32_t n_alias = 0, n_folded = 0, n_mux_chain = 0, n_ops_input = 0;
   // per-op arrays in device order (level-major, run-major)
   std::vector<uint32_t> opw;        // param word
   std::vector<uint64_t> opk;        // hash weight of the op's output (0 for copies)
@@ -100,8 +104,27 @@ inline uint64_t splitmix_next(uint64_t x) {
 inline uint64_t hash_weight(uint64_t s) { return splitmix_next(0x5EED000000000000ull + s) | 1ull; }
 inline uint64_t width_mask(uint32_t w) { return w >= 64 ? ~0ull : ((1ull << w) - 1ull); }
 
-// Returns RS_OK or an error status with *err set.
+// Returns RS_OK or an error status with *err set.  mode: RS_MODE_LANES or
+// RS_MODE_SINGLE, optionally | RS_LOAD_PASSES (constant / copy propagation,
+// passes.cpp).
 rs_status compile_graph(const rs_graph_desc* d, uint32_t mode, CompiledGraph* out, std::string* err);
+
+// ---------------------------------------------------------------- graph passes (NEXT-1)
+// Result of run_passes: the rewritten circuit (surviving ops, operands renamed to
+// their representatives, folded signals turned into constants) plus, per
+// canonical signal, its representative (itself unless it became an alias).
+struct PassResult {
+  std::vector<uint32_t> rep;       // [n_signals]
+  std::vector<uint32_t> folded;    // signals turned into constants
+  uint32_t n_alias = 0, n_mux_chain = 0;
+  std::vector<uint8_t> width, opcode;
+  std::vector<uint32_t> input_id, reg_id, reg_next_id, const_id, out_id, arg_off, arg_id, param, level, cat_wb;
+  std::vector<uint64_t> reg_init, const_val;
+  rs_graph_desc desc;              // points into the vectors above
+};
+// topo: the ops in a topological order.
+void run_passes(const rs_graph_desc* d, const std::vector<int64_t>& drv, const std::vector<uint32_t>& topo,
+                PassResult* out);
 
 // ---------------------------------------------------------------- stages
 // The lane kernel walks a fixed per-cycle schedule of *stages*; each stage's

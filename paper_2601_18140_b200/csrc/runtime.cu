@@ -472,7 +472,9 @@ rs_status rs_graph_info_get(const rs_graph* g, rs_graph_info* o) {
   o->alg_bytes_per_lane_cycle = cg.alg_bytes_per_lane_cycle;
   o->identity_ops_naive = cg.identity_ops_naive;
   o->rows_bit = cg.rows_bit;
-  o->pad_ = 0;
+  o->n_alias = cg.n_alias;
+  o->n_folded = cg.n_folded;
+  o->n_mux_chain = cg.n_mux_chain;
   return RS_OK;
 }
 
@@ -1283,7 +1285,8 @@ rs_status rs_write_registers(rs_lanes* s, const uint32_t* reg_ids, uint32_t n, u
   std::vector<uint32_t> cw(2 * (size_t)n);
   for (uint32_t i = 0; i < n; ++i) {
     const uint32_t id = reg_ids[i];
-    if (id >= s->g->cg.n_signals || s->g->cg.sig_kind[id] != 1) return set_err(RS_E_RANGE, "signal %u is not a register", id);
+    if (id >= s->g->cg.n_signals || s->g->cg.sig_kind[id] != 1 || s->g->cg.sig_rep[id] != id)
+      return set_err(RS_E_RANGE, "signal %u is not a register", id);
     cw[i] = s->g->cg.sig_coord[id];
     cw[n + i] = s->g->cg.reg_w[s->g->cg.sig_reg_index[id]];
   }

@@ -17,6 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("RTLSIM_LIB") or os.path.join(_HERE, "lib", "librtlsim.so")
 
 RS_MODE_LANES, RS_MODE_SINGLE = 0, 1
+RS_LOAD_PASSES = 0x100
 RS_MEM_NONE, RS_MEM_HOST, RS_MEM_DEVICE = 0, 1, 2
 STATUS = {0: "RS_OK", -1: "RS_E_INVALID_ARG", -2: "RS_E_GRAPH", -3: "RS_E_CAPACITY", -4: "RS_E_OOM",
           -5: "RS_E_CUDA", -6: "RS_E_STATE", -7: "RS_E_RANGE", -8: "RS_E_UNSUPPORTED"}
@@ -58,7 +59,8 @@ class GraphInfo(C.Structure):
         ("n_runs", C.c_uint32), ("n_coords", C.c_uint32), ("rows", C.c_uint32 * 4),
         ("state_bytes_per_lane", C.c_uint64), ("graph_device_bytes", C.c_uint64),
         ("graph_alg_bytes", C.c_uint64), ("alg_bytes_per_lane_cycle", C.c_uint64),
-        ("identity_ops_naive", C.c_uint64), ("rows_bit", C.c_uint32), ("pad_", C.c_uint32),
+        ("identity_ops_naive", C.c_uint64), ("rows_bit", C.c_uint32), ("n_alias", C.c_uint32),
+        ("n_folded", C.c_uint32), ("n_mux_chain", C.c_uint32),
     ]
 
 
@@ -141,7 +143,7 @@ class Graph:
     """rs_load_graph: compile a circuit (synth.Circuit or any object with the
     same arrays) into the GPU graph format on ``device``."""
 
-    def __init__(self, circuit, device: int = 0, mode: str = "lanes", use_levels: bool = True):
+    def __init__(self, circuit, device: int = 0, mode: str = "lanes", use_levels: bool = True, passes: bool = False):
         c = circuit.normalized() if hasattr(circuit, "normalized") else circuit
         self._keep = dict(
             width=_arr(c.width, np.uint8), input_id=_arr(c.input_id, np.uint32),
@@ -165,7 +167,8 @@ class Graph:
         self.mode = RS_MODE_SINGLE if mode == "single" else RS_MODE_LANES
         self.device = device
         h = C.c_void_p()
-        _check(lib().rs_load_graph(C.byref(self.desc), device, self.mode, C.byref(h)))
+        _check(lib().rs_load_graph(C.byref(self.desc), device, self.mode | (RS_LOAD_PASSES if passes else 0),
+                                   C.byref(h)))
         self.h = h
 
     def info(self) -> dict:

@@ -111,3 +111,65 @@ def edge_values(rng: np.random.Generator, shape) -> np.ndarray:
         np.where(kind < 55, np.uint64(1) << np.uint64(63),
         np.where(kind < 70, sparse, rand)))))
     return v.reshape(shape)
+
+
+def pass_circuit(seed: int = 0, n: int = 400) -> Circuit:
+    """A random circuit rich in what the compiler's graph passes remove (SURVEY.md
+    §8(f) NEXT-1): constants feeding ops (constant propagation), identity ops --
+    shifts by 0, full-width bits, and with all ones, or / xor / add with 0, sub of
+    0, mul by 1, mux with a constant selector or equal branches, cat(0, x) -- and
+    absorbing ones (and with 0, x ^ x, x - x, eq(x, x)), in chains, feeding
+    registers and each other, mixed with ordinary ops.  Structure only."""
+    rng = np.random.default_rng(9000 + seed)
+    b = Builder(f"passes{seed}")
+    pool = [b.input(int(w)) for w in rng.choice([1, 4, 8, 13, 32, 64], size=6)]
+    regs = [b.reg(int(w), init=int(rng.integers(0, 2**40))) for w in (1, 8, 32, 64, 5)]
+    pool += regs
+    consts = [b.const(w, v) for w, v in ((64, 0), (64, 2**64 - 1), (8, 1), (1, 1), (1, 0), (16, 0xABCD), (64, 1))]
+    W = b.width
+    zero64, ones64, one8, one1, zero1, k16, one64 = consts
+
+    def pick():
+        return int(rng.choice(pool))
+
+    for _ in range(n):
+        x = pick()
+        w = W[x]
+        kind = int(rng.integers(0, 18))
+        if kind == 0:
+            s = b.op("shl", [x], w + int(rng.integers(0, 65 - w)), p0=0)
+        elif kind == 1:
+            s = b.op("shr", [x], w, p0=0)
+        elif kind == 2:
+            s = b.op("bits", [x], w, p0=min(63, w - 1 + int(rng.integers(0, 3))), p1=0)
+        elif kind == 3:
+            s = b.op("and", [x, ones64] if rng.random() < 0.5 else [ones64, x], w)
+        elif kind == 4:
+            s = b.op(str(rng.choice(["or", "xor", "add"])), [x, zero64] if rng.random() < 0.5 else [zero64, x], 64)
+        elif kind == 5:
+            s = b.op("sub", [x, zero64], w)
+        elif kind == 6:
+            s = b.op("mul", [x, one64], w)
+        elif kind == 7:
+            s = b.op("mux", [int(rng.choice([one1, zero1, k16, zero64])), x, pick()], 64)
+        elif kind == 8:
+            s = b.op("mux", [pick(), x, x], w)
+        elif kind == 9:
+            s = b.op("cat", [zero64, x], w)
+        elif kind == 10:
+            s = b.op(str(rng.choice(["and", "mul"])), [x, zero64], w)
+        elif kind == 11:
+            s = b.op(str(rng.choice(["xor", "sub", "eq", "lt", "or", "and"])), [x, x], w)
+        elif kind == 12:
+            s = b.op(str(rng.choice(["add", "xor", "mul", "eq", "lt", "cat"])),
+                     [int(rng.choice(consts)), int(rng.choice(consts))], int(rng.integers(1, 65)))
+        elif kind == 13:
+            s = b.op("not", [int(rng.choice(consts))], int(rng.integers(1, 65)))
+        else:
+            s = b.op(str(rng.choice(["add", "xor", "and", "or", "sub", "mul", "eq", "lt", "cat"])), [x, pick()],
+                     int(rng.integers(1, 65)))
+        pool.append(s)
+    ops_out = [s for s in pool[len(pool) - n:]]
+    for r in regs:
+        b.set_next(r, int(rng.choice(ops_out)))
+    return b.build()

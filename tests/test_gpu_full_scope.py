@@ -39,7 +39,7 @@ def _load(name, fname):
 
 def _gpu_sampled(rs, c, seed, n_lanes, lane0, cycles, local_lanes, chunk):
     import torch
-    g = rs.Graph(c, device=0)
+    g = rs.Graph(c, device=0, passes=True)       # bench.py's default compile (graph passes on)
     L = rs.Lanes(g, n_lanes, lane0=lane0)
     L.set_seed(seed)
     dev = torch.empty(chunk * n_lanes, dtype=torch.int64, device="cuda")
@@ -81,7 +81,7 @@ def test_c4_shards_full_cycles_sampled_lanes(rs):
 
 def test_c5_all_100k_cycles(rs):
     z, c, cfg = _load("C5", "C5_full.npz")
-    g = rs.Graph(c, device=0, mode="single")
+    g = rs.Graph(c, device=0, mode="single", passes=True)
     L = rs.Lanes(g, 1)
     L.set_seed(cfg.stim_seed)
     H = np.concatenate([L.step(20_000, hashes="host") for _ in range(cfg.cycles // 20_000)])
