@@ -458,6 +458,7 @@ constexpr uint32_t kMaxStageOps = 8191;   // 13-bit op field of a work item
 
 void build_stages(const CompiledGraph& g, uint32_t stage_bytes, uint32_t batch, std::vector<uint8_t>* blob,
                   std::vector<StageRef>* table) {
+  stage_bytes = std::max<uint32_t>(stage_bytes, 4096);  // room for >= 1 entry per stage (always progresses)
   blob->clear();
   table->clear();
   StageWriter W{blob, table};

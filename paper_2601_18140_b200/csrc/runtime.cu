@@ -446,7 +446,7 @@ rs_status rs_load_graph(const rs_graph_desc* desc, int device, uint32_t mode, rs
   d.const_hash = cg.const_hash;
   g->d_sig_coord = (uint32_t*)P(o_sig);
   cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, device);
-  if (mode == RS_MODE_LANES) {
+  if (cg.mode == RS_MODE_LANES) {  // (mode may carry RS_LOAD_PASSES)
     g->stage_bytes = kStageBytes;
     build_stages(cg, g->stage_bytes, kBatch, &g->stage_blob[0], &g->stage_tab[0]);
     g->stages_built[0] = true;
