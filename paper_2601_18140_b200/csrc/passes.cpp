@@ -58,8 +58,9 @@ void run_passes(const rs_graph_desc* d, const std::vector<int64_t>& drv, const s
   r = PassResult();
   r.rep.resize(NS);
   for (uint32_t s = 0; s < NS; ++s) r.rep[s] = s;
-  std::vector<uint8_t> is_const(NS, 0);
+  std::vector<uint8_t> is_const(NS, 0), is_reg(NS, 0);
   std::vector<uint64_t> cval(NS, 0);
+  for (uint32_t i = 0; i < d->n_regs; ++i) is_reg[d->reg_id[i]] = 1;
   for (uint32_t i = 0; i < d->n_consts; ++i) {
     is_const[d->const_id[i]] = 1;
     cval[d->const_id[i]] = d->const_val[i] & width_mask(d->width[d->const_id[i]]);
@@ -89,9 +90,13 @@ void run_passes(const rs_graph_desc* d, const std::vector<int64_t>& drv, const s
       r.folded.push_back(out_s);
     };
     auto make_alias = [&](uint32_t x) {  // result == value of x for every input
+      // never a register: after the commit a register holds its NEXT value, while
+      // an op's signal keeps the cycle's value (rs_read_signals would differ)
+      if (is_reg[x]) return false;
       r.rep[out_s] = x;
       removed[j] = 1;
       r.n_alias++;
+      return true;
     };
     auto kc = [&](uint32_t i, uint64_t v) { return is_const[args[i]] && (cval[args[i]] & width_mask(w)) == v; };
     auto ones = [&](uint32_t i, uint32_t other) {  // constant i covers every bit of the other operand
@@ -108,26 +113,26 @@ void run_passes(const rs_graph_desc* d, const std::vector<int64_t>& drv, const s
       switch (op) {
         case RS_OP_AND:
           if (kc(0, 0) || kc(1, 0)) { make_const(0); continue; }
-          if (ones(1, 0) && w >= wid(x0)) { make_alias(x0); continue; }
-          if (ones(0, 1) && w >= wid(x1)) { make_alias(x1); continue; }
-          if (same && w >= wid(x0)) { make_alias(x0); continue; }
+          if (ones(1, 0) && w >= wid(x0)) { if (make_alias(x0)) continue; }
+          if (ones(0, 1) && w >= wid(x1)) { if (make_alias(x1)) continue; }
+          if (same && w >= wid(x0)) { if (make_alias(x0)) continue; }
           break;
         case RS_OP_OR:
         case RS_OP_XOR:
         case RS_OP_ADD:
           if (op == RS_OP_XOR && same) { make_const(0); continue; }
-          if (op == RS_OP_OR && same && w >= wid(x0)) { make_alias(x0); continue; }
-          if (is_const[x1] && cval[x1] == 0 && w >= wid(x0)) { make_alias(x0); continue; }
-          if (is_const[x0] && cval[x0] == 0 && w >= wid(x1)) { make_alias(x1); continue; }
+          if (op == RS_OP_OR && same && w >= wid(x0)) { if (make_alias(x0)) continue; }
+          if (is_const[x1] && cval[x1] == 0 && w >= wid(x0)) { if (make_alias(x0)) continue; }
+          if (is_const[x0] && cval[x0] == 0 && w >= wid(x1)) { if (make_alias(x1)) continue; }
           break;
         case RS_OP_SUB:
           if (same) { make_const(0); continue; }
-          if (is_const[x1] && cval[x1] == 0 && w >= wid(x0)) { make_alias(x0); continue; }
+          if (is_const[x1] && cval[x1] == 0 && w >= wid(x0)) { if (make_alias(x0)) continue; }
           break;
         case RS_OP_MUL:
           if (kc(0, 0) || kc(1, 0)) { make_const(0); continue; }
-          if (is_const[x1] && cval[x1] == 1 && w >= wid(x0)) { make_alias(x0); continue; }
-          if (is_const[x0] && cval[x0] == 1 && w >= wid(x1)) { make_alias(x1); continue; }
+          if (is_const[x1] && cval[x1] == 1 && w >= wid(x0)) { if (make_alias(x0)) continue; }
+          if (is_const[x0] && cval[x0] == 1 && w >= wid(x1)) { if (make_alias(x1)) continue; }
           break;
         case RS_OP_EQ:
           if (same) { make_const(1); continue; }
@@ -136,15 +141,15 @@ void run_passes(const rs_graph_desc* d, const std::vector<int64_t>& drv, const s
           if (same) { make_const(0); continue; }
           break;
         case RS_OP_CAT:
-          if (is_const[x0] && cval[x0] == 0 && w >= wid(x1)) { make_alias(x1); continue; }
+          if (is_const[x0] && cval[x0] == 0 && w >= wid(x1)) { if (make_alias(x1)) continue; }
           break;
         default:
           break;
       }
     } else if (n == 1) {
       const uint32_t x0 = args[0];
-      if ((op == RS_OP_SHL || op == RS_OP_SHR) && p0 == 0 && w >= wid(x0)) { make_alias(x0); continue; }
-      if (op == RS_OP_BITS && p1 == 0 && p0 + 1 >= wid(x0) && w >= wid(x0)) { make_alias(x0); continue; }
+      if ((op == RS_OP_SHL || op == RS_OP_SHR) && p0 == 0 && w >= wid(x0)) { if (make_alias(x0)) continue; }
+      if (op == RS_OP_BITS && p1 == 0 && p0 + 1 >= wid(x0) && w >= wid(x0)) { if (make_alias(x0)) continue; }
       if ((op == RS_OP_SHL && p0 >= w) || (op == RS_OP_SHR && p0 >= wid(x0)) || (op == RS_OP_BITS && p1 >= wid(x0))) {
         make_const(0);
         continue;
@@ -153,9 +158,9 @@ void run_passes(const rs_graph_desc* d, const std::vector<int64_t>& drv, const s
       const uint32_t s = args[0], xa = args[1], xb = args[2];
       if (is_const[s]) {
         const uint32_t x = cval[s] != 0 ? xa : xb;
-        if (w >= wid(x)) { make_alias(x); continue; }
+        if (w >= wid(x)) { if (make_alias(x)) continue; }
       }
-      if (xa == xb && w >= wid(xa)) { make_alias(xa); continue; }
+      if (xa == xb && w >= wid(xa)) { if (make_alias(xa)) continue; }
     }
   }
   // mux chains: a mux whose O=2 (else) branch is produced by another mux
