@@ -171,6 +171,12 @@ typedef struct {
   uint32_t repcut_global;  /* RepCut kernel choice: 0 = auto (shared-memory slices with 8-byte signal
                               slots if they fit, else width-packed slots, else global replicas);
                               1 = global replicas; 2 = width-packed shared-memory slices */
+  uint32_t part_world;     /* RS_MODE_SINGLE level cut ACROSS PROCESSES / GPUs: 0 = off,
+                              else 2..8 partitions, one per process; this allocation runs partition
+                              part_rank only, on its own state replica, and reaches the other partitions'
+                              replicas and cycle flags through peer-mapped device memory (CUDA IPC over
+                              NVLink: rs_ipc_handle / rs_ipc_connect).  Excludes parts and repcut. */
+  uint32_t part_rank;      /* this process's partition, < part_world */
 } rs_lane_opts;
 
 typedef struct rs_graph rs_graph;
@@ -302,6 +308,29 @@ rs_status rs_watch(rs_lanes* s, const uint32_t* ids, uint32_t n_ids, uint64_t ca
  * lost to capacity since the last read (either pointer may be NULL).
  * Synchronises the lanes' stream. */
 rs_status rs_wave_read(rs_lanes* s, rs_change* out, uint64_t cap, uint64_t* n_out, uint64_t* dropped);
+
+/* ---- Level cut across processes / GPUs (rs_lane_opts.part_world > 1; SURVEY.md §8(e) row 2;
+ * PAPER.md App. B P:1961-1963 partition synchronisation, App. C Cascade 2's per-cycle exchange
+ * P:2053-2059).  Every process loads the same graph, allocates its partition with
+ * part_world / part_rank, exports the handle of its replica + cycle flag with rs_ipc_handle
+ * (RS_IPC_HANDLE_BYTES bytes, host memory, caller-owned), gathers all ranks' handles (e.g. a
+ * torch.distributed all_gather; rank order) and passes them to rs_ipc_connect, which maps the
+ * peers' memory (cudaIpcOpenMemHandle; NVLink peer access when the devices differ).  Then
+ * rs_step_cycles on every rank advances the single lane: partition k evaluates its level range,
+ * stores the cut signals and register values other partitions read straight into their
+ * replicas (peer stores) and releases its cycle flag (system scope); partition k + 1 acquires it.
+ * hashes (RS_MEM_HOST / DEVICE, [n_cycles] u64) receive THIS partition's share of each cycle's
+ * hash (its levels' ops, its registers, and for partition 0 the inputs and constants): the
+ * cycle's hash is the sum over ranks mod 2^64.  rs_read_signals reads this rank's replica, which
+ * holds the partition's own signals, the registers and inputs.  Partitions wait on one another
+ * inside the kernel, so they must run on distinct devices to step freely; ranks that share a
+ * device must step one cycle per call, in rank order, with a host barrier between calls (the
+ * flags then never wait).  A hash-off step followed by a hash-on step returns RS_E_UNSUPPORTED
+ * (the per-partition register carry is only kept by hashed steps).  rs_ipc_connect:
+ * RS_E_STATE if not a part_world allocation, RS_E_CUDA if a handle cannot be opened. */
+#define RS_IPC_HANDLE_BYTES 64
+rs_status rs_ipc_handle(rs_lanes* s, void* handle);
+rs_status rs_ipc_connect(rs_lanes* s, const void* handles);
 
 /* Diagnostics (builds with -DRS_TRACE only, else RS_E_UNSUPPORTED): the first
  * call arms a per-stage clock64 trace of CTA 0; later calls copy up to n u64

@@ -126,6 +126,12 @@ struct rs_lanes {
   uint32_t slice_max = 0;
   // level cut: parts partitions x gp CTAs, replica k = tile k of state_mem
   uint32_t parts = 1, gp = 1;
+  // level cut across processes (rs_lane_opts.part_world): this rank's partition, its own
+  // replica (state_mem) with the cycle flag after it, the peers' mapped replicas / flags
+  uint32_t part_world = 0, part_rank = 0;
+  bool connected = false;
+  uint8_t* peer_rep[kMaxParts] = {};
+  unsigned long long* peer_flag[kMaxParts] = {};
   bool tail_global = false;
   std::vector<uint8_t> sig_part;         // canonical id -> partition whose replica holds it
   size_t total_bytes = 0;
@@ -562,6 +568,20 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     rs_free_lanes(s);
     return set_err(RS_E_INVALID_ARG, "repcut_global must be 0, 1 or 2");
   }
+  if (o.part_world == 1) o.part_world = 0;
+  if (o.part_world && (g->cg.mode != RS_MODE_SINGLE || o.part_world > kMaxParts || o.part_rank >= o.part_world ||
+                       o.parts > 1 || o.repcut || (o.kernel && o.kernel != 5) ||
+                       o.part_world > std::max<uint32_t>(1, g->cg.n_levels))) {
+    rs_free_lanes(s);
+    return set_err(RS_E_INVALID_ARG, "part_world = %u / part_rank = %u: a single-lane level cut of 2..%u partitions "
+                   "(<= n_levels), without parts / repcut", o.part_world, o.part_rank, kMaxParts);
+  }
+  if (o.part_world) {
+    o.parts = o.part_world;
+    o.kernel = 5;
+    s->part_world = o.part_world;
+    s->part_rank = o.part_rank;
+  }
   if (g->cg.mode == RS_MODE_SINGLE && o.kernel == 5 && o.repcut) {
     rs_free_lanes(s);
     return set_err(RS_E_INVALID_ARG, "kernel 5 (level-synchronous) excludes repcut");
@@ -597,7 +617,8 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
       rs_free_lanes(s);  // partially built: frees what exists
       return set_err(RS_E_INVALID_ARG, "parts = %u: must be <= %u and <= n_levels (%u)", p, kMaxParts, g->cg.n_levels);
     }
-    s->n_tiles = s->parts;  // one state replica per partition (lane index = replica in the aux kernels)
+    s->n_tiles = s->part_world ? 1u : s->parts;  // one state replica per partition (lane index = replica in the
+                                                 // aux kernels); across processes: this rank's replica only
   } else {
     if (o.parts > 1) {
       rs_free_lanes(s);  // partially built: frees what exists
@@ -759,7 +780,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     const CompiledGraph& cg = g->cg;
     const uint64_t est = 4ull * cg.n_ops_total() + 4ull * cg.coord.size() + 12ull * cg.n_regs + 8ull * cg.n_inputs;
     const uint32_t kMaxSlice = 212 * 1024;  // + static shared memory stays below the 227 KB per-CTA limit
-    const uint32_t P = s->parts, maxG = (uint32_t)g->sm_count / P;
+    const uint32_t P = s->parts, maxG = (uint32_t)g->sm_count / (s->part_world ? 1u : P);
     uint32_t G = (uint32_t)std::max<uint64_t>({1, (est + kMaxSlice / 2) / (kMaxSlice * 3 / 4) / P, (maxops + 1023) / 1024});
     G = std::min<uint32_t>(G, maxG);
     std::vector<uint8_t> sblob;
@@ -808,7 +829,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
       s->slice_blob = (const uint8_t*)s->dslices;
       s->slice_off = (const uint64_t*)((const uint8_t*)s->dslices + off_off);
       s->slice_max = smax;
-      s->ctas = G;
+      s->ctas = s->part_world ? s->gp : G;  // across processes: this rank's partition only
       s->total_bytes += off_off + G * 8;
     } else {  // graph too large for resident slices: descriptors streamed from global memory
       const uint32_t need = std::max(work, maxops);
@@ -852,7 +873,9 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
   }
   s->state_bytes = (size_t)s->tile_bytes * s->n_tiles;
   cudaError_t e;
-  if ((e = cudaMalloc(&s->state_mem, s->state_bytes)) != cudaSuccess) {
+  // across processes the cycle flag follows the replica in the same allocation (one IPC handle)
+  const size_t flag_bytes = s->part_world ? 256 : 0;
+  if ((e = cudaMalloc(&s->state_mem, s->state_bytes + flag_bytes)) != cudaSuccess) {
     rs_free_lanes(s);  // partially built: frees what exists
     return set_err(RS_E_OOM, "cudaMalloc state (%zu B): %s", s->state_bytes, cudaGetErrorString(e));
   }
@@ -900,7 +923,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
   }
   // init: zero, constants, register init, hash carry
   StepArgs a = base_args(s);
-  e = cudaMemsetAsync(s->state_mem, 0, s->state_bytes, s->stream);
+  e = cudaMemsetAsync(s->state_mem, 0, s->state_bytes + flag_bytes, s->stream);
   std::vector<uint32_t> coords;
   std::vector<uint64_t> vals;
   coords.insert(coords.end(), g->cg.const_coord.begin(), g->cg.const_coord.end());
@@ -923,7 +946,8 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     }
   }
   if (e == cudaSuccess) {
-    std::vector<uint64_t> hc(lanes_pad, g->cg.init_reg_hash);
+    // across processes each partition carries its own registers' term: all of it on rank 0 at first
+    std::vector<uint64_t> hc(lanes_pad, (s->part_world && s->part_rank != 0) ? 0ull : g->cg.init_reg_hash);
     e = cudaMemcpy(s->hcarry, hc.data(), lanes_pad * 8, cudaMemcpyHostToDevice);
   }
   if (e != cudaSuccess) {
@@ -937,6 +961,9 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
 }
 
 void rs_free_lanes(rs_lanes* s) {
+  if (s && s->connected)
+    for (uint32_t k = 0; k < s->part_world; ++k)
+      if (k != s->part_rank && s->peer_rep[k]) cudaIpcCloseMemHandle(s->peer_rep[k]);
   if (!s) return;
   cudaSetDevice(s->g->device);
   if (s->stream) cudaStreamSynchronize(s->stream);
@@ -1052,6 +1079,8 @@ rs_status rs_set_inputs(rs_lanes* s, uint64_t first_cycle, uint32_t n_cycles, co
 
 static rs_status refresh_hcarry(rs_lanes* s) {
   if (s->hc_valid) return RS_OK;
+  if (s->part_world)
+    return set_err(RS_E_UNSUPPORTED, "level cut across processes: a hashed step after a hash-off step");
   StepArgs a = base_args(s);
   k_reg_hash<<<std::max<uint32_t>(1, (s->n_lanes + 127) / 128), 128, 0, s->stream>>>(
       a, s->n_lanes, s->hcarry + s->hc_cur * (size_t)s->n_tiles * s->LT);
@@ -1127,7 +1156,9 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
       CU(cudaMemsetAsync(a.hcarry_out, 0, 8, s->stream));
       if (hout) CU(cudaMemsetAsync(hout, 0, hn * 8, s->stream));
     }
-    CU(cudaMemsetAsync(s->bar, 0, kBarBytes, s->stream));
+    // grid-barrier counters only: level-cut cycle flags hold absolute cycles and persist
+    CU(cudaMemsetAsync(s->bar, 0, kFlagOffset * 8, s->stream));
+    if (s->part_world && !s->connected) return set_err(RS_E_STATE, "level cut across processes: rs_ipc_connect first");
     cudaError_t e;
     if (s->repcut && s->rep_smem) {
       RepSmemArgs ra = s->reps;
@@ -1160,8 +1191,19 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
       sa.parts = s->parts;
       sa.tail_global = s->tail_global ? 1u : 0u;
       sa.gp = s->gp;
-      sa.flags = s->bar + kFlagOffset;
-      for (uint32_t k = 0; k < s->parts; ++k) sa.rep[k] = (uint8_t*)s->state_mem + (size_t)k * s->tile_bytes;
+      if (s->part_world) {  // this rank's partition; the others through peer-mapped memory
+        sa.part_base = s->part_rank * s->gp;
+        sa.sys = 1;
+        for (uint32_t k = 0; k < s->parts; ++k) {
+          sa.rep[k] = s->peer_rep[k];
+          sa.flag[k] = s->peer_flag[k];
+        }
+      } else {
+        for (uint32_t k = 0; k < s->parts; ++k) {
+          sa.rep[k] = (uint8_t*)s->state_mem + (size_t)k * s->tile_bytes;
+          sa.flag[k] = s->bar + kFlagOffset + k;
+        }
+      }
       void* args[] = {&sa};
       const void* fn = grid ? (hash ? (const void*)k_single2<true, true> : (const void*)k_single2<true, false>)
                             : (hash ? (const void*)k_single2<false, true> : (const void*)k_single2<false, false>);
@@ -1330,7 +1372,55 @@ rs_status rs_get_cycle(const rs_lanes* s, uint64_t* cycle) {
 
 rs_status rs_set_cycle(rs_lanes* s, uint64_t cycle) {
   if (!s) return set_err(RS_E_INVALID_ARG, "NULL lanes");
+  if (s->parts > 1 && cycle != s->cycle) {  // level-cut flags hold absolute cycles: restart them
+    rs_status st = set_device(s->g);
+    if (st != RS_OK) return st;
+    CU(cudaMemsetAsync(s->bar + kFlagOffset, 0, kBarBytes - kFlagOffset * 8, s->stream));
+    if (s->part_world) CU(cudaMemsetAsync((uint8_t*)s->state_mem + s->state_bytes, 0, 8, s->stream));
+    CU(cudaStreamSynchronize(s->stream));
+  }
   s->cycle = cycle;
+  return RS_OK;
+}
+
+rs_status rs_ipc_handle(rs_lanes* s, void* handle) {
+  if (!s || !handle) return set_err(RS_E_INVALID_ARG, "NULL argument");
+  if (!s->part_world) return set_err(RS_E_STATE, "not a level-cut-across-processes allocation (part_world)");
+  static_assert(sizeof(cudaIpcMemHandle_t) <= RS_IPC_HANDLE_BYTES, "IPC handle size");
+  rs_status st = set_device(s->g);
+  if (st != RS_OK) return st;
+  cudaIpcMemHandle_t h;
+  CU(cudaIpcGetMemHandle(&h, s->state_mem));
+  std::memset(handle, 0, RS_IPC_HANDLE_BYTES);
+  std::memcpy(handle, &h, sizeof h);
+  return RS_OK;
+}
+
+rs_status rs_ipc_connect(rs_lanes* s, const void* handles) {
+  if (!s || !handles) return set_err(RS_E_INVALID_ARG, "NULL argument");
+  if (!s->part_world) return set_err(RS_E_STATE, "not a level-cut-across-processes allocation (part_world)");
+  if (s->connected) return set_err(RS_E_STATE, "already connected");
+  rs_status st = set_device(s->g);
+  if (st != RS_OK) return st;
+  for (uint32_t k = 0; k < s->part_world; ++k) {
+    if (k == s->part_rank) {
+      s->peer_rep[k] = (uint8_t*)s->state_mem;
+    } else {
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, (const uint8_t*)handles + (size_t)k * RS_IPC_HANDLE_BYTES, sizeof h);
+      void* p = nullptr;
+      cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        for (uint32_t m = 0; m < k; ++m)
+          if (m != s->part_rank && s->peer_rep[m]) cudaIpcCloseMemHandle(s->peer_rep[m]);
+        return set_err(RS_E_CUDA, "cudaIpcOpenMemHandle(rank %u): %s", k, cudaGetErrorString(e));
+      }
+      s->peer_rep[k] = (uint8_t*)p;
+    }
+    // every replica has the same layout: the flag follows tile_bytes of state
+    s->peer_flag[k] = reinterpret_cast<unsigned long long*>(s->peer_rep[k] + s->state_bytes);
+  }
+  s->connected = true;
   return RS_OK;
 }
 

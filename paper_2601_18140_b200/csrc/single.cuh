@@ -20,14 +20,29 @@ struct SingleArgs {
   const uint64_t* slice_off;
   uint32_t slice_max;    // bytes of the largest slice (128-aligned; dynamic shared memory)
   uint32_t state_smem;   // single-CTA launches: bytes of signal state kept in shared memory (0 = off)
-  // level cut (compiler.hpp SliceHdr): CTAs [k*gp, (k+1)*gp)
-  // run partition k on replica rep[k]; partition k publishes "cycle c done"
-  // as flags[k] = c + 1 (launch-relative).  parts == 1: plain single-lane.
+  // level cut (compiler.hpp SliceHdr): slices [k*gp, (k+1)*gp)
+  // run partition k on replica rep[k]; partition k publishes "absolute cycle c
+  // done" as *flag[k] = c + 1.  On one device every partition is a CTA group of
+  // one cooperative launch (part_base = 0); across devices (rs_ipc_connect) each
+  // process launches its own partition's gp CTAs (part_base = rank * gp), rep[m]
+  // and flag[m] of the other partitions are peer-mapped device memory, and the
+  // flags and fences are system scope (sys = 1).  parts == 1: plain single-lane.
   uint32_t parts, gp;
   uint32_t tail_global;  // slice tails (push / latch / inject lists) read from global memory
-  unsigned long long* flags;
+  uint32_t part_base;    // slice index of this launch's CTA 0
+  uint32_t sys;          // partitions on other devices: .sys-scope flags and fences
+  unsigned long long* flag[kMaxParts];
   uint8_t* rep[kMaxParts];
 };
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 
 __device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v) {
   asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -161,7 +176,7 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
   __shared__ uint64_t wsum[32];
   const uint32_t tid = threadIdx.x, T = blockDim.x;
   {  // this CTA's slice of the graph, resident for the whole launch
-    const uint8_t* src = sa.slice_blob + sa.slice_off[blockIdx.x];
+    const uint8_t* src = sa.slice_blob + sa.slice_off[sa.part_base + blockIdx.x];
     const SliceHdr* sh = reinterpret_cast<const SliceHdr*>(src);
     const uint32_t bytes = sa.tail_global ? sh->head_bytes : sh->bytes;
     for (uint32_t i = tid * 16; i < bytes; i += T * 16)
@@ -174,12 +189,13 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
   const SliceSeg* seg = reinterpret_cast<const SliceSeg*>(smem + h->off_seg);
   const uint32_t* pws = reinterpret_cast<const uint32_t*>(smem + h->off_pw);
   const uint32_t* crd = reinterpret_cast<const uint32_t*>(smem + h->off_coord);
-  const uint8_t* tail = sa.tail_global ? sa.slice_blob + sa.slice_off[blockIdx.x] : smem;
+  const uint8_t* tail = sa.tail_global ? sa.slice_blob + sa.slice_off[sa.part_base + blockIdx.x] : smem;
   const uint32_t* lat = reinterpret_cast<const uint32_t*>(tail + h->off_latch);
   const uint32_t* inj = reinterpret_cast<const uint32_t*>(tail + h->off_inj);
   const uint32_t* psh = reinterpret_cast<const uint32_t*>(tail + h->off_push);
   const uint32_t part = h->part, P = sa.parts;
-  const bool lead = blockIdx.x == 0;               // adds the launch-wide hash terms
+  const bool lead = blockIdx.x == 0;               // adds this launch's carry (its registers' hash term)
+  const bool lead0 = lead && sa.part_base == 0;    // ... and the constants' term, once over all partitions
   unsigned long long* bar = a.bar + 4 * part;      // partition-local grid barrier
 
   // single CTA with a small state: the whole signal state lives in shared memory
@@ -207,7 +223,7 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
     }
   };
   unsigned long long target = 0;
-  uint64_t hacc = (HASH && lead && tid == 0) ? a.hcarry_in[0] + a.g.const_hash : 0ull;
+  uint64_t hacc = (HASH && lead && tid == 0) ? a.hcarry_in[0] + (lead0 ? a.g.const_hash : 0ull) : 0ull;
 
   // inputs are injected into every replica; partition 0 hashes them
   const bool hin_on = HASH && part == 0;
@@ -251,9 +267,14 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
   for (uint32_t cyc = 0; cyc < a.n_cycles; ++cyc) {
     if (P > 1) {  // token ring: partition k runs cycle c after k-1 finished it; 0 after P-1 finished c-1
       if (tid == 0) {
-        const unsigned long long* f = sa.flags + (part == 0 ? P - 1 : part - 1);
-        const unsigned long long want = part == 0 ? cyc : cyc + 1;
-        while (ld_acquire(f) < want) {
+        const unsigned long long* f = sa.flag[part == 0 ? P - 1 : part - 1];
+        const unsigned long long want = part == 0 ? a.cycle0 + cyc : a.cycle0 + cyc + 1;
+        if (sa.sys) {
+          while (ld_acquire_sys(f) < want) {
+          }
+        } else {
+          while (ld_acquire(f) < want) {
+          }
         }
       }
       __syncthreads();
@@ -312,13 +333,17 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
     if (cyc + 1 < a.n_cycles) hin = inject(a.cycle0 + cyc + 1);
     if (HASH) {
       warp_partial(hacc, wsum);
-      hacc = hr + hin + ((lead && tid == 0) ? a.g.const_hash : 0ull);
+      hacc = hr + hin + ((lead0 && tid == 0) ? a.g.const_hash : 0ull);
     }
 #ifdef RS_TRACE
     if (blockIdx.x == 0 && tid == 0 && a.trace && cyc < 8) a.trace[cyc * 64 + 60] = clock64();
 #endif
+    if (sa.sys) __threadfence_system();  // this CTA's peer stores, visible system-wide before the flag
     single_barrier<GRID>(bar, target, sa.gp, wsum, (HASH && a.hashes) ? (unsigned long long*)(a.hashes + cyc) : nullptr);
-    if (P > 1 && tid == 0 && blockIdx.x == part * sa.gp) st_release(sa.flags + part, cyc + 1);
+    if (P > 1 && tid == 0 && blockIdx.x + sa.part_base == part * sa.gp) {
+      if (sa.sys) st_release_sys(sa.flag[part], a.cycle0 + cyc + 1);
+      else st_release(sa.flag[part], a.cycle0 + cyc + 1);
+    }
 #ifdef RS_TRACE
     if (blockIdx.x == 0 && tid == 0 && a.trace && cyc < 8) a.trace[cyc * 64 + 61] = clock64();
 #endif

@@ -27,7 +27,7 @@ EXPORTS = ["rs_version", "rs_last_error", "rs_load_graph", "rs_graph_info_get", 
            "rs_alloc_lanes", "rs_free_lanes", "rs_lanes_bytes", "rs_set_input_seed", "rs_set_inputs",
            "rs_step_cycles", "rs_read_signals", "rs_write_registers", "rs_get_cycle", "rs_set_cycle",
            "rs_launch_count", "rs_launch_shape", "rs_lanes_kernel", "rs_repcut_stats", "rs_watch", "rs_wave_read", "rs_sync", "rs_graph_export", "rs_debug_trace",
-           "rs_level_cut"]
+           "rs_level_cut", "rs_ipc_handle", "rs_ipc_connect"]
 RS_DEVICE_NONE = -1
 EXPORT = {"runs": (0, np.uint32), "level_run_begin": (1, np.uint32), "level_op_begin": (2, np.uint32),
           "opw": (3, np.uint32), "opk": (4, np.uint64), "coord_off": (5, np.uint32), "coord": (6, np.uint32),
@@ -68,7 +68,8 @@ class LaneOpts(C.Structure):
     _fields_ = [("lane0", C.c_uint64), ("lane_tile", C.c_uint32), ("threads", C.c_uint32),
                 ("stage_cycles", C.c_uint32), ("cluster", C.c_uint32), ("stream", C.c_void_p),
                 ("parts", C.c_uint32), ("kernel", C.c_uint32),
-                ("repcut", C.c_uint32), ("repcut_global", C.c_uint32)]
+                ("repcut", C.c_uint32), ("repcut_global", C.c_uint32),
+                ("part_world", C.c_uint32), ("part_rank", C.c_uint32)]
 
 
 _lib = None
@@ -110,6 +111,8 @@ def lib() -> C.CDLL:
             "rs_graph_export": (i32, [vp, u32, vp, C.POINTER(u64)]),
             "rs_debug_trace": (i32, [vp, vp, u64]),
             "rs_level_cut": (i32, [vp, u32, vp]),
+            "rs_ipc_handle": (i32, [vp, vp]),
+            "rs_ipc_connect": (i32, [vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -218,12 +221,13 @@ class Lanes:
 
     def __init__(self, graph: Graph, n_lanes: int, lane0: int = 0, lane_tile: int = 0, threads: int = 0,
                  stage_cycles: int = 0, stream=None, cluster: int = 0, parts: int = 0, kernel: int = 0,
-                 repcut: int = 0, repcut_global: int = 0):
+                 repcut: int = 0, repcut_global: int = 0, part_world: int = 0, part_rank: int = 0):
         self.graph = graph
         self.n_lanes = n_lanes
         self.lane0 = lane0
         st = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
-        self.opts = LaneOpts(lane0, lane_tile, threads, stage_cycles, cluster, st, parts, kernel, repcut, int(repcut_global))
+        self.opts = LaneOpts(lane0, lane_tile, threads, stage_cycles, cluster, st, parts, kernel, repcut,
+                             int(repcut_global), part_world, part_rank)
         h = C.c_void_p()
         _check(lib().rs_alloc_lanes(graph.h, n_lanes, C.byref(self.opts), C.byref(h)))
         self.h = h
@@ -314,6 +318,20 @@ class Lanes:
         n, d = C.c_uint64(), C.c_uint64()
         _check(lib().rs_wave_read(self.h, _ptr(out), cap, C.byref(n), C.byref(d)))
         return out[:n.value], d.value
+
+    # ---- level cut across processes (rs_ipc_handle / rs_ipc_connect)
+    IPC_HANDLE_BYTES = 64
+
+    def ipc_handle(self) -> bytes:
+        buf = C.create_string_buffer(self.IPC_HANDLE_BYTES)
+        _check(lib().rs_ipc_handle(self.h, buf))
+        return buf.raw
+
+    def ipc_connect(self, handles: Sequence[bytes]) -> None:
+        """handles: every rank's rs_ipc_handle bytes, in rank order."""
+        blob = b"".join(bytes(h) for h in handles)
+        buf = C.create_string_buffer(blob, len(blob))
+        _check(lib().rs_ipc_connect(self.h, buf))
 
     def nbytes(self) -> int:
         return int(lib().rs_lanes_bytes(self.h))

@@ -1,4 +1,5 @@
-"""Lane sharding with the product library in several processes.
+"""Lane sharding and the cross-process level cut with the product library in several
+processes.
 
 Two ranks (gloo process group, sharing this lease's one GPU -- their kernels
 never wait on each other: lanes are independent) each simulate their global
@@ -91,3 +92,70 @@ def test_bench_spawns_ranks():
     assert d["n_gpus"] == 2 and d["scaling"] == "strong"
     assert d["config"]["lanes_total"] == 256 and d["config"]["lanes_per_gpu"] == 128
     assert d["value"] > 0 and d["gpu_launches"] >= 2
+
+
+def _levelcut_worker(rank, world, port, q, name, n_cycles):
+    """One partition of a level cut across processes (rs_lane_opts.part_world) on this
+    lease's one GPU: the ranks share the device, so they step one cycle per call in rank
+    order with a host barrier between calls (their kernels never wait on each other)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2601_18140_b200 import rtlsim as rs
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        c = _lc_circ(name)
+        g = rs.Graph(c, device=0, mode="single")
+        L = rs.Lanes(g, 1, part_world=world, part_rank=rank)
+        L.set_seed(31)
+        hs = [None] * world
+        dist.all_gather_object(hs, L.ipc_handle())
+        L.ipc_connect(hs)
+        dist.barrier()
+        part = np.zeros(n_cycles, dtype=np.uint64)
+        for cyc in range(n_cycles):
+            for r in range(world):
+                if r == rank:
+                    part[cyc] = L.step(1, hashes="host")[0, 0]
+                    L.sync()
+                dist.barrier()
+        regs = L.read(c.reg_id)[:, 0]
+        q.put((rank, part, regs, L.launches))
+        dist.barrier()       # peers keep their memory mapped until everyone is done
+    finally:
+        dist.destroy_process_group()
+
+
+def _lc_circ(name):
+    from synth import config_circuit
+    return config_circuit("C1") if name == "C1" else config_circuit("C5", n_ops=20_000, n_levels=30, n_regs=2_000)
+
+
+@pytest.mark.parametrize("name,world", [("C1", 2), ("C5s", 3)])
+def test_level_cut_across_processes(rs, name, world):
+    """SURVEY.md §8(e) row 2 transport: partitions in separate processes reach each other's
+    replicas and cycle flags through CUDA IPC mappings; the per-cycle hash is the sum of the
+    partitions' shares and equals the oracle's, cycle by cycle."""
+    import oracle
+    port, n = _free_port(), 25
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_levelcut_worker, args=(r, world, port, q, name, n)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=900) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    H = np.zeros(n, dtype=np.uint64)
+    for _, part, _, launches in out:
+        H += part                                    # mod 2^64
+        assert launches >= n
+    c = _lc_circ(name)
+    r = oracle.simulate(c, n, seed=31, final=True)
+    assert np.array_equal(H, r.hashes[:, 0])
+    # registers: each rank's replica holds every register's committed value
+    for _, _, regs, _ in out:
+        assert np.array_equal(regs, r.final_state[np.asarray(c.reg_id, dtype=np.int64), 0])
