@@ -269,8 +269,8 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
       if (tid == 0) {
         const unsigned long long* f = sa.flag[part == 0 ? P - 1 : part - 1];
         const unsigned long long want = part == 0 ? a.cycle0 + cyc : a.cycle0 + cyc + 1;
-        if (sa.sys) {
-          while (ld_acquire_sys(f) < want) {
+        if (sa.sys) {  // bounded: a peer that never arrives must not hang the device (results then differ)
+          for (uint32_t spin = 0; ld_acquire_sys(f) < want && spin < (1u << 26); ++spin) {
           }
         } else {
           while (ld_acquire(f) < want) {
