@@ -1372,12 +1372,17 @@ rs_status rs_get_cycle(const rs_lanes* s, uint64_t* cycle) {
 
 rs_status rs_set_cycle(rs_lanes* s, uint64_t cycle) {
   if (!s) return set_err(RS_E_INVALID_ARG, "NULL lanes");
-  if (s->parts > 1 && cycle != s->cycle) {  // level-cut flags hold absolute cycles: restart them
+  if (s->parts > 1 && cycle != s->cycle) {
+    // level-cut flags hold absolute cycles ("partition k finished cycle c - 1" = c):
+    // restart them as if every partition had just finished cycle - 1
     rs_status st = set_device(s->g);
     if (st != RS_OK) return st;
-    CU(cudaMemsetAsync(s->bar + kFlagOffset, 0, kBarBytes - kFlagOffset * 8, s->stream));
-    if (s->part_world) CU(cudaMemsetAsync((uint8_t*)s->state_mem + s->state_bytes, 0, 8, s->stream));
+    const std::vector<unsigned long long> f(kMaxParts, (unsigned long long)cycle);
     CU(cudaStreamSynchronize(s->stream));
+    if (s->part_world)
+      CU(cudaMemcpy((uint8_t*)s->state_mem + s->state_bytes, f.data(), 8, cudaMemcpyHostToDevice));
+    else
+      CU(cudaMemcpy(s->bar + kFlagOffset, f.data(), 8 * kMaxParts, cudaMemcpyHostToDevice));
   }
   s->cycle = cycle;
   return RS_OK;

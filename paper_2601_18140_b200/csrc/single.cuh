@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
           for (uint32_t spin = 0; ld_acquire_sys(f) < want && spin < (1u << 26); ++spin) {
           }
         } else {
-          while (ld_acquire(f) < want) {
+          for (uint32_t spin = 0; ld_acquire(f) < want && spin < (1u << 26); ++spin) {
           }
         }
       }
