@@ -141,10 +141,12 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def workload(cfg_name, total_lanes, lanes_rank, cycles, n_ops, n_levels, n_gpus, scaling):
+def workload(cfg_name, total_lanes, lanes_rank, cycles, n_ops, n_levels, n_gpus, scaling, levelcut=False):
     if cfg_name in SINGLE:
+        how = (f", level cut across {n_gpus} GPUs" if levelcut else f", {n_gpus} independent replicas") \
+            if n_gpus > 1 else ""
         return (f"{cfg_name}: {n_ops} ops / {n_levels} levels, 1 lane x {cycles} cycles per step"
-                + (f", {n_gpus} independent replicas" if n_gpus > 1 else "") + ", synthetic seeded circuit + stimulus")
+                + how + ", synthetic seeded circuit + stimulus")
     return (f"{cfg_name}: {n_ops} ops / {n_levels} levels, {total_lanes} lanes x {cycles} cycles per step, "
             f"{n_gpus} GPU(s) ({lanes_rank} lanes per GPU, {scaling} scaling), synthetic seeded circuit + stimulus")
 
@@ -281,6 +283,8 @@ def main():
     ap.add_argument("--repcut", type=int, default=0, help="single-lane configs: RepCut partitions (rs_lane_opts.repcut)")
     ap.add_argument("--ref-step-s", type=float, default=4.0)
     ap.add_argument("--watch", type=int, default=0, help="waveform capture of N signals during the timed steps")
+    ap.add_argument("--replicas", action="store_true",
+                    help="C1/C5 at N > 1: independent replicas instead of the level cut across GPUs")
     args = ap.parse_args()
 
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -316,13 +320,24 @@ def main():
         shard = D.shard_weak(rank, world, args.lanes or cfg.lanes)
         total_lanes = shard.n_lanes * world
     lanes = shard.n_lanes
+    # C1 / C5 at N > 1: the level cut across the ranks' GPUs, one
+    # partition per rank, peer-mapped replicas and flags (rs_ipc_connect); ranks sharing a
+    # device would wait on one another, so that case falls back to independent replicas
+    levelcut = single and world > 1 and args.config in ("C1", "C5") and not args.replicas and ndev >= world
     stream = torch.cuda.Stream()
     g = rs.Graph(circ, device=dev, mode="single" if single else "lanes", passes=not args.no_passes)
     info = g.info()
     info0 = rs.Graph(circ, device=rs.RS_DEVICE_NONE, mode="single" if single else "lanes").info()
     mk = dict(lane0=shard.lane0, lane_tile=args.lane_tile, threads=args.threads, stream=stream,
               cluster=args.cluster, parts=args.parts, kernel=args.kernel, repcut=args.repcut)
-    L = rs.Lanes(g, lanes, **mk)
+    if levelcut:
+        L = rs.Lanes(g, 1, stream=stream, part_world=world, part_rank=rank)
+        hs = [None] * world
+        dist.all_gather_object(hs, L.ipc_handle())
+        L.ipc_connect(hs)
+        dist.barrier()
+    else:
+        L = rs.Lanes(g, lanes, **mk)
     L.set_seed(cfg.stim_seed)
     if args.watch:
         wids = np.linspace(0, circ.n_signals - 1, args.watch).astype(np.uint32)
@@ -348,7 +363,8 @@ def main():
             hash_off = off_ms
     total_ms = D.max_over_ranks(float(sum(step_ms)), dist)
     med_ms = D.max_over_ranks(float(np.median(step_ms)), dist)
-    all_lane_cycles = (total_lanes * world if single else total_lanes) * cycles * args.steps
+    n_replicas = world if (single and not levelcut) else 1
+    all_lane_cycles = (total_lanes * n_replicas if single else total_lanes) * cycles * args.steps
     value = all_lane_cycles / (total_ms / 1e3)
 
     kid = L.shape()["kernel"]
@@ -371,7 +387,7 @@ def main():
     # end to end through the public API with host buffers: staged inputs H2D from
     # pinned memory and hashes D2H, every chunk, inside the timed region.
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not levelcut:
         chunk = min(cycles, max(1, (256 << 20) // max(1, 8 * circ.n_inputs * lanes)))
         Ls = rs.Lanes(g, lanes, stage_cycles=2 * chunk, **mk)
         rng = np.random.default_rng(rank)
@@ -406,7 +422,7 @@ def main():
         el = time.perf_counter() - t0
         barrier()
         el = D.max_over_ranks(el, dist)
-        e2e = {"value": (total_lanes * world if single else total_lanes) * cycles * e2e_steps / el, "unit": UNIT,
+        e2e = {"value": (total_lanes * n_replicas if single else total_lanes) * cycles * e2e_steps / el, "unit": UNIT,
                "h2d_bytes_per_step": int(cycles * circ.n_inputs * lanes * 8),
                "d2h_bytes_per_step": int(cycles * lanes * 8), "steps": e2e_steps,
                "path": "rs_set_inputs(host pinned, next chunk, copy stream) + rs_step_cycles(hashes=HOST) "
@@ -422,14 +438,15 @@ def main():
                "sample": f"{nl} lanes x {nc} cycles of {args.config} ({dt:.2f} s)"}
 
     if rank == 0:
-        scaling = "weak" if (single or args.scaling == "weak") else "strong"
+        scaling = "strong" if levelcut else "weak" if (single or args.scaling == "weak") else "strong"
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "ms_per_step_median": med_ms,
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u64",
             "data": "synthetic",
             "config": {"workload": workload(args.config, total_lanes, lanes, cycles, circ.n_ops, info["n_levels"],
-                                            world, scaling),
+                                            world, scaling, levelcut),
+                       **({"level_cut_across_gpus": world} if levelcut else {}),
                        "lanes_total": total_lanes, "lanes_per_gpu": lanes, "cycles_per_step": cycles,
                        "hash": not args.no_hash,
                        "l2": "flushed (256 MB write) before every timed step",
@@ -456,7 +473,7 @@ def main():
         }
         if hash_off:
             off_med = float(np.median(hash_off))
-            line["hash_off"] = {"value": (total_lanes * world if single else total_lanes) * cycles / (off_med / 1e3),
+            line["hash_off"] = {"value": (total_lanes * n_replicas if single else total_lanes) * cycles / (off_med / 1e3),
                                 "ms_per_step_median": off_med, "steps": len(hash_off),
                                 "roofline_frac": alg_bytes / (off_med / 1e3) / 1e9 / peak}
         if e2e:
