@@ -177,6 +177,12 @@ typedef struct {
                               replicas and cycle flags through peer-mapped device memory (CUDA IPC over
                               NVLink: rs_ipc_handle / rs_ipc_connect).  Excludes parts and repcut. */
   uint32_t part_rank;      /* this process's partition, < part_world */
+  uint32_t l2_policy;      /* RS_MODE_LANES L2-residency policy (north star: "an L2-residency policy for
+                              state"), applied per launch as a CUDA access-policy window: 0 = none;
+                              1 = the stage schedule (graph tensor, re-read by every CTA every cycle)
+                              persisting; 2 = the signal state persisting (hit ratio = the device's
+                              persisting-L2 limit / state bytes, the rest streaming).  Results are
+                              identical; only speed differs (measured in DESIGN.md §8). */
 } rs_lane_opts;
 
 typedef struct rs_graph rs_graph;

@@ -130,6 +130,8 @@ struct rs_lanes {
   // replica (state_mem) with the cycle flag after it, the peers' mapped replicas / flags
   uint32_t part_world = 0, part_rank = 0;
   bool connected = false;
+  uint32_t l2_policy = 0;           // rs_lane_opts.l2_policy
+  size_t l2_persist_max = 0;        // cudaDevAttrMaxPersistingL2CacheSize
   uint8_t* peer_rep[kMaxParts] = {};
   unsigned long long* peer_flag[kMaxParts] = {};
   bool tail_global = false;
@@ -567,6 +569,21 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
   if (o.repcut_global > 2) {
     rs_free_lanes(s);
     return set_err(RS_E_INVALID_ARG, "repcut_global must be 0, 1 or 2");
+  }
+  if (o.l2_policy > 2) {
+    rs_free_lanes(s);
+    return set_err(RS_E_INVALID_ARG, "l2_policy must be 0, 1 or 2");
+  }
+  s->l2_policy = g->cg.mode == RS_MODE_LANES ? o.l2_policy : 0u;
+  if (s->l2_policy) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, g->device);
+    s->l2_persist_max = (size_t)std::max(0, v);
+    // the persisting carve-out is a device-wide limit: raise it to the maximum once
+    size_t cur = 0;
+    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+    if (cur < s->l2_persist_max) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, s->l2_persist_max);
+    (void)cudaGetLastError();
   }
   if (o.part_world == 1) o.part_world = 0;
   if (o.part_world && (g->cg.mode != RS_MODE_SINGLE || o.part_world > kMaxParts || o.part_rank >= o.part_world ||
@@ -1245,13 +1262,24 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
     cfg.blockDim = dim3(s->threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s->stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = s->cluster;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (s->l2_policy && s->l2_persist_max) {  // L2-residency policy: one access-policy window per launch
+      cudaAccessPolicyWindow& w = attr[1].val.accessPolicyWindow;
+      attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
+      const size_t bytes = s->l2_policy == 1 ? s->sched_bytes : s->state_bytes;
+      w.base_ptr = s->l2_policy == 1 ? s->dstages : s->state_mem;
+      w.num_bytes = std::min(bytes, s->l2_persist_max);
+      w.hitRatio = s->l2_policy == 1 ? 1.0f : (float)std::min(1.0, (double)s->l2_persist_max / (double)std::max<size_t>(1, bytes));
+      w.hitProp = cudaAccessPropertyPersisting;
+      w.missProp = cudaAccessPropertyStreaming;
+      cfg.numAttrs = 2;
+    }
     void* args[] = {&a};
     cudaError_t e = cudaLaunchKernelExC(&cfg, fns[fi], args);
     if (e != cudaSuccess) return set_err(RS_E_CUDA, "k_lanes launch: %s", cudaGetErrorString(e));

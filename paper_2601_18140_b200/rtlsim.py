@@ -69,7 +69,7 @@ class LaneOpts(C.Structure):
                 ("stage_cycles", C.c_uint32), ("cluster", C.c_uint32), ("stream", C.c_void_p),
                 ("parts", C.c_uint32), ("kernel", C.c_uint32),
                 ("repcut", C.c_uint32), ("repcut_global", C.c_uint32),
-                ("part_world", C.c_uint32), ("part_rank", C.c_uint32)]
+                ("part_world", C.c_uint32), ("part_rank", C.c_uint32), ("l2_policy", C.c_uint32)]
 
 
 _lib = None
@@ -221,13 +221,14 @@ class Lanes:
 
     def __init__(self, graph: Graph, n_lanes: int, lane0: int = 0, lane_tile: int = 0, threads: int = 0,
                  stage_cycles: int = 0, stream=None, cluster: int = 0, parts: int = 0, kernel: int = 0,
-                 repcut: int = 0, repcut_global: int = 0, part_world: int = 0, part_rank: int = 0):
+                 repcut: int = 0, repcut_global: int = 0, part_world: int = 0, part_rank: int = 0,
+                 l2_policy: int = 0):
         self.graph = graph
         self.n_lanes = n_lanes
         self.lane0 = lane0
         st = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
         self.opts = LaneOpts(lane0, lane_tile, threads, stage_cycles, cluster, st, parts, kernel, repcut,
-                             int(repcut_global), part_world, part_rank)
+                             int(repcut_global), part_world, part_rank, l2_policy)
         h = C.c_void_p()
         _check(lib().rs_alloc_lanes(graph.h, n_lanes, C.byref(self.opts), C.byref(h)))
         self.h = h
