@@ -18,11 +18,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 def run_gpu(rs, c, n_cycles, n_lanes=1, seed=0, mode="lanes", lane0=0, lane_tile=0, threads=0,
             staged=None, chunks=None, final=True, cluster=0, parts=0, kernel=0, repcut=0,
-            repcut_global=False):
+            repcut_global=False, l2_policy=0):
     g = rs.Graph(c, device=0, mode=mode)
     L = rs.Lanes(g, n_lanes, lane0=lane0, lane_tile=lane_tile, threads=threads, cluster=cluster,
                  stage_cycles=(n_cycles if staged is not None else 0), parts=parts, kernel=kernel,
-                 repcut=repcut, repcut_global=repcut_global)
+                 repcut=repcut, repcut_global=repcut_global, l2_policy=l2_policy)
     if staged is not None:
         L.set_inputs(0, staged)
     else:
@@ -453,3 +453,12 @@ def test_watch_errors(rs):
             Ls.watch([0])
         assert e.value.name == "RS_E_UNSUPPORTED"
     assert L.wave_read()[0].shape[0] == 0           # nothing watched: empty
+
+
+@pytest.mark.parametrize("policy", [1, 2])
+@pytest.mark.parametrize("kernel", [1, 2, 6])
+def test_l2_policy_results_identical(rs, policy, kernel):
+    """rs_lane_opts.l2_policy (access-policy window over the schedule / the state) changes
+    speed only."""
+    c = config_circuit("C3", n_ops=20000, n_levels=20, n_regs=2000)
+    check(rs, c, 8, 150, seed=4, kernel=kernel, l2_policy=policy)
