@@ -183,6 +183,9 @@ typedef struct {
                               persisting; 2 = the signal state persisting (hit ratio = the device's
                               persisting-L2 limit / state bytes, the rest streaming).  Results are
                               identical; only speed differs (measured in DESIGN.md §8). */
+  uint32_t defer_state;    /* 1: do not allocate the signal state; the caller binds its own device buffer
+                              (e.g. a torch tensor) with rs_lanes_bind_state before stepping, sized by
+                              rs_lanes_state_bytes.  Not with part_world. */
 } rs_lane_opts;
 
 typedef struct rs_graph rs_graph;
@@ -238,6 +241,14 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
 void rs_free_lanes(rs_lanes* s);
 /* Device bytes held by this allocation. */
 uint64_t rs_lanes_bytes(const rs_lanes* s);
+/* Caller-owned state (rs_lane_opts.defer_state = 1; SURVEY.md §8(b) "torch-owned memory"):
+ * rs_lanes_state_bytes = the bytes the signal state needs; rs_lanes_bind_state binds `state`
+ * (device memory of the graph's device, 256-byte aligned, >= those bytes, owned by the caller,
+ * kept alive until rs_free_lanes) and initialises it (registers = init, constants, all else 0;
+ * synchronises the lanes' stream).  Stepping or reading before binding returns RS_E_STATE;
+ * RS_E_CAPACITY if the buffer is too small, RS_E_INVALID_ARG if not such device memory. */
+uint64_t rs_lanes_state_bytes(const rs_lanes* s);
+rs_status rs_lanes_bind_state(rs_lanes* s, void* state, uint64_t bytes);
 
 /* Input source = counter-based stimulus of (seed, input k, absolute cycle,
  * global lane) (reading R13). */

@@ -36,7 +36,7 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
     cmd = [NVCC, "-std=c++17", "-O3", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-shared",
            "-I", os.path.join(ROOT, "include"),
            *["-D" + d for d in defines],
-           *[os.path.join(CSRC, f) for f in SOURCES], "-o", lib + ".tmp"]
+           *[os.path.join(CSRC, f) for f in SOURCES], "-ldl", "-o", lib + ".tmp"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)

@@ -2,6 +2,7 @@
 // staged-input ring, launches.  No host fallback: every simulated cycle runs
 // in the kernels of kernels.cuh.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // NVTX ranges around the ABI's device work (header-only; no-ops without a tool)
 
 #include <algorithm>
 #include <cstdarg>
@@ -24,6 +25,11 @@ using namespace rtlsim;
 
 namespace {
 thread_local std::string g_err = "no error";
+
+struct NvtxRange {  // an NVTX range for the scope (nsys / ncu --nvtx timelines)
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 rs_status set_err(rs_status st, const char* fmt, ...) {
   char buf[512];
@@ -131,6 +137,8 @@ struct rs_lanes {
   uint32_t part_world = 0, part_rank = 0;
   bool connected = false;
   uint32_t l2_policy = 0;           // rs_lane_opts.l2_policy
+  bool state_owned = true;          // false: the caller's buffer (rs_lanes_bind_state)
+  size_t flag_bytes = 0;            // level cut across processes: the cycle flag after the replica
   size_t l2_persist_max = 0;        // cudaDevAttrMaxPersistingL2CacheSize
   uint8_t* peer_rep[kMaxParts] = {};
   unsigned long long* peer_flag[kMaxParts] = {};
@@ -374,6 +382,8 @@ void choose_tiling(uint32_t kernel, uint32_t n_lanes, int sms, uint32_t want_lt,
 
 extern "C" {
 
+static rs_status init_state(rs_lanes* s);
+
 const char* rs_version(void) { return "rtlsim-b200 0.1 (sm_100a)"; }
 const char* rs_last_error(void) { return g_err.c_str(); }
 
@@ -544,6 +554,7 @@ void rs_free_graph(rs_graph* g) {
 constexpr uint32_t kRepSmemMax = 227u * 1024u - 2048u;
 
 rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts, rs_lanes** out) {
+  NvtxRange nvtx_range("rs_alloc_lanes");
   if (!g || !out) return set_err(RS_E_INVALID_ARG, "NULL graph/out");
   *out = nullptr;
   if (n_lanes == 0) return set_err(RS_E_INVALID_ARG, "n_lanes must be >= 1");
@@ -892,7 +903,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
   cudaError_t e;
   // across processes the cycle flag follows the replica in the same allocation (one IPC handle)
   const size_t flag_bytes = s->part_world ? 256 : 0;
-  if ((e = cudaMalloc(&s->state_mem, s->state_bytes + flag_bytes)) != cudaSuccess) {
+  if (!o.defer_state && (e = cudaMalloc(&s->state_mem, s->state_bytes + flag_bytes)) != cudaSuccess) {
     rs_free_lanes(s);  // partially built: frees what exists
     return set_err(RS_E_OOM, "cudaMalloc state (%zu B): %s", s->state_bytes, cudaGetErrorString(e));
   }
@@ -927,7 +938,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     }
     s->stage_cap = o.stage_cycles;
   }
-  s->total_bytes += s->state_bytes + 2 * lanes_pad * 8 + kBarBytes +
+  s->total_bytes += (o.defer_state ? 0 : s->state_bytes) + 2 * lanes_pad * 8 + kBarBytes +
                    (size_t)s->stage_cap * std::max<uint32_t>(1, g->cg.n_inputs) * n_lanes * 8;
   if (o.stream) {
     s->stream = (cudaStream_t)o.stream;
@@ -938,9 +949,27 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     }
     s->own_stream = true;
   }
-  // init: zero, constants, register init, hash carry
+  s->flag_bytes = flag_bytes;
+  g->live_lanes++;
+  s->counted = true;
+  if (o.defer_state) {  // the caller binds its own device buffer (rs_lanes_bind_state)
+    *out = s;
+    return RS_OK;
+  }
+  if ((st = init_state(s)) != RS_OK) {
+    rs_free_lanes(s);
+    return st;
+  }
+  *out = s;
+  return RS_OK;
+}
+
+// Initial state: zero, constants, register init, hash carry.
+static rs_status init_state(rs_lanes* s) {
+  rs_graph* g = s->g;
+  const size_t lanes_pad = (size_t)s->n_tiles * s->LT;
   StepArgs a = base_args(s);
-  e = cudaMemsetAsync(s->state_mem, 0, s->state_bytes + flag_bytes, s->stream);
+  cudaError_t e = cudaMemsetAsync(s->state_mem, 0, s->state_bytes + s->flag_bytes, s->stream);
   std::vector<uint32_t> coords;
   std::vector<uint64_t> vals;
   coords.insert(coords.end(), g->cg.const_coord.begin(), g->cg.const_coord.end());
@@ -967,14 +996,31 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     std::vector<uint64_t> hc(lanes_pad, (s->part_world && s->part_rank != 0) ? 0ull : g->cg.init_reg_hash);
     e = cudaMemcpy(s->hcarry, hc.data(), lanes_pad * 8, cudaMemcpyHostToDevice);
   }
-  if (e != cudaSuccess) {
-    rs_free_lanes(s);
-    return set_err(RS_E_CUDA, "state init: %s", cudaGetErrorString(e));
-  }
-  g->live_lanes++;
-  s->counted = true;
-  *out = s;
+  if (e != cudaSuccess) return set_err(RS_E_CUDA, "state init: %s", cudaGetErrorString(e));
   return RS_OK;
+}
+
+uint64_t rs_lanes_state_bytes(const rs_lanes* s) { return s ? (uint64_t)(s->state_bytes + s->flag_bytes) : 0; }
+
+rs_status rs_lanes_bind_state(rs_lanes* s, void* state, uint64_t bytes) {
+  if (!s || !state) return set_err(RS_E_INVALID_ARG, "NULL argument");
+  if (s->state_mem) return set_err(RS_E_STATE, "the allocation already has its state");
+  if (s->part_world) return set_err(RS_E_UNSUPPORTED, "a level cut across processes owns its state (CUDA IPC)");
+  if (bytes < s->state_bytes + s->flag_bytes)
+    return set_err(RS_E_CAPACITY, "state buffer of %llu B; needs %llu B (rs_lanes_state_bytes)",
+                   (unsigned long long)bytes, (unsigned long long)(s->state_bytes + s->flag_bytes));
+  if ((uintptr_t)state % 256) return set_err(RS_E_INVALID_ARG, "state buffer must be 256-byte aligned");
+  rs_status st = set_device(s->g);
+  if (st != RS_OK) return st;
+  cudaPointerAttributes pa;
+  if (cudaPointerGetAttributes(&pa, state) != cudaSuccess || pa.type != cudaMemoryTypeDevice ||
+      pa.device != s->g->device) {
+    (void)cudaGetLastError();
+    return set_err(RS_E_INVALID_ARG, "state buffer is not device memory of device %d", s->g->device);
+  }
+  s->state_mem = state;
+  s->state_owned = false;
+  return init_state(s);
 }
 
 void rs_free_lanes(rs_lanes* s) {
@@ -984,7 +1030,7 @@ void rs_free_lanes(rs_lanes* s) {
   if (!s) return;
   cudaSetDevice(s->g->device);
   if (s->stream) cudaStreamSynchronize(s->stream);
-  if (s->state_mem) cudaFree(s->state_mem);
+  if (s->state_mem && s->state_owned) cudaFree(s->state_mem);
   if (s->dstages) cudaFree(s->dstages);
   if (s->dslices) cudaFree(s->dslices);
   if (s->hcarry) cudaFree(s->hcarry);
@@ -1021,6 +1067,7 @@ rs_status rs_set_input_seed(rs_lanes* s, uint64_t seed) {
 }
 
 rs_status rs_set_inputs(rs_lanes* s, uint64_t first_cycle, uint32_t n_cycles, const uint64_t* values, int on_device) {
+  NvtxRange nvtx_range("rs_set_inputs");
   if (!s) return set_err(RS_E_INVALID_ARG, "NULL lanes");
   if (!s->stage_cap) return set_err(RS_E_STATE, "no staged-input ring (rs_lane_opts.stage_cycles = 0)");
   if (n_cycles > s->stage_cap) return set_err(RS_E_RANGE, "n_cycles %u > stage_cycles %u", n_cycles, s->stage_cap);
@@ -1108,7 +1155,9 @@ static rs_status refresh_hcarry(rs_lanes* s) {
 }
 
 rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int hashes_mem) {
+  NvtxRange nvtx_range("rs_step_cycles");
   if (!s) return set_err(RS_E_INVALID_ARG, "NULL lanes");
+  if (!s->state_mem) return set_err(RS_E_STATE, "no state bound (rs_lanes_bind_state)");
   if (hashes_mem != RS_MEM_NONE && hashes_mem != RS_MEM_HOST && hashes_mem != RS_MEM_DEVICE)
     return set_err(RS_E_INVALID_ARG, "bad hashes_mem %d", hashes_mem);
   if (hashes_mem != RS_MEM_NONE && !hashes && n_cycles) return set_err(RS_E_INVALID_ARG, "NULL hashes");
@@ -1304,7 +1353,9 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
 
 rs_status rs_read_signals(rs_lanes* s, const uint32_t* ids, uint32_t n_ids, uint32_t lane_begin, uint32_t n_lanes,
                           uint64_t* out) {
+  NvtxRange nvtx_range("rs_read_signals");
   if (!s || (n_ids && (!ids || !out))) return set_err(RS_E_INVALID_ARG, "NULL argument");
+  if (!s->state_mem) return set_err(RS_E_STATE, "no state bound (rs_lanes_bind_state)");
   if ((uint64_t)lane_begin + n_lanes > s->n_lanes) return set_err(RS_E_RANGE, "lanes [%u, %u) out of range (%u lanes)", lane_begin, lane_begin + n_lanes, s->n_lanes);
   if (n_ids == 0 || n_lanes == 0) return RS_OK;
   std::vector<uint32_t> coords(n_ids);

@@ -27,7 +27,7 @@ EXPORTS = ["rs_version", "rs_last_error", "rs_load_graph", "rs_graph_info_get", 
            "rs_alloc_lanes", "rs_free_lanes", "rs_lanes_bytes", "rs_set_input_seed", "rs_set_inputs",
            "rs_step_cycles", "rs_read_signals", "rs_write_registers", "rs_get_cycle", "rs_set_cycle",
            "rs_launch_count", "rs_launch_shape", "rs_lanes_kernel", "rs_repcut_stats", "rs_watch", "rs_wave_read", "rs_sync", "rs_graph_export", "rs_debug_trace",
-           "rs_level_cut", "rs_ipc_handle", "rs_ipc_connect"]
+           "rs_level_cut", "rs_ipc_handle", "rs_ipc_connect", "rs_lanes_state_bytes", "rs_lanes_bind_state"]
 RS_DEVICE_NONE = -1
 EXPORT = {"runs": (0, np.uint32), "level_run_begin": (1, np.uint32), "level_op_begin": (2, np.uint32),
           "opw": (3, np.uint32), "opk": (4, np.uint64), "coord_off": (5, np.uint32), "coord": (6, np.uint32),
@@ -69,7 +69,8 @@ class LaneOpts(C.Structure):
                 ("stage_cycles", C.c_uint32), ("cluster", C.c_uint32), ("stream", C.c_void_p),
                 ("parts", C.c_uint32), ("kernel", C.c_uint32),
                 ("repcut", C.c_uint32), ("repcut_global", C.c_uint32),
-                ("part_world", C.c_uint32), ("part_rank", C.c_uint32), ("l2_policy", C.c_uint32)]
+                ("part_world", C.c_uint32), ("part_rank", C.c_uint32), ("l2_policy", C.c_uint32),
+                ("defer_state", C.c_uint32)]
 
 
 _lib = None
@@ -113,6 +114,8 @@ def lib() -> C.CDLL:
             "rs_level_cut": (i32, [vp, u32, vp]),
             "rs_ipc_handle": (i32, [vp, vp]),
             "rs_ipc_connect": (i32, [vp, vp]),
+            "rs_lanes_state_bytes": (u64, [vp]),
+            "rs_lanes_bind_state": (i32, [vp, vp, u64]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -222,16 +225,19 @@ class Lanes:
     def __init__(self, graph: Graph, n_lanes: int, lane0: int = 0, lane_tile: int = 0, threads: int = 0,
                  stage_cycles: int = 0, stream=None, cluster: int = 0, parts: int = 0, kernel: int = 0,
                  repcut: int = 0, repcut_global: int = 0, part_world: int = 0, part_rank: int = 0,
-                 l2_policy: int = 0):
+                 l2_policy: int = 0, state=None):
         self.graph = graph
         self.n_lanes = n_lanes
         self.lane0 = lane0
         st = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
         self.opts = LaneOpts(lane0, lane_tile, threads, stage_cycles, cluster, st, parts, kernel, repcut,
-                             int(repcut_global), part_world, part_rank, l2_policy)
+                             int(repcut_global), part_world, part_rank, l2_policy, 1 if state is not None else 0)
         h = C.c_void_p()
         _check(lib().rs_alloc_lanes(graph.h, n_lanes, C.byref(self.opts), C.byref(h)))
         self.h = h
+        if state is not None:
+            # caller-owned signal state: "torch" -> a torch CUDA tensor allocated here; or a tensor
+            self.state = self.bind_state(state)
 
     # ---- inputs
     def set_seed(self, seed: int) -> None:
@@ -319,6 +325,23 @@ class Lanes:
         n, d = C.c_uint64(), C.c_uint64()
         _check(lib().rs_wave_read(self.h, _ptr(out), cap, C.byref(n), C.byref(d)))
         return out[:n.value], d.value
+
+    def state_bytes(self) -> int:
+        return int(lib().rs_lanes_state_bytes(self.h))
+
+    def bind_state(self, state):
+        """rs_lanes_bind_state: state = "torch" (allocate a torch CUDA uint8 tensor of
+        rs_lanes_state_bytes on the graph's device) or a torch CUDA tensor; returns it
+        (keep it alive as long as this allocation)."""
+        if isinstance(state, str) and state == "torch":
+            import torch
+            n = self.state_bytes()
+            state = torch.empty(n + 256, dtype=torch.uint8, device=f"cuda:{self.graph.device}")
+            off = (-state.data_ptr()) % 256
+            state = state[off:off + n]
+        _check(lib().rs_lanes_bind_state(self.h, C.c_void_p(_dev_ptr(state)),
+                                         state.numel() * state.element_size()))
+        return state
 
     # ---- level cut across processes (rs_ipc_handle / rs_ipc_connect)
     IPC_HANDLE_BYTES = 64

@@ -462,3 +462,36 @@ def test_l2_policy_results_identical(rs, policy, kernel):
     speed only."""
     c = config_circuit("C3", n_ops=20000, n_levels=20, n_regs=2000)
     check(rs, c, 8, 150, seed=4, kernel=kernel, l2_policy=policy)
+
+
+@pytest.mark.parametrize("kernel", [1, 2, 6])
+def test_caller_owned_state(rs, kernel):
+    """rs_lane_opts.defer_state + rs_lanes_bind_state (SURVEY.md §8(b) torch-owned memory):
+    the signal state lives in a torch tensor; results equal the oracle's, and the library
+    refuses to step before the state is bound or with a too-small buffer."""
+    import torch
+    c = config_circuit("C2", n_ops=3000, n_levels=15, n_regs=300)
+    g = rs.Graph(c)
+    L = rs.Lanes(g, 50, kernel=kernel, state="torch")
+    assert L.state.is_cuda and L.state.numel() == L.state_bytes()
+    L.set_seed(8)
+    h = L.step(9, hashes="host")
+    r = oracle.simulate(c, 9, seed=8, n_lanes=50, final=True)
+    assert np.array_equal(h, r.hashes)
+    assert np.array_equal(L.read(list(range(c.n_signals))), r.final_state)
+    raw = rs.Lanes.__new__(rs.Lanes)
+    M = rs.Lanes(g, 50, kernel=kernel, state=None)
+    assert M.state_bytes() == L.state_bytes()
+    import ctypes
+    opts = rs.LaneOpts(0, 0, 0, 0, 0, None, 0, kernel, 0, 0, 0, 0, 0, 1)
+    hnd = ctypes.c_void_p()
+    rs._check(rs.lib().rs_alloc_lanes(g.h, 50, ctypes.byref(opts), ctypes.byref(hnd)))
+    with pytest.raises(rs.RtlSimError) as e:
+        rs._check(rs.lib().rs_step_cycles(hnd, 1, None, 0))
+    assert e.value.name == "RS_E_STATE"
+    small = torch.empty(256, dtype=torch.uint8, device="cuda")
+    with pytest.raises(rs.RtlSimError) as e:
+        rs._check(rs.lib().rs_lanes_bind_state(hnd, ctypes.c_void_p(small.data_ptr()), 256))
+    assert e.value.name == "RS_E_CAPACITY"
+    rs.lib().rs_free_lanes(hnd)
+    del raw
