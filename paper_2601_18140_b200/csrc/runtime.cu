@@ -350,27 +350,32 @@ size_t lanes_smem(uint32_t stage_bytes, uint32_t threads) {
   return 128 + 2ull * stage_bytes + lanes_smem_extra(threads);
 }
 
-// Lane tile and cluster size: the widest tile (most lanes per warp
-// instruction), spread over the fewest CTAs of a cluster that keeps >= 80% of
-// the SMs busy; narrower tiles only when even an 8-CTA cluster per tile
-// cannot fill the GPU.  Kernel 1 tiles are 32 * P lanes (P = 1, 2, 4 lanes per
-// thread), kernel 2 tiles 8, 16 or 32 lanes.
+// Lane tile and cluster size: the widest tile (most lanes per warp instruction)
+// spread over the fewest CTAs of a cluster (at most 4) that keeps >= 80% of the
+// SMs busy; 8-CTA clusters only when no tile reaches that with 4.  Measured on
+// B200 (profiles/r02/sweep_shapes): the best C3-shaped shapes at 4096 / 2048 /
+// 1024 / 512 lanes are 128x4 (kernel 1), 64x4 (kernel 1), 32x4 and 16x4
+// (kernel 2) -- 8-CTA clusters lost everywhere (e.g. 2048 lanes: 128x8 took
+// 1.44 ms per cycle, 64x4 0.93 ms).  Kernel 1 tiles are 32 * P lanes (P = 1, 2,
+// 4 lanes per thread), kernel 2 tiles 8, 16 or 32 lanes, kernel 6 64 or 128.
 void choose_tiling(uint32_t kernel, uint32_t n_lanes, int sms, uint32_t want_lt, uint32_t want_cs, uint32_t* lt,
                    uint32_t* cs) {
   const uint32_t k1[3] = {128u, 64u, 32u}, k2[3] = {32u, 16u, 8u}, k6[2] = {128u, 64u};
   const uint32_t* cand = kernel == 1 ? k1 : kernel == 6 ? k6 : k2;
   const int nc = kernel == 6 ? 2 : 3;
   const uint32_t smallest = cand[nc - 1];
-  for (int i = 0; i < nc; ++i) {
-    const uint32_t t = cand[i];
-    if (want_lt && t != want_lt) continue;
-    const uint64_t tiles = (n_lanes + t - 1) / t;
-    for (uint32_t c : {1u, 2u, 4u, 8u}) {
-      if (want_cs && c != want_cs) continue;
-      if (tiles * c * 10 >= (uint64_t)sms * 8 || (want_lt && want_cs) || (t == smallest && c == 8)) {
-        *lt = t;
-        *cs = c;
-        return;
+  for (const uint32_t cmax : {4u, 8u}) {
+    for (int i = 0; i < nc; ++i) {
+      const uint32_t t = cand[i];
+      if (want_lt && t != want_lt) continue;
+      const uint64_t tiles = (n_lanes + t - 1) / t;
+      for (uint32_t c : {1u, 2u, 4u, 8u}) {
+        if (c > cmax || (want_cs && c != want_cs)) continue;
+        if (tiles * c * 10 >= (uint64_t)sms * 8 || (want_lt && want_cs)) {
+          *lt = t;
+          *cs = c;
+          return;
+        }
       }
     }
   }
