@@ -187,6 +187,10 @@ __device__ __forceinline__ void batch_ops_t(const LaneT& L, uint32_t op, uint32_
     uint32_t c[A];
 #pragma unroll
     for (int o = 0; o < A; ++o) c[o] = lds32(s_c + 4 * (uu * A + o));
+#ifdef RS_EXPERIMENT_FAKE_GATHER  // diagnostic build only (tools/): every operand read from row 0 of its class
+#pragma unroll
+    for (int o = 0; o < A; ++o) c[o] &= 0xC0000000u;
+#endif
     gather_t<A, P>(L, c, x[u]);
     pw[u] = lds32(s_w + 4 * uu);
   }
