@@ -1,0 +1,284 @@
+// lanes_r.cuh -- the record-based tile lane kernel (k_lanes_r, rs_lane_opts.kernel = 7).
+//
+// Same state layout and tile interleave as lanes_t.cuh (tile = 32 * P lanes, thread t
+// owns lanes t + 32k, one warp evaluates one op for all LT lanes, four width classes),
+// but the level's op tensor is staged as one 32-byte RECORD per op, prepared at bind
+// time (runtime.cu bind_stages_r):
+//   {c0, c1, c2, pw, out coordinate, K lo, K hi, sel}
+// sel = gather selector (arity and operand class signature, one jump table over every
+// arity: gather_r.cuh) | tail index << 8 (opcode, arity, out class: one specialised
+// compute / mask / hash / store tail).  The warps of the cluster split a stage's ops
+// into contiguous ranges; per op a warp issues two shared-memory vector loads, one
+// jump into the gather, one into the tail -- no run / work-item decode, no per-op
+// address recomputation (the Format-c runs of P:1123-1129 survive as the record order).
+// Results <= 32 bits are computed, masked and hashed in 32-bit arithmetic.  The hash
+// partials are summed with shared-memory atomics (as lanes_b.cuh).
+#pragma once
+#include "gather_r.cuh"
+#include "lanes_b.cuh"
+
+#ifndef RS_LANES_R_MAX_THREADS
+#define RS_LANES_R_MAX_THREADS 768
+#endif
+
+namespace rtlsim {
+
+constexpr uint32_t kRecBytes = 32;
+constexpr uint32_t kTailFold = 84;  // arity > 3: generic left fold
+
+// Dense tail combo index of (opcode, arity); tail = combo * 4 + out class.
+__host__ __device__ constexpr int tail_combo(int A, int op) {
+  return A == 1 ? (op == RS_OP_NOT ? 0 : op == RS_OP_SHL ? 1 : op == RS_OP_SHR ? 2 : op == RS_OP_BITS ? 3 : 4)
+       : A == 2 ? 5 + (op <= RS_OP_MUL ? op - (op > RS_OP_XOR ? 1 : 0) : op == RS_OP_EQ ? 6 : op == RS_OP_LT ? 7 : 8)
+                : 14 + (op <= RS_OP_MUL ? op - (op > RS_OP_XOR ? 1 : 0) : 6);
+}
+// Gather selector of an op with A <= 3 operands of classes cls[0..A).
+__host__ __device__ constexpr uint32_t gather_sel(int A, uint32_t c0, uint32_t c1, uint32_t c2) {
+  return A == 1 ? c0 : A == 2 ? 4 + c0 + 4 * c1 : 20 + c0 + 4 * c1 + 16 * c2;
+}
+
+template <int P>
+__device__ __forceinline__ void gather_r(const LaneT& L, uint32_t g, uint32_t c0, uint32_t c1, uint32_t c2,
+                                         uint64_t (&x)[3][P]) {
+  if constexpr (P == 2) gatherr_p2(g, L.p0, L.p1, L.p2, L.p3, c0, c1, c2, x);
+  else gatherr_p4(g, L.p0, L.p1, L.p2, L.p3, c0, c1, c2, x);
+}
+
+// One op's tail: compute, mask to w_out, hash, store (out class OC, lanes_t layout).
+template <int P, bool HASH, int A, int OP, int OC>
+__device__ __forceinline__ void tail_r(const LaneT& L, const uint64_t (&x)[3][P], uint32_t pw, uint32_t oc,
+                                       uint64_t K, uint64_t (&hacc)[P]) {
+  if constexpr (OC == 3) {
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      uint64_t xs[A];
+#pragma unroll
+      for (int o = 0; o < A; ++o) xs[o] = x[o][k];
+      const uint64_t v = apply_op<OP, A>(xs, pw);  // masked to w_out
+      if constexpr (HASH) hacc[k] += v * K;
+      reinterpret_cast<uint64_t*>(const_cast<uint8_t*>(L.p3) + oc)[32 * k] = v;
+    }
+  } else {
+    const uint32_t m = 0xFFFFFFFFu >> (32u - (pw & 127u));  // w_out <= 32
+    const uint32_t klo = (uint32_t)K, khi = (uint32_t)(K >> 32);
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      uint64_t xs[A];
+#pragma unroll
+      for (int o = 0; o < A; ++o) xs[o] = x[o][k];
+      const uint32_t v = low32<OP, A>(xs, pw) & m;
+      if constexpr (HASH) hacc[k] += (uint64_t)v * klo + ((uint64_t)(v * khi) << 32);
+      if constexpr (OC == 0) (const_cast<uint8_t*>(L.p0) + oc)[32 * k] = (uint8_t)v;
+      else if constexpr (OC == 1) reinterpret_cast<uint16_t*>(const_cast<uint8_t*>(L.p1) + oc)[32 * k] = (uint16_t)v;
+      else reinterpret_cast<uint32_t*>(const_cast<uint8_t*>(L.p2) + oc)[32 * k] = v;
+    }
+  }
+}
+
+// Folds with more than 3 operands: c0 = shared-memory address of the coordinate
+// list, c1 = arity, opcode in sel bits [31:24].
+template <int P, bool HASH>
+__device__ __forceinline__ void fold_r(const LaneT& L, uint32_t s_list, uint32_t ar, uint32_t op, uint32_t pw,
+                                       uint32_t oc, uint64_t K, uint64_t (&hacc)[P]) {
+  uint64_t r[P], x[P];
+  gather1_t<P>(L, lds32(s_list), r);
+#pragma unroll 1
+  for (uint32_t o = 1; o < ar; ++o) {
+    gather1_t<P>(L, lds32(s_list + 4 * o), x);
+#pragma unroll
+    for (int k = 0; k < P; ++k) r[k] = fold_step(op, r[k], x[k]);
+  }
+  const uint64_t m = wmask(pw & 127u);
+#pragma unroll
+  for (int k = 0; k < P; ++k) {
+    r[k] &= m;
+    if constexpr (HASH) hacc[k] += r[k] * K;
+  }
+  store_t<P>(L, oc, r);
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+
+// OPS stage: records at buf + off_c (h->n of them); this warp takes ops [b, e).
+template <int P, bool HASH>
+__device__ __forceinline__ void stage_ops_r(const LaneT& L, const uint8_t* buf, uint32_t b, uint32_t e,
+                                            uint64_t (&hacc)[P]) {
+  const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
+  const uint32_t base = smem_addr(buf), rec0 = base + h->off_c;
+#pragma unroll 1
+  for (uint32_t j = b; j < e; ++j) {
+    const uint4 r0 = lds128(rec0 + kRecBytes * j), r1 = lds128(rec0 + kRecBytes * j + 16);
+    const uint32_t pw = r0.w, oc = r1.x, sel = r1.w, t = (sel >> 8) & 0xffu;
+    const uint64_t K = HASH ? ((uint64_t)r1.z << 32 | r1.y) : 0ull;
+    if (t == kTailFold) {
+      fold_r<P, HASH>(L, base + r0.x, r0.y, sel >> 24, pw, oc, K, hacc);
+      continue;
+    }
+    uint64_t x[3][P];
+    gather_r<P>(L, sel & 0xffu, r0.x, r0.y, r0.z, x);
+#define RS_R4(C, A, OPC)                                                      \
+  case 4 * C + 0: tail_r<P, HASH, A, OPC, 0>(L, x, pw, oc, K, hacc); break;   \
+  case 4 * C + 1: tail_r<P, HASH, A, OPC, 1>(L, x, pw, oc, K, hacc); break;   \
+  case 4 * C + 2: tail_r<P, HASH, A, OPC, 2>(L, x, pw, oc, K, hacc); break;   \
+  case 4 * C + 3: tail_r<P, HASH, A, OPC, 3>(L, x, pw, oc, K, hacc); break;
+    switch (t) {
+      RS_R4(0, 1, RS_OP_NOT) RS_R4(1, 1, RS_OP_SHL) RS_R4(2, 1, RS_OP_SHR) RS_R4(3, 1, RS_OP_BITS) RS_R4(4, 1, OP_COPY)
+      RS_R4(5, 2, RS_OP_AND) RS_R4(6, 2, RS_OP_OR) RS_R4(7, 2, RS_OP_XOR) RS_R4(8, 2, RS_OP_ADD)
+      RS_R4(9, 2, RS_OP_SUB) RS_R4(10, 2, RS_OP_MUL) RS_R4(11, 2, RS_OP_EQ) RS_R4(12, 2, RS_OP_LT)
+      RS_R4(13, 2, RS_OP_CAT)
+      RS_R4(14, 3, RS_OP_AND) RS_R4(15, 3, RS_OP_OR) RS_R4(16, 3, RS_OP_XOR) RS_R4(17, 3, RS_OP_ADD)
+      RS_R4(18, 3, RS_OP_SUB) RS_R4(19, 3, RS_OP_MUL) RS_R4(20, 3, RS_OP_MUX)
+      default: break;
+    }
+#undef RS_R4
+  }
+}
+
+template <int P, bool HASH>
+__global__ void __launch_bounds__(RS_LANES_R_MAX_THREADS, 1) k_lanes_r(const StepArgs a) {
+  constexpr uint32_t LT = 32u * P;
+  extern __shared__ __align__(128) uint8_t smem[];
+  // [mbarriers | stage buffer 0 | stage buffer 1 | scyc[4][LT] | sreg[4][LT]] (hash partials as k_lanes_b)
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
+  const uint32_t T = blockDim.x, tid = threadIdx.x;
+  uint64_t* scyc = reinterpret_cast<uint64_t*>(smem + 128 + 2 * (size_t)a.stage_bytes);
+  uint64_t* sreg = scyc + 4 * LT;
+
+  const uint32_t CS = a.cluster;
+  const uint32_t rank = blockIdx.x % CS, tile = blockIdx.x / CS;
+  const uint32_t lin = tid & 31u, warp = tid >> 5, nwarp = T >> 5;
+  const uint32_t gw = rank * nwarp + warp, ngw = CS * nwarp;
+  const uint32_t lane = tile * LT + lin;
+  const LaneT L = make_lanet(a.state + (size_t)tile * a.tile_bytes, lin);
+
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    mbar_fence_init();
+  }
+  if constexpr (HASH) {
+    for (uint32_t i = tid; i < 8 * LT; i += T) {
+      const uint32_t l = tile * LT + (i % LT);
+      scyc[i] = (i >= 4 * LT && i < 5 * LT && rank == 0 && l < a.n_lanes) ? a.hcarry_in[l] : 0ull;  // sreg[0]
+    }
+  }
+  __syncthreads();
+  const uint32_t S = a.n_stages;
+  const uint32_t total = a.n_cycles * S;
+  if (tid == T - 1 && total) {
+    const StageRef r = a.stage_tab[0];
+    tma_load_1d(smem + 128, a.stage_blob + r.off, r.bytes, &mbar[0]);
+  }
+  const uint32_t producer = T - 1;
+  StageRef nref{};
+  if (tid == producer && total > 1) nref = a.stage_tab[S > 1 ? 1 : 0];
+  if (CS > 1) stage_barrier(CS);
+
+  uint64_t hacc[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) hacc[k] = 0;
+  uint32_t s = 0, cyc = 0;
+#pragma unroll 1
+  for (uint32_t gi = 0; gi < total; ++gi) {
+    const uint32_t bsel = gi & 1u;
+    if (tid == producer && gi + 1 < total) {
+      tma_load_1d(smem + 128 + (bsel ^ 1u) * a.stage_bytes, a.stage_blob + nref.off, nref.bytes, &mbar[bsel ^ 1u]);
+      nref = a.stage_tab[(s + 2) % S];
+    }
+    mbar_wait(&mbar[bsel], (gi >> 1) & 1u);
+    const uint8_t* buf = smem + 128 + bsel * a.stage_bytes;
+    const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
+    const uint32_t type = h->type;
+    uint32_t b, e;
+    chunk_of(h->n, gw, ngw, b, e);
+    if (type == ST_OPS) {
+      if (b < e) stage_ops_r<P, HASH>(L, buf, b, e, hacc);
+    } else if (type == ST_LATCH) {
+      if (b < e) {
+        const uint32_t base = smem_addr(buf);
+        uint64_t hr[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) hr[k] = 0;
+        stage_latch_t<P, HASH>(L, base + h->off_c, base + h->off_w, base + h->off_k, b, e, hr);
+        if constexpr (HASH) {
+          uint64_t* sr = sreg + ((cyc + 1u) & 3u) * LT;
+#pragma unroll
+          for (int k = 0; k < P; ++k) atomicAdd((unsigned long long*)&sr[lin + 32 * k], (unsigned long long)hr[k]);
+        }
+      }
+    } else if (type == ST_INJECT) {
+      if (b < e) {
+        const uint32_t base = smem_addr(buf);
+        stage_inject_t<P, HASH>(L, base + h->off_c, base + h->off_w, base + h->off_k, h->first, b, e, a, lane,
+                                a.cycle0 + cyc, hacc);
+      }
+    } else if (type == ST_WATCH) {
+      uint32_t ln[P];
+#pragma unroll
+      for (int k = 0; k < P; ++k) ln[k] = lin + 32 * k;
+      if (b < e)
+        stage_watch<P>(a, a.state + (size_t)tile * a.tile_bytes, reinterpret_cast<const uint32_t*>(buf + h->off_c), b,
+                       e, ln, tile, a.cycle0 + cyc);
+    }
+    const bool eoc = (s + 1 == S);
+    if constexpr (HASH) {
+      if (eoc) {
+        uint64_t* sc = scyc + (cyc & 3u) * LT;
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+          if (hacc[k]) atomicAdd((unsigned long long*)&sc[lin + 32 * k], (unsigned long long)hacc[k]);
+          hacc[k] = 0;
+        }
+        if (warp == nwarp - 1) {  // clear the slots of cycle c + 2 (read two cycles ago)
+#pragma unroll
+          for (int k = 0; k < P; ++k) {
+            scyc[((cyc + 2u) & 3u) * LT + lin + 32 * k] = 0;
+            sreg[((cyc + 2u) & 3u) * LT + lin + 32 * k] = 0;
+          }
+        }
+      }
+    }
+    stage_barrier(CS);
+    if constexpr (HASH) {
+      if (eoc && warp == 0 && rank == 0 && a.hashes != nullptr) {
+        const uint32_t sl = (cyc & 3u) * LT;
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+          const uint32_t li = lin + 32 * k;
+          uint64_t sum = a.g.const_hash + scyc[sl + li] + sreg[sl + li];
+          for (uint32_t r = 1; r < CS; ++r) {
+            const uint64_t* pc = dsmem(scyc, r);
+            sum += pc[sl + li] + pc[4 * LT + sl + li];
+          }
+          if (lane + 32 * k < a.n_lanes) a.hashes[(size_t)cyc * a.n_lanes + lane + 32 * k] = sum;
+        }
+      }
+    }
+    if (eoc) {
+      s = 0;
+      ++cyc;
+    } else {
+      ++s;
+    }
+  }
+  if constexpr (HASH) {
+    stage_barrier(CS);
+    if (warp == 0 && rank == 0) {
+      const uint32_t sl = (cyc & 3u) * LT;
+#pragma unroll
+      for (int k = 0; k < P; ++k) {
+        const uint32_t li = lin + 32 * k, l = lane + 32 * k;
+        uint64_t sum = sreg[sl + li];
+        for (uint32_t r = 1; r < CS; ++r) sum += dsmem(sreg, r)[sl + li];
+        if (l < a.n_lanes) a.hcarry_out[l] = sum;
+      }
+    }
+    if (CS > 1) stage_barrier(CS);
+  }
+}
+
+}  // namespace rtlsim

@@ -18,6 +18,7 @@
 #include "lanes.cuh"
 #include "lanes_t.cuh"
 #include "lanes_b.cuh"
+#include "lanes_r.cuh"
 #include "single.cuh"
 #include "repcut.cuh"
 
@@ -275,16 +276,110 @@ void bind_stages_b(const rs_lanes* s, std::vector<uint8_t>* out) {
   }
 }
 
+// Record-based allocations (kernel 7, lanes_r.cuh): the kernel-1 bound schedule
+// with every OPS stage rewritten as 32-byte op records {c0, c1, c2, pw, out
+// coordinate, K, sel} (split into several stages when the records outgrow a
+// stage buffer; an extra barrier is harmless).  Other stages are kept as bound.
+void bind_stages_r(const rs_lanes* s, std::vector<uint8_t>* out, std::vector<StageRef>* tab) {
+  const rs_graph* g = s->g;
+  std::vector<uint8_t> k1;
+  bind_stages(g, s->batch_idx, s->LT, s->region, &k1);
+  out->clear();
+  tab->clear();
+  auto emit = [&](const uint8_t* src, uint32_t bytes, uint32_t type) {
+    const size_t at = (out->size() + 15) & ~(size_t)15;
+    out->resize(at + bytes, 0);
+    std::memcpy(out->data() + at, src, bytes);
+    tab->push_back({at, bytes, type});
+  };
+  const uint32_t cap = g->stage_bytes;
+  for (const StageRef& r : g->stage_tab[s->batch_idx]) {
+    const uint8_t* p = k1.data() + r.off;
+    StageHdr h;
+    std::memcpy(&h, p, sizeof h);
+    if (h.type != ST_OPS) {
+      emit(p, r.bytes, r.type);
+      continue;
+    }
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(p + h.off_w);
+    const uint64_t* kk = reinterpret_cast<const uint64_t*>(p + h.off_k);
+    const uint32_t* c = reinterpret_cast<const uint32_t*>(p + h.off_c);
+    const StageRun* runs = reinterpret_cast<const StageRun*>(p + h.off_runs);
+    // records (and fold coordinate lists) per op, in stage order
+    struct Rec { uint32_t v[8]; std::vector<uint32_t> fold; };
+    std::vector<Rec> recs(h.n);
+    for (uint32_t ri = 0; ri < h.n_runs; ++ri) {
+      const StageRun& R = runs[ri];
+      const uint32_t op = R.meta & 0xffu, ar = (R.meta >> 8) & 0xffu, cls = (R.meta >> 16) & 3u;
+      for (uint32_t k = 0; k < R.count; ++k) {
+        Rec& q = recs[R.op_begin + k];
+        const uint32_t* cc = c + R.coord_begin + k * ar;
+        const uint32_t j = R.op_begin + k;
+        q.v[3] = w[j];
+        q.v[4] = ((cls << 30) | R.out_row0) + k * (s->LT << cls);
+        q.v[5] = (uint32_t)kk[j];
+        q.v[6] = (uint32_t)(kk[j] >> 32);
+        if (ar <= 3) {
+          q.v[0] = cc[0];
+          q.v[1] = ar > 1 ? cc[1] : 0u;
+          q.v[2] = ar > 2 ? cc[2] : 0u;
+          const uint32_t gs = gather_sel((int)ar, cc[0] >> 30, ar > 1 ? cc[1] >> 30 : 0u, ar > 2 ? cc[2] >> 30 : 0u);
+          q.v[7] = gs | ((uint32_t)(4 * tail_combo((int)ar, (int)op)) + cls) << 8 | op << 24;
+        } else {
+          q.fold.assign(cc, cc + ar);
+          q.v[1] = ar;
+          q.v[2] = 0;
+          q.v[7] = kTailFold << 8 | op << 24;
+        }
+      }
+    }
+    uint32_t i = 0;
+    while (i < h.n) {  // pack records (+ fold lists) into stages of at most `cap` bytes
+      const uint32_t off_rec = (uint32_t)((sizeof(StageHdr) + 15) & ~(size_t)15);
+      uint32_t n = 0, nfold = 0;
+      while (i + n < h.n) {
+        const uint32_t nf = nfold + (uint32_t)recs[i + n].fold.size();
+        if (off_rec + kRecBytes * (n + 1) + 4 * nf > cap && n > 0) break;
+        nfold = nf;
+        ++n;
+      }
+      StageHdr q{};
+      q.type = ST_OPS;
+      q.n = n;
+      q.first = h.first + i;
+      q.level = h.level;
+      q.off_c = off_rec;
+      q.bytes = (off_rec + kRecBytes * n + 4 * nfold + 15) & ~15u;
+      std::vector<uint8_t> blk(q.bytes, 0);
+      std::memcpy(blk.data(), &q, sizeof q);
+      uint32_t fo = off_rec + kRecBytes * n;
+      for (uint32_t m = 0; m < n; ++m) {
+        Rec& rr = recs[i + m];
+        if (!rr.fold.empty()) {
+          rr.v[0] = fo;  // stage-relative byte offset of the coordinate list
+          std::memcpy(blk.data() + fo, rr.fold.data(), 4 * rr.fold.size());
+          fo += 4 * (uint32_t)rr.fold.size();
+        }
+        std::memcpy(blk.data() + off_rec + kRecBytes * m, rr.v, kRecBytes);
+      }
+      emit(blk.data(), q.bytes, ST_OPS);
+      i += n;
+    }
+  }
+}
+
 // Bind the graph's schedule to the allocation and upload it; with watched
 // signals (rs_watch) a WATCH stage is spliced in before the register commit.
 rs_status upload_schedule(rs_lanes* s) {
   const rs_graph* g = s->g;
   std::vector<uint8_t> bound;
+  std::vector<StageRef> tab = g->stage_tab[s->batch_idx];
   if (s->variant == 6)
     bind_stages_b(s, &bound);
+  else if (s->variant == 7)
+    bind_stages_r(s, &bound, &tab);
   else
     bind_stages(g, s->batch_idx, s->LT, s->region, &bound);
-  std::vector<StageRef> tab = g->stage_tab[s->batch_idx];
   if (!s->watch.empty()) {
     StageHdr h{};
     h.type = ST_WATCH;
@@ -361,8 +456,8 @@ size_t lanes_smem(uint32_t stage_bytes, uint32_t threads) {
 void choose_tiling(uint32_t kernel, uint32_t n_lanes, int sms, uint32_t want_lt, uint32_t want_cs, uint32_t* lt,
                    uint32_t* cs) {
   const uint32_t k1[3] = {128u, 64u, 32u}, k2[3] = {32u, 16u, 8u}, k6[2] = {128u, 64u};
-  const uint32_t* cand = kernel == 1 ? k1 : kernel == 6 ? k6 : k2;
-  const int nc = kernel == 6 ? 2 : 3;
+  const uint32_t* cand = kernel == 1 ? k1 : (kernel == 6 || kernel == 7) ? k6 : k2;
+  const int nc = (kernel == 6 || kernel == 7) ? 2 : 3;
   const uint32_t smallest = cand[nc - 1];
   for (const uint32_t cmax : {4u, 8u}) {
     for (int i = 0; i < nc; ++i) {
@@ -662,7 +757,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     // ones kernel 1's 32 * P-lane tiles (P = 4 amortizes the per-op decode).
     const uint32_t kern = o.kernel ? o.kernel : (n_lanes < 2048u ? 2u : 1u);
     if (o.lane_tile && (kern == 2   ? (o.lane_tile != 8 && o.lane_tile != 16 && o.lane_tile != 32)
-                        : kern == 6 ? (o.lane_tile != 64 && o.lane_tile != 128)
+                        : kern >= 6 ? (o.lane_tile != 64 && o.lane_tile != 128)
                                     : (o.lane_tile != 32 && o.lane_tile != 64 && o.lane_tile != 128))) {
       rs_free_lanes(s);  // partially built: frees what exists
       return set_err(RS_E_INVALID_ARG, "lane_tile must be 32, 64 or 128 (kernel 1), 8, 16 or 32 (kernel 2) or "
@@ -672,9 +767,9 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
       rs_free_lanes(s);  // partially built: frees what exists
       return set_err(RS_E_INVALID_ARG, "cluster must be 1, 2, 4 or 8");
     }
-    if (o.kernel > 2 && o.kernel != 6) {
+    if (o.kernel > 2 && o.kernel != 6 && o.kernel != 7) {
       rs_free_lanes(s);  // partially built: frees what exists
-      return set_err(RS_E_INVALID_ARG, "lane kernel must be 0, 1, 2 or 6");
+      return set_err(RS_E_INVALID_ARG, "lane kernel must be 0, 1, 2, 6 or 7");
     }
     s->variant = kern;
     uint32_t lt, cs;
@@ -688,6 +783,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     const uint32_t tmax = g->cg.mode == RS_MODE_SINGLE ? 1024u
                           : s->variant == 1            ? (uint32_t)RS_LANES_T_MAX_THREADS
                           : s->variant == 6            ? (uint32_t)RS_LANES_B_MAX_THREADS
+                          : s->variant == 7            ? (uint32_t)RS_LANES_R_MAX_THREADS
                                                        : (uint32_t)RS_LANES_MAX_THREADS;
     if (o.threads % 32 || o.threads > tmax || o.threads < (s->variant != 2 ? 32u : s->LT)) {
       rs_free_lanes(s);
@@ -700,6 +796,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     const uint32_t per_sm = (s->n_tiles * s->cluster + g->sm_count - 1) / g->sm_count;
     const uint32_t tmax = s->variant == 1   ? (uint32_t)RS_LANES_T_MAX_THREADS
                           : s->variant == 6 ? (uint32_t)RS_LANES_B_MAX_THREADS
+                          : s->variant == 7 ? (uint32_t)RS_LANES_R_MAX_THREADS
                                             : (uint32_t)RS_LANES_MAX_THREADS;
     uint32_t th = tmax / std::max<uint32_t>(1, per_sm);
     th = std::max<uint32_t>(64, th & ~31u);
@@ -1289,7 +1386,7 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
     if (hash) s->hc_cur = 1 - s->hc_cur;
   } else {
     a.hcarry_out = a.hcarry_in;
-    const size_t smem = s->variant == 6   ? 128 + 2ull * s->g->stage_bytes + lanes_b_smem_extra(s->LT / 32)
+    const size_t smem = s->variant >= 6   ? 128 + 2ull * s->g->stage_bytes + lanes_b_smem_extra(s->LT / 32)
                         : s->variant == 1 ? 128 + 2ull * s->g->stage_bytes + lanes_t_smem_extra(s->threads, s->LT / 32)
                                           : lanes_smem(s->g->stage_bytes, s->threads);
     const void* fns[] = {(const void*)k_lanes<32, true>, (const void*)k_lanes<32, false>,
@@ -1299,7 +1396,9 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
                          (const void*)k_lanes_t<2, true>, (const void*)k_lanes_t<2, false>,
                          (const void*)k_lanes_t<4, true>, (const void*)k_lanes_t<4, false>,
                          (const void*)k_lanes_b<2, true>, (const void*)k_lanes_b<2, false>,
-                         (const void*)k_lanes_b<4, true>, (const void*)k_lanes_b<4, false>};
+                         (const void*)k_lanes_b<4, true>, (const void*)k_lanes_b<4, false>,
+                         (const void*)k_lanes_r<2, true>, (const void*)k_lanes_r<2, false>,
+                         (const void*)k_lanes_r<4, true>, (const void*)k_lanes_r<4, false>};
     // the dynamic shared-memory limit is a per-device function attribute: raise it
     // once per device to the largest size any allocation there has needed
     static thread_local size_t attr_set[64] = {};
@@ -1310,6 +1409,7 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
     }
     const int fi = (s->variant == 1   ? 6 + (s->LT == 32 ? 0 : s->LT == 64 ? 2 : 4)
                     : s->variant == 6 ? 12 + (s->LT == 64 ? 0 : 2)
+                    : s->variant == 7 ? 16 + (s->LT == 64 ? 0 : 2)
                                       : (s->LT == 32 ? 0 : s->LT == 16 ? 2 : 4)) + (hash ? 0 : 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(s->n_tiles * s->cluster);

@@ -61,7 +61,8 @@ def test_edge_circuit_covers_the_corners():
 GPU_LANE_CASES = [dict(kernel=1, lane_tile=32), dict(kernel=1, lane_tile=64), dict(kernel=1, lane_tile=128),
                   dict(kernel=1, lane_tile=64, cluster=2), dict(kernel=2, lane_tile=8),
                   dict(kernel=2, lane_tile=16), dict(kernel=2, lane_tile=32, cluster=2),
-                  dict(kernel=6, lane_tile=64), dict(kernel=6, lane_tile=128), dict(kernel=6, lane_tile=128, cluster=2)]
+                  dict(kernel=6, lane_tile=64), dict(kernel=6, lane_tile=128), dict(kernel=6, lane_tile=128, cluster=2),
+                  dict(kernel=7, lane_tile=64), dict(kernel=7, lane_tile=128), dict(kernel=7, lane_tile=128, cluster=2)]
 
 
 @pytest.mark.gpu
@@ -116,7 +117,7 @@ def test_gpu_edges_seeded_stimulus_all_kernels(rs):
     so wide selectors are mostly nonzero -- the complement of the staged mix."""
     c = edge_circuit(2)
     r = oracle.simulate(c, 8, seed=99, lane0=0, n_lanes=70, final=True)
-    for kernel in (1, 2, 6):
+    for kernel in (1, 2, 6, 7):
         g = rs.Graph(c, device=0)
         L = rs.Lanes(g, 70, kernel=kernel)
         L.set_seed(99)

@@ -88,7 +88,7 @@ def test_c1_full(rs, mode, kernel):
 @pytest.mark.parametrize("kernel,lt,cs", [(2, 8, 1), (2, 16, 1), (2, 32, 1), (2, 32, 4), (2, 16, 2), (2, 8, 8),
                                           (1, 32, 1), (1, 64, 1), (1, 128, 1), (1, 32, 4), (1, 64, 2),
                                           (1, 128, 8), (6, 64, 1), (6, 128, 1), (6, 64, 2), (6, 128, 4),
-                                          (6, 128, 8)])
+                                          (6, 128, 8), (7, 64, 1), (7, 128, 1), (7, 64, 2), (7, 128, 4)])
 def test_c2_structure_ragged_lanes(rs, lt, cs, kernel):
     """Full C2 circuit, 37 lanes (ragged last tile), 25 cycles, each lane tile,
     one CTA or a thread-block cluster per tile, both lane kernels."""
@@ -104,9 +104,10 @@ def test_c2_threads_variants(rs):
         check(rs, c, 12, 70, seed=7, threads=th, lane_tile=64, kernel=1)
     for th in (32, 160, 768):
         check(rs, c, 12, 200, seed=7, threads=th, lane_tile=128, kernel=6)
+        check(rs, c, 12, 200, seed=7, threads=th, lane_tile=128, kernel=7)
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 6])
+@pytest.mark.parametrize("kernel", [1, 2, 6, 7])
 def test_c3_structure(rs, kernel):
     check(rs, config_circuit("C3"), 6, 40, seed=CONFIGS["C3"].stim_seed, kernel=kernel)
 
@@ -122,7 +123,7 @@ def test_fuzz_corpus(rs):
     wide folds, permuted ids; 60 cycles, both modes."""
     for seed in range(200):
         c = fuzz_circuit(seed)
-        check(rs, c, 60, 3, seed=seed, kernel=(1, 2, 6)[seed % 3])
+        check(rs, c, 60, 3, seed=seed, kernel=(1, 2, 6, 7)[seed % 4])
         if seed % 4 == 0:
             check(rs, c, 60, 1, seed=seed, mode="single", kernel=5 if seed % 8 else 0)
 
@@ -149,7 +150,7 @@ def test_closed_forms_on_gpu(rs):
     check(rs, c, 40, 1, staged=vals)
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 6])
+@pytest.mark.parametrize("kernel", [1, 2, 6, 7])
 def test_chunking_and_hash_toggle(rs, kernel):
     c = config_circuit("C2", n_ops=4000, n_levels=20, n_regs=400)
     g = rs.Graph(c)
@@ -167,7 +168,7 @@ def test_chunking_and_hash_toggle(rs, kernel):
     assert L.cycle == 21
 
 
-@pytest.mark.parametrize("kernel", [1, 6])
+@pytest.mark.parametrize("kernel", [1, 6, 7])
 @pytest.mark.parametrize("cluster", [1, 2])
 def test_wide_work_items(rs, cluster, kernel):
     """Kernels 1 and 6 with kBatchWide-op work items (>= 2,048 ops per CTA and
@@ -176,7 +177,8 @@ def test_wide_work_items(rs, cluster, kernel):
     check(rs, c, 5, 70, seed=9, kernel=kernel, lane_tile=64, cluster=cluster)
 
 
-@pytest.mark.parametrize("mode,kernel", [("lanes", 1), ("lanes", 2), ("lanes", 6), ("single", 0), ("single", 5)])
+@pytest.mark.parametrize("mode,kernel", [("lanes", 1), ("lanes", 2), ("lanes", 6), ("lanes", 7), ("single", 0),
+                                         ("single", 5)])
 def test_staged_inputs_pipelined(rs, mode, kernel):
     """The next chunk is staged (copy stream) before the current one is stepped,
     with a ring of two chunks: every copy must wait for the launch that last
@@ -221,7 +223,7 @@ def test_staged_inputs_from_device_stream(rs):
     assert np.array_equal(H, r.hashes)
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 6])
+@pytest.mark.parametrize("kernel", [1, 2, 6, 7])
 def test_staged_inputs_chunks(rs, kernel):
     c = config_circuit("C2", n_ops=3000, n_levels=15, n_regs=300)
     rng = np.random.default_rng(3)
@@ -240,7 +242,7 @@ def test_staged_inputs_chunks(rs, kernel):
     assert e.value.name == "RS_E_STATE"
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 6])
+@pytest.mark.parametrize("kernel", [1, 2, 6, 7])
 def test_checkpoint_restore(rs, kernel):
     c = config_circuit("C2", n_ops=3000, n_levels=15, n_regs=300)
     full = oracle.simulate(c, 20, seed=5, n_lanes=24)
@@ -249,7 +251,7 @@ def test_checkpoint_restore(rs, kernel):
     a.set_seed(5)
     h0 = a.step(10, hashes="host")
     regs = a.read(c.reg_id)
-    b = rs.Lanes(g, 24, kernel={1: 2, 2: 6, 6: 1}[kernel])   # restored into another lane kernel's layout
+    b = rs.Lanes(g, 24, kernel={1: 2, 2: 6, 6: 7, 7: 1}[kernel])   # restored into another lane kernel's layout
     b.set_seed(5)
     b.write_registers(c.reg_id, regs)
     b.cycle = 10
@@ -274,6 +276,8 @@ def test_lane_sharding_invariance(rs):
     assert np.array_equal(Hb, Hc) and np.array_equal(Fb, Fc)
     Hd, Fd, _ = run_gpu(rs, c, 15, 37, seed=9, lane0=37, kernel=6)
     assert np.array_equal(Hb, Hd) and np.array_equal(Fb, Fd)
+    He, Fe, _ = run_gpu(rs, c, 15, 37, seed=9, lane0=37, kernel=7)
+    assert np.array_equal(Hb, He) and np.array_equal(Fb, Fe)
 
 
 def test_error_statuses(rs):
@@ -367,7 +371,7 @@ def test_auto_kernel_choice(rs):
         assert np.array_equal(h[:, [0, L.n_lanes - 1]], r.hashes)
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 6])
+@pytest.mark.parametrize("kernel", [1, 2, 6, 7])
 def test_waveform_changes(rs, kernel):
     """Waveform capture (rs_watch): the fused per-cycle change
     records equal the change set of the oracle's per-cycle trace of the same
@@ -456,7 +460,7 @@ def test_watch_errors(rs):
 
 
 @pytest.mark.parametrize("policy", [1, 2])
-@pytest.mark.parametrize("kernel", [1, 2, 6])
+@pytest.mark.parametrize("kernel", [1, 2, 6, 7])
 def test_l2_policy_results_identical(rs, policy, kernel):
     """rs_lane_opts.l2_policy (access-policy window over the schedule / the state) changes
     speed only."""
@@ -464,7 +468,7 @@ def test_l2_policy_results_identical(rs, policy, kernel):
     check(rs, c, 8, 150, seed=4, kernel=kernel, l2_policy=policy)
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 6])
+@pytest.mark.parametrize("kernel", [1, 2, 6, 7])
 def test_caller_owned_state(rs, kernel):
     """rs_lane_opts.defer_state + rs_lanes_bind_state (SURVEY.md §8(b) torch-owned memory):
     the signal state lives in a torch tensor; results equal the oracle's, and the library

@@ -45,7 +45,8 @@ def test_passes_on_the_c3_recipe(rs):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode,kernel", [("lanes", 1), ("lanes", 2), ("lanes", 6), ("single", 3), ("single", 5)])
+@pytest.mark.parametrize("mode,kernel", [("lanes", 1), ("lanes", 2), ("lanes", 6), ("lanes", 7), ("single", 3),
+                                         ("single", 5)])
 @pytest.mark.parametrize("seed", [0, 1, 2])
 def test_gpu_passes_parity(rs, mode, kernel, seed):
     c = pass_circuit(seed)
