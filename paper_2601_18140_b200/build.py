@@ -18,7 +18,7 @@ LIB = os.path.join(LIBDIR, "librtlsim.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = ["runtime.cu", "compiler.cpp", "passes.cpp"]
-HEADERS = ["kernels.cuh", "lanes.cuh", "lanes_t.cuh", "gather_brx.cuh", "lanes_b.cuh", "gather_b.cuh", "lanes_r.cuh", "gather_r.cuh", "single.cuh", "repcut.cuh", "compiler.hpp"]
+HEADERS = ["kernels.cuh", "lanes.cuh", "lanes_t.cuh", "gather_brx.cuh", "lanes_b.cuh", "gather_b.cuh", "lanes_r.cuh", "single.cuh", "repcut.cuh", "compiler.hpp"]
 
 
 def _newest_input() -> float:

@@ -5,16 +5,15 @@
 // but the level's op tensor is staged as one 32-byte RECORD per op, prepared at bind
 // time (runtime.cu bind_stages_r):
 //   {c0, c1, c2, pw, out coordinate, K lo, K hi, sel}
-// sel = gather selector (arity and operand class signature, one jump table over every
-// arity: gather_r.cuh) | tail index << 8 (opcode, arity, out class: one specialised
-// compute / mask / hash / store tail).  The warps of the cluster split a stage's ops
+// sel = tail index << 8 (opcode, arity, out class: one specialised compute / mask /
+// hash / store tail) | arity << 16 | opcode << 24; the operands are gathered through the
+// per-arity class-signature jump tables of gather_brx.cuh.  The warps of the cluster split a stage's ops
 // into contiguous ranges; per op a warp issues two shared-memory vector loads, one
 // jump into the gather, one into the tail -- no run / work-item decode, no per-op
 // address recomputation (the Format-c runs of P:1123-1129 survive as the record order).
 // Results <= 32 bits are computed, masked and hashed in 32-bit arithmetic.  The hash
 // partials are summed with shared-memory atomics (as lanes_b.cuh).
 #pragma once
-#include "gather_r.cuh"
 #include "lanes_b.cuh"
 
 #ifndef RS_LANES_R_MAX_THREADS
@@ -37,16 +36,10 @@ __host__ __device__ constexpr uint32_t gather_sel(int A, uint32_t c0, uint32_t c
   return A == 1 ? c0 : A == 2 ? 4 + c0 + 4 * c1 : 20 + c0 + 4 * c1 + 16 * c2;
 }
 
-template <int P>
-__device__ __forceinline__ void gather_r(const LaneT& L, uint32_t g, uint32_t c0, uint32_t c1, uint32_t c2,
-                                         uint64_t (&x)[3][P]) {
-  if constexpr (P == 2) gatherr_p2(g, L.p0, L.p1, L.p2, L.p3, c0, c1, c2, x);
-  else gatherr_p4(g, L.p0, L.p1, L.p2, L.p3, c0, c1, c2, x);
-}
 
 // One op's tail: compute, mask to w_out, hash, store (out class OC, lanes_t layout).
 template <int P, bool HASH, int A, int OP, int OC>
-__device__ __forceinline__ void tail_r(const LaneT& L, const uint64_t (&x)[3][P], uint32_t pw, uint32_t oc,
+__device__ __forceinline__ void tail_r(const LaneT& L, const uint64_t (&x)[A][P], uint32_t pw, uint32_t oc,
                                        uint64_t K, uint64_t (&hacc)[P]) {
   if constexpr (OC == 3) {
 #pragma unroll
@@ -103,14 +96,16 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
   return v;
 }
 
-// OPS stage: records at buf + off_c (h->n of them); this warp takes ops [b, e).
+// OPS stage: records at buf + off_c (h->n of them); this warp takes ops j0, j0 + nw,
+// ... -- interleaved across the runs, so every warp gets the same mix of cheap and
+// expensive ops and the stage barrier waits for nobody in particular.
 template <int P, bool HASH>
-__device__ __forceinline__ void stage_ops_r(const LaneT& L, const uint8_t* buf, uint32_t b, uint32_t e,
+__device__ __forceinline__ void stage_ops_r(const LaneT& L, const uint8_t* buf, uint32_t j0, uint32_t nw,
                                             uint64_t (&hacc)[P]) {
   const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
-  const uint32_t base = smem_addr(buf), rec0 = base + h->off_c;
+  const uint32_t base = smem_addr(buf), rec0 = base + h->off_c, n = h->n;
 #pragma unroll 1
-  for (uint32_t j = b; j < e; ++j) {
+  for (uint32_t j = j0; j < n; j += nw) {
     const uint4 r0 = lds128(rec0 + kRecBytes * j), r1 = lds128(rec0 + kRecBytes * j + 16);
     const uint32_t pw = r0.w, oc = r1.x, sel = r1.w, t = (sel >> 8) & 0xffu;
     const uint64_t K = HASH ? ((uint64_t)r1.z << 32 | r1.y) : 0ull;
@@ -118,21 +113,42 @@ __device__ __forceinline__ void stage_ops_r(const LaneT& L, const uint8_t* buf, 
       fold_r<P, HASH>(L, base + r0.x, r0.y, sel >> 24, pw, oc, K, hacc);
       continue;
     }
-    uint64_t x[3][P];
-    gather_r<P>(L, sel & 0xffu, r0.x, r0.y, r0.z, x);
-#define RS_R4(C, A, OPC)                                                      \
-  case 4 * C + 0: tail_r<P, HASH, A, OPC, 0>(L, x, pw, oc, K, hacc); break;   \
-  case 4 * C + 1: tail_r<P, HASH, A, OPC, 1>(L, x, pw, oc, K, hacc); break;   \
-  case 4 * C + 2: tail_r<P, HASH, A, OPC, 2>(L, x, pw, oc, K, hacc); break;   \
-  case 4 * C + 3: tail_r<P, HASH, A, OPC, 3>(L, x, pw, oc, K, hacc); break;
-    switch (t) {
-      RS_R4(0, 1, RS_OP_NOT) RS_R4(1, 1, RS_OP_SHL) RS_R4(2, 1, RS_OP_SHR) RS_R4(3, 1, RS_OP_BITS) RS_R4(4, 1, OP_COPY)
-      RS_R4(5, 2, RS_OP_AND) RS_R4(6, 2, RS_OP_OR) RS_R4(7, 2, RS_OP_XOR) RS_R4(8, 2, RS_OP_ADD)
-      RS_R4(9, 2, RS_OP_SUB) RS_R4(10, 2, RS_OP_MUL) RS_R4(11, 2, RS_OP_EQ) RS_R4(12, 2, RS_OP_LT)
-      RS_R4(13, 2, RS_OP_CAT)
-      RS_R4(14, 3, RS_OP_AND) RS_R4(15, 3, RS_OP_OR) RS_R4(16, 3, RS_OP_XOR) RS_R4(17, 3, RS_OP_ADD)
-      RS_R4(18, 3, RS_OP_SUB) RS_R4(19, 3, RS_OP_MUL) RS_R4(20, 3, RS_OP_MUX)
-      default: break;
+    const uint32_t A = (sel >> 16) & 3u;
+#define RS_R4(C, AA, OPC)                                                      \
+  case 4 * C + 0: tail_r<P, HASH, AA, OPC, 0>(L, x, pw, oc, K, hacc); break;   \
+  case 4 * C + 1: tail_r<P, HASH, AA, OPC, 1>(L, x, pw, oc, K, hacc); break;   \
+  case 4 * C + 2: tail_r<P, HASH, AA, OPC, 2>(L, x, pw, oc, K, hacc); break;   \
+  case 4 * C + 3: tail_r<P, HASH, AA, OPC, 3>(L, x, pw, oc, K, hacc); break;
+    // one gather per arity (the class-signature jump tables of gather_brx.cuh), so an op
+    // holds only its own operands' registers
+    if (A == 2) {
+      const uint32_t c[2] = {r0.x, r0.y};
+      uint64_t x[2][P];
+      gather_t<2, P>(L, c, x);
+      switch (t) {
+        RS_R4(5, 2, RS_OP_AND) RS_R4(6, 2, RS_OP_OR) RS_R4(7, 2, RS_OP_XOR) RS_R4(8, 2, RS_OP_ADD)
+        RS_R4(9, 2, RS_OP_SUB) RS_R4(10, 2, RS_OP_MUL) RS_R4(11, 2, RS_OP_EQ) RS_R4(12, 2, RS_OP_LT)
+        RS_R4(13, 2, RS_OP_CAT)
+        default: break;
+      }
+    } else if (A == 1) {
+      const uint32_t c[1] = {r0.x};
+      uint64_t x[1][P];
+      gather_t<1, P>(L, c, x);
+      switch (t) {
+        RS_R4(0, 1, RS_OP_NOT) RS_R4(1, 1, RS_OP_SHL) RS_R4(2, 1, RS_OP_SHR) RS_R4(3, 1, RS_OP_BITS)
+        RS_R4(4, 1, OP_COPY)
+        default: break;
+      }
+    } else {
+      const uint32_t c[3] = {r0.x, r0.y, r0.z};
+      uint64_t x[3][P];
+      gather_t<3, P>(L, c, x);
+      switch (t) {
+        RS_R4(14, 3, RS_OP_AND) RS_R4(15, 3, RS_OP_OR) RS_R4(16, 3, RS_OP_XOR) RS_R4(17, 3, RS_OP_ADD)
+        RS_R4(18, 3, RS_OP_SUB) RS_R4(19, 3, RS_OP_MUL) RS_R4(20, 3, RS_OP_MUX)
+        default: break;
+      }
     }
 #undef RS_R4
   }
@@ -196,7 +212,7 @@ __global__ void __launch_bounds__(RS_LANES_R_MAX_THREADS, 1) k_lanes_r(const Ste
     uint32_t b, e;
     chunk_of(h->n, gw, ngw, b, e);
     if (type == ST_OPS) {
-      if (b < e) stage_ops_r<P, HASH>(L, buf, b, e, hacc);
+      stage_ops_r<P, HASH>(L, buf, gw, ngw, hacc);
     } else if (type == ST_LATCH) {
       if (b < e) {
         const uint32_t base = smem_addr(buf);

@@ -168,6 +168,8 @@ struct rs_lanes {
 
 namespace {
 
+// kernel 7 stage buffers: a C3 level's op records (~1,650 x 32 B) fit one stage
+constexpr uint32_t kStageBytesR = 96 * 1024;
 constexpr size_t kBarBytes = 1024;      // partition k's grid barrier at u64 [4k]; level-cut flags at [kFlagOffset + k]
 constexpr size_t kFlagOffset = 64;
 
@@ -191,7 +193,7 @@ StepArgs base_args(const rs_lanes* s) {
   a.stage_blob = s->stage_blob;
   a.stage_tab = s->stage_tab;
   a.n_stages = s->n_stages;
-  a.stage_bytes = s->g->stage_bytes;
+  a.stage_bytes = s->variant == 7 ? kStageBytesR : s->g->stage_bytes;
   a.trace = s->trace;
   a.cluster = s->cluster;
   a.wave_prev = s->wave_prev;
@@ -292,52 +294,17 @@ void bind_stages_r(const rs_lanes* s, std::vector<uint8_t>* out, std::vector<Sta
     std::memcpy(out->data() + at, src, bytes);
     tab->push_back({at, bytes, type});
   };
-  const uint32_t cap = g->stage_bytes;
-  for (const StageRef& r : g->stage_tab[s->batch_idx]) {
-    const uint8_t* p = k1.data() + r.off;
-    StageHdr h;
-    std::memcpy(&h, p, sizeof h);
-    if (h.type != ST_OPS) {
-      emit(p, r.bytes, r.type);
-      continue;
-    }
-    const uint32_t* w = reinterpret_cast<const uint32_t*>(p + h.off_w);
-    const uint64_t* kk = reinterpret_cast<const uint64_t*>(p + h.off_k);
-    const uint32_t* c = reinterpret_cast<const uint32_t*>(p + h.off_c);
-    const StageRun* runs = reinterpret_cast<const StageRun*>(p + h.off_runs);
-    // records (and fold coordinate lists) per op, in stage order
-    struct Rec { uint32_t v[8]; std::vector<uint32_t> fold; };
-    std::vector<Rec> recs(h.n);
-    for (uint32_t ri = 0; ri < h.n_runs; ++ri) {
-      const StageRun& R = runs[ri];
-      const uint32_t op = R.meta & 0xffu, ar = (R.meta >> 8) & 0xffu, cls = (R.meta >> 16) & 3u;
-      for (uint32_t k = 0; k < R.count; ++k) {
-        Rec& q = recs[R.op_begin + k];
-        const uint32_t* cc = c + R.coord_begin + k * ar;
-        const uint32_t j = R.op_begin + k;
-        q.v[3] = w[j];
-        q.v[4] = ((cls << 30) | R.out_row0) + k * (s->LT << cls);
-        q.v[5] = (uint32_t)kk[j];
-        q.v[6] = (uint32_t)(kk[j] >> 32);
-        if (ar <= 3) {
-          q.v[0] = cc[0];
-          q.v[1] = ar > 1 ? cc[1] : 0u;
-          q.v[2] = ar > 2 ? cc[2] : 0u;
-          const uint32_t gs = gather_sel((int)ar, cc[0] >> 30, ar > 1 ? cc[1] >> 30 : 0u, ar > 2 ? cc[2] >> 30 : 0u);
-          q.v[7] = gs | ((uint32_t)(4 * tail_combo((int)ar, (int)op)) + cls) << 8 | op << 24;
-        } else {
-          q.fold.assign(cc, cc + ar);
-          q.v[1] = ar;
-          q.v[2] = 0;
-          q.v[7] = kTailFold << 8 | op << 24;
-        }
-      }
-    }
+  const uint32_t cap = kStageBytesR;
+  struct Rec { uint32_t v[8]; std::vector<uint32_t> fold; };
+  std::vector<Rec> recs;   // the current level's records (kernel-1 OPS stages of one level merged)
+  uint32_t rec_level = 0, rec_first = 0;
+  auto flush = [&]() {
     uint32_t i = 0;
-    while (i < h.n) {  // pack records (+ fold lists) into stages of at most `cap` bytes
+    const uint32_t total_n = (uint32_t)recs.size();
+    while (i < total_n) {  // pack records (+ fold lists) into stages of at most `cap` bytes
       const uint32_t off_rec = (uint32_t)((sizeof(StageHdr) + 15) & ~(size_t)15);
       uint32_t n = 0, nfold = 0;
-      while (i + n < h.n) {
+      while (i + n < total_n) {
         const uint32_t nf = nfold + (uint32_t)recs[i + n].fold.size();
         if (off_rec + kRecBytes * (n + 1) + 4 * nf > cap && n > 0) break;
         nfold = nf;
@@ -346,8 +313,8 @@ void bind_stages_r(const rs_lanes* s, std::vector<uint8_t>* out, std::vector<Sta
       StageHdr q{};
       q.type = ST_OPS;
       q.n = n;
-      q.first = h.first + i;
-      q.level = h.level;
+      q.first = rec_first + i;
+      q.level = rec_level;
       q.off_c = off_rec;
       q.bytes = (off_rec + kRecBytes * n + 4 * nfold + 15) & ~15u;
       std::vector<uint8_t> blk(q.bytes, 0);
@@ -365,7 +332,54 @@ void bind_stages_r(const rs_lanes* s, std::vector<uint8_t>* out, std::vector<Sta
       emit(blk.data(), q.bytes, ST_OPS);
       i += n;
     }
+    recs.clear();
+  };
+  for (const StageRef& r : g->stage_tab[s->batch_idx]) {
+    const uint8_t* p = k1.data() + r.off;
+    StageHdr h;
+    std::memcpy(&h, p, sizeof h);
+    if (h.type != ST_OPS || (!recs.empty() && h.level != rec_level)) flush();
+    if (h.type != ST_OPS) {
+      emit(p, r.bytes, r.type);
+      continue;
+    }
+    if (recs.empty()) {
+      rec_level = h.level;
+      rec_first = h.first;
+    }
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(p + h.off_w);
+    const uint64_t* kk = reinterpret_cast<const uint64_t*>(p + h.off_k);
+    const uint32_t* c = reinterpret_cast<const uint32_t*>(p + h.off_c);
+    const StageRun* runs = reinterpret_cast<const StageRun*>(p + h.off_runs);
+    // records (and fold coordinate lists) per op, in stage order
+    const size_t rb = recs.size();
+    recs.resize(rb + h.n);
+    for (uint32_t ri = 0; ri < h.n_runs; ++ri) {
+      const StageRun& R = runs[ri];
+      const uint32_t op = R.meta & 0xffu, ar = (R.meta >> 8) & 0xffu, cls = (R.meta >> 16) & 3u;
+      for (uint32_t k = 0; k < R.count; ++k) {
+        Rec& q = recs[rb + R.op_begin + k];
+        const uint32_t* cc = c + R.coord_begin + k * ar;
+        const uint32_t j = R.op_begin + k;
+        q.v[3] = w[j];
+        q.v[4] = ((cls << 30) | R.out_row0) + k * (s->LT << cls);
+        q.v[5] = (uint32_t)kk[j];
+        q.v[6] = (uint32_t)(kk[j] >> 32);
+        if (ar <= 3) {
+          q.v[0] = cc[0];
+          q.v[1] = ar > 1 ? cc[1] : 0u;
+          q.v[2] = ar > 2 ? cc[2] : 0u;
+          q.v[7] = ((uint32_t)(4 * tail_combo((int)ar, (int)op)) + cls) << 8 | ar << 16 | op << 24;
+        } else {
+          q.fold.assign(cc, cc + ar);
+          q.v[1] = ar;
+          q.v[2] = 0;
+          q.v[7] = kTailFold << 8 | op << 24;
+        }
+      }
+    }
   }
+  flush();
 }
 
 // Bind the graph's schedule to the allocation and upload it; with watched
@@ -1386,7 +1400,8 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
     if (hash) s->hc_cur = 1 - s->hc_cur;
   } else {
     a.hcarry_out = a.hcarry_in;
-    const size_t smem = s->variant >= 6   ? 128 + 2ull * s->g->stage_bytes + lanes_b_smem_extra(s->LT / 32)
+    const size_t smem = s->variant == 7   ? 128 + 2ull * kStageBytesR + lanes_b_smem_extra(s->LT / 32)
+                        : s->variant == 6 ? 128 + 2ull * s->g->stage_bytes + lanes_b_smem_extra(s->LT / 32)
                         : s->variant == 1 ? 128 + 2ull * s->g->stage_bytes + lanes_t_smem_extra(s->threads, s->LT / 32)
                                           : lanes_smem(s->g->stage_bytes, s->threads);
     const void* fns[] = {(const void*)k_lanes<32, true>, (const void*)k_lanes<32, false>,
