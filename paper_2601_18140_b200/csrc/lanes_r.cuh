@@ -90,6 +90,27 @@ __device__ __forceinline__ void fold_r(const LaneT& L, uint32_t s_list, uint32_t
   store_t<P>(L, oc, r);
 }
 
+// The tail of a 1- or 2-operand op whose operands were gathered two-operand wide.
+template <int P, bool HASH>
+__device__ __forceinline__ void tail_pair(const LaneT& L, const uint64_t (&x)[2][P], uint32_t pw, uint32_t oc,
+                                          uint64_t K, uint32_t t, uint64_t (&hacc)[P]) {
+  const uint64_t(&x1)[1][P] = reinterpret_cast<const uint64_t(&)[1][P]>(x);
+#define RS_P4(C, AA, XX, OPC)                                                   \
+  case 4 * C + 0: tail_r<P, HASH, AA, OPC, 0>(L, XX, pw, oc, K, hacc); break;   \
+  case 4 * C + 1: tail_r<P, HASH, AA, OPC, 1>(L, XX, pw, oc, K, hacc); break;   \
+  case 4 * C + 2: tail_r<P, HASH, AA, OPC, 2>(L, XX, pw, oc, K, hacc); break;   \
+  case 4 * C + 3: tail_r<P, HASH, AA, OPC, 3>(L, XX, pw, oc, K, hacc); break;
+  switch (t) {
+    RS_P4(0, 1, x1, RS_OP_NOT) RS_P4(1, 1, x1, RS_OP_SHL) RS_P4(2, 1, x1, RS_OP_SHR) RS_P4(3, 1, x1, RS_OP_BITS)
+    RS_P4(4, 1, x1, OP_COPY)
+    RS_P4(5, 2, x, RS_OP_AND) RS_P4(6, 2, x, RS_OP_OR) RS_P4(7, 2, x, RS_OP_XOR) RS_P4(8, 2, x, RS_OP_ADD)
+    RS_P4(9, 2, x, RS_OP_SUB) RS_P4(10, 2, x, RS_OP_MUL) RS_P4(11, 2, x, RS_OP_EQ) RS_P4(12, 2, x, RS_OP_LT)
+    RS_P4(13, 2, x, RS_OP_CAT)
+    default: break;
+  }
+#undef RS_P4
+}
+
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
   uint4 v;
   asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
@@ -104,8 +125,27 @@ __device__ __forceinline__ void stage_ops_r(const LaneT& L, const uint8_t* buf, 
                                             uint64_t (&hacc)[P]) {
   const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
   const uint32_t base = smem_addr(buf), rec0 = base + h->off_c, n = h->n;
+  uint32_t j = j0;
+#ifndef RS_NO_PAIRS
+  // pairs of ops with <= 2 operands: both ops' loads are in flight before either is
+  // computed (the PSU partial unrolling, for memory-level parallelism); a
+  // one-operand op is gathered as two-operand (its operand twice) so one path serves both
 #pragma unroll 1
-  for (uint32_t j = j0; j < n; j += nw) {
+  for (; j + nw < n; j += 2 * nw) {
+    const uint4 a0 = lds128(rec0 + kRecBytes * j), a1 = lds128(rec0 + kRecBytes * j + 16);
+    const uint4 b0 = lds128(rec0 + kRecBytes * (j + nw)), b1 = lds128(rec0 + kRecBytes * (j + nw) + 16);
+    const uint32_t aA = (a1.w >> 16) & 3u, bA = (b1.w >> 16) & 3u;
+    if (aA == 0u || aA == 3u || bA == 0u || bA == 3u) break;  // a fold or a 3-operand op: single path
+    const uint32_t ca[2] = {a0.x, aA == 2u ? a0.y : a0.x}, cb[2] = {b0.x, bA == 2u ? b0.y : b0.x};
+    uint64_t xa[2][P], xb[2][P];
+    gather_t<2, P>(L, ca, xa);
+    gather_t<2, P>(L, cb, xb);
+    tail_pair<P, HASH>(L, xa, a0.w, a1.x, HASH ? ((uint64_t)a1.z << 32 | a1.y) : 0ull, (a1.w >> 8) & 0xffu, hacc);
+    tail_pair<P, HASH>(L, xb, b0.w, b1.x, HASH ? ((uint64_t)b1.z << 32 | b1.y) : 0ull, (b1.w >> 8) & 0xffu, hacc);
+  }
+#endif
+#pragma unroll 1
+  for (; j < n; j += nw) {
     const uint4 r0 = lds128(rec0 + kRecBytes * j), r1 = lds128(rec0 + kRecBytes * j + 16);
     const uint32_t pw = r0.w, oc = r1.x, sel = r1.w, t = (sel >> 8) & 0xffu;
     const uint64_t K = HASH ? ((uint64_t)r1.z << 32 | r1.y) : 0ull;

@@ -299,6 +299,12 @@ void bind_stages_r(const rs_lanes* s, std::vector<uint8_t>* out, std::vector<Sta
   std::vector<Rec> recs;   // the current level's records (kernel-1 OPS stages of one level merged)
   uint32_t rec_level = 0, rec_first = 0;
   auto flush = [&]() {
+    // ops with <= 2 operands first: the kernel evaluates them in pairs (lanes_r.cuh);
+    // every record carries its own output coordinate, so the order is free
+    std::stable_partition(recs.begin(), recs.end(), [](const Rec& r) {
+      const uint32_t ar = (r.v[7] >> 16) & 3u;
+      return ((r.v[7] >> 8) & 0xffu) != kTailFold && ar >= 1u && ar <= 2u;
+    });
     uint32_t i = 0;
     const uint32_t total_n = (uint32_t)recs.size();
     while (i < total_n) {  // pack records (+ fold lists) into stages of at most `cap` bytes
