@@ -370,7 +370,8 @@ def main():
     value = all_lane_cycles / (total_ms / 1e3)
 
     kid = L.shape()["kernel"]
-    kernel_name = {1: "k_lanes_t", 2: "k_lanes", 3: "k_repcut_smem", 4: "k_repcut", 5: "k_single2"}.get(kid, "?")
+    kernel_name = {1: "k_lanes_t", 2: "k_lanes", 3: "k_repcut_smem", 4: "k_repcut", 5: "k_single2", 6: "k_lanes_b",
+                   7: "k_lanes_r"}.get(kid, "?")
     # roofline of the dominant (only) kernel: algorithmic bytes per launch / launch duration
     # (this rank's launch; the max-over-ranks time)
     bytes_per_cycle = lanes * info["alg_bytes_per_lane_cycle"] + info["graph_alg_bytes"]

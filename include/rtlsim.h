@@ -146,12 +146,15 @@ typedef struct {
                               one cooperative launch.  RS_E_CAPACITY if the slices do not fit
                               co-resident, RS_E_INVALID_ARG if parts > n_levels or > 8. */
   uint32_t kernel;         /* RS_MODE_LANES step kernel (results identical): 0 = auto (2 below 2048
-                              lanes, else 1); 1 = tile-interleaved: tile = 32 * P lanes (P = 1, 2, 4),
+                              lanes, else 7); 1 = tile-interleaved: tile = 32 * P lanes (P = 1, 2, 4),
                               thread t owns lanes t + 32k, one op per warp, operand container widths
                               dispatched once per op through a jump table on the class signature;
                               2 = two adjacent lanes per thread, 8/16/32-lane tiles, aligned 64-bit
-                              word gathers + extraction.  lane_tile must match (32/64/128 for 1,
-                              8/16/32 for 2).  RS_E_INVALID_ARG otherwise.
+                              word gathers + extraction; 6 = kernel 1's tiles with the 1-bit signals as
+                              bit planes (32 lanes per word); 7 = kernel 1's
+                              tiles driven by 32-byte per-op records (one jump into the gather, one
+                              into an (opcode, arity, out class) tail).  lane_tile must match (32/64/128
+                              for 1, 8/16/32 for 2, 64/128 for 6 and 7).  RS_E_INVALID_ARG otherwise.
                               RS_MODE_SINGLE: 0 = auto (RepCut with one partition when the whole design
                               fits one SM's shared memory, else the level-synchronous grid); 3 = RepCut,
                               shared-memory slices; 4 = RepCut, global replicas; 5 = level-synchronous

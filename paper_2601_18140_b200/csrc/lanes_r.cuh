@@ -126,10 +126,10 @@ __device__ __forceinline__ void stage_ops_r(const LaneT& L, const uint8_t* buf, 
   const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
   const uint32_t base = smem_addr(buf), rec0 = base + h->off_c, n = h->n;
   uint32_t j = j0;
-#ifndef RS_NO_PAIRS
-  // pairs of ops with <= 2 operands: both ops' loads are in flight before either is
-  // computed (the PSU partial unrolling, for memory-level parallelism); a
-  // one-operand op is gathered as two-operand (its operand twice) so one path serves both
+#ifdef RS_PAIRS
+  // (opt-in build, measured slower on C3: 1.29 vs 1.23 ms per cycle) pairs of ops with
+  // <= 2 operands: both ops' loads are in flight before either is computed (the PSU
+  // partial unrolling); a one-operand op is gathered as two-operand
 #pragma unroll 1
   for (; j + nw < n; j += 2 * nw) {
     const uint4 a0 = lds128(rec0 + kRecBytes * j), a1 = lds128(rec0 + kRecBytes * j + 16);

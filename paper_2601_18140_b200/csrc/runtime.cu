@@ -775,7 +775,9 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     // auto: lane-poor allocations (< 2048 lanes: per-level work per SM is a few
     // hundred lane-ops, latency-bound) take kernel 2's 8..32-lane tiles; lane-rich
     // ones kernel 1's 32 * P-lane tiles (P = 4 amortizes the per-op decode).
-    const uint32_t kern = o.kernel ? o.kernel : (n_lanes < 2048u ? 2u : 1u);
+    // (kernel 7, the record-based tile kernel, measured fastest at >= 2048 lanes: C3 1.23 vs
+    // 1.30 ms per cycle for kernel 1, C4 31.6 vs 34.8 ms; profiles/r02)
+    const uint32_t kern = o.kernel ? o.kernel : (n_lanes < 2048u ? 2u : 7u);
     if (o.lane_tile && (kern == 2   ? (o.lane_tile != 8 && o.lane_tile != 16 && o.lane_tile != 32)
                         : kern >= 6 ? (o.lane_tile != 64 && o.lane_tile != 128)
                                     : (o.lane_tile != 32 && o.lane_tile != 64 && o.lane_tile != 128))) {

@@ -357,13 +357,13 @@ def test_c4_c5_full_size_sampled(rs):
 
 
 def test_auto_kernel_choice(rs):
-    """rs_lane_opts.kernel = 0: kernel 2 below 2048 lanes, kernel 1 (32 * P-lane tiles) above."""
+    """rs_lane_opts.kernel = 0: kernel 2 below 2048 lanes, kernel 7 (records, 32 * P-lane tiles) above."""
     c = config_circuit("C2", n_ops=2000, n_levels=10, n_regs=100)
     g = rs.Graph(c)
     a = rs.Lanes(g, 1024)
     b = rs.Lanes(g, 4096)
     assert a.shape()["kernel"] == 2 and a.shape()["lane_tile"] in (8, 16, 32)
-    assert b.shape()["kernel"] == 1 and b.shape()["lane_tile"] in (32, 64, 128)
+    assert b.shape()["kernel"] == 7 and b.shape()["lane_tile"] in (64, 128)
     for L in (a, b):
         L.set_seed(3)
         h = L.step(3, hashes="host")
