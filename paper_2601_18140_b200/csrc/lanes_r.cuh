@@ -16,6 +16,9 @@
 #pragma once
 #include "lanes_b.cuh"
 
+#ifndef RS_K7_BLOCK
+#define RS_K7_BLOCK 1
+#endif
 #ifndef RS_LANES_R_MAX_THREADS
 #define RS_LANES_R_MAX_THREADS 768
 #endif
@@ -145,7 +148,11 @@ __device__ __forceinline__ void stage_ops_r(const LaneT& L, const uint8_t* buf, 
   }
 #endif
 #pragma unroll 1
-  for (; j < n; j += nw) {
+  // blocks of RS_K7_BLOCK consecutive records (same run mostly: the same tail code) dealt
+  // round-robin to the warps
+  for (uint32_t jb = j * RS_K7_BLOCK; jb < n; jb += nw * RS_K7_BLOCK)
+#pragma unroll 1
+  for (uint32_t j = jb; j < min(n, jb + RS_K7_BLOCK); ++j) {
     const uint4 r0 = lds128(rec0 + kRecBytes * j), r1 = lds128(rec0 + kRecBytes * j + 16);
     const uint32_t pw = r0.w, oc = r1.x, sel = r1.w, t = (sel >> 8) & 0xffu;
     const uint64_t K = HASH ? ((uint64_t)r1.z << 32 | r1.y) : 0ull;
