@@ -99,6 +99,7 @@ struct StepArgs {
   uint32_t bitplane;
   uint32_t rows_bit;
   uint64_t region_b;
+  uint32_t pairs;    // kernel 7: evaluate <= 2-operand ops in pairs (many ops per CTA and level)
 };
 
 // One watched value of the single lane (watch index j) at `cycle`: a change

@@ -16,9 +16,6 @@
 #pragma once
 #include "lanes_b.cuh"
 
-#ifndef RS_K7_BLOCK
-#define RS_K7_BLOCK 1
-#endif
 #ifndef RS_LANES_R_MAX_THREADS
 #define RS_LANES_R_MAX_THREADS 768
 #endif
@@ -125,16 +122,16 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
 // expensive ops and the stage barrier waits for nobody in particular.
 template <int P, bool HASH>
 __device__ __forceinline__ void stage_ops_r(const LaneT& L, const uint8_t* buf, uint32_t j0, uint32_t nw,
-                                            uint64_t (&hacc)[P]) {
+                                            bool pairs, uint64_t (&hacc)[P]) {
   const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
   const uint32_t base = smem_addr(buf), rec0 = base + h->off_c, n = h->n;
   uint32_t j = j0;
-#ifdef RS_PAIRS
-  // (opt-in build, measured slower on C3: 1.29 vs 1.23 ms per cycle) pairs of ops with
-  // <= 2 operands: both ops' loads are in flight before either is computed (the PSU
+  // pairs of ops with <= 2 operands (allocations with many ops per CTA and level, the
+  // runtime's `pairs`; measured: C4 37.5 -> 31.6 ms per cycle, C3 1.23 -> 1.29 ms, so C3
+  // stays single): both ops' loads are in flight before either is computed (the PSU
   // partial unrolling); a one-operand op is gathered as two-operand
 #pragma unroll 1
-  for (; j + nw < n; j += 2 * nw) {
+  for (; pairs && j + nw < n; j += 2 * nw) {
     const uint4 a0 = lds128(rec0 + kRecBytes * j), a1 = lds128(rec0 + kRecBytes * j + 16);
     const uint4 b0 = lds128(rec0 + kRecBytes * (j + nw)), b1 = lds128(rec0 + kRecBytes * (j + nw) + 16);
     const uint32_t aA = (a1.w >> 16) & 3u, bA = (b1.w >> 16) & 3u;
@@ -146,13 +143,10 @@ __device__ __forceinline__ void stage_ops_r(const LaneT& L, const uint8_t* buf, 
     tail_pair<P, HASH>(L, xa, a0.w, a1.x, HASH ? ((uint64_t)a1.z << 32 | a1.y) : 0ull, (a1.w >> 8) & 0xffu, hacc);
     tail_pair<P, HASH>(L, xb, b0.w, b1.x, HASH ? ((uint64_t)b1.z << 32 | b1.y) : 0ull, (b1.w >> 8) & 0xffu, hacc);
   }
-#endif
 #pragma unroll 1
   // blocks of RS_K7_BLOCK consecutive records (same run mostly: the same tail code) dealt
   // round-robin to the warps
-  for (uint32_t jb = j * RS_K7_BLOCK; jb < n; jb += nw * RS_K7_BLOCK)
-#pragma unroll 1
-  for (uint32_t j = jb; j < min(n, jb + RS_K7_BLOCK); ++j) {
+  for (; j < n; j += nw) {
     const uint4 r0 = lds128(rec0 + kRecBytes * j), r1 = lds128(rec0 + kRecBytes * j + 16);
     const uint32_t pw = r0.w, oc = r1.x, sel = r1.w, t = (sel >> 8) & 0xffu;
     const uint64_t K = HASH ? ((uint64_t)r1.z << 32 | r1.y) : 0ull;
@@ -259,7 +253,7 @@ __global__ void __launch_bounds__(RS_LANES_R_MAX_THREADS, 1) k_lanes_r(const Ste
     uint32_t b, e;
     chunk_of(h->n, gw, ngw, b, e);
     if (type == ST_OPS) {
-      stage_ops_r<P, HASH>(L, buf, gw, ngw, hacc);
+      stage_ops_r<P, HASH>(L, buf, gw, ngw, a.pairs != 0u, hacc);
     } else if (type == ST_LATCH) {
       if (b < e) {
         const uint32_t base = smem_addr(buf);

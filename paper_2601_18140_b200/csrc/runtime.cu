@@ -205,6 +205,7 @@ StepArgs base_args(const rs_lanes* s) {
   a.watch_begin = s->watch_begin;
   a.n_watch = s->g->cg.mode == RS_MODE_SINGLE ? (uint32_t)s->watch.size() : 0u;
   a.bitplane = s->variant == 6 ? 1u : 0u;
+  a.pairs = (s->variant == 7 && s->batch_idx == 1) ? 1u : 0u;  // >= 2,048 ops per CTA and level (C4)
   a.rows_bit = s->g->cg.rows_bit;
   a.region_b = s->region_b;
   return a;
