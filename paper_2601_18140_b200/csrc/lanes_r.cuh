@@ -120,18 +120,18 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
 // OPS stage: records at buf + off_c (h->n of them); this warp takes ops j0, j0 + nw,
 // ... -- interleaved across the runs, so every warp gets the same mix of cheap and
 // expensive ops and the stage barrier waits for nobody in particular.
-template <int P, bool HASH>
+template <int P, bool HASH, bool PAIRS>
 __device__ __forceinline__ void stage_ops_r(const LaneT& L, const uint8_t* buf, uint32_t j0, uint32_t nw,
-                                            bool pairs, uint64_t (&hacc)[P]) {
+                                            uint64_t (&hacc)[P]) {
   const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
   const uint32_t base = smem_addr(buf), rec0 = base + h->off_c, n = h->n;
   uint32_t j = j0;
   // pairs of ops with <= 2 operands (allocations with many ops per CTA and level, the
-  // runtime's `pairs`; measured: C4 37.5 -> 31.6 ms per cycle, C3 1.23 -> 1.29 ms, so C3
+  // PAIRS instantiation; measured: C4 37.5 -> 31.6 ms per cycle, C3 1.23 -> 1.29 ms, so C3
   // stays single): both ops' loads are in flight before either is computed (the PSU
   // partial unrolling); a one-operand op is gathered as two-operand
 #pragma unroll 1
-  for (; pairs && j + nw < n; j += 2 * nw) {
+  for (; PAIRS && j + nw < n; j += 2 * nw) {
     const uint4 a0 = lds128(rec0 + kRecBytes * j), a1 = lds128(rec0 + kRecBytes * j + 16);
     const uint4 b0 = lds128(rec0 + kRecBytes * (j + nw)), b1 = lds128(rec0 + kRecBytes * (j + nw) + 16);
     const uint32_t aA = (a1.w >> 16) & 3u, bA = (b1.w >> 16) & 3u;
@@ -195,7 +195,7 @@ __device__ __forceinline__ void stage_ops_r(const LaneT& L, const uint8_t* buf, 
   }
 }
 
-template <int P, bool HASH>
+template <int P, bool HASH, bool PAIRS>
 __global__ void __launch_bounds__(RS_LANES_R_MAX_THREADS, 1) k_lanes_r(const StepArgs a) {
   constexpr uint32_t LT = 32u * P;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(RS_LANES_R_MAX_THREADS, 1) k_lanes_r(const Ste
     uint32_t b, e;
     chunk_of(h->n, gw, ngw, b, e);
     if (type == ST_OPS) {
-      stage_ops_r<P, HASH>(L, buf, gw, ngw, a.pairs != 0u, hacc);
+      stage_ops_r<P, HASH, PAIRS>(L, buf, gw, ngw, hacc);
     } else if (type == ST_LATCH) {
       if (b < e) {
         const uint32_t base = smem_addr(buf);

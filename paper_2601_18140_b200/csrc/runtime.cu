@@ -205,7 +205,7 @@ StepArgs base_args(const rs_lanes* s) {
   a.watch_begin = s->watch_begin;
   a.n_watch = s->g->cg.mode == RS_MODE_SINGLE ? (uint32_t)s->watch.size() : 0u;
   a.bitplane = s->variant == 6 ? 1u : 0u;
-  a.pairs = (s->variant == 7 && s->batch_idx == 1) ? 1u : 0u;  // >= 2,048 ops per CTA and level (C4)
+  a.pairs = (s->variant == 7 && s->batch_idx == 1) ? 1u : 0u;  // >= 2,048 ops per CTA and level (C4): k_lanes_r<.., true>
   a.rows_bit = s->g->cg.rows_bit;
   a.region_b = s->region_b;
   return a;
@@ -1421,8 +1421,10 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
                          (const void*)k_lanes_t<4, true>, (const void*)k_lanes_t<4, false>,
                          (const void*)k_lanes_b<2, true>, (const void*)k_lanes_b<2, false>,
                          (const void*)k_lanes_b<4, true>, (const void*)k_lanes_b<4, false>,
-                         (const void*)k_lanes_r<2, true>, (const void*)k_lanes_r<2, false>,
-                         (const void*)k_lanes_r<4, true>, (const void*)k_lanes_r<4, false>};
+                         (const void*)k_lanes_r<2, true, false>, (const void*)k_lanes_r<2, false, false>,
+                         (const void*)k_lanes_r<4, true, false>, (const void*)k_lanes_r<4, false, false>,
+                         (const void*)k_lanes_r<2, true, true>, (const void*)k_lanes_r<2, false, true>,
+                         (const void*)k_lanes_r<4, true, true>, (const void*)k_lanes_r<4, false, true>};
     // the dynamic shared-memory limit is a per-device function attribute: raise it
     // once per device to the largest size any allocation there has needed
     static thread_local size_t attr_set[64] = {};
@@ -1433,7 +1435,7 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
     }
     const int fi = (s->variant == 1   ? 6 + (s->LT == 32 ? 0 : s->LT == 64 ? 2 : 4)
                     : s->variant == 6 ? 12 + (s->LT == 64 ? 0 : 2)
-                    : s->variant == 7 ? 16 + (s->LT == 64 ? 0 : 2)
+                    : s->variant == 7 ? 16 + (s->LT == 64 ? 0 : 2) + (s->batch_idx == 1 ? 4 : 0)
                                       : (s->LT == 32 ? 0 : s->LT == 16 ? 2 : 4)) + (hash ? 0 : 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(s->n_tiles * s->cluster);
