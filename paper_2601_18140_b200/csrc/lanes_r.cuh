@@ -143,21 +143,9 @@ __device__ __forceinline__ void stage_ops_r(const LaneT& L, const uint8_t* buf, 
     tail_pair<P, HASH>(L, xa, a0.w, a1.x, HASH ? ((uint64_t)a1.z << 32 | a1.y) : 0ull, (a1.w >> 8) & 0xffu, hacc);
     tail_pair<P, HASH>(L, xb, b0.w, b1.x, HASH ? ((uint64_t)b1.z << 32 | b1.y) : 0ull, (b1.w >> 8) & 0xffu, hacc);
   }
-#ifdef RS_K7_RECPREFETCH  // (A/B) next record loaded one op ahead
-  uint4 n0 = j < n ? lds128(rec0 + kRecBytes * j) : make_uint4(0, 0, 0, 0);
-  uint4 n1 = j < n ? lds128(rec0 + kRecBytes * j + 16) : make_uint4(0, 0, 0, 0);
-#endif
 #pragma unroll 1
   for (; j < n; j += nw) {
-#ifdef RS_K7_RECPREFETCH
-    const uint4 r0 = n0, r1 = n1;
-    if (j + nw < n) {
-      n0 = lds128(rec0 + kRecBytes * (j + nw));
-      n1 = lds128(rec0 + kRecBytes * (j + nw) + 16);
-    }
-#else
     const uint4 r0 = lds128(rec0 + kRecBytes * j), r1 = lds128(rec0 + kRecBytes * j + 16);
-#endif
     const uint32_t pw = r0.w, oc = r1.x, sel = r1.w, t = (sel >> 8) & 0xffu;
     const uint64_t K = HASH ? ((uint64_t)r1.z << 32 | r1.y) : 0ull;
     if (t == kTailFold) {
