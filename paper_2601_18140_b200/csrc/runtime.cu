@@ -725,6 +725,10 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     return set_err(RS_E_INVALID_ARG, "part_world = %u / part_rank = %u: a single-lane level cut of 2..%u partitions "
                    "(<= n_levels), without parts / repcut", o.part_world, o.part_rank, kMaxParts);
   }
+  if (o.part_world && o.defer_state) {
+    rs_free_lanes(s);
+    return set_err(RS_E_INVALID_ARG, "defer_state: a level cut across processes owns its state (CUDA IPC)");
+  }
   if (o.part_world) {
     o.parts = o.part_world;
     o.kernel = 5;
@@ -1149,12 +1153,12 @@ rs_status rs_lanes_bind_state(rs_lanes* s, void* state, uint64_t bytes) {
 }
 
 void rs_free_lanes(rs_lanes* s) {
-  if (s && s->connected)
-    for (uint32_t k = 0; k < s->part_world; ++k)
-      if (k != s->part_rank && s->peer_rep[k]) cudaIpcCloseMemHandle(s->peer_rep[k]);
   if (!s) return;
   cudaSetDevice(s->g->device);
-  if (s->stream) cudaStreamSynchronize(s->stream);
+  if (s->stream) cudaStreamSynchronize(s->stream);  // no launch may still use a peer mapping
+  if (s->connected)
+    for (uint32_t k = 0; k < s->part_world; ++k)
+      if (k != s->part_rank && s->peer_rep[k]) cudaIpcCloseMemHandle(s->peer_rep[k]);
   if (s->state_mem && s->state_owned) cudaFree(s->state_mem);
   if (s->dstages) cudaFree(s->dstages);
   if (s->dslices) cudaFree(s->dslices);
