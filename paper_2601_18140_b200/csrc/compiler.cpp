@@ -799,6 +799,13 @@ bool build_repcut(const CompiledGraph& g, uint32_t P, RepCutPlan* out, std::stri
   for (uint32_t i = 0; i < R; ++i) reg_of_coord[g.reg_coord[i]] = i;
   std::unordered_map<uint32_t, uint32_t> in_of_coord;
   for (uint32_t i = 0; i < g.n_inputs; ++i) in_of_coord[g.in_coord[i]] = i;
+  // canonical id of each op's output (identity copies: none)
+  std::vector<uint32_t> out_sig(NT, UINT32_MAX);
+  for (uint32_t s2 = 0; s2 < g.n_signals; ++s2)
+    if (g.sig_kind[s2] == 3 && (g.sig_rep.empty() || g.sig_rep[s2] == s2)) {
+      const int32_t q = producer(g.sig_coord[s2]);
+      if (q >= 0) out_sig[q] = s2;
+    }
   for (uint32_t j = 0; j < NT; ++j)
     if (owner[j] < 0) {
       int32_t p = -1;
@@ -806,16 +813,20 @@ bool build_repcut(const CompiledGraph& g, uint32_t P, RepCutPlan* out, std::stri
         const int32_t q = producer(g.coord[a]);
         if (q >= 0) p = owner[q];
       }
-      for (uint32_t a = g.coord_off[j]; a < g.coord_off[j + 1] && p < 0; ++a) {
-        auto it = reg_of_coord.find(g.coord[a]);
-        if (it != reg_of_coord.end()) p = (int32_t)reg_part[it->second];
-      }
-      // inputs, like registers, in contiguous index blocks (a multi-core design's
-      // inputs follow its module order)
+      // then inputs, then registers, both in contiguous index blocks (a multi-core
+      // design's inputs and registers follow its module order); inputs first: an
+      // operand that is another block's register is how cores couple, and a dead op
+      // placed by it would drag its dependents' cones into that block (the graph
+      // passes turn copies of inputs into direct input operands, exposing this)
       for (uint32_t a = g.coord_off[j]; a < g.coord_off[j + 1] && p < 0; ++a) {
         auto it = in_of_coord.find(g.coord[a]);
         if (it != in_of_coord.end()) p = (int32_t)((uint64_t)it->second * P / g.n_inputs);
       }
+      // else the block its own canonical id falls in (signals in contiguous id blocks, like
+      // registers: a netlist lists each module's signals together); not a register
+      // operand's block -- registers are how cores couple, so an op reading only a
+      // foreign register (and constants) would drag its dependents' cones there
+      if (p < 0 && out_sig[j] != UINT32_MAX) p = (int32_t)((uint64_t)out_sig[j] * P / g.n_signals);
       if (p < 0) p = (int32_t)(j % P);
       close((uint32_t)p, (int32_t)j);
       owner[j] = p;

@@ -44,6 +44,21 @@ def test_passes_on_the_c3_recipe(rs):
     assert i["alg_bytes_per_lane_cycle"] < i0["alg_bytes_per_lane_cycle"]
 
 
+def test_passes_keep_repcut_replication_free(rs):
+    """A multi-core design cut at its cores replicates nothing, with or without the passes:
+    dead logic left by constant folding (an op of a folded constant and another core's
+    register) must not be placed by that register's block (it would drag its dependents'
+    cones into the other core's partition)."""
+    from synth import multicore_circuit
+    c = multicore_circuit()
+    for passes in (False, True):
+        g = rs.Graph(c, device=rs.RS_DEVICE_NONE, mode="single", passes=passes)
+        i = g.info()
+        st = g.repcut_stats(16)
+        assert st["ops_total"] == i["n_ops"] + i["n_copy_ops"], passes
+        assert st["max_ops"] <= 12_500
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("mode,kernel", [("lanes", 1), ("lanes", 2), ("lanes", 6), ("lanes", 7), ("single", 3),
                                          ("single", 5)])
