@@ -483,8 +483,7 @@ def test_caller_owned_state(rs, kernel):
     r = oracle.simulate(c, 9, seed=8, n_lanes=50, final=True)
     assert np.array_equal(h, r.hashes)
     assert np.array_equal(L.read(list(range(c.n_signals))), r.final_state)
-    raw = rs.Lanes.__new__(rs.Lanes)
-    M = rs.Lanes(g, 50, kernel=kernel, state=None)
+    M = rs.Lanes(g, 50, kernel=kernel)          # library-owned state: same size
     assert M.state_bytes() == L.state_bytes()
     import ctypes
     opts = rs.LaneOpts(0, 0, 0, 0, 0, None, 0, kernel, 0, 0, 0, 0, 0, 1)
@@ -498,4 +497,3 @@ def test_caller_owned_state(rs, kernel):
         rs._check(rs.lib().rs_lanes_bind_state(hnd, ctypes.c_void_p(small.data_ptr()), 256))
     assert e.value.name == "RS_E_CAPACITY"
     rs.lib().rs_free_lanes(hnd)
-    del raw
