@@ -154,7 +154,7 @@ typedef struct {
                               bit planes (32 lanes per word); 7 = kernel 1's
                               tiles driven by 32-byte per-op records (one jump into the gather, one
                               into an (opcode, arity, out class) tail).  lane_tile must match (32/64/128
-                              for 1, 8/16/32 for 2, 64/128 for 6 and 7).  RS_E_INVALID_ARG otherwise.
+                              for 1 and 7, 8/16/32 for 2, 64/128 for 6).  RS_E_INVALID_ARG otherwise.
                               RS_MODE_SINGLE: 0 = auto (RepCut with one partition when the whole design
                               fits one SM's shared memory, else the level-synchronous grid); 3 = RepCut,
                               shared-memory slices; 4 = RepCut, global replicas; 5 = level-synchronous

@@ -477,8 +477,8 @@ size_t lanes_smem(uint32_t stage_bytes, uint32_t threads) {
 void choose_tiling(uint32_t kernel, uint32_t n_lanes, int sms, uint32_t want_lt, uint32_t want_cs, uint32_t* lt,
                    uint32_t* cs) {
   const uint32_t k1[3] = {128u, 64u, 32u}, k2[3] = {32u, 16u, 8u}, k6[2] = {128u, 64u};
-  const uint32_t* cand = kernel == 1 ? k1 : (kernel == 6 || kernel == 7) ? k6 : k2;
-  const int nc = (kernel == 6 || kernel == 7) ? 2 : 3;
+  const uint32_t* cand = (kernel == 1 || kernel == 7) ? k1 : kernel == 6 ? k6 : k2;
+  const int nc = kernel == 6 ? 2 : 3;
   const uint32_t smallest = cand[nc - 1];
   for (const uint32_t cmax : {4u, 8u}) {
     for (int i = 0; i < nc; ++i) {
@@ -784,11 +784,11 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     // 1.30 ms per cycle for kernel 1, C4 31.6 vs 34.8 ms; profiles/r02)
     const uint32_t kern = o.kernel ? o.kernel : (n_lanes < 2048u ? 2u : 7u);
     if (o.lane_tile && (kern == 2   ? (o.lane_tile != 8 && o.lane_tile != 16 && o.lane_tile != 32)
-                        : kern >= 6 ? (o.lane_tile != 64 && o.lane_tile != 128)
+                        : kern == 6 ? (o.lane_tile != 64 && o.lane_tile != 128)
                                     : (o.lane_tile != 32 && o.lane_tile != 64 && o.lane_tile != 128))) {
       rs_free_lanes(s);  // partially built: frees what exists
-      return set_err(RS_E_INVALID_ARG, "lane_tile must be 32, 64 or 128 (kernel 1), 8, 16 or 32 (kernel 2) or "
-                                       "64 or 128 (kernel 6)");
+      return set_err(RS_E_INVALID_ARG, "lane_tile must be 32, 64 or 128 (kernels 1 and 7), 8, 16 or 32 (kernel 2) "
+                                       "or 64 or 128 (kernel 6)");
     }
     if (o.cluster && o.cluster != 1 && o.cluster != 2 && o.cluster != 4 && o.cluster != 8) {
       rs_free_lanes(s);  // partially built: frees what exists
@@ -1428,7 +1428,8 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
                          (const void*)k_lanes_r<2, true, false>, (const void*)k_lanes_r<2, false, false>,
                          (const void*)k_lanes_r<4, true, false>, (const void*)k_lanes_r<4, false, false>,
                          (const void*)k_lanes_r<2, true, true>, (const void*)k_lanes_r<2, false, true>,
-                         (const void*)k_lanes_r<4, true, true>, (const void*)k_lanes_r<4, false, true>};
+                         (const void*)k_lanes_r<4, true, true>, (const void*)k_lanes_r<4, false, true>,
+                         (const void*)k_lanes_r<1, true, false>, (const void*)k_lanes_r<1, false, false>};
     // the dynamic shared-memory limit is a per-device function attribute: raise it
     // once per device to the largest size any allocation there has needed
     static thread_local size_t attr_set[64] = {};
@@ -1439,7 +1440,7 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
     }
     const int fi = (s->variant == 1   ? 6 + (s->LT == 32 ? 0 : s->LT == 64 ? 2 : 4)
                     : s->variant == 6 ? 12 + (s->LT == 64 ? 0 : 2)
-                    : s->variant == 7 ? 16 + (s->LT == 64 ? 0 : 2) + (s->batch_idx == 1 ? 4 : 0)
+                    : s->variant == 7 ? (s->LT == 32 ? 24 : 16 + (s->LT == 64 ? 0 : 2) + (s->batch_idx == 1 ? 4 : 0))
                                       : (s->LT == 32 ? 0 : s->LT == 16 ? 2 : 4)) + (hash ? 0 : 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(s->n_tiles * s->cluster);

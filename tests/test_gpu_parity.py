@@ -88,7 +88,8 @@ def test_c1_full(rs, mode, kernel):
 @pytest.mark.parametrize("kernel,lt,cs", [(2, 8, 1), (2, 16, 1), (2, 32, 1), (2, 32, 4), (2, 16, 2), (2, 8, 8),
                                           (1, 32, 1), (1, 64, 1), (1, 128, 1), (1, 32, 4), (1, 64, 2),
                                           (1, 128, 8), (6, 64, 1), (6, 128, 1), (6, 64, 2), (6, 128, 4),
-                                          (6, 128, 8), (7, 64, 1), (7, 128, 1), (7, 64, 2), (7, 128, 4)])
+                                          (6, 128, 8), (7, 32, 1), (7, 32, 4), (7, 64, 1), (7, 128, 1), (7, 64, 2),
+                                          (7, 128, 4)])
 def test_c2_structure_ragged_lanes(rs, lt, cs, kernel):
     """Full C2 circuit, 37 lanes (ragged last tile), 25 cycles, each lane tile,
     one CTA or a thread-block cluster per tile, both lane kernels."""
