@@ -499,6 +499,78 @@ void choose_tiling(uint32_t kernel, uint32_t n_lanes, int sms, uint32_t want_lt,
   *cs = want_cs ? want_cs : 8;
 }
 
+
+// Lane-mode step kernel of an allocation (variant, tile, hash, pairs) and its
+// dynamic shared memory; the shared-memory cap is a per-device function attribute,
+// raised once per device to the largest size any allocation there has needed.
+const void* const kLaneFns[] = {
+    (const void*)k_lanes<32, true>,        (const void*)k_lanes<32, false>,
+    (const void*)k_lanes<16, true>,        (const void*)k_lanes<16, false>,
+    (const void*)k_lanes<8, true>,         (const void*)k_lanes<8, false>,
+    (const void*)k_lanes_t<1, true>,       (const void*)k_lanes_t<1, false>,
+    (const void*)k_lanes_t<2, true>,       (const void*)k_lanes_t<2, false>,
+    (const void*)k_lanes_t<4, true>,       (const void*)k_lanes_t<4, false>,
+    (const void*)k_lanes_b<2, true>,       (const void*)k_lanes_b<2, false>,
+    (const void*)k_lanes_b<4, true>,       (const void*)k_lanes_b<4, false>,
+    (const void*)k_lanes_r<2, true, false>, (const void*)k_lanes_r<2, false, false>,
+    (const void*)k_lanes_r<4, true, false>, (const void*)k_lanes_r<4, false, false>,
+    (const void*)k_lanes_r<2, true, true>,  (const void*)k_lanes_r<2, false, true>,
+    (const void*)k_lanes_r<4, true, true>,  (const void*)k_lanes_r<4, false, true>,
+    (const void*)k_lanes_r<1, true, false>, (const void*)k_lanes_r<1, false, false>};
+
+const void* lane_kernel_fn(const rs_lanes* s, bool hash) {
+  const int fi = (s->variant == 1   ? 6 + (s->LT == 32 ? 0 : s->LT == 64 ? 2 : 4)
+                  : s->variant == 6 ? 12 + (s->LT == 64 ? 0 : 2)
+                  : s->variant == 7 ? (s->LT == 32 ? 24 : 16 + (s->LT == 64 ? 0 : 2) + (s->batch_idx == 1 ? 4 : 0))
+                                    : (s->LT == 32 ? 0 : s->LT == 16 ? 2 : 4)) + (hash ? 0 : 1);
+  return kLaneFns[fi];
+}
+
+size_t lane_smem_bytes(const rs_lanes* s) {
+  return s->variant == 7   ? 128 + 2ull * kStageBytesR + lanes_b_smem_extra(s->LT / 32)
+         : s->variant == 6 ? 128 + 2ull * s->g->stage_bytes + lanes_b_smem_extra(s->LT / 32)
+         : s->variant == 1 ? 128 + 2ull * s->g->stage_bytes + lanes_t_smem_extra(s->threads, s->LT / 32)
+                           : lanes_smem(s->g->stage_bytes, s->threads);
+}
+
+cudaError_t raise_smem_attr(int device, size_t smem) {
+  static thread_local size_t attr_set[64] = {};
+  size_t& have = attr_set[device & 63];
+  if (have >= smem) return cudaSuccess;
+  for (const void* f : kLaneFns) {
+    const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  have = smem;
+  return cudaSuccess;
+}
+
+// Clusters of this allocation's launch shape that fit the device at once.  A launch
+// with more clusters runs them in waves -- which the measured "8-CTA clusters are slow"
+// (2,048 C3 lanes: 16 clusters of 8 took 1.44 ms per cycle, 8 clusters of 8 ran fine)
+// turned out to be.
+int co_resident_clusters(const rs_lanes* s) {
+  const size_t smem = lane_smem_bytes(s);
+  if (raise_smem_attr(s->g->device, smem) != cudaSuccess) return 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(s->n_tiles * s->cluster);
+  cfg.blockDim = dim3(s->threads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = s->cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, lane_kernel_fn(s, true), &cfg) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return -1;  // unknown
+  }
+  return n;
+}
+
 }  // namespace
 
 extern "C" {
@@ -828,6 +900,16 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     uint32_t th = tmax / std::max<uint32_t>(1, per_sm);
     th = std::max<uint32_t>(64, th & ~31u);
     s->threads = th;
+  }
+  // lane mode: every cluster of the launch must be co-resident, else the launch runs in
+  // waves; an automatic shape halves its cluster until it fits (fewer CTAs, one wave)
+  if (g->cg.mode == RS_MODE_LANES && !o.cluster) {
+    s->batch_idx = 0;  // not chosen yet; it only picks a kernel-7 variant of the same shared memory
+    int fit = co_resident_clusters(s);
+    while (fit >= 0 && (uint32_t)fit < s->n_tiles && s->cluster > 1) {
+      s->cluster /= 2;
+      fit = co_resident_clusters(s);
+    }
   }
   if (s->repcut) {
     RepCutPlan plan;
@@ -1413,35 +1495,9 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
     if (hash) s->hc_cur = 1 - s->hc_cur;
   } else {
     a.hcarry_out = a.hcarry_in;
-    const size_t smem = s->variant == 7   ? 128 + 2ull * kStageBytesR + lanes_b_smem_extra(s->LT / 32)
-                        : s->variant == 6 ? 128 + 2ull * s->g->stage_bytes + lanes_b_smem_extra(s->LT / 32)
-                        : s->variant == 1 ? 128 + 2ull * s->g->stage_bytes + lanes_t_smem_extra(s->threads, s->LT / 32)
-                                          : lanes_smem(s->g->stage_bytes, s->threads);
-    const void* fns[] = {(const void*)k_lanes<32, true>, (const void*)k_lanes<32, false>,
-                         (const void*)k_lanes<16, true>, (const void*)k_lanes<16, false>,
-                         (const void*)k_lanes<8, true>,  (const void*)k_lanes<8, false>,
-                         (const void*)k_lanes_t<1, true>, (const void*)k_lanes_t<1, false>,
-                         (const void*)k_lanes_t<2, true>, (const void*)k_lanes_t<2, false>,
-                         (const void*)k_lanes_t<4, true>, (const void*)k_lanes_t<4, false>,
-                         (const void*)k_lanes_b<2, true>, (const void*)k_lanes_b<2, false>,
-                         (const void*)k_lanes_b<4, true>, (const void*)k_lanes_b<4, false>,
-                         (const void*)k_lanes_r<2, true, false>, (const void*)k_lanes_r<2, false, false>,
-                         (const void*)k_lanes_r<4, true, false>, (const void*)k_lanes_r<4, false, false>,
-                         (const void*)k_lanes_r<2, true, true>, (const void*)k_lanes_r<2, false, true>,
-                         (const void*)k_lanes_r<4, true, true>, (const void*)k_lanes_r<4, false, true>,
-                         (const void*)k_lanes_r<1, true, false>, (const void*)k_lanes_r<1, false, false>};
-    // the dynamic shared-memory limit is a per-device function attribute: raise it
-    // once per device to the largest size any allocation there has needed
-    static thread_local size_t attr_set[64] = {};
-    size_t& have = attr_set[s->g->device & 63];
-    if (have < smem) {
-      for (const void* f : fns) CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      have = smem;
-    }
-    const int fi = (s->variant == 1   ? 6 + (s->LT == 32 ? 0 : s->LT == 64 ? 2 : 4)
-                    : s->variant == 6 ? 12 + (s->LT == 64 ? 0 : 2)
-                    : s->variant == 7 ? (s->LT == 32 ? 24 : 16 + (s->LT == 64 ? 0 : 2) + (s->batch_idx == 1 ? 4 : 0))
-                                      : (s->LT == 32 ? 0 : s->LT == 16 ? 2 : 4)) + (hash ? 0 : 1);
+    const size_t smem = lane_smem_bytes(s);
+    const void* fn = lane_kernel_fn(s, hash);
+    CU(raise_smem_attr(s->g->device, smem));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(s->n_tiles * s->cluster);
     cfg.blockDim = dim3(s->threads);
@@ -1466,7 +1522,7 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
       cfg.numAttrs = 2;
     }
     void* args[] = {&a};
-    cudaError_t e = cudaLaunchKernelExC(&cfg, fns[fi], args);
+    cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
     if (e != cudaSuccess) return set_err(RS_E_CUDA, "k_lanes launch: %s", cudaGetErrorString(e));
   }
   s->launches++;
