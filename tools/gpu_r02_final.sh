@@ -2,7 +2,7 @@
 # Round-2 final GPU evidence: the whole -m gpu suite (full-scope C3 / C4 / C5 streams included), smoke,
 # bench lines for every config, the ncu launch list of the default bench and one ncu --set full capture of
 # its step kernel (traffic), the reference arm.
-cd "$GRAFT_REPO_ROOT"; O=gpurun_out/final; mkdir -p $O
+cd "$GRAFT_REPO_ROOT"; O=gpurun_out/${FINAL_DIR:-final}; mkdir -p $O
 nvidia-smi > $O/smi.txt 2>&1
 timeout 3000 python -m pytest tests -m gpu -q -p no:cacheprovider --durations=25 > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
