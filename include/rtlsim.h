@@ -132,8 +132,9 @@ typedef struct {
   uint32_t lane_tile;      /* RS_MODE_LANES: lanes per CTA tile, 0 = auto, else 8, 16 or 32 (kernel 2)
                               or 32, 64 or 128 (kernel 1) */
   uint32_t threads;        /* threads per CTA, 0 = auto; a multiple of 32, at most the CTA size the kernel's
-                              register budget is compiled for: 768 for lane kernel 1, 640 for lane
-                              kernel 2 (RS_LANES_T_MAX_THREADS / RS_LANES_MAX_THREADS), 1024 single-lane */
+                              register budget is compiled for: 768 for lane kernels 1 and 6, 640 for lane
+                              kernel 2, 896 for lane kernel 7 (768 when it pairs ops: >= 2,048 ops per CTA
+                              and level), 1024 single-lane */
   uint32_t stage_cycles;   /* capacity (cycles) of the staged-input ring, 0 = none */
   uint32_t cluster;        /* RS_MODE_LANES: CTAs (a thread-block cluster on as many SMs) sharing one
                               lane tile, 0 = auto, else 1, 2, 4 or 8 */

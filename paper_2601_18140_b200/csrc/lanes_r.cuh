@@ -16,8 +16,14 @@
 #pragma once
 #include "lanes_b.cuh"
 
+// CTA sizes the register budgets are compiled for: single ops 896 threads (72 registers,
+// measured C3 1.148 vs 1.227 ms per cycle at 768), op pairs 768 (80 registers; pairs at
+// 896 threads: C4 34.8 vs 31.6 ms)
 #ifndef RS_LANES_R_MAX_THREADS
-#define RS_LANES_R_MAX_THREADS 768
+#define RS_LANES_R_MAX_THREADS 896
+#endif
+#ifndef RS_LANES_R_PAIRS_MAX_THREADS
+#define RS_LANES_R_PAIRS_MAX_THREADS 768
 #endif
 
 namespace rtlsim {
@@ -194,7 +200,8 @@ __device__ __forceinline__ void stage_ops_r(const LaneT& L, const uint8_t* buf, 
 }
 
 template <int P, bool HASH, bool PAIRS>
-__global__ void __launch_bounds__(RS_LANES_R_MAX_THREADS, 1) k_lanes_r(const StepArgs a) {
+__global__ void __launch_bounds__(PAIRS ? RS_LANES_R_PAIRS_MAX_THREADS : RS_LANES_R_MAX_THREADS, 1)
+    k_lanes_r(const StepArgs a) {
   constexpr uint32_t LT = 32u * P;
   extern __shared__ __align__(128) uint8_t smem[];
   // [mbarriers | stage buffer 0 | stage buffer 1 | scyc[4][LT] | sreg[4][LT]] (hash partials as k_lanes_b)

@@ -518,6 +518,16 @@ const void* const kLaneFns[] = {
     (const void*)k_lanes_r<4, true, true>,  (const void*)k_lanes_r<4, false, true>,
     (const void*)k_lanes_r<1, true, false>, (const void*)k_lanes_r<1, false, false>};
 
+// >= 2,048 ops per CTA and level: kBatchWide work items (kernels 1 / 6) and op pairs (kernel 7)
+bool wide_items(const rs_graph* g, uint32_t cluster) {
+  const uint64_t ops_per_cta_level =
+      g->cg.n_levels ? (uint64_t)g->cg.n_ops_total() / g->cg.n_levels / std::max<uint32_t>(1, cluster) : 0;
+  return ops_per_cta_level >= 2048;
+}
+uint32_t k7_max_threads(const rs_graph* g, uint32_t cluster) {
+  return wide_items(g, cluster) ? (uint32_t)RS_LANES_R_PAIRS_MAX_THREADS : (uint32_t)RS_LANES_R_MAX_THREADS;
+}
+
 const void* lane_kernel_fn(const rs_lanes* s, bool hash) {
   const int fi = (s->variant == 1   ? 6 + (s->LT == 32 ? 0 : s->LT == 64 ? 2 : 4)
                   : s->variant == 6 ? 12 + (s->LT == 64 ? 0 : 2)
@@ -882,7 +892,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     const uint32_t tmax = g->cg.mode == RS_MODE_SINGLE ? 1024u
                           : s->variant == 1            ? (uint32_t)RS_LANES_T_MAX_THREADS
                           : s->variant == 6            ? (uint32_t)RS_LANES_B_MAX_THREADS
-                          : s->variant == 7            ? (uint32_t)RS_LANES_R_MAX_THREADS
+                          : s->variant == 7            ? k7_max_threads(g, s->cluster)
                                                        : (uint32_t)RS_LANES_MAX_THREADS;
     if (o.threads % 32 || o.threads > tmax || o.threads < (s->variant != 2 ? 32u : s->LT)) {
       rs_free_lanes(s);
@@ -895,7 +905,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     const uint32_t per_sm = (s->n_tiles * s->cluster + g->sm_count - 1) / g->sm_count;
     const uint32_t tmax = s->variant == 1   ? (uint32_t)RS_LANES_T_MAX_THREADS
                           : s->variant == 6 ? (uint32_t)RS_LANES_B_MAX_THREADS
-                          : s->variant == 7 ? (uint32_t)RS_LANES_R_MAX_THREADS
+                          : s->variant == 7 ? k7_max_threads(g, s->cluster)
                                             : (uint32_t)RS_LANES_MAX_THREADS;
     uint32_t th = tmax / std::max<uint32_t>(1, per_sm);
     th = std::max<uint32_t>(64, th & ~31u);
@@ -910,6 +920,13 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
       s->cluster /= 2;
       fit = co_resident_clusters(s);
     }
+  }
+  if (g->cg.mode == RS_MODE_LANES && s->variant == 7 && s->threads > k7_max_threads(g, s->cluster)) {
+    if (o.threads) {
+      rs_free_lanes(s);
+      return set_err(RS_E_INVALID_ARG, "threads > %u for kernel 7 at this shape", k7_max_threads(g, s->cluster));
+    }
+    s->threads = k7_max_threads(g, s->cluster);
   }
   if (s->repcut) {
     RepCutPlan plan;
@@ -1122,9 +1139,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     // work items: kernel 1 takes kBatchWide-op items when its CTAs have many ops
     // per level (C4: ~6,700; fewer, longer items cut the per-item decode), else
     // kBatch-op items (more items to deal when a level is short: C3 ~470)
-    const uint64_t ops_per_cta_level =
-        g->cg.n_levels ? (uint64_t)g->cg.n_ops_total() / g->cg.n_levels / std::max<uint32_t>(1, s->cluster) : 0;
-    s->batch_idx = (s->variant != 2 && ops_per_cta_level >= 2048) ? 1u : 0u;
+    s->batch_idx = (s->variant != 2 && wide_items(g, s->cluster)) ? 1u : 0u;
     if (!g->stages_built[s->batch_idx]) {
       build_stages(g->cg, g->stage_bytes, s->batch_idx ? kBatchWide : kBatch, &g->stage_blob[s->batch_idx],
                    &g->stage_tab[s->batch_idx]);
