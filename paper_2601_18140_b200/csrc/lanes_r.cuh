@@ -117,39 +117,6 @@ __device__ __forceinline__ void tail_pair(const LaneT& L, const uint64_t (&x)[2]
 #undef RS_P4
 }
 
-#ifdef RS_K7_SPLIT3
-// A 3-operand op of a P = 4 tile as two passes over lanes {0, 1} and {2, 3} of each
-// thread: the second pass uses class bases moved 64 lanes on.
-template <bool HASH>
-__device__ __forceinline__ void split3_half(const LaneT& L, const uint32_t (&c)[3], uint32_t t, uint32_t pw,
-                                            uint32_t oc, uint64_t K, uint64_t (&h)[2]) {
-  uint64_t x[3][2];
-  gather_t<3, 2>(L, c, x);
-#define RS_H4(C, OPC)                                                     \
-  case 4 * C + 0: tail_r<2, HASH, 3, OPC, 0>(L, x, pw, oc, K, h); break;  \
-  case 4 * C + 1: tail_r<2, HASH, 3, OPC, 1>(L, x, pw, oc, K, h); break;  \
-  case 4 * C + 2: tail_r<2, HASH, 3, OPC, 2>(L, x, pw, oc, K, h); break;  \
-  case 4 * C + 3: tail_r<2, HASH, 3, OPC, 3>(L, x, pw, oc, K, h); break;
-  switch (t) {
-    RS_H4(14, RS_OP_AND) RS_H4(15, RS_OP_OR) RS_H4(16, RS_OP_XOR) RS_H4(17, RS_OP_ADD) RS_H4(18, RS_OP_SUB)
-    RS_H4(19, RS_OP_MUL) RS_H4(20, RS_OP_MUX)
-    default: break;
-  }
-#undef RS_H4
-}
-template <bool HASH>
-__device__ __forceinline__ void split3(const LaneT& L, const uint32_t (&c)[3], uint32_t t, uint32_t pw, uint32_t oc,
-                                       uint64_t K, uint64_t (&hacc)[4]) {
-  split3_half<HASH>(L, c, t, pw, oc, K, reinterpret_cast<uint64_t(&)[2]>(hacc[0]));
-  LaneT H;
-  H.p0 = L.p0 + 64;
-  H.p1 = L.p1 + 128;
-  H.p2 = L.p2 + 256;
-  H.p3 = L.p3 + 512;
-  split3_half<HASH>(H, c, t, pw, oc, K, reinterpret_cast<uint64_t(&)[2]>(hacc[2]));
-}
-#endif
-
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
   uint4 v;
   asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
@@ -220,19 +187,12 @@ __device__ __forceinline__ void stage_ops_r(const LaneT& L, const uint8_t* buf, 
       }
     } else {
       const uint32_t c[3] = {r0.x, r0.y, r0.z};
-#ifdef RS_K7_SPLIT3
-      if constexpr (P == 4) {  // two halves of two lanes: 12 value registers at the peak instead of 24
-        split3<HASH>(L, c, t, pw, oc, K, hacc);
-      } else
-#endif
-      {
-        uint64_t x[3][P];
-        gather_t<3, P>(L, c, x);
-        switch (t) {
-          RS_R4(14, 3, RS_OP_AND) RS_R4(15, 3, RS_OP_OR) RS_R4(16, 3, RS_OP_XOR) RS_R4(17, 3, RS_OP_ADD)
-          RS_R4(18, 3, RS_OP_SUB) RS_R4(19, 3, RS_OP_MUL) RS_R4(20, 3, RS_OP_MUX)
-          default: break;
-        }
+      uint64_t x[3][P];
+      gather_t<3, P>(L, c, x);
+      switch (t) {
+        RS_R4(14, 3, RS_OP_AND) RS_R4(15, 3, RS_OP_OR) RS_R4(16, 3, RS_OP_XOR) RS_R4(17, 3, RS_OP_ADD)
+        RS_R4(18, 3, RS_OP_SUB) RS_R4(19, 3, RS_OP_MUL) RS_R4(20, 3, RS_OP_MUX)
+        default: break;
       }
     }
 #undef RS_R4
