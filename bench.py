@@ -283,6 +283,7 @@ def main():
     ap.add_argument("--repcut", type=int, default=0, help="single-lane configs: RepCut partitions (rs_lane_opts.repcut)")
     ap.add_argument("--ref-step-s", type=float, default=4.0)
     ap.add_argument("--watch", type=int, default=0, help="waveform capture of N signals during the timed steps")
+    ap.add_argument("--op-pairs", type=int, default=0, help="rs_lane_opts.op_pairs (kernel 7: 0 auto, 1 off, 2 on)")
     ap.add_argument("--l2-policy", type=int, default=0, help="rs_lane_opts.l2_policy (0 none, 1 schedule, 2 state)")
     ap.add_argument("--replicas", action="store_true",
                     help="C1/C5 at N > 1: independent replicas instead of the level cut across GPUs")
@@ -331,7 +332,7 @@ def main():
     info0 = rs.Graph(circ, device=rs.RS_DEVICE_NONE, mode="single" if single else "lanes").info()
     mk = dict(lane0=shard.lane0, lane_tile=args.lane_tile, threads=args.threads, stream=stream,
               cluster=args.cluster, parts=args.parts, kernel=args.kernel, repcut=args.repcut,
-              l2_policy=args.l2_policy if not single else 0)
+              l2_policy=args.l2_policy if not single else 0, op_pairs=args.op_pairs)
     if levelcut:
         L = rs.Lanes(g, 1, stream=stream, part_world=world, part_rank=rank)
         hs = [None] * world

@@ -190,6 +190,10 @@ typedef struct {
   uint32_t defer_state;    /* 1: do not allocate the signal state; the caller binds its own device buffer
                               (e.g. a torch tensor) with rs_lanes_bind_state before stepping, sized by
                               rs_lanes_state_bytes.  Not with part_world. */
+  uint32_t op_pairs;       /* RS_MODE_LANES kernel 7: 0 = auto (ops with <= 2 operands evaluated in pairs,
+                              both pairs' loads in flight before either is computed, when a CTA has
+                              >= 2,048 ops per level), 1 = one op at a time, 2 = pairs (CTAs of at most
+                              768 threads).  Results identical.  RS_E_INVALID_ARG if > 2. */
 } rs_lane_opts;
 
 typedef struct rs_graph rs_graph;

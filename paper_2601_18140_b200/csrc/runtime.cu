@@ -110,6 +110,7 @@ struct rs_lanes {
   uint32_t stage_cap = 0;
   uint64_t st_lo = 0, st_hi = 0;    // staged window [st_lo, st_hi)
   uint32_t batch_idx = 0;           // rs_graph stage schedule in use (work-item size)
+  uint32_t op_pairs = 0;            // rs_lane_opts.op_pairs (kernel 7: 0 auto, 1 single ops, 2 pairs)
   // staged-input copies run on their own stream so the next chunk's transfer
   // overlaps the current chunk's step: a copy waits for the last launch that
   // read the ring slots it overwrites; a step waits for the copies before it
@@ -173,6 +174,8 @@ constexpr uint32_t kStageBytesR = 96 * 1024;
 constexpr size_t kBarBytes = 1024;      // partition k's grid barrier at u64 [4k]; level-cut flags at [kFlagOffset + k]
 constexpr size_t kFlagOffset = 64;
 
+bool k7_pairs(const rs_lanes* s);
+
 StepArgs base_args(const rs_lanes* s) {
   StepArgs a{};
   a.g = s->g->gd;
@@ -205,7 +208,7 @@ StepArgs base_args(const rs_lanes* s) {
   a.watch_begin = s->watch_begin;
   a.n_watch = s->g->cg.mode == RS_MODE_SINGLE ? (uint32_t)s->watch.size() : 0u;
   a.bitplane = s->variant == 6 ? 1u : 0u;
-  a.pairs = (s->variant == 7 && s->batch_idx == 1) ? 1u : 0u;  // >= 2,048 ops per CTA and level (C4): k_lanes_r<.., true>
+  a.pairs = (s->variant == 7 && k7_pairs(s)) ? 1u : 0u;  // k_lanes_r<.., true>
   a.rows_bit = s->g->cg.rows_bit;
   a.region_b = s->region_b;
   return a;
@@ -516,7 +519,8 @@ const void* const kLaneFns[] = {
     (const void*)k_lanes_r<4, true, false>, (const void*)k_lanes_r<4, false, false>,
     (const void*)k_lanes_r<2, true, true>,  (const void*)k_lanes_r<2, false, true>,
     (const void*)k_lanes_r<4, true, true>,  (const void*)k_lanes_r<4, false, true>,
-    (const void*)k_lanes_r<1, true, false>, (const void*)k_lanes_r<1, false, false>};
+    (const void*)k_lanes_r<1, true, false>, (const void*)k_lanes_r<1, false, false>,
+    (const void*)k_lanes_r<1, true, true>,  (const void*)k_lanes_r<1, false, true>};
 
 // >= 2,048 ops per CTA and level: kBatchWide work items (kernels 1 / 6) and op pairs (kernel 7)
 bool wide_items(const rs_graph* g, uint32_t cluster) {
@@ -524,14 +528,16 @@ bool wide_items(const rs_graph* g, uint32_t cluster) {
       g->cg.n_levels ? (uint64_t)g->cg.n_ops_total() / g->cg.n_levels / std::max<uint32_t>(1, cluster) : 0;
   return ops_per_cta_level >= 2048;
 }
-uint32_t k7_max_threads(const rs_graph* g, uint32_t cluster) {
-  return wide_items(g, cluster) ? (uint32_t)RS_LANES_R_PAIRS_MAX_THREADS : (uint32_t)RS_LANES_R_MAX_THREADS;
+// kernel 7 evaluates ops in pairs (rs_lane_opts.op_pairs; auto: >= 2,048 ops per CTA and level)
+bool k7_pairs(const rs_lanes* s) { return s->op_pairs ? s->op_pairs == 2u : wide_items(s->g, s->cluster); }
+uint32_t k7_max_threads(const rs_lanes* s) {
+  return k7_pairs(s) ? (uint32_t)RS_LANES_R_PAIRS_MAX_THREADS : (uint32_t)RS_LANES_R_MAX_THREADS;
 }
 
 const void* lane_kernel_fn(const rs_lanes* s, bool hash) {
   const int fi = (s->variant == 1   ? 6 + (s->LT == 32 ? 0 : s->LT == 64 ? 2 : 4)
                   : s->variant == 6 ? 12 + (s->LT == 64 ? 0 : 2)
-                  : s->variant == 7 ? (s->LT == 32 ? 24 : 16 + (s->LT == 64 ? 0 : 2) + (s->batch_idx == 1 ? 4 : 0))
+                  : s->variant == 7 ? (s->LT == 32 ? 24 + (k7_pairs(s) ? 2 : 0) : 16 + (s->LT == 64 ? 0 : 2) + (k7_pairs(s) ? 4 : 0))
                                     : (s->LT == 32 ? 0 : s->LT == 16 ? 2 : 4)) + (hash ? 0 : 1);
   return kLaneFns[fi];
 }
@@ -880,6 +886,11 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
       rs_free_lanes(s);  // partially built: frees what exists
       return set_err(RS_E_INVALID_ARG, "lane kernel must be 0, 1, 2, 6 or 7");
     }
+    if (o.op_pairs > 2) {
+      rs_free_lanes(s);  // partially built: frees what exists
+      return set_err(RS_E_INVALID_ARG, "op_pairs must be 0, 1 or 2");
+    }
+    s->op_pairs = o.op_pairs;
     s->variant = kern;
     uint32_t lt, cs;
     choose_tiling(kern, n_lanes, g->sm_count, o.lane_tile, o.cluster, &lt, &cs);
@@ -892,7 +903,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     const uint32_t tmax = g->cg.mode == RS_MODE_SINGLE ? 1024u
                           : s->variant == 1            ? (uint32_t)RS_LANES_T_MAX_THREADS
                           : s->variant == 6            ? (uint32_t)RS_LANES_B_MAX_THREADS
-                          : s->variant == 7            ? k7_max_threads(g, s->cluster)
+                          : s->variant == 7            ? k7_max_threads(s)
                                                        : (uint32_t)RS_LANES_MAX_THREADS;
     if (o.threads % 32 || o.threads > tmax || o.threads < (s->variant != 2 ? 32u : s->LT)) {
       rs_free_lanes(s);
@@ -905,7 +916,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     const uint32_t per_sm = (s->n_tiles * s->cluster + g->sm_count - 1) / g->sm_count;
     const uint32_t tmax = s->variant == 1   ? (uint32_t)RS_LANES_T_MAX_THREADS
                           : s->variant == 6 ? (uint32_t)RS_LANES_B_MAX_THREADS
-                          : s->variant == 7 ? k7_max_threads(g, s->cluster)
+                          : s->variant == 7 ? k7_max_threads(s)
                                             : (uint32_t)RS_LANES_MAX_THREADS;
     uint32_t th = tmax / std::max<uint32_t>(1, per_sm);
     th = std::max<uint32_t>(64, th & ~31u);
@@ -921,12 +932,12 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
       fit = co_resident_clusters(s);
     }
   }
-  if (g->cg.mode == RS_MODE_LANES && s->variant == 7 && s->threads > k7_max_threads(g, s->cluster)) {
+  if (g->cg.mode == RS_MODE_LANES && s->variant == 7 && s->threads > k7_max_threads(s)) {
     if (o.threads) {
       rs_free_lanes(s);
-      return set_err(RS_E_INVALID_ARG, "threads > %u for kernel 7 at this shape", k7_max_threads(g, s->cluster));
+      return set_err(RS_E_INVALID_ARG, "threads > %u for kernel 7 at this shape", k7_max_threads(s));
     }
-    s->threads = k7_max_threads(g, s->cluster);
+    s->threads = k7_max_threads(s);
   }
   if (s->repcut) {
     RepCutPlan plan;

@@ -70,7 +70,7 @@ class LaneOpts(C.Structure):
                 ("parts", C.c_uint32), ("kernel", C.c_uint32),
                 ("repcut", C.c_uint32), ("repcut_global", C.c_uint32),
                 ("part_world", C.c_uint32), ("part_rank", C.c_uint32), ("l2_policy", C.c_uint32),
-                ("defer_state", C.c_uint32)]
+                ("defer_state", C.c_uint32), ("op_pairs", C.c_uint32)]
 
 
 _lib = None
@@ -225,13 +225,14 @@ class Lanes:
     def __init__(self, graph: Graph, n_lanes: int, lane0: int = 0, lane_tile: int = 0, threads: int = 0,
                  stage_cycles: int = 0, stream=None, cluster: int = 0, parts: int = 0, kernel: int = 0,
                  repcut: int = 0, repcut_global: int = 0, part_world: int = 0, part_rank: int = 0,
-                 l2_policy: int = 0, state=None):
+                 l2_policy: int = 0, state=None, op_pairs: int = 0):
         self.graph = graph
         self.n_lanes = n_lanes
         self.lane0 = lane0
         st = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
         self.opts = LaneOpts(lane0, lane_tile, threads, stage_cycles, cluster, st, parts, kernel, repcut,
-                             int(repcut_global), part_world, part_rank, l2_policy, 1 if state is not None else 0)
+                             int(repcut_global), part_world, part_rank, l2_policy, 1 if state is not None else 0,
+                             op_pairs)
         h = C.c_void_p()
         _check(lib().rs_alloc_lanes(graph.h, n_lanes, C.byref(self.opts), C.byref(h)))
         self.h = h

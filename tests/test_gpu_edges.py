@@ -62,7 +62,8 @@ GPU_LANE_CASES = [dict(kernel=1, lane_tile=32), dict(kernel=1, lane_tile=64), di
                   dict(kernel=1, lane_tile=64, cluster=2), dict(kernel=2, lane_tile=8),
                   dict(kernel=2, lane_tile=16), dict(kernel=2, lane_tile=32, cluster=2),
                   dict(kernel=6, lane_tile=64), dict(kernel=6, lane_tile=128), dict(kernel=6, lane_tile=128, cluster=2),
-                  dict(kernel=7, lane_tile=64), dict(kernel=7, lane_tile=128), dict(kernel=7, lane_tile=128, cluster=2)]
+                  dict(kernel=7, lane_tile=64), dict(kernel=7, lane_tile=128), dict(kernel=7, lane_tile=128, cluster=2),
+                  dict(kernel=7, lane_tile=32, op_pairs=2), dict(kernel=7, lane_tile=64, cluster=2, op_pairs=2)]
 
 
 @pytest.mark.gpu

@@ -97,6 +97,13 @@ def test_c2_structure_ragged_lanes(rs, lt, cs, kernel):
           kernel=kernel)
 
 
+@pytest.mark.parametrize("lt,cs,pairs", [(32, 1, 2), (32, 4, 2), (64, 2, 2), (128, 1, 2), (128, 4, 1), (64, 1, 1)])
+def test_c2_kernel7_op_pairs(rs, lt, cs, pairs):
+    """Kernel 7 with op pairs forced on (rs_lane_opts.op_pairs = 2; P = 1 included) or off."""
+    check(rs, config_circuit("C2"), 25, 37, seed=CONFIGS["C2"].stim_seed, lane_tile=lt, cluster=cs, kernel=7,
+          op_pairs=pairs)
+
+
 def test_c2_threads_variants(rs):
     c = config_circuit("C2", n_ops=5000, n_levels=40, n_regs=500)
     for th in (64, 256, 512):
