@@ -137,7 +137,8 @@ typedef struct {
                               and level), 1024 single-lane */
   uint32_t stage_cycles;   /* capacity (cycles) of the staged-input ring, 0 = none */
   uint32_t cluster;        /* RS_MODE_LANES: CTAs (a thread-block cluster on as many SMs) sharing one
-                              lane tile, 0 = auto, else 1, 2, 4 or 8 */
+                              lane tile, 0 = auto, else 1, 2, 4 or 8, or 16 (a non-portable cluster size)
+                              for kernel 7 */
   void* stream;            /* cudaStream_t to run on; NULL = a stream the library creates */
   uint32_t parts;          /* RS_MODE_SINGLE level cut: 0/1 = off, else 2..8 partitions,
                               each owning a contiguous level range (balanced by op weight) and a full

@@ -25,6 +25,10 @@
 #ifndef RS_LANES_R_PAIRS_MAX_THREADS
 #define RS_LANES_R_PAIRS_MAX_THREADS 768
 #endif
+// 32-lane tiles (P = 1, single ops) fit 64 registers: 1,024 threads
+#ifndef RS_LANES_R1_MAX_THREADS
+#define RS_LANES_R1_MAX_THREADS 1024
+#endif
 
 namespace rtlsim {
 
@@ -123,84 +127,103 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
   return v;
 }
 
-// OPS stage: records at buf + off_c (h->n of them); this warp takes ops j0, j0 + nw,
-// ... -- interleaved across the runs, so every warp gets the same mix of cheap and
-// expensive ops and the stage barrier waits for nobody in particular.
+// One op from its record at shared address `rec` (base = the stage buffer, for fold lists).
+template <int P, bool HASH>
+__device__ __forceinline__ void op_r(const LaneT& L, uint32_t base, uint32_t rec, uint64_t (&hacc)[P]) {
+  const uint4 r0 = lds128(rec), r1 = lds128(rec + 16);
+  const uint32_t pw = r0.w, oc = r1.x, sel = r1.w, t = (sel >> 8) & 0xffu;
+  const uint64_t K = HASH ? ((uint64_t)r1.z << 32 | r1.y) : 0ull;
+  if (t == kTailFold) {
+    fold_r<P, HASH>(L, base + r0.x, r0.y, sel >> 24, pw, oc, K, hacc);
+    return;
+  }
+  const uint32_t A = (sel >> 16) & 3u;
+#define RS_R4(C, AA, OPC)                                                      \
+  case 4 * C + 0: tail_r<P, HASH, AA, OPC, 0>(L, x, pw, oc, K, hacc); break;   \
+  case 4 * C + 1: tail_r<P, HASH, AA, OPC, 1>(L, x, pw, oc, K, hacc); break;   \
+  case 4 * C + 2: tail_r<P, HASH, AA, OPC, 2>(L, x, pw, oc, K, hacc); break;   \
+  case 4 * C + 3: tail_r<P, HASH, AA, OPC, 3>(L, x, pw, oc, K, hacc); break;
+  // one gather per arity (the class-signature jump tables of gather_brx.cuh), so an op
+  // holds only its own operands' registers
+  if (A == 2) {
+    const uint32_t c[2] = {r0.x, r0.y};
+    uint64_t x[2][P];
+    gather_t<2, P>(L, c, x);
+    switch (t) {
+      RS_R4(5, 2, RS_OP_AND) RS_R4(6, 2, RS_OP_OR) RS_R4(7, 2, RS_OP_XOR) RS_R4(8, 2, RS_OP_ADD)
+      RS_R4(9, 2, RS_OP_SUB) RS_R4(10, 2, RS_OP_MUL) RS_R4(11, 2, RS_OP_EQ) RS_R4(12, 2, RS_OP_LT)
+      RS_R4(13, 2, RS_OP_CAT)
+      default: break;
+    }
+  } else if (A == 1) {
+    const uint32_t c[1] = {r0.x};
+    uint64_t x[1][P];
+    gather_t<1, P>(L, c, x);
+    switch (t) {
+      RS_R4(0, 1, RS_OP_NOT) RS_R4(1, 1, RS_OP_SHL) RS_R4(2, 1, RS_OP_SHR) RS_R4(3, 1, RS_OP_BITS)
+      RS_R4(4, 1, OP_COPY)
+      default: break;
+    }
+  } else {
+    const uint32_t c[3] = {r0.x, r0.y, r0.z};
+    uint64_t x[3][P];
+    gather_t<3, P>(L, c, x);
+    switch (t) {
+      RS_R4(14, 3, RS_OP_AND) RS_R4(15, 3, RS_OP_OR) RS_R4(16, 3, RS_OP_XOR) RS_R4(17, 3, RS_OP_ADD)
+      RS_R4(18, 3, RS_OP_SUB) RS_R4(19, 3, RS_OP_MUL) RS_R4(20, 3, RS_OP_MUX)
+      default: break;
+    }
+  }
+#undef RS_R4
+}
+
+// Two ops with <= 2 operands from records (a0, a1), (b0, b1): both ops' loads are in flight
+// before either is computed (the PSU partial unrolling); a one-operand op is
+// gathered as two-operand.
+template <int P, bool HASH>
+__device__ __forceinline__ void pair_r(const LaneT& L, const uint4& a0, const uint4& a1, const uint4& b0,
+                                       const uint4& b1, uint64_t (&hacc)[P]) {
+  const uint32_t aA = (a1.w >> 16) & 3u, bA = (b1.w >> 16) & 3u;
+  const uint32_t ca[2] = {a0.x, aA == 2u ? a0.y : a0.x}, cb[2] = {b0.x, bA == 2u ? b0.y : b0.x};
+  uint64_t xa[2][P], xb[2][P];
+  gather_t<2, P>(L, ca, xa);
+  gather_t<2, P>(L, cb, xb);
+  tail_pair<P, HASH>(L, xa, a0.w, a1.x, HASH ? ((uint64_t)a1.z << 32 | a1.y) : 0ull, (a1.w >> 8) & 0xffu, hacc);
+  tail_pair<P, HASH>(L, xb, b0.w, b1.x, HASH ? ((uint64_t)b1.z << 32 | b1.y) : 0ull, (b1.w >> 8) & 0xffu, hacc);
+}
+
+__device__ __forceinline__ bool pairable(const uint4& r1) {
+  const uint32_t A = (r1.w >> 16) & 3u;
+  return A == 1u || A == 2u;  // folds carry arity 0, 3-operand ops 3
+}
+
+// OPS stage: records at buf + off_c (h->n of them).
+// This warp takes ops j0, j0 + nw, ... -- interleaved across the runs, so every warp gets
+// the same mix of cheap and expensive ops and the stage barrier waits for nobody in
+// particular (dynamic claiming from a shared-memory counter lost: C3 1.185 vs 1.150 ms
+// per cycle, C2 153 vs 125 us).  PAIRS (allocations with many ops per CTA and level;
+// measured: C4 37.5 -> 31.6 ms per cycle, C3 1.23 -> 1.29 ms, so C3 stays single): ops
+// with <= 2 operands (sorted first in every level) in pairs.
 template <int P, bool HASH, bool PAIRS>
 __device__ __forceinline__ void stage_ops_r(const LaneT& L, const uint8_t* buf, uint32_t j0, uint32_t nw,
                                             uint64_t (&hacc)[P]) {
   const StageHdr* h = reinterpret_cast<const StageHdr*>(buf);
   const uint32_t base = smem_addr(buf), rec0 = base + h->off_c, n = h->n;
   uint32_t j = j0;
-  // pairs of ops with <= 2 operands (allocations with many ops per CTA and level, the
-  // PAIRS instantiation; measured: C4 37.5 -> 31.6 ms per cycle, C3 1.23 -> 1.29 ms, so C3
-  // stays single): both ops' loads are in flight before either is computed (the PSU
-  // partial unrolling); a one-operand op is gathered as two-operand
 #pragma unroll 1
   for (; PAIRS && j + nw < n; j += 2 * nw) {
     const uint4 a0 = lds128(rec0 + kRecBytes * j), a1 = lds128(rec0 + kRecBytes * j + 16);
     const uint4 b0 = lds128(rec0 + kRecBytes * (j + nw)), b1 = lds128(rec0 + kRecBytes * (j + nw) + 16);
-    const uint32_t aA = (a1.w >> 16) & 3u, bA = (b1.w >> 16) & 3u;
-    if (aA == 0u || aA == 3u || bA == 0u || bA == 3u) break;  // a fold or a 3-operand op: single path
-    const uint32_t ca[2] = {a0.x, aA == 2u ? a0.y : a0.x}, cb[2] = {b0.x, bA == 2u ? b0.y : b0.x};
-    uint64_t xa[2][P], xb[2][P];
-    gather_t<2, P>(L, ca, xa);
-    gather_t<2, P>(L, cb, xb);
-    tail_pair<P, HASH>(L, xa, a0.w, a1.x, HASH ? ((uint64_t)a1.z << 32 | a1.y) : 0ull, (a1.w >> 8) & 0xffu, hacc);
-    tail_pair<P, HASH>(L, xb, b0.w, b1.x, HASH ? ((uint64_t)b1.z << 32 | b1.y) : 0ull, (b1.w >> 8) & 0xffu, hacc);
+    if (!pairable(a1) || !pairable(b1)) break;  // a fold or a 3-operand op: single path
+    pair_r<P, HASH>(L, a0, a1, b0, b1, hacc);
   }
 #pragma unroll 1
-  for (; j < n; j += nw) {
-    const uint4 r0 = lds128(rec0 + kRecBytes * j), r1 = lds128(rec0 + kRecBytes * j + 16);
-    const uint32_t pw = r0.w, oc = r1.x, sel = r1.w, t = (sel >> 8) & 0xffu;
-    const uint64_t K = HASH ? ((uint64_t)r1.z << 32 | r1.y) : 0ull;
-    if (t == kTailFold) {
-      fold_r<P, HASH>(L, base + r0.x, r0.y, sel >> 24, pw, oc, K, hacc);
-      continue;
-    }
-    const uint32_t A = (sel >> 16) & 3u;
-#define RS_R4(C, AA, OPC)                                                      \
-  case 4 * C + 0: tail_r<P, HASH, AA, OPC, 0>(L, x, pw, oc, K, hacc); break;   \
-  case 4 * C + 1: tail_r<P, HASH, AA, OPC, 1>(L, x, pw, oc, K, hacc); break;   \
-  case 4 * C + 2: tail_r<P, HASH, AA, OPC, 2>(L, x, pw, oc, K, hacc); break;   \
-  case 4 * C + 3: tail_r<P, HASH, AA, OPC, 3>(L, x, pw, oc, K, hacc); break;
-    // one gather per arity (the class-signature jump tables of gather_brx.cuh), so an op
-    // holds only its own operands' registers
-    if (A == 2) {
-      const uint32_t c[2] = {r0.x, r0.y};
-      uint64_t x[2][P];
-      gather_t<2, P>(L, c, x);
-      switch (t) {
-        RS_R4(5, 2, RS_OP_AND) RS_R4(6, 2, RS_OP_OR) RS_R4(7, 2, RS_OP_XOR) RS_R4(8, 2, RS_OP_ADD)
-        RS_R4(9, 2, RS_OP_SUB) RS_R4(10, 2, RS_OP_MUL) RS_R4(11, 2, RS_OP_EQ) RS_R4(12, 2, RS_OP_LT)
-        RS_R4(13, 2, RS_OP_CAT)
-        default: break;
-      }
-    } else if (A == 1) {
-      const uint32_t c[1] = {r0.x};
-      uint64_t x[1][P];
-      gather_t<1, P>(L, c, x);
-      switch (t) {
-        RS_R4(0, 1, RS_OP_NOT) RS_R4(1, 1, RS_OP_SHL) RS_R4(2, 1, RS_OP_SHR) RS_R4(3, 1, RS_OP_BITS)
-        RS_R4(4, 1, OP_COPY)
-        default: break;
-      }
-    } else {
-      const uint32_t c[3] = {r0.x, r0.y, r0.z};
-      uint64_t x[3][P];
-      gather_t<3, P>(L, c, x);
-      switch (t) {
-        RS_R4(14, 3, RS_OP_AND) RS_R4(15, 3, RS_OP_OR) RS_R4(16, 3, RS_OP_XOR) RS_R4(17, 3, RS_OP_ADD)
-        RS_R4(18, 3, RS_OP_SUB) RS_R4(19, 3, RS_OP_MUL) RS_R4(20, 3, RS_OP_MUX)
-        default: break;
-      }
-    }
-#undef RS_R4
-  }
+  for (; j < n; j += nw) op_r<P, HASH>(L, base, rec0 + kRecBytes * j, hacc);
 }
 
 template <int P, bool HASH, bool PAIRS>
-__global__ void __launch_bounds__(PAIRS ? RS_LANES_R_PAIRS_MAX_THREADS : RS_LANES_R_MAX_THREADS, 1)
+__global__ void __launch_bounds__(PAIRS ? RS_LANES_R_PAIRS_MAX_THREADS
+                                        : P == 1 ? RS_LANES_R1_MAX_THREADS : RS_LANES_R_MAX_THREADS, 1)
     k_lanes_r(const StepArgs a) {
   constexpr uint32_t LT = 32u * P;
   extern __shared__ __align__(128) uint8_t smem[];

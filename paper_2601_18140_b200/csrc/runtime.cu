@@ -531,7 +531,9 @@ bool wide_items(const rs_graph* g, uint32_t cluster) {
 // kernel 7 evaluates ops in pairs (rs_lane_opts.op_pairs; auto: >= 2,048 ops per CTA and level)
 bool k7_pairs(const rs_lanes* s) { return s->op_pairs ? s->op_pairs == 2u : wide_items(s->g, s->cluster); }
 uint32_t k7_max_threads(const rs_lanes* s) {
-  return k7_pairs(s) ? (uint32_t)RS_LANES_R_PAIRS_MAX_THREADS : (uint32_t)RS_LANES_R_MAX_THREADS;
+  return k7_pairs(s)     ? (uint32_t)RS_LANES_R_PAIRS_MAX_THREADS
+         : s->LT == 32u ? (uint32_t)RS_LANES_R1_MAX_THREADS
+                        : (uint32_t)RS_LANES_R_MAX_THREADS;
 }
 
 const void* lane_kernel_fn(const rs_lanes* s, bool hash) {
@@ -553,6 +555,13 @@ cudaError_t raise_smem_attr(int device, size_t smem) {
   static thread_local size_t attr_set[64] = {};
   size_t& have = attr_set[device & 63];
   if (have >= smem) return cudaSuccess;
+  if (have == 0) {
+    // 16-CTA clusters (kernel 7 only) are a non-portable cluster size
+    for (const void* f : kLaneFns) {
+      const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
+  }
   for (const void* f : kLaneFns) {
     const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -878,9 +887,10 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
       return set_err(RS_E_INVALID_ARG, "lane_tile must be 32, 64 or 128 (kernels 1 and 7), 8, 16 or 32 (kernel 2) "
                                        "or 64 or 128 (kernel 6)");
     }
-    if (o.cluster && o.cluster != 1 && o.cluster != 2 && o.cluster != 4 && o.cluster != 8) {
+    if (o.cluster && o.cluster != 1 && o.cluster != 2 && o.cluster != 4 && o.cluster != 8 &&
+        !(o.cluster == 16 && kern == 7)) {
       rs_free_lanes(s);  // partially built: frees what exists
-      return set_err(RS_E_INVALID_ARG, "cluster must be 1, 2, 4 or 8");
+      return set_err(RS_E_INVALID_ARG, "cluster must be 1, 2, 4 or 8 (or 16 for kernel 7)");
     }
     if (o.kernel > 2 && o.kernel != 6 && o.kernel != 7) {
       rs_free_lanes(s);  // partially built: frees what exists

@@ -18,11 +18,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 def run_gpu(rs, c, n_cycles, n_lanes=1, seed=0, mode="lanes", lane0=0, lane_tile=0, threads=0,
             staged=None, chunks=None, final=True, cluster=0, parts=0, kernel=0, repcut=0,
-            repcut_global=False, l2_policy=0):
+            repcut_global=False, l2_policy=0, op_pairs=0):
     g = rs.Graph(c, device=0, mode=mode)
     L = rs.Lanes(g, n_lanes, lane0=lane0, lane_tile=lane_tile, threads=threads, cluster=cluster,
                  stage_cycles=(n_cycles if staged is not None else 0), parts=parts, kernel=kernel,
-                 repcut=repcut, repcut_global=repcut_global, l2_policy=l2_policy)
+                 repcut=repcut, repcut_global=repcut_global, l2_policy=l2_policy, op_pairs=op_pairs)
     if staged is not None:
         L.set_inputs(0, staged)
     else:
@@ -101,6 +101,13 @@ def test_c2_structure_ragged_lanes(rs, lt, cs, kernel):
 def test_c2_kernel7_op_pairs(rs, lt, cs, pairs):
     """Kernel 7 with op pairs forced on (rs_lane_opts.op_pairs = 2; P = 1 included) or off."""
     check(rs, config_circuit("C2"), 25, 37, seed=CONFIGS["C2"].stim_seed, lane_tile=lt, cluster=cs, kernel=7,
+          op_pairs=pairs)
+
+
+@pytest.mark.parametrize("lt,pairs", [(128, 1), (64, 2), (32, 1)])
+def test_c2_kernel7_cluster16(rs, lt, pairs):
+    """Kernel 7 on 16-CTA (non-portable) clusters, ragged last tile."""
+    check(rs, config_circuit("C2"), 25, 300, seed=CONFIGS["C2"].stim_seed, lane_tile=lt, cluster=16, kernel=7,
           op_pairs=pairs)
 
 
