@@ -278,7 +278,7 @@ def main():
     ap.add_argument("--lane-tile", type=int, default=0)
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--cluster", type=int, default=0)
-    ap.add_argument("--kernel", type=int, default=0, help="lane kernel: 0 auto, 1 lane/thread, 2 two lanes/thread")
+    ap.add_argument("--kernel", type=int, default=0, help="rs_lane_opts.kernel (0 auto; C1 defaults to 8, specialised)")
     ap.add_argument("--parts", type=int, default=0, help="C1/C5: level-cut partitions emulated on this GPU")
     ap.add_argument("--repcut", type=int, default=0, help="single-lane configs: RepCut partitions (rs_lane_opts.repcut)")
     ap.add_argument("--ref-step-s", type=float, default=4.0)
@@ -330,8 +330,11 @@ def main():
     g = rs.Graph(circ, device=dev, mode="single" if single else "lanes", passes=not args.no_passes)
     info = g.info()
     info0 = rs.Graph(circ, device=rs.RS_DEVICE_NONE, mode="single" if single else "lanes").info()
+    kernel = args.kernel
+    if kernel == 0 and args.config == "C1" and args.parts <= 1 and not args.repcut and not args.watch:
+        kernel = 8  # C1 fits the specialised kernel (rs_specialize): 1.53 vs 4.07 us per cycle (RepCut)
     mk = dict(lane0=shard.lane0, lane_tile=args.lane_tile, threads=args.threads, stream=stream,
-              cluster=args.cluster, parts=args.parts, kernel=args.kernel, repcut=args.repcut,
+              cluster=args.cluster, parts=args.parts, kernel=kernel, repcut=args.repcut,
               l2_policy=args.l2_policy if not single else 0, op_pairs=args.op_pairs)
     if levelcut:
         L = rs.Lanes(g, 1, stream=stream, part_world=world, part_rank=rank)
@@ -372,7 +375,7 @@ def main():
 
     kid = L.shape()["kernel"]
     kernel_name = {1: "k_lanes_t", 2: "k_lanes", 3: "k_repcut_smem", 4: "k_repcut", 5: "k_single2", 6: "k_lanes_b",
-                   7: "k_lanes_r"}.get(kid, "?")
+                   7: "k_lanes_r", 8: "rs_su (specialised PTX)"}.get(kid, "?")
     # roofline of the dominant (only) kernel: algorithmic bytes per launch / launch duration
     # (this rank's launch; the max-over-ranks time)
     bytes_per_cycle = lanes * info["alg_bytes_per_lane_cycle"] + info["graph_alg_bytes"]

@@ -160,7 +160,12 @@ typedef struct {
                               RS_MODE_SINGLE: 0 = auto (RepCut with one partition when the whole design
                               fits one SM's shared memory, else the level-synchronous grid); 3 = RepCut,
                               shared-memory slices; 4 = RepCut, global replicas; 5 = level-synchronous
-                              grid (k_single2; the level cut uses it). */
+                              grid (k_single2; the level cut uses it).
+                              Both modes: 8 = the design's own specialised kernel (rs_specialize: every op
+                              a straight-line expression with its operands, widths and hash weight baked
+                              in, one thread per lane, the SU analog of PAPER.md
+                              P:1215-1216); lane_tile 0/32/64/128 sets the state layout only; excludes
+                              parts / repcut / part_world and waveform capture.  Errors of rs_specialize. */
   uint32_t repcut;         /* RS_MODE_SINGLE replicated cut (App. C, Cascade 2; SURVEY.md §8(f)
                               NEXT-2): 0 = off, else P >= 1 partitions = CTAs of one cooperative launch; the
                               registers are cut into P contiguous blocks, partition p evaluates the cone of
@@ -242,6 +247,24 @@ rs_status rs_repcut_stats(const rs_graph* g, uint32_t P, uint64_t* ops_total, ui
  * is caller-owned host memory of parts + 1 entries.  Host-only (works on a
  * RS_DEVICE_NONE graph).  RS_E_INVALID_ARG if parts is 0, > 8 or > n_levels. */
 rs_status rs_level_cut(const rs_graph* g, uint32_t parts, uint32_t* cut);
+
+/* Per-design specialisation (rs_lane_opts.kernel = 8; §5.2
+ * P:1215-1216 "S fully unrolled; OIM embedded in the binary", Tables 4-6): generate the
+ * design's step kernel as PTX for sm_100a -- each op of the compiled graph (after
+ * RS_LOAD_PASSES, if given) a few register instructions with its operands, widths,
+ * parameters and hash weight as immediates, the design's registers held in registers
+ * across cycles, one thread per lane -- and load it (the driver JIT-compiles it).  Cached
+ * in the graph; rs_alloc_lanes(kernel = 8) calls it.  With RS_DEVICE_NONE it only
+ * generates the PTX (see rs_specialized_ptx).
+ * Errors: RS_E_CAPACITY above 4,096 ops (ptxas time grows superlinearly with the
+ * straight-line cycle: 0.4 s for C1's 256 ops, 25 min for C2's 20k); RS_E_CUDA if the JIT
+ * or the module load fails. */
+rs_status rs_specialize(rs_graph* g);
+
+/* The PTX rs_specialize generated (host memory, caller-owned): copies at most cap - 1
+ * bytes + a NUL into buf (buf may be NULL), *len = the full length.  RS_E_STATE before
+ * rs_specialize. */
+rs_status rs_specialized_ptx(const rs_graph* g, char* buf, uint64_t cap, uint64_t* len);
 
 /* Allocate the signal state for n_lanes lanes (RS_MODE_SINGLE: n_lanes must
  * be 1), initialised to: registers = init & M(w), constants = value, all

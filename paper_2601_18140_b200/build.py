@@ -17,8 +17,8 @@ LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "librtlsim.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["runtime.cu", "compiler.cpp", "passes.cpp"]
-HEADERS = ["kernels.cuh", "lanes.cuh", "lanes_t.cuh", "gather_brx.cuh", "lanes_b.cuh", "gather_b.cuh", "lanes_r.cuh", "single.cuh", "repcut.cuh", "compiler.hpp"]
+SOURCES = ["runtime.cu", "compiler.cpp", "passes.cpp", "codegen.cpp"]
+HEADERS = ["kernels.cuh", "lanes.cuh", "lanes_t.cuh", "gather_brx.cuh", "lanes_b.cuh", "gather_b.cuh", "lanes_r.cuh", "single.cuh", "repcut.cuh", "compiler.hpp", "codegen.hpp"]
 
 
 def _newest_input() -> float:

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "../../include/rtlsim.h"
+#include "codegen.hpp"
 #include "compiler.hpp"
 #include "kernels.cuh"
 #include "lanes.cuh"
@@ -79,6 +80,11 @@ struct rs_graph {
   std::vector<StageRef> stage_tab[2];
   bool stages_built[2] = {false, false};
   uint32_t stage_bytes = 0;
+  // kernel 8 (codegen.hpp): the design's specialised kernel, compiled once (rs_specialize)
+  bool su_built = false;
+  std::string su_ptx;
+  cudaLibrary_t su_lib = nullptr;
+  cudaKernel_t su_fn = nullptr;
 };
 
 struct rs_lanes {
@@ -759,12 +765,49 @@ rs_status rs_level_cut(const rs_graph* g, uint32_t parts, uint32_t* cut) {
   return RS_OK;
 }
 
+rs_status rs_specialize(rs_graph* g) {
+  NvtxRange nvtx_range("rs_specialize");
+  if (!g) return set_err(RS_E_INVALID_ARG, "NULL graph");
+  if (!g->su_built) {
+    if (g->cg.n_ops_total() > kSuMaxOps)
+      return set_err(RS_E_CAPACITY, "kernel 8 (specialised) is capped at %u ops (graph has %u)", kSuMaxOps,
+                     g->cg.n_ops_total());
+    g->su_ptx = su_ptx(g->cg);
+    g->su_built = true;
+  }
+  if (g->dmem && !g->su_fn) {
+    rs_status st = set_device(g);
+    if (st != RS_OK) return st;
+    // the driver JIT-compiles the PTX for this device (ptxas)
+    cudaError_t e = cudaLibraryLoadData(&g->su_lib, g->su_ptx.c_str(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+    if (e == cudaSuccess) e = cudaLibraryGetKernel(&g->su_fn, g->su_lib, "rs_su");
+    if (e != cudaSuccess) {
+      g->su_fn = nullptr;
+      return set_err(RS_E_CUDA, "kernel 8 load (PTX JIT): %s", cudaGetErrorString(e));
+    }
+  }
+  return RS_OK;
+}
+
+rs_status rs_specialized_ptx(const rs_graph* g, char* buf, uint64_t cap, uint64_t* len) {
+  if (!g) return set_err(RS_E_INVALID_ARG, "NULL graph");
+  if (!g->su_built) return set_err(RS_E_STATE, "rs_specialize first");
+  if (len) *len = g->su_ptx.size();
+  if (buf && cap) {
+    const size_t n = (size_t)std::min<uint64_t>(cap - 1, g->su_ptx.size());
+    std::memcpy(buf, g->su_ptx.data(), n);
+    buf[n] = 0;
+  }
+  return RS_OK;
+}
+
 void rs_free_graph(rs_graph* g) {
   if (!g) return;
   if (g->dmem) {
     cudaSetDevice(g->device);
     cudaFree(g->dmem);
   }
+  if (g->su_lib) cudaLibraryUnload(g->su_lib);
   delete g;
 }
 
@@ -788,10 +831,31 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
   s->g = g;
   s->n_lanes = n_lanes;
   s->lane0 = o.lane0;
-  if (g->cg.mode == RS_MODE_SINGLE && o.kernel && o.kernel != 3 && o.kernel != 4 && o.kernel != 5) {
+  if (g->cg.mode == RS_MODE_SINGLE && o.kernel && o.kernel != 3 && o.kernel != 4 && o.kernel != 5 && o.kernel != 8) {
     rs_free_lanes(s);
     return set_err(RS_E_INVALID_ARG, "single-lane kernel must be 0 (auto), 3 (RepCut, shared memory), 4 (RepCut, "
-                                     "global replicas) or 5 (level-synchronous grid)");
+                                     "global replicas), 5 (level-synchronous grid) or 8 (specialised)");
+  }
+  if (o.kernel == 8) {  // the design's own straight-line kernel (codegen.hpp): one thread per lane
+    if (o.parts > 1 || o.repcut || o.part_world) {
+      rs_free_lanes(s);
+      return set_err(RS_E_INVALID_ARG, "kernel 8 (specialised) excludes parts / repcut / part_world");
+    }
+    if (o.lane_tile && o.lane_tile != 32 && o.lane_tile != 64 && o.lane_tile != 128) {
+      rs_free_lanes(s);
+      return set_err(RS_E_INVALID_ARG, "kernel 8: lane_tile must be 0, 32, 64 or 128");
+    }
+    rs_status st8 = rs_specialize(g);
+    if (st8 != RS_OK) {
+      rs_free_lanes(s);
+      return st8;
+    }
+    s->variant = 8;
+    s->LT = g->cg.mode == RS_MODE_SINGLE ? 1u : (o.lane_tile ? o.lane_tile : 32u);
+    s->n_tiles = (n_lanes + s->LT - 1) / s->LT;
+    s->parts = 1;
+    s->threads = g->cg.mode == RS_MODE_SINGLE ? 32u : 128u;
+    s->ctas = (n_lanes + s->threads - 1) / s->threads;
   }
   if (g->cg.mode == RS_MODE_SINGLE && (o.kernel == 3 || o.kernel == 4) && !o.repcut) o.repcut = 1;
   if (g->cg.mode == RS_MODE_SINGLE && o.kernel == 4) o.repcut_global = 1;
@@ -849,7 +913,9 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
         build_repcut_slices(g->cg, plan, kRepSmemMax, false, &b1, &b3, &b4, &b2, &err))
       o.repcut = 1;
   }
-  if (g->cg.mode == RS_MODE_SINGLE && o.repcut >= 1) {
+  if (s->variant == 8) {
+    // shape set above (one thread per lane, LT-lane tiles of the usual layout)
+  } else if (g->cg.mode == RS_MODE_SINGLE && o.repcut >= 1) {
     if (o.parts > 1 || o.repcut > (uint32_t)g->sm_count) {
       rs_free_lanes(s);  // partially built: frees what exists
       return set_err(RS_E_INVALID_ARG, "repcut = %u: must be <= %d SMs and not combined with parts (level cut)", o.repcut,
@@ -909,7 +975,9 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     s->n_tiles = (n_lanes + lt - 1) / lt;
   }
   // launch shape
-  if (o.threads) {
+  if (s->variant == 8) {
+    // set with the kernel choice
+  } else if (o.threads) {
     const uint32_t tmax = g->cg.mode == RS_MODE_SINGLE ? 1024u
                           : s->variant == 1            ? (uint32_t)RS_LANES_T_MAX_THREADS
                           : s->variant == 6            ? (uint32_t)RS_LANES_B_MAX_THREADS
@@ -934,7 +1002,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
   }
   // lane mode: every cluster of the launch must be co-resident, else the launch runs in
   // waves; an automatic shape halves its cluster until it fits (fewer CTAs, one wave)
-  if (g->cg.mode == RS_MODE_LANES && !o.cluster) {
+  if (g->cg.mode == RS_MODE_LANES && !o.cluster && s->variant != 8) {
     s->batch_idx = 0;  // not chosen yet; it only picks a kernel-7 variant of the same shared memory
     int fit = co_resident_clusters(s);
     while (fit >= 0 && (uint32_t)fit < s->n_tiles && s->cluster > 1) {
@@ -1048,6 +1116,8 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
         return set_err(RS_E_CUDA, "repcut smem attribute: %s", cudaGetErrorString(e2));
       }
     }
+  } else if (s->variant == 8) {
+    // shape set with the kernel choice
   } else if (g->cg.mode == RS_MODE_SINGLE) {
     const uint32_t work = std::max<uint32_t>(1, std::max(g->cg.n_inputs, g->cg.n_regs));
     uint32_t maxops = 0;
@@ -1156,7 +1226,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     rs_free_lanes(s);  // partially built: frees what exists
     return set_err(RS_E_OOM, "cudaMalloc state (%zu B): %s", s->state_bytes, cudaGetErrorString(e));
   }
-  if (g->cg.mode == RS_MODE_LANES) {
+  if (g->cg.mode == RS_MODE_LANES && s->variant != 8) {
     // work items: kernel 1 takes kBatchWide-op items when its CTAs have many ops
     // per level (C4: ~6,700; fewer, longer items cut the per-item decode), else
     // kBatch-op items (more items to deal when a level is short: C3 ~470)
@@ -1463,7 +1533,26 @@ rs_status rs_step_cycles(rs_lanes* s, uint32_t n_cycles, uint64_t* hashes, int h
   a.hashes = hout;
   const size_t lanes_pad = (size_t)s->n_tiles * s->LT;
   a.hcarry_in = s->hcarry + s->hc_cur * lanes_pad;
-  if (s->g->cg.mode == RS_MODE_SINGLE) {
+  if (s->variant == 8) {  // the design's specialised kernel (codegen.hpp)
+    SuArgs u{};
+    u.state = a.state;
+    u.tile_bytes = a.tile_bytes;
+    for (int c = 0; c < 4; ++c) u.region[c] = a.region[c];
+    u.LT = s->LT;
+    u.n_lanes = s->n_lanes;
+    u.lane0 = s->lane0;
+    u.cycle0 = a.cycle0;
+    u.n_cycles = n_cycles;
+    u.staged = a.staged ? 1u : 0u;
+    u.seed = a.seed;
+    u.stage = a.stage;
+    u.stage_cap = a.stage_cap;
+    u.hashes = hout;
+    u.hcarry = a.hcarry_in;
+    void* args[] = {&u};
+    cudaError_t e = cudaLaunchKernel((const void*)s->g->su_fn, dim3(s->ctas), dim3(s->threads), args, 0, s->stream);
+    if (e != cudaSuccess) return set_err(RS_E_CUDA, "kernel 8 launch: %s", cudaGetErrorString(e));
+  } else if (s->g->cg.mode == RS_MODE_SINGLE) {
     a.hcarry_out = s->hcarry + (1 - s->hc_cur) * lanes_pad;
     if (hash) {
       CU(cudaMemsetAsync(a.hcarry_out, 0, 8, s->stream));
@@ -1759,6 +1848,7 @@ rs_status rs_debug_trace(rs_lanes* s, uint64_t* out, uint64_t n) {
 rs_status rs_watch(rs_lanes* s, const uint32_t* ids, uint32_t n_ids, uint64_t capacity) {
   if (!s || (n_ids && !ids)) return set_err(RS_E_INVALID_ARG, "NULL argument");
   const bool single = s->g->cg.mode == RS_MODE_SINGLE;
+  if (s->variant == 8) return set_err(RS_E_UNSUPPORTED, "waveform capture is not built into kernel 8 (specialised)");
   if (single && (s->parts > 1 && !s->repcut))
     return set_err(RS_E_UNSUPPORTED, "waveform capture with a level cut (parts > 1) is not supported");
   if (single && s->repcut && !s->rep_smem)
@@ -1859,7 +1949,7 @@ rs_status rs_wave_read(rs_lanes* s, rs_change* out, uint64_t cap, uint64_t* n_ou
 
 uint32_t rs_lanes_kernel(const rs_lanes* s) {
   if (!s) return 0u;
-  if (s->g->cg.mode == RS_MODE_LANES) return s->variant;
+  if (s->g->cg.mode == RS_MODE_LANES || s->variant == 8) return s->variant;
   return s->repcut ? (s->rep_smem ? 3u : 4u) : 5u;
 }
 

@@ -27,7 +27,8 @@ EXPORTS = ["rs_version", "rs_last_error", "rs_load_graph", "rs_graph_info_get", 
            "rs_alloc_lanes", "rs_free_lanes", "rs_lanes_bytes", "rs_set_input_seed", "rs_set_inputs",
            "rs_step_cycles", "rs_read_signals", "rs_write_registers", "rs_get_cycle", "rs_set_cycle",
            "rs_launch_count", "rs_launch_shape", "rs_lanes_kernel", "rs_repcut_stats", "rs_watch", "rs_wave_read", "rs_sync", "rs_graph_export", "rs_debug_trace",
-           "rs_level_cut", "rs_ipc_handle", "rs_ipc_connect", "rs_lanes_state_bytes", "rs_lanes_bind_state"]
+           "rs_level_cut", "rs_ipc_handle", "rs_ipc_connect", "rs_lanes_state_bytes", "rs_lanes_bind_state",
+           "rs_specialize", "rs_specialized_ptx"]
 RS_DEVICE_NONE = -1
 EXPORT = {"runs": (0, np.uint32), "level_run_begin": (1, np.uint32), "level_op_begin": (2, np.uint32),
           "opw": (3, np.uint32), "opk": (4, np.uint64), "coord_off": (5, np.uint32), "coord": (6, np.uint32),
@@ -116,6 +117,8 @@ def lib() -> C.CDLL:
             "rs_ipc_connect": (i32, [vp, vp]),
             "rs_lanes_state_bytes": (u64, [vp]),
             "rs_lanes_bind_state": (i32, [vp, vp, u64]),
+            "rs_specialize": (i32, [vp]),
+            "rs_specialized_ptx": (i32, [vp, vp, u64, C.POINTER(u64)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -199,6 +202,15 @@ class Graph:
         t, m, p = C.c_uint64(), C.c_uint32(), C.c_uint64()
         _check(lib().rs_repcut_stats(self.h, parts, C.byref(t), C.byref(m), C.byref(p)))
         return {"ops_total": t.value, "max_ops": m.value, "push": p.value}
+
+    def specialize(self) -> str:
+        """rs_specialize: generate (and, on a device, load) this design's kernel 8; returns its PTX."""
+        _check(lib().rs_specialize(self.h))
+        n = C.c_uint64()
+        _check(lib().rs_specialized_ptx(self.h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        _check(lib().rs_specialized_ptx(self.h, buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
 
     def level_cut(self, parts: int) -> np.ndarray:
         """rs_level_cut: level boundaries [parts + 1] of a parts-way level cut."""
