@@ -332,7 +332,7 @@ def main():
     info0 = rs.Graph(circ, device=rs.RS_DEVICE_NONE, mode="single" if single else "lanes").info()
     kernel = args.kernel
     if kernel == 0 and args.config == "C1" and args.parts <= 1 and not args.repcut and not args.watch:
-        kernel = 8  # C1 fits the specialised kernel (rs_specialize): 1.53 vs 4.07 us per cycle (RepCut)
+        kernel = 8  # C1 fits the specialised kernel (rs_specialize): 1.02 vs 4.07 us per cycle (RepCut)
     mk = dict(lane0=shard.lane0, lane_tile=args.lane_tile, threads=args.threads, stream=stream,
               cluster=args.cluster, parts=args.parts, kernel=kernel, repcut=args.repcut,
               l2_policy=args.l2_policy if not single else 0, op_pairs=args.op_pairs)

@@ -14,9 +14,12 @@
 // accumulator plus a 32-bit high one: v·K = lo·Klo + 2^32 (lo·Khi + hi·Klo) mod 2^64.
 #include "codegen.hpp"
 
+#include <algorithm>
 #include <cinttypes>
 #include <cstdio>
+#include <cstdlib>
 #include <unordered_map>
+#include <unordered_set>
 
 namespace rtlsim {
 namespace {
@@ -71,7 +74,7 @@ class Gen {
   // hash accumulators: kAcc independent (lo, hi) pairs, dealt round-robin, so the Σ v·K
   // chain does not serialise the cycle on the multiply-add latency
   static constexpr int kAcc = 8;
-  std::string hl_[kAcc], hh_[kAcc], wl_, pw0_, pst_;
+  std::string hl_[kAcc], hh_[kAcc], wl_, wid_, pw0_, pst_;
   int acc_ = 0;
   void acc_zero(uint64_t init);
   std::string acc_sum();  // H = Σ hl + (Σ hh << 32)
@@ -85,6 +88,18 @@ class Gen {
   void store(uint32_t coord, const Val& v);
   std::string op_expr(uint32_t j);
   void body(bool wb);
+  void inputs(const std::string& sfx, bool do_hash, bool do_store);
+  // multi-warp single lane (W_ > 1): ops of every level dealt to W_ warps, values another
+  // warp reads exchanged through shared memory, one named barrier per level
+  uint32_t W_ = 1;
+  std::vector<uint32_t> owner_;          // op -> warp
+  std::vector<int32_t> xslot_;           // op -> shared slot of its value (another warp reads it), or -1
+  uint32_t n_x_ = 0, off_reg_ = 0, off_hs_ = 0, smem_bytes_ = 0;
+  std::string smb_, ci_par_;             // shared base address (u32), cycle parity
+  void plan_warps();
+  void body_mw(uint32_t w, bool wb);
+ public:
+  uint32_t threads() const { return warp_ ? 32u * W_ : 128u; }
 };
 
 std::string Gen::as(const Val& v, bool w64) {
@@ -251,9 +266,7 @@ std::string Gen::op_expr(uint32_t j) {
   return d;
 }
 
-void Gen::body(bool wb) {
-  const std::string sfx = wb ? "_w" : "_l";
-  acc_zero(cg_.const_hash);
+void Gen::inputs(const std::string& sfx, bool do_hash, bool do_store) {
   // step 1: inputs (staged ring or counter-based stimulus)
   const uint32_t NI = cg_.n_inputs;
   if (NI) {
@@ -314,10 +327,16 @@ void Gen::body(bool wb) {
     }
     e_.label("INJ" + sfx);
     for (uint32_t k = 0; k < NI; ++k) {
-      hash_add(sig(cg_.in_coord[k]), cg_.in_k[k]);
-      if (wb) store(cg_.in_coord[k], sig(cg_.in_coord[k]));
+      if (do_hash) hash_add(sig(cg_.in_coord[k]), cg_.in_k[k]);
+      if (do_store) store(cg_.in_coord[k], sig(cg_.in_coord[k]));
     }
   }
+}
+
+void Gen::body(bool wb) {
+  const std::string sfx = wb ? "_w" : "_l";
+  acc_zero(cg_.const_hash);
+  inputs(sfx, true, wb);
   // register term of the hash (values at the start of the cycle)
   for (uint32_t j = 0; j < cg_.n_regs; ++j) hash_add(sig(cg_.reg_coord[j]), cg_.reg_k[j]);
   // steps 2a-2c, level by level (device order is level-major)
@@ -370,6 +389,157 @@ void Gen::body(bool wb) {
   }
 }
 
+void Gen::plan_warps() {
+  const uint32_t NO = cg_.n_ops_total(), NL = cg_.n_levels;
+  W_ = 1;
+  if (!warp_ || NO == 0) return;
+  const uint32_t avg = NO / std::max<uint32_t>(1, NL);
+  // measured on C1 (18.6 ops per level; profiles/r02/kernel8): 1 / 2 / 3 / 4 / 6 / 8 warps = 1.53 / 1.33 /
+  // 1.18 / 1.05 / 1.02 / 1.09 us per cycle
+  W_ = std::min<uint32_t>(8, std::max<uint32_t>(1, avg / 3));
+  if (const char* e = std::getenv("RTLSIM_K8_WARPS")) W_ = std::min<uint32_t>(8, std::max(1, std::atoi(e)));
+  if (W_ == 1) return;
+  std::unordered_map<uint32_t, uint32_t> prod;  // op output coordinate -> op
+  for (uint32_t j = 0; j < NO; ++j) prod[out_coord_[j]] = j;
+  owner_.assign(NO, 0);
+  for (uint32_t l = 0; l < NL; ++l) {
+    const uint32_t lb = cg_.level_op_begin[l], le = cg_.level_op_begin[l + 1], cap = (le - lb + W_ - 1) / W_;
+    std::vector<uint32_t> load(W_, 0);
+    for (uint32_t j = lb; j < le; ++j) {  // the warp that produced most operands, among those with room
+      std::vector<uint32_t> score(W_, 0);
+      for (uint32_t o = cg_.coord_off[j]; o < cg_.coord_off[j + 1]; ++o) {
+        auto it = prod.find(cg_.coord[o]);
+        if (it != prod.end()) score[owner_[it->second]]++;
+      }
+      uint32_t best = W_;
+      for (uint32_t w = 0; w < W_; ++w) {
+        if (load[w] >= cap) continue;
+        if (best == W_ || score[w] > score[best] || (score[w] == score[best] && load[w] < load[best])) best = w;
+      }
+      owner_[j] = best;
+      load[best]++;
+    }
+  }
+  xslot_.assign(NO, -1);
+  for (uint32_t j = 0; j < NO; ++j)
+    for (uint32_t o = cg_.coord_off[j]; o < cg_.coord_off[j + 1]; ++o) {
+      auto it = prod.find(cg_.coord[o]);
+      if (it != prod.end() && owner_[it->second] != owner_[j] && xslot_[it->second] < 0)
+        xslot_[it->second] = (int32_t)n_x_++;
+    }
+  off_reg_ = 8 * n_x_;
+  off_hs_ = off_reg_ + 16 * cg_.n_regs;
+  smem_bytes_ = off_hs_ + 16 * W_;
+}
+
+void Gen::body_mw(uint32_t w, bool wb) {
+  const std::string sfx = "_" + num(w) + (wb ? "w" : "l");
+  const uint32_t NR = cg_.n_regs, NO = cg_.n_ops_total();
+  static const char* sty[2] = {"u32", "u64"};
+  // this cycle's buffers: registers [2][NR], hash partials [2][W] by cycle parity
+  std::string regcur = e_.r32(), regnxt = e_.r32(), hsb = e_.r32();
+  {
+    const std::string p = e_.r32(), q = e_.r32();
+    e_.ins("cvt.u32.u64 " + p + ", " + ci_);
+    e_.ins("and.b32 " + p + ", " + p + ", 1");
+    e_.ins("xor.b32 " + q + ", " + p + ", 1");
+    e_.ins("mad.lo.u32 " + regcur + ", " + p + ", " + num(8 * NR) + ", " + smb_);
+    e_.ins("mad.lo.u32 " + regnxt + ", " + q + ", " + num(8 * NR) + ", " + smb_);
+    e_.ins("mad.lo.u32 " + hsb + ", " + p + ", " + num(8 * W_) + ", " + smb_);
+  }
+  acc_zero(w == 0 ? cg_.const_hash : 0);
+  inputs(sfx, w == 0, wb && w == 0);
+  // registers this warp reads or hashes
+  std::unordered_set<uint32_t> regs_read;
+  std::unordered_map<uint32_t, uint32_t> reg_of;  // register coordinate -> register index
+  for (uint32_t j = 0; j < NR; ++j) reg_of[cg_.reg_coord[j]] = j;
+  for (uint32_t j = 0; j < NO; ++j)
+    if (owner_[j] == w)
+      for (uint32_t o = cg_.coord_off[j]; o < cg_.coord_off[j + 1]; ++o)
+        if (reg_of.count(cg_.coord[o])) regs_read.insert(reg_of[cg_.coord[o]]);
+  for (uint32_t j = 0; j < NR; ++j) {
+    if (!regs_read.count(j) && j % W_ != w) continue;
+    const Val& R = sig(cg_.reg_coord[j]);
+    e_.ins(std::string("ld.shared.") + sty[R.w64] + " " + R.reg + ", [" + regcur + "+" + num(off_reg_ + 8 * j) + "]");
+    if (j % W_ == w) hash_add(R, cg_.reg_k[j]);
+  }
+  // registers whose next value is not an op's (a constant): warp 0 posts it now
+  std::unordered_map<uint32_t, std::vector<uint32_t>> next_of;  // next-source coordinate -> registers
+  for (uint32_t j = 0; j < NR; ++j) next_of[cg_.reg_next_coord[j]].push_back(j);
+  std::unordered_set<uint32_t> op_out(out_coord_.begin(), out_coord_.end());
+  auto post_next = [&](uint32_t r, const Val& src) {
+    const Val& R = sig(cg_.reg_coord[r]);
+    std::string v = as(src, R.w64);
+    if (cg_.reg_w[r] < (R.w64 ? 64u : 32u)) {
+      const std::string t = e_.reg(R.w64);
+      e_.ins(std::string(R.w64 ? "and.b64 " : "and.b32 ") + t + ", " + v + ", " + hex(width_mask(cg_.reg_w[r])));
+      v = t;
+    }
+    e_.ins("@" + pw0_ + " st.shared." + sty[R.w64] + " [" + regnxt + "+" + num(off_reg_ + 8 * r) + "], " + v);
+  };
+  if (w == 0)
+    for (uint32_t r = 0; r < NR; ++r)
+      if (!op_out.count(cg_.reg_next_coord[r])) post_next(r, sig(cg_.reg_next_coord[r]));
+  std::unordered_map<uint32_t, uint32_t> prod;
+  for (uint32_t j = 0; j < NO; ++j) prod[out_coord_[j]] = j;
+  std::unordered_set<uint32_t> loaded;
+  const uint32_t NL = std::max<uint32_t>(1, cg_.n_levels);
+  for (uint32_t l = 0; l < NL; ++l) {
+    const uint32_t lb = cg_.n_levels ? cg_.level_op_begin[l] : 0, le = cg_.n_levels ? cg_.level_op_begin[l + 1] : 0;
+    for (uint32_t j = lb; j < le; ++j) {
+      if (owner_[j] != w) continue;
+      for (uint32_t o = cg_.coord_off[j]; o < cg_.coord_off[j + 1]; ++o) {  // other warps' values
+        auto it = prod.find(cg_.coord[o]);
+        if (it == prod.end() || owner_[it->second] == w || loaded.count(cg_.coord[o])) continue;
+        const Val& v = sig(cg_.coord[o]);
+        e_.ins(std::string("ld.shared.") + sty[v.w64] + " " + v.reg + ", [" + smb_ + "+" + num(8 * xslot_[it->second]) + "]");
+        loaded.insert(cg_.coord[o]);
+      }
+      const Val& out = sig_.at(out_coord_[j]);
+      const std::string d = op_expr(j);
+      e_.ins(std::string(out.w64 ? "mov.b64 " : "mov.b32 ") + out.reg + ", " + d);
+      hash_add(out, cg_.opk[j]);
+      if (xslot_[j] >= 0)
+        e_.ins("@" + pw0_ + " st.shared." + sty[out.w64] + " [" + smb_ + "+" + num(8 * xslot_[j]) + "], " + out.reg);
+      auto nx = next_of.find(out_coord_[j]);
+      if (nx != next_of.end())
+        for (uint32_t r : nx->second) post_next(r, out);
+      if (wb) store(out_coord_[j], out);
+    }
+    if (l + 1 == NL) {  // this warp's share of the cycle's hash
+      const std::string H = acc_sum();
+      e_.ins("@" + pw0_ + " st.shared.u64 [" + hsb + "+" + num(off_hs_ + 8 * w) + "], " + H);
+    }
+    e_.ins("bar.sync 1, " + num(32 * W_));
+  }
+  if (w == 0) {
+    std::string H = e_.r64();
+    e_.ins("ld.shared.u64 " + H + ", [" + hsb + "+" + num(off_hs_) + "]");
+    for (uint32_t k = 1; k < W_; ++k) {
+      const std::string t = e_.r64(), H2 = e_.r64();
+      e_.ins("ld.shared.u64 " + t + ", [" + hsb + "+" + num(off_hs_ + 8 * k) + "]");
+      e_.ins("add.u64 " + H2 + ", " + H + ", " + t);
+      H = H2;
+    }
+    e_.ins("@" + pst_ + " st.global.u64 [" + hp_ + "], " + H);
+  }
+  e_.ins("add.u64 " + hp_ + ", " + hp_ + ", " + hstride_);
+  if (wb && w == 0) {  // the registers after the last latch: state write-back and the hash carry
+    acc_zero(0);
+    for (uint32_t j = 0; j < NR; ++j) {
+      const Val& R = sig(cg_.reg_coord[j]);
+      e_.ins(std::string("ld.shared.") + sty[R.w64] + " " + R.reg + ", [" + regnxt + "+" + num(off_reg_ + 8 * j) + "]");
+      store(cg_.reg_coord[j], R);
+      hash_add(R, cg_.reg_k[j]);
+    }
+    const std::string H = acc_sum(), a = e_.r64(), hc = e_.r64();
+    e_.ins("ld.param.u64 " + hc + ", [rs_su_a+" + num(F_HCARRY) + "]");
+    e_.ins("cvta.to.global.u64 " + hc + ", " + hc);
+    e_.ins("mad.lo.u64 " + a + ", " + lane_ + ", 8, " + hc);
+    e_.ins("@" + pw0_ + " st.global.u64 [" + a + "], " + H);
+  }
+}
+
 std::string Gen::run() {
   // registers of the design's signals
   out_coord_.resize(cg_.n_ops_total());
@@ -387,6 +557,7 @@ std::string Gen::run() {
   for (uint32_t j = 0; j < cg_.n_regs; ++j) declare(cg_.reg_coord[j]);
   for (size_t k = 0; k < cg_.const_coord.size(); ++k) declare(cg_.const_coord[k]);
   for (uint32_t j = 0; j < cg_.n_ops_total(); ++j) declare(out_coord_[j]);
+  plan_warps();
 
   // prologue: lane, tile, state bases, stimulus prefixes, registers
   auto param = [&](uint32_t off) {
@@ -404,7 +575,9 @@ std::string Gen::run() {
       wl_ = e_.r32();
       pw0_ = e_.pr();
       e_.ins("and.b32 " + wl_ + ", " + t + ", 31");
-      e_.ins("setp.eq.u32 " + pw0_ + ", " + t + ", 0");
+      e_.ins("setp.eq.u32 " + pw0_ + ", " + wl_ + ", 0");
+      wid_ = e_.r32();
+      e_.ins("shr.u32 " + wid_ + ", " + t + ", 5");
       e_.ins("mov.u64 " + lane_ + ", 0");
     } else {
       const std::string t64 = e_.r64();
@@ -504,23 +677,64 @@ std::string Gen::run() {
   nlast_ = e_.r64();
   e_.ins("mov.u64 " + ci_ + ", 0");
   e_.ins("sub.u64 " + nlast_ + ", " + ncyc + ", 1");
-  e_.label("LOOP");
-  {
-    const std::string p = e_.pr();
-    e_.ins("setp.ge.u64 " + p + ", " + ci_ + ", " + nlast_);
-    e_.ins("@" + p + " bra FINAL");
+  if (W_ == 1) {
+    e_.label("LOOP");
+    {
+      const std::string p = e_.pr();
+      e_.ins("setp.ge.u64 " + p + ", " + ci_ + ", " + nlast_);
+      e_.ins("@" + p + " bra FINAL");
+    }
+    body(false);
+    e_.ins("add.u64 " + ci_ + ", " + ci_ + ", 1");
+    e_.ins("add.u64 " + c_ + ", " + c_ + ", 1");
+    e_.ins("bra.uni LOOP");
+    e_.label("FINAL");
+    body(true);
+  } else {
+    // the registers' values for cycle 0 into shared buffer 0, then one stream per warp
+    smb_ = e_.r32();
+    e_.ins("mov.u32 " + smb_ + ", su_sm");
+    {
+      const std::string p0 = e_.pr();
+      e_.ins("setp.eq.u32 " + p0 + ", " + wid_ + ", 0");
+      const std::string pt0 = e_.pr();
+      e_.ins("and.pred " + pt0 + ", " + p0 + ", " + pw0_);
+      for (uint32_t j = 0; j < cg_.n_regs; ++j) {
+        const Val& R = sig(cg_.reg_coord[j]);
+        e_.ins("@" + pt0 + " st.shared." + (R.w64 ? std::string("u64") : std::string("u32")) + " [" + smb_ + "+" +
+               num(off_reg_ + 8 * j) + "], " + R.reg);
+      }
+    }
+    e_.ins("bar.sync 1, " + num(32 * W_));
+    for (uint32_t w = 1; w < W_; ++w) {
+      const std::string p = e_.pr();
+      e_.ins("setp.eq.u32 " + p + ", " + wid_ + ", " + num(w));
+      e_.ins("@" + p + " bra WS_" + num(w));
+    }
+    for (uint32_t w = 0; w < W_; ++w) {
+      e_.label("WS_" + num(w));
+      e_.label("LOOP_" + num(w));
+      {
+        const std::string p = e_.pr();
+        e_.ins("setp.ge.u64 " + p + ", " + ci_ + ", " + nlast_);
+        e_.ins("@" + p + " bra FINAL_" + num(w));
+      }
+      body_mw(w, false);
+      e_.ins("add.u64 " + ci_ + ", " + ci_ + ", 1");
+      e_.ins("add.u64 " + c_ + ", " + c_ + ", 1");
+      e_.ins("bra.uni LOOP_" + num(w));
+      e_.label("FINAL_" + num(w));
+      body_mw(w, true);
+      e_.ins("bra.uni DONE");
+    }
   }
-  body(false);
-  e_.ins("add.u64 " + ci_ + ", " + ci_ + ", 1");
-  e_.ins("add.u64 " + c_ + ", " + c_ + ", 1");
-  e_.ins("bra.uni LOOP");
-  e_.label("FINAL");
-  body(true);
   e_.label("DONE");
   e_.ins("ret");
 
   std::string head = ".version 8.7\n.target sm_100a\n.address_size 64\n\n";
-  head += ".visible .entry rs_su(.param .align 8 .b8 rs_su_a[" + num(sizeof(SuArgs)) + "])\n.maxntid 128, 1, 1\n{\n";
+  if (W_ > 1) head += ".shared .align 8 .b8 su_sm[" + num(std::max<uint32_t>(8, smem_bytes_)) + "];\n\n";
+  head += ".visible .entry rs_su(.param .align 8 .b8 rs_su_a[" + num(sizeof(SuArgs)) + "])\n.maxntid " +
+          num(threads()) + ", 1, 1\n{\n";
   head += "\t.reg .pred %p<" + num(e_.np + 1) + ">;\n";
   head += "\t.reg .b32 %r<" + num(e_.n32 + 1) + ">;\n";
   head += "\t.reg .b64 %d<" + num(e_.n64 + 1) + ">;\n";
@@ -529,6 +743,11 @@ std::string Gen::run() {
 
 }  // namespace
 
-std::string su_ptx(const CompiledGraph& cg) { return Gen(cg).run(); }
+std::string su_ptx(const CompiledGraph& cg, uint32_t* threads) {
+  Gen g(cg);
+  std::string p = g.run();
+  if (threads) *threads = g.threads();
+  return p;
+}
 
 }  // namespace rtlsim

@@ -42,7 +42,8 @@ static_assert(sizeof(SuArgs) == 17 * 8, "SuArgs: 17 eight-byte fields");
 
 constexpr uint32_t kSuMaxOps = 4096;  // ptxas time: C1 256 ops 0.4 s, C2 20k ops 25 min
 
-// PTX of the specialised kernel for `cg` (.entry rs_su(SuArgs)), for sm_100a.
-std::string su_ptx(const CompiledGraph& cg);
+// PTX of the specialised kernel for `cg` (.entry rs_su(SuArgs)), for sm_100a; *threads =
+// the CTA size it is written for (single lane: 32 per warp of the multi-warp split; lanes: 128).
+std::string su_ptx(const CompiledGraph& cg, uint32_t* threads);
 
 }  // namespace rtlsim

@@ -83,6 +83,7 @@ struct rs_graph {
   // kernel 8 (codegen.hpp): the design's specialised kernel, compiled once (rs_specialize)
   bool su_built = false;
   std::string su_ptx;
+  uint32_t su_threads = 32;
   cudaLibrary_t su_lib = nullptr;
   cudaKernel_t su_fn = nullptr;
 };
@@ -772,7 +773,7 @@ rs_status rs_specialize(rs_graph* g) {
     if (g->cg.n_ops_total() > kSuMaxOps)
       return set_err(RS_E_CAPACITY, "kernel 8 (specialised) is capped at %u ops (graph has %u)", kSuMaxOps,
                      g->cg.n_ops_total());
-    g->su_ptx = su_ptx(g->cg);
+    g->su_ptx = su_ptx(g->cg, &g->su_threads);
     g->su_built = true;
   }
   if (g->dmem && !g->su_fn) {
@@ -854,7 +855,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     s->LT = g->cg.mode == RS_MODE_SINGLE ? 1u : (o.lane_tile ? o.lane_tile : 32u);
     s->n_tiles = (n_lanes + s->LT - 1) / s->LT;
     s->parts = 1;
-    s->threads = g->cg.mode == RS_MODE_SINGLE ? 32u : 128u;
+    s->threads = g->su_threads;
     s->ctas = (n_lanes + s->threads - 1) / s->threads;
   }
   if (g->cg.mode == RS_MODE_SINGLE && (o.kernel == 3 || o.kernel == 4) && !o.repcut) o.repcut = 1;

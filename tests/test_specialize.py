@@ -111,3 +111,20 @@ def test_k8_rejects_what_it_does_not_build(rs):
     L = rs.Lanes(g, 1, kernel=8)
     with pytest.raises(rs.RtlSimError, match="UNSUPPORTED|not built"):
         L.watch([0, 1])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("warps", [2, 3, 5, 8])
+def test_k8_single_lane_multiwarp(rs, monkeypatch, warps):
+    """Single lane split over several warps (shared-memory exchange, one named barrier per
+    level): C1, the edge circuit with staged corner values, pass-rich and fuzz circuits."""
+    monkeypatch.setenv("RTLSIM_K8_WARPS", str(warps))
+    cfg = CONFIGS["C1"]
+    L = _check(rs, config_circuit("C1"), 120, 1, mode="single", seed=cfg.stim_seed, chunks=(1, 50))
+    assert L.shape()["threads"] == 32 * warps
+    c = edge_circuit(warps % 2)
+    staged = edge_values(np.random.default_rng(400 + warps), (9, c.n_inputs, 1))
+    _check(rs, c, 9, 1, mode="single", staged=staged, chunks=(4,))
+    _check(rs, pass_circuit(warps), 15, 1, mode="single", passes=True, seed=warps)
+    for seed in range(warps, 40, 7):
+        _check(rs, fuzz_circuit(seed), 20, 1, mode="single", seed=seed, chunks=(5,))
