@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstring>
 #include <numeric>
+#include <functional>
 #include <unordered_map>
 
 namespace rtlsim {
@@ -749,8 +750,84 @@ bool build_single_slices(const CompiledGraph& g, uint32_t P, uint32_t Gp, uint32
   return true;
 }
 
+namespace {
+
+// Register partition by cone clustering (the partitioning step of RepCut, PAPER.md
+// P:1981-1982, which uses a hypergraph partitioner; reading R20): a register's
+// replication cost is the overlap of its next-value cone with other partitions' cones,
+// and cones only meet inside connected combinational logic -- registers and inputs end
+// a cone.  So the ops are joined with their operands' producers (union-find), each
+// register goes with the component of its next value's producer, and the components
+// (the cores of a multi-core design, coupled only through registers) are cut to size
+// and bin-packed, largest first, into P partitions.  Returns an empty vector when the
+// logic is one component (a random single core: nothing to find).
+std::vector<uint32_t> cone_cluster_partition(const CompiledGraph& g, uint32_t P,
+                                             const std::function<int32_t(uint32_t)>& producer,
+                                             std::vector<int32_t>* op_home) {
+  const uint32_t NT = g.n_ops_total(), R = g.n_regs;
+  std::vector<uint32_t> uf(NT);
+  for (uint32_t j = 0; j < NT; ++j) uf[j] = j;
+  auto find = [&](uint32_t x) {
+    while (uf[x] != x) x = uf[x] = uf[uf[x]];
+    return x;
+  };
+  for (uint32_t j = 0; j < NT; ++j)
+    for (uint32_t a = g.coord_off[j]; a < g.coord_off[j + 1]; ++a) {
+      const int32_t q = producer(g.coord[a]);
+      if (q >= 0) uf[find(j)] = find((uint32_t)q);
+    }
+  std::unordered_map<uint32_t, std::vector<uint32_t>> comp;
+  for (uint32_t i = 0; i < R; ++i) {
+    const int32_t q = producer(g.reg_next_coord[i]);
+    comp[q >= 0 ? find((uint32_t)q) : NT + i].push_back(i);
+  }
+  if (comp.size() <= 1) return {};
+  // pieces of at most ~R / P registers (index order within a component), bin-packed
+  const uint32_t target = std::max<uint32_t>(1, (R + P - 1) / P);
+  std::vector<std::vector<uint32_t>> pieces;
+  for (auto& kv : comp) {
+    std::vector<uint32_t>& v = kv.second;
+    if (v.size() <= target + target / 2) {
+      pieces.push_back(std::move(v));
+      continue;
+    }
+    for (size_t b = 0; b < v.size(); b += target)
+      pieces.emplace_back(v.begin() + b, v.begin() + std::min(v.size(), b + target));
+  }
+  std::sort(pieces.begin(), pieces.end(), [](const std::vector<uint32_t>& a, const std::vector<uint32_t>& b) {
+    return a.size() != b.size() ? a.size() > b.size() : a[0] < b[0];
+  });
+  std::vector<uint32_t> part(R, 0), load(P, 0);
+  for (const auto& pc : pieces) {
+    const uint32_t p = (uint32_t)(std::min_element(load.begin(), load.end()) - load.begin());
+    for (uint32_t i : pc) part[i] = p;
+    load[p] += (uint32_t)pc.size();
+  }
+  for (uint32_t p = 0; p < P; ++p)
+    if (!load[p]) return {};  // a partition without registers: keep the blocks
+  // home of every op: the partition of its component's (first) registers -- where dead
+  // logic of that component goes, so it drags no cone into another partition
+  std::unordered_map<uint32_t, int32_t> home;
+  for (uint32_t i = 0; i < R; ++i) {
+    const int32_t q = producer(g.reg_next_coord[i]);
+    if (q >= 0) home.emplace(find((uint32_t)q), (int32_t)part[i]);
+  }
+  op_home->assign(NT, -1);
+  for (uint32_t j = 0; j < NT; ++j) {
+    auto it = home.find(find(j));
+    if (it != home.end()) (*op_home)[j] = it->second;
+  }
+  return part;
+}
+
+bool build_repcut_with(const CompiledGraph& g, uint32_t P, const std::vector<uint32_t>& reg_part,
+                       const std::function<int32_t(uint32_t)>& producer, const std::vector<int32_t>* op_home,
+                       RepCutPlan* out);
+
+}  // namespace
+
 bool build_repcut(const CompiledGraph& g, uint32_t P, RepCutPlan* out, std::string* err) {
-  const uint32_t NT = g.n_ops_total(), NL = g.n_levels, R = g.n_regs;
+  const uint32_t R = g.n_regs;
   if (P == 0 || P > 255 || (R && P > R) || (!R && P > 1)) {
     *err = "repcut: partitions must be in [1, min(255, n_regs)]";
     return false;
@@ -762,10 +839,32 @@ bool build_repcut(const CompiledGraph& g, uint32_t P, RepCutPlan* out, std::stri
     const uint32_t cls = (r.meta >> 16) & 3u;
     for (uint32_t k = 0; k < r.count; ++k) prod[cls][r.out_row0 + k] = (int32_t)(r.op_begin + k);
   }
-  auto producer = [&](uint32_t c) -> int32_t { return prod[c >> 30][c & ROW_MASK]; };
-  // register blocks
-  std::vector<uint32_t> reg_part(R);
-  for (uint32_t i = 0; i < R; ++i) reg_part[i] = (uint32_t)((uint64_t)i * P / R);
+  const std::function<int32_t(uint32_t)> producer = [&](uint32_t c) -> int32_t { return prod[c >> 30][c & ROW_MASK]; };
+  // register partition: contiguous index blocks (a netlist lists each module's registers
+  // together), or the cone clustering when it replicates less (the largest partition
+  // first, then the total)
+  std::vector<uint32_t> blocks(R);
+  for (uint32_t i = 0; i < R; ++i) blocks[i] = (uint32_t)((uint64_t)i * P / R);
+  build_repcut_with(g, P, blocks, producer, nullptr, out);
+  if (P > 1) {
+    std::vector<int32_t> home;
+    const std::vector<uint32_t> cc = cone_cluster_partition(g, P, producer, &home);
+    if (!cc.empty() && cc != blocks) {
+      RepCutPlan alt;
+      build_repcut_with(g, P, cc, producer, &home, &alt);
+      if (alt.max_ops < out->max_ops || (alt.max_ops == out->max_ops && alt.ops_total < out->ops_total))
+        *out = std::move(alt);
+    }
+  }
+  return true;
+}
+
+namespace {
+
+bool build_repcut_with(const CompiledGraph& g, uint32_t P, const std::vector<uint32_t>& reg_part,
+                       const std::function<int32_t(uint32_t)>& producer, const std::vector<int32_t>* op_home,
+                       RepCutPlan* out) {
+  const uint32_t NT = g.n_ops_total(), NL = g.n_levels, R = g.n_regs;
   // cones: member[p] bitmaps over ops
   std::vector<std::vector<uint8_t>> member(P, std::vector<uint8_t>(NT, 0));
   std::vector<uint32_t> stack;
@@ -808,7 +907,7 @@ bool build_repcut(const CompiledGraph& g, uint32_t P, RepCutPlan* out, std::stri
     }
   for (uint32_t j = 0; j < NT; ++j)
     if (owner[j] < 0) {
-      int32_t p = -1;
+      int32_t p = op_home ? (*op_home)[j] : -1;  // the clustering's home of its logic component
       for (uint32_t a = g.coord_off[j]; a < g.coord_off[j + 1] && p < 0; ++a) {
         const int32_t q = producer(g.coord[a]);
         if (q >= 0) p = owner[q];
@@ -891,6 +990,8 @@ bool build_repcut(const CompiledGraph& g, uint32_t P, RepCutPlan* out, std::stri
   }
   return true;
 }
+
+}  // namespace
 
 
 bool build_repcut_slices(const CompiledGraph& g, const RepCutPlan& plan, uint32_t max_smem, bool wide,

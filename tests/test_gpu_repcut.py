@@ -109,6 +109,24 @@ def test_repcut_multicore16_smem(rs):
     check(rs, c, 20, 1, seed=206, mode="single", repcut=16)
 
 
+def test_repcut_multicore_shuffled_registers(rs):
+    """Registers listed in a random order: contiguous index blocks would replicate ~10x;
+    the cone clustering (compiler.cpp cone_cluster_partition) finds the cores again, so the
+    16-core design still fits shared-memory slices, replication-free, and stays bit-exact."""
+    import dataclasses
+    c = multicore_circuit()
+    perm = np.random.default_rng(3).permutation(c.n_regs)
+    c = dataclasses.replace(c, reg_id=c.reg_id[perm], reg_next_id=c.reg_next_id[perm], reg_init=c.reg_init[perm])
+    assert kernel_of(rs, c, repcut=16) == 3
+    check(rs, c, 20, 1, seed=206, mode="single", repcut=16)
+    small = multicore_circuit(n_cores=4, ops_per_core=2000, regs_per_core=200, n_levels=30, cross_p=0.05)
+    perm = np.random.default_rng(4).permutation(small.n_regs)
+    small = dataclasses.replace(small, reg_id=small.reg_id[perm], reg_next_id=small.reg_next_id[perm],
+                                reg_init=small.reg_init[perm])
+    for P, gl in [(4, 0), (4, 1), (2, 2), (8, 0)]:
+        check(rs, small, 40, 1, seed=7, mode="single", repcut=P, repcut_global=gl)
+
+
 def test_repcut_errors(rs):
     c = config_circuit("C1")
     g = rs.Graph(c, device=0, mode="single")
