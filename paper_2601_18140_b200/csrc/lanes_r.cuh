@@ -30,6 +30,16 @@
 #define RS_LANES_R1_MAX_THREADS 1024
 #endif
 
+// registers per latch batch in kernel 7 (0: lanes_t.cuh's default, 2 at P = 4).  Measured
+// (profiles/r02/kernel7/ab3_latch_u.txt): 4 at P = 4 single ops C3 1.150 -> 1.193 ms per
+// cycle (lost), with op pairs C4 634 -> 625 ms per 20 cycles (kept for the pairs kernel)
+#ifndef RS_K7_LATCH_U
+#define RS_K7_LATCH_U 0
+#endif
+#ifndef RS_K7_LATCH_U_PAIRS
+#define RS_K7_LATCH_U_PAIRS 4
+#endif
+
 namespace rtlsim {
 
 constexpr uint32_t kRecBytes = 32;
@@ -127,6 +137,30 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
   return v;
 }
 
+// gather_t with the class signature taken from the record (sel bits 0..7, set at bind
+// time) instead of recomputed from the coordinates' class bits -- a few dependent
+// instructions off every op's path to its loads (RS_K7_NO_PRESIG: recompute, for A/B).
+template <int A, int P>
+__device__ __forceinline__ void gather_rs(const LaneT& L, uint32_t sig, const uint32_t (&c)[A], uint64_t (&x)[A][P]) {
+#ifdef RS_K7_NO_PRESIG
+  gather_t<A, P>(L, c, x);
+#else
+  if constexpr (P == 1) {
+    if constexpr (A == 1) gather_sig1_p1(sig, L.p0, L.p1, L.p2, L.p3, c[0], x);
+    else if constexpr (A == 2) gather_sig2_p1(sig, L.p0, L.p1, L.p2, L.p3, c[0], c[1], x);
+    else gather_sig3_p1(sig, L.p0, L.p1, L.p2, L.p3, c[0], c[1], c[2], x);
+  } else if constexpr (P == 2) {
+    if constexpr (A == 1) gather_sig1_p2(sig, L.p0, L.p1, L.p2, L.p3, c[0], x);
+    else if constexpr (A == 2) gather_sig2_p2(sig, L.p0, L.p1, L.p2, L.p3, c[0], c[1], x);
+    else gather_sig3_p2(sig, L.p0, L.p1, L.p2, L.p3, c[0], c[1], c[2], x);
+  } else {
+    if constexpr (A == 1) gather_sig1_p4(sig, L.p0, L.p1, L.p2, L.p3, c[0], x);
+    else if constexpr (A == 2) gather_sig2_p4(sig, L.p0, L.p1, L.p2, L.p3, c[0], c[1], x);
+    else gather_sig3_p4(sig, L.p0, L.p1, L.p2, L.p3, c[0], c[1], c[2], x);
+  }
+#endif
+}
+
 // One op from its record at shared address `rec` (base = the stage buffer, for fold lists).
 template <int P, bool HASH>
 __device__ __forceinline__ void op_r(const LaneT& L, uint32_t base, uint32_t rec, uint64_t (&hacc)[P]) {
@@ -148,7 +182,7 @@ __device__ __forceinline__ void op_r(const LaneT& L, uint32_t base, uint32_t rec
   if (A == 2) {
     const uint32_t c[2] = {r0.x, r0.y};
     uint64_t x[2][P];
-    gather_t<2, P>(L, c, x);
+    gather_rs<2, P>(L, sel & 0xffu, c, x);
     switch (t) {
       RS_R4(5, 2, RS_OP_AND) RS_R4(6, 2, RS_OP_OR) RS_R4(7, 2, RS_OP_XOR) RS_R4(8, 2, RS_OP_ADD)
       RS_R4(9, 2, RS_OP_SUB) RS_R4(10, 2, RS_OP_MUL) RS_R4(11, 2, RS_OP_EQ) RS_R4(12, 2, RS_OP_LT)
@@ -158,7 +192,7 @@ __device__ __forceinline__ void op_r(const LaneT& L, uint32_t base, uint32_t rec
   } else if (A == 1) {
     const uint32_t c[1] = {r0.x};
     uint64_t x[1][P];
-    gather_t<1, P>(L, c, x);
+    gather_rs<1, P>(L, sel & 0xffu, c, x);
     switch (t) {
       RS_R4(0, 1, RS_OP_NOT) RS_R4(1, 1, RS_OP_SHL) RS_R4(2, 1, RS_OP_SHR) RS_R4(3, 1, RS_OP_BITS)
       RS_R4(4, 1, OP_COPY)
@@ -167,7 +201,7 @@ __device__ __forceinline__ void op_r(const LaneT& L, uint32_t base, uint32_t rec
   } else {
     const uint32_t c[3] = {r0.x, r0.y, r0.z};
     uint64_t x[3][P];
-    gather_t<3, P>(L, c, x);
+    gather_rs<3, P>(L, sel & 0xffu, c, x);
     switch (t) {
       RS_R4(14, 3, RS_OP_AND) RS_R4(15, 3, RS_OP_OR) RS_R4(16, 3, RS_OP_XOR) RS_R4(17, 3, RS_OP_ADD)
       RS_R4(18, 3, RS_OP_SUB) RS_R4(19, 3, RS_OP_MUL) RS_R4(20, 3, RS_OP_MUX)
@@ -288,7 +322,8 @@ __global__ void __launch_bounds__(PAIRS ? RS_LANES_R_PAIRS_MAX_THREADS
         uint64_t hr[P];
 #pragma unroll
         for (int k = 0; k < P; ++k) hr[k] = 0;
-        stage_latch_t<P, HASH>(L, base + h->off_c, base + h->off_w, base + h->off_k, b, e, hr);
+        stage_latch_t<P, HASH, PAIRS ? RS_K7_LATCH_U_PAIRS : RS_K7_LATCH_U>(L, base + h->off_c, base + h->off_w,
+                                                                             base + h->off_k, b, e, hr);
         if constexpr (HASH) {
           uint64_t* sr = sreg + ((cyc + 1u) & 3u) * LT;
 #pragma unroll

@@ -273,10 +273,11 @@ __device__ __forceinline__ void stage_ops_t(const LaneT& L, const uint8_t* buf, 
 
 // LATCH stage: tmp = LI[next] & M(w_r); LI[r] = tmp.  One pass is hazard-free
 // because every next row is an op row (compiler identity copies; reading R8).
-template <int P, bool HASH>
+// UU > 0: registers per batch (their next-value loads in flight together); 0: the default.
+template <int P, bool HASH, int UU = 0>
 __device__ __forceinline__ void stage_latch_t(const LaneT& L, uint32_t s_c, uint32_t s_w, uint32_t s_k, uint32_t b,
                                               uint32_t e, uint64_t (&hr)[P]) {
-  constexpr int U = (P == 4) ? 2 : 4;
+  constexpr int U = UU > 0 ? UU : (P == 4) ? 2 : 4;
 #pragma unroll 1
   for (uint32_t j = b; j < e; j += U) {
     uint64_t v[U][P];

@@ -387,6 +387,8 @@ void bind_stages_r(const rs_lanes* s, std::vector<uint8_t>* out, std::vector<Sta
           q.v[1] = ar > 1 ? cc[1] : 0u;
           q.v[2] = ar > 2 ? cc[2] : 0u;
           q.v[7] = ((uint32_t)(4 * tail_combo((int)ar, (int)op)) + cls) << 8 | ar << 16 | op << 24;
+          // bits 0..7: the operands' class signature (the gather's jump index, lanes_r.cuh op_r)
+          for (uint32_t o = 0; o < ar; ++o) q.v[7] |= (cc[o] >> 30) << (2 * o);
         } else {
           q.fold.assign(cc, cc + ar);
           q.v[1] = ar;
