@@ -314,11 +314,18 @@ __global__ void __launch_bounds__(1024, 1) k_single2(const SingleArgs sa) {
 #pragma unroll 1
     for (uint32_t i = tid; i < h->n_latch; i += T) {
       const uint32_t wf = lat[4 * i + 2];
+      // differential exchange: a register other partitions read is sent to
+      // their replicas only when its value changed -- every replica already holds the
+      // value it had (each change was sent); the first cycle of a launch sends all, so
+      // host writes between launches (rs_write_registers) cannot leave replicas apart
+      const bool diff = (wf >> 8) != 0u && cyc > 0;
+      const uint64_t old = diff ? S.ld(lat[4 * i + 1]) : 0ull;
       const uint64_t x = S.ld(lat[4 * i]) & wmask(wf & 127u);
       S.st(lat[4 * i + 1], x);
       if (wf & 128u) {  // own register: hash it; publish it to the replicas that finished the cycle
         if (HASH) hr += x * (i == tid ? klat : __ldg(a.g.reg_k + lat[4 * i + 3]));
-        for (uint32_t m = wf >> 8; m; m &= m - 1) peer_st(lat[4 * i + 1], __ffs(m) - 1, x);
+        if (!diff || x != old)
+          for (uint32_t m = wf >> 8; m; m &= m - 1) peer_st(lat[4 * i + 1], __ffs(m) - 1, x);
       }
     }
     if (P > 1) {  // cut signals to the later partitions that read them
