@@ -948,7 +948,15 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     // ones kernel 1's 32 * P-lane tiles (P = 4 amortizes the per-op decode).
     // (kernel 7, the record-based tile kernel, measured fastest at >= 2048 lanes: C3 1.23 vs
     // 1.30 ms per cycle for kernel 1, C4 31.6 vs 34.8 ms; profiles/r02)
-    const uint32_t kern = o.kernel ? o.kernel : (n_lanes < 2048u ? 2u : 7u);
+    // Designs with few ops per level (<= 1,024: C2's 500) are latency-bound at every lane
+    // count; there kernel 7's 32-lane tiles at 1,024 threads beat kernel 2 where their
+    // clusters are co-resident with >= 64 CTAs or the lanes are few (profiles/r02/k7low:
+    // C2 at 1,024 / 256 / 128 lanes 123.6 / 90.6 / 90.6 vs 130.6 / 104.7 / 103.1 us per
+    // cycle), not at 512 lanes (120.7 vs 100.7: the 8-CTA clusters it needs are not
+    // co-resident) nor for C3 / C4-sized levels at < 2,048 lanes (C3 1,024 lanes 689 vs 626).
+    const uint32_t opl = g->cg.n_levels ? g->cg.n_ops_total() / g->cg.n_levels : 0;
+    const bool k7_low = opl <= 1024u && (n_lanes >= 1024u || n_lanes <= 256u);
+    const uint32_t kern = o.kernel ? o.kernel : (n_lanes >= 2048u || k7_low) ? 7u : 2u;
     if (o.lane_tile && (kern == 2   ? (o.lane_tile != 8 && o.lane_tile != 16 && o.lane_tile != 32)
                         : kern == 6 ? (o.lane_tile != 64 && o.lane_tile != 128)
                                     : (o.lane_tile != 32 && o.lane_tile != 64 && o.lane_tile != 128))) {

@@ -15,6 +15,10 @@ the bench's launch configuration on the GPU box and compare every sampled
   C5  the single lane x all 100,000 cycles  -> streams/C5_full.npz
       (state carries across cycles, so no sampling is possible)
 
+  C2  all 1,024 lanes x all 10,000 cycles (the "Full" scope): a per-cycle digest
+      of every lane's hash (lane_digest below) plus 8 lanes exactly
+                                            -> streams/C2_digest.npz
+
 Each file holds `lanes` (global lane ids), `hashes` [cycles, lanes] (u64,
 DESIGN.md reading R12), `seed`, `cycles`, the generator version tag and the
 circuit's size, so a stale cache (generator changed) is detected by the test.
@@ -74,6 +78,43 @@ def make_sampled(name, threads):
     print(f"{name}: {len(lanes)} lanes x {cfg.cycles} cycles in {time.time() - t:.0f} s", flush=True)
 
 
+def _mix64(x):
+    """splitmix64 finaliser on a uint64 array (test infrastructure: the digest below)."""
+    x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return x ^ (x >> np.uint64(31))
+
+
+def lane_digest(H, lanes):
+    """Per-cycle digest of a [cycles, lanes] hash block: sum over lanes of
+    mix64(H[c, l] + (l + 1) * golden) mod 2^64.  A wrong hash in any (cycle, lane)
+    changes that cycle's digest (up to a 2^-64 collision); lanes are position-keyed."""
+    with np.errstate(over="ignore"):
+        key = (np.asarray(lanes, dtype=np.uint64) + np.uint64(1)) * np.uint64(0x9E3779B97F4A7C15)
+        return _mix64(H.astype(np.uint64) + key[None, :]).sum(axis=1, dtype=np.uint64)
+
+
+def make_digest(name, threads, chunk=1000):
+    c = config_circuit(name)
+    cfg = CONFIGS[name]
+    lanes = np.arange(cfg.lanes)
+    exact = [0, 1, 2, 3, cfg.lanes - 4, cfg.lanes - 3, cfg.lanes - 2, cfg.lanes - 1]
+    D = np.zeros(cfg.cycles, dtype=np.uint64)
+    E = np.zeros((cfg.cycles, len(exact)), dtype=np.uint64)
+    t = time.time()
+    regs = None
+    for c0 in range(0, cfg.cycles, chunk):  # chunks of cycles (state carried), all lanes each
+        n = min(chunk, cfg.cycles - c0)
+        r = oracle.simulate(c, n, seed=cfg.stim_seed, cycle0=c0, n_lanes=cfg.lanes, reg_state0=regs, final=True,
+                            threads=threads)
+        D[c0:c0 + n] = lane_digest(r.hashes, lanes)
+        E[c0:c0 + n] = r.hashes[:, exact]
+        regs = np.ascontiguousarray(r.final_state[np.asarray(c.reg_id, dtype=np.int64)])
+        print(f"{name}: {c0 + n} cycles ({time.time() - t:.0f} s)", flush=True)
+    np.savez(os.path.join(OUT, f"{name}_digest.npz"), digest=D, lanes=np.array(exact, dtype=np.int64), hashes=E,
+             n_lanes=cfg.lanes, cycles=cfg.cycles, **meta(name, c))
+
+
 def make_c5(chunk=5000):
     name = "C5"
     c = config_circuit(name)
@@ -109,5 +150,7 @@ if __name__ == "__main__":
     for nm in a.names:
         if nm == "C5":
             make_c5()
+        elif nm == "C2":
+            make_digest(nm, a.threads)
         else:
             make_sampled(nm, a.threads)

@@ -13,6 +13,9 @@ long to recompute on every GPU run):
       SURVEY.md §8(e)) x all 2,000 cycles, one shard at a time on this GPU;
       8 sampled lanes per shard compared at every cycle
   C5  the single lane x all 100,000 cycles (auto single-lane kernel, as bench.py)
+  C2  all 1,024 lanes x all 10,000 cycles ("Full"): a per-cycle digest of every
+      lane's hash (make_streams.lane_digest) plus 8 lanes exactly, on kernel 7's
+      32-lane tiles (the auto launch shape bench.py times) and on kernel 2
 """
 import os
 
@@ -87,3 +90,27 @@ def test_c5_all_100k_cycles(rs):
     H = np.concatenate([L.step(20_000, hashes="host") for _ in range(cfg.cycles // 20_000)])
     bad = np.argwhere(H != z["hashes"])
     assert bad.shape[0] == 0, f"C5 {L.shape()}: mismatch at cycles {bad[:5, 0].tolist()}"
+
+
+@pytest.mark.parametrize("kernel", [2, 7])
+def test_c2_all_lanes_all_cycles(rs, kernel):
+    import torch
+    from tests.golden.make_streams import lane_digest
+    z, c, cfg = _load("C2", "C2_digest.npz")
+    g = rs.Graph(c, device=0, passes=True)
+    L = rs.Lanes(g, cfg.lanes, kernel=kernel, lane_tile=32)
+    L.set_seed(cfg.stim_seed)
+    n_l, chunk = cfg.lanes, 1000
+    dev = torch.empty(chunk * n_l, dtype=torch.int64, device="cuda")
+    lanes = np.arange(n_l)
+    exact = np.asarray(z["lanes"], dtype=np.int64)
+    for c0 in range(0, cfg.cycles, chunk):
+        n = min(chunk, cfg.cycles - c0)
+        L.step(n, hashes=dev[:n * n_l])
+        L.sync()
+        H = dev[:n * n_l].view(n, n_l).cpu().numpy().view(np.uint64)
+        bad = np.nonzero(lane_digest(H, lanes) != z["digest"][c0:c0 + n])[0]
+        assert bad.size == 0, f"C2 {L.shape()}: digest mismatch at cycles {(bad[:5] + c0).tolist()}"
+        assert np.array_equal(H[:, exact], z["hashes"][c0:c0 + n]), f"C2 {L.shape()}: exact lanes differ"
+    L.close()
+    g.close()

@@ -372,17 +372,26 @@ def test_c4_c5_full_size_sampled(rs):
 
 
 def test_auto_kernel_choice(rs):
-    """rs_lane_opts.kernel = 0: kernel 2 below 2048 lanes, kernel 7 (records, 32 * P-lane tiles) above."""
-    c = config_circuit("C2", n_ops=2000, n_levels=10, n_regs=100)
-    g = rs.Graph(c)
-    a = rs.Lanes(g, 1024)
+    """rs_lane_opts.kernel = 0: kernel 7 (records, 32 * P-lane tiles) at >= 2048 lanes; below,
+    kernel 2 -- except for designs with <= 1,024 ops per level at >= 1,024 or <= 256 lanes,
+    which take kernel 7's 32-lane tiles (runtime.cu, profiles/r02/k7low)."""
+    c = config_circuit("C2", n_ops=2000, n_levels=10, n_regs=100)      # 200 ops per level
+    cw = config_circuit("C2", n_ops=12000, n_levels=8, n_regs=100)     # 1,500 ops per level
+    g, gw = rs.Graph(c), rs.Graph(cw)
+    a = rs.Lanes(gw, 1024)
     b = rs.Lanes(g, 4096)
+    d = rs.Lanes(g, 1024)
+    e = rs.Lanes(g, 512)
+    f = rs.Lanes(g, 200)
     assert a.shape()["kernel"] == 2 and a.shape()["lane_tile"] in (8, 16, 32)
     assert b.shape()["kernel"] == 7 and b.shape()["lane_tile"] in (64, 128)
-    for L in (a, b):
+    assert d.shape()["kernel"] == 7 and d.shape()["lane_tile"] == 32
+    assert e.shape()["kernel"] == 2
+    assert f.shape()["kernel"] == 7 and f.shape()["lane_tile"] == 32
+    for L, cc in ((a, cw), (b, c), (d, c), (e, c), (f, c)):
         L.set_seed(3)
         h = L.step(3, hashes="host")
-        r = oracle.simulate(c, 3, seed=3, lanes=[0, L.n_lanes - 1], threads=2)
+        r = oracle.simulate(cc, 3, seed=3, lanes=[0, L.n_lanes - 1], threads=2)
         assert np.array_equal(h[:, [0, L.n_lanes - 1]], r.hashes)
 
 
