@@ -147,8 +147,9 @@ typedef struct {
                               values) into its replica.  On one device the partitions are CTA groups of
                               one cooperative launch.  RS_E_CAPACITY if the slices do not fit
                               co-resident, RS_E_INVALID_ARG if parts > n_levels or > 8. */
-  uint32_t kernel;         /* RS_MODE_LANES step kernel (results identical): 0 = auto (2 below 2048
-                              lanes, else 7); 1 = tile-interleaved: tile = 32 * P lanes (P = 1, 2, 4),
+  uint32_t kernel;         /* RS_MODE_LANES step kernel (results identical): 0 = auto (7 at >= 2048
+                              lanes, and for designs with <= 1,024 ops per level at >= 1,024 or
+                              <= 256 lanes with 32-lane tiles; else 2); 1 = tile-interleaved: tile = 32 * P lanes (P = 1, 2, 4),
                               thread t owns lanes t + 32k, one op per warp, operand container widths
                               dispatched once per op through a jump table on the class signature;
                               2 = two adjacent lanes per thread, 8/16/32-lane tiles, aligned 64-bit
