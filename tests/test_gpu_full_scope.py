@@ -11,7 +11,8 @@ long to recompute on every GPU run):
       at every cycle
   C4  the 8 lane shards of the 8-GPU split (1,024 lanes each, lane0 = d * 1,024,
       SURVEY.md §8(e)) x all 2,000 cycles, one shard at a time on this GPU;
-      8 sampled lanes per shard compared at every cycle
+      8 sampled lanes per shard compared at every cycle; and all 8,192 lanes in
+      one allocation (the 1-GPU bench shape, kernel 7 with op pairs), 64 lanes
   C5  the single lane x all 100,000 cycles (auto single-lane kernel, as bench.py)
   C2  all 1,024 lanes x all 10,000 cycles ("Full"): a per-cycle digest of every
       lane's hash (make_streams.lane_digest) plus 8 lanes exactly, on kernel 7's
@@ -80,6 +81,18 @@ def test_c4_shards_full_cycles_sampled_lanes(rs):
                                 (lanes[sel] - d * shard).tolist(), 250)
         bad = np.argwhere(H != z["hashes"][:, sel])
         assert bad.shape[0] == 0, f"C4 shard {d} {shape}: mismatch at (cycle, sample) {bad[:5].tolist()}"
+
+
+def test_c4_bench_shape_full_cycles_sampled_lanes(rs):
+    """C4 as bench.py times it on one GPU: all 8,192 lanes in one allocation (auto: kernel 7 with op
+    pairs), graph passes on, all 2,000 cycles; the 64 cached lanes (spread over the 8 shards) compared
+    at every cycle."""
+    z, c, cfg = _load("C4", "C4_sampled.npz")
+    lanes = [int(x) for x in z["lanes"]]
+    H, shape = _gpu_sampled(rs, c, cfg.stim_seed, cfg.lanes, 0, cfg.cycles, lanes, 250)
+    assert shape["kernel"] == 7
+    bad = np.argwhere(H != z["hashes"])
+    assert bad.shape[0] == 0, f"C4 {shape}: mismatch at (cycle, sample) {bad[:5].tolist()}"
 
 
 def test_c5_all_100k_cycles(rs):
