@@ -281,6 +281,8 @@ def main():
     ap.add_argument("--kernel", type=int, default=0, help="rs_lane_opts.kernel (0 auto; C1 defaults to 8, specialised)")
     ap.add_argument("--parts", type=int, default=0, help="C1/C5: level-cut partitions emulated on this GPU")
     ap.add_argument("--repcut", type=int, default=0, help="single-lane configs: RepCut partitions (rs_lane_opts.repcut)")
+    ap.add_argument("--repcut-global", type=int, default=0,
+                    help="rs_lane_opts.repcut_global (0 auto, 1 the global-memory RepCut kernel, 2 shared-memory slices)")
     ap.add_argument("--ref-step-s", type=float, default=4.0)
     ap.add_argument("--watch", type=int, default=0, help="waveform capture of N signals during the timed steps")
     ap.add_argument("--op-pairs", type=int, default=0, help="rs_lane_opts.op_pairs (kernel 7: 0 auto, 1 off, 2 on)")
@@ -335,6 +337,7 @@ def main():
         kernel = 8  # C1 fits the specialised kernel (rs_specialize): 1.02 vs 4.07 us per cycle (RepCut)
     mk = dict(lane0=shard.lane0, lane_tile=args.lane_tile, threads=args.threads, stream=stream,
               cluster=args.cluster, parts=args.parts, kernel=kernel, repcut=args.repcut,
+              **({"repcut_global": args.repcut_global} if args.repcut_global else {}),
               l2_policy=args.l2_policy if not single else 0, op_pairs=args.op_pairs)
     if levelcut:
         L = rs.Lanes(g, 1, stream=stream, part_world=world, part_rank=rank)

@@ -28,6 +28,7 @@ struct RepArgs {
   const uint32_t* regs;
   const uint32_t* push_begin;  // [P + 1]
   const uint32_t* push;        // (register, reader partition) pairs
+  uint8_t* chg;                // [n_regs]: the register's committed value changed this cycle
 };
 
 template <bool HASH>
@@ -68,19 +69,24 @@ __global__ void __launch_bounds__(1024, 1) k_repcut(const RepArgs ra) {
 #pragma unroll 1
     for (uint32_t k = ra.reg_begin[p] + tid; k < ra.reg_begin[p + 1]; k += T) {
       const uint32_t r = __ldg(ra.regs + k), rc = __ldg(a.g.reg_coord + r);
-      if (HASH) hacc += t.ld(rc) * __ldg(a.g.reg_k + r);
-      t.stc(rc, t.ld(__ldg(a.g.reg_next_coord + r)) & wmask(__ldg(a.g.reg_w + r)));
+      const uint64_t old = t.ld(rc), nv = t.ld(__ldg(a.g.reg_next_coord + r)) & wmask(__ldg(a.g.reg_w + r));
+      if (HASH) hacc += old * __ldg(a.g.reg_k + r);
+      t.stc(rc, nv);
+      if (ra.chg) ra.chg[r] = nv != old ? 1 : 0;
     }
     if (HASH) {
       const uint64_t s = block_sum(hacc, wsum) + (p == 0 ? a.g.const_hash : 0ull);
       if (tid == 0 && a.hashes) atomicAdd((unsigned long long*)(a.hashes + cyc), (unsigned long long)s);
     }
     grid_barrier(a.bar, target);  // every partition has finished reading this cycle's register values
-    // Register Update Map: new register values into the replicas that read them
+    // Register Update Map: new register values into the replicas that read them -- with
+    // differential exchange only the registers whose value changed: every
+    // reader replica already holds the previous value (each change was pushed), and the
+    // first cycle of a launch pushes all (host writes between launches)
 #pragma unroll 1
     for (uint32_t k = ra.push_begin[p] + tid; k < ra.push_begin[p + 1]; k += T) {
       const uint32_t r = __ldg(ra.push + 2 * k), q = __ldg(ra.push + 2 * k + 1), rc = __ldg(a.g.reg_coord + r);
-      tile_ptrs<1>(a, q, 0).stc(rc, t.ld(rc));
+      if (cyc == 0 || !ra.chg || ra.chg[r]) tile_ptrs<1>(a, q, 0).stc(rc, t.ld(rc));
     }
     grid_barrier(a.bar, target);  // pushes visible before the next cycle's reads
   }

@@ -1085,6 +1085,10 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     put(blob, off, plan.regs, &o_regs);
     put(blob, off, plan.push_begin, &o_pb);
     put(blob, off, plan.push, &o_push);
+    size_t o_chg = 0;  // k_repcut's per-register "changed" flags (differential exchange; RTLSIM_REPCUT_DIFFX=0: off)
+    const char* dx = std::getenv("RTLSIM_REPCUT_DIFFX");
+    const bool diffx = !(dx && dx[0] == '0');
+    put(blob, off, std::vector<uint8_t>(diffx ? std::max<uint32_t>(1, g->cg.n_regs) : 0), &o_chg);
     blob.resize(std::max<size_t>(off, 256));
     cudaError_t e2 = cudaMalloc(&s->drep, blob.size());
     if (e2 == cudaSuccess) e2 = cudaMemcpy(s->drep, blob.data(), blob.size(), cudaMemcpyHostToDevice);
@@ -1099,6 +1103,7 @@ rs_status rs_alloc_lanes(rs_graph* g, uint32_t n_lanes, const rs_lane_opts* opts
     s->rep.regs = (const uint32_t*)(b + o_regs);
     s->rep.push_begin = (const uint32_t*)(b + o_pb);
     s->rep.push = (const uint32_t*)(b + o_push);
+    s->rep.chg = diffx ? (uint8_t*)s->drep + o_chg : nullptr;
     s->total_bytes += blob.size();
     if (s->rep_smem) {
       s->reps.blob = b + (uintptr_t)s->reps.blob;
